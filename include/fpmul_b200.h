@@ -1,0 +1,127 @@
+/*
+ * fpmul_b200.h -- C-ABI of the B200-native Frobenius-partition additive-FFT multiplier of
+ * GF(2)[x] polynomials (arXiv 1803.11301), implemented in libfpmul_b200.so.
+ *
+ * This is the drop-in boundary for the reference's hot path (/root/reference/proj).  The
+ * reference has no FFI of its own; its boundary is the C++ API in proj/include/fpmul/, and each
+ * entry point below is what a binding of that API needs.  The C++ mirror
+ * of the reference API (namespace fpmul, paper_1803_11301_b200/cpp/include/fpmul/) is implemented
+ * on top of these functions; INTEGRATION.md shows the bindings.
+ *
+ * Conventions
+ *  - Polynomials are packed little-endian uint64 words: coefficient k is bit k%64 of word k/64
+ *    (proj/include/fpmul/bitpoly.hpp:28-31).  An EvalVec of 2^l GF(2^128) elements is 2*2^l
+ *    uint64 words {lo, hi} per element (gf.hpp:24-52, butterfly.hpp:30-31).
+ *  - The field is GF(2^128) = GF(2)[x]/(x^128+x^7+x^2+x+1) (gf.hpp:115-123), the north-star field.
+ *  - *_dev functions take device pointers and a cudaStream_t (NULL = legacy default stream) and
+ *    are asynchronous; the others take host pointers and are synchronous.
+ *  - Every function returns an fpm_status; on error fpm_last_error() (thread-local) says why.
+ *    FPM_EINVAL is what the reference reports as std::invalid_argument, FPM_ECUDA / FPM_ENOMEM
+ *    replace its std::runtime_error failures (SURVEY.md section 8(b) "Errors").
+ *  - Thread safety: reentrant; per-device state (tables, stream, scratch) is created lazily under
+ *    a mutex, mirroring the reference's thread-safe singletons (cantor.cpp:136-140,
+ *    polymul.cpp:63-74).  Results are deterministic and bit-identical to the reference.
+ */
+#ifndef FPMUL_B200_H_
+#define FPMUL_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FPM_OK = 0,
+  FPM_EINVAL = 1, /* invalid argument (reference: std::invalid_argument) */
+  FPM_ECUDA = 2,  /* CUDA/NCCL failure, no device, or missing kernels */
+  FPM_ENOMEM = 3  /* device or host allocation failed */
+} fpm_status;
+
+/* Field selection, mirroring FieldChoice (proj/include/fpmul/polymul.hpp:28-32). */
+enum { FPM_FIELD_AUTO = 0, FPM_FIELD_GF64 = 64, FPM_FIELD_GF128 = 128 };
+
+/* MulPlan (polymul.hpp:36-43). */
+typedef struct {
+  uint64_t n_bits;
+  uint32_t log2_n;
+  uint32_t field_degree;
+  uint32_t log2_field_degree;
+  uint32_t l;
+  uint64_t n_p;
+} fpm_plan;
+
+/* Per-stage seconds in the order of StageSeconds (polymul.hpp:51-59):
+ * basiscvt, encode, butterfly, pointwise, ibutterfly, decode, ibasiscvt. */
+#define FPM_NUM_STAGES 7
+
+const char* fpm_last_error(void);
+/* Library version string. */
+const char* fpm_version(void);
+/* Number of CUDA devices visible (0 when none); never fails. */
+int fpm_device_count(void);
+
+/* plan_mul (proj/src/polymul.cpp:187-219).  field: FPM_FIELD_*.  The GPU pipeline always runs
+ * GF(2^128); plan_mul still reports the reference's choice for the requested field. */
+fpm_status fpm_plan_mul(size_t a_bits, size_t b_bits, int field, fpm_plan* out);
+
+/* fp_polymul (polymul.hpp:74-75, polymul.cpp:223-239) on host buffers.
+ * c receives ceil((a_bits+b_bits-1)/64) words (bits >= a_bits+b_bits-1 cleared); nothing is
+ * written when either length is 0.  field: FPM_FIELD_AUTO or FPM_FIELD_GF128 (GF(2^64) is not
+ * built yet -> FPM_EINVAL).  stage_seconds: NULL or double[FPM_NUM_STAGES] (accumulated).
+ * device: CUDA ordinal. */
+fpm_status fpm_polymul(const uint64_t* a, size_t a_bits, const uint64_t* b, size_t b_bits, uint64_t* c,
+                       int field, int device, double* stage_seconds);
+
+/* The same on device-resident buffers (d_c sized as above).  Uses the calling thread's current
+ * device.  Synchronizes `stream` only when stage_seconds != NULL. */
+fpm_status fpm_polymul_dev(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_t b_bits, uint64_t* d_c,
+                           int field, void* stream, double* stage_seconds);
+
+/* `count` independent products of equal shapes (BASELINE config 2): operand k is at
+ * d_a + k*a_stride_words etc.; product k at d_c + k*c_stride_words.  Requires
+ * next_pow2(2*max(a_bits,b_bits)) <= 2^17 bits (one CTA per product, all in shared memory). */
+fpm_status fpm_polymul_batch_dev(const uint64_t* d_a, size_t a_bits, size_t a_stride_words, const uint64_t* d_b,
+                                 size_t b_bits, size_t b_stride_words, uint64_t* d_c, size_t c_stride_words,
+                                 size_t count, void* stream);
+
+/* ---- stage entry points on device buffers, field GF(2^128) ---- */
+
+/* basis_cvt (proj/include/fpmul/basis_convert.hpp:34-35): in place on n_bits (power of two)
+ * bits; bits >= content_bits must be zero (content_bits = (size_t)-1 for "all"). */
+fpm_status fpm_basis_cvt_dev(uint64_t* d_w, size_t n_bits, size_t content_bits, void* stream);
+/* i_basis_cvt (basis_convert.hpp:37). */
+fpm_status fpm_i_basis_cvt_dev(uint64_t* d_w, size_t n_bits, void* stream);
+/* encode<gf128> with make_partition_spec<gf128>(l) (encode.hpp:84-86, 40-41): d_poly holds
+ * 128*2^l bits, d_ev receives 2^l elements.  l < 64. */
+fpm_status fpm_encode_dev(const uint64_t* d_poly, unsigned l, uint64_t* d_ev, void* stream);
+/* decode<gf128> (encode.hpp:88-91): inverse of fpm_encode_dev. */
+fpm_status fpm_decode_dev(const uint64_t* d_ev, unsigned l, uint64_t* d_poly, void* stream);
+/* lch_butterfly / i_lch_butterfly<gf128> with plan_butterflies(l, e_{l+64}) (butterfly.hpp:58-68). */
+fpm_status fpm_butterfly_dev(uint64_t* d_ev, unsigned l, int inverse, void* stream);
+/* pointwise_mul<gf128> (polymul.hpp:78-80): d_out[i] = d_u[i]*d_v[i] over n elements (may alias). */
+fpm_status fpm_pointwise_dev(const uint64_t* d_u, const uint64_t* d_v, uint64_t* d_out, size_t n, void* stream);
+
+/* ---- host-buffer stage wrappers (synchronous; same semantics as the *_dev calls) ---- */
+fpm_status fpm_basis_cvt(uint64_t* w, size_t n_bits, size_t content_bits, int device);
+fpm_status fpm_i_basis_cvt(uint64_t* w, size_t n_bits, int device);
+fpm_status fpm_encode(const uint64_t* poly, unsigned l, uint64_t* ev, int device);
+fpm_status fpm_decode(const uint64_t* ev, unsigned l, uint64_t* poly, int device);
+fpm_status fpm_butterfly(uint64_t* ev, unsigned l, int inverse, int device);
+fpm_status fpm_pointwise(const uint64_t* u, const uint64_t* v, uint64_t* out, size_t n, int device);
+fpm_status fpm_gf128_mul(const uint64_t* a, const uint64_t* b, uint64_t* out, size_t n, int device);
+
+/* Field tables as built by the library (CantorField<gf128>::basis, EncodeMatrix<gf128>::row /
+ * inv_row): each 128 elements x {lo, hi}.  Host-only, no GPU needed. */
+fpm_status fpm_tables128(uint64_t* cantor, uint64_t* rows, uint64_t* inv_rows);
+
+/* Number of kernel launches issued by this library on the calling thread since the last reset
+ * (for the bench's gpu_launches accounting). */
+uint64_t fpm_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FPMUL_B200_H_ */

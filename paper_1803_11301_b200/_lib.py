@@ -1,0 +1,263 @@
+"""ctypes binding of libfpmul_b200.so (include/fpmul_b200.h).
+
+Host-buffer calls take numpy uint64 arrays (packed little-endian words, coefficient k = bit k%64
+of word k//64, as proj/include/fpmul/bitpoly.hpp).  Device calls take torch CUDA tensors (any
+8-byte dtype) and run on the current torch stream.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfpmul_b200.so")
+
+FIELD_AUTO, FIELD_GF64, FIELD_GF128 = 0, 64, 128
+NUM_STAGES = 7
+# StageSeconds order (proj/include/fpmul/polymul.hpp:51-59)
+STAGE_NAMES = ("basiscvt", "encode", "butterfly", "pointwise", "ibutterfly", "decode", "ibasiscvt")
+
+_u64p = C.POINTER(C.c_uint64)
+
+
+class FpmError(RuntimeError):
+    """A CUDA-side failure (FPM_ECUDA / FPM_ENOMEM)."""
+
+
+class _Plan(C.Structure):
+    _fields_ = [("n_bits", C.c_uint64), ("log2_n", C.c_uint32), ("field_degree", C.c_uint32),
+                ("log2_field_degree", C.c_uint32), ("l", C.c_uint32), ("n_p", C.c_uint64)]
+
+
+_LIB = None
+
+
+def lib():
+    """Loads the in-tree CUDA library; raises if it was not built (no fallback exists)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise FpmError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                           "(there is no CPU fallback for the B200 path)")
+        L = C.CDLL(LIB_PATH)
+        vp = C.c_void_p
+        sz = C.c_size_t
+        L.fpm_last_error.restype = C.c_char_p
+        L.fpm_version.restype = C.c_char_p
+        L.fpm_launch_count.restype = C.c_uint64
+        L.fpm_launch_count.argtypes = [C.c_int]
+        L.fpm_plan_mul.argtypes = [sz, sz, C.c_int, C.POINTER(_Plan)]
+        L.fpm_polymul.argtypes = [_u64p, sz, _u64p, sz, _u64p, C.c_int, C.c_int, C.POINTER(C.c_double)]
+        L.fpm_polymul_dev.argtypes = [vp, sz, vp, sz, vp, C.c_int, vp, C.POINTER(C.c_double)]
+        L.fpm_polymul_batch_dev.argtypes = [vp, sz, sz, vp, sz, sz, vp, sz, sz, vp]
+        L.fpm_basis_cvt_dev.argtypes = [vp, sz, sz, vp]
+        L.fpm_i_basis_cvt_dev.argtypes = [vp, sz, vp]
+        L.fpm_encode_dev.argtypes = [vp, C.c_uint, vp, vp]
+        L.fpm_decode_dev.argtypes = [vp, C.c_uint, vp, vp]
+        L.fpm_butterfly_dev.argtypes = [vp, C.c_uint, C.c_int, vp]
+        L.fpm_pointwise_dev.argtypes = [vp, vp, vp, sz, vp]
+        L.fpm_basis_cvt.argtypes = [_u64p, sz, sz, C.c_int]
+        L.fpm_i_basis_cvt.argtypes = [_u64p, sz, C.c_int]
+        L.fpm_encode.argtypes = [_u64p, C.c_uint, _u64p, C.c_int]
+        L.fpm_decode.argtypes = [_u64p, C.c_uint, _u64p, C.c_int]
+        L.fpm_butterfly.argtypes = [_u64p, C.c_uint, C.c_int, C.c_int]
+        L.fpm_pointwise.argtypes = [_u64p, _u64p, _u64p, sz, C.c_int]
+        L.fpm_gf128_mul.argtypes = [_u64p, _u64p, _u64p, sz, C.c_int]
+        L.fpm_tables128.argtypes = [_u64p, _u64p, _u64p]
+        _LIB = L
+    return _LIB
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = lib().fpm_last_error().decode()
+    if rc == 1:
+        raise ValueError(msg)
+    raise FpmError(msg)
+
+
+def _ptr(a: np.ndarray):
+    if a.dtype != np.uint64 or not a.flags["C_CONTIGUOUS"]:
+        raise TypeError("expected a C-contiguous uint64 array")
+    return a.ctypes.data_as(_u64p)
+
+
+def _words(bits: int) -> int:
+    return (bits + 63) // 64
+
+
+def _as_u64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.uint64)
+
+
+def device_count() -> int:
+    return int(lib().fpm_device_count())
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(lib().fpm_launch_count(int(reset)))
+
+
+def plan_mul(a_bits: int, b_bits: int, field: int = FIELD_AUTO) -> dict:
+    """plan_mul (proj/src/polymul.cpp:187-219)."""
+    p = _Plan()
+    _check(lib().fpm_plan_mul(a_bits, b_bits, field, C.byref(p)))
+    return {k: int(getattr(p, k)) for k, _ in _Plan._fields_}
+
+
+def tables128():
+    """(cantor, rows, inv_rows): CantorField<gf128> basis and EncodeMatrix<gf128> rows, each 256 words."""
+    out = [np.zeros(256, np.uint64) for _ in range(3)]
+    _check(lib().fpm_tables128(*[_ptr(o) for o in out]))
+    return tuple(out)
+
+
+# ----------------------------------------------------------------------------- host buffers
+def fp_polymul(a, a_bits: int, b, b_bits: int, field: int = FIELD_AUTO, device: int = 0,
+               stage_seconds: list | None = None) -> np.ndarray:
+    """fp_polymul (proj/src/polymul.cpp:223-239): returns ceil((a_bits+b_bits-1)/64) words."""
+    a, b = _as_u64(a), _as_u64(b)
+    if a.size < _words(a_bits) or b.size < _words(b_bits):
+        raise ValueError("fp_polymul: word arrays shorter than the declared bit lengths")
+    if a_bits == 0 or b_bits == 0:
+        return np.zeros(0, np.uint64)
+    c = np.zeros(_words(a_bits + b_bits - 1), np.uint64)
+    st = (C.c_double * NUM_STAGES)()
+    _check(lib().fpm_polymul(_ptr(a), a_bits, _ptr(b), b_bits, _ptr(c), field, device,
+                             st if stage_seconds is not None else None))
+    if stage_seconds is not None:
+        stage_seconds[:] = list(st)
+    return c
+
+
+def basis_cvt(w, n_bits: int, content_bits: int | None = None, device: int = 0) -> np.ndarray:
+    """basis_cvt (proj/src/basis_convert.cpp:337-341); returns the converted copy."""
+    w = _as_u64(w).copy()
+    if w.size < _words(n_bits):
+        raise ValueError("basis_cvt: word array shorter than n_bits")
+    cb = (1 << 64) - 1 if content_bits is None else content_bits
+    _check(lib().fpm_basis_cvt(_ptr(w), n_bits, cb, device))
+    return w
+
+
+def i_basis_cvt(w, n_bits: int, device: int = 0) -> np.ndarray:
+    w = _as_u64(w).copy()
+    if w.size < _words(n_bits):
+        raise ValueError("i_basis_cvt: word array shorter than n_bits")
+    _check(lib().fpm_i_basis_cvt(_ptr(w), n_bits, device))
+    return w
+
+
+def encode(poly, l: int, device: int = 0) -> np.ndarray:
+    """encode<gf128> with make_partition_spec<gf128>(l) (proj/src/encode.cpp:165-193)."""
+    poly = _as_u64(poly)
+    if l >= 64:
+        raise ValueError("PartitionSpec: l must satisfy l < m/2")
+    if poly.size * 64 != (128 << l):
+        raise ValueError("encode: input length must be m * n_p bits")
+    ev = np.zeros(2 << l, np.uint64)
+    _check(lib().fpm_encode(_ptr(poly), l, _ptr(ev), device))
+    return ev
+
+
+def decode(ev, l: int, device: int = 0) -> np.ndarray:
+    ev = _as_u64(ev)
+    if l >= 64:
+        raise ValueError("PartitionSpec: l must satisfy l < m/2")
+    if ev.size != (2 << l):
+        raise ValueError("decode: length must equal n_p")
+    poly = np.zeros(max(1, (128 << l) // 64), np.uint64)
+    _check(lib().fpm_decode(_ptr(ev), l, _ptr(poly), device))
+    return poly
+
+
+def butterfly(ev, l: int, inverse: bool = False, device: int = 0) -> np.ndarray:
+    ev = _as_u64(ev).copy()
+    if ev.size != (2 << l):
+        raise ValueError("lch_butterfly: vector length does not match plan")
+    _check(lib().fpm_butterfly(_ptr(ev), l, int(inverse), device))
+    return ev
+
+
+def lch_butterfly(ev, l: int, device: int = 0) -> np.ndarray:
+    """lch_butterfly<gf128> with plan_butterflies(l, make_partition_spec(l).base)."""
+    return butterfly(ev, l, False, device)
+
+
+def i_lch_butterfly(ev, l: int, device: int = 0) -> np.ndarray:
+    return butterfly(ev, l, True, device)
+
+
+def pointwise_mul(u, v, device: int = 0) -> np.ndarray:
+    """pointwise_mul<gf128> (proj/src/polymul.cpp:241-257)."""
+    u, v = _as_u64(u), _as_u64(v)
+    if u.size != v.size:
+        raise ValueError("pointwise_mul: length mismatch")
+    out = np.zeros_like(u)
+    _check(lib().fpm_pointwise(_ptr(u), _ptr(v), _ptr(out), u.size // 2, device))
+    return out
+
+
+def gf128_mul(a, b, device: int = 0) -> np.ndarray:
+    return pointwise_mul(a, b, device)
+
+
+# ----------------------------------------------------------------------------- device buffers
+def _dptr(t) -> int:
+    if t is None:
+        return 0
+    if not t.is_cuda or not t.is_contiguous() or t.element_size() != 8:
+        raise TypeError("expected a contiguous CUDA tensor of 8-byte elements")
+    return t.data_ptr()
+
+
+def _stream(stream):
+    if stream is not None:
+        return stream
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+def fp_polymul_dev(a, a_bits: int, b, b_bits: int, c, field: int = FIELD_AUTO, stream=None,
+                   stage_seconds: list | None = None) -> None:
+    """fp_polymul on device-resident tensors; c must hold ceil((a_bits+b_bits-1)/64) words."""
+    st = (C.c_double * NUM_STAGES)()
+    _check(lib().fpm_polymul_dev(_dptr(a), a_bits, _dptr(b), b_bits, _dptr(c), field, _stream(stream),
+                                 st if stage_seconds is not None else None))
+    if stage_seconds is not None:
+        stage_seconds[:] = [x + y for x, y in zip(stage_seconds, st)] if len(stage_seconds) == NUM_STAGES else list(st)
+
+
+def fp_polymul_batch_dev(a, a_bits: int, a_stride: int, b, b_bits: int, b_stride: int, c, c_stride: int,
+                         count: int, stream=None) -> None:
+    _check(lib().fpm_polymul_batch_dev(_dptr(a), a_bits, a_stride, _dptr(b), b_bits, b_stride, _dptr(c),
+                                       c_stride, count, _stream(stream)))
+
+
+def stage_dev(name: str, *args, stream=None) -> None:
+    """Device-buffer stage entry points: basis_cvt(w, n_bits, content_bits), i_basis_cvt(w, n_bits),
+    encode(poly, l, ev), decode(ev, l, poly), butterfly(ev, l, inverse), pointwise(u, v, out, n)."""
+    L, s = lib(), _stream(stream)
+    if name == "basis_cvt":
+        w, n_bits, cb = args
+        _check(L.fpm_basis_cvt_dev(_dptr(w), n_bits, cb, s))
+    elif name == "i_basis_cvt":
+        w, n_bits = args
+        _check(L.fpm_i_basis_cvt_dev(_dptr(w), n_bits, s))
+    elif name == "encode":
+        poly, l, ev = args
+        _check(L.fpm_encode_dev(_dptr(poly), l, _dptr(ev), s))
+    elif name == "decode":
+        ev, l, poly = args
+        _check(L.fpm_decode_dev(_dptr(ev), l, _dptr(poly), s))
+    elif name == "butterfly":
+        ev, l, inv = args
+        _check(L.fpm_butterfly_dev(_dptr(ev), l, int(inv), s))
+    elif name == "pointwise":
+        u, v, out, n = args
+        _check(L.fpm_pointwise_dev(_dptr(u), _dptr(v), _dptr(out), n, s))
+    else:
+        raise ValueError(f"unknown stage {name!r}")

@@ -1,0 +1,498 @@
+// fpm_capi.cu -- the C-ABI (include/fpmul_b200.h): device tables, the fp_polymul pipeline and
+// the stage entry points.  The pipeline follows run_pipeline<gf128> (proj/src/polymul.cpp:78-135):
+//
+//   per operand X in (a, b):  load+zero-pad -> basis_cvt -> encode -> forward butterflies
+//   pointwise -> inverse butterflies -> decode -> i_basis_cvt -> trim (polymul.cpp:237)
+//
+// B200 specifics: everything stays in HBM (inputs are read once, the product written once); the
+// bottom 12 butterfly layers run on 64 KiB shared-memory tiles and the pointwise product is fused
+// between operand b's last forward tile layers and the first inverse tile layers; products with
+// n <= 2^17 bits run whole inside one CTA (k_batch.cu).  There is no CPU fallback: without a
+// device every entry point returns FPM_ECUDA.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fpmul_b200.h"
+#include "fpm_internal.h"
+#include "gf128.cuh"
+
+namespace fpm {
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+template <class Fn>
+fpm_status guard(Fn&& fn) {
+  try {
+    fn();
+    return FPM_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return (fpm_status)e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = e.what();
+    return FPM_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FPM_ECUDA;
+  }
+}
+
+void require_device() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    throw Error(kCuda, std::string("no CUDA device available (the B200 path has no CPU fallback): ") +
+                           (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
+}
+
+inline uint4 to4(U128 v) { return make_uint4((uint32_t)v.lo, (uint32_t)(v.lo >> 32), (uint32_t)v.hi, (uint32_t)(v.hi >> 32)); }
+
+// ------------------------------------------------------------------ small helper kernels
+// dst[0 .. dst_words) <- src bits [0, src_bits), zero above.
+__global__ void load_operand_kernel(uint64_t* __restrict__ dst, uint64_t dst_words, const uint64_t* __restrict__ src,
+                                    uint64_t src_bits) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < dst_words; k += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t v = 0;
+    if (k * 64 < src_bits) {
+      v = src[k];
+      if (src_bits - k * 64 < 64) v &= (((uint64_t)1) << (src_bits - k * 64)) - 1;
+    }
+    dst[k] = v;
+  }
+}
+
+__global__ void store_product_kernel(uint64_t* __restrict__ dst, const uint64_t* __restrict__ src, uint64_t out_bits) {
+  const uint64_t words = (out_bits + 63) / 64;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < words; k += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t v = src[k];
+    if (k == words - 1 && (out_bits & 63)) v &= (((uint64_t)1) << (out_bits & 63)) - 1;
+    dst[k] = v;
+  }
+}
+
+int grid_1d(uint64_t n, int per_sm = 16) {
+  int dev, sms;
+  FPM_CUDA(cudaGetDevice(&dev));
+  FPM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const uint64_t g = std::min<uint64_t>((n + 255) / 256, (uint64_t)sms * per_sm);
+  return (int)(g ? g : 1);
+}
+
+// ------------------------------------------------------------------ plan (polymul.cpp:187-219)
+unsigned log2_ceil(size_t n) {
+  unsigned l = 0;
+  while (((size_t)1 << l) < n) ++l;
+  return l;
+}
+bool field_supports(unsigned m, size_t n_bits) {  // polymul.cpp:45-49
+  if (n_bits < m) return false;
+  const unsigned l = log2_ceil(n_bits) - log2_ceil(m);
+  return l < m / 2 && l + 1 < m / 2;
+}
+fpm_plan plan_mul(size_t a_bits, size_t b_bits, int field) {
+  if (a_bits == 0 || b_bits == 0) throw Error(kInvalid, "plan_mul: input lengths must be positive");
+  const size_t mx = a_bits > b_bits ? a_bits : b_bits;
+  if (mx > ((size_t)1 << 62)) throw Error(kInvalid, "plan_mul: input length out of range");
+  size_t n = (size_t)1 << log2_ceil(2 * mx);
+  unsigned m = 0;
+  if (field == FPM_FIELD_GF64) m = 64;
+  else if (field == FPM_FIELD_GF128) m = 128;
+  else if (field == FPM_FIELD_AUTO) m = field_supports(64, n < 64 ? 64 : n) ? 64 : 128;
+  else throw Error(kInvalid, "plan_mul: unknown field choice");
+  if (n < m) n = m;
+  if (!field_supports(m, n)) throw Error(kInvalid, "plan_mul: length exceeds the field's supported bound");
+  fpm_plan p{};
+  p.n_bits = n;
+  p.log2_n = log2_ceil(n);
+  p.field_degree = m;
+  p.log2_field_degree = m == 64 ? 6 : 7;
+  p.l = p.log2_n - p.log2_field_degree;
+  p.n_p = (uint64_t)1 << p.l;
+  return p;
+}
+
+// ------------------------------------------------------------------ stage timing
+struct StageClock {
+  cudaStream_t s;
+  double* out;
+  std::vector<std::pair<int, cudaEvent_t>> marks;
+  StageClock(cudaStream_t st, double* o) : s(st), out(o) {}
+  void mark(int stage) {  // stage = index the interval ending at the NEXT mark belongs to
+    if (!out) return;
+    cudaEvent_t e;
+    FPM_CUDA(cudaEventCreate(&e));
+    FPM_CUDA(cudaEventRecord(e, s));
+    marks.emplace_back(stage, e);
+  }
+  void finish() {
+    if (!out) return;
+    mark(-1);
+    FPM_CUDA(cudaEventSynchronize(marks.back().second));
+    for (size_t k = 0; k + 1 < marks.size(); ++k) {
+      float ms = 0;
+      FPM_CUDA(cudaEventElapsedTime(&ms, marks[k].second, marks[k + 1].second));
+      if (marks[k].first >= 0) out[marks[k].first] += ms * 1e-3;
+    }
+    for (auto& m : marks) cudaEventDestroy(m.second);
+    marks.clear();
+  }
+};
+enum { kStBasis = 0, kStEncode, kStBfly, kStPointwise, kStIBfly, kStDecode, kStIBasis };
+
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t s;
+  DevBuf(size_t bytes, cudaStream_t st) : s(st) { FPM_CUDA(cudaMallocAsync(&p, bytes, st)); }
+  ~DevBuf() { if (p) cudaFreeAsync(p, s); }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_t b_bits, uint64_t* d_c,
+                    int field, cudaStream_t s, double* stages) {
+  if (!a_bits || !b_bits) return;
+  if (field == FPM_FIELD_GF64)
+    throw Error(kInvalid, "fp_polymul: the GF(2^64) pipeline is not built on the GPU (use GF(2^128) or auto)");
+  if (field != FPM_FIELD_AUTO && field != FPM_FIELD_GF128) throw Error(kInvalid, "fp_polymul: unknown field choice");
+  const fpm_plan p = plan_mul(a_bits, b_bits, FPM_FIELD_GF128);
+  const size_t out_bits = a_bits + b_bits - 1;
+  StageClock clk(s, stages);
+  if (p.l <= 10) {  // whole product in one CTA
+    clk.mark(kStPointwise);
+    polymul_batch_device(d_a, a_bits, 0, d_b, b_bits, 0, d_c, 0, 1, s);
+    clk.finish();
+    return;
+  }
+  const unsigned l = p.l, T = fft_tile_log2(l);
+  const size_t n = p.n_bits, n_p = p.n_p;
+  DevBuf P(n / 8, s), EA(n_p * 16, s), EB(n_p * 16, s);
+  const uint64_t* xs[2] = {d_a, d_b};
+  const size_t xbits[2] = {a_bits, b_bits};
+  uint4* es[2] = {EA.as<uint4>(), EB.as<uint4>()};
+  for (int k = 0; k < 2; ++k) {
+    clk.mark(kStBasis);
+    const uint64_t half_words = n / 128;  // n/2 bits in uint64 words
+    load_operand_kernel<<<grid_1d(half_words), 256, 0, s>>>(P.as<uint64_t>(), half_words, xs[k], xbits[k]);
+    FPM_LAUNCH_CHECK();
+    size_t count = (size_t)1 << log2_ceil(xbits[k]);
+    if (count < 32) count = 32;
+    basis_cvt_device(P.as<uint32_t>(), count, xbits[k], false, s);
+    clk.mark(kStEncode);
+    encode_device_rows(P.as<uint32_t>(), l, es[k], 64, s);
+    clk.mark(kStBfly);
+    butterfly_top_device(es[k], l, T, false, s);
+    if (k == 0) butterfly_tile_device(es[k], l, T, false, s);
+  }
+  clk.mark(kStPointwise);  // + operand b's bottom T forward and the bottom T inverse layers (fused)
+  butterfly_tile_fused_device(EA.as<uint4>(), EB.as<uint4>(), l, T, s);
+  clk.mark(kStIBfly);
+  butterfly_top_device(EB.as<uint4>(), l, T, true, s);
+  clk.mark(kStDecode);
+  decode_device(EB.as<uint4>(), l, P.as<uint32_t>(), s);
+  clk.mark(kStIBasis);
+  basis_cvt_device(P.as<uint32_t>(), n, n, true, s);
+  store_product_kernel<<<grid_1d((out_bits + 63) / 64), 256, 0, s>>>(d_c, P.as<uint64_t>(), out_bits);
+  FPM_LAUNCH_CHECK();
+  clk.finish();
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    require_device();
+    FPM_CUDA(cudaGetDevice(&prev));
+    if (dev != prev) FPM_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+cudaStream_t host_stream(int dev) {
+  static std::mutex mu;
+  static cudaStream_t streams[64] = {};
+  std::lock_guard<std::mutex> lock(mu);
+  if (!streams[dev]) FPM_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+  return streams[dev];
+}
+
+}  // namespace
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+const DeviceTables& device_tables(int dev) {
+  static std::mutex mu;
+  static DeviceTables tabs[64];
+  static bool have[64];
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 0 || dev >= 64) throw Error(kInvalid, "device ordinal out of range");
+  if (have[dev]) return tabs[dev];
+  const FieldTables& ft = field_tables();
+  std::vector<uint4> cantor(128), rows(128), inv(128), enc(kM4RUint4), dec(kM4RUint4), c2p(4 * 512);
+  for (int i = 0; i < 128; ++i) { cantor[i] = to4(ft.cantor[i]); rows[i] = to4(ft.enc_rows[i]); inv[i] = to4(ft.inv_rows[i]); }
+  for (int c = 0; c < kM4RChunks; ++c)
+    for (int v = 0; v < 16; ++v) {
+      U128 e, d;
+      for (int j = 0; j < 4; ++j)
+        if (v >> j & 1) {
+          e.lo ^= ft.enc_rows[4 * c + j].lo; e.hi ^= ft.enc_rows[4 * c + j].hi;
+          d.lo ^= ft.inv_rows[4 * c + j].lo; d.hi ^= ft.inv_rows[4 * c + j].hi;
+        }
+      for (int r = 0; r < kM4RCopies; ++r) {
+        enc[(c * 16 + v) * kM4RCopies + r] = to4(e);
+        dec[(c * 16 + v) * kM4RCopies + r] = to4(d);
+      }
+    }
+  for (int part = 0; part < 4; ++part)
+    for (int e = 0; e < 512; ++e) {
+      U128 acc;
+      for (int k = 0; k < 9; ++k)
+        if (e >> k & 1) {
+          const int idx = 9 * part + k + 1;  // C2P(2 * (e << 9 part)): Cantor bit 9p+k+1
+          acc.lo ^= ft.cantor[idx].lo;
+          acc.hi ^= ft.cantor[idx].hi;
+        }
+      c2p[part * 512 + e] = to4(acc);
+    }
+  int prev;
+  FPM_CUDA(cudaGetDevice(&prev));
+  FPM_CUDA(cudaSetDevice(dev));
+  DeviceTables t;
+  auto up = [](uint4** dst, const std::vector<uint4>& v) {
+    FPM_CUDA(cudaMalloc(dst, v.size() * sizeof(uint4)));
+    FPM_CUDA(cudaMemcpy(*dst, v.data(), v.size() * sizeof(uint4), cudaMemcpyHostToDevice));
+  };
+  up(&t.cantor, cantor); up(&t.enc_rows, rows); up(&t.inv_rows, inv);
+  up(&t.enc_m4r, enc); up(&t.dec_m4r, dec); up(&t.c2p, c2p);
+  // Keep freed pool memory cached: the pipeline allocates its scratch per call (reentrant).
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  FPM_CUDA(cudaSetDevice(prev));
+  tabs[dev] = t;
+  have[dev] = true;
+  return tabs[dev];
+}
+
+}  // namespace fpm
+
+namespace fpm {
+namespace {
+template <class Fn>
+fpm_status host_call(int device, Fn&& fn) {
+  return guard([&] {
+    DeviceGuard g(device);
+    cudaStream_t s = host_stream(device);
+    fn(s);
+    FPM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+}  // namespace
+}  // namespace fpm
+
+using namespace fpm;
+
+extern "C" {
+
+const char* fpm_last_error(void) { return g_err.c_str(); }
+const char* fpm_version(void) { return "fpmul_b200 0.1 (sm_100a)"; }
+int fpm_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+uint64_t fpm_launch_count(int reset) {
+  return reset ? g_launches.exchange(0) : g_launches.load();
+}
+
+fpm_status fpm_plan_mul(size_t a_bits, size_t b_bits, int field, fpm_plan* out) {
+  return guard([&] {
+    if (!out) throw Error(kInvalid, "plan_mul: null output");
+    *out = plan_mul(a_bits, b_bits, field);
+  });
+}
+
+fpm_status fpm_tables128(uint64_t* cantor, uint64_t* rows, uint64_t* inv_rows) {
+  return guard([&] {
+    const FieldTables& t = field_tables();
+    for (int i = 0; i < 128; ++i) {
+      if (cantor) { cantor[2 * i] = t.cantor[i].lo; cantor[2 * i + 1] = t.cantor[i].hi; }
+      if (rows) { rows[2 * i] = t.enc_rows[i].lo; rows[2 * i + 1] = t.enc_rows[i].hi; }
+      if (inv_rows) { inv_rows[2 * i] = t.inv_rows[i].lo; inv_rows[2 * i + 1] = t.inv_rows[i].hi; }
+    }
+  });
+}
+
+fpm_status fpm_polymul_dev(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_t b_bits, uint64_t* d_c,
+                           int field, void* stream, double* stage_seconds) {
+  return guard([&] {
+    require_device();
+    polymul_device(d_a, a_bits, d_b, b_bits, d_c, field, (cudaStream_t)stream, stage_seconds);
+  });
+}
+
+fpm_status fpm_polymul(const uint64_t* a, size_t a_bits, const uint64_t* b, size_t b_bits, uint64_t* c, int field,
+                       int device, double* stage_seconds) {
+  return guard([&] {
+    if (!a_bits || !b_bits) return;
+    (void)plan_mul(a_bits, b_bits, field == FPM_FIELD_GF64 ? FPM_FIELD_GF64 : FPM_FIELD_GF128);
+    DeviceGuard g(device);
+    cudaStream_t s = host_stream(device);
+    const size_t wa = (a_bits + 63) / 64, wb = (b_bits + 63) / 64, wc = (a_bits + b_bits - 1 + 63) / 64;
+    DevBuf A(wa * 8, s), B(wb * 8, s), C(wc * 8, s);
+    FPM_CUDA(cudaMemcpyAsync(A.p, a, wa * 8, cudaMemcpyHostToDevice, s));
+    FPM_CUDA(cudaMemcpyAsync(B.p, b, wb * 8, cudaMemcpyHostToDevice, s));
+    polymul_device(A.as<uint64_t>(), a_bits, B.as<uint64_t>(), b_bits, C.as<uint64_t>(), field, s, stage_seconds);
+    FPM_CUDA(cudaMemcpyAsync(c, C.p, wc * 8, cudaMemcpyDeviceToHost, s));
+    FPM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+fpm_status fpm_polymul_batch_dev(const uint64_t* d_a, size_t a_bits, size_t a_stride_words, const uint64_t* d_b,
+                                 size_t b_bits, size_t b_stride_words, uint64_t* d_c, size_t c_stride_words,
+                                 size_t count, void* stream) {
+  return guard([&] {
+    require_device();
+    if (!a_bits || !b_bits || !count) return;
+    polymul_batch_device(d_a, a_bits, a_stride_words, d_b, b_bits, b_stride_words, d_c, c_stride_words, count,
+                         (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_basis_cvt_dev(uint64_t* d_w, size_t n_bits, size_t content_bits, void* stream) {
+  return guard([&] {
+    require_device();
+    if (n_bits == 0 || (n_bits & (n_bits - 1))) throw Error(kInvalid, "basis_cvt: length must be a power of two");
+    if (n_bits <= 2) return;  // identity (basis_convert.cpp:280)
+    if (n_bits < 64) throw Error(kInvalid, "basis_cvt: device arrays must hold at least one 64-bit word");
+    basis_cvt_device(reinterpret_cast<uint32_t*>(d_w), n_bits, content_bits ? std::min(content_bits, n_bits) : 1,
+                     false, (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_i_basis_cvt_dev(uint64_t* d_w, size_t n_bits, void* stream) {
+  return guard([&] {
+    require_device();
+    if (n_bits == 0 || (n_bits & (n_bits - 1))) throw Error(kInvalid, "basis_cvt: length must be a power of two");
+    if (n_bits <= 2) return;
+    if (n_bits < 64) throw Error(kInvalid, "basis_cvt: device arrays must hold at least one 64-bit word");
+    basis_cvt_device(reinterpret_cast<uint32_t*>(d_w), n_bits, n_bits, true, (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_encode_dev(const uint64_t* d_poly, unsigned l, uint64_t* d_ev, void* stream) {
+  return guard([&] {
+    require_device();
+    if (l >= 64) throw Error(kInvalid, "PartitionSpec: l must satisfy l < m/2");
+    encode_device(reinterpret_cast<const uint32_t*>(d_poly), l, reinterpret_cast<uint4*>(d_ev), (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_decode_dev(const uint64_t* d_ev, unsigned l, uint64_t* d_poly, void* stream) {
+  return guard([&] {
+    require_device();
+    if (l >= 64) throw Error(kInvalid, "PartitionSpec: l must satisfy l < m/2");
+    decode_device(reinterpret_cast<const uint4*>(d_ev), l, reinterpret_cast<uint32_t*>(d_poly), (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_butterfly_dev(uint64_t* d_ev, unsigned l, int inverse, void* stream) {
+  return guard([&] {
+    require_device();
+    if (l >= 64) throw Error(kInvalid, "PartitionSpec: l must satisfy l < m/2");
+    if (l == 0) return;
+    butterfly_device(reinterpret_cast<uint4*>(d_ev), l, inverse != 0, (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_pointwise_dev(const uint64_t* d_u, const uint64_t* d_v, uint64_t* d_out, size_t n, void* stream) {
+  return guard([&] {
+    require_device();
+    pointwise_device(reinterpret_cast<const uint4*>(d_u), reinterpret_cast<const uint4*>(d_v),
+                     reinterpret_cast<uint4*>(d_out), n, (cudaStream_t)stream);
+  });
+}
+
+// ---- host wrappers
+
+fpm_status fpm_basis_cvt(uint64_t* w, size_t n_bits, size_t content_bits, int device) {
+  return host_call(device, [&](cudaStream_t s) {
+    if (n_bits == 0 || (n_bits & (n_bits - 1))) throw Error(kInvalid, "basis_cvt: length must be a power of two");
+    if (n_bits <= 2) return;
+    if (n_bits < 64) throw Error(kInvalid, "basis_cvt: device arrays must hold at least one 64-bit word");
+    DevBuf W(n_bits / 8, s);
+    FPM_CUDA(cudaMemcpyAsync(W.p, w, n_bits / 8, cudaMemcpyHostToDevice, s));
+    basis_cvt_device(W.as<uint32_t>(), n_bits, content_bits ? std::min(content_bits, n_bits) : 1, false, s);
+    FPM_CUDA(cudaMemcpyAsync(w, W.p, n_bits / 8, cudaMemcpyDeviceToHost, s));
+  });
+}
+
+fpm_status fpm_i_basis_cvt(uint64_t* w, size_t n_bits, int device) {
+  return host_call(device, [&](cudaStream_t s) {
+    if (n_bits == 0 || (n_bits & (n_bits - 1))) throw Error(kInvalid, "basis_cvt: length must be a power of two");
+    if (n_bits <= 2) return;
+    if (n_bits < 64) throw Error(kInvalid, "basis_cvt: device arrays must hold at least one 64-bit word");
+    DevBuf W(n_bits / 8, s);
+    FPM_CUDA(cudaMemcpyAsync(W.p, w, n_bits / 8, cudaMemcpyHostToDevice, s));
+    basis_cvt_device(W.as<uint32_t>(), n_bits, n_bits, true, s);
+    FPM_CUDA(cudaMemcpyAsync(w, W.p, n_bits / 8, cudaMemcpyDeviceToHost, s));
+  });
+}
+
+fpm_status fpm_encode(const uint64_t* poly, unsigned l, uint64_t* ev, int device) {
+  return host_call(device, [&](cudaStream_t s) {
+    if (l >= 64) throw Error(kInvalid, "PartitionSpec: l must satisfy l < m/2");
+    const size_t pb = ((size_t)128 << l) / 8, eb = ((size_t)16 << l);
+    DevBuf P(pb, s), E(eb, s);
+    FPM_CUDA(cudaMemcpyAsync(P.p, poly, pb, cudaMemcpyHostToDevice, s));
+    encode_device(P.as<uint32_t>(), l, E.as<uint4>(), s);
+    FPM_CUDA(cudaMemcpyAsync(ev, E.p, eb, cudaMemcpyDeviceToHost, s));
+  });
+}
+
+fpm_status fpm_decode(const uint64_t* ev, unsigned l, uint64_t* poly, int device) {
+  return host_call(device, [&](cudaStream_t s) {
+    if (l >= 64) throw Error(kInvalid, "PartitionSpec: l must satisfy l < m/2");
+    const size_t pb = ((size_t)128 << l) / 8, eb = ((size_t)16 << l);
+    DevBuf P(pb, s), E(eb, s);
+    FPM_CUDA(cudaMemcpyAsync(E.p, ev, eb, cudaMemcpyHostToDevice, s));
+    decode_device(E.as<uint4>(), l, P.as<uint32_t>(), s);
+    FPM_CUDA(cudaMemcpyAsync(poly, P.p, pb, cudaMemcpyDeviceToHost, s));
+  });
+}
+
+fpm_status fpm_butterfly(uint64_t* ev, unsigned l, int inverse, int device) {
+  return host_call(device, [&](cudaStream_t s) {
+    if (l >= 64) throw Error(kInvalid, "PartitionSpec: l must satisfy l < m/2");
+    if (l == 0) return;
+    const size_t eb = ((size_t)16 << l);
+    DevBuf E(eb, s);
+    FPM_CUDA(cudaMemcpyAsync(E.p, ev, eb, cudaMemcpyHostToDevice, s));
+    butterfly_device(E.as<uint4>(), l, inverse != 0, s);
+    FPM_CUDA(cudaMemcpyAsync(ev, E.p, eb, cudaMemcpyDeviceToHost, s));
+  });
+}
+
+fpm_status fpm_pointwise(const uint64_t* u, const uint64_t* v, uint64_t* out, size_t n, int device) {
+  return host_call(device, [&](cudaStream_t s) {
+    if (!n) return;
+    DevBuf U(n * 16, s), V(n * 16, s);
+    FPM_CUDA(cudaMemcpyAsync(U.p, u, n * 16, cudaMemcpyHostToDevice, s));
+    FPM_CUDA(cudaMemcpyAsync(V.p, v, n * 16, cudaMemcpyHostToDevice, s));
+    pointwise_device(U.as<uint4>(), V.as<uint4>(), U.as<uint4>(), n, s);
+    FPM_CUDA(cudaMemcpyAsync(out, U.p, n * 16, cudaMemcpyDeviceToHost, s));
+  });
+}
+
+fpm_status fpm_gf128_mul(const uint64_t* a, const uint64_t* b, uint64_t* out, size_t n, int device) {
+  return fpm_pointwise(a, b, out, n, device);
+}
+
+}  // extern "C"

@@ -1,0 +1,81 @@
+// fpm_internal.h -- shared host-side declarations of the CUDA library (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "fpm_tables.h"
+
+namespace fpm {
+
+// Status codes of the C-ABI (include/fpmul_b200.h).
+enum Status : int { kOk = 0, kInvalid = 1, kCuda = 2, kNoMem = 3 };
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define FPM_CUDA(x)                                                                            \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess)                                                                     \
+      throw ::fpm::Error(e_ == cudaErrorMemoryAllocation ? ::fpm::kNoMem : ::fpm::kCuda,        \
+                         std::string(#x) + ": " + cudaGetErrorString(e_));                     \
+  } while (0)
+// Every kernel launch of the library goes through this check; it also feeds fpm_launch_count().
+void note_launch();
+#define FPM_LAUNCH_CHECK()             \
+  do {                                 \
+    ::fpm::note_launch();              \
+    FPM_CUDA(cudaGetLastError());      \
+  } while (0)
+
+// Per-device immutable tables (uploaded once, lazily, under a mutex -- the reference's
+// thread-safe singletons CantorField::get / EncodeMatrix::get, cantor.cpp:136-140).
+struct DeviceTables {
+  uint4* cantor = nullptr;    // 128 x v_i
+  uint4* enc_rows = nullptr;  // 128 x r_j
+  uint4* inv_rows = nullptr;  // 128 rows of E^{-1}
+  uint4* enc_m4r = nullptr;   // 32 chunks x 16 x 8 copies (x*E by nibbles)
+  uint4* dec_m4r = nullptr;   // 32 chunks x 16 x 8 copies (x*E^{-1})
+  uint4* c2p = nullptr;       // 4 x 512: part p entry e = C2P(2 * (e << 9p))
+};
+
+// Twiddle generator inputs: w(i, b) = v_{l+64-i} ^ C2P(2b).
+struct TwiddleSrc {
+  const uint4* cantor;
+  const uint4* c2p;
+};
+
+const DeviceTables& device_tables(int device);
+
+// Basis conversion (k_basis.cu).  w: n_bits/32 uint32 words on the device, in place.
+// live_bits: forward only; bits >= live_bits are zero on entry (zero-tail skip).
+void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s);
+
+// Encode / decode (k_codec.cu).  poly has 128 * 2^l bits; ev has 2^l uint4.
+void encode_device(const uint32_t* poly, unsigned l, uint4* ev, cudaStream_t s);
+// rows_live = 64: rows >= 64 of poly are known zero (pipeline operands) and not read.
+void encode_device_rows(const uint32_t* poly, unsigned l, uint4* ev, int rows_live, cudaStream_t s);
+void decode_device(const uint4* ev, unsigned l, uint32_t* poly, cudaStream_t s);
+
+// Butterflies (k_fft.cu).
+void butterfly_device(uint4* ev, unsigned l, bool inverse, cudaStream_t s);
+void pointwise_device(const uint4* u, const uint4* v, uint4* out, size_t n, cudaStream_t s);
+// Fused: forward layers [0, T) of b's tiles, * a, inverse layers [0, T); top layers excluded.
+// Pipeline helpers exposing the split between top (global) and bottom (tile) layers.
+unsigned fft_tile_log2(unsigned l);
+void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, cudaStream_t s);
+void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, cudaStream_t s);
+void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, cudaStream_t s);
+
+// Whole small products in one CTA each (k_batch.cu); n_bits = padded product length <= 2^17.
+void polymul_batch_device(const uint64_t* a, size_t a_bits, size_t a_stride_words,
+                          const uint64_t* b, size_t b_bits, size_t b_stride_words, uint64_t* c,
+                          size_t c_stride_words, size_t count, cudaStream_t s);
+
+}  // namespace fpm

@@ -1,0 +1,129 @@
+// fpm_tables.cpp -- host construction of the GF(2^128) Cantor basis and encode matrices.
+// Restates proj/src/cantor.cpp:103-134 and proj/src/encode.cpp:52-70 (init-time only).
+#include "fpm_tables.h"
+
+#include <mutex>
+#include <stdexcept>
+
+namespace fpm {
+namespace {
+
+inline bool bit(U128 v, unsigned i) { return i < 64 ? (v.lo >> i) & 1 : (v.hi >> (i - 64)) & 1; }
+inline U128 unit(unsigned i) {
+  U128 r;
+  if (i < 64) r.lo = uint64_t{1} << i; else r.hi = uint64_t{1} << (i - 64);
+  return r;
+}
+inline U128 x(U128 a, U128 b) { return {a.lo ^ b.lo, a.hi ^ b.hi}; }
+inline bool nz(U128 a) { return a.lo | a.hi; }
+inline bool eq(U128 a, U128 b) { return a.lo == b.lo && a.hi == b.hi; }
+
+U128 row_mul(U128 v, const U128* rows) {
+  U128 acc;
+  for (unsigned j = 0; j < 128; ++j)
+    if (bit(v, j)) acc = x(acc, rows[j]);
+  return acc;
+}
+
+// x * rows = target over GF(2) (row-echelon; bitmat.hpp:79-111).
+bool solve(const U128* rows, U128 target, U128* out) {
+  U128 ech[128], tag[128];
+  unsigned lead[128], ne = 0;
+  for (unsigned i = 0; i < 128; ++i) {
+    U128 r = rows[i], t = unit(i);
+    for (unsigned j = 0; j < ne; ++j)
+      if (bit(r, lead[j])) { r = x(r, ech[j]); t = x(t, tag[j]); }
+    if (nz(r)) {
+      unsigned ld = 0;
+      while (!bit(r, ld)) ++ld;
+      ech[ne] = r; tag[ne] = t; lead[ne] = ld; ++ne;
+    }
+  }
+  U128 acc = target, sol;
+  for (unsigned j = 0; j < ne; ++j)
+    if (bit(acc, lead[j])) { acc = x(acc, ech[j]); sol = x(sol, tag[j]); }
+  if (nz(acc)) return false;
+  *out = sol;
+  return true;
+}
+
+bool invert(const U128* rows, U128* inv_out) {  // bitmat.hpp:55-74
+  U128 a[128], inv[128];
+  for (unsigned i = 0; i < 128; ++i) { a[i] = rows[i]; inv[i] = unit(i); }
+  for (unsigned col = 0; col < 128; ++col) {
+    unsigned piv = col;
+    while (piv < 128 && !bit(a[piv], col)) ++piv;
+    if (piv == 128) return false;
+    std::swap(a[col], a[piv]);
+    std::swap(inv[col], inv[piv]);
+    for (unsigned r = 0; r < 128; ++r)
+      if (r != col && bit(a[r], col)) { a[r] = x(a[r], a[col]); inv[r] = x(inv[r], inv[col]); }
+  }
+  for (unsigned i = 0; i < 128; ++i) inv_out[i] = inv[i];
+  return true;
+}
+
+void build(FieldTables& t) {
+  // Artin-Schreier map y -> y^2 + y, rows in polynomial representation.
+  U128 artin[128];
+  for (unsigned k = 0; k < 128; ++k) artin[k] = x(host_gf128_mul(unit(k), unit(k)), unit(k));
+  t.cantor[0] = unit(0);
+  for (unsigned i = 1; i < 128; ++i) {
+    U128 y;
+    if (!solve(artin, t.cantor[i - 1], &y))
+      throw std::runtime_error("CantorField: Artin-Schreier equation has no solution (wrong modulus?)");
+    y.lo &= ~uint64_t{1};  // of the roots {y, y+1} keep the one with bit 0 clear
+    if (!eq(x(host_gf128_mul(y, y), y), t.cantor[i - 1]))
+      throw std::runtime_error("CantorField: basis recurrence check failed");
+    t.cantor[i] = y;
+  }
+  U128 probe[128];
+  if (!invert(t.cantor, probe)) throw std::runtime_error("CantorField: basis-change matrix not invertible");
+  for (unsigned j = 0; j < 128; ++j) {
+    U128 r = unit(0);
+    for (unsigned k = 0; k < 7; ++k)
+      if ((j >> k) & 1) r = host_gf128_mul(r, t.cantor[64 - k]);
+    t.enc_rows[j] = r;
+  }
+  if (!invert(t.enc_rows, t.inv_rows))
+    throw std::runtime_error("EncodeMatrix: matrix is singular (field construction bug)");
+}
+
+}  // namespace
+
+U128 host_gf128_mul(U128 a, U128 b) {
+  // bit-serial, high bit first, modulo x^128 + x^7 + x^2 + x + 1 (gf.hpp:115-123)
+  U128 acc;
+  for (int i = 127; i >= 0; --i) {
+    const uint64_t carry = acc.hi >> 63;
+    acc.hi = (acc.hi << 1) | (acc.lo >> 63);
+    acc.lo = (acc.lo << 1) ^ (carry ? 0x87u : 0u);
+    if (bit(b, (unsigned)i)) acc = x(acc, a);
+  }
+  return acc;
+}
+
+U128 host_cantor_to_poly(const FieldTables& t, U128 c) { return row_mul(c, t.cantor); }
+
+const FieldTables& field_tables() {
+  static FieldTables tables;
+  static std::once_flag once;
+  std::call_once(once, [] { build(tables); });
+  return tables;
+}
+
+size_t digit_size(size_t count) {
+  size_t t = 2;
+  while (t <= (count / 2) / t) t *= t;
+  return t;
+}
+
+void build_schedule(Pass* out, size_t* n, size_t count, size_t unit) {
+  if (count <= 2) return;
+  const size_t t = digit_size(count);
+  for (size_t s = count; s >= 2 * t; s /= 2) out[(*n)++] = Pass{s * unit, (s / 2 - s / (2 * t)) * unit};
+  build_schedule(out, n, count / t, unit * t);
+  build_schedule(out, n, t, unit);
+}
+
+}  // namespace fpm

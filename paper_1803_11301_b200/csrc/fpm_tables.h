@@ -1,0 +1,38 @@
+// fpm_tables.h -- host-side field tables for the GF(2^128) Frobenius-partition pipeline.
+//
+// Product code (not the oracle): the CUDA library builds its own tables at first use, mirroring
+// the reference singletons CantorField<gf128> (proj/src/cantor.cpp:103-140) and
+// EncodeMatrix<gf128> (proj/src/encode.cpp:52-102).  They are uploaded once per device.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+namespace fpm {
+
+struct U128 {
+  uint64_t lo = 0, hi = 0;
+};
+
+struct FieldTables {
+  U128 cantor[128];    // v_i in polynomial representation (C2P rows), cantor.cpp:111-128
+  U128 enc_rows[128];  // r_j = prod_{bits k of j} v_{64-k}, encode.cpp:60-66
+  U128 inv_rows[128];  // rows of E^{-1}, encode.cpp:68-70
+};
+
+// Builds (once, thread-safe) and returns the tables; throws std::runtime_error on the same
+// construction failures the reference reports (cantor.cpp:108-133, encode.cpp:69-70).
+const FieldTables& field_tables();
+
+U128 host_gf128_mul(U128 a, U128 b);
+U128 host_cantor_to_poly(const FieldTables& t, U128 c);  // bitmat.hpp:29-35
+
+// Basis-conversion schedule (basis_convert.cpp:53-67) with the overflow-safe digit size
+// (the reference loops forever for arrays of >= 2^33 bits).
+struct Pass {
+  size_t span;   // S (bits)
+  size_t shift;  // D (bits)
+};
+size_t digit_size(size_t count);
+void build_schedule(Pass* out, size_t* n, size_t count, size_t unit);
+
+}  // namespace fpm

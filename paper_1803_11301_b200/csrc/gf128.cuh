@@ -1,0 +1,124 @@
+// gf128.cuh -- GF(2^128) arithmetic for sm_100a (no carry-less multiply instruction on the GPU).
+//
+// Field: x^128 + x^7 + x^2 + x + 1 (reference proj/include/fpmul/gf.hpp:115-123), element layout
+// uint4 {x,y,z,w} = 32-bit limbs, bit k of the element is bit (k%32) of limb k/32 -- byte-identical
+// to the reference u128 {lo, hi} (gf.hpp:24-52) so device EvalVecs are reference EvalVecs.
+//
+// Two multipliers, chosen per call site by measurement (profiles/r01_ubench_gf128_mul.log):
+//  * gf_mul():      generic a*b.  Karatsuba 128 -> 3x64 -> 9x32; each 32x32 carry-less product is
+//                   16 IMAD.WIDE.U32 on "holed" operands (every 4th bit), whose digit sums stay < 16 so
+//                   bit 4k+r of the integer product is the GF(2) coefficient; XOR-combine, mask.
+//                   IMAD runs on the FMA pipe, the masks/XORs on the ALU pipe (7.0 clk/mul/SM measured).
+//  * M4R tables:    w*x for a twiddle w shared by a whole butterfly block: 32 nibble-chunk tables of
+//                   w*(v << 4c), replicated 8x so a quarter-warp's LDS.128 never bank-conflicts
+//                   (4.2 clk/mul/SM measured).  Replaces PCLMULQDQ (reference gf_pclmul.cpp:25-30).
+#pragma once
+#include <cstdint>
+
+namespace fpm {
+
+__device__ __forceinline__ uint4 x4(uint4 a, uint4 b) { return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w); }
+__device__ __forceinline__ uint4 xor3(uint4 a, uint4 b, uint4 c) {
+  return make_uint4(a.x ^ b.x ^ c.x, a.y ^ b.y ^ c.y, a.z ^ b.z ^ c.z, a.w ^ b.w ^ c.w);
+}
+__device__ __forceinline__ bool is_zero(uint4 a) { return (a.x | a.y | a.z | a.w) == 0; }
+
+// 32x32 -> 64 carry-less product via integer multiply with 4-bit holes.
+__device__ __forceinline__ uint64_t clmul32(uint32_t a, uint32_t b) {
+  const uint32_t m = 0x11111111u;
+  const uint32_t a0 = a & m, a1 = a & (m << 1), a2 = a & (m << 2), a3 = a & (m << 3);
+  const uint32_t b0 = b & m, b1 = b & (m << 1), b2 = b & (m << 2), b3 = b & (m << 3);
+  const uint64_t r0 = (uint64_t)a0 * b0 ^ (uint64_t)a1 * b3 ^ (uint64_t)a2 * b2 ^ (uint64_t)a3 * b1;
+  const uint64_t r1 = (uint64_t)a0 * b1 ^ (uint64_t)a1 * b0 ^ (uint64_t)a2 * b3 ^ (uint64_t)a3 * b2;
+  const uint64_t r2 = (uint64_t)a0 * b2 ^ (uint64_t)a1 * b1 ^ (uint64_t)a2 * b0 ^ (uint64_t)a3 * b3;
+  const uint64_t r3 = (uint64_t)a0 * b3 ^ (uint64_t)a1 * b2 ^ (uint64_t)a2 * b1 ^ (uint64_t)a3 * b0;
+  const uint64_t M = 0x1111111111111111ull;
+  return (r0 & M) | (r1 & (M << 1)) | (r2 & (M << 2)) | (r3 & (M << 3));
+}
+
+__device__ __forceinline__ void clmul64(uint64_t a, uint64_t b, uint64_t& lo, uint64_t& hi) {
+  const uint32_t a0 = (uint32_t)a, a1 = (uint32_t)(a >> 32), b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+  const uint64_t p0 = clmul32(a0, b0), p2 = clmul32(a1, b1);
+  const uint64_t p1 = clmul32(a0 ^ a1, b0 ^ b1) ^ p0 ^ p2;
+  lo = p0 ^ (p1 << 32);
+  hi = p2 ^ (p1 >> 32);
+}
+
+// Fold a 256-bit product r0..r3 (64-bit words) modulo x^128 + x^7 + x^2 + x + 1
+// (the two-step fold of kernels.hpp:51-55 restated on 64-bit halves).
+__device__ __forceinline__ uint4 gf_reduce(uint64_t r0, uint64_t r1, uint64_t r2, uint64_t r3) {
+  const uint64_t o = (r3 >> 63) ^ (r3 >> 62) ^ (r3 >> 57);
+  r2 ^= o;
+  r1 ^= r3 ^ (r3 << 1) ^ (r3 << 2) ^ (r3 << 7);
+  r0 ^= r2 ^ (r2 << 1) ^ (r2 << 2) ^ (r2 << 7);
+  r1 ^= (r2 >> 63) ^ (r2 >> 62) ^ (r2 >> 57);
+  return make_uint4((uint32_t)r0, (uint32_t)(r0 >> 32), (uint32_t)r1, (uint32_t)(r1 >> 32));
+}
+
+__device__ __forceinline__ uint4 gf_mul(uint4 a, uint4 b) {
+  const uint64_t al = a.x | ((uint64_t)a.y << 32), ah = a.z | ((uint64_t)a.w << 32);
+  const uint64_t bl = b.x | ((uint64_t)b.y << 32), bh = b.z | ((uint64_t)b.w << 32);
+  uint64_t c0l, c0h, c2l, c2h, c1l, c1h;
+  clmul64(al, bl, c0l, c0h);
+  clmul64(ah, bh, c2l, c2h);
+  clmul64(al ^ ah, bl ^ bh, c1l, c1h);
+  c1l ^= c0l ^ c2l;
+  c1h ^= c0h ^ c2h;
+  return gf_reduce(c0l, c0h ^ c1l, c2l ^ c1h, c2h);
+}
+
+// w * x^k mod P for 0 <= k < 128 (shift then fold), used to build M4R rows.
+__device__ __forceinline__ uint4 gf_mul_xk(uint4 w, unsigned k) {
+  uint64_t lo = w.x | ((uint64_t)w.y << 32), hi = w.z | ((uint64_t)w.w << 32);
+  uint64_t r0, r1, r2, r3;
+  if (k == 0) { r0 = lo; r1 = hi; r2 = 0; r3 = 0; }
+  else if (k < 64) { r0 = lo << k; r1 = (hi << k) | (lo >> (64 - k)); r2 = hi >> (64 - k); r3 = 0; }
+  else if (k == 64) { r0 = 0; r1 = lo; r2 = hi; r3 = 0; }
+  else { const unsigned s = k - 64; r0 = 0; r1 = lo << s; r2 = (hi << s) | (lo >> (64 - s)); r3 = hi >> (64 - s); }
+  return gf_reduce(r0, r1, r2, r3);
+}
+
+// ---------------------------------------------------------------- M4R twiddle tables
+// Layout: entry (chunk c in [0,32), nibble v in [0,16)) replicated 8x; copy r of entry e at
+// uint4 index e*8 + r.  A lane always reads copy (lane & 7): the 8 lanes of a quarter-warp hit
+// 8 distinct 16-byte bank groups -> conflict-free LDS.128.
+constexpr int kM4RChunks = 32;
+constexpr int kM4REntries = kM4RChunks * 16;   // 512
+constexpr int kM4RCopies = 8;
+constexpr int kM4RUint4 = kM4REntries * kM4RCopies;  // 4096 uint4 = 64 KiB
+
+// Cooperative build of the table for twiddle w by the whole CTA (nthreads threads, tid).
+// rows_scratch: 128 uint4 of shared memory.
+__device__ __forceinline__ void m4r_build(uint4* __restrict__ tab, uint4* __restrict__ rows_scratch, uint4 w,
+                                          int tid, int nthreads) {
+  for (int k = tid; k < 128; k += nthreads) rows_scratch[k] = gf_mul_xk(w, (unsigned)k);
+  __syncthreads();
+  for (int e = tid; e < kM4REntries; e += nthreads) {
+    const int c = e >> 4, v = e & 15;
+    uint4 acc = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (v >> j & 1) acc = x4(acc, rows_scratch[4 * c + j]);
+#pragma unroll
+    for (int r = 0; r < kM4RCopies; ++r) tab[e * kM4RCopies + r] = acc;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint4 m4r_mul(const uint4* __restrict__ tab, uint4 x, int copy) {
+  uint4 acc0 = make_uint4(0, 0, 0, 0), acc1 = make_uint4(0, 0, 0, 0);
+  const uint32_t wds[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+#pragma unroll
+    for (int s = 0; s < 8; s += 2) {
+      const uint32_t n0 = (wds[q] >> (4 * s)) & 15u, n1 = (wds[q] >> (4 * s + 4)) & 15u;
+      const int c0 = q * 8 + s;
+      acc0 = x4(acc0, tab[((c0 * 16 + n0) << 3) + copy]);
+      acc1 = x4(acc1, tab[(((c0 + 1) * 16 + n1) << 3) + copy]);
+    }
+  }
+  return x4(acc0, acc1);
+}
+
+}  // namespace fpm

@@ -1,0 +1,229 @@
+// k_fft.cu -- LCH butterflies over GF(2^128) on sm_100a (north-star subsystems 2, 3, 4).
+//
+// Reference: proj/include/fpmul/detail/kernels_impl.hpp:29-123 and proj/src/butterfly.cpp.
+// Layer i pairs p[j], p[j+2^i] inside blocks of 2^(i+1) elements; block b uses the twiddle
+//     w(i, b) = C2P((base >> i) ^ 2b),  base = e_{l+64}  =>  w(i, b) = v_{l+64-i} ^ C2P(2b)
+// (butterfly.cpp:45-49, encode.cpp:47).  Twiddles are generated on the fly from the Cantor basis
+// and three 512-entry C2P tables (C2P is GF(2)-linear in b), so the reference's
+// 2^l - 1 entry plan (1 GiB at l = 26) never exists on the GPU.
+//   forward  p0 ^= w*p1; p1 ^= p0          inverse  p1 ^= p0; p0 ^= w*p1
+//
+// Kernels:
+//  * fft_top_kernel: one layer i >= T per launch.  Each CTA owns <= 4096 pairs of ONE block, builds
+//    the 64 KiB M4R table of that block's twiddle in shared memory, then streams its pairs
+//    (4.2 clk/mul/SM, bank-conflict free).
+//  * fft_tile_kernel: layers [0, T) of a 2^T-element tile held in shared memory (one HBM read and
+//    write for T layers); twiddles vary per block there, so products use the generic IMAD gf_mul.
+//  * fft_tile_fused_kernel: forward layers [0,T) of operand b, the pointwise product with operand
+//    a (subsystem 3, kernels_impl.hpp:116-123), and inverse layers [0,T) in one tile pass.
+#include <cuda_runtime.h>
+
+#include "fpm_internal.h"
+#include "gf128.cuh"
+
+namespace fpm {
+
+
+namespace {
+
+constexpr int kTileMax = 12;         // 2^12 elements x 16 B = 64 KiB tile
+
+__device__ __forceinline__ uint4 c2p2(const uint4* __restrict__ c2p, uint64_t b) {  // C2P(2b)
+  uint4 r = c2p[b & 511];
+  if (b >> 9) r = x4(r, c2p[512 + ((b >> 9) & 511)]);
+  if (b >> 18) r = x4(r, c2p[1024 + ((b >> 18) & 511)]);
+  if (b >> 27) r = x4(r, c2p[1536 + ((b >> 27) & 511)]);
+  return r;
+}
+
+__device__ __forceinline__ uint4 twiddle(TwiddleSrc tw, unsigned l, unsigned i, uint64_t b) {
+  return x4(tw.cantor[l + 64 - i], c2p2(tw.c2p, b));
+}
+
+// ------------------------------------------------------------------ top layers (i >= T)
+template <bool INV>
+__global__ void __launch_bounds__(256) fft_top_kernel(uint4* __restrict__ ev, unsigned l, unsigned i, int ppc, TwiddleSrc tw) {
+  extern __shared__ uint4 tab[];            // kM4RUint4
+  __shared__ uint4 rows[128];
+  const uint64_t half = (uint64_t)1 << i;
+  const uint64_t pair0 = (uint64_t)blockIdx.x * ppc;   // ppc <= 2^i: CTA pairs never straddle a block
+  const uint64_t b = pair0 >> i;
+  const uint4 w = twiddle(tw, l, i, b);
+  m4r_build(tab, rows, w, threadIdx.x, blockDim.x);
+  const int copy = threadIdx.x & 7;
+  uint4* base = ev + (b << (i + 1));
+#pragma unroll 4
+  for (int k = threadIdx.x; k < ppc; k += blockDim.x) {
+    const uint64_t j = (pair0 & (half - 1)) + k;
+    uint4 u0 = base[j], u1 = base[j + half];
+    if (!INV) {
+      u0 = x4(u0, m4r_mul(tab, u1, copy));
+      u1 = x4(u1, u0);
+    } else {
+      u1 = x4(u1, u0);
+      u0 = x4(u0, m4r_mul(tab, u1, copy));
+    }
+    base[j] = u0;
+    base[j + half] = u1;
+  }
+}
+
+// ------------------------------------------------------------------ tile layers (i < T)
+template <bool INV>
+__device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, unsigned l, uint64_t tile_idx,
+                                            TwiddleSrc tw) {
+  const int npairs = 1 << (T - 1);
+  for (unsigned step = 0; step < T; ++step) {
+    const unsigned i = INV ? step : T - 1 - step;
+    const uint64_t bhi = tile_idx << (T - 1 - i);  // global block index of the tile's first block
+    // w = v_{l+64-i} ^ C2P(2*(bhi + blk)) = Z ^ C2P(2*blk)  (bit ranges disjoint, C2P linear)
+    const uint4 Z = twiddle(tw, l, i, bhi);
+    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+      const int blk = p >> i, j = p & ((1 << i) - 1);
+      const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+      const uint4 w = x4(Z, c2p2(tw.c2p, (uint64_t)blk));
+      uint4 u0 = s[i0], u1 = s[i1];
+      if (!INV) {
+        u0 = x4(u0, gf_mul(w, u1));
+        u1 = x4(u1, u0);
+      } else {
+        u1 = x4(u1, u0);
+        u0 = x4(u0, gf_mul(w, u1));
+      }
+      s[i0] = u0;
+      s[i1] = u1;
+    }
+    __syncthreads();
+  }
+}
+
+template <bool INV>
+__global__ void __launch_bounds__(256) fft_tile_kernel(uint4* __restrict__ ev, unsigned l, unsigned T, TwiddleSrc tw) {
+  extern __shared__ uint4 s[];
+  const int n = 1 << T;
+  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint4* g = ev + (t << T);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) s[k] = g[k];
+    __syncthreads();
+    tile_layers<INV>(s, T, l, t, tw);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) g[k] = s[k];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) fft_tile_fused_kernel(const uint4* __restrict__ ea, uint4* __restrict__ eb,
+                                                             unsigned l, unsigned T, TwiddleSrc tw) {
+  extern __shared__ uint4 s[];
+  const int n = 1 << T;
+  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint4* g = eb + (t << T);
+    const uint4* ga = ea + (t << T);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) s[k] = g[k];
+    __syncthreads();
+    tile_layers<false>(s, T, l, t, tw);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) s[k] = gf_mul(ga[k], s[k]);
+    __syncthreads();
+    tile_layers<true>(s, T, l, t, tw);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) g[k] = s[k];
+    __syncthreads();
+  }
+}
+
+__global__ void pointwise_kernel(const uint4* __restrict__ u, const uint4* __restrict__ v, uint4* __restrict__ out,
+                                 uint64_t n) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
+    out[k] = gf_mul(u[k], v[k]);
+}
+
+int sms() {
+  int dev, n;
+  FPM_CUDA(cudaGetDevice(&dev));
+  FPM_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  return n;
+}
+
+TwiddleSrc twiddle_src() {
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  const DeviceTables& dt = device_tables(dev);
+  return TwiddleSrc{dt.cantor, dt.c2p};
+}
+
+template <class K>
+void set_smem(K kernel, size_t bytes) {
+  FPM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+}  // namespace
+
+unsigned fft_tile_log2(unsigned l) { return l < (unsigned)kTileMax ? l : (unsigned)kTileMax; }
+
+void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, cudaStream_t s) {
+  if (l <= T) return;
+  const TwiddleSrc tw = twiddle_src();
+  const size_t smem = kM4RUint4 * sizeof(uint4);
+  static bool attr = false;
+  if (!attr) { set_smem(fft_top_kernel<false>, smem); set_smem(fft_top_kernel<true>, smem); attr = true; }
+  // Pairs per CTA: 4096 amortise the 64 KiB table build; smaller layers still fill 2 CTAs/SM.
+  const uint64_t pairs = ((uint64_t)1 << l) / 2;
+  uint64_t ppc = 4096;
+  while (ppc > 256 && pairs / ppc < (uint64_t)sms() * 2) ppc /= 2;
+  const uint64_t ctas = pairs / ppc;
+  if (T < 8 || ctas == 0) throw Error(kInvalid, "butterfly_top: layer too small for the M4R layer kernel");
+  for (unsigned k = 0; k < l - T; ++k) {
+    const unsigned i = inverse ? T + k : l - 1 - k;
+    if (!inverse) fft_top_kernel<false><<<(unsigned)ctas, 256, smem, s>>>(ev, l, i, (int)ppc, tw);
+    else fft_top_kernel<true><<<(unsigned)ctas, 256, smem, s>>>(ev, l, i, (int)ppc, tw);
+    FPM_LAUNCH_CHECK();
+  }
+}
+
+void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, cudaStream_t s) {
+  if (T == 0) return;
+  const TwiddleSrc tw = twiddle_src();
+  const size_t smem = ((size_t)1 << T) * sizeof(uint4);
+  static bool attr = false;
+  if (!attr) {
+    set_smem(fft_tile_kernel<false>, (size_t)1 << kTileMax << 4);
+    set_smem(fft_tile_kernel<true>, (size_t)1 << kTileMax << 4);
+    attr = true;
+  }
+  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
+  const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)sms() * 3);
+  if (!inverse) fft_tile_kernel<false><<<grid, 256, smem, s>>>(ev, l, T, tw);
+  else fft_tile_kernel<true><<<grid, 256, smem, s>>>(ev, l, T, tw);
+  FPM_LAUNCH_CHECK();
+}
+
+void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, cudaStream_t s) {
+  const TwiddleSrc tw = twiddle_src();
+  const size_t smem = ((size_t)1 << T) * sizeof(uint4);
+  static bool attr = false;
+  if (!attr) { set_smem(fft_tile_fused_kernel, (size_t)1 << kTileMax << 4); attr = true; }
+  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
+  const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)sms() * 3);
+  fft_tile_fused_kernel<<<grid, 256, smem, s>>>(ea, eb, l, T, tw);
+  FPM_LAUNCH_CHECK();
+}
+
+void butterfly_device(uint4* ev, unsigned l, bool inverse, cudaStream_t s) {
+  const unsigned T = fft_tile_log2(l);
+  if (!inverse) {
+    butterfly_top_device(ev, l, T, false, s);
+    butterfly_tile_device(ev, l, T, false, s);
+  } else {
+    butterfly_tile_device(ev, l, T, true, s);
+    butterfly_top_device(ev, l, T, true, s);
+  }
+}
+
+void pointwise_device(const uint4* u, const uint4* v, uint4* out, size_t n, cudaStream_t s) {
+  if (!n) return;
+  const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms() * 16);
+  pointwise_kernel<<<grid, 256, 0, s>>>(u, v, out, n);
+  FPM_LAUNCH_CHECK();
+}
+
+}  // namespace fpm

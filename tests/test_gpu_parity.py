@@ -1,0 +1,111 @@
+"""GPU parity: every stage and the full product through the C-ABI, bit-exact against the oracle
+(the reference library compiled from /root/reference when present, else our C restatement)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rnd_words(rng, bits):
+    w = rng.integers(0, 2**63, size=max(1, (bits + 63) // 64), dtype=np.uint64) * np.uint64(2) \
+        + rng.integers(0, 2, size=max(1, (bits + 63) // 64), dtype=np.uint64)
+    if bits % 64:
+        w[-1] &= np.uint64((1 << (bits % 64)) - 1)
+    return w[: (bits + 63) // 64] if bits else w[:0]
+
+
+def test_tables_match(gpu, port):
+    c, r, i = gpu.tables128()
+    assert np.array_equal(c, port.cantor_basis(128))
+    pr, pi = port.encode_matrix(128)
+    assert np.array_equal(r, pr) and np.array_equal(i, pi)
+
+
+def test_gf128_mul(gpu, checker):
+    rng = np.random.default_rng(13)
+    u = rnd_words(rng, 128 * 4096)
+    v = rnd_words(rng, 128 * 4096)
+    assert np.array_equal(gpu.gf128_mul(u, v), checker.pointwise(u, v))
+    one = np.zeros_like(u)
+    one[0::2] = 1
+    assert np.array_equal(gpu.gf128_mul(u, one), u)
+
+
+@pytest.mark.parametrize("lg", list(range(6, 23)))
+def test_basis_cvt_roundtrip(gpu, checker, lg):
+    n = 1 << lg
+    rng = np.random.default_rng(lg)
+    w = rnd_words(rng, n)
+    fwd = gpu.basis_cvt(w, n)
+    assert np.array_equal(fwd, checker.basis_cvt(w, n)), "forward"
+    back = gpu.i_basis_cvt(fwd, n)
+    assert np.array_equal(back, w), "inverse"
+    # declared zero tail (basis_convert.cpp:337-341)
+    for content in (n // 2, 3 * n // 8, 1):
+        z = rnd_words(rng, content)
+        zz = np.zeros(n // 64, np.uint64)
+        zz[: z.size] = z
+        assert np.array_equal(gpu.basis_cvt(zz, n, content), checker.basis_cvt(zz, n)), content
+
+
+@pytest.mark.parametrize("l", [0, 1, 3, 5, 9, 10, 11, 13, 15])
+def test_encode_decode(gpu, checker, l):
+    rng = np.random.default_rng(100 + l)
+    a = rnd_words(rng, 128 << l)
+    ev = gpu.encode(a, l)
+    assert np.array_equal(ev, checker.encode(a, l))
+    assert np.array_equal(gpu.decode(ev, l), a)
+
+
+@pytest.mark.parametrize("l", [1, 2, 4, 7, 10, 12, 13, 14, 16])
+def test_butterfly(gpu, checker, l):
+    rng = np.random.default_rng(200 + l)
+    ev = rnd_words(rng, 128 << l)
+    f = gpu.lch_butterfly(ev, l)
+    assert np.array_equal(f, checker.butterfly(ev, l)), "forward"
+    assert np.array_equal(gpu.i_lch_butterfly(f, l), ev), "inverse"
+
+
+SHAPES = [(1, 1), (1, 5), (63, 64), (64, 64), (100, 3000), (4095, 4096), (5000, 3000), (1 << 12, 1 << 12),
+          (1 << 14, (1 << 14) - 17), (1 << 16, 1 << 16), ((1 << 16) + 1, 9), ((1 << 17) - 3, (1 << 16) + 5),
+          (1 << 18, 1 << 18), (300000, 1 << 19), (1 << 20, 1 << 20), ((1 << 20) + 77, 12345)]
+
+
+@pytest.mark.parametrize("la,lb", SHAPES)
+def test_polymul_shapes(gpu, checker, port, la, lb):
+    a = port.random_bitpoly(la, 1000 + la)
+    b = port.random_bitpoly(lb, 2000 + lb)
+    got = gpu.fp_polymul(a, la, b, lb, field=gpu.FIELD_GF128)
+    assert np.array_equal(got, checker.polymul(a, la, b, lb))
+
+
+def test_polymul_edge_values(gpu, port):
+    # identity, monomial shift, zero, empty (test_polymul.cpp:50-66)
+    one = np.array([1], np.uint64)
+    b = port.random_bitpoly(50000, 6)
+    assert np.array_equal(gpu.fp_polymul(one, 1, b, 50000), b)
+    xa = np.zeros(16, np.uint64); xa[1000 // 64] = np.uint64(1 << (1000 % 64))
+    xb = np.zeros(65, np.uint64); xb[4096 // 64] = np.uint64(1)
+    prod = gpu.fp_polymul(xa, 1001, xb, 4097)
+    assert prod.size == (1001 + 4097 - 1 + 63) // 64
+    nz = np.flatnonzero(prod)
+    assert nz.tolist() == [(1000 + 4096) // 64] and int(prod[nz[0]]) == 1 << ((1000 + 4096) % 64)
+    assert gpu.fp_polymul(np.zeros(0, np.uint64), 0, b, 50000).size == 0
+    assert not gpu.fp_polymul(b, 50000, np.zeros(1, np.uint64), 17).any()
+
+
+def test_batch(gpu, port, checker):
+    import torch
+    la = lb = 1 << 16
+    count = 64
+    A = np.stack([port.random_bitpoly(la, 7000 + k) for k in range(count)])
+    B = np.stack([port.random_bitpoly(lb, 9000 + k) for k in range(count)])
+    wa, wb, wc = A.shape[1], B.shape[1], (la + lb - 1 + 63) // 64
+    dA = torch.from_numpy(A.view(np.int64)).cuda()
+    dB = torch.from_numpy(B.view(np.int64)).cuda()
+    dC = torch.zeros((count, wc), dtype=torch.int64, device="cuda")
+    gpu.fp_polymul_batch_dev(dA, la, wa, dB, lb, wb, dC, wc, count)
+    torch.cuda.synchronize()
+    C = dC.cpu().numpy().view(np.uint64)
+    for k in (0, 1, count - 1):
+        assert np.array_equal(C[k], checker.polymul(A[k], la, B[k], lb)), k
