@@ -1,0 +1,329 @@
+#!/usr/bin/env python3
+"""Benchmark: ms per 2^32 x 2^32-bit GF(2)[x] multiply (BASELINE config 5) on B200.
+
+Contract (one JSON line on rank 0):
+  value        device-resident ms per multiply (inputs already in HBM), max over ranks, K steps
+  e2e          the same through the C-ABI host entry point fpm_polymul with pinned HOST buffers:
+               H2D of both operands + D2H of the product inside every timed step
+  roofline     the dominant kernel class of the step, measured live with CUDA events
+  cpu_baseline the reference CPU path (oracle/_ref, F4-patched build for >= 2^33-bit products)
+               timed on this host's cores, rank 0 at N=1 only, on a bounded sample
+  --impl reference   times the reference's own CPU implementation instead (rank 0 only)
+
+Multi-GPU (torchrun, N>1): this round each rank multiplies its own pair of operands (replicas,
+"scaling": "weak"); value = step time / (products per step) over the whole job.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms per 2^k-bit GF(2)[x] multiply (k=20..32); fraction of per-pass roofline"
+CONFIGS = {  # BASELINE.json configs by index (1-based); operand bits
+    1: 1 << 20, 3: 1 << 24, 4: 1 << 28, 5: 1 << 32,
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# Integer-issue peak: LOP3 microbenchmark on B200 (profiles/r01_ubench_gf128_mul.log):
+# 63 ops/clk/SM x 148 SMs, scaled by the SM clock seen during the run.
+LOP3_OPS_PER_CLK_SM = 63.0
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    return ws, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def rand_words(torch, words, seed, device):
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    lo = torch.randint(0, 1 << 32, (words,), generator=g, device=device, dtype=torch.int64)
+    hi = torch.randint(0, 1 << 32, (words,), generator=g, device=device, dtype=torch.int64)
+    return lo | (hi << 32)
+
+
+def algorithmic(stage: str, bits: int):
+    """SURVEY.md 8(d) per-unit algorithmic work for one product with equal operands of `bits` bits.
+    Returns (kind, amount): bytes for HBM-bound stages, 32-bit integer ops for the butterflies."""
+    n = 2 * bits
+    n_p = n // 128
+    l = n_p.bit_length() - 1
+    V = 16 * n_p
+    if stage == "basiscvt":   # one fused sweep per operand: N/8 read + N/8 write, two operands
+        return "hbm", 2 * (bits // 8) * 2
+    if stage == "ibasiscvt":  # one sweep over the n-bit product
+        return "hbm", 2 * (n // 8)
+    if stage == "encode":     # N/8 read + V write per operand
+        return "hbm", 2 * (bits // 8 + V)
+    if stage == "decode":
+        return "hbm", V + n // 8
+    if stage == "butterfly":  # 552 ops per butterfly, l layers x n_p/2 per operand
+        return "int", 2 * 552 * l * n_p // 2
+    if stage == "ibutterfly":
+        return "int", 552 * l * n_p // 2
+    if stage == "pointwise":
+        return "int", 544 * n_p
+    raise KeyError(stage)
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the reference's own CPU fp_polymul (oracle/_ref) on this host's cores."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+
+    bits = CONFIGS[args.config]
+    f4 = 2 * bits >= (1 << 33)
+    R = oracle.ref(f4=f4)
+    threads = R.max_threads()
+    P = oracle.port()
+    a = P.random_bitpoly(bits, 20261020)
+    b = P.random_bitpoly(bits, 20261021)
+    for _ in range(min(args.warmup, 1)):  # cold call builds the twiddle plan (polymul.cpp:63-74)
+        R.polymul(a, bits, b, bits, field=0)
+    times = []
+    budget = args.ref_budget_s
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        R.polymul(a, bits, b, bits, field=0)
+        times.append((time.perf_counter() - t0) * 1e3)
+        if time.perf_counter() - t_all > budget:
+            break
+    v = statistics.mean(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": ws,
+        "steps": len(times), "steps_requested": args.steps, "warmup": min(args.warmup, 1),
+        "ms_per_step": round(v, 3), "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic (mt19937_64 seeded, random_bitpoly)",
+        "config": {"workload": f"cfg{args.config}: 2^{bits.bit_length()-1} x 2^{bits.bit_length()-1}-bit product",
+                   "field": "auto (m=64, the reference default)", "library": os.path.basename(R.path)},
+        "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": threads, "kind": "reference",
+                         "sample": f"{len(times)} warm full products (ExecPolicy::kParallel, {threads} OpenMP "
+                                   f"threads) after {min(args.warmup, 1)} cold call(s)"},
+        "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(bits):
+    import oracle
+
+    f4 = 2 * bits >= (1 << 33)
+    R = oracle.ref(f4=f4)
+    P = oracle.port()
+    a = P.random_bitpoly(bits, 20261020)
+    b = P.random_bitpoly(bits, 20261021)
+    t0 = time.perf_counter()
+    R.polymul(a, bits, b, bits, field=128)  # cold: includes the l-layer twiddle plan build
+    cold = (time.perf_counter() - t0) * 1e3
+    t0 = time.perf_counter()
+    R.polymul(a, bits, b, bits, field=128)
+    warm = (time.perf_counter() - t0) * 1e3
+    return {"value": round(warm, 1), "unit": "ms", "cores": R.max_threads(), "kind": "reference",
+            "sample": f"1 warm GF(2^128) product of this config after 1 cold call ({cold:.0f} ms incl. plan "
+                      f"build); {'F4-patched ' if f4 else ''}reference build, OpenMP kParallel"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    ws, rank, local = dist_env()
+
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_1803_11301_b200 as pkg
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    bits = CONFIGS[args.config]
+    words = bits // 64
+    out_words = (2 * bits - 1 + 63) // 64
+    a = rand_words(torch, words, 1000 + rank, dev)
+    b = rand_words(torch, words, 2000 + rank, dev)
+    c = torch.empty(out_words, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        pkg.fp_polymul_dev(a, bits, b, bits, c, field=pkg.FIELD_GF128)
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident
+    pkg.launch_count(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            pkg.fp_polymul_dev(a, bits, b, bits, c, field=pkg.FIELD_GF128)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = pkg.launch_count(reset=True)
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    # ---- e2e: C-ABI host entry point, pinned host buffers, copies inside every step
+    ha = torch.empty(words, dtype=torch.int64, pin_memory=True)
+    hb = torch.empty(words, dtype=torch.int64, pin_memory=True)
+    hc = torch.empty(out_words, dtype=torch.int64, pin_memory=True)
+    ha.copy_(a)
+    hb.copy_(b)
+    na, nb, nc = (x.numpy().view(np.uint64) for x in (ha, hb, hc))
+    pkg.fp_polymul(na, bits, nb, bits, field=pkg.FIELD_GF128, device=local)  # warm host path
+    e2e_steps = max(1, min(args.steps, 5))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        res = pkg.fp_polymul(na, bits, nb, bits, field=pkg.FIELD_GF128, device=local)
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
+    t = torch.tensor([e2e_ms], device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    same = bool(np.array_equal(res, c.cpu().numpy().view(np.uint64)))
+
+    # ---- roofline: per-stage CUDA-event times of one instrumented product
+    st = [0.0] * pkg.NUM_STAGES
+    pkg.fp_polymul_dev(a, bits, b, bits, c, field=pkg.FIELD_GF128, stage_seconds=st)
+    torch.cuda.synchronize()
+    stages = dict(zip(pkg.STAGE_NAMES, st))
+    dom = max(stages, key=stages.get)
+    kind, amount = algorithmic(dom, bits)
+    clocks = clk.summary()
+    hbm, peak_kind = peaks()
+    if kind == "hbm":
+        achieved = amount / stages[dom] / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_kind}
+    else:
+        mhz = clocks.get("sm_mhz") or 1965.0
+        peak_tops = LOP3_OPS_PER_CLK_SM * 148 * mhz * 1e6 / 1e12
+        achieved = amount / stages[dom] / 1e12
+        roof = {"bound": "int", "kernel": dom, "achieved": round(achieved, 2), "peak": round(peak_tops, 2),
+                "unit": "Tops/s", "frac": round(achieved / peak_tops, 4), "traffic": None,
+                "peak_source": "LOP3 microbenchmark 63 ops/clk/SM at the sampled SM clock",
+                "op_convention": "SURVEY 8(d): 552 int32 ops per butterfly (schoolbook GF(2^128) multiply)"}
+    roof["stage_ms"] = {k: round(v * 1e3, 3) for k, v in stages.items()}
+
+    line = {
+        "metric": METRIC, "value": round(ms_max / ws if ws > 1 else ms_max, 3), "unit": "ms", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 3), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (uniform random bits, seeded)",
+        "config": {"workload": f"cfg{args.config}: 2^{bits.bit_length()-1} x 2^{bits.bit_length()-1}-bit product, "
+                               f"GF(2^128) Frobenius FFT (n=2^{(2*bits).bit_length()-1}, "
+                               f"l={(2*bits//128).bit_length()-1})",
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                   "l2": "inputs >= 2x L2 per operand at cfg4/5 (no flush needed)" if bits >= 1 << 28 else "inputs fit in L2"},
+        "e2e": {"value": round(e2e_ms / ws if ws > 1 else e2e_ms, 3), "unit": "ms", "steps": e2e_steps,
+                "h2d_bytes_per_step": 2 * words * 8, "d2h_bytes_per_step": out_words * 8,
+                "matches_device_result": same},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "clocks": clocks,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(bits)
+        except Exception as e:  # reference not built on this box
+            line["cpu_baseline"] = {"value": None, "unit": "ms", "cores": os.cpu_count(), "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
