@@ -1,0 +1,142 @@
+// conv_tile.cuh -- basis conversion of 2^r-bit chunks (r <= 16) inside one 8 KiB shared-memory tile.
+//
+// The reference conversion (proj/src/basis_convert.cpp) is build_schedule's fold-pass list; its
+// recursion is  conv(2^r) = C_rows(conv(256)) o C_cols(conv(D)) o L1(256, D)  with the chunk seen as
+// D = 2^(r-8) rows of 256 bits.  L1 (the level passes, a radix-y Taylor expansion, y = x^256 + x)
+// has the closed form (Lucas' theorem; verified against the pass list in tools/models/bc_model.py):
+//     G_k = sum_{d superset of k} x^(d-k) F_d ,   g_k = (G_k mod x^256) + x (G_k div x^256) + (G_{k-1} div x^256)
+// and its inverse  F'_d = sum_{k superset of d} x^(k-d) g_k ,  F_d = (F'_d mod x^256) + (F'_{d-1} div x^256).
+// Skewing row d left by d bits turns the shifted subset sums into plain XOR butterflies over the row
+// index (shuffles for row distances < 32, shared memory above).  C_cols is conv(D) with whole rows
+// as units (pure row XORs, kRowSched*), C_rows is conv(256) in registers (conv_regs_gen.cuh).
+//
+// Tile layout: 256 rows x 8 words (row-major); thread t owns row t.  A tile holds 2^(16-r)
+// independent chunks (r >= 8) or 256 rows each holding 2^(8-r) chunks (r < 8).
+#pragma once
+#include <cstdint>
+
+#include "conv_regs_gen.cuh"
+
+namespace fpm {
+
+constexpr int kTileRows = 256;
+constexpr int kScPitch = 17;  // scratch row pitch (words) for 512-bit widened rows
+
+__device__ __forceinline__ uint32_t sm_get32(const uint32_t* row, int nwords, int pos) {
+  // 32 bits of `row` (nwords words) starting at bit pos (may be negative / past the end: zeros)
+  const int iw = pos >> 5, s = pos & 31;
+  const uint32_t lo = (iw >= 0 && iw < nwords) ? row[iw] : 0u;
+  if (!s) return lo;
+  const uint32_t hi = (iw + 1 >= 0 && iw + 1 < nwords) ? row[iw + 1] : 0u;
+  return __funnelshift_r(lo, hi, s);
+}
+
+// L1(256, 2^g) forward (carry) or inverse (overflow) on the chunk rows; m = this thread's row.
+template <bool INV>
+__device__ __forceinline__ void l1_tile(uint32_t (&m)[8], uint32_t* sc, int g, int d) {
+  const int tid = threadIdx.x;
+  uint32_t* my = sc + tid * kScPitch;
+  uint32_t W[16];
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) my[i] = m[i];
+  // skew: W = m << d  (own row only: no barrier needed)
+#pragma unroll
+  for (int i = 0; i < 16; ++i) W[i] = sm_get32(my, 8, 32 * i - d);
+  // subset-zeta over the g row bits: rows with bit b clear ^= row | 2^b
+  for (int b = 0; b < g; ++b) {
+    const bool lower = !((d >> b) & 1);
+    if ((1 << b) < 32) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, W[i], 1 << b);
+        if (lower) W[i] ^= y;
+      }
+    } else {
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) my[i] = W[i];
+      __syncthreads();
+      if (lower) {
+        const uint32_t* pr = sc + (tid + (1 << b)) * kScPitch;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) W[i] ^= pr[i];
+      }
+    }
+  }
+  // unskew: G = W >> d
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) my[i] = W[i];
+  uint32_t G[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) G[i] = sm_get32(my, 16, 32 * i + d);
+  // carry (forward) / overflow (inverse) with the previous row's high half H_{d-1}
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) my[i] = G[8 + i];
+  __syncthreads();
+  uint32_t prevH[8];
+  const uint32_t* pr = sc + (tid - 1) * kScPitch;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) prevH[i] = d >= 1 ? pr[i] : 0u;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint32_t v = G[i] ^ prevH[i];
+    if (!INV) v ^= (G[8 + i] << 1) | (i ? (G[7 + i] >> 31) : 0u);  // x * H_d
+    m[i] = v;
+  }
+}
+
+// conv(2^g) over the chunk's rows (rows as units): pass (S, D) -> rows q of each S-span with
+// q in [S/2-D, S-D) get row q+D (and row q+2D if q+2D < S, forward).
+template <bool INV>
+__device__ __forceinline__ void rowpasses(uint32_t (&m)[8], uint32_t* tile, int g, int d) {
+  const int tid = threadIdx.x;
+  const int n = kRowSchedN[g];
+  for (int kk = 0; kk < n; ++kk) {
+    const int k = INV ? n - 1 - kk : kk;
+    const int S = kRowSchedS[g][k], D = kRowSchedD[g][k];
+    __syncthreads();
+    uint4* my4 = reinterpret_cast<uint4*>(tile + tid * 8);
+    my4[0] = make_uint4(m[0], m[1], m[2], m[3]);
+    my4[1] = make_uint4(m[4], m[5], m[6], m[7]);
+    __syncthreads();
+    const int q = d & (S - 1);
+    if (q >= S / 2 - D && q < S - D) {
+      const uint4* s1 = reinterpret_cast<const uint4*>(tile + (tid + D) * 8);
+      uint4 a = s1[0], b = s1[1];
+      if (!INV && q + 2 * D < S) {
+        const uint4* s2 = reinterpret_cast<const uint4*>(tile + (tid + 2 * D) * 8);
+        const uint4 c = s2[0], e = s2[1];
+        a.x ^= c.x; a.y ^= c.y; a.z ^= c.z; a.w ^= c.w;
+        b.x ^= e.x; b.y ^= e.y; b.z ^= e.z; b.w ^= e.w;
+      }
+      m[0] ^= a.x; m[1] ^= a.y; m[2] ^= a.z; m[3] ^= a.w;
+      m[4] ^= b.x; m[5] ^= b.y; m[6] ^= b.z; m[7] ^= b.w;
+    }
+  }
+}
+
+// Converts every aligned 2^r-bit chunk of the tile (thread t's row in m), r in [1, 16].
+// tile: 256 x 8 words of shared memory; sc: 256 x kScPitch words of shared memory.
+// All 256 threads must call it (barriers inside when r > 8).
+template <bool INV>
+__device__ __forceinline__ void conv_tile(uint32_t (&m)[8], uint32_t* tile, uint32_t* sc, int r) {
+  if (r <= 8) {
+    conv_regs<INV>(r, m);
+    return;
+  }
+  const int g = r - 8, d = threadIdx.x & ((1 << g) - 1);
+  if (!INV) {
+    l1_tile<false>(m, sc, g, d);
+    rowpasses<false>(m, tile, g, d);
+    conv_regs<false>(8, m);
+  } else {
+    conv_regs<true>(8, m);
+    rowpasses<true>(m, tile, g, d);
+    l1_tile<true>(m, sc, g, d);
+  }
+}
+
+}  // namespace fpm

@@ -371,7 +371,6 @@ fpm_status fpm_basis_cvt_dev(uint64_t* d_w, size_t n_bits, size_t content_bits, 
     require_device();
     if (n_bits == 0 || (n_bits & (n_bits - 1))) throw Error(kInvalid, "basis_cvt: length must be a power of two");
     if (n_bits <= 2) return;  // identity (basis_convert.cpp:280)
-    if (n_bits < 64) throw Error(kInvalid, "basis_cvt: device arrays must hold at least one 64-bit word");
     basis_cvt_device(reinterpret_cast<uint32_t*>(d_w), n_bits, content_bits ? std::min(content_bits, n_bits) : 1,
                      false, (cudaStream_t)stream);
   });
@@ -382,7 +381,6 @@ fpm_status fpm_i_basis_cvt_dev(uint64_t* d_w, size_t n_bits, void* stream) {
     require_device();
     if (n_bits == 0 || (n_bits & (n_bits - 1))) throw Error(kInvalid, "basis_cvt: length must be a power of two");
     if (n_bits <= 2) return;
-    if (n_bits < 64) throw Error(kInvalid, "basis_cvt: device arrays must hold at least one 64-bit word");
     basis_cvt_device(reinterpret_cast<uint32_t*>(d_w), n_bits, n_bits, true, (cudaStream_t)stream);
   });
 }
@@ -426,11 +424,11 @@ fpm_status fpm_basis_cvt(uint64_t* w, size_t n_bits, size_t content_bits, int de
   return host_call(device, [&](cudaStream_t s) {
     if (n_bits == 0 || (n_bits & (n_bits - 1))) throw Error(kInvalid, "basis_cvt: length must be a power of two");
     if (n_bits <= 2) return;
-    if (n_bits < 64) throw Error(kInvalid, "basis_cvt: device arrays must hold at least one 64-bit word");
-    DevBuf W(n_bits / 8, s);
-    FPM_CUDA(cudaMemcpyAsync(W.p, w, n_bits / 8, cudaMemcpyHostToDevice, s));
+    const size_t bytes = (n_bits + 63) / 64 * 8;
+    DevBuf W(bytes, s);
+    FPM_CUDA(cudaMemcpyAsync(W.p, w, bytes, cudaMemcpyHostToDevice, s));
     basis_cvt_device(W.as<uint32_t>(), n_bits, content_bits ? std::min(content_bits, n_bits) : 1, false, s);
-    FPM_CUDA(cudaMemcpyAsync(w, W.p, n_bits / 8, cudaMemcpyDeviceToHost, s));
+    FPM_CUDA(cudaMemcpyAsync(w, W.p, bytes, cudaMemcpyDeviceToHost, s));
   });
 }
 
@@ -438,11 +436,11 @@ fpm_status fpm_i_basis_cvt(uint64_t* w, size_t n_bits, int device) {
   return host_call(device, [&](cudaStream_t s) {
     if (n_bits == 0 || (n_bits & (n_bits - 1))) throw Error(kInvalid, "basis_cvt: length must be a power of two");
     if (n_bits <= 2) return;
-    if (n_bits < 64) throw Error(kInvalid, "basis_cvt: device arrays must hold at least one 64-bit word");
-    DevBuf W(n_bits / 8, s);
-    FPM_CUDA(cudaMemcpyAsync(W.p, w, n_bits / 8, cudaMemcpyHostToDevice, s));
+    const size_t bytes = (n_bits + 63) / 64 * 8;
+    DevBuf W(bytes, s);
+    FPM_CUDA(cudaMemcpyAsync(W.p, w, bytes, cudaMemcpyHostToDevice, s));
     basis_cvt_device(W.as<uint32_t>(), n_bits, n_bits, true, s);
-    FPM_CUDA(cudaMemcpyAsync(w, W.p, n_bits / 8, cudaMemcpyDeviceToHost, s));
+    FPM_CUDA(cudaMemcpyAsync(w, W.p, bytes, cudaMemcpyDeviceToHost, s));
   });
 }
 

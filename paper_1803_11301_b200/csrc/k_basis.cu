@@ -1,92 +1,378 @@
 // k_basis.cu -- monomial <-> novel-polynomial basis conversion (Taylor expansion) on sm_100a.
 //
-// Reference: proj/src/basis_convert.cpp.  The conversion is the fixed sequence of fold passes of
-// build_schedule (:53-67); pass (S, D) acts on every aligned S-bit span:
-//     forward  y[q] = x[q] ^ x[q+D] ^ (q+2D < S ? x[q+2D] : 0)      q in [S/2-D, S-D)
-//     inverse  x[q] = y[q] ^ y[q+D]                                 (reverse pass order)
-// with all right-hand sides pre-pass values (:34-46).
-//
-// GPU structure (HBM-bound work; bytes only):
-//  * bc_tile_kernel: the maximal run of passes with S <= 2^16 at the end of the forward schedule
-//    (start of the inverse) -- the per-digit conversion build_schedule(2^16, 1) -- runs on 8 KiB
-//    tiles double-buffered in shared memory: one HBM read + one write for ~32 passes.
-//  * bc_pass_kernel: each larger pass as an in-place sweep in two race-free phases:
-//    region L = [S/2-D, S/2) (reads the pre-pass upper half), then U = [S/2, S-D) (reads only
-//    [S/2+D, S), never written by the pass).  Spans whose sources lie in the zero tail are skipped
-//    (the reference's content_bits skip, :167).
+// Reference: proj/src/basis_convert.cpp -- the fixed fold-pass list of build_schedule (:53-67),
+//     forward  y[q] = x[q] ^ x[q+D] ^ (q+2D < S ? x[q+2D] : 0)   q in [S/2-D, S-D) of each S-span
+//     inverse  x[q] = y[q] ^ y[q+D]                              (reverse pass order)
+// applied one pass per sweep (81 sweeps for a 2^33-bit array).  Here the same linear map is
+// evaluated in a handful of HBM sweeps, using the schedule's recursion
+//     conv(2^K) = C_rows(conv(t)) o C_cols(conv(D)) o L1(t, D),  t = 2^16, D = 2^(K-16)  (17 <= K <= 32)
+// with L1 in closed form (see conv_tile.cuh; model check: tools/models/bc_model.py):
+//   Z     zeta_kernel       skew row d by d bits (fused into the load) and XOR-butterfly the row index
+//                           over 256-row groups (stride 1, then stride 256): pure streaming XOR tiles
+//   C     carry_rows_kernel unskew + single carry level, then conv(2^16) of the row in shared memory
+//                           (forward; the inverse uses overflow_kernel and a separate row pass)
+//   C_D   conv over the row index: D <= 256 -> slab tiles of D rows x 256 bits (row XOR passes);
+//         D > 256 -> bit transpose, conv(D) per transposed row, transpose back
+// HBM traffic at K = 32: ~9 GiB (vs ~70 GiB for 48 separate passes).  Arrays of <= 2^16 bits run in
+// one shared-memory tile; > 2^32 bits run their top passes with the generic in-place pass kernel
+// and recurse per 2^32-bit block.
 #include <cuda_runtime.h>
 
 #include <cstdio>
 #include <vector>
 
 #include "basis_dev.cuh"
+#include "conv_tile.cuh"
 #include "fpm_internal.h"
 
 namespace fpm {
 namespace {
 
-constexpr int kTileLog2 = 16;                // 2^16-bit tiles (8 KiB)
-
-// ------------------------------------------------------------------ big passes, in place
-__global__ void bc_pass_kernel(uint32_t* __restrict__ w, uint64_t nwords, uint64_t S, uint64_t D, int inverse,
-                               uint64_t w_first, uint64_t nw_span, uint64_t nspans, uint64_t rlo, uint64_t rhi,
-                               uint64_t live_bits) {
-  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t total = nw_span * nspans;
-  for (uint64_t k = t; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t span = k / nw_span;
-    const uint64_t base = span * S;
-    if (!inverse && base + S / 2 >= live_bits) continue;  // sources in the zero tail
-    const uint64_t wi = (base >> 5) + w_first + (k - span * nw_span);
-    const uint32_t nv = fold_word(w, nwords, wi, S, D, inverse != 0, rlo, rhi);
-    w[wi] = nv;
-  }
-}
-
-// ------------------------------------------------------------------ small passes, SMEM tiles
-__global__ void __launch_bounds__(256) bc_tile_kernel(uint32_t* __restrict__ w, uint64_t nwords, int tile_words,
-                                                      PassList pl, int inverse, uint64_t live_words) {
-  extern __shared__ uint32_t sm[];
-  uint32_t* bufA = sm;
-  uint32_t* bufB = sm + tile_words;
-  const uint64_t ntiles = nwords / tile_words;
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint64_t off = tile * tile_words;
-    if (!inverse && off >= live_words) continue;  // all-zero tile stays zero
-    for (int i = threadIdx.x; i < tile_words; i += blockDim.x) bufA[i] = w[off + i];
-    __syncthreads();
-    const uint32_t* a = smem_passes(bufA, bufB, tile_words, pl, inverse != 0);
-    for (int i = threadIdx.x; i < tile_words; i += blockDim.x) w[off + i] = a[i];
-    __syncthreads();
-  }
-}
+constexpr int kTLog2 = 16;                  // digit size t = 2^16 bits for 2^17..2^32-bit arrays
+constexpr uint64_t kT = (uint64_t)1 << kTLog2;
+constexpr int kTWords = (int)(kT / 32);     // 2048
+constexpr size_t kTileSmem = (kTileRows * 8 + kTileRows * kScPitch) * sizeof(uint32_t);
 
 int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev;
-    FPM_CUDA(cudaGetDevice(&dev));
-    FPM_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
-  }
+  int dev, n;
+  FPM_CUDA(cudaGetDevice(&dev));
+  FPM_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
   return n;
 }
 
-void run_tile_passes(uint32_t* w, uint64_t nwords, const std::vector<Pass>& passes, bool inverse, uint64_t live_bits,
-                     cudaStream_t s) {
-  if (passes.empty()) return;
-  const PassList pl = make_passlist(passes, inverse);
-  uint64_t tile_bits = 32;
-  for (const Pass& p : passes) tile_bits = std::max<uint64_t>(tile_bits, p.span);
-  // Tile: at least 256 words (one per thread), at most the array.
-  uint64_t tile_words = tile_bits / 32;
-  if (tile_words < 256) tile_words = 256;
-  if (tile_words > nwords) tile_words = nwords;
-  const size_t smem = 2 * tile_words * sizeof(uint32_t);
+__device__ __forceinline__ uint32_t g_get32(const uint32_t* __restrict__ row, uint64_t nwords, int64_t pos) {
+  if (pos <= -32) return 0u;
+  const int64_t iw = pos >> 5;
+  const uint32_t s = (uint32_t)(pos & 31);
+  const uint32_t lo = (iw >= 0 && (uint64_t)iw < nwords) ? __ldg(row + iw) : 0u;
+  if (!s) return lo;
+  const uint32_t hi = (iw + 1 >= 0 && (uint64_t)(iw + 1) < nwords) ? __ldg(row + iw + 1) : 0u;
+  return __funnelshift_r(lo, hi, s);
+}
+
+// ------------------------------------------------------------------ generic in-place pass (K > 32)
+__global__ void bc_pass_kernel(uint32_t* __restrict__ w, uint64_t nwords, uint64_t S, uint64_t D, int inverse,
+                               uint64_t w_first, uint64_t nw_span, uint64_t nspans, uint64_t rlo, uint64_t rhi,
+                               uint64_t live_bits) {
+  const uint64_t total = nw_span * nspans;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t span = k / nw_span;
+    const uint64_t base = span * S;
+    if (!inverse && base + S / 2 >= live_bits) continue;
+    const uint64_t wi = (base >> 5) + w_first + (k - span * nw_span);
+    w[wi] = fold_word(w, nwords, wi, S, D, inverse != 0, rlo, rhi);
+  }
+}
+
+// ------------------------------------------------------------------ small arrays (< 2^8 bits)
+__global__ void bc_small_kernel(uint32_t* __restrict__ w, int words, PassList pl, int inverse) {
+  extern __shared__ uint32_t sm[];
+  for (int i = threadIdx.x; i < words; i += blockDim.x) sm[i] = w[i];
+  __syncthreads();
+  const uint32_t* a = smem_passes(sm, sm + words, words, pl, inverse != 0);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) w[i] = a[i];
+}
+
+// ------------------------------------------------------------------ conv of 2^r-bit chunks, 8 KiB tiles
+template <bool INV>
+__global__ void __launch_bounds__(256) conv_rows_kernel(uint32_t* __restrict__ data, uint64_t nwords, int r) {
+  extern __shared__ uint32_t smem[];
+  uint32_t* tile = smem;
+  uint32_t* sc = smem + kTileRows * 8;
+  const int tid = threadIdx.x;
+  const uint64_t tile_words = nwords < 2048 ? nwords : 2048;
   const uint64_t ntiles = nwords / tile_words;
-  const uint64_t live_words = (live_bits + 31) / 32;
-  const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)sm_count() * 8);
-  bc_tile_kernel<<<grid, 256, smem, s>>>(w, nwords, (int)tile_words, pl, inverse ? 1 : 0, live_words);
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint64_t off = t * tile_words + (uint64_t)tid * 8;
+    uint32_t m[8];
+    const bool valid = (uint64_t)tid * 8 < tile_words;
+    if (valid) {
+      const uint4 a = reinterpret_cast<const uint4*>(data + off)[0];
+      const uint4 b = reinterpret_cast<const uint4*>(data + off)[1];
+      m[0] = a.x; m[1] = a.y; m[2] = a.z; m[3] = a.w; m[4] = b.x; m[5] = b.y; m[6] = b.z; m[7] = b.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) m[i] = 0;
+    }
+    conv_tile<INV>(m, tile, sc, r);
+    if (valid) {
+      reinterpret_cast<uint4*>(data + off)[0] = make_uint4(m[0], m[1], m[2], m[3]);
+      reinterpret_cast<uint4*>(data + off)[1] = make_uint4(m[4], m[5], m[6], m[7]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ Z: subset-zeta over row bits
+// Tile = 256 tile rows x 32 words (one 128 B line per row): tile row R = s * 2^nb + j is row
+// d = base + j * 2^b0 of the group, window wi = wb * (256 >> nb) + s.  Two thread mappings make
+// every butterfly stage register-local with ONE shared-memory exchange between them:
+//   A: thread t holds word t&31 of tile rows (t>>5) + 8k, k < 32   -> row bits 3..7 local
+//   B: thread t holds words 4(t&7).. of tile rows 8(t>>3) + k, k < 8 -> row bits 0..2 local
+// skew=1: the source row d is an unskewed t-bit row read at bit offset -d (the skew of L1).
+constexpr int kZW = 32;
+constexpr int kZP = 36;  // shared row pitch (16 B aligned, conflict-free for both mappings)
+__global__ void __launch_bounds__(256) zeta_kernel(const uint32_t* __restrict__ src, uint64_t src_pitch,
+                                                   uint32_t* __restrict__ dst, uint64_t dst_pitch, uint64_t D,
+                                                   int b0, int nb, int skew, uint64_t src_row_words,
+                                                   uint64_t windows) {
+  extern __shared__ __align__(16) uint32_t sx[];  // 256 x kZP
+  const int tid = threadIdx.x;
+  const int wpc = 256 >> nb;  // windows per CTA
+  const uint64_t groups = D >> nb;
+  const uint64_t wblocks = (windows + wpc - 1) / wpc;
+  const uint64_t items = groups * wblocks;
+  const uint64_t lowmask = ((uint64_t)1 << b0) - 1;
+  for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const uint64_t gid = it / wblocks, wb = it - gid * wblocks;
+    const uint64_t base = (gid & lowmask) | ((gid >> b0) << (b0 + nb));
+    // ---- mapping A: load, stages on tile-row bits 3..7
+    const int c = tid & 31;
+    uint32_t a[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const int R = (tid >> 5) + 8 * k;
+      const uint64_t d = base + ((uint64_t)(R & ((1 << nb) - 1)) << b0);
+      const uint64_t wi = wb * wpc + (R >> nb);
+      uint32_t v = 0;
+      if (wi < windows) {
+        const uint32_t* row = src + d * src_pitch;
+        if (skew) {
+          const int64_t pos = (int64_t)(wi * 32 * kZW) + 32 * c - (int64_t)d;
+          v = g_get32(row, src_row_words, pos);
+        } else {
+          v = __ldg(row + wi * kZW + c);
+        }
+      }
+      a[k] = v;
+    }
+#pragma unroll
+    for (int b = 3; b < 8; ++b) {
+      if (b < nb) {
+        const int kb = 1 << (b - 3);
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (!(k & kb)) a[k] ^= a[k | kb];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 32; ++k) sx[((tid >> 5) + 8 * k) * kZP + c] = a[k];
+    __syncthreads();
+    // ---- mapping B: stages on tile-row bits 0..2, store
+    const int q = tid & 7, R0 = 8 * (tid >> 3);
+    uint4 bq[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) bq[k] = *reinterpret_cast<const uint4*>(sx + (R0 + k) * kZP + 4 * q);
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      if (b < nb) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (!(k & (1 << b))) bq[k] = make_uint4(bq[k].x ^ bq[k | (1 << b)].x, bq[k].y ^ bq[k | (1 << b)].y,
+                                                   bq[k].z ^ bq[k | (1 << b)].z, bq[k].w ^ bq[k | (1 << b)].w);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int R = R0 + k;
+      const uint64_t d = base + ((uint64_t)(R & ((1 << nb) - 1)) << b0);
+      const uint64_t wi = wb * wpc + (R >> nb);
+      if (wi < windows) *reinterpret_cast<uint4*>(dst + d * dst_pitch + wi * kZW + 4 * q) = bq[k];
+    }
+    __syncthreads();
+  }
+}
+// ------------------------------------------------------------------ C: carry + unskew + conv(2^16)
+// g_k[p] = Gs[k][p+k] ^ (p >= 1 ? Gs[k][t+p-1+k] : 0) ^ (k >= 1 ? Gs[k-1][t+p+k-1] : 0), then conv(g_k).
+__global__ void __launch_bounds__(256) carry_rows_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch,
+                                                         uint32_t* __restrict__ out, uint64_t D) {
+  extern __shared__ uint32_t smem[];
+  uint32_t* tile = smem;
+  uint32_t* sc = smem + kTileRows * 8;
+  const int tid = threadIdx.x;
+  for (uint64_t k = blockIdx.x; k < D; k += gridDim.x) {
+    const uint32_t* rk = gs + k * gs_pitch;
+    const uint32_t* rk1 = k ? gs + (k - 1) * gs_pitch : nullptr;
+    uint32_t m[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int64_t p = (int64_t)(tid * 8 + i) * 32;
+      uint32_t v = g_get32(rk, gs_pitch, p + (int64_t)k);
+      uint32_t hi = g_get32(rk, gs_pitch, (int64_t)kT + p - 1 + (int64_t)k);
+      if (p == 0) hi &= ~1u;
+      if (k) hi ^= g_get32(rk1, gs_pitch, (int64_t)kT + p + (int64_t)k - 1);
+      m[i] = v ^ hi;
+    }
+    conv_tile<false>(m, tile, sc, kTLog2);
+    uint4* o = reinterpret_cast<uint4*>(out + k * kTWords + tid * 8);
+    o[0] = make_uint4(m[0], m[1], m[2], m[3]);
+    o[1] = make_uint4(m[4], m[5], m[6], m[7]);
+  }
+}
+
+// ------------------------------------------------------------------ O: overflow + unskew (inverse)
+// F_d[p] = Gs[d][p+d] ^ (d >= 1 ? Gs[d-1][t+p+d-1] : 0)
+__global__ void overflow_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch, uint32_t* __restrict__ out,
+                                uint64_t D) {
+  const uint64_t total = D * kTWords;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t d = k / kTWords, w = k % kTWords;
+    const int64_t p = (int64_t)w * 32;
+    uint32_t v = g_get32(gs + d * gs_pitch, gs_pitch, p + (int64_t)d);
+    if (d) v ^= g_get32(gs + (d - 1) * gs_pitch, gs_pitch, (int64_t)kT + p + (int64_t)d - 1);
+    out[k] = v;
+  }
+}
+
+// ------------------------------------------------------------------ C_D for D <= 256: slab tiles
+// Tile = (256 / D) slabs x D rows x 8 words; rows of the array are t bits (kTWords words) apart.
+template <bool INV>
+__global__ void __launch_bounds__(256) slab_kernel(uint32_t* __restrict__ data, int g) {
+  __shared__ __align__(16) uint32_t tile[kTileRows * 8];
+  const int tid = threadIdx.x;
+  const int Dr = 1 << g;
+  const int d = tid & (Dr - 1), slot = tid >> g;
+  const int spc = 256 >> g;  // slabs per CTA
+  const uint64_t nslabs = kTWords / 8;
+  for (uint64_t sb = (uint64_t)blockIdx.x * spc; sb < nslabs; sb += (uint64_t)gridDim.x * spc) {
+    const uint64_t slab = sb + slot;
+    uint32_t* p = data + (uint64_t)d * kTWords + slab * 8;
+    const uint4 a = reinterpret_cast<const uint4*>(p)[0], b = reinterpret_cast<const uint4*>(p)[1];
+    uint32_t m[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    rowpasses<INV>(m, tile, g, d);
+    reinterpret_cast<uint4*>(p)[0] = make_uint4(m[0], m[1], m[2], m[3]);
+    reinterpret_cast<uint4*>(p)[1] = make_uint4(m[4], m[5], m[6], m[7]);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ bit-matrix transpose
+// src: R rows x C bits (pitch C/32 words) -> dst: C rows x R bits (pitch R/32 words); R, C >= 512.
+// 512 x 512-bit tiles: 64 B per row segment on both sides; 32x32 blocks via warp shuffles.
+constexpr int kTT = 512, kTTW = kTT / 32, kTTP = kTTW + 1;
+__global__ void __launch_bounds__(256) transpose_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                                                        uint64_t R, uint64_t C) {
+  extern __shared__ uint32_t tsm[];
+  uint32_t* sin = tsm;
+  uint32_t* sout = tsm + kTT * kTTP;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t rt = R / kTT, ct = C / kTT;
+  const uint64_t srcp = C / 32, dstp = R / 32;
+  for (uint64_t it = blockIdx.x; it < rt * ct; it += gridDim.x) {
+    const uint64_t tr = it / ct, tc = it - tr * ct;
+    for (int rr = tid; rr < kTT; rr += 256) {
+      const uint4* p = reinterpret_cast<const uint4*>(src + (tr * kTT + rr) * srcp + tc * kTTW);
+      uint32_t* s = sin + rr * kTTP;
+#pragma unroll
+      for (int q = 0; q < kTTW / 4; ++q) {
+        const uint4 a = p[q];
+        s[4 * q] = a.x; s[4 * q + 1] = a.y; s[4 * q + 2] = a.z; s[4 * q + 3] = a.w;
+      }
+    }
+    __syncthreads();
+    for (int blk = warp; blk < kTTW * kTTW; blk += 8) {
+      const int rb = blk / kTTW, cw = blk % kTTW;
+      uint32_t x = sin[(rb * 32 + lane) * kTTP + cw];
+      const uint32_t masks[5] = {0xFFFF0000u, 0xFF00FF00u, 0xF0F0F0F0u, 0xCCCCCCCCu, 0xAAAAAAAAu};
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const int s = 16 >> k;
+        const uint32_t mk = masks[k];
+        const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, s);
+        x = (lane & s) ? ((x & mk) | ((y >> s) & ~mk)) : ((x & ~mk) | ((y << s) & mk));
+      }
+      sout[(cw * 32 + lane) * kTTP + rb] = x;  // output row cw*32+lane, word rb (input rows 32rb..)
+    }
+    __syncthreads();
+    for (int rr = tid; rr < kTT; rr += 256) {
+      uint4* p = reinterpret_cast<uint4*>(dst + (tc * kTT + rr) * dstp + tr * kTTW);
+      const uint32_t* s = sout + rr * kTTP;
+#pragma unroll
+      for (int q = 0; q < kTTW / 4; ++q) p[q] = make_uint4(s[4 * q], s[4 * q + 1], s[4 * q + 2], s[4 * q + 3]);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ host orchestration
+void set_smem_attr() {
+  static bool done[64];
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  if (done[dev]) return;
+  FPM_CUDA(cudaFuncSetAttribute(conv_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
+  FPM_CUDA(cudaFuncSetAttribute(conv_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
+  FPM_CUDA(cudaFuncSetAttribute(carry_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
+  FPM_CUDA(cudaFuncSetAttribute(transpose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(2 * kTT * kTTP * sizeof(uint32_t))));
+  done[dev] = true;
+}
+
+int grid_cap(uint64_t items, int per_sm) {
+  const uint64_t g = std::min<uint64_t>(items, (uint64_t)sm_count() * per_sm);
+  return (int)(g ? g : 1);
+}
+
+void conv_rows(uint32_t* data, uint64_t nwords, int r, bool inv, cudaStream_t s) {
+  const uint64_t tiles = nwords < 2048 ? 1 : nwords / 2048;
+  if (inv) conv_rows_kernel<true><<<grid_cap(tiles, 4), 256, kTileSmem, s>>>(data, nwords, r);
+  else conv_rows_kernel<false><<<grid_cap(tiles, 4), 256, kTileSmem, s>>>(data, nwords, r);
   FPM_LAUNCH_CHECK();
+}
+
+void zeta(const uint32_t* src, uint64_t src_pitch, uint32_t* dst, uint64_t dst_pitch, uint64_t D, int b0, int nb,
+          bool skew, uint64_t windows, cudaStream_t s) {
+  if (nb <= 0) return;
+  const int wpc = 256 >> nb;
+  const uint64_t items = (D >> nb) * ((windows + wpc - 1) / wpc);
+  zeta_kernel<<<grid_cap(items, 4), 256, 256 * kZP * sizeof(uint32_t), s>>>(
+      src, src_pitch, dst, dst_pitch, D, b0, nb, skew ? 1 : 0, kTWords, windows);
+  FPM_LAUNCH_CHECK();
+}
+
+void transpose(const uint32_t* src, uint32_t* dst, uint64_t R, uint64_t C, cudaStream_t s) {
+  transpose_kernel<<<grid_cap((R / kTT) * (C / kTT), 3), 256, 2 * kTT * kTTP * sizeof(uint32_t), s>>>(src, dst, R, C);
+  FPM_LAUNCH_CHECK();
+}
+
+// conv over the row index (D rows of t bits), forward or inverse.
+void conv_cols(uint32_t* w, uint32_t* scratch, int lgD, bool inv, cudaStream_t s) {
+  if (lgD <= 1) return;  // conv(2) is the identity (no passes)
+  if (lgD <= 8) {
+    const int spc = 256 >> lgD;
+    const uint64_t ctas = (kTWords / 8 + spc - 1) / spc;
+    if (inv) slab_kernel<true><<<grid_cap(ctas, 8), 256, 0, s>>>(w, lgD);
+    else slab_kernel<false><<<grid_cap(ctas, 8), 256, 0, s>>>(w, lgD);
+    FPM_LAUNCH_CHECK();
+    return;
+  }
+  const uint64_t D = (uint64_t)1 << lgD;
+  transpose(w, scratch, D, kT, s);           // (D x t) -> (t x D)
+  conv_rows(scratch, kT * D / 32, lgD, inv, s);
+  transpose(scratch, w, kT, D, s);           // back
+}
+
+// conv(2^K) for 17 <= K <= 32 on w (2^K bits).  scratch >= 2^(K-16) * (2^16 + max(2^(K-16), 1024)) bits.
+void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s) {
+  const int lgD = K - kTLog2;
+  const uint64_t D = (uint64_t)1 << lgD;
+  const uint64_t wsk_bits = kT + std::max<uint64_t>(D, 32 * kZW);
+  const uint64_t wsk = wsk_bits / 32;  // skewed row pitch (words)
+  const uint64_t windows = wsk / kZW;
+  const int nb_lo = std::min(lgD, 8), nb_hi = lgD - nb_lo;
+  if (!inv) {
+    zeta(w, kTWords, scratch, wsk, D, 0, nb_lo, true, windows, s);
+    zeta(scratch, wsk, scratch, wsk, D, 8, nb_hi, false, windows, s);
+    carry_rows_kernel<<<grid_cap(D, 4), 256, kTileSmem, s>>>(scratch, wsk, w, D);
+    FPM_LAUNCH_CHECK();
+    conv_cols(w, scratch, lgD, false, s);
+  } else {
+    conv_rows(w, D * kTWords, kTLog2, true, s);
+    conv_cols(w, scratch, lgD, true, s);
+    zeta(w, kTWords, scratch, wsk, D, 0, nb_lo, true, windows, s);
+    zeta(scratch, wsk, scratch, wsk, D, 8, nb_hi, false, windows, s);
+    overflow_kernel<<<grid_cap(D * kTWords / 256, 32), 256, 0, s>>>(scratch, wsk, w, D);
+    FPM_LAUNCH_CHECK();
+  }
 }
 
 void run_big_pass(uint32_t* w, uint64_t nwords, Pass p, bool inverse, uint64_t live_bits, cudaStream_t s) {
@@ -99,34 +385,65 @@ void run_big_pass(uint32_t* w, uint64_t nwords, Pass p, bool inverse, uint64_t l
     const uint64_t w_first = rlo / 32, w_last = (rhi + 31) / 32;
     const uint64_t nw_span = w_last - w_first;
     const uint64_t total = nw_span * nspans;
-    const int threads = 256;
-    const uint64_t blocks = std::min<uint64_t>((total + threads - 1) / threads, (uint64_t)sm_count() * 32);
-    bc_pass_kernel<<<(unsigned)blocks, threads, 0, s>>>(w, nwords, S, D, inverse ? 1 : 0, w_first, nw_span, nspans,
-                                                       rlo, rhi, live_bits);
+    bc_pass_kernel<<<grid_cap((total + 255) / 256, 32), 256, 0, s>>>(w, nwords, S, D, inverse ? 1 : 0, w_first,
+                                                                     nw_span, nspans, rlo, rhi, live_bits);
     FPM_LAUNCH_CHECK();
   }
 }
 
+struct Scratch {
+  void* p = nullptr;
+  cudaStream_t s;
+  Scratch(size_t bytes, cudaStream_t st) : s(st) { if (bytes) FPM_CUDA(cudaMallocAsync(&p, bytes, st)); }
+  ~Scratch() { if (p) cudaFreeAsync(p, s); }
+};
+
 }  // namespace
 
 void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s) {
-  if (n_bits < 32 || (n_bits & (n_bits - 1))) throw Error(kInvalid, "basis_cvt: length must be a power of two >= 32");
-  static thread_local Pass sched[512];
-  size_t np = 0;
-  build_schedule(sched, &np, n_bits, 1);
-  // Split: [big passes][maximal suffix with S <= 2^16].
-  size_t split = np;
-  while (split > 0 && sched[split - 1].span <= ((size_t)1 << kTileLog2)) --split;
-  std::vector<Pass> big(sched, sched + split), small(sched + split, sched + np);
-  const uint64_t nwords = n_bits / 32;
-  if (!inverse) {
-    for (const Pass& p : big) run_big_pass(w, nwords, p, false, live_bits, s);
-    run_tile_passes(w, nwords, small, false, live_bits, s);
-  } else {
-    std::vector<Pass> rsmall(small.rbegin(), small.rend());
-    run_tile_passes(w, nwords, rsmall, true, n_bits, s);
-    for (size_t k = big.size(); k-- > 0;) run_big_pass(w, nwords, big[k], true, n_bits, s);
+  if (n_bits < 4 || (n_bits & (n_bits - 1))) throw Error(kInvalid, "basis_cvt: length must be a power of two >= 4");
+  set_smem_attr();
+  int K = 0;
+  while (((size_t)1 << K) < n_bits) ++K;
+  const uint64_t nwords = n_bits < 32 ? 1 : n_bits / 32;
+  if (K < 8) {  // < 256 bits: the pass list directly, in shared memory
+    Pass sched[64];
+    size_t np = 0;
+    build_schedule(sched, &np, n_bits, 1);
+    std::vector<Pass> v(sched, sched + np);
+    if (inverse) v = std::vector<Pass>(sched, sched + np), v = std::vector<Pass>(v.rbegin(), v.rend());
+    const PassList pl = make_passlist(v, inverse);
+    bc_small_kernel<<<1, 32, 2 * nwords * sizeof(uint32_t), s>>>(w, (int)nwords, pl, inverse ? 1 : 0);
+    FPM_LAUNCH_CHECK();
+    return;
   }
+  if (K <= kTLog2) {
+    conv_rows(w, nwords, K, inverse, s);
+    return;
+  }
+  const int Kb = std::min(K, 32);
+  const uint64_t lgD = Kb - kTLog2, D = (uint64_t)1 << lgD;
+  Scratch scr(D * (kT + std::max<uint64_t>(D, 32 * kZW)) / 8, s);
+  uint32_t* scratch = static_cast<uint32_t*>(scr.p);
+  const uint64_t block_words = ((uint64_t)1 << Kb) / 32;
+  // Arrays above 2^32 bits: their passes with S > 2^32 come first (forward) / last (inverse);
+  // what remains is conv(2^32) of every 2^32-bit block (build_schedule's per-digit recursion).
+  std::vector<Pass> top;
+  if (K > 32) {
+    static thread_local Pass sched[512];
+    size_t np = 0;
+    build_schedule(sched, &np, n_bits, 1);
+    for (size_t k = 0; k < np; ++k)
+      if (sched[k].span > ((size_t)1 << 32)) top.push_back(sched[k]);
+  }
+  if (!inverse)
+    for (const Pass& p : top) run_big_pass(w, nwords, p, false, live_bits, s);
+  for (uint64_t b = 0; b < nwords / block_words; ++b) {
+    if (!inverse && b * block_words * 32 >= live_bits) continue;  // all-zero block stays zero
+    conv2d(w + b * block_words, Kb, inverse, scratch, s);
+  }
+  if (inverse)
+    for (size_t k = top.size(); k-- > 0;) run_big_pass(w, nwords, top[k], true, n_bits, s);
 }
 
 }  // namespace fpm
