@@ -100,6 +100,9 @@ fpm_status fpm_encode_dev(const uint64_t* d_poly, unsigned l, uint64_t* d_ev, vo
 fpm_status fpm_decode_dev(const uint64_t* d_ev, unsigned l, uint64_t* d_poly, void* stream);
 /* lch_butterfly / i_lch_butterfly<gf128> with plan_butterflies(l, e_{l+64}) (butterfly.hpp:58-68). */
 fpm_status fpm_butterfly_dev(uint64_t* d_ev, unsigned l, int inverse, void* stream);
+/* The same for any plan_butterflies(l, base) (butterfly.cpp:32-53): base = Cantor coordinates
+ * {lo, hi}; twiddle of layer i, block b = C2P((base >> i) ^ 2b).  l <= 64. */
+fpm_status fpm_lch_butterfly_dev(uint64_t* d_ev, unsigned l, const uint64_t* base, int inverse, void* stream);
 /* pointwise_mul<gf128> (polymul.hpp:78-80): d_out[i] = d_u[i]*d_v[i] over n elements (may alias). */
 fpm_status fpm_pointwise_dev(const uint64_t* d_u, const uint64_t* d_v, uint64_t* d_out, size_t n, void* stream);
 
@@ -109,6 +112,7 @@ fpm_status fpm_i_basis_cvt(uint64_t* w, size_t n_bits, int device);
 fpm_status fpm_encode(const uint64_t* poly, unsigned l, uint64_t* ev, int device);
 fpm_status fpm_decode(const uint64_t* ev, unsigned l, uint64_t* poly, int device);
 fpm_status fpm_butterfly(uint64_t* ev, unsigned l, int inverse, int device);
+fpm_status fpm_lch_butterfly(uint64_t* ev, unsigned l, const uint64_t* base, int inverse, int device);
 fpm_status fpm_pointwise(const uint64_t* u, const uint64_t* v, uint64_t* out, size_t n, int device);
 fpm_status fpm_gf128_mul(const uint64_t* a, const uint64_t* b, uint64_t* out, size_t n, int device);
 

@@ -171,6 +171,9 @@ void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, siz
     return;
   }
   const unsigned l = p.l, T = fft_tile_log2(l);
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  const TwiddleSrc tw = make_twiddle_src(dev, l, partition_base(l));
   const size_t n = p.n_bits, n_p = p.n_p;
   DevBuf P(n / 8, s), EA(n_p * 16, s), EB(n_p * 16, s);
   const uint64_t* xs[2] = {d_a, d_b};
@@ -187,13 +190,13 @@ void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, siz
     clk.mark(kStEncode);
     encode_device_rows(P.as<uint32_t>(), l, es[k], 64, s);
     clk.mark(kStBfly);
-    butterfly_top_device(es[k], l, T, false, s);
-    if (k == 0) butterfly_tile_device(es[k], l, T, false, s);
+    butterfly_top_device(es[k], l, T, false, tw, s);
+    if (k == 0) butterfly_tile_device(es[k], l, T, false, tw, s);
   }
   clk.mark(kStPointwise);  // + operand b's bottom T forward and the bottom T inverse layers (fused)
-  butterfly_tile_fused_device(EA.as<uint4>(), EB.as<uint4>(), l, T, s);
+  butterfly_tile_fused_device(EA.as<uint4>(), EB.as<uint4>(), l, T, tw, s);
   clk.mark(kStIBfly);
-  butterfly_top_device(EB.as<uint4>(), l, T, true, s);
+  butterfly_top_device(EB.as<uint4>(), l, T, true, tw, s);
   clk.mark(kStDecode);
   decode_device(EB.as<uint4>(), l, P.as<uint32_t>(), s);
   clk.mark(kStIBasis);
@@ -406,7 +409,20 @@ fpm_status fpm_butterfly_dev(uint64_t* d_ev, unsigned l, int inverse, void* stre
     require_device();
     if (l >= 64) throw Error(kInvalid, "PartitionSpec: l must satisfy l < m/2");
     if (l == 0) return;
-    butterfly_device(reinterpret_cast<uint4*>(d_ev), l, inverse != 0, (cudaStream_t)stream);
+    butterfly_device(reinterpret_cast<uint4*>(d_ev), l, partition_base(l), inverse != 0, (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_lch_butterfly_dev(uint64_t* d_ev, unsigned l, const uint64_t* base, int inverse, void* stream) {
+  return guard([&] {
+    require_device();
+    if (l > 64) throw Error(kInvalid, "lch_butterfly: at most 64 layers");
+    if (l == 0) return;
+    if (!base) throw Error(kInvalid, "lch_butterfly: null base");
+    U128 b;
+    b.lo = base[0];
+    b.hi = base[1];
+    butterfly_device(reinterpret_cast<uint4*>(d_ev), l, b, inverse != 0, (cudaStream_t)stream);
   });
 }
 
@@ -466,6 +482,22 @@ fpm_status fpm_decode(const uint64_t* ev, unsigned l, uint64_t* poly, int device
   });
 }
 
+fpm_status fpm_lch_butterfly(uint64_t* ev, unsigned l, const uint64_t* base, int inverse, int device) {
+  return host_call(device, [&](cudaStream_t s) {
+    if (l > 64) throw Error(kInvalid, "lch_butterfly: at most 64 layers");
+    if (l == 0) return;
+    if (!base) throw Error(kInvalid, "lch_butterfly: null base");
+    U128 b;
+    b.lo = base[0];
+    b.hi = base[1];
+    const size_t eb = ((size_t)16 << l);
+    DevBuf E(eb, s);
+    FPM_CUDA(cudaMemcpyAsync(E.p, ev, eb, cudaMemcpyHostToDevice, s));
+    butterfly_device(E.as<uint4>(), l, b, inverse != 0, s);
+    FPM_CUDA(cudaMemcpyAsync(ev, E.p, eb, cudaMemcpyDeviceToHost, s));
+  });
+}
+
 fpm_status fpm_butterfly(uint64_t* ev, unsigned l, int inverse, int device) {
   return host_call(device, [&](cudaStream_t s) {
     if (l >= 64) throw Error(kInvalid, "PartitionSpec: l must satisfy l < m/2");
@@ -473,7 +505,7 @@ fpm_status fpm_butterfly(uint64_t* ev, unsigned l, int inverse, int device) {
     const size_t eb = ((size_t)16 << l);
     DevBuf E(eb, s);
     FPM_CUDA(cudaMemcpyAsync(E.p, ev, eb, cudaMemcpyHostToDevice, s));
-    butterfly_device(E.as<uint4>(), l, inverse != 0, s);
+    butterfly_device(E.as<uint4>(), l, partition_base(l), inverse != 0, s);
     FPM_CUDA(cudaMemcpyAsync(ev, E.p, eb, cudaMemcpyDeviceToHost, s));
   });
 }

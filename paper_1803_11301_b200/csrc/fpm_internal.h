@@ -45,11 +45,21 @@ struct DeviceTables {
   uint4* c2p = nullptr;       // 4 x 512: part p entry e = C2P(2 * (e << 9p))
 };
 
-// Twiddle generator inputs: w(i, b) = v_{l+64-i} ^ C2P(2b).
+// Twiddle generator inputs (passed by value as a kernel parameter):
+//   w(i, b) = C2P((base >> i) ^ 2b) = layer[i] ^ C2P(2b)      (butterfly.cpp:45-49; C2P is linear)
+// layer[i] = C2P(base >> i); the pipeline's base is e_{l+64} (encode.cpp:47) so layer[i] = v_{l+64-i}.
+constexpr int kMaxLayers = 64;
 struct TwiddleSrc {
-  const uint4* cantor;
-  const uint4* c2p;
+  const uint4* c2p;          // device: 4 x 512 C2P(2 * (e << 9p)) tables
+  uint4 layer[kMaxLayers];   // C2P(base >> i)
 };
+// Host: twiddle source for plan_butterflies(l, base) (base in Cantor coordinates).
+TwiddleSrc make_twiddle_src(int device, unsigned l, U128 base);
+inline U128 partition_base(unsigned l) {  // make_partition_spec<gf128>(l).base = e_{l+64}
+  U128 b;
+  if (l + 64 < 64) b.lo = uint64_t{1} << (l + 64); else b.hi = uint64_t{1} << (l + 64 - 64);
+  return b;
+}
 
 const DeviceTables& device_tables(int device);
 
@@ -64,14 +74,15 @@ void encode_device_rows(const uint32_t* poly, unsigned l, uint4* ev, int rows_li
 void decode_device(const uint4* ev, unsigned l, uint32_t* poly, cudaStream_t s);
 
 // Butterflies (k_fft.cu).
-void butterfly_device(uint4* ev, unsigned l, bool inverse, cudaStream_t s);
+void butterfly_device(uint4* ev, unsigned l, U128 base, bool inverse, cudaStream_t s);
 void pointwise_device(const uint4* u, const uint4* v, uint4* out, size_t n, cudaStream_t s);
-// Fused: forward layers [0, T) of b's tiles, * a, inverse layers [0, T); top layers excluded.
-// Pipeline helpers exposing the split between top (global) and bottom (tile) layers.
+// Pipeline helpers exposing the split between top (global, M4R) and bottom (tile) layers.
 unsigned fft_tile_log2(unsigned l);
-void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, cudaStream_t s);
-void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, cudaStream_t s);
-void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, cudaStream_t s);
+void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s);
+void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s);
+// Fused: forward layers [0, T) of b's tiles, pointwise * a, inverse layers [0, T).
+void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
+                                 cudaStream_t s);
 
 // Whole small products in one CTA each (k_batch.cu); n_bits = padded product length <= 2^17.
 void polymul_batch_device(const uint64_t* a, size_t a_bits, size_t a_stride_words,

@@ -44,7 +44,7 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 // Forward transform of one operand: W0 <- x (n/2 bits), basis conversion, encode into E, butterflies.
 __device__ void transform_operand(const uint64_t* __restrict__ x, uint64_t x_bits, uint32_t* W0, uint32_t* W1,
                                   uint4* E, unsigned l, int half_words, const PassList& pl_half,
-                                  const uint4* __restrict__ enc_rows, TwiddleSrc tw) {
+                                  const uint4* __restrict__ enc_rows, const TwiddleSrc& tw) {
   const int tid = threadIdx.x;
   const uint32_t* x32 = reinterpret_cast<const uint32_t*>(x);
   for (int i = tid; i < half_words; i += blockDim.x) {
@@ -86,7 +86,7 @@ __device__ void transform_operand(const uint64_t* __restrict__ x, uint64_t x_bit
   __syncthreads();
   // forward butterflies, layers l-1 .. 0 (kernels_impl.hpp:29-47)
   for (int i = (int)l - 1; i >= 0; --i) {
-    const uint4 vbase = tw.cantor[l + 64 - i];
+    const uint4 vbase = tw.layer[i];
     for (int p = tid; p < n_p / 2; p += blockDim.x) {
       const int blk = p >> i, j = p & ((1 << i) - 1);
       const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(256) batch_kernel(const uint64_t* __restrict__
   __syncthreads();
   // inverse butterflies, layers 0 .. l-1 (kernels_impl.hpp:48-61)
   for (unsigned i = 0; i < l; ++i) {
-    const uint4 vbase = tw.cantor[l + 64 - i];
+    const uint4 vbase = tw.layer[i];
     for (int p = tid; p < n_p / 2; p += blockDim.x) {
       const int blk = p >> i, j = p & ((1 << i) - 1);
       const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
@@ -217,7 +217,7 @@ void polymul_batch_device(const uint64_t* a, size_t a_bits, size_t a_stride_word
     batch_kernel<<<(unsigned)cnt, 256, smem, s>>>(a + off * a_stride_words, a_bits, a_stride_words,
                                                   b + off * b_stride_words, b_bits, b_stride_words,
                                                   c + off * c_stride_words, c_stride_words, l, pl_half, pl_full_inv,
-                                                  dt.enc_rows, dt.inv_rows, TwiddleSrc{dt.cantor, dt.c2p});
+                                                  dt.enc_rows, dt.inv_rows, make_twiddle_src(dev, l, partition_base(l)));
     FPM_LAUNCH_CHECK();
   }
 }

@@ -36,8 +36,8 @@ __device__ __forceinline__ uint4 c2p2(const uint4* __restrict__ c2p, uint64_t b)
   return r;
 }
 
-__device__ __forceinline__ uint4 twiddle(TwiddleSrc tw, unsigned l, unsigned i, uint64_t b) {
-  return x4(tw.cantor[l + 64 - i], c2p2(tw.c2p, b));
+__device__ __forceinline__ uint4 twiddle(const TwiddleSrc& tw, unsigned l, unsigned i, uint64_t b) {
+  return x4(tw.layer[i], c2p2(tw.c2p, b));
 }
 
 // ------------------------------------------------------------------ top layers (i >= T)
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(256) fft_top_kernel(uint4* __restrict__ ev, un
 // ------------------------------------------------------------------ tile layers (i < T)
 template <bool INV>
 __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, unsigned l, uint64_t tile_idx,
-                                            TwiddleSrc tw) {
+                                            const TwiddleSrc& tw) {
   const int npairs = 1 << (T - 1);
   for (unsigned step = 0; step < T; ++step) {
     const unsigned i = INV ? step : T - 1 - step;
@@ -144,13 +144,6 @@ int sms() {
   return n;
 }
 
-TwiddleSrc twiddle_src() {
-  int dev;
-  FPM_CUDA(cudaGetDevice(&dev));
-  const DeviceTables& dt = device_tables(dev);
-  return TwiddleSrc{dt.cantor, dt.c2p};
-}
-
 template <class K>
 void set_smem(K kernel, size_t bytes) {
   FPM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
@@ -160,9 +153,23 @@ void set_smem(K kernel, size_t bytes) {
 
 unsigned fft_tile_log2(unsigned l) { return l < (unsigned)kTileMax ? l : (unsigned)kTileMax; }
 
-void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, cudaStream_t s) {
+TwiddleSrc make_twiddle_src(int device, unsigned l, U128 base) {
+  if (l > (unsigned)kMaxLayers) throw Error(kInvalid, "butterfly: too many layers");
+  TwiddleSrc tw{};
+  tw.c2p = device_tables(device).c2p;
+  const FieldTables& ft = field_tables();
+  for (unsigned i = 0; i < l; ++i) {
+    U128 c;  // base >> i (Cantor coordinates)
+    c.lo = i == 0 ? base.lo : (i < 64 ? (base.lo >> i) | (base.hi << (64 - i)) : base.hi >> (i - 64));
+    c.hi = i < 64 ? (i == 0 ? base.hi : base.hi >> i) : 0;
+    const U128 p = host_cantor_to_poly(ft, c);
+    tw.layer[i] = make_uint4((uint32_t)p.lo, (uint32_t)(p.lo >> 32), (uint32_t)p.hi, (uint32_t)(p.hi >> 32));
+  }
+  return tw;
+}
+
+void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s) {
   if (l <= T) return;
-  const TwiddleSrc tw = twiddle_src();
   const size_t smem = kM4RUint4 * sizeof(uint4);
   static bool attr = false;
   if (!attr) { set_smem(fft_top_kernel<false>, smem); set_smem(fft_top_kernel<true>, smem); attr = true; }
@@ -180,9 +187,8 @@ void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, cudaS
   }
 }
 
-void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, cudaStream_t s) {
+void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s) {
   if (T == 0) return;
-  const TwiddleSrc tw = twiddle_src();
   const size_t smem = ((size_t)1 << T) * sizeof(uint4);
   static bool attr = false;
   if (!attr) {
@@ -197,8 +203,8 @@ void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, cuda
   FPM_LAUNCH_CHECK();
 }
 
-void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, cudaStream_t s) {
-  const TwiddleSrc tw = twiddle_src();
+void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
+                                 cudaStream_t s) {
   const size_t smem = ((size_t)1 << T) * sizeof(uint4);
   static bool attr = false;
   if (!attr) { set_smem(fft_tile_fused_kernel, (size_t)1 << kTileMax << 4); attr = true; }
@@ -208,14 +214,17 @@ void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigne
   FPM_LAUNCH_CHECK();
 }
 
-void butterfly_device(uint4* ev, unsigned l, bool inverse, cudaStream_t s) {
+void butterfly_device(uint4* ev, unsigned l, U128 base, bool inverse, cudaStream_t s) {
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  const TwiddleSrc tw = make_twiddle_src(dev, l, base);
   const unsigned T = fft_tile_log2(l);
   if (!inverse) {
-    butterfly_top_device(ev, l, T, false, s);
-    butterfly_tile_device(ev, l, T, false, s);
+    butterfly_top_device(ev, l, T, false, tw, s);
+    butterfly_tile_device(ev, l, T, false, tw, s);
   } else {
-    butterfly_tile_device(ev, l, T, true, s);
-    butterfly_top_device(ev, l, T, true, s);
+    butterfly_tile_device(ev, l, T, true, tw, s);
+    butterfly_top_device(ev, l, T, true, tw, s);
   }
 }
 
