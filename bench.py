@@ -10,8 +10,9 @@ Contract (one JSON line on rank 0):
                timed on this host's cores, rank 0 at N=1 only, on a bounded sample
   --impl reference   times the reference's own CPU implementation instead (rank 0 only)
 
-Multi-GPU (torchrun, N>1): this round each rank multiplies its own pair of operands (replicas,
-"scaling": "weak"); value = step time / (products per step) over the whole job.
+Multi-GPU (torchrun, N>1): by default ONE product is sharded over the N GPUs
+(paper_1803_11301_b200/dist.py: the top log2 N butterfly layers exchange halves over NCCL P2P;
+"scaling": "strong"); --mode replicas runs N independent products instead ("weak").
 """
 from __future__ import annotations
 
@@ -200,6 +201,8 @@ def main():
     ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
+    ap.add_argument("--mode", default="shard", choices=["shard", "replicas"],
+                    help="N>1: shard one product over the GPUs (default) or run independent replicas")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     ws, rank, local = dist_env()
@@ -226,16 +229,27 @@ def main():
     bits = CONFIGS[args.config]
     words = bits // 64
     out_words = (2 * bits - 1 + 63) // 64
-    a = rand_words(torch, words, 1000 + rank, dev)
-    b = rand_words(torch, words, 2000 + rank, dev)
+    mode = "single" if ws == 1 else args.mode
+    seed_off = rank if mode == "replicas" else 0  # shard: every rank holds the same operands
+    a = rand_words(torch, words, 1000 + seed_off, dev)
+    b = rand_words(torch, words, 2000 + seed_off, dev)
     c = torch.empty(out_words, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
+    from paper_1803_11301_b200 import dist as pdist
+    backend = pdist.GpuBackend() if mode == "shard" else None
+    plan = pdist.make_plan(bits, bits, ws, rank) if mode == "shard" else None
+
+    def step(x, y):
+        if mode == "shard":
+            return pdist.polymul_sharded(x, bits, y, bits, backend, plan)
+        pkg.fp_polymul_dev(x, bits, y, bits, c, field=pkg.FIELD_GF128)
+        return c
 
     for _ in range(args.warmup):
-        pkg.fp_polymul_dev(a, bits, b, bits, c, field=pkg.FIELD_GF128)
+        step(a, b)
     torch.cuda.synchronize()
 
-    # ---- timed region: device-resident
+    # ---- timed region: device-resident inputs
     pkg.launch_count(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -243,7 +257,7 @@ def main():
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(args.steps):
-            pkg.fp_polymul_dev(a, bits, b, bits, c, field=pkg.FIELD_GF128)
+            res_dev = step(a, b)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -253,26 +267,38 @@ def main():
     if ws > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(t.item())
+    dev_result = res_dev.cpu().numpy().view(np.uint64).copy()
 
-    # ---- e2e: C-ABI host entry point, pinned host buffers, copies inside every step
+    # ---- e2e: pinned HOST buffers; H2D of both operands and D2H of the product in every step
     ha = torch.empty(words, dtype=torch.int64, pin_memory=True)
     hb = torch.empty(words, dtype=torch.int64, pin_memory=True)
     hc = torch.empty(out_words, dtype=torch.int64, pin_memory=True)
     ha.copy_(a)
     hb.copy_(b)
     na, nb, nc = (x.numpy().view(np.uint64) for x in (ha, hb, hc))
-    pkg.fp_polymul(na, bits, nb, bits, field=pkg.FIELD_GF128, device=local)  # warm host path
+
+    def e2e_step():
+        if mode == "single":  # the C-ABI host entry point fpm_polymul (include/fpmul_b200.h)
+            return pkg.fp_polymul(na, bits, nb, bits, field=pkg.FIELD_GF128, device=local, out=nc)
+        xa = ha.to(dev, non_blocking=True)
+        xb = hb.to(dev, non_blocking=True)
+        r = step(xa, xb)
+        hc.copy_(r)
+        torch.cuda.synchronize()
+        return nc
+
+    e2e_step()
     e2e_steps = max(1, min(args.steps, 5))
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        res = pkg.fp_polymul(na, bits, nb, bits, field=pkg.FIELD_GF128, device=local)
+        res = e2e_step()
     e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
     t = torch.tensor([e2e_ms], device=dev)
     if ws > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     e2e_ms = float(t.item())
-    same = bool(np.array_equal(res, c.cpu().numpy().view(np.uint64)))
+    same = bool(np.array_equal(res, dev_result))
 
     # ---- roofline: per-stage CUDA-event times of one instrumented product
     st = [0.0] * pkg.NUM_STAGES
@@ -298,15 +324,17 @@ def main():
     roof["stage_ms"] = {k: round(v * 1e3, 3) for k, v in stages.items()}
 
     line = {
-        "metric": METRIC, "value": round(ms_max / ws if ws > 1 else ms_max, 3), "unit": "ms", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 3), "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (uniform random bits, seeded)",
+        "metric": METRIC, "value": round(ms_max / ws if mode == "replicas" else ms_max, 3), "unit": "ms",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 3),
+        "higher_is_better": False, "scaling": "weak" if mode == "replicas" else "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic (uniform random bits, seeded)",
         "config": {"workload": f"cfg{args.config}: 2^{bits.bit_length()-1} x 2^{bits.bit_length()-1}-bit product, "
                                f"GF(2^128) Frobenius FFT (n=2^{(2*bits).bit_length()-1}, "
                                f"l={(2*bits//128).bit_length()-1})",
-                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
+                   "parallelism": {"single": "single GPU", "replicas": f"{ws} independent products (replicas)",
+                                   "shard": f"one product sharded over {ws} GPUs: top {ws.bit_length() - 1} butterfly "
+                                            "layers exchanged over NCCL P2P, basis conversions replicated"}[mode],
                    "l2": "inputs >= 2x L2 per operand at cfg4/5 (no flush needed)" if bits >= 1 << 28 else "inputs fit in L2"},
-        "e2e": {"value": round(e2e_ms / ws if ws > 1 else e2e_ms, 3), "unit": "ms", "steps": e2e_steps,
+        "e2e": {"value": round(e2e_ms / ws if mode == "replicas" else e2e_ms, 3), "unit": "ms", "steps": e2e_steps,
                 "h2d_bytes_per_step": 2 * words * 8, "d2h_bytes_per_step": out_words * 8,
                 "matches_device_result": same},
         "gpu_launches": int(launches),

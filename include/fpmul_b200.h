@@ -106,6 +106,25 @@ fpm_status fpm_lch_butterfly_dev(uint64_t* d_ev, unsigned l, const uint64_t* bas
 /* pointwise_mul<gf128> (polymul.hpp:78-80): d_out[i] = d_u[i]*d_v[i] over n elements (may alias). */
 fpm_status fpm_pointwise_dev(const uint64_t* d_u, const uint64_t* d_v, uint64_t* d_out, size_t n, void* stream);
 
+/* ---- sharded multi-GPU building blocks (one process per GPU) ----
+ * Rank g of P owns elements [g*n_p/P, (g+1)*n_p/P) of every EvalVec.  Encode/decode are
+ * element-local, the lower l - log2(P) butterfly layers are a sub-FFT with base ^ (g*n_p/P)
+ * (fpm_lch_butterfly_dev), and only the top log2(P) layers exchange halves with a partner. */
+/* encode of element columns [col0, col0+ncols) of the 128 x 2^l partition matrix in d_poly
+ * (rows_live 64: rows >= 64 known zero, as for pipeline operands; else 128).  1024-aligned. */
+fpm_status fpm_encode_cols_dev(const uint64_t* d_poly, unsigned l, size_t col0, size_t ncols, int rows_live,
+                               uint64_t* d_ev, void* stream);
+/* decode of ncols elements into a 128-row x ncols-bit slice (row pitch ncols bits). */
+fpm_status fpm_decode_cols_dev(const uint64_t* d_ev, size_t ncols, uint64_t* d_slice, void* stream);
+/* One exchanged butterfly layer: d_mine holds this rank's half (side 0 = the p0 block half,
+ * side 1 = the p1 half), d_theirs the partner's; w (2 words, polynomial rep) is the layer's
+ * twiddle for this block.  Forward: p0' = p0 + w p1, p1' = p1 + p0'; inverse undoes it. */
+fpm_status fpm_bfly_pair_dev(uint64_t* d_mine, const uint64_t* d_theirs, size_t n, const uint64_t* w, int side,
+                             int inverse, void* stream);
+/* Host: the twiddle C2P((base >> i) ^ 2b) of layer i, block b (butterfly.cpp:45-49); base in
+ * Cantor coordinates {lo, hi}; out = {lo, hi} polynomial representation. */
+fpm_status fpm_twiddle128(unsigned i, uint64_t b, const uint64_t* base, uint64_t* out);
+
 /* ---- host-buffer stage wrappers (synchronous; same semantics as the *_dev calls) ---- */
 fpm_status fpm_basis_cvt(uint64_t* w, size_t n_bits, size_t content_bits, int device);
 fpm_status fpm_i_basis_cvt(uint64_t* w, size_t n_bits, int device);

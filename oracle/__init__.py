@@ -155,6 +155,7 @@ class _Ref:
         L.ref_decode128.argtypes = [_u64p, C.c_uint, _u64p, C.c_int]
         L.ref_butterfly128.argtypes = [_u64p, C.c_uint, C.c_int, C.c_int]
         L.ref_pointwise128.argtypes = [_u64p, _u64p, _u64p, C.c_size_t]
+        L.ref_butterfly128_base.argtypes = [_u64p, C.c_uint, C.c_uint64, C.c_uint64, C.c_int]
         L.ref_gf128_mul.argtypes = [_u64p, _u64p, _u64p]
         L.ref_tables128.argtypes = [_u64p, _u64p, _u64p]
         L.ref_twiddles128.argtypes = [C.c_uint, _u64p]
@@ -228,6 +229,11 @@ class _Ref:
     def butterfly128(self, ev, l, inverse=False, parallel=True):
         ev = np.ascontiguousarray(ev, np.uint64).copy()
         self._chk(self.L.ref_butterfly128(_ptr(ev), l, int(inverse), int(parallel)))
+        return ev
+
+    def butterfly128_base(self, ev, l, base_lo, base_hi, inverse=False):
+        ev = np.ascontiguousarray(ev, np.uint64).copy()
+        self._chk(self.L.ref_butterfly128_base(_ptr(ev), l, base_lo, base_hi, int(inverse)))
         return ev
 
     def pointwise128(self, u, v):

@@ -182,6 +182,17 @@ int ref_butterfly128(uint64_t* ev, unsigned l, int inverse, int parallel) {
     store_ev(v, ev);
   });
 }
+// lch_butterfly / i_lch_butterfly<gf128> with plan_butterflies(l, base) for an arbitrary base
+// (Cantor coordinates {lo, hi}) -- butterfly.cpp:32-85.
+int ref_butterfly128_base(uint64_t* ev, unsigned l, uint64_t base_lo, uint64_t base_hi, int inverse) {
+  return guard([&] {
+    const auto plan = plan_butterflies<gf128>(l, CantorVec<gf128>{u128{base_hi, base_lo}});
+    auto v = load_ev(ev, size_t{1} << l);
+    if (inverse) i_lch_butterfly<gf128>(std::span<FieldElem<gf128>>(v), plan, ExecPolicy::kSerial);
+    else lch_butterfly<gf128>(std::span<FieldElem<gf128>>(v), plan, ExecPolicy::kSerial);
+    store_ev(v, ev);
+  });
+}
 int ref_pointwise128(const uint64_t* u, const uint64_t* v, uint64_t* out, size_t n) {
   return guard([&] {
     auto a = load_ev(u, n), b = load_ev(v, n);

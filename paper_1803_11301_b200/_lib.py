@@ -66,6 +66,12 @@ def lib():
         L.fpm_pointwise.argtypes = [_u64p, _u64p, _u64p, sz, C.c_int]
         L.fpm_gf128_mul.argtypes = [_u64p, _u64p, _u64p, sz, C.c_int]
         L.fpm_tables128.argtypes = [_u64p, _u64p, _u64p]
+        L.fpm_lch_butterfly_dev.argtypes = [vp, C.c_uint, _u64p, C.c_int, vp]
+        L.fpm_lch_butterfly.argtypes = [_u64p, C.c_uint, _u64p, C.c_int, C.c_int]
+        L.fpm_encode_cols_dev.argtypes = [vp, C.c_uint, sz, sz, C.c_int, vp, vp]
+        L.fpm_decode_cols_dev.argtypes = [vp, sz, vp, vp]
+        L.fpm_bfly_pair_dev.argtypes = [vp, vp, sz, _u64p, C.c_int, C.c_int, vp]
+        L.fpm_twiddle128.argtypes = [C.c_uint, C.c_uint64, _u64p, _u64p]
         _LIB = L
     return _LIB
 
@@ -117,14 +123,20 @@ def tables128():
 
 # ----------------------------------------------------------------------------- host buffers
 def fp_polymul(a, a_bits: int, b, b_bits: int, field: int = FIELD_AUTO, device: int = 0,
-               stage_seconds: list | None = None) -> np.ndarray:
-    """fp_polymul (proj/src/polymul.cpp:223-239): returns ceil((a_bits+b_bits-1)/64) words."""
+               stage_seconds: list | None = None, out: np.ndarray | None = None) -> np.ndarray:
+    """fp_polymul (proj/src/polymul.cpp:223-239): returns ceil((a_bits+b_bits-1)/64) words
+    (written into `out` when given, e.g. a pinned buffer)."""
     a, b = _as_u64(a), _as_u64(b)
     if a.size < _words(a_bits) or b.size < _words(b_bits):
         raise ValueError("fp_polymul: word arrays shorter than the declared bit lengths")
     if a_bits == 0 or b_bits == 0:
         return np.zeros(0, np.uint64)
-    c = np.zeros(_words(a_bits + b_bits - 1), np.uint64)
+    if out is not None:
+        if out.dtype != np.uint64 or out.size < _words(a_bits + b_bits - 1):
+            raise ValueError("fp_polymul: output buffer too small")
+        c = out
+    else:
+        c = np.zeros(_words(a_bits + b_bits - 1), np.uint64)
     st = (C.c_double * NUM_STAGES)()
     _check(lib().fpm_polymul(_ptr(a), a_bits, _ptr(b), b_bits, _ptr(c), field, device,
                              st if stage_seconds is not None else None))

@@ -426,6 +426,51 @@ fpm_status fpm_lch_butterfly_dev(uint64_t* d_ev, unsigned l, const uint64_t* bas
   });
 }
 
+fpm_status fpm_encode_cols_dev(const uint64_t* d_poly, unsigned l, size_t col0, size_t ncols, int rows_live,
+                               uint64_t* d_ev, void* stream) {
+  return guard([&] {
+    require_device();
+    if (l >= 64) throw Error(kInvalid, "PartitionSpec: l must satisfy l < m/2");
+    encode_cols_device(reinterpret_cast<const uint32_t*>(d_poly), l, col0, ncols, reinterpret_cast<uint4*>(d_ev),
+                       rows_live == 64 ? 64 : 128, (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_decode_cols_dev(const uint64_t* d_ev, size_t ncols, uint64_t* d_slice, void* stream) {
+  return guard([&] {
+    require_device();
+    decode_cols_device(reinterpret_cast<const uint4*>(d_ev), ncols, reinterpret_cast<uint32_t*>(d_slice),
+                       (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_bfly_pair_dev(uint64_t* d_mine, const uint64_t* d_theirs, size_t n, const uint64_t* w, int side,
+                             int inverse, void* stream) {
+  return guard([&] {
+    require_device();
+    if (!w || (side != 0 && side != 1)) throw Error(kInvalid, "bfly_pair: bad twiddle or side");
+    U128 t;
+    t.lo = w[0];
+    t.hi = w[1];
+    bfly_pair_device(reinterpret_cast<uint4*>(d_mine), reinterpret_cast<const uint4*>(d_theirs), n, t, side,
+                     inverse != 0, (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_twiddle128(unsigned i, uint64_t b, const uint64_t* base, uint64_t* out) {
+  return guard([&] {
+    if (!base || !out || i >= 128) throw Error(kInvalid, "twiddle: bad arguments");
+    U128 c;  // (base >> i) ^ 2b
+    c.lo = i == 0 ? base[0] : (i < 64 ? (base[0] >> i) | (base[1] << (64 - i)) : base[1] >> (i - 64));
+    c.hi = i == 0 ? base[1] : (i < 64 ? base[1] >> i : 0);
+    c.lo ^= b << 1;
+    c.hi ^= b >> 63;
+    const U128 p = host_cantor_to_poly(field_tables(), c);
+    out[0] = p.lo;
+    out[1] = p.hi;
+  });
+}
+
 fpm_status fpm_pointwise_dev(const uint64_t* d_u, const uint64_t* d_v, uint64_t* d_out, size_t n, void* stream) {
   return guard([&] {
     require_device();

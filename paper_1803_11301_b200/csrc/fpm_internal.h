@@ -71,6 +71,13 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
 void encode_device(const uint32_t* poly, unsigned l, uint4* ev, cudaStream_t s);
 // rows_live = 64: rows >= 64 of poly are known zero (pipeline operands) and not read.
 void encode_device_rows(const uint32_t* poly, unsigned l, uint4* ev, int rows_live, cudaStream_t s);
+// Column (element) range of the partition matrix; used by the sharded multi-GPU product.
+void encode_cols_device(const uint32_t* poly, unsigned l, uint64_t col0, uint64_t ncols, uint4* ev, int rows_live,
+                        cudaStream_t s);
+void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaStream_t s);
+// One exchanged butterfly layer (sharded FFT): this rank holds `mine` (side 0 = p0 half, 1 = p1 half),
+// the partner's half arrived in `theirs`; uniform twiddle w.  Result replaces `mine`.
+void bfly_pair_device(uint4* mine, const uint4* theirs, uint64_t n, U128 w, int side, bool inverse, cudaStream_t s);
 void decode_device(const uint4* ev, unsigned l, uint32_t* poly, cudaStream_t s);
 
 // Butterflies (k_fft.cu).

@@ -37,22 +37,21 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
 }
 
 template <int ROWS>  // 64: rows >= 64 are known zero (pipeline); 128: general encode
-__global__ void __launch_bounds__(256) encode_kernel(const uint32_t* __restrict__ poly, uint64_t n_p,
+__global__ void __launch_bounds__(256) encode_kernel(const uint32_t* __restrict__ poly, uint64_t row_words,
+                                                     uint64_t col0_words, uint64_t nslabs,
                                                      const uint4* __restrict__ tab_g, uint4* __restrict__ ev) {
   extern __shared__ uint4 smem4[];
   uint4* tab = smem4;                                           // (ROWS/4) chunks x 16 x 8 copies
   uint32_t* slab = reinterpret_cast<uint32_t*>(smem4 + (ROWS / 4) * 16 * kM4RCopies);  // ROWS x kPad
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < (ROWS / 4) * 16 * kM4RCopies; i += blockDim.x) tab[i] = tab_g[i];
-  const uint64_t row_words = n_p / 32;
-  const uint64_t nslabs = row_words / kSlabWords;
   const int copy = lane & 7;
   for (uint64_t sl = blockIdx.x; sl < nslabs; sl += gridDim.x) {
     const uint64_t w0 = sl * kSlabWords;
     __syncthreads();
     for (int i = tid; i < ROWS * kSlabWords; i += blockDim.x) {
       const int r = i / kSlabWords, c = i % kSlabWords;
-      slab[r * kPad + c] = poly[(uint64_t)r * row_words + w0 + c];
+      slab[r * kPad + c] = poly[(uint64_t)r * row_words + col0_words + w0 + c];
     }
     __syncthreads();
 #pragma unroll 1
@@ -82,15 +81,14 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint32_t* __restrict_
   }
 }
 
-__global__ void __launch_bounds__(256) decode_kernel(const uint4* __restrict__ ev, uint64_t n_p,
+__global__ void __launch_bounds__(256) decode_kernel(const uint4* __restrict__ ev, uint64_t nslabs,
+                                                     uint64_t row_words,
                                                      const uint4* __restrict__ tab_g, uint32_t* __restrict__ poly) {
   extern __shared__ uint4 smem4[];
   uint4* tab = smem4;  // 32 chunks x 16 x 8 copies
   uint32_t* slab = reinterpret_cast<uint32_t*>(smem4 + kM4RUint4);  // 128 x kPad
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < kM4RUint4; i += blockDim.x) tab[i] = tab_g[i];
-  const uint64_t row_words = n_p / 32;
-  const uint64_t nslabs = row_words / kSlabWords;
   const int copy = lane & 7;
   __syncthreads();
   for (uint64_t sl = blockIdx.x; sl < nslabs; sl += gridDim.x) {
@@ -181,53 +179,67 @@ int grid_for(uint64_t work, int per_sm) {
 
 }  // namespace
 
-// rows_live: 64 when rows >= 64 are known zero (pipeline), else 128.
-void encode_device_rows(const uint32_t* poly, unsigned l, uint4* ev, int rows_live, cudaStream_t s) {
+// Column range [col0, col0 + ncols) of the 128-row partition matrix (row pitch n_p bits) -> ncols
+// elements.  rows_live: 64 when rows >= 64 are known zero (pipeline operands), else 128.
+void encode_cols_device(const uint32_t* poly, unsigned l, uint64_t col0, uint64_t ncols, uint4* ev, int rows_live,
+                        cudaStream_t s) {
   int dev;
   FPM_CUDA(cudaGetDevice(&dev));
   const uint64_t n_p = (uint64_t)1 << l;
   if (n_p < 1024) {
+    if (col0 != 0 || ncols != n_p) throw Error(kInvalid, "encode: column ranges need n_p >= 1024");
     encode_small_kernel<<<(unsigned)((n_p + 127) / 128), 128, 0, s>>>(poly, n_p, row_tables(dev).rows, ev);
     FPM_LAUNCH_CHECK();
     return;
   }
+  if (col0 % 1024 || ncols % 1024 || col0 + ncols > n_p) throw Error(kInvalid, "encode: column range not 1024-aligned");
   const DeviceTables& dt = device_tables(dev);
-  const uint64_t nslabs = n_p / 32 / kSlabWords;
+  const uint64_t nslabs = ncols / 32 / kSlabWords;
   if (rows_live == 64) {
     const size_t smem = 16 * 16 * kM4RCopies * sizeof(uint4) + 64 * kPad * sizeof(uint32_t);
     static bool attr = false;
     if (!attr) { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); attr = true; }
-    encode_kernel<64><<<grid_for(nslabs, 4), 256, smem, s>>>(poly, n_p, dt.enc_m4r, ev);
+    encode_kernel<64><<<grid_for(nslabs, 4), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, dt.enc_m4r, ev);
   } else {
     const size_t smem = 32 * 16 * kM4RCopies * sizeof(uint4) + 128 * kPad * sizeof(uint32_t);
     static bool attr = false;
     if (!attr) { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); attr = true; }
-    encode_kernel<128><<<grid_for(nslabs, 2), 256, smem, s>>>(poly, n_p, dt.enc_m4r, ev);
+    encode_kernel<128><<<grid_for(nslabs, 2), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, dt.enc_m4r, ev);
   }
   FPM_LAUNCH_CHECK();
+}
+
+void encode_device_rows(const uint32_t* poly, unsigned l, uint4* ev, int rows_live, cudaStream_t s) {
+  encode_cols_device(poly, l, 0, (uint64_t)1 << l, ev, rows_live, s);
 }
 
 void encode_device(const uint32_t* poly, unsigned l, uint4* ev, cudaStream_t s) {
   encode_device_rows(poly, l, ev, 128, s);
 }
 
-void decode_device(const uint4* ev, unsigned l, uint32_t* poly, cudaStream_t s) {
+// ncols elements -> a 128-row x ncols-bit slice (row pitch ncols bits).
+void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaStream_t s) {
   int dev;
   FPM_CUDA(cudaGetDevice(&dev));
-  const uint64_t n_p = (uint64_t)1 << l;
-  if (n_p < 1024) {
-    const uint64_t nwords = (128 * n_p + 31) / 32;
-    decode_small_kernel<<<(unsigned)((nwords + 127) / 128), 128, 0, s>>>(ev, n_p, row_tables(dev).inv, poly);
+  if (ncols < 1024) {
+    if (ncols & (ncols - 1)) throw Error(kInvalid, "decode: element count must be a power of two");
+    const uint64_t nwords = (128 * ncols + 31) / 32;
+    decode_small_kernel<<<(unsigned)((nwords + 127) / 128), 128, 0, s>>>(ev, ncols, row_tables(dev).inv, slice);
     FPM_LAUNCH_CHECK();
     return;
   }
+  if (ncols % 1024) throw Error(kInvalid, "decode: column count not 1024-aligned");
   const DeviceTables& dt = device_tables(dev);
   const size_t smem = kM4RUint4 * sizeof(uint4) + 128 * kPad * sizeof(uint32_t);
   static bool attr = false;
   if (!attr) { FPM_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); attr = true; }
-  const uint64_t nslabs = n_p / 32 / kSlabWords;
-  decode_kernel<<<grid_for(nslabs, 2), 256, smem, s>>>(ev, n_p, dt.dec_m4r, poly);
+  const uint64_t nslabs = ncols / 32 / kSlabWords;
+  decode_kernel<<<grid_for(nslabs, 2), 256, smem, s>>>(ev, nslabs, ncols / 32, dt.dec_m4r, slice);
   FPM_LAUNCH_CHECK();
+}
+
+void decode_device(const uint4* ev, unsigned l, uint32_t* poly, cudaStream_t s) {
+  decode_cols_device(ev, (uint64_t)1 << l, poly, s);
 }
 
 }  // namespace fpm

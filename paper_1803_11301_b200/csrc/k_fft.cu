@@ -131,6 +131,29 @@ __global__ void __launch_bounds__(256) fft_tile_fused_kernel(const uint4* __rest
   }
 }
 
+// Exchanged layer of the sharded FFT: all local elements share one twiddle w.
+template <bool INV>
+__global__ void __launch_bounds__(256) fft_pair_kernel(uint4* __restrict__ mine, const uint4* __restrict__ theirs,
+                                                       uint64_t n, uint4 w, int side, int ppc) {
+  extern __shared__ uint4 tab[];
+  __shared__ uint4 rows[128];
+  m4r_build(tab, rows, w, threadIdx.x, blockDim.x);
+  const int copy = threadIdx.x & 7;
+  const uint64_t k0 = (uint64_t)blockIdx.x * ppc;
+  for (int k = threadIdx.x; k < ppc; k += blockDim.x) {
+    const uint64_t e = k0 + k;
+    if (e >= n) break;
+    const uint4 a = mine[e], b = theirs[e];
+    uint4 r;
+    if (!INV) {  // p0' = p0 + w p1 ; p1' = p1 + p0'
+      r = side == 0 ? x4(a, m4r_mul(tab, b, copy)) : xor3(a, b, m4r_mul(tab, a, copy));
+    } else {     // p1' = p1 + p0 ; p0' = p0 + w p1'
+      r = side == 0 ? x4(a, m4r_mul(tab, x4(a, b), copy)) : x4(a, b);
+    }
+    mine[e] = r;
+  }
+}
+
 __global__ void pointwise_kernel(const uint4* __restrict__ u, const uint4* __restrict__ v, uint4* __restrict__ out,
                                  uint64_t n) {
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
@@ -226,6 +249,20 @@ void butterfly_device(uint4* ev, unsigned l, U128 base, bool inverse, cudaStream
     butterfly_tile_device(ev, l, T, true, tw, s);
     butterfly_top_device(ev, l, T, true, tw, s);
   }
+}
+
+void bfly_pair_device(uint4* mine, const uint4* theirs, uint64_t n, U128 w, int side, bool inverse, cudaStream_t s) {
+  if (!n) return;
+  const size_t smem = kM4RUint4 * sizeof(uint4);
+  static bool attr = false;
+  if (!attr) { set_smem(fft_pair_kernel<false>, smem); set_smem(fft_pair_kernel<true>, smem); attr = true; }
+  uint64_t ppc = 4096;
+  while (ppc > 256 && n / ppc < (uint64_t)sms() * 2) ppc /= 2;
+  const unsigned ctas = (unsigned)((n + ppc - 1) / ppc);
+  const uint4 w4 = make_uint4((uint32_t)w.lo, (uint32_t)(w.lo >> 32), (uint32_t)w.hi, (uint32_t)(w.hi >> 32));
+  if (!inverse) fft_pair_kernel<false><<<ctas, 256, smem, s>>>(mine, theirs, n, w4, side, (int)ppc);
+  else fft_pair_kernel<true><<<ctas, 256, smem, s>>>(mine, theirs, n, w4, side, (int)ppc);
+  FPM_LAUNCH_CHECK();
 }
 
 void pointwise_device(const uint4* u, const uint4* v, uint4* out, size_t n, cudaStream_t s) {

@@ -1,0 +1,204 @@
+"""Sharded single-product multiplication across GPUs (one process per GPU, torch.distributed).
+
+SURVEY.md 8(e): rank g of P owns elements [g*m, (g+1)*m), m = n_p / P, of every EvalVec.
+
+* basis conversion of the operands: replicated (every rank holds both inputs);
+* encode: element-local -- rank g encodes columns [g*m, (g+1)*m) of the partition matrix;
+* forward FFT: layers i >= l' = l - log2 P pair element e with e ^ 2^i, which lives on rank
+  g ^ 2^(i - l'): ONE exchange of the rank's whole slice with that partner per layer, then a local
+  half-butterfly with the block's (rank-uniform) twiddle C2P((base >> i) ^ 2b), b = g*m >> (i+1);
+* layers < l' are a complete sub-FFT on the slice: lch_butterfly(l', base ^ g*m) -- the twiddle
+  C2P((base >> i) ^ 2b) with b = (g*m >> (i+1)) + b_local equals C2P(((base ^ g*m) >> i) ^ 2 b_local);
+* pointwise: local; inverse FFT mirrors the forward (local layers, then exchanged top layers);
+* decode: local columns -> a 128 x m-bit slice; all_gather + column interleave -> the n-bit
+  product array; inverse basis conversion (replicated); trim.
+
+Exchange volume per top layer: m * 16 B per rank (config 5, P = 8: 128 MiB).  The compute goes
+through a `backend` (GpuBackend here: the CUDA C-ABI; the gloo CPU tests plug in an oracle
+backend), so the partition / exchange logic is one piece of code tested on CPU and run on GPUs.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+@dataclass
+class ShardPlan:
+    a_bits: int
+    b_bits: int
+    n_bits: int
+    l: int
+    P: int
+    rank: int
+
+    @property
+    def n_p(self) -> int:
+        return 1 << self.l
+
+    @property
+    def m(self) -> int:
+        return self.n_p // self.P
+
+    @property
+    def col0(self) -> int:
+        return self.rank * self.m
+
+    @property
+    def lp(self) -> int:  # local layers
+        return self.l - (self.P.bit_length() - 1)
+
+    @property
+    def base(self) -> int:  # make_partition_spec<gf128>(l).base = e_{l+64} (encode.cpp:47)
+        return 1 << (self.l + 64)
+
+    def top_layers(self, inverse: bool):
+        r = range(self.lp, self.l)
+        return list(r) if inverse else list(reversed(r))
+
+    def partner(self, i: int) -> int:
+        return self.rank ^ (1 << (i - self.lp))
+
+    def side(self, i: int) -> int:
+        return (self.rank >> (i - self.lp)) & 1
+
+    def block(self, i: int) -> int:
+        return self.col0 >> (i + 1)
+
+
+def make_plan(a_bits: int, b_bits: int, P: int, rank: int) -> ShardPlan:
+    """plan_mul over GF(2^128) (polymul.cpp:187-219) plus the shard geometry."""
+    if P & (P - 1):
+        raise ValueError("sharded product: the number of ranks must be a power of two")
+    mx = max(a_bits, b_bits)
+    n = 1
+    while n < 2 * mx:
+        n <<= 1
+    n = max(n, 128)
+    l = n.bit_length() - 1 - 7
+    plan = ShardPlan(a_bits, b_bits, n, l, P, rank)
+    if plan.m < 1024:
+        raise ValueError(f"sharded product: {P} ranks need n_p >= {1024 * P} elements (n_p = {plan.n_p})")
+    return plan
+
+
+def polymul_sharded(a, a_bits: int, b, b_bits: int, backend, plan: ShardPlan | None = None):
+    """Product of two polynomials (backend arrays of packed words) over backend.world ranks;
+    every rank returns the full product words."""
+    P, rank = backend.world()
+    plan = plan or make_plan(a_bits, b_bits, P, rank)
+    evs = []
+    for x, bits in ((a, a_bits), (b, b_bits)):
+        poly = backend.convert_operand(x, bits, plan.n_bits)          # basis_cvt, replicated
+        ev = backend.encode_cols(poly, plan.l, plan.col0, plan.m)      # local columns
+        for i in plan.top_layers(inverse=False):                       # exchanged layers
+            theirs = backend.exchange(ev, plan.partner(i))
+            backend.pair(ev, theirs, backend.twiddle(i, plan.block(i), plan.base), plan.side(i), inverse=False)
+        backend.butterfly(ev, plan.lp, plan.base ^ plan.col0, inverse=False)
+        evs.append(ev)
+    c = backend.pointwise(evs[0], evs[1])
+    backend.butterfly(c, plan.lp, plan.base ^ plan.col0, inverse=True)
+    for i in plan.top_layers(inverse=True):
+        theirs = backend.exchange(c, plan.partner(i))
+        backend.pair(c, theirs, backend.twiddle(i, plan.block(i), plan.base), plan.side(i), inverse=True)
+    slice_ = backend.decode_cols(c, plan.m)                             # 128 rows x m bits
+    full = backend.gather_columns(slice_, plan)                         # 128 rows x n_p bits
+    return backend.finish(full, plan.n_bits, a_bits + b_bits - 1)       # i_basis_cvt + trim
+
+
+class GpuBackend:
+    """The CUDA C-ABI on torch CUDA tensors (int64 words), NCCL point-to-point exchanges."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        self.torch, self.dist, self.L, self.group = torch, dist, _lib, group
+
+    def world(self):
+        d = self.dist
+        if not d.is_initialized():
+            return 1, 0
+        return d.get_world_size(self.group), d.get_rank(self.group)
+
+    def _s(self):
+        return self.torch.cuda.current_stream().cuda_stream
+
+    def convert_operand(self, x, bits: int, n_bits: int):
+        t = self.torch
+        half_words = n_bits // 128
+        poly = t.zeros(half_words, dtype=t.int64, device=x.device)
+        w = (bits + 63) // 64
+        poly[:w] = x[:w]
+        if bits % 64:
+            poly[w - 1] &= (1 << (bits % 64)) - 1
+        count = 1
+        while count < bits:
+            count <<= 1
+        count = max(count, 64)
+        self.L.stage_dev("basis_cvt", poly, count, bits, stream=self._s())
+        return poly
+
+    def encode_cols(self, poly, l: int, col0: int, ncols: int):
+        ev = self.torch.empty(2 * ncols, dtype=self.torch.int64, device=poly.device)
+        self.L._check(self.L.lib().fpm_encode_cols_dev(poly.data_ptr(), l, col0, ncols, 64, ev.data_ptr(), self._s()))
+        return ev
+
+    def exchange(self, t, partner: int):
+        d = self.dist
+        buf = self.torch.empty_like(t)
+        reqs = d.batch_isend_irecv([d.P2POp(d.isend, t, partner, self.group), d.P2POp(d.irecv, buf, partner, self.group)])
+        for r in reqs:
+            r.wait()
+        return buf
+
+    def twiddle(self, i: int, b: int, base: int):
+        import ctypes as C
+
+        import numpy as np
+        out = np.zeros(2, np.uint64)
+        bb = np.array([base & (2**64 - 1), base >> 64], np.uint64)
+        self.L._check(self.L.lib().fpm_twiddle128(i, b, bb.ctypes.data_as(self.L._u64p), out.ctypes.data_as(self.L._u64p)))
+        return out
+
+    def pair(self, mine, theirs, w, side: int, inverse: bool):
+        self.L._check(self.L.lib().fpm_bfly_pair_dev(mine.data_ptr(), theirs.data_ptr(), mine.numel() // 2,
+                                                     w.ctypes.data_as(self.L._u64p), side, int(inverse), self._s()))
+
+    def butterfly(self, ev, l: int, base: int, inverse: bool):
+        import numpy as np
+        if l == 0:
+            return
+        bb = np.array([base & (2**64 - 1), base >> 64], np.uint64)
+        self.L._check(self.L.lib().fpm_lch_butterfly_dev(ev.data_ptr(), l, bb.ctypes.data_as(self.L._u64p),
+                                                         int(inverse), self._s()))
+
+    def pointwise(self, u, v):
+        self.L.stage_dev("pointwise", u, v, u, u.numel() // 2, stream=self._s())
+        return u
+
+    def decode_cols(self, ev, ncols: int):
+        out = self.torch.empty(128 * ncols // 64, dtype=self.torch.int64, device=ev.device)
+        self.L._check(self.L.lib().fpm_decode_cols_dev(ev.data_ptr(), ncols, out.data_ptr(), self._s()))
+        return out
+
+    def gather_columns(self, slice_, plan: ShardPlan):
+        t = self.torch
+        P = plan.P
+        parts = [t.empty_like(slice_) for _ in range(P)]
+        if P > 1:
+            self.dist.all_gather(parts, slice_, group=self.group)
+        else:
+            parts[0] = slice_
+        # each part: 128 rows x (m/64) words -> full: 128 rows x (n_p/64) words, columns interleaved by rank
+        stacked = t.stack([p.view(128, plan.m // 64) for p in parts], dim=1)  # 128 x P x m/64
+        return stacked.reshape(-1).contiguous()
+
+    def finish(self, full, n_bits: int, out_bits: int):
+        self.L.stage_dev("i_basis_cvt", full, n_bits, stream=self._s())
+        w = (out_bits + 63) // 64
+        out = full[:w].clone()
+        if out_bits % 64:
+            out[w - 1] &= (1 << (out_bits % 64)) - 1
+        return out
