@@ -93,16 +93,64 @@ __device__ __forceinline__ void m4r_build(uint4* __restrict__ tab, uint4* __rest
                                           int tid, int nthreads) {
   for (int k = tid; k < 128; k += nthreads) rows_scratch[k] = gf_mul_xk(w, (unsigned)k);
   __syncthreads();
-  for (int e = tid; e < kM4REntries; e += nthreads) {
-    const int c = e >> 4, v = e & 15;
+  // Flat slot order (consecutive threads -> consecutive 16 B slots): conflict-free STS.128; the
+  // 8 threads writing one entry's copies each recompute it (<= 3 uint4 XORs, cheaper than a
+  // 32-way bank conflict on strided stores).
+  for (int f = tid; f < kM4RUint4; f += nthreads) {
+    const int e = f >> 3, c = e >> 4, v = e & 15;
     uint4 acc = make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       if (v >> j & 1) acc = x4(acc, rows_scratch[4 * c + j]);
-#pragma unroll
-    for (int r = 0; r < kM4RCopies; ++r) tab[e * kM4RCopies + r] = acc;
+    tab[f] = acc;
   }
   __syncthreads();
+}
+
+// ---------------------------------------------------------------- rotated 8-bit M4R tables
+// 16 byte-chunk tables of w*(v << 8c), 256 entries each, 64 KiB total, no replication: entry
+// (c, v) lives at uint4 index (c >> 3) * 2048 + v * 8 + (c & 7), i.e. in 16-byte bank group c & 7.
+// Lane q (= lane & 7) of a quarter-warp visits chunks in the rotated order (k + q) & 7, so at
+// every lookup the 8 lanes of a quarter-warp hit 8 distinct bank groups: conflict-free LDS.128,
+// 16 lookups per product (2 clk/mul/SM of shared-memory bandwidth).
+constexpr int kM8Uint4 = 4096;
+
+// Build by exactly 256 threads: thread (c = tid & 15, s = tid >> 4) writes entries v = 16s..16s+15
+// of chunk c -- the high nibble s once from rows 8c+4..8c+7, the 16 low-nibble combinations
+// incrementally in registers; stores are conflict-free (a quarter-warp covers 8 bank groups).
+// rows_scratch: 144 uint4 of shared memory (row k padded to k + k/8).
+__device__ __forceinline__ void m8_build(uint4* __restrict__ tab, uint4* __restrict__ rows_scratch, uint4 w, int tid) {
+  if (tid < 128) rows_scratch[tid + (tid >> 3)] = gf_mul_xk(w, (unsigned)tid);
+  __syncthreads();
+  const int c = tid & 15, s = tid >> 4;
+  uint4 r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = rows_scratch[9 * c + j];
+  uint4 t[16];
+  t[0] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (s >> j & 1) t[0] = x4(t[0], r[4 + j]);
+#pragma unroll
+  for (int u = 1; u < 16; ++u) t[u] = x4(t[u & (u - 1)], r[(u & 1) ? 0 : (u & 2) ? 1 : (u & 4) ? 2 : 3]);
+  uint4* dst = tab + (c >> 3) * 2048 + 16 * s * 8 + (c & 7);
+#pragma unroll
+  for (int u = 0; u < 16; ++u) dst[u * 8] = t[u];
+  __syncthreads();
+}
+
+__device__ __forceinline__ uint4 m8_mul(const uint4* __restrict__ tab, uint4 x, int q) {
+  uint4 acc0 = make_uint4(0, 0, 0, 0), acc1 = make_uint4(0, 0, 0, 0);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int c = (k + q) & 7;                         // low chunks 0..7 live in x.x, x.y
+    const uint32_t sel = 0x4440u | (uint32_t)(c & 3);  // PRMT: byte (c&3) -> low byte, zeros above
+    const uint32_t lo = __byte_perm(c < 4 ? x.x : x.y, 0, sel);
+    const uint32_t hi = __byte_perm(c < 4 ? x.z : x.w, 0, sel);  // chunk 8 + c
+    acc0 = x4(acc0, tab[lo * 8 + c]);
+    acc1 = x4(acc1, tab[2048 + hi * 8 + c]);
+  }
+  return x4(acc0, acc1);
 }
 
 __device__ __forceinline__ uint4 m4r_mul(const uint4* __restrict__ tab, uint4 x, int copy) {

@@ -246,9 +246,9 @@ __global__ void __launch_bounds__(256) slab_kernel(uint32_t* __restrict__ data, 
 }
 
 // ------------------------------------------------------------------ bit-matrix transpose
-// src: R rows x C bits (pitch C/32 words) -> dst: C rows x R bits (pitch R/32 words); R, C >= 512.
-// 512 x 512-bit tiles: 64 B per row segment on both sides; 32x32 blocks via warp shuffles.
-constexpr int kTT = 512, kTTW = kTT / 32, kTTP = kTTW + 1;
+// src: R rows x C bits (pitch C/32 words) -> dst: C rows x R bits (pitch R/32 words); R, C >= 256.
+// 256 x 256-bit tiles (32 B row segments, sector-complete), 32x32 blocks via warp shuffles.
+constexpr int kTT = 256, kTTW = kTT / 32, kTTP = kTTW + 1;  // 18 KiB smem -> 8 CTAs/SM hide latency
 __global__ void __launch_bounds__(256) transpose_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
                                                         uint64_t R, uint64_t C) {
   extern __shared__ uint32_t tsm[];
@@ -330,7 +330,7 @@ void zeta(const uint32_t* src, uint64_t src_pitch, uint32_t* dst, uint64_t dst_p
 }
 
 void transpose(const uint32_t* src, uint32_t* dst, uint64_t R, uint64_t C, cudaStream_t s) {
-  transpose_kernel<<<grid_cap((R / kTT) * (C / kTT), 3), 256, 2 * kTT * kTTP * sizeof(uint32_t), s>>>(src, dst, R, C);
+  transpose_kernel<<<grid_cap((R / kTT) * (C / kTT), 8), 256, 2 * kTT * kTTP * sizeof(uint32_t), s>>>(src, dst, R, C);
   FPM_LAUNCH_CHECK();
 }
 

@@ -44,12 +44,12 @@ __device__ __forceinline__ uint4 twiddle(const TwiddleSrc& tw, unsigned l, unsig
 template <bool INV>
 __global__ void __launch_bounds__(256) fft_top_kernel(uint4* __restrict__ ev, unsigned l, unsigned i, int ppc, TwiddleSrc tw) {
   extern __shared__ uint4 tab[];            // kM4RUint4
-  __shared__ uint4 rows[128];
+  __shared__ uint4 rows[144];
   const uint64_t half = (uint64_t)1 << i;
   const uint64_t pair0 = (uint64_t)blockIdx.x * ppc;   // ppc <= 2^i: CTA pairs never straddle a block
   const uint64_t b = pair0 >> i;
   const uint4 w = twiddle(tw, l, i, b);
-  m4r_build(tab, rows, w, threadIdx.x, blockDim.x);
+  m8_build(tab, rows, w, threadIdx.x);
   const int copy = threadIdx.x & 7;
   uint4* base = ev + (b << (i + 1));
 #pragma unroll 4
@@ -57,11 +57,11 @@ __global__ void __launch_bounds__(256) fft_top_kernel(uint4* __restrict__ ev, un
     const uint64_t j = (pair0 & (half - 1)) + k;
     uint4 u0 = base[j], u1 = base[j + half];
     if (!INV) {
-      u0 = x4(u0, m4r_mul(tab, u1, copy));
+      u0 = x4(u0, m8_mul(tab, u1, copy));
       u1 = x4(u1, u0);
     } else {
       u1 = x4(u1, u0);
-      u0 = x4(u0, m4r_mul(tab, u1, copy));
+      u0 = x4(u0, m8_mul(tab, u1, copy));
     }
     base[j] = u0;
     base[j + half] = u1;
@@ -136,8 +136,8 @@ template <bool INV>
 __global__ void __launch_bounds__(256) fft_pair_kernel(uint4* __restrict__ mine, const uint4* __restrict__ theirs,
                                                        uint64_t n, uint4 w, int side, int ppc) {
   extern __shared__ uint4 tab[];
-  __shared__ uint4 rows[128];
-  m4r_build(tab, rows, w, threadIdx.x, blockDim.x);
+  __shared__ uint4 rows[144];
+  m8_build(tab, rows, w, threadIdx.x);
   const int copy = threadIdx.x & 7;
   const uint64_t k0 = (uint64_t)blockIdx.x * ppc;
   for (int k = threadIdx.x; k < ppc; k += blockDim.x) {
@@ -146,9 +146,9 @@ __global__ void __launch_bounds__(256) fft_pair_kernel(uint4* __restrict__ mine,
     const uint4 a = mine[e], b = theirs[e];
     uint4 r;
     if (!INV) {  // p0' = p0 + w p1 ; p1' = p1 + p0'
-      r = side == 0 ? x4(a, m4r_mul(tab, b, copy)) : xor3(a, b, m4r_mul(tab, a, copy));
+      r = side == 0 ? x4(a, m8_mul(tab, b, copy)) : xor3(a, b, m8_mul(tab, a, copy));
     } else {     // p1' = p1 + p0 ; p0' = p0 + w p1'
-      r = side == 0 ? x4(a, m4r_mul(tab, x4(a, b), copy)) : x4(a, b);
+      r = side == 0 ? x4(a, m8_mul(tab, x4(a, b), copy)) : x4(a, b);
     }
     mine[e] = r;
   }
