@@ -118,6 +118,46 @@ __device__ __forceinline__ void rowpasses(uint32_t (&m)[8], uint32_t* tile, int 
   }
 }
 
+// rowpasses over W adjacent 8-word columns at once (W * 32 B per row and barrier); tile is
+// 256 x kRowPitchW(W) words (one uint4 of padding keeps the 16 B stores conflict-free).
+template <int W>
+constexpr int kRowPitchW = 8 * W + 4;
+template <bool INV, int W>
+__device__ __forceinline__ void rowpasses_w(uint32_t (&m)[W][8], uint32_t* tile, int g, int d) {
+  const int tid = threadIdx.x;
+  const int n = kRowSchedN[g];
+  constexpr int P = kRowPitchW<W>;
+  for (int kk = 0; kk < n; ++kk) {
+    const int k = INV ? n - 1 - kk : kk;
+    const int S = kRowSchedS[g][k], D = kRowSchedD[g][k];
+    __syncthreads();
+    uint4* my4 = reinterpret_cast<uint4*>(tile + tid * P);
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      my4[2 * c] = make_uint4(m[c][0], m[c][1], m[c][2], m[c][3]);
+      my4[2 * c + 1] = make_uint4(m[c][4], m[c][5], m[c][6], m[c][7]);
+    }
+    __syncthreads();
+    const int q = d & (S - 1);
+    if (q >= S / 2 - D && q < S - D) {
+      const uint4* s1 = reinterpret_cast<const uint4*>(tile + (tid + D) * P);
+      const uint4* s2 = reinterpret_cast<const uint4*>(tile + (tid + 2 * D) * P);
+      const bool two = !INV && q + 2 * D < S;
+#pragma unroll
+      for (int c = 0; c < W; ++c) {
+        uint4 a = s1[2 * c], b = s1[2 * c + 1];
+        if (two) {
+          const uint4 e = s2[2 * c], f = s2[2 * c + 1];
+          a.x ^= e.x; a.y ^= e.y; a.z ^= e.z; a.w ^= e.w;
+          b.x ^= f.x; b.y ^= f.y; b.z ^= f.z; b.w ^= f.w;
+        }
+        m[c][0] ^= a.x; m[c][1] ^= a.y; m[c][2] ^= a.z; m[c][3] ^= a.w;
+        m[c][4] ^= b.x; m[c][5] ^= b.y; m[c][6] ^= b.z; m[c][7] ^= b.w;
+      }
+    }
+  }
+}
+
 // Converts every aligned 2^r-bit chunk of the tile (thread t's row in m), r in [1, 16].
 // tile: 256 x 8 words of shared memory; sc: 256 x kScPitch words of shared memory.
 // All 256 threads must call it (barriers inside when r > 8).

@@ -113,7 +113,7 @@ constexpr int kZW = 32;
 constexpr int kZP = 36;  // shared row pitch (16 B aligned, conflict-free for both mappings)
 __global__ void __launch_bounds__(256) zeta_kernel(const uint32_t* __restrict__ src, uint64_t src_pitch,
                                                    uint32_t* __restrict__ dst, uint64_t dst_pitch, uint64_t D,
-                                                   int b0, int nb, int skew, uint64_t src_row_words,
+                                                   int b0, int nb, uint64_t skew_unit, uint64_t src_row_words,
                                                    uint64_t windows) {
   extern __shared__ __align__(16) uint32_t sx[];  // 256 x kZP
   const int tid = threadIdx.x;
@@ -136,8 +136,8 @@ __global__ void __launch_bounds__(256) zeta_kernel(const uint32_t* __restrict__ 
       uint32_t v = 0;
       if (wi < windows) {
         const uint32_t* row = src + d * src_pitch;
-        if (skew) {
-          const int64_t pos = (int64_t)(wi * 32 * kZW) + 32 * c - (int64_t)d;
+        if (skew_unit) {
+          const int64_t pos = (int64_t)(wi * 32 * kZW) + 32 * c - (int64_t)(d * skew_unit);
           v = g_get32(row, src_row_words, pos);
         } else {
           v = __ldg(row + wi * kZW + c);
@@ -225,23 +225,107 @@ __global__ void overflow_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pit
 
 // ------------------------------------------------------------------ C_D for D <= 256: slab tiles
 // Tile = (256 / D) slabs x D rows x 8 words; rows of the array are t bits (kTWords words) apart.
+// Generalised: rows r = outer * (Dr * rstride) + d * rstride + inner, inner < rstride (row units of
+// kTWords words); a slab = (outer, inner, 8W-word column) -- conv over d at row stride rstride.
+constexpr int kSlabW = 4;  // 128 B of each row per slab: full lines, 4x fewer barriers
 template <bool INV>
-__global__ void __launch_bounds__(256) slab_kernel(uint32_t* __restrict__ data, int g) {
-  __shared__ __align__(16) uint32_t tile[kTileRows * 8];
+__global__ void __launch_bounds__(256) slab_kernel(uint32_t* __restrict__ data, int g, uint64_t rstride,
+                                                   uint64_t nslabs) {
+  extern __shared__ __align__(16) uint32_t tile[];  // 256 x kRowPitchW<kSlabW>
+  constexpr int W = kSlabW, cpr = kTWords / (8 * W);  // slabs per row
   const int tid = threadIdx.x;
   const int Dr = 1 << g;
   const int d = tid & (Dr - 1), slot = tid >> g;
   const int spc = 256 >> g;  // slabs per CTA
-  const uint64_t nslabs = kTWords / 8;
   for (uint64_t sb = (uint64_t)blockIdx.x * spc; sb < nslabs; sb += (uint64_t)gridDim.x * spc) {
     const uint64_t slab = sb + slot;
-    uint32_t* p = data + (uint64_t)d * kTWords + slab * 8;
-    const uint4 a = reinterpret_cast<const uint4*>(p)[0], b = reinterpret_cast<const uint4*>(p)[1];
-    uint32_t m[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    rowpasses<INV>(m, tile, g, d);
-    reinterpret_cast<uint4*>(p)[0] = make_uint4(m[0], m[1], m[2], m[3]);
-    reinterpret_cast<uint4*>(p)[1] = make_uint4(m[4], m[5], m[6], m[7]);
-    __syncthreads();
+    const uint64_t col = slab % cpr, rest = slab / cpr;
+    const uint64_t inner = rest % rstride, outer = rest / rstride;
+    const uint64_t row = outer * ((uint64_t)Dr * rstride) + (uint64_t)d * rstride + inner;
+    uint4* p = reinterpret_cast<uint4*>(data + row * kTWords + col * 8 * W);
+    const bool valid = slab < nslabs;
+    uint32_t m[W][8];
+#pragma unroll
+    for (int c = 0; c < W; ++c) {
+      uint4 a = make_uint4(0, 0, 0, 0), b = a;
+      if (valid) { a = p[2 * c]; b = p[2 * c + 1]; }
+      m[c][0] = a.x; m[c][1] = a.y; m[c][2] = a.z; m[c][3] = a.w;
+      m[c][4] = b.x; m[c][5] = b.y; m[c][6] = b.z; m[c][7] = b.w;
+    }
+    rowpasses_w<INV, W>(m, tile, g, d);
+    if (valid) {
+#pragma unroll
+      for (int c = 0; c < W; ++c) {
+        p[2 * c] = make_uint4(m[c][0], m[c][1], m[c][2], m[c][3]);
+        p[2 * c + 1] = make_uint4(m[c][4], m[c][5], m[c][6], m[c][7]);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ unit-level L1 carry + C_cols
+// Rows of t bits are units; row d = 256 * dh + v (digit dh, offset v).  After the unit-skewed zeta,
+// Gs[kh] holds units u = 0 .. 256+Dd-1 (pitch gs_pitch words).  Output unit (kh, v):
+//   g = Gs[kh][v+kh] ^ (v >= 1 ? Gs[kh][256+v-1+kh] : 0) ^ (kh >= 1 ? Gs[kh-1][256+v+kh-1] : 0)
+// followed by conv(Dd) over kh (C_cols, row passes in shared memory).  Item = (v, 8-word column).
+__global__ void __launch_bounds__(256) unit_carry_cols_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch,
+                                                              uint32_t* __restrict__ out, int gd, uint64_t items) {
+  extern __shared__ __align__(16) uint32_t tile[];  // 256 x kRowPitchW<kSlabW>
+  constexpr int W = kSlabW, cpr = kTWords / (8 * W);
+  const int tid = threadIdx.x;
+  const int kh = tid & ((1 << gd) - 1), slot = tid >> gd;
+  const int ipc = 256 >> gd;
+  const uint64_t Dd = (uint64_t)1 << gd;
+  for (uint64_t ib = (uint64_t)blockIdx.x * ipc; ib < items; ib += (uint64_t)gridDim.x * ipc) {
+    const uint64_t item = ib + slot;
+    const uint64_t v = item / cpr, col = item % cpr;
+    uint32_t m[W][8];
+#pragma unroll
+    for (int c = 0; c < W; ++c)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m[c][k] = 0;
+    if (item < items) {
+      auto add = [&](const uint32_t* p) {
+        const uint4* q = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+        for (int c = 0; c < W; ++c) {
+          const uint4 a = q[2 * c], b = q[2 * c + 1];
+          m[c][0] ^= a.x; m[c][1] ^= a.y; m[c][2] ^= a.z; m[c][3] ^= a.w;
+          m[c][4] ^= b.x; m[c][5] ^= b.y; m[c][6] ^= b.z; m[c][7] ^= b.w;
+        }
+      };
+      // units >= 256 + Dd of a skewed digit row are zero (not stored)
+      const uint32_t* rk = gs + (uint64_t)kh * gs_pitch + col * 8 * W;
+      add(rk + (v + kh) * kTWords);
+      if (v >= 1 && v - 1 + kh < Dd) add(rk + (256 + v - 1 + kh) * kTWords);
+      if (kh >= 1 && v + kh - 1 < Dd) add(rk - gs_pitch + (256 + v + kh - 1) * kTWords);
+    }
+    rowpasses_w<false, W>(m, tile, gd, kh);
+    if (item < items) {
+      uint4* o = reinterpret_cast<uint4*>(out + ((uint64_t)kh * 256 + v) * kTWords + col * 8 * W);
+#pragma unroll
+      for (int c = 0; c < W; ++c) {
+        o[2 * c] = make_uint4(m[c][0], m[c][1], m[c][2], m[c][3]);
+        o[2 * c + 1] = make_uint4(m[c][4], m[c][5], m[c][6], m[c][7]);
+      }
+    }
+  }
+}
+
+// Unit-level L1 inverse tail: F[256 dh + v] = Gs[dh][v+dh] ^ (dh >= 1 ? Gs[dh-1][256+v+dh-1] : 0).
+__global__ void unit_overflow_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch, uint32_t* __restrict__ out,
+                                     uint64_t Dd) {
+  const uint64_t q_per_row = kTWords / 4;
+  const uint64_t total = Dd * 256 * q_per_row;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t row = k / q_per_row, q = k % q_per_row;
+    const uint64_t dh = row >> 8, v = row & 255;
+    uint4 a = reinterpret_cast<const uint4*>(gs + dh * gs_pitch + (v + dh) * kTWords)[q];
+    if (dh && v + dh - 1 < Dd) {
+      const uint4 b = reinterpret_cast<const uint4*>(gs + (dh - 1) * gs_pitch + (256 + v + dh - 1) * kTWords)[q];
+      a.x ^= b.x; a.y ^= b.y; a.z ^= b.z; a.w ^= b.w;
+    }
+    reinterpret_cast<uint4*>(out)[k] = a;
   }
 }
 
@@ -319,13 +403,15 @@ void conv_rows(uint32_t* data, uint64_t nwords, int r, bool inv, cudaStream_t s)
   FPM_LAUNCH_CHECK();
 }
 
+// skew_unit: 0 = none; 1 = row d read at bit offset -d (bit-level L1); kT = row d read at offset
+// -d * 2^16 bits (unit-level L1 over whole rows, src_row_words = one row of units).
 void zeta(const uint32_t* src, uint64_t src_pitch, uint32_t* dst, uint64_t dst_pitch, uint64_t D, int b0, int nb,
-          bool skew, uint64_t windows, cudaStream_t s) {
+          uint64_t skew_unit, uint64_t windows, cudaStream_t s, uint64_t src_row_words = kTWords) {
   if (nb <= 0) return;
   const int wpc = 256 >> nb;
   const uint64_t items = (D >> nb) * ((windows + wpc - 1) / wpc);
   zeta_kernel<<<grid_cap(items, 4), 256, 256 * kZP * sizeof(uint32_t), s>>>(
-      src, src_pitch, dst, dst_pitch, D, b0, nb, skew ? 1 : 0, kTWords, windows);
+      src, src_pitch, dst, dst_pitch, D, b0, nb, skew_unit, src_row_words, windows);
   FPM_LAUNCH_CHECK();
 }
 
@@ -334,21 +420,57 @@ void transpose(const uint32_t* src, uint32_t* dst, uint64_t R, uint64_t C, cudaS
   FPM_LAUNCH_CHECK();
 }
 
+constexpr size_t kSlabSmem = 256 * kRowPitchW<kSlabW> * sizeof(uint32_t);
+// nslabs counts 8-word columns (callers' unit); the kernels take kSlabW of them per slab.
+void slab(uint32_t* w, int g, uint64_t rstride, uint64_t nslabs, bool inv, cudaStream_t s) {
+  static_assert(kSlabSmem <= 48 * 1024, "slab tile fits the default dynamic smem limit");
+  nslabs /= kSlabW;
+  const int spc = 256 >> g;
+  const uint64_t ctas = (nslabs + spc - 1) / spc;
+  if (inv) slab_kernel<true><<<grid_cap(ctas, 6), 256, kSlabSmem, s>>>(w, g, rstride, nslabs);
+  else slab_kernel<false><<<grid_cap(ctas, 6), 256, kSlabSmem, s>>>(w, g, rstride, nslabs);
+  FPM_LAUNCH_CHECK();
+}
+
+void unit_carry_cols(const uint32_t* gs, uint64_t gs_pitch, uint32_t* out, int gd, cudaStream_t s) {
+  const uint64_t items = 256 * (kTWords / (8 * kSlabW));
+  const int spc = 256 >> gd;
+  unit_carry_cols_kernel<<<grid_cap((items + spc - 1) / spc, 6), 256, kSlabSmem, s>>>(gs, gs_pitch, out, gd, items);
+  FPM_LAUNCH_CHECK();
+}
+
+void unit_overflow(const uint32_t* gs, uint64_t gs_pitch, uint32_t* out, uint64_t Dd, cudaStream_t s) {
+  const uint64_t total = Dd * 256 * (kTWords / 4);
+  unit_overflow_kernel<<<grid_cap((total + 255) / 256, 16), 256, 0, s>>>(gs, gs_pitch, out, Dd);
+  FPM_LAUNCH_CHECK();
+}
+
 // conv over the row index (D rows of t bits), forward or inverse.
 void conv_cols(uint32_t* w, uint32_t* scratch, int lgD, bool inv, cudaStream_t s) {
   if (lgD <= 1) return;  // conv(2) is the identity (no passes)
   if (lgD <= 8) {
-    const int spc = 256 >> lgD;
-    const uint64_t ctas = (kTWords / 8 + spc - 1) / spc;
-    if (inv) slab_kernel<true><<<grid_cap(ctas, 8), 256, 0, s>>>(w, lgD);
-    else slab_kernel<false><<<grid_cap(ctas, 8), 256, 0, s>>>(w, lgD);
-    FPM_LAUNCH_CHECK();
+    slab(w, lgD, 1, kTWords / 8, inv, s);
     return;
   }
-  const uint64_t D = (uint64_t)1 << lgD;
-  transpose(w, scratch, D, kT, s);           // (D x t) -> (t x D)
-  conv_rows(scratch, kT * D / 32, lgD, inv, s);
-  transpose(scratch, w, kT, D, s);           // back
+  // D > 256 rows: conv(2^lgD) over the row index with whole rows as units, by the same recursion
+  // one level up: digits of 256 rows, Dd = D / 256 digits.
+  //   forward  L1(256, Dd) over units (row-skew + zeta, then carry fused with C_cols), C_rows
+  //   inverse  C_rows^-1, C_cols^-1, L1^-1 (row-skew + zeta, then overflow)
+  const int gd = lgD - 8;
+  const uint64_t Dd = (uint64_t)1 << gd;
+  const uint64_t su = 256 + std::max<uint64_t>(Dd, 1);           // skewed units per digit row
+  const uint64_t sk_pitch = su * kTWords;                         // words
+  const uint64_t windows = sk_pitch / kZW;
+  if (!inv) {
+    zeta(w, 256 * (uint64_t)kTWords, scratch, sk_pitch, Dd, 0, gd, kT, windows, s, 256 * (uint64_t)kTWords);
+    unit_carry_cols(scratch, sk_pitch, w, gd, s);
+    slab(w, 8, 1, (Dd * 256 / 256) * (kTWords / 8), false, s);   // C_rows: conv(256) over consecutive rows
+  } else {
+    slab(w, 8, 1, (Dd * 256 / 256) * (kTWords / 8), true, s);
+    slab(w, gd, 256, 256 * (kTWords / 8), true, s);               // C_cols^-1: conv(Dd) at row stride 256
+    zeta(w, 256 * (uint64_t)kTWords, scratch, sk_pitch, Dd, 0, gd, kT, windows, s, 256 * (uint64_t)kTWords);
+    unit_overflow(scratch, sk_pitch, w, Dd, s);
+  }
 }
 
 // conv(2^K) for 17 <= K <= 32 on w (2^K bits).  scratch >= 2^(K-16) * (2^16 + max(2^(K-16), 1024)) bits.
@@ -360,16 +482,16 @@ void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s) {
   const uint64_t windows = wsk / kZW;
   const int nb_lo = std::min(lgD, 8), nb_hi = lgD - nb_lo;
   if (!inv) {
-    zeta(w, kTWords, scratch, wsk, D, 0, nb_lo, true, windows, s);
-    zeta(scratch, wsk, scratch, wsk, D, 8, nb_hi, false, windows, s);
+    zeta(w, kTWords, scratch, wsk, D, 0, nb_lo, 1, windows, s);
+    zeta(scratch, wsk, scratch, wsk, D, 8, nb_hi, 0, windows, s);
     carry_rows_kernel<<<grid_cap(D, 4), 256, kTileSmem, s>>>(scratch, wsk, w, D);
     FPM_LAUNCH_CHECK();
     conv_cols(w, scratch, lgD, false, s);
   } else {
     conv_rows(w, D * kTWords, kTLog2, true, s);
     conv_cols(w, scratch, lgD, true, s);
-    zeta(w, kTWords, scratch, wsk, D, 0, nb_lo, true, windows, s);
-    zeta(scratch, wsk, scratch, wsk, D, 8, nb_hi, false, windows, s);
+    zeta(w, kTWords, scratch, wsk, D, 0, nb_lo, 1, windows, s);
+    zeta(scratch, wsk, scratch, wsk, D, 8, nb_hi, 0, windows, s);
     overflow_kernel<<<grid_cap(D * kTWords / 256, 32), 256, 0, s>>>(scratch, wsk, w, D);
     FPM_LAUNCH_CHECK();
   }

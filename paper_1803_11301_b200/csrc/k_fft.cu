@@ -68,6 +68,86 @@ __global__ void __launch_bounds__(256) fft_top_kernel(uint4* __restrict__ ev, un
   }
 }
 
+// ------------------------------------------------------------------ top layers, two per pass
+// Layers i+1 and i in one HBM round trip.  A block of 2^(i+2) elements splits into quarters
+// q0..q3 of h = 2^i; layer i+1 pairs (q0,q2), (q1,q3) with w(i+1, B); layer i pairs (q0,q1) with
+// w(i, 2B) and (q2,q3) with w(i, 2B+1).  The three M8 tables (192 KiB) are built by three groups of
+// 256 threads; one 768-thread CTA per SM then streams its quads.
+constexpr int kTop4Threads = 768;
+constexpr size_t kTop4Smem = (3 * (size_t)kM8Uint4 + 3 * 144) * sizeof(uint4);
+
+template <bool INV>
+__global__ void __launch_bounds__(kTop4Threads, 1) fft_top4_kernel(uint4* __restrict__ ev, unsigned l, unsigned i,
+                                                                   int qpc, TwiddleSrc tw) {
+  extern __shared__ uint4 sm4[];
+  uint4* t1 = sm4;                   // w(i+1, B)
+  uint4* t0a = sm4 + kM8Uint4;       // w(i, 2B)
+  uint4* t0b = sm4 + 2 * kM8Uint4;   // w(i, 2B+1)
+  uint4* rows = sm4 + 3 * kM8Uint4;  // 3 x 144
+  const uint64_t h = (uint64_t)1 << i;
+  const uint64_t quad0 = (uint64_t)blockIdx.x * qpc;  // qpc <= h: a CTA never straddles a block
+  const uint64_t B = quad0 >> i;
+  const int tid = threadIdx.x, grp = tid >> 8, lt = tid & 255;
+  {
+    uint4 w = make_uint4(0, 0, 0, 0);
+    if (grp == 0) w = twiddle(tw, l, i + 1, B);
+    else if (grp == 1) w = twiddle(tw, l, i, 2 * B);
+    else if (grp == 2) w = twiddle(tw, l, i, 2 * B + 1);
+    uint4* tab = sm4 + grp * kM8Uint4;
+    uint4* rs = rows + grp * 144;
+    if (grp < 3 && lt < 128) rs[lt + (lt >> 3)] = gf_mul_xk(w, (unsigned)lt);
+    __syncthreads();
+    if (grp < 3) {
+      const int c = lt & 15, sv = lt >> 4;
+      uint4 r[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = rs[9 * c + j];
+      uint4 t[16];
+      t[0] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (sv >> j & 1) t[0] = x4(t[0], r[4 + j]);
+#pragma unroll
+      for (int u = 1; u < 16; ++u) t[u] = x4(t[u & (u - 1)], r[(u & 1) ? 0 : (u & 2) ? 1 : (u & 4) ? 2 : 3]);
+      uint4* dst = tab + (c >> 3) * 2048 + 16 * sv * 8 + (c & 7);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) dst[u * 8] = t[u];
+    }
+    __syncthreads();
+  }
+  const int q = tid & 7;
+  uint4* base = ev + (B << (i + 2));
+  const uint64_t j0 = quad0 & (h - 1);
+#pragma unroll 1
+  for (int k = tid; k < qpc; k += kTop4Threads) {
+    uint4* p = base + j0 + k;
+    uint4 a0 = p[0], a1 = p[h], a2 = p[2 * h], a3 = p[3 * h];
+    if (!INV) {
+      a0 = x4(a0, m8_mul(t1, a2, q));
+      a1 = x4(a1, m8_mul(t1, a3, q));
+      a2 = x4(a2, a0);
+      a3 = x4(a3, a1);
+      a0 = x4(a0, m8_mul(t0a, a1, q));
+      a2 = x4(a2, m8_mul(t0b, a3, q));
+      a1 = x4(a1, a0);
+      a3 = x4(a3, a2);
+    } else {
+      a1 = x4(a1, a0);
+      a3 = x4(a3, a2);
+      a0 = x4(a0, m8_mul(t0a, a1, q));
+      a2 = x4(a2, m8_mul(t0b, a3, q));
+      a2 = x4(a2, a0);
+      a3 = x4(a3, a1);
+      a0 = x4(a0, m8_mul(t1, a2, q));
+      a1 = x4(a1, m8_mul(t1, a3, q));
+    }
+    p[0] = a0;
+    p[h] = a1;
+    p[2 * h] = a2;
+    p[3 * h] = a3;
+  }
+}
+
 // ------------------------------------------------------------------ tile layers (i < T)
 template <bool INV>
 __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, unsigned l, uint64_t tile_idx,
@@ -197,16 +277,41 @@ void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const
   static bool attr = false;
   if (!attr) { set_smem(fft_top_kernel<false>, smem); set_smem(fft_top_kernel<true>, smem); attr = true; }
   // Pairs per CTA: 4096 amortise the 64 KiB table build; smaller layers still fill 2 CTAs/SM.
+  static bool attr4 = false;
+  if (!attr4) {
+    set_smem(fft_top4_kernel<false>, kTop4Smem);
+    set_smem(fft_top4_kernel<true>, kTop4Smem);
+    attr4 = true;
+  }
   const uint64_t pairs = ((uint64_t)1 << l) / 2;
   uint64_t ppc = 4096;
   while (ppc > 256 && pairs / ppc < (uint64_t)sms() * 2) ppc /= 2;
   const uint64_t ctas = pairs / ppc;
   if (T < 8 || ctas == 0) throw Error(kInvalid, "butterfly_top: layer too small for the M4R layer kernel");
-  for (unsigned k = 0; k < l - T; ++k) {
-    const unsigned i = inverse ? T + k : l - 1 - k;
+  auto radix2 = [&](unsigned i) {
     if (!inverse) fft_top_kernel<false><<<(unsigned)ctas, 256, smem, s>>>(ev, l, i, (int)ppc, tw);
     else fft_top_kernel<true><<<(unsigned)ctas, 256, smem, s>>>(ev, l, i, (int)ppc, tw);
     FPM_LAUNCH_CHECK();
+  };
+  // layer pairs (i+1, i) from the top down (forward) / bottom up (inverse); an odd count leaves
+  // the lowest top layer T to the one-layer kernel.
+  const uint64_t quads = ((uint64_t)1 << l) / 4;
+  uint64_t qpc = 8192;
+  while (qpc > 1024 && quads / qpc < (uint64_t)sms() * 4) qpc /= 2;
+  auto radix4 = [&](unsigned i) {
+    const unsigned q = (unsigned)std::min<uint64_t>(qpc, (uint64_t)1 << i);
+    if (!inverse) fft_top4_kernel<false><<<(unsigned)(quads / q), kTop4Threads, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
+    else fft_top4_kernel<true><<<(unsigned)(quads / q), kTop4Threads, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
+    FPM_LAUNCH_CHECK();
+  };
+  const unsigned n = l - T;
+  const bool odd = n & 1;
+  if (!inverse) {
+    for (unsigned k = 0; k + 1 < n; k += 2) radix4(l - 2 - k);
+    if (odd) radix2(T);
+  } else {
+    if (odd) radix2(T);
+    for (unsigned i = T + (odd ? 1 : 0); i + 1 < l; i += 2) radix4(i);
   }
 }
 
