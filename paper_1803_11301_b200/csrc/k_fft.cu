@@ -18,6 +18,9 @@
 //    a (subsystem 3, kernels_impl.hpp:116-123), and inverse layers [0,T) in one tile pass.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "fpm_internal.h"
 #include "gf128.cuh"
 
@@ -254,7 +257,18 @@ void set_smem(K kernel, size_t bytes) {
 
 }  // namespace
 
-unsigned fft_tile_log2(unsigned l) { return l < (unsigned)kTileMax ? l : (unsigned)kTileMax; }
+// Tile depth: layers below T run in shared-memory tiles (generic multiplies), layers >= T in
+// radix-4 M8-table passes (~3x cheaper per product, measured).  T = 10 for large transforms (16 KiB
+// tiles; B200 cfg5 sweep T = 8..12: 83.4 / 80.0 / 79.5 / 80.2 / 81.0 ms); T = 8 below
+// 2^18 elements so the tile pass still has >= 2^10 tiles to spread over the SMs.
+unsigned fft_tile_log2(unsigned l) {
+  static const int knob = [] {
+    const char* e = std::getenv("FPM_TILE_LOG2");  // tuning override (8..12)
+    return e ? std::max(8, std::min(kTileMax, std::atoi(e))) : 0;
+  }();
+  const unsigned cap = knob ? (unsigned)knob : (l >= 18 ? 10u : 8u);
+  return l < cap ? l : cap;
+}
 
 TwiddleSrc make_twiddle_src(int device, unsigned l, U128 base) {
   if (l > (unsigned)kMaxLayers) throw Error(kInvalid, "butterfly: too many layers");
@@ -289,8 +303,9 @@ void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const
   const uint64_t ctas = pairs / ppc;
   if (T < 8 || ctas == 0) throw Error(kInvalid, "butterfly_top: layer too small for the M4R layer kernel");
   auto radix2 = [&](unsigned i) {
-    if (!inverse) fft_top_kernel<false><<<(unsigned)ctas, 256, smem, s>>>(ev, l, i, (int)ppc, tw);
-    else fft_top_kernel<true><<<(unsigned)ctas, 256, smem, s>>>(ev, l, i, (int)ppc, tw);
+    const uint64_t p = std::min<uint64_t>(ppc, (uint64_t)1 << i);  // a CTA stays inside one block
+    if (!inverse) fft_top_kernel<false><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, l, i, (int)p, tw);
+    else fft_top_kernel<true><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, l, i, (int)p, tw);
     FPM_LAUNCH_CHECK();
   };
   // layer pairs (i+1, i) from the top down (forward) / bottom up (inverse); an odd count leaves

@@ -57,13 +57,36 @@ def test_encode_decode(gpu, checker, l):
     assert np.array_equal(gpu.decode(ev, l), a)
 
 
-@pytest.mark.parametrize("l", [1, 2, 4, 7, 10, 12, 13, 14, 16])
+@pytest.mark.parametrize("l", [1, 2, 4, 7, 10, 12, 13, 14, 16, 17, 18, 19])
 def test_butterfly(gpu, checker, l):
     rng = np.random.default_rng(200 + l)
     ev = rnd_words(rng, 128 << l)
     f = gpu.lch_butterfly(ev, l)
     assert np.array_equal(f, checker.butterfly(ev, l)), "forward"
     assert np.array_equal(gpu.i_lch_butterfly(f, l), ev), "inverse"
+
+
+@pytest.mark.parametrize("tile", [9, 11, 12])
+def test_butterfly_tile_depths(tile):
+    """Every shared-memory tile depth (odd ones leave a single radix-2 top layer) gives the same
+    transform: run the product in a child process with the FPM_TILE_LOG2 override."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, oracle, paper_1803_11301_b200 as g\n"
+        "P = oracle.port()\n"
+        "for l in (15, 18):\n"
+        "    rng = np.random.default_rng(l)\n"
+        "    ev = rng.integers(0, 2**63, size=2 << l, dtype=np.uint64)\n"
+        "    f = g.lch_butterfly(ev, l)\n"
+        "    assert np.array_equal(f, P.butterfly(128, ev, l, False)), l\n"
+        "    assert np.array_equal(g.i_lch_butterfly(f, l), ev), l\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, FPM_TILE_LOG2=str(tile)))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
 SHAPES = [(1, 1), (1, 5), (63, 64), (64, 64), (100, 3000), (4095, 4096), (5000, 3000), (1 << 12, 1 << 12),
