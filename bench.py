@@ -107,27 +107,42 @@ def rand_words(torch, words, seed, device):
     return lo | (hi << 32)
 
 
-def algorithmic(stage: str, bits: int):
-    """SURVEY.md 8(d) per-unit algorithmic work for one product with equal operands of `bits` bits.
-    Returns (kind, amount): bytes for HBM-bound stages, 32-bit integer ops for the butterflies."""
+def stage_traffic(stage: str, bits: int):
+    """DRAM bytes (read + write) per launch of the stage's kernel from the committed ncu capture
+    (profiles/traffic.json, written by tools/ncu_traffic.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        return t.get(f"{bits}:{stage}")
+    except (OSError, ValueError):
+        return None
+
+
+def algorithmic(stage: str, bits: int, T: int):
+    """SURVEY.md 8(d) per-unit algorithmic work of one product with equal operands of `bits` bits,
+    per pipeline stage (each stage is one kernel class).
+    Returns (bytes, int32 ops): HBM bytes a perfect kernel moves, and 552 ops per GF(2^128)
+    product (the schoolbook convention of 8(d)); the roofline time is the slower of the two."""
     n = 2 * bits
-    n_p = n // 128
+    n_p = n // 128                      # field elements per operand transform
     l = n_p.bit_length() - 1
-    V = 16 * n_p
-    if stage == "basiscvt":   # one fused sweep per operand: N/8 read + N/8 write, two operands
-        return "hbm", 2 * (bits // 8) * 2
-    if stage == "ibasiscvt":  # one sweep over the n-bit product
-        return "hbm", 2 * (n // 8)
-    if stage == "encode":     # N/8 read + V write per operand
-        return "hbm", 2 * (bits // 8 + V)
+    V = 16 * n_p                        # bytes of one evaluation vector
+    if stage == "basiscvt":             # one read + write sweep per operand
+        return 2 * 2 * (bits // 8), 0
+    if stage == "ibasiscvt":
+        return 2 * (n // 8), 0
+    if stage == "encode":
+        return 2 * (bits // 8 + V), 0
     if stage == "decode":
-        return "hbm", V + n // 8
-    if stage == "butterfly":  # 552 ops per butterfly, l layers x n_p/2 per operand
-        return "int", 2 * 552 * l * n_p // 2
+        return V + n // 8, 0
+    if stage == "butterfly":            # radix-4 passes over layers [T, l) of both operands + tile pass of a
+        passes = (l - T + 1) // 2
+        return 2 * passes * 2 * V + 2 * V, 552 * ((l - T) * n_p + T * n_p // 2)
+    if stage == "pointwise":            # fft_tile_fused_kernel: b's tile layers, a*b, inverse tile layers
+        return 3 * V, 552 * (T * n_p + n_p)
     if stage == "ibutterfly":
-        return "int", 552 * l * n_p // 2
-    if stage == "pointwise":
-        return "int", 544 * n_p
+        passes = (l - T + 1) // 2
+        return passes * 2 * V, 552 * (l - T) * n_p // 2
     raise KeyError(stage)
 
 
@@ -306,21 +321,35 @@ def main():
     torch.cuda.synchronize()
     stages = dict(zip(pkg.STAGE_NAMES, st))
     dom = max(stages, key=stages.get)
-    kind, amount = algorithmic(dom, bits)
+    l_fft = (2 * bits // 128).bit_length() - 1
+    T = pkg.fft_tile_log2(l_fft)
+    nbytes, ops = algorithmic(dom, bits, T)
     clocks = clk.summary()
     hbm, peak_kind = peaks()
-    if kind == "hbm":
-        achieved = amount / stages[dom] / 1e9
-        roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": None, "peak_source": peak_kind}
-    else:
-        mhz = clocks.get("sm_mhz") or 1965.0
-        peak_tops = LOP3_OPS_PER_CLK_SM * 148 * mhz * 1e6 / 1e12
-        achieved = amount / stages[dom] / 1e12
-        roof = {"bound": "int", "kernel": dom, "achieved": round(achieved, 2), "peak": round(peak_tops, 2),
-                "unit": "Tops/s", "frac": round(achieved / peak_tops, 4), "traffic": None,
+    mhz = clocks.get("sm_mhz") or 1965.0
+    peak_tops = LOP3_OPS_PER_CLK_SM * 148 * mhz * 1e6 / 1e12
+    t_hbm = nbytes / (hbm * 1e9)
+    t_int = ops / (peak_tops * 1e12)
+    if t_int >= t_hbm:
+        achieved = ops / stages[dom] / 1e12
+        roof = {"bound": "int", "achieved": round(achieved, 2), "peak": round(peak_tops, 2), "unit": "Tops/s",
+                "frac": round(achieved / peak_tops, 4),
                 "peak_source": "LOP3 microbenchmark 63 ops/clk/SM at the sampled SM clock",
-                "op_convention": "SURVEY 8(d): 552 int32 ops per butterfly (schoolbook GF(2^128) multiply)"}
+                "op_convention": "SURVEY 8(d): 552 int32 ops per GF(2^128) product (schoolbook)"}
+    else:
+        achieved = nbytes / stages[dom] / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "peak_source": peak_kind}
+    roof["kernel"] = {"pointwise": "fft_tile_fused_kernel", "butterfly": "fft_top4_kernel + fft_tile_kernel",
+                      "ibutterfly": "fft_top4_kernel<inverse>"}.get(dom, dom)
+    roof["stage"] = dom
+    roof["traffic"] = stage_traffic(dom, bits)
+    # whole step against the sum of per-stage roofline times (slower of bytes and ops per stage)
+    t_roof = 0.0
+    for k in stages:
+        nb, op = algorithmic(k, bits, T)
+        t_roof += max(nb / (hbm * 1e9), op / (peak_tops * 1e12))
+    roof["step_frac"] = round(t_roof / (sum(stages.values())), 4)
     roof["stage_ms"] = {k: round(v * 1e3, 3) for k, v in stages.items()}
 
     line = {

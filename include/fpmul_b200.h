@@ -62,6 +62,11 @@ const char* fpm_version(void);
 /* Number of CUDA devices visible (0 when none); never fails. */
 int fpm_device_count(void);
 
+/* Schedule introspection (no reference counterpart): the butterfly layers [0, T) of a 2^l-element
+ * transform run in shared-memory tiles (one launch per operand pass), layers [T, l) in radix-4
+ * passes.  Used by bench.py to attribute work to kernels; never fails. */
+unsigned fpm_fft_tile_log2(unsigned l);
+
 /* plan_mul (proj/src/polymul.cpp:187-219).  field: FPM_FIELD_*.  The GPU pipeline always runs
  * GF(2^128); plan_mul still reports the reference's choice for the requested field. */
 fpm_status fpm_plan_mul(size_t a_bits, size_t b_bits, int field, fpm_plan* out);

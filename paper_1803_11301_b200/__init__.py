@@ -33,6 +33,7 @@ from ._lib import (  # noqa: F401
     launch_count,
     lch_butterfly,
     lib,
+    fft_tile_log2,
     plan_mul,
     pointwise_mul,
     stage_dev,

@@ -46,6 +46,8 @@ def lib():
         sz = C.c_size_t
         L.fpm_last_error.restype = C.c_char_p
         L.fpm_version.restype = C.c_char_p
+        L.fpm_fft_tile_log2.restype = C.c_uint
+        L.fpm_fft_tile_log2.argtypes = [C.c_uint]
         L.fpm_launch_count.restype = C.c_uint64
         L.fpm_launch_count.argtypes = [C.c_int]
         L.fpm_plan_mul.argtypes = [sz, sz, C.c_int, C.POINTER(_Plan)]
@@ -105,6 +107,11 @@ def device_count() -> int:
 
 def launch_count(reset: bool = False) -> int:
     return int(lib().fpm_launch_count(int(reset)))
+
+
+def fft_tile_log2(l: int) -> int:
+    """Butterfly layers below this run in shared-memory tiles, the rest in radix-4 passes."""
+    return int(lib().fpm_fft_tile_log2(l))
 
 
 def plan_mul(a_bits: int, b_bits: int, field: int = FIELD_AUTO) -> dict:

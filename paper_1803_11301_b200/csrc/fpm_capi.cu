@@ -69,9 +69,10 @@ __global__ void load_operand_kernel(uint64_t* __restrict__ dst, uint64_t dst_wor
   }
 }
 
-__global__ void store_product_kernel(uint64_t* __restrict__ dst, const uint64_t* __restrict__ src, uint64_t out_bits) {
+__global__ void store_product_kernel(uint64_t* __restrict__ dst, const uint64_t* __restrict__ src, uint64_t out_bits,
+                                     uint64_t k0, uint64_t k1) {
   const uint64_t words = (out_bits + 63) / 64;
-  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < words; k += (uint64_t)gridDim.x * blockDim.x) {
+  for (uint64_t k = k0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < k1; k += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t v = src[k];
     if (k == words - 1 && (out_bits & 63)) v &= (((uint64_t)1) << (out_bits & 63)) - 1;
     dst[k] = v;
@@ -155,8 +156,18 @@ struct DevBuf {
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+// Host-buffer pipelining for fpm_polymul: the compute stream waits for operand k's upload only
+// right before operand k is first read (operand b's copy overlaps operand a's transforms), and
+// product words are copied to h_out on the d2h stream as soon as the inverse basis conversion has
+// finished them (the upper half overlaps the lower half's conversion at 2^33 bits).
+struct HostIO {
+  cudaEvent_t ready[2] = {nullptr, nullptr};
+  uint64_t* h_out = nullptr;
+  cudaStream_t d2h = nullptr;
+};
+
 void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_t b_bits, uint64_t* d_c,
-                    int field, cudaStream_t s, double* stages) {
+                    int field, cudaStream_t s, double* stages, const HostIO* io = nullptr) {
   if (!a_bits || !b_bits) return;
   if (field == FPM_FIELD_GF64)
     throw Error(kInvalid, "fp_polymul: the GF(2^64) pipeline is not built on the GPU (use GF(2^128) or auto)");
@@ -164,10 +175,26 @@ void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, siz
   const fpm_plan p = plan_mul(a_bits, b_bits, FPM_FIELD_GF128);
   const size_t out_bits = a_bits + b_bits - 1;
   StageClock clk(s, stages);
+  const uint64_t out_words = (out_bits + 63) / 64;
+  auto wait_operand = [&](int k) {
+    if (io && io->ready[k]) FPM_CUDA(cudaStreamWaitEvent(s, io->ready[k], 0));
+  };
+  auto copy_out = [&](uint64_t w0, uint64_t w1) {  // 64-bit words of d_c, final on s
+    if (!io || !io->h_out || w0 >= w1) return;
+    cudaEvent_t e;
+    FPM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    FPM_CUDA(cudaEventRecord(e, s));
+    FPM_CUDA(cudaStreamWaitEvent(io->d2h, e, 0));
+    FPM_CUDA(cudaEventDestroy(e));  // released once the wait is satisfied
+    FPM_CUDA(cudaMemcpyAsync(io->h_out + w0, d_c + w0, (w1 - w0) * 8, cudaMemcpyDeviceToHost, io->d2h));
+  };
   if (p.l <= 10) {  // whole product in one CTA
+    wait_operand(0);
+    wait_operand(1);
     clk.mark(kStPointwise);
     polymul_batch_device(d_a, a_bits, 0, d_b, b_bits, 0, d_c, 0, 1, s);
     clk.finish();
+    copy_out(0, out_words);
     return;
   }
   const unsigned l = p.l, T = fft_tile_log2(l);
@@ -180,6 +207,7 @@ void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, siz
   const size_t xbits[2] = {a_bits, b_bits};
   uint4* es[2] = {EA.as<uint4>(), EB.as<uint4>()};
   for (int k = 0; k < 2; ++k) {
+    wait_operand(k);
     clk.mark(kStBasis);
     const uint64_t half_words = n / 128;  // n/2 bits in uint64 words
     load_operand_kernel<<<grid_1d(half_words), 256, 0, s>>>(P.as<uint64_t>(), half_words, xs[k], xbits[k]);
@@ -200,9 +228,17 @@ void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, siz
   clk.mark(kStDecode);
   decode_device(EB.as<uint4>(), l, P.as<uint32_t>(), s);
   clk.mark(kStIBasis);
-  basis_cvt_device(P.as<uint32_t>(), n, n, true, s);
-  store_product_kernel<<<grid_1d((out_bits + 63) / 64), 256, 0, s>>>(d_c, P.as<uint64_t>(), out_bits);
-  FPM_LAUNCH_CHECK();
+  // Each finished range of the product is trimmed into d_c (and copied out) right away.
+  const FinalFn on_final = [&](uint64_t w0, uint64_t w1) {  // 32-bit word range of P
+    // 64-bit word q holds 32-bit words 2q, 2q+1: rounding both ends up keeps the reported ranges a
+    // partition and only ever copies a word once both of its halves are final.
+    const uint64_t q0 = std::min<uint64_t>((w0 + 1) / 2, out_words), q1 = std::min<uint64_t>((w1 + 1) / 2, out_words);
+    if (q0 >= q1) return;
+    store_product_kernel<<<grid_1d(q1 - q0), 256, 0, s>>>(d_c, P.as<uint64_t>(), out_bits, q0, q1);
+    FPM_LAUNCH_CHECK();
+    copy_out(q0, q1);
+  };
+  basis_cvt_device(P.as<uint32_t>(), n, n, true, s, &on_final);
   clk.finish();
 }
 
@@ -223,6 +259,22 @@ cudaStream_t host_stream(int dev) {
   if (!streams[dev]) FPM_CUDA(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
   return streams[dev];
 }
+
+cudaStream_t copy_stream(int dev, int which) {
+  static std::mutex mu;
+  static cudaStream_t streams[64][2] = {};
+  std::lock_guard<std::mutex> lock(mu);
+  if (!streams[dev][which]) FPM_CUDA(cudaStreamCreateWithFlags(&streams[dev][which], cudaStreamNonBlocking));
+  return streams[dev][which];
+}
+
+struct Ev {
+  cudaEvent_t e = nullptr;
+  Ev() { FPM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+  ~Ev() { if (e) cudaEventDestroy(e); }
+  Ev(const Ev&) = delete;
+  Ev& operator=(const Ev&) = delete;
+};
 
 }  // namespace
 
@@ -306,6 +358,8 @@ extern "C" {
 
 const char* fpm_last_error(void) { return g_err.c_str(); }
 const char* fpm_version(void) { return "fpmul_b200 0.1 (sm_100a)"; }
+
+unsigned fpm_fft_tile_log2(unsigned l) { return fpm::fft_tile_log2(l); }
 int fpm_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
@@ -349,11 +403,24 @@ fpm_status fpm_polymul(const uint64_t* a, size_t a_bits, const uint64_t* b, size
     DeviceGuard g(device);
     cudaStream_t s = host_stream(device);
     const size_t wa = (a_bits + 63) / 64, wb = (b_bits + 63) / 64, wc = (a_bits + b_bits - 1 + 63) / 64;
+    cudaStream_t h2d = copy_stream(device, 0), d2h = copy_stream(device, 1);
     DevBuf A(wa * 8, s), B(wb * 8, s), C(wc * 8, s);
-    FPM_CUDA(cudaMemcpyAsync(A.p, a, wa * 8, cudaMemcpyHostToDevice, s));
-    FPM_CUDA(cudaMemcpyAsync(B.p, b, wb * 8, cudaMemcpyHostToDevice, s));
-    polymul_device(A.as<uint64_t>(), a_bits, B.as<uint64_t>(), b_bits, C.as<uint64_t>(), field, s, stage_seconds);
-    FPM_CUDA(cudaMemcpyAsync(c, C.p, wc * 8, cudaMemcpyDeviceToHost, s));
+    Ev allocated, ready_a, ready_b, copied;
+    FPM_CUDA(cudaEventRecord(allocated.e, s));  // stream-ordered allocations visible to the copy streams
+    FPM_CUDA(cudaStreamWaitEvent(h2d, allocated.e, 0));
+    FPM_CUDA(cudaStreamWaitEvent(d2h, allocated.e, 0));
+    FPM_CUDA(cudaMemcpyAsync(A.p, a, wa * 8, cudaMemcpyHostToDevice, h2d));
+    FPM_CUDA(cudaEventRecord(ready_a.e, h2d));
+    FPM_CUDA(cudaMemcpyAsync(B.p, b, wb * 8, cudaMemcpyHostToDevice, h2d));
+    FPM_CUDA(cudaEventRecord(ready_b.e, h2d));
+    HostIO io;
+    io.ready[0] = ready_a.e;
+    io.ready[1] = ready_b.e;
+    io.h_out = c;
+    io.d2h = d2h;
+    polymul_device(A.as<uint64_t>(), a_bits, B.as<uint64_t>(), b_bits, C.as<uint64_t>(), field, s, stage_seconds, &io);
+    FPM_CUDA(cudaEventRecord(copied.e, d2h));
+    FPM_CUDA(cudaStreamWaitEvent(s, copied.e, 0));  // frees below are ordered after the copies
     FPM_CUDA(cudaStreamSynchronize(s));
   });
 }

@@ -4,6 +4,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 
@@ -65,7 +66,12 @@ const DeviceTables& device_tables(int device);
 
 // Basis conversion (k_basis.cu).  w: n_bits/32 uint32 words on the device, in place.
 // live_bits: forward only; bits >= live_bits are zero on entry (zero-tail skip).
-void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s);
+// on_final (inverse only, may be null): called with word ranges [w0, w1) of w (32-bit words) as soon
+// as the work enqueued on s so far leaves them final, so callers can start copying them out while
+// the rest of the conversion runs; every word is reported exactly once.
+using FinalFn = std::function<void(uint64_t w0, uint64_t w1)>;
+void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s,
+                      const FinalFn* on_final = nullptr);
 
 // Encode / decode (k_codec.cu).  poly has 128 * 2^l bits; ev has 2^l uint4.
 void encode_device(const uint32_t* poly, unsigned l, uint4* ev, cudaStream_t s);

@@ -522,7 +522,8 @@ struct Scratch {
 
 }  // namespace
 
-void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s) {
+void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s,
+                      const FinalFn* on_final) {
   if (n_bits < 4 || (n_bits & (n_bits - 1))) throw Error(kInvalid, "basis_cvt: length must be a power of two >= 4");
   set_smem_attr();
   int K = 0;
@@ -537,10 +538,12 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
     const PassList pl = make_passlist(v, inverse);
     bc_small_kernel<<<1, 32, 2 * nwords * sizeof(uint32_t), s>>>(w, (int)nwords, pl, inverse ? 1 : 0);
     FPM_LAUNCH_CHECK();
+    if (inverse && on_final) (*on_final)(0, nwords);
     return;
   }
   if (K <= kTLog2) {
     conv_rows(w, nwords, K, inverse, s);
+    if (inverse && on_final) (*on_final)(0, nwords);
     return;
   }
   const int Kb = std::min(K, 32);
@@ -558,14 +561,30 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
     for (size_t k = 0; k < np; ++k)
       if (sched[k].span > ((size_t)1 << 32)) top.push_back(sched[k]);
   }
-  if (!inverse)
+  const uint64_t nblocks = nwords / block_words;
+  if (!inverse) {
     for (const Pass& p : top) run_big_pass(w, nwords, p, false, live_bits, s);
-  for (uint64_t b = 0; b < nwords / block_words; ++b) {
-    if (!inverse && b * block_words * 32 >= live_bits) continue;  // all-zero block stays zero
-    conv2d(w + b * block_words, Kb, inverse, scratch, s);
+    for (uint64_t b = 0; b < nblocks; ++b) {
+      if (b * block_words * 32 >= live_bits) continue;  // all-zero block stays zero
+      conv2d(w + b * block_words, Kb, inverse, scratch, s);
+    }
+    return;
   }
-  if (inverse)
-    for (size_t k = top.size(); k-- > 0;) run_big_pass(w, nwords, top[k], true, n_bits, s);
+  // Inverse: per-block conversions, then the top passes.  With a single top pass (2^33 bits: S =
+  // 2^33, D = 2^32 - 1) the pass rewrites bits [S/2 - D, S - D) = [1, 2^32 + 1) only, so the upper
+  // block is final, but for its first word, once its own conversion is done: convert it first.
+  uint64_t early_from = nwords;  // words >= early_from are final after their block's conversion
+  if (top.size() == 1 && nblocks == 2) {
+    const uint64_t hi_bit = top[0].span - top[0].shift;  // exclusive end of the rewritten bits
+    early_from = (hi_bit + 31) / 32;
+  }
+  for (uint64_t b = nblocks; b-- > 0;) {
+    conv2d(w + b * block_words, Kb, inverse, scratch, s);
+    const uint64_t w0 = std::max(b * block_words, early_from), w1 = (b + 1) * block_words;
+    if (on_final && w0 < w1) (*on_final)(w0, w1);
+  }
+  for (size_t k = top.size(); k-- > 0;) run_big_pass(w, nwords, top[k], true, n_bits, s);
+  if (on_final) (*on_final)(0, std::min<uint64_t>(early_from, nwords));
 }
 
 }  // namespace fpm
