@@ -330,6 +330,10 @@ void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const
   }
 }
 
+// One thread per butterfly of a tile layer (2^(T-1) pairs), at most 256: small tiles run more CTAs
+// per SM instead of idling half the threads.
+int tile_threads(unsigned T) { return T >= 9 ? 256 : std::max(32, 1 << (T - 1)); }
+
 void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s) {
   if (T == 0) return;
   const size_t smem = ((size_t)1 << T) * sizeof(uint4);
@@ -340,9 +344,10 @@ void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, cons
     attr = true;
   }
   const uint64_t ntiles = ((uint64_t)1 << l) >> T;
-  const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)sms() * 3);
-  if (!inverse) fft_tile_kernel<false><<<grid, 256, smem, s>>>(ev, l, T, tw);
-  else fft_tile_kernel<true><<<grid, 256, smem, s>>>(ev, l, T, tw);
+  const int threads = tile_threads(T);
+  const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)sms() * (768 / threads));
+  if (!inverse) fft_tile_kernel<false><<<grid, threads, smem, s>>>(ev, l, T, tw);
+  else fft_tile_kernel<true><<<grid, threads, smem, s>>>(ev, l, T, tw);
   FPM_LAUNCH_CHECK();
 }
 
@@ -352,8 +357,9 @@ void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigne
   static bool attr = false;
   if (!attr) { set_smem(fft_tile_fused_kernel, (size_t)1 << kTileMax << 4); attr = true; }
   const uint64_t ntiles = ((uint64_t)1 << l) >> T;
-  const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)sms() * 3);
-  fft_tile_fused_kernel<<<grid, 256, smem, s>>>(ea, eb, l, T, tw);
+  const int threads = tile_threads(T);
+  const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)sms() * (768 / threads));
+  fft_tile_fused_kernel<<<grid, threads, smem, s>>>(ea, eb, l, T, tw);
   FPM_LAUNCH_CHECK();
 }
 
