@@ -90,34 +90,6 @@ __device__ __forceinline__ void l1_tile(uint32_t (&m)[8], uint32_t* sc, int g, i
 
 // conv(2^g) over the chunk's rows (rows as units): pass (S, D) -> rows q of each S-span with
 // q in [S/2-D, S-D) get row q+D (and row q+2D if q+2D < S, forward).
-template <bool INV>
-__device__ __forceinline__ void rowpasses(uint32_t (&m)[8], uint32_t* tile, int g, int d) {
-  const int tid = threadIdx.x;
-  const int n = kRowSchedN[g];
-  for (int kk = 0; kk < n; ++kk) {
-    const int k = INV ? n - 1 - kk : kk;
-    const int S = kRowSchedS[g][k], D = kRowSchedD[g][k];
-    __syncthreads();
-    uint4* my4 = reinterpret_cast<uint4*>(tile + tid * 8);
-    my4[0] = make_uint4(m[0], m[1], m[2], m[3]);
-    my4[1] = make_uint4(m[4], m[5], m[6], m[7]);
-    __syncthreads();
-    const int q = d & (S - 1);
-    if (q >= S / 2 - D && q < S - D) {
-      const uint4* s1 = reinterpret_cast<const uint4*>(tile + (tid + D) * 8);
-      uint4 a = s1[0], b = s1[1];
-      if (!INV && q + 2 * D < S) {
-        const uint4* s2 = reinterpret_cast<const uint4*>(tile + (tid + 2 * D) * 8);
-        const uint4 c = s2[0], e = s2[1];
-        a.x ^= c.x; a.y ^= c.y; a.z ^= c.z; a.w ^= c.w;
-        b.x ^= e.x; b.y ^= e.y; b.z ^= e.z; b.w ^= e.w;
-      }
-      m[0] ^= a.x; m[1] ^= a.y; m[2] ^= a.z; m[3] ^= a.w;
-      m[4] ^= b.x; m[5] ^= b.y; m[6] ^= b.z; m[7] ^= b.w;
-    }
-  }
-}
-
 // rowpasses over W adjacent 8-word columns at once (W * 32 B per row and barrier); tile is
 // 256 x kRowPitchW(W) words (one uint4 of padding keeps the 16 B stores conflict-free).
 template <int W>
@@ -159,7 +131,7 @@ __device__ __forceinline__ void rowpasses_w(uint32_t (&m)[W][8], uint32_t* tile,
 }
 
 // Converts every aligned 2^r-bit chunk of the tile (thread t's row in m), r in [1, 16].
-// tile: 256 x 8 words of shared memory; sc: 256 x kScPitch words of shared memory.
+// tile: 256 x kRowPitchW<1> words of shared memory; sc: 256 x kScPitch words of shared memory.
 // All 256 threads must call it (barriers inside when r > 8).
 template <bool INV>
 __device__ __forceinline__ void conv_tile(uint32_t (&m)[8], uint32_t* tile, uint32_t* sc, int r) {
@@ -170,11 +142,11 @@ __device__ __forceinline__ void conv_tile(uint32_t (&m)[8], uint32_t* tile, uint
   const int g = r - 8, d = threadIdx.x & ((1 << g) - 1);
   if (!INV) {
     l1_tile<false>(m, sc, g, d);
-    rowpasses<false>(m, tile, g, d);
+    rowpasses_w<false, 1>(*reinterpret_cast<uint32_t(*)[1][8]>(&m), tile, g, d);
     conv_regs<false>(8, m);
   } else {
     conv_regs<true>(8, m);
-    rowpasses<true>(m, tile, g, d);
+    rowpasses_w<true, 1>(*reinterpret_cast<uint32_t(*)[1][8]>(&m), tile, g, d);
     l1_tile<true>(m, sc, g, d);
   }
 }

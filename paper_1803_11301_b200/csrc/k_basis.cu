@@ -31,7 +31,7 @@ namespace {
 constexpr int kTLog2 = 16;                  // digit size t = 2^16 bits for 2^17..2^32-bit arrays
 constexpr uint64_t kT = (uint64_t)1 << kTLog2;
 constexpr int kTWords = (int)(kT / 32);     // 2048
-constexpr size_t kTileSmem = (kTileRows * 8 + kTileRows * kScPitch) * sizeof(uint32_t);
+constexpr size_t kTileSmem = (kTileRows * kRowPitchW<1> + kTileRows * kScPitch) * sizeof(uint32_t);
 
 int sm_count() {
   int dev, n;
@@ -78,7 +78,7 @@ template <bool INV>
 __global__ void __launch_bounds__(256) conv_rows_kernel(uint32_t* __restrict__ data, uint64_t nwords, int r) {
   extern __shared__ uint32_t smem[];
   uint32_t* tile = smem;
-  uint32_t* sc = smem + kTileRows * 8;
+  uint32_t* sc = smem + kTileRows * kRowPitchW<1>;
   const int tid = threadIdx.x;
   const uint64_t tile_words = nwords < 2048 ? nwords : 2048;
   const uint64_t ntiles = nwords / tile_words;
@@ -108,12 +108,19 @@ __global__ void __launch_bounds__(256) conv_rows_kernel(uint32_t* __restrict__ d
 // every butterfly stage register-local with ONE shared-memory exchange between them:
 //   A: thread t holds word t&31 of tile rows (t>>5) + 8k, k < 32   -> row bits 3..7 local
 //   B: thread t holds words 4(t&7).. of tile rows 8(t>>3) + k, k < 8 -> row bits 0..2 local
-// skew=1: the source row d is an unskewed t-bit row read at bit offset -d (the skew of L1).
+// Skew: source row d is read at bit offset -(((d >> lo) & mask) << log) (mask 0: no skew).  The
+// L1 skew by d bits is split over the two launches of a 2^16-row conversion: the first skews by
+// the low digit d & 255 (rows grow by 256 bits only), the second by 256 * (d >> 8) bits, which is
+// word aligned; whole-row (unit) skews use log = 16.
+struct Skew {
+  uint64_t mask = 0;
+  int lo = 0, log = 0;
+};
 constexpr int kZW = 32;
 constexpr int kZP = 36;  // shared row pitch (16 B aligned, conflict-free for both mappings)
-__global__ void __launch_bounds__(256) zeta_kernel(const uint32_t* __restrict__ src, uint64_t src_pitch,
+__global__ void __launch_bounds__(256, 2) zeta_kernel(const uint32_t* __restrict__ src, uint64_t src_pitch,
                                                    uint32_t* __restrict__ dst, uint64_t dst_pitch, uint64_t D,
-                                                   int b0, int nb, uint64_t skew_unit, uint64_t src_row_words,
+                                                   int b0, int nb, Skew skew, uint64_t src_row_words,
                                                    uint64_t windows) {
   extern __shared__ __align__(16) uint32_t sx[];  // 256 x kZP
   const int tid = threadIdx.x;
@@ -128,22 +135,47 @@ __global__ void __launch_bounds__(256) zeta_kernel(const uint32_t* __restrict__ 
     // ---- mapping A: load, stages on tile-row bits 3..7
     const int c = tid & 31;
     uint32_t a[32];
+    if (skew.mask && skew.log >= 5) {  // word-aligned skew: plain coalesced loads
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      const int R = (tid >> 5) + 8 * k;
-      const uint64_t d = base + ((uint64_t)(R & ((1 << nb) - 1)) << b0);
-      const uint64_t wi = wb * wpc + (R >> nb);
-      uint32_t v = 0;
-      if (wi < windows) {
-        const uint32_t* row = src + d * src_pitch;
-        if (skew_unit) {
-          const int64_t pos = (int64_t)(wi * 32 * kZW) + 32 * c - (int64_t)(d * skew_unit);
-          v = g_get32(row, src_row_words, pos);
-        } else {
-          v = __ldg(row + wi * kZW + c);
-        }
+      for (int k = 0; k < 32; ++k) {
+        const int R = (tid >> 5) + 8 * k;
+        const uint64_t d = base + ((uint64_t)(R & ((1 << nb) - 1)) << b0);
+        const uint64_t wi = wb * wpc + (R >> nb);
+        const int64_t iw = (int64_t)(wi * kZW) - (int64_t)((((d >> skew.lo) & skew.mask) << skew.log) >> 5) + c;
+        a[k] = (wi < windows && iw >= 0 && iw < (int64_t)src_row_words) ? __ldg(src + d * src_pitch + iw) : 0u;
       }
-      a[k] = v;
+    } else if (skew.mask) {
+      // R (so d, wi, the shift) is warp-uniform: one coalesced word per lane and row, all rows'
+      // loads in flight at once (lane 31 also fetches the word after the window), then the
+      // neighbour word comes by shuffle and a funnel shift aligns the window.
+      uint32_t e[32];
+      int sh[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const int R = (tid >> 5) + 8 * k;
+        const uint64_t d = base + ((uint64_t)(R & ((1 << nb) - 1)) << b0);
+        const uint64_t wi = wb * wpc + (R >> nb);
+        const uint32_t* row = src + d * src_pitch;
+        const int64_t pos0 = (int64_t)(wi * 32 * kZW) - (int64_t)(((d >> skew.lo) & skew.mask) << skew.log);
+        const int64_t iw = (pos0 >> 5) + c;
+        sh[k] = (int)(pos0 & 31);
+        const bool ok = wi < windows;
+        a[k] = (ok && iw >= 0 && iw < (int64_t)src_row_words) ? __ldg(row + iw) : 0u;
+        e[k] = (ok && c == 31 && iw + 1 >= 0 && iw + 1 < (int64_t)src_row_words) ? __ldg(row + iw + 1) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const uint32_t nx = __shfl_down_sync(0xFFFFFFFFu, a[k], 1);
+        a[k] = __funnelshift_r(a[k], c == 31 ? e[k] : nx, sh[k]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const int R = (tid >> 5) + 8 * k;
+        const uint64_t d = base + ((uint64_t)(R & ((1 << nb) - 1)) << b0);
+        const uint64_t wi = wb * wpc + (R >> nb);
+        a[k] = wi < windows ? __ldg(src + d * src_pitch + wi * kZW + c) : 0u;
+      }
     }
 #pragma unroll
     for (int b = 3; b < 8; ++b) {
@@ -187,7 +219,7 @@ __global__ void __launch_bounds__(256) carry_rows_kernel(const uint32_t* __restr
                                                          uint32_t* __restrict__ out, uint64_t D) {
   extern __shared__ uint32_t smem[];
   uint32_t* tile = smem;
-  uint32_t* sc = smem + kTileRows * 8;
+  uint32_t* sc = smem + kTileRows * kRowPitchW<1>;
   const int tid = threadIdx.x;
   for (uint64_t k = blockIdx.x; k < D; k += gridDim.x) {
     const uint32_t* rk = gs + k * gs_pitch;
@@ -403,15 +435,14 @@ void conv_rows(uint32_t* data, uint64_t nwords, int r, bool inv, cudaStream_t s)
   FPM_LAUNCH_CHECK();
 }
 
-// skew_unit: 0 = none; 1 = row d read at bit offset -d (bit-level L1); kT = row d read at offset
-// -d * 2^16 bits (unit-level L1 over whole rows, src_row_words = one row of units).
+// src_row_words: words of one source row (reads beyond are zeros).
 void zeta(const uint32_t* src, uint64_t src_pitch, uint32_t* dst, uint64_t dst_pitch, uint64_t D, int b0, int nb,
-          uint64_t skew_unit, uint64_t windows, cudaStream_t s, uint64_t src_row_words = kTWords) {
+          Skew skew, uint64_t windows, cudaStream_t s, uint64_t src_row_words) {
   if (nb <= 0) return;
   const int wpc = 256 >> nb;
   const uint64_t items = (D >> nb) * ((windows + wpc - 1) / wpc);
   zeta_kernel<<<grid_cap(items, 4), 256, 256 * kZP * sizeof(uint32_t), s>>>(
-      src, src_pitch, dst, dst_pitch, D, b0, nb, skew_unit, src_row_words, windows);
+      src, src_pitch, dst, dst_pitch, D, b0, nb, skew, src_row_words, windows);
   FPM_LAUNCH_CHECK();
 }
 
@@ -461,14 +492,17 @@ void conv_cols(uint32_t* w, uint32_t* scratch, int lgD, bool inv, cudaStream_t s
   const uint64_t su = 256 + std::max<uint64_t>(Dd, 1);           // skewed units per digit row
   const uint64_t sk_pitch = su * kTWords;                         // words
   const uint64_t windows = sk_pitch / kZW;
+  Skew unit_skew;  // digit row dh read at offset -dh whole rows
+  unit_skew.mask = ~(uint64_t)0;
+  unit_skew.log = kTLog2;
   if (!inv) {
-    zeta(w, 256 * (uint64_t)kTWords, scratch, sk_pitch, Dd, 0, gd, kT, windows, s, 256 * (uint64_t)kTWords);
+    zeta(w, 256 * (uint64_t)kTWords, scratch, sk_pitch, Dd, 0, gd, unit_skew, windows, s, 256 * (uint64_t)kTWords);
     unit_carry_cols(scratch, sk_pitch, w, gd, s);
     slab(w, 8, 1, (Dd * 256 / 256) * (kTWords / 8), false, s);   // C_rows: conv(256) over consecutive rows
   } else {
     slab(w, 8, 1, (Dd * 256 / 256) * (kTWords / 8), true, s);
     slab(w, gd, 256, 256 * (kTWords / 8), true, s);               // C_cols^-1: conv(Dd) at row stride 256
-    zeta(w, 256 * (uint64_t)kTWords, scratch, sk_pitch, Dd, 0, gd, kT, windows, s, 256 * (uint64_t)kTWords);
+    zeta(w, 256 * (uint64_t)kTWords, scratch, sk_pitch, Dd, 0, gd, unit_skew, windows, s, 256 * (uint64_t)kTWords);
     unit_overflow(scratch, sk_pitch, w, Dd, s);
   }
 }
@@ -481,17 +515,27 @@ void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s) {
   const uint64_t wsk = wsk_bits / 32;  // skewed row pitch (words)
   const uint64_t windows = wsk / kZW;
   const int nb_lo = std::min(lgD, 8), nb_hi = lgD - nb_lo;
+  // first launch: skew by the low 8 digit bits into rows of t + 1024 bits (scratch tail), second:
+  // the word-aligned 256 * (d >> 8) skew, into full skewed rows (scratch head)
+  const uint64_t w1 = (kT + 32 * kZW) / 32;
+  uint32_t* s1 = nb_hi ? scratch + D * wsk : scratch;
+  const uint64_t p1 = nb_hi ? w1 : wsk;
+  Skew lo_skew, hi_skew;
+  lo_skew.mask = 255;
+  hi_skew.mask = ~(uint64_t)0; hi_skew.lo = 8; hi_skew.log = 8;
+  auto l1_zeta = [&](const uint32_t* src) {
+    zeta(src, kTWords, s1, p1, D, 0, nb_lo, lo_skew, p1 / kZW, s, kTWords);
+    if (nb_hi) zeta(s1, w1, scratch, wsk, D, 8, nb_hi, hi_skew, windows, s, w1);
+  };
   if (!inv) {
-    zeta(w, kTWords, scratch, wsk, D, 0, nb_lo, 1, windows, s);
-    zeta(scratch, wsk, scratch, wsk, D, 8, nb_hi, 0, windows, s);
+    l1_zeta(w);
     carry_rows_kernel<<<grid_cap(D, 4), 256, kTileSmem, s>>>(scratch, wsk, w, D);
     FPM_LAUNCH_CHECK();
     conv_cols(w, scratch, lgD, false, s);
   } else {
     conv_rows(w, D * kTWords, kTLog2, true, s);
     conv_cols(w, scratch, lgD, true, s);
-    zeta(w, kTWords, scratch, wsk, D, 0, nb_lo, 1, windows, s);
-    zeta(scratch, wsk, scratch, wsk, D, 8, nb_hi, 0, windows, s);
+    l1_zeta(w);
     overflow_kernel<<<grid_cap(D * kTWords / 256, 32), 256, 0, s>>>(scratch, wsk, w, D);
     FPM_LAUNCH_CHECK();
   }
@@ -548,7 +592,8 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
   }
   const int Kb = std::min(K, 32);
   const uint64_t lgD = Kb - kTLog2, D = (uint64_t)1 << lgD;
-  Scratch scr(D * (kT + std::max<uint64_t>(D, 32 * kZW)) / 8, s);
+  // skewed rows (t + max(D, 1024) bits) + the first zeta's rows (t + 1024 bits) when D > 256
+  Scratch scr(D * (kT + std::max<uint64_t>(D, 32 * kZW)) / 8 + (D > 256 ? D * (kT + 32 * kZW) / 8 : 0), s);
   uint32_t* scratch = static_cast<uint32_t*>(scr.p);
   const uint64_t block_words = ((uint64_t)1 << Kb) / 32;
   // Arrays above 2^32 bits: their passes with S > 2^32 come first (forward) / last (inverse);
