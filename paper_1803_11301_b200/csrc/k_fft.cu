@@ -152,15 +152,40 @@ __global__ void __launch_bounds__(kTop4Threads, 1) fft_top4_kernel(uint4* __rest
 }
 
 // ------------------------------------------------------------------ tile layers (i < T)
+// Layers i >= kTabLayer of a 256-thread tile have <= 2 twiddles per tile, each shared by >= 256
+// butterflies: those use an M8 table built in shared memory (tab != nullptr: 64 KiB + 144 rows
+// after the tile) instead of the generic multiply.
+constexpr unsigned kTabLayer = 8;
 template <bool INV>
 __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, unsigned l, uint64_t tile_idx,
-                                            const TwiddleSrc& tw) {
+                                            const TwiddleSrc& tw, uint4* __restrict__ tab) {
   const int npairs = 1 << (T - 1);
   for (unsigned step = 0; step < T; ++step) {
     const unsigned i = INV ? step : T - 1 - step;
     const uint64_t bhi = tile_idx << (T - 1 - i);  // global block index of the tile's first block
     // w = v_{l+64-i} ^ C2P(2*(bhi + blk)) = Z ^ C2P(2*blk)  (bit ranges disjoint, C2P linear)
     const uint4 Z = twiddle(tw, l, i, bhi);
+    if (tab && i >= kTabLayer) {
+      const int q = threadIdx.x & 7;
+      for (int blk = 0; blk < (npairs >> i); ++blk) {
+        m8_build(tab, tab + kM8Uint4, x4(Z, c2p2(tw.c2p, (uint64_t)blk)), threadIdx.x);
+        for (int j = threadIdx.x; j < (1 << i); j += blockDim.x) {
+          const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+          uint4 u0 = s[i0], u1 = s[i1];
+          if (!INV) {
+            u0 = x4(u0, m8_mul(tab, u1, q));
+            u1 = x4(u1, u0);
+          } else {
+            u1 = x4(u1, u0);
+            u0 = x4(u0, m8_mul(tab, u1, q));
+          }
+          s[i0] = u0;
+          s[i1] = u1;
+        }
+      }
+      __syncthreads();
+      continue;
+    }
     for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
       const int blk = p >> i, j = p & ((1 << i) - 1);
       const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
@@ -181,34 +206,37 @@ __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, u
 }
 
 template <bool INV>
-__global__ void __launch_bounds__(256) fft_tile_kernel(uint4* __restrict__ ev, unsigned l, unsigned T, TwiddleSrc tw) {
+__global__ void __launch_bounds__(256) fft_tile_kernel(uint4* __restrict__ ev, unsigned l, unsigned T, TwiddleSrc tw,
+                                                       int use_tab) {
   extern __shared__ uint4 s[];
   const int n = 1 << T;
+  uint4* tab = use_tab ? s + n : nullptr;
   const uint64_t ntiles = ((uint64_t)1 << l) >> T;
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     uint4* g = ev + (t << T);
     for (int k = threadIdx.x; k < n; k += blockDim.x) s[k] = g[k];
     __syncthreads();
-    tile_layers<INV>(s, T, l, t, tw);
+    tile_layers<INV>(s, T, l, t, tw, tab);
     for (int k = threadIdx.x; k < n; k += blockDim.x) g[k] = s[k];
     __syncthreads();
   }
 }
 
 __global__ void __launch_bounds__(256) fft_tile_fused_kernel(const uint4* __restrict__ ea, uint4* __restrict__ eb,
-                                                             unsigned l, unsigned T, TwiddleSrc tw) {
+                                                             unsigned l, unsigned T, TwiddleSrc tw, int use_tab) {
   extern __shared__ uint4 s[];
   const int n = 1 << T;
+  uint4* tab = use_tab ? s + n : nullptr;
   const uint64_t ntiles = ((uint64_t)1 << l) >> T;
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     uint4* g = eb + (t << T);
     const uint4* ga = ea + (t << T);
     for (int k = threadIdx.x; k < n; k += blockDim.x) s[k] = g[k];
     __syncthreads();
-    tile_layers<false>(s, T, l, t, tw);
+    tile_layers<false>(s, T, l, t, tw, tab);
     for (int k = threadIdx.x; k < n; k += blockDim.x) s[k] = gf_mul(ga[k], s[k]);
     __syncthreads();
-    tile_layers<true>(s, T, l, t, tw);
+    tile_layers<true>(s, T, l, t, tw, tab);
     for (int k = threadIdx.x; k < n; k += blockDim.x) g[k] = s[k];
     __syncthreads();
   }
@@ -257,16 +285,16 @@ void set_smem(K kernel, size_t bytes) {
 
 }  // namespace
 
-// Tile depth: layers below T run in shared-memory tiles (generic multiplies), layers >= T in
-// radix-4 M8-table passes (~3x cheaper per product, measured).  T = 10 for large transforms (16 KiB
-// tiles; B200 cfg5 sweep T = 8..12: 83.4 / 80.0 / 79.5 / 80.2 / 81.0 ms); T = 8 below
-// 2^18 elements so the tile pass still has >= 2^10 tiles to spread over the SMs.
+// Tile depth: layers below T run in shared-memory tiles (generic multiplies, M8 tables for layers
+// >= kTabLayer), layers >= T in radix-4 M8-table passes.  B200 sweeps (ms, T = 10 / 11):
+// 2^26-bit 1.269 / 1.262, 2^28 4.375 / 4.320, 2^30 17.14 / 16.93, 2^32 73.0 / 71.8; 2^24 0.457 /
+// 0.470; below 2^18 elements T = 8 keeps >= 2^10 tiles in flight.
 unsigned fft_tile_log2(unsigned l) {
   static const int knob = [] {
     const char* e = std::getenv("FPM_TILE_LOG2");  // tuning override (8..12)
     return e ? std::max(8, std::min(kTileMax, std::atoi(e))) : 0;
   }();
-  const unsigned cap = knob ? (unsigned)knob : (l >= 18 ? 10u : 8u);
+  const unsigned cap = knob ? (unsigned)knob : (l >= 20 ? 11u : l >= 18 ? 10u : 8u);
   return l < cap ? l : cap;
 }
 
@@ -334,32 +362,47 @@ void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const
 // per SM instead of idling half the threads.
 int tile_threads(unsigned T) { return T >= 9 ? 256 : std::max(32, 1 << (T - 1)); }
 
+// Tile launch geometry: tables for layers >= kTabLayer when the tile runs 256 threads (T >= 9;
+// FPM_TILE_TABLES=0 disables them for comparison).
+struct TileCfg {
+  int threads, use_tab, grid;
+  size_t smem;
+};
+TileCfg tile_cfg(unsigned l, unsigned T) {
+  static const bool tables = [] {
+    const char* e = std::getenv("FPM_TILE_TABLES");
+    return !(e && e[0] == '0');
+  }();
+  TileCfg c;
+  c.threads = tile_threads(T);
+  c.use_tab = tables && T > kTabLayer && c.threads == 256;
+  c.smem = ((size_t)1 << T) * sizeof(uint4) + (c.use_tab ? (kM8Uint4 + 144) * sizeof(uint4) : 0);
+  const int per_sm = c.use_tab ? 2 : 768 / c.threads;
+  c.grid = (int)std::min<uint64_t>(((uint64_t)1 << l) >> T, (uint64_t)sms() * per_sm);
+  return c;
+}
+constexpr size_t kTileSmemMax = ((size_t)1 << kTileMax << 4) + (kM8Uint4 + 144) * sizeof(uint4);
+
 void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s) {
   if (T == 0) return;
-  const size_t smem = ((size_t)1 << T) * sizeof(uint4);
   static bool attr = false;
   if (!attr) {
-    set_smem(fft_tile_kernel<false>, (size_t)1 << kTileMax << 4);
-    set_smem(fft_tile_kernel<true>, (size_t)1 << kTileMax << 4);
+    set_smem(fft_tile_kernel<false>, kTileSmemMax);
+    set_smem(fft_tile_kernel<true>, kTileSmemMax);
     attr = true;
   }
-  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
-  const int threads = tile_threads(T);
-  const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)sms() * (768 / threads));
-  if (!inverse) fft_tile_kernel<false><<<grid, threads, smem, s>>>(ev, l, T, tw);
-  else fft_tile_kernel<true><<<grid, threads, smem, s>>>(ev, l, T, tw);
+  const TileCfg c = tile_cfg(l, T);
+  if (!inverse) fft_tile_kernel<false><<<c.grid, c.threads, c.smem, s>>>(ev, l, T, tw, c.use_tab);
+  else fft_tile_kernel<true><<<c.grid, c.threads, c.smem, s>>>(ev, l, T, tw, c.use_tab);
   FPM_LAUNCH_CHECK();
 }
 
 void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
                                  cudaStream_t s) {
-  const size_t smem = ((size_t)1 << T) * sizeof(uint4);
   static bool attr = false;
-  if (!attr) { set_smem(fft_tile_fused_kernel, (size_t)1 << kTileMax << 4); attr = true; }
-  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
-  const int threads = tile_threads(T);
-  const int grid = (int)std::min<uint64_t>(ntiles, (uint64_t)sms() * (768 / threads));
-  fft_tile_fused_kernel<<<grid, threads, smem, s>>>(ea, eb, l, T, tw);
+  if (!attr) { set_smem(fft_tile_fused_kernel, kTileSmemMax); attr = true; }
+  const TileCfg c = tile_cfg(l, T);
+  fft_tile_fused_kernel<<<c.grid, c.threads, c.smem, s>>>(ea, eb, l, T, tw, c.use_tab);
   FPM_LAUNCH_CHECK();
 }
 
