@@ -303,6 +303,19 @@ const DeviceTables& device_tables(int dev) {
         dec[(c * 16 + v) * kM4RCopies + r] = to4(d);
       }
     }
+  // rotated 8-bit tables (gf128.cuh m8 layout): entry (c, v) at (c >> 3) * 2048 + v * 8 + (c & 7)
+  std::vector<uint4> enc8(kM8Uint4), dec8(kM8Uint4);
+  for (int c = 0; c < 16; ++c)
+    for (int v = 0; v < 256; ++v) {
+      U128 e, d;
+      for (int j = 0; j < 8; ++j)
+        if (v >> j & 1) {
+          e.lo ^= ft.enc_rows[8 * c + j].lo; e.hi ^= ft.enc_rows[8 * c + j].hi;
+          d.lo ^= ft.inv_rows[8 * c + j].lo; d.hi ^= ft.inv_rows[8 * c + j].hi;
+        }
+      enc8[(c >> 3) * 2048 + v * 8 + (c & 7)] = to4(e);
+      dec8[(c >> 3) * 2048 + v * 8 + (c & 7)] = to4(d);
+    }
   for (int part = 0; part < 4; ++part)
     for (int e = 0; e < 512; ++e) {
       U128 acc;
@@ -324,6 +337,7 @@ const DeviceTables& device_tables(int dev) {
   };
   up(&t.cantor, cantor); up(&t.enc_rows, rows); up(&t.inv_rows, inv);
   up(&t.enc_m4r, enc); up(&t.dec_m4r, dec); up(&t.c2p, c2p);
+  up(&t.enc_m8, enc8); up(&t.dec_m8, dec8);
   // Keep freed pool memory cached: the pipeline allocates its scratch per call (reentrant).
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {

@@ -43,6 +43,8 @@ struct DeviceTables {
   uint4* inv_rows = nullptr;  // 128 rows of E^{-1}
   uint4* enc_m4r = nullptr;   // 32 chunks x 16 x 8 copies (x*E by nibbles)
   uint4* dec_m4r = nullptr;   // 32 chunks x 16 x 8 copies (x*E^{-1})
+  uint4* enc_m8 = nullptr;    // rotated 8-bit tables (gf128.cuh m8 layout) of x*E
+  uint4* dec_m8 = nullptr;    // ... of x*E^{-1}
   uint4* c2p = nullptr;       // 4 x 512: part p entry e = C2P(2 * (e << 9p))
 };
 

@@ -11,8 +11,9 @@
 //                           over 256-row groups (stride 1, then stride 256): pure streaming XOR tiles
 //   C     carry_rows_kernel unskew + single carry level, then conv(2^16) of the row in shared memory
 //                           (forward; the inverse uses overflow_kernel and a separate row pass)
-//   C_D   conv over the row index: D <= 256 -> slab tiles of D rows x 256 bits (row XOR passes);
-//         D > 256 -> bit transpose, conv(D) per transposed row, transpose back
+//   C_D   conv over the row index: D <= 256 -> slab tiles of D rows x 1024 bits (row XOR passes);
+//         D > 256 -> the same recursion one level up with whole rows as units (row-skewed zeta,
+//         unit carry fused with the row passes over the high digit, slab passes over the low one)
 // HBM traffic at K = 32: ~9 GiB (vs ~70 GiB for 48 separate passes).  Arrays of <= 2^16 bits run in
 // one shared-memory tile; > 2^32 bits run their top passes with the generic in-place pass kernel
 // and recurse per 2^32-bit block.
@@ -361,54 +362,6 @@ __global__ void unit_overflow_kernel(const uint32_t* __restrict__ gs, uint64_t g
   }
 }
 
-// ------------------------------------------------------------------ bit-matrix transpose
-// src: R rows x C bits (pitch C/32 words) -> dst: C rows x R bits (pitch R/32 words); R, C >= 256.
-// 256 x 256-bit tiles (32 B row segments, sector-complete), 32x32 blocks via warp shuffles.
-constexpr int kTT = 256, kTTW = kTT / 32, kTTP = kTTW + 1;  // 18 KiB smem -> 8 CTAs/SM hide latency
-__global__ void __launch_bounds__(256) transpose_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
-                                                        uint64_t R, uint64_t C) {
-  extern __shared__ uint32_t tsm[];
-  uint32_t* sin = tsm;
-  uint32_t* sout = tsm + kTT * kTTP;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t rt = R / kTT, ct = C / kTT;
-  const uint64_t srcp = C / 32, dstp = R / 32;
-  for (uint64_t it = blockIdx.x; it < rt * ct; it += gridDim.x) {
-    const uint64_t tr = it / ct, tc = it - tr * ct;
-    for (int rr = tid; rr < kTT; rr += 256) {
-      const uint4* p = reinterpret_cast<const uint4*>(src + (tr * kTT + rr) * srcp + tc * kTTW);
-      uint32_t* s = sin + rr * kTTP;
-#pragma unroll
-      for (int q = 0; q < kTTW / 4; ++q) {
-        const uint4 a = p[q];
-        s[4 * q] = a.x; s[4 * q + 1] = a.y; s[4 * q + 2] = a.z; s[4 * q + 3] = a.w;
-      }
-    }
-    __syncthreads();
-    for (int blk = warp; blk < kTTW * kTTW; blk += 8) {
-      const int rb = blk / kTTW, cw = blk % kTTW;
-      uint32_t x = sin[(rb * 32 + lane) * kTTP + cw];
-      const uint32_t masks[5] = {0xFFFF0000u, 0xFF00FF00u, 0xF0F0F0F0u, 0xCCCCCCCCu, 0xAAAAAAAAu};
-#pragma unroll
-      for (int k = 0; k < 5; ++k) {
-        const int s = 16 >> k;
-        const uint32_t mk = masks[k];
-        const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, s);
-        x = (lane & s) ? ((x & mk) | ((y >> s) & ~mk)) : ((x & ~mk) | ((y << s) & mk));
-      }
-      sout[(cw * 32 + lane) * kTTP + rb] = x;  // output row cw*32+lane, word rb (input rows 32rb..)
-    }
-    __syncthreads();
-    for (int rr = tid; rr < kTT; rr += 256) {
-      uint4* p = reinterpret_cast<uint4*>(dst + (tc * kTT + rr) * dstp + tr * kTTW);
-      const uint32_t* s = sout + rr * kTTP;
-#pragma unroll
-      for (int q = 0; q < kTTW / 4; ++q) p[q] = make_uint4(s[4 * q], s[4 * q + 1], s[4 * q + 2], s[4 * q + 3]);
-    }
-    __syncthreads();
-  }
-}
-
 // ------------------------------------------------------------------ host orchestration
 void set_smem_attr() {
   static bool done[64];
@@ -418,8 +371,6 @@ void set_smem_attr() {
   FPM_CUDA(cudaFuncSetAttribute(conv_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
   FPM_CUDA(cudaFuncSetAttribute(conv_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
   FPM_CUDA(cudaFuncSetAttribute(carry_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
-  FPM_CUDA(cudaFuncSetAttribute(transpose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(2 * kTT * kTTP * sizeof(uint32_t))));
   done[dev] = true;
 }
 
@@ -443,11 +394,6 @@ void zeta(const uint32_t* src, uint64_t src_pitch, uint32_t* dst, uint64_t dst_p
   const uint64_t items = (D >> nb) * ((windows + wpc - 1) / wpc);
   zeta_kernel<<<grid_cap(items, 4), 256, 256 * kZP * sizeof(uint32_t), s>>>(
       src, src_pitch, dst, dst_pitch, D, b0, nb, skew, src_row_words, windows);
-  FPM_LAUNCH_CHECK();
-}
-
-void transpose(const uint32_t* src, uint32_t* dst, uint64_t R, uint64_t C, cudaStream_t s) {
-  transpose_kernel<<<grid_cap((R / kTT) * (C / kTT), 8), 256, 2 * kTT * kTTP * sizeof(uint32_t), s>>>(src, dst, R, C);
   FPM_LAUNCH_CHECK();
 }
 

@@ -22,30 +22,49 @@ constexpr int kSlabWords = 32;                 // words per row per CTA slab -> 
 constexpr int kPad = kSlabWords + 1;
 
 // 32x32 bit transpose across a warp: on entry lane r holds row r (bit c = M[r][c]); on exit lane c
-// holds column c (bit r = M[r][c]).
-__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
-  const uint32_t masks[5] = {0xFFFF0000u, 0xFF00FF00u, 0xF0F0F0F0u, 0xCCCCCCCCu, 0xAAAAAAAAu};
+// holds column c (bit r = M[r][c]).  Five exchange steps with the lane at distance s = 16..1: the
+// byte-granular steps are one PRMT with a lane-dependent selector, the bit steps one rotate (left
+// by s in the lower lane, right in the upper) and one masked merge (LOP3) -- 8 ALU ops + 5 SHFL.
+struct Transpose32 {
+  uint32_t sel16, sel8, amt[3], msk[3];
+  __device__ explicit Transpose32(int lane) {
+    sel16 = (lane & 16) ? 0x3276u : 0x5410u;
+    sel8 = (lane & 8) ? 0x3715u : 0x6240u;
+    const uint32_t m[3] = {0xF0F0F0F0u, 0xCCCCCCCCu, 0xAAAAAAAAu};
 #pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    const int s = 16 >> k;
-    const uint32_t m = masks[k];
-    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, s);
-    if (lane & s) x = (x & m) | ((y >> s) & ~m);
-    else x = (x & ~m) | ((y << s) & m);
+    for (int k = 0; k < 3; ++k) {
+      const int sft = 4 >> k;
+      const bool up = lane & sft;
+      amt[k] = up ? 32 - sft : sft;
+      msk[k] = up ? ~m[k] : m[k];
+    }
   }
-  return x;
-}
+  __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+    x = __byte_perm(x, __shfl_xor_sync(0xFFFFFFFFu, x, 16), sel16);
+    x = __byte_perm(x, __shfl_xor_sync(0xFFFFFFFFu, x, 8), sel8);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, 4 >> k);
+      const uint32_t r = __funnelshift_l(y, y, amt[k]);
+      x = (x & ~msk[k]) | (r & msk[k]);
+    }
+    return x;
+  }
+};
 
 template <int ROWS>  // 64: rows >= 64 are known zero (pipeline); 128: general encode
 __global__ void __launch_bounds__(256) encode_kernel(const uint32_t* __restrict__ poly, uint64_t row_words,
                                                      uint64_t col0_words, uint64_t nslabs,
                                                      const uint4* __restrict__ tab_g, uint4* __restrict__ ev) {
   extern __shared__ uint4 smem4[];
-  uint4* tab = smem4;                                           // (ROWS/4) chunks x 16 x 8 copies
-  uint32_t* slab = reinterpret_cast<uint32_t*>(smem4 + (ROWS / 4) * 16 * kM4RCopies);  // ROWS x kPad
+  // rotated 8-bit table of x*E (gf128.cuh m8 layout): chunks 0..7 (ROWS = 64) or all 16
+  constexpr int kTab = ROWS == 64 ? kM8Uint4 / 2 : kM8Uint4;
+  uint4* tab = smem4;
+  uint32_t* slab = reinterpret_cast<uint32_t*>(smem4 + kTab);  // ROWS x kPad
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < (ROWS / 4) * 16 * kM4RCopies; i += blockDim.x) tab[i] = tab_g[i];
-  const int copy = lane & 7;
+  for (int i = tid; i < kTab; i += blockDim.x) tab[i] = tab_g[i];
+  const int q8 = lane & 7;
+  const Transpose32 tr(lane);
   for (uint64_t sl = blockIdx.x; sl < nslabs; sl += gridDim.x) {
     const uint64_t w0 = sl * kSlabWords;
     __syncthreads();
@@ -59,22 +78,21 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint32_t* __restrict_
       const int col = warp * (kSlabWords / 8) + k;
       uint32_t xw[4];
 #pragma unroll
-      for (int q = 0; q < ROWS / 32; ++q) xw[q] = warp_transpose32(slab[(q * 32 + lane) * kPad + col], lane);
+      for (int q = 0; q < ROWS / 32; ++q) xw[q] = tr(slab[(q * 32 + lane) * kPad + col]);
       uint4 f;
-      if (ROWS == 64) {
-        // x has 64 bits -> 16 nibble chunks
+      if (ROWS == 64) {  // 8 byte chunks, lane-rotated order: conflict-free LDS.128
         uint4 acc0 = make_uint4(0, 0, 0, 0), acc1 = make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int q = 0; q < 2; ++q)
-#pragma unroll
-          for (int s = 0; s < 8; s += 2) {
-            const int c0 = q * 8 + s;
-            acc0 = x4(acc0, tab[((c0 * 16 + ((xw[q] >> (4 * s)) & 15u)) << 3) + copy]);
-            acc1 = x4(acc1, tab[(((c0 + 1) * 16 + ((xw[q] >> (4 * s + 4)) & 15u)) << 3) + copy]);
-          }
+        for (int kk = 0; kk < 8; kk += 2) {
+          const int c0 = (kk + q8) & 7, c1 = (kk + 1 + q8) & 7;
+          const uint32_t b0 = __byte_perm(c0 < 4 ? xw[0] : xw[1], 0, 0x4440u | (uint32_t)(c0 & 3));
+          const uint32_t b1 = __byte_perm(c1 < 4 ? xw[0] : xw[1], 0, 0x4440u | (uint32_t)(c1 & 3));
+          acc0 = x4(acc0, tab[b0 * 8 + c0]);
+          acc1 = x4(acc1, tab[b1 * 8 + c1]);
+        }
         f = x4(acc0, acc1);
       } else {
-        f = m4r_mul(tab, make_uint4(xw[0], xw[1], xw[ROWS / 32 > 2 ? 2 : 0], xw[ROWS / 32 > 3 ? 3 : 0]), copy);
+        f = m8_mul(tab, make_uint4(xw[0], xw[1], xw[ROWS / 32 > 2 ? 2 : 0], xw[ROWS / 32 > 3 ? 3 : 0]), q8);
       }
       ev[(w0 + col) * 32 + lane] = f;
     }
@@ -85,22 +103,23 @@ __global__ void __launch_bounds__(256) decode_kernel(const uint4* __restrict__ e
                                                      uint64_t row_words,
                                                      const uint4* __restrict__ tab_g, uint32_t* __restrict__ poly) {
   extern __shared__ uint4 smem4[];
-  uint4* tab = smem4;  // 32 chunks x 16 x 8 copies
-  uint32_t* slab = reinterpret_cast<uint32_t*>(smem4 + kM4RUint4);  // 128 x kPad
+  uint4* tab = smem4;  // rotated 8-bit table of x*E^-1 (gf128.cuh m8 layout)
+  uint32_t* slab = reinterpret_cast<uint32_t*>(smem4 + kM8Uint4);  // 128 x kPad
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < kM4RUint4; i += blockDim.x) tab[i] = tab_g[i];
-  const int copy = lane & 7;
+  for (int i = tid; i < kM8Uint4; i += blockDim.x) tab[i] = tab_g[i];
+  const int q8 = lane & 7;
+  const Transpose32 tr(lane);
   __syncthreads();
   for (uint64_t sl = blockIdx.x; sl < nslabs; sl += gridDim.x) {
     const uint64_t w0 = sl * kSlabWords;
 #pragma unroll 1
     for (int k = 0; k < kSlabWords / 8; ++k) {
       const int col = warp * (kSlabWords / 8) + k;
-      const uint4 y = m4r_mul(tab, ev[(w0 + col) * 32 + lane], copy);
-      slab[(0 * 32 + lane) * kPad + col] = warp_transpose32(y.x, lane);
-      slab[(1 * 32 + lane) * kPad + col] = warp_transpose32(y.y, lane);
-      slab[(2 * 32 + lane) * kPad + col] = warp_transpose32(y.z, lane);
-      slab[(3 * 32 + lane) * kPad + col] = warp_transpose32(y.w, lane);
+      const uint4 y = m8_mul(tab, ev[(w0 + col) * 32 + lane], q8);
+      slab[(0 * 32 + lane) * kPad + col] = tr(y.x);
+      slab[(1 * 32 + lane) * kPad + col] = tr(y.y);
+      slab[(2 * 32 + lane) * kPad + col] = tr(y.z);
+      slab[(3 * 32 + lane) * kPad + col] = tr(y.w);
     }
     __syncthreads();
     for (int i = tid; i < 128 * kSlabWords; i += blockDim.x) {
@@ -196,15 +215,15 @@ void encode_cols_device(const uint32_t* poly, unsigned l, uint64_t col0, uint64_
   const DeviceTables& dt = device_tables(dev);
   const uint64_t nslabs = ncols / 32 / kSlabWords;
   if (rows_live == 64) {
-    const size_t smem = 16 * 16 * kM4RCopies * sizeof(uint4) + 64 * kPad * sizeof(uint32_t);
+    const size_t smem = kM8Uint4 / 2 * sizeof(uint4) + 64 * kPad * sizeof(uint32_t);
     static bool attr = false;
     if (!attr) { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); attr = true; }
-    encode_kernel<64><<<grid_for(nslabs, 4), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, dt.enc_m4r, ev);
+    encode_kernel<64><<<grid_for(nslabs, 4), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, dt.enc_m8, ev);
   } else {
-    const size_t smem = 32 * 16 * kM4RCopies * sizeof(uint4) + 128 * kPad * sizeof(uint32_t);
+    const size_t smem = kM8Uint4 * sizeof(uint4) + 128 * kPad * sizeof(uint32_t);
     static bool attr = false;
     if (!attr) { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); attr = true; }
-    encode_kernel<128><<<grid_for(nslabs, 2), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, dt.enc_m4r, ev);
+    encode_kernel<128><<<grid_for(nslabs, 2), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, dt.enc_m8, ev);
   }
   FPM_LAUNCH_CHECK();
 }
@@ -230,11 +249,11 @@ void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaSt
   }
   if (ncols % 1024) throw Error(kInvalid, "decode: column count not 1024-aligned");
   const DeviceTables& dt = device_tables(dev);
-  const size_t smem = kM4RUint4 * sizeof(uint4) + 128 * kPad * sizeof(uint32_t);
+  const size_t smem = kM8Uint4 * sizeof(uint4) + 128 * kPad * sizeof(uint32_t);
   static bool attr = false;
   if (!attr) { FPM_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); attr = true; }
   const uint64_t nslabs = ncols / 32 / kSlabWords;
-  decode_kernel<<<grid_for(nslabs, 2), 256, smem, s>>>(ev, nslabs, ncols / 32, dt.dec_m4r, slice);
+  decode_kernel<<<grid_for(nslabs, 2), 256, smem, s>>>(ev, nslabs, ncols / 32, dt.dec_m8, slice);
   FPM_LAUNCH_CHECK();
 }
 
