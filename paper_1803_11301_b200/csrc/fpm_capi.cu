@@ -166,16 +166,54 @@ struct HostIO {
   cudaStream_t d2h = nullptr;
 };
 
-void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_t b_bits, uint64_t* d_c,
-                    int field, cudaStream_t s, double* stages, const HostIO* io = nullptr) {
-  if (!a_bits || !b_bits) return;
-  if (field == FPM_FIELD_GF64)
-    throw Error(kInvalid, "fp_polymul: the GF(2^64) pipeline is not built on the GPU (use GF(2^128) or auto)");
-  if (field != FPM_FIELD_AUTO && field != FPM_FIELD_GF128) throw Error(kInvalid, "fp_polymul: unknown field choice");
-  const fpm_plan p = plan_mul(a_bits, b_bits, FPM_FIELD_GF128);
+// Field plumbing of run_pipeline<F> (polymul.cpp:78-135) for the two fields built on the GPU.
+struct Gf128Ops {
+  using E = uint4;
+  using Tw = TwiddleSrc;
+  static constexpr int kLiveRows = 64;  // rows >= m/2 of a padded operand are zero
+  static Tw twiddles(int dev, unsigned l) { return make_twiddle_src(dev, l, partition_base(l)); }
+  static unsigned tile_log2(unsigned l) { return fft_tile_log2(l); }
+  static void encode(const uint32_t* p, unsigned l, E* ev, cudaStream_t s) { encode_device_rows(p, l, ev, kLiveRows, s); }
+  static void decode(const E* ev, unsigned l, uint32_t* p, cudaStream_t s) { decode_device(ev, l, p, s); }
+  static void top(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s) {
+    butterfly_top_device(ev, l, T, inv, tw, s);
+  }
+  static void tile(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s) {
+    butterfly_tile_device(ev, l, T, inv, tw, s);
+  }
+  static void fused(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s) {
+    butterfly_tile_fused_device(ea, eb, l, T, tw, s);
+  }
+};
+struct Gf64Ops {
+  using E = uint2;
+  using Tw = TwiddleSrc64;
+  static constexpr int kLiveRows = 32;
+  static Tw twiddles(int dev, unsigned l) { return make_twiddle_src64(dev, l, partition_base64(l)); }
+  static unsigned tile_log2(unsigned l) { return fft64_tile_log2(l); }
+  static void encode(const uint32_t* p, unsigned l, E* ev, cudaStream_t s) { encode64_device(p, l, ev, kLiveRows, s); }
+  static void decode(const E* ev, unsigned l, uint32_t* p, cudaStream_t s) { decode64_device(ev, l, p, s); }
+  static void top(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s) {
+    butterfly64_top_device(ev, l, T, inv, tw, s);
+  }
+  static void tile(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s) {
+    butterfly64_tile_device(ev, l, T, inv, tw, s);
+  }
+  static void fused(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s) {
+    butterfly64_tile_fused_device(ea, eb, l, T, tw, s);
+  }
+};
+
+// fp_polymul on device buffers.  field: FPM_FIELD_GF128, FPM_FIELD_GF64, or FPM_FIELD_AUTO (the
+// reference's plan_mul choice: GF(2^64) whenever it supports the size, polymul.cpp:203-205).
+// Products are field-independent; the field only selects the transform.
+template <class F>
+void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_t b_bits, uint64_t* d_c,
+                  const fpm_plan& p, cudaStream_t s, double* stages, const HostIO* io) {
+  using E = typename F::E;
   const size_t out_bits = a_bits + b_bits - 1;
-  StageClock clk(s, stages);
   const uint64_t out_words = (out_bits + 63) / 64;
+  StageClock clk(s, stages);
   auto wait_operand = [&](int k) {
     if (io && io->ready[k]) FPM_CUDA(cudaStreamWaitEvent(s, io->ready[k], 0));
   };
@@ -188,7 +226,7 @@ void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, siz
     FPM_CUDA(cudaEventDestroy(e));  // released once the wait is satisfied
     FPM_CUDA(cudaMemcpyAsync(io->h_out + w0, d_c + w0, (w1 - w0) * 8, cudaMemcpyDeviceToHost, io->d2h));
   };
-  if (p.l <= 10) {  // whole product in one CTA
+  if (p.n_bits <= ((size_t)1 << 17)) {  // whole product in one CTA (the same product in any field)
     wait_operand(0);
     wait_operand(1);
     clk.mark(kStPointwise);
@@ -197,15 +235,15 @@ void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, siz
     copy_out(0, out_words);
     return;
   }
-  const unsigned l = p.l, T = fft_tile_log2(l);
+  const unsigned l = p.l, T = F::tile_log2(l);
   int dev;
   FPM_CUDA(cudaGetDevice(&dev));
-  const TwiddleSrc tw = make_twiddle_src(dev, l, partition_base(l));
+  const typename F::Tw tw = F::twiddles(dev, l);
   const size_t n = p.n_bits, n_p = p.n_p;
-  DevBuf P(n / 8, s), EA(n_p * 16, s), EB(n_p * 16, s);
+  DevBuf P(n / 8, s), EA(n_p * sizeof(E), s), EB(n_p * sizeof(E), s);
   const uint64_t* xs[2] = {d_a, d_b};
   const size_t xbits[2] = {a_bits, b_bits};
-  uint4* es[2] = {EA.as<uint4>(), EB.as<uint4>()};
+  E* es[2] = {EA.as<E>(), EB.as<E>()};
   for (int k = 0; k < 2; ++k) {
     wait_operand(k);
     clk.mark(kStBasis);
@@ -216,17 +254,17 @@ void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, siz
     if (count < 32) count = 32;
     basis_cvt_device(P.as<uint32_t>(), count, xbits[k], false, s);
     clk.mark(kStEncode);
-    encode_device_rows(P.as<uint32_t>(), l, es[k], 64, s);
+    F::encode(P.as<uint32_t>(), l, es[k], s);
     clk.mark(kStBfly);
-    butterfly_top_device(es[k], l, T, false, tw, s);
-    if (k == 0) butterfly_tile_device(es[k], l, T, false, tw, s);
+    F::top(es[k], l, T, false, tw, s);
+    if (k == 0) F::tile(es[k], l, T, false, tw, s);
   }
   clk.mark(kStPointwise);  // + operand b's bottom T forward and the bottom T inverse layers (fused)
-  butterfly_tile_fused_device(EA.as<uint4>(), EB.as<uint4>(), l, T, tw, s);
+  F::fused(EA.as<E>(), EB.as<E>(), l, T, tw, s);
   clk.mark(kStIBfly);
-  butterfly_top_device(EB.as<uint4>(), l, T, true, tw, s);
+  F::top(EB.as<E>(), l, T, true, tw, s);
   clk.mark(kStDecode);
-  decode_device(EB.as<uint4>(), l, P.as<uint32_t>(), s);
+  F::decode(EB.as<E>(), l, P.as<uint32_t>(), s);
   clk.mark(kStIBasis);
   // Each finished range of the product is trimmed into d_c (and copied out) right away.
   const FinalFn on_final = [&](uint64_t w0, uint64_t w1) {  // 32-bit word range of P
@@ -240,6 +278,14 @@ void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, siz
   };
   basis_cvt_device(P.as<uint32_t>(), n, n, true, s, &on_final);
   clk.finish();
+}
+
+void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_t b_bits, uint64_t* d_c,
+                    int field, cudaStream_t s, double* stages, const HostIO* io = nullptr) {
+  if (!a_bits || !b_bits) return;
+  const fpm_plan p = plan_mul(a_bits, b_bits, field);  // validates the field and the size bound
+  if (p.field_degree == 64) run_pipeline<Gf64Ops>(d_a, a_bits, d_b, b_bits, d_c, p, s, stages, io);
+  else run_pipeline<Gf128Ops>(d_a, a_bits, d_b, b_bits, d_c, p, s, stages, io);
 }
 
 struct DeviceGuard {
@@ -327,6 +373,31 @@ const DeviceTables& device_tables(int dev) {
         }
       c2p[part * 512 + e] = to4(acc);
     }
+  // GF(2^64): G8 tables (gf64.cuh: entry (c, v) copy h at v*16 + 8h + c), C2P tables, rows
+  const FieldTables& f64 = field_tables64();
+  auto u2 = [](uint64_t v) { return make_uint2((uint32_t)v, (uint32_t)(v >> 32)); };
+  std::vector<uint2> enc64(4096), dec64(4096), c2p64(4 * 512), rows64(64), inv64(64);
+  for (int c = 0; c < 8; ++c)
+    for (int v = 0; v < 256; ++v) {
+      uint64_t e = 0, d = 0;
+      for (int j = 0; j < 8; ++j)
+        if (v >> j & 1) { e ^= f64.enc_rows[8 * c + j].lo; d ^= f64.inv_rows[8 * c + j].lo; }
+      for (int h = 0; h < 2; ++h) {
+        enc64[v * 16 + 8 * h + c] = u2(e);
+        dec64[v * 16 + 8 * h + c] = u2(d);
+      }
+    }
+  for (int part = 0; part < 4; ++part)
+    for (int e = 0; e < 512; ++e) {
+      uint64_t acc = 0;
+      for (int k = 0; k < 9; ++k)
+        if (e >> k & 1) {
+          const int idx = 9 * part + k + 1;
+          if (idx < 64) acc ^= f64.cantor[idx].lo;
+        }
+      c2p64[part * 512 + e] = u2(acc);
+    }
+  for (int j = 0; j < 64; ++j) { rows64[j] = u2(f64.enc_rows[j].lo); inv64[j] = u2(f64.inv_rows[j].lo); }
   int prev;
   FPM_CUDA(cudaGetDevice(&prev));
   FPM_CUDA(cudaSetDevice(dev));
@@ -338,6 +409,11 @@ const DeviceTables& device_tables(int dev) {
   up(&t.cantor, cantor); up(&t.enc_rows, rows); up(&t.inv_rows, inv);
   up(&t.enc_m4r, enc); up(&t.dec_m4r, dec); up(&t.c2p, c2p);
   up(&t.enc_m8, enc8); up(&t.dec_m8, dec8);
+  auto up2 = [](uint2** dst, const std::vector<uint2>& v) {
+    FPM_CUDA(cudaMalloc(dst, v.size() * sizeof(uint2)));
+    FPM_CUDA(cudaMemcpy(*dst, v.data(), v.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+  };
+  up2(&t.enc_g8, enc64); up2(&t.dec_g8, dec64); up2(&t.c2p64, c2p64); up2(&t.rows64, rows64); up2(&t.inv64, inv64);
   // Keep freed pool memory cached: the pipeline allocates its scratch per call (reentrant).
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
@@ -413,7 +489,7 @@ fpm_status fpm_polymul(const uint64_t* a, size_t a_bits, const uint64_t* b, size
                        int device, double* stage_seconds) {
   return guard([&] {
     if (!a_bits || !b_bits) return;
-    (void)plan_mul(a_bits, b_bits, field == FPM_FIELD_GF64 ? FPM_FIELD_GF64 : FPM_FIELD_GF128);
+    (void)plan_mul(a_bits, b_bits, field);
     DeviceGuard g(device);
     cudaStream_t s = host_stream(device);
     const size_t wa = (a_bits + 63) / 64, wb = (b_bits + 63) / 64, wc = (a_bits + b_bits - 1 + 63) / 64;

@@ -46,6 +46,12 @@ struct DeviceTables {
   uint4* enc_m8 = nullptr;    // rotated 8-bit tables (gf128.cuh m8 layout) of x*E
   uint4* dec_m8 = nullptr;    // ... of x*E^{-1}
   uint4* c2p = nullptr;       // 4 x 512: part p entry e = C2P(2 * (e << 9p))
+  // GF(2^64) (run_pipeline<gf64>): G8 tables (gf64.cuh layout) of x*E and x*E^{-1}, C2P tables
+  uint2* enc_g8 = nullptr;
+  uint2* dec_g8 = nullptr;
+  uint2* c2p64 = nullptr;     // 4 x 512, as c2p
+  uint2* rows64 = nullptr;    // 64 x r_j
+  uint2* inv64 = nullptr;     // 64 rows of E^{-1}
 };
 
 // Twiddle generator inputs (passed by value as a kernel parameter):
@@ -58,6 +64,12 @@ struct TwiddleSrc {
 };
 // Host: twiddle source for plan_butterflies(l, base) (base in Cantor coordinates).
 TwiddleSrc make_twiddle_src(int device, unsigned l, U128 base);
+struct TwiddleSrc64 {
+  const uint2* c2p;
+  uint2 layer[kMaxLayers];
+};
+TwiddleSrc64 make_twiddle_src64(int device, unsigned l, uint64_t base);
+inline uint64_t partition_base64(unsigned l) { return uint64_t{1} << (l + 32); }  // e_{l+32}
 inline U128 partition_base(unsigned l) {  // make_partition_spec<gf128>(l).base = e_{l+64}
   U128 b;
   if (l + 64 < 64) b.lo = uint64_t{1} << (l + 64); else b.hi = uint64_t{1} << (l + 64 - 64);
@@ -98,6 +110,18 @@ void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, cons
 // Fused: forward layers [0, T) of b's tiles, pointwise * a, inverse layers [0, T).
 void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
                                  cudaStream_t s);
+
+// GF(2^64) stages (k_fft64.cu, k_codec.cu): 64-row partition matrix, 8-byte elements.
+unsigned fft64_tile_log2(unsigned l);
+void butterfly64_device(uint2* ev, unsigned l, uint64_t base, bool inverse, cudaStream_t s);
+void butterfly64_top_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s);
+void butterfly64_tile_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s);
+void butterfly64_tile_fused_device(const uint2* ea, uint2* eb, unsigned l, unsigned T, const TwiddleSrc64& tw,
+                                   cudaStream_t s);
+void pointwise64_device(const uint2* u, const uint2* v, uint2* out, size_t n, cudaStream_t s);
+// rows_live = 32: rows >= 32 known zero (pipeline operands); 64: general.
+void encode64_device(const uint32_t* poly, unsigned l, uint2* ev, int rows_live, cudaStream_t s);
+void decode64_device(const uint2* ev, unsigned l, uint32_t* poly, cudaStream_t s);
 
 // Whole small products in one CTA each (k_batch.cu); n_bits = padded product length <= 2^17.
 void polymul_batch_device(const uint64_t* a, size_t a_bits, size_t a_stride_words,

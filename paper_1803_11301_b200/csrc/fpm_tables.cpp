@@ -1,4 +1,4 @@
-// fpm_tables.cpp -- host construction of the GF(2^128) Cantor basis and encode matrices.
+// fpm_tables.cpp -- host construction of the GF(2^128) / GF(2^64) Cantor bases and encode matrices.
 // Restates proj/src/cantor.cpp:103-134 and proj/src/encode.cpp:52-70 (init-time only).
 #include "fpm_tables.h"
 
@@ -18,18 +18,18 @@ inline U128 x(U128 a, U128 b) { return {a.lo ^ b.lo, a.hi ^ b.hi}; }
 inline bool nz(U128 a) { return a.lo | a.hi; }
 inline bool eq(U128 a, U128 b) { return a.lo == b.lo && a.hi == b.hi; }
 
-U128 row_mul(U128 v, const U128* rows) {
+U128 row_mul(U128 v, const U128* rows, unsigned m = 128) {
   U128 acc;
-  for (unsigned j = 0; j < 128; ++j)
+  for (unsigned j = 0; j < m; ++j)
     if (bit(v, j)) acc = x(acc, rows[j]);
   return acc;
 }
 
 // x * rows = target over GF(2) (row-echelon; bitmat.hpp:79-111).
-bool solve(const U128* rows, U128 target, U128* out) {
+bool solve(const U128* rows, U128 target, U128* out, unsigned m) {
   U128 ech[128], tag[128];
   unsigned lead[128], ne = 0;
-  for (unsigned i = 0; i < 128; ++i) {
+  for (unsigned i = 0; i < m; ++i) {
     U128 r = rows[i], t = unit(i);
     for (unsigned j = 0; j < ne; ++j)
       if (bit(r, lead[j])) { r = x(r, ech[j]); t = x(t, tag[j]); }
@@ -47,45 +47,48 @@ bool solve(const U128* rows, U128 target, U128* out) {
   return true;
 }
 
-bool invert(const U128* rows, U128* inv_out) {  // bitmat.hpp:55-74
+bool invert(const U128* rows, U128* inv_out, unsigned m) {  // bitmat.hpp:55-74
   U128 a[128], inv[128];
-  for (unsigned i = 0; i < 128; ++i) { a[i] = rows[i]; inv[i] = unit(i); }
-  for (unsigned col = 0; col < 128; ++col) {
+  for (unsigned i = 0; i < m; ++i) { a[i] = rows[i]; inv[i] = unit(i); }
+  for (unsigned col = 0; col < m; ++col) {
     unsigned piv = col;
-    while (piv < 128 && !bit(a[piv], col)) ++piv;
-    if (piv == 128) return false;
+    while (piv < m && !bit(a[piv], col)) ++piv;
+    if (piv == m) return false;
     std::swap(a[col], a[piv]);
     std::swap(inv[col], inv[piv]);
-    for (unsigned r = 0; r < 128; ++r)
+    for (unsigned r = 0; r < m; ++r)
       if (r != col && bit(a[r], col)) { a[r] = x(a[r], a[col]); inv[r] = x(inv[r], inv[col]); }
   }
-  for (unsigned i = 0; i < 128; ++i) inv_out[i] = inv[i];
+  for (unsigned i = 0; i < m; ++i) inv_out[i] = inv[i];
   return true;
 }
 
-void build(FieldTables& t) {
+// Generic over the field degree m (128: gf128, 64: gf64; cantor.cpp and encode.cpp are templates).
+void build(FieldTables& t, unsigned m) {
+  auto mul = [m](U128 a, U128 b) { return m == 128 ? host_gf128_mul(a, b) : host_gf64_mul(a, b); };
   // Artin-Schreier map y -> y^2 + y, rows in polynomial representation.
   U128 artin[128];
-  for (unsigned k = 0; k < 128; ++k) artin[k] = x(host_gf128_mul(unit(k), unit(k)), unit(k));
+  for (unsigned k = 0; k < m; ++k) artin[k] = x(mul(unit(k), unit(k)), unit(k));
   t.cantor[0] = unit(0);
-  for (unsigned i = 1; i < 128; ++i) {
+  for (unsigned i = 1; i < m; ++i) {
     U128 y;
-    if (!solve(artin, t.cantor[i - 1], &y))
+    if (!solve(artin, t.cantor[i - 1], &y, m))
       throw std::runtime_error("CantorField: Artin-Schreier equation has no solution (wrong modulus?)");
     y.lo &= ~uint64_t{1};  // of the roots {y, y+1} keep the one with bit 0 clear
-    if (!eq(x(host_gf128_mul(y, y), y), t.cantor[i - 1]))
+    if (!eq(x(mul(y, y), y), t.cantor[i - 1]))
       throw std::runtime_error("CantorField: basis recurrence check failed");
     t.cantor[i] = y;
   }
   U128 probe[128];
-  if (!invert(t.cantor, probe)) throw std::runtime_error("CantorField: basis-change matrix not invertible");
-  for (unsigned j = 0; j < 128; ++j) {
+  if (!invert(t.cantor, probe, m)) throw std::runtime_error("CantorField: basis-change matrix not invertible");
+  const unsigned logm = m == 128 ? 7 : 6;
+  for (unsigned j = 0; j < m; ++j) {  // r_j = prod over bits k of j of v_{m/2-k} (encode.cpp:60-66)
     U128 r = unit(0);
-    for (unsigned k = 0; k < 7; ++k)
-      if ((j >> k) & 1) r = host_gf128_mul(r, t.cantor[64 - k]);
+    for (unsigned k = 0; k < logm; ++k)
+      if ((j >> k) & 1) r = mul(r, t.cantor[m / 2 - k]);
     t.enc_rows[j] = r;
   }
-  if (!invert(t.enc_rows, t.inv_rows))
+  if (!invert(t.enc_rows, t.inv_rows, m))
     throw std::runtime_error("EncodeMatrix: matrix is singular (field construction bug)");
 }
 
@@ -103,12 +106,37 @@ U128 host_gf128_mul(U128 a, U128 b) {
   return acc;
 }
 
+U128 host_gf64_mul(U128 a, U128 b) {
+  // bit-serial modulo x^64 + x^4 + x^3 + x + 1 (gf.hpp:105-113); only the lo words are used
+  uint64_t acc = 0;
+  for (int i = 63; i >= 0; --i) {
+    const uint64_t carry = acc >> 63;
+    acc = (acc << 1) ^ (carry ? 0x1Bu : 0u);
+    if ((b.lo >> i) & 1) acc ^= a.lo;
+  }
+  U128 r;
+  r.lo = acc;
+  return r;
+}
+
 U128 host_cantor_to_poly(const FieldTables& t, U128 c) { return row_mul(c, t.cantor); }
+U128 host_cantor_to_poly64(const FieldTables& t, uint64_t c) {
+  U128 v;
+  v.lo = c;
+  return row_mul(v, t.cantor, 64);
+}
 
 const FieldTables& field_tables() {
   static FieldTables tables;
   static std::once_flag once;
-  std::call_once(once, [] { build(tables); });
+  std::call_once(once, [] { build(tables, 128); });
+  return tables;
+}
+
+const FieldTables& field_tables64() {
+  static FieldTables tables;
+  static std::once_flag once;
+  std::call_once(once, [] { build(tables, 64); });
   return tables;
 }
 

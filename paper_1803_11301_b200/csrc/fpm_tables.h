@@ -1,4 +1,4 @@
-// fpm_tables.h -- host-side field tables for the GF(2^128) Frobenius-partition pipeline.
+// fpm_tables.h -- host-side field tables for the GF(2^128) / GF(2^64) Frobenius-partition pipelines.
 //
 // Product code (not the oracle): the CUDA library builds its own tables at first use, mirroring
 // the reference singletons CantorField<gf128> (proj/src/cantor.cpp:103-140) and
@@ -22,9 +22,13 @@ struct FieldTables {
 // Builds (once, thread-safe) and returns the tables; throws std::runtime_error on the same
 // construction failures the reference reports (cantor.cpp:108-133, encode.cpp:69-70).
 const FieldTables& field_tables();
+// GF(2^64) (CantorField<gf64>, EncodeMatrix<gf64>): entries 0..63 used, hi words zero.
+const FieldTables& field_tables64();
 
 U128 host_gf128_mul(U128 a, U128 b);
+U128 host_gf64_mul(U128 a, U128 b);                      // lo words only
 U128 host_cantor_to_poly(const FieldTables& t, U128 c);  // bitmat.hpp:29-35
+U128 host_cantor_to_poly64(const FieldTables& t, uint64_t c);
 
 // Basis-conversion schedule (basis_convert.cpp:53-67) with the overflow-safe digit size
 // (the reference loops forever for arrays of >= 2^33 bits).

@@ -14,6 +14,7 @@
 
 #include "fpm_internal.h"
 #include "gf128.cuh"
+#include "gf64.cuh"
 
 namespace fpm {
 namespace {
@@ -169,6 +170,113 @@ __global__ void decode_small_kernel(const uint4* __restrict__ ev, uint64_t n_p, 
   poly[wi] = out;
 }
 
+// ------------------------------------------------------------------ GF(2^64) (m = 64)
+// Element i of EvalVec<gf64> is x_i * E with x_i = (a_{j*n_p+i})_{j<64} (encode.cpp:165-193 at
+// m = 64).  Same slab scheme as above: ROWS (32: pipeline operands, rows >= 32 zero; 64: general)
+// rows x 1024 elements, warp transposes, then x*E by 4 or 8 G8 lookups (gf64.cuh layout).
+template <int ROWS>
+__global__ void __launch_bounds__(256) encode64_kernel(const uint32_t* __restrict__ poly, uint64_t row_words,
+                                                       uint64_t nslabs, const uint2* __restrict__ tab_g,
+                                                       uint2* __restrict__ ev) {
+  extern __shared__ uint2 smem2[];
+  uint2* tab = smem2;                                               // kG8Uint2
+  uint32_t* slab = reinterpret_cast<uint32_t*>(smem2 + kG8Uint2);  // ROWS x kPad
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < kG8Uint2; i += blockDim.x) tab[i] = tab_g[i];
+  const Transpose32 tr(lane);
+  const int q = lane & 7, h8 = lane & 8;
+  for (uint64_t sl = blockIdx.x; sl < nslabs; sl += gridDim.x) {
+    const uint64_t w0 = sl * kSlabWords;
+    __syncthreads();
+    for (int i = tid; i < ROWS * kSlabWords; i += blockDim.x) {
+      const int r = i / kSlabWords, c = i % kSlabWords;
+      slab[r * kPad + c] = poly[(uint64_t)r * row_words + w0 + c];
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int k = 0; k < kSlabWords / 8; ++k) {
+      const int col = warp * (kSlabWords / 8) + k;
+      uint2 x;
+      x.x = tr(slab[lane * kPad + col]);
+      x.y = ROWS == 64 ? tr(slab[(32 + lane) * kPad + col]) : 0u;
+      uint2 acc0 = make_uint2(0, 0), acc1 = make_uint2(0, 0);
+      constexpr int kChunks = ROWS / 8;
+#pragma unroll
+      for (int kk = 0; kk < kChunks; kk += 2) {
+        const int c0 = (kk + q) % kChunks, c1 = (kk + 1 + q) % kChunks;
+        const uint32_t b0 = __byte_perm(c0 < 4 ? x.x : x.y, 0, 0x4440u | (uint32_t)(c0 & 3));
+        const uint32_t b1 = __byte_perm(c1 < 4 ? x.x : x.y, 0, 0x4440u | (uint32_t)(c1 & 3));
+        acc0 = x2(acc0, tab[b0 * 16 + h8 + c0]);
+        acc1 = x2(acc1, tab[b1 * 16 + h8 + c1]);
+      }
+      ev[(w0 + col) * 32 + lane] = x2(acc0, acc1);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) decode64_kernel(const uint2* __restrict__ ev, uint64_t nslabs,
+                                                       uint64_t row_words, const uint2* __restrict__ tab_g,
+                                                       uint32_t* __restrict__ poly) {
+  extern __shared__ uint2 smem2[];
+  uint2* tab = smem2;
+  uint32_t* slab = reinterpret_cast<uint32_t*>(smem2 + kG8Uint2);  // 64 x kPad
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < kG8Uint2; i += blockDim.x) tab[i] = tab_g[i];
+  const Transpose32 tr(lane);
+  __syncthreads();
+  for (uint64_t sl = blockIdx.x; sl < nslabs; sl += gridDim.x) {
+    const uint64_t w0 = sl * kSlabWords;
+#pragma unroll 1
+    for (int k = 0; k < kSlabWords / 8; ++k) {
+      const int col = warp * (kSlabWords / 8) + k;
+      const uint2 y = g8_mul(tab, ev[(w0 + col) * 32 + lane], lane);
+      slab[lane * kPad + col] = tr(y.x);
+      slab[(32 + lane) * kPad + col] = tr(y.y);
+    }
+    __syncthreads();
+    for (int i = tid; i < 64 * kSlabWords; i += blockDim.x) {
+      const int r = i / kSlabWords, c = i % kSlabWords;
+      poly[(uint64_t)r * row_words + w0 + c] = slab[r * kPad + c];
+    }
+    __syncthreads();
+  }
+}
+
+// Tiny shapes: one thread per element / output word, direct row products.
+__global__ void encode64_small_kernel(const uint32_t* __restrict__ poly, uint64_t n_p, const uint2* __restrict__ rows,
+                                      uint2* __restrict__ ev) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_p) return;
+  uint2 acc = make_uint2(0, 0);
+  for (int j = 0; j < 64; ++j) {
+    const uint64_t k = (uint64_t)j * n_p + i;
+    if ((poly[k >> 5] >> (k & 31)) & 1u) acc = x2(acc, rows[j]);
+  }
+  ev[i] = acc;
+}
+
+__global__ void decode64_small_kernel(const uint2* __restrict__ ev, uint64_t n_p, const uint2* __restrict__ inv_rows,
+                                      uint32_t* __restrict__ poly) {
+  const uint64_t wi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nwords = (64 * n_p + 31) / 32;
+  if (wi >= nwords) return;
+  uint32_t out = 0;
+  for (int b = 0; b < 32; ++b) {
+    const uint64_t k = wi * 32 + b;
+    if (k >= 64 * n_p) break;
+    const uint64_t j = k / n_p, i = k % n_p;
+    const uint64_t f = ev[i].x | ((uint64_t)ev[i].y << 32);
+    uint32_t acc = 0;
+    for (int t = 0; t < 64; ++t)
+      if ((f >> t) & 1u) {
+        const uint64_t r = inv_rows[t].x | ((uint64_t)inv_rows[t].y << 32);
+        acc ^= (uint32_t)(r >> j) & 1u;
+      }
+    out |= acc << b;
+  }
+  poly[wi] = out;
+}
+
 // Device copies of the plain row tables for the tiny-shape kernels.
 struct RowTables {
   uint4* rows = nullptr;
@@ -254,6 +362,44 @@ void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaSt
   if (!attr) { FPM_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); attr = true; }
   const uint64_t nslabs = ncols / 32 / kSlabWords;
   decode_kernel<<<grid_for(nslabs, 2), 256, smem, s>>>(ev, nslabs, ncols / 32, dt.dec_m8, slice);
+  FPM_LAUNCH_CHECK();
+}
+
+void encode64_device(const uint32_t* poly, unsigned l, uint2* ev, int rows_live, cudaStream_t s) {
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  const DeviceTables& dt = device_tables(dev);
+  const uint64_t n_p = (uint64_t)1 << l;
+  if (n_p < 1024) {
+    encode64_small_kernel<<<(unsigned)((n_p + 127) / 128), 128, 0, s>>>(poly, n_p, dt.rows64, ev);
+    FPM_LAUNCH_CHECK();
+    return;
+  }
+  const uint64_t nslabs = n_p / 32 / kSlabWords;
+  if (rows_live <= 32) {
+    const size_t smem = kG8Uint2 * sizeof(uint2) + 32 * kPad * sizeof(uint32_t);
+    encode64_kernel<32><<<grid_for(nslabs, 4), 256, smem, s>>>(poly, n_p / 32, nslabs, dt.enc_g8, ev);
+  } else {
+    const size_t smem = kG8Uint2 * sizeof(uint2) + 64 * kPad * sizeof(uint32_t);
+    encode64_kernel<64><<<grid_for(nslabs, 4), 256, smem, s>>>(poly, n_p / 32, nslabs, dt.enc_g8, ev);
+  }
+  FPM_LAUNCH_CHECK();
+}
+
+void decode64_device(const uint2* ev, unsigned l, uint32_t* poly, cudaStream_t s) {
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  const DeviceTables& dt = device_tables(dev);
+  const uint64_t n_p = (uint64_t)1 << l;
+  if (n_p < 1024) {
+    const uint64_t nwords = (64 * n_p + 31) / 32;
+    decode64_small_kernel<<<(unsigned)((nwords + 127) / 128), 128, 0, s>>>(ev, n_p, dt.inv64, poly);
+    FPM_LAUNCH_CHECK();
+    return;
+  }
+  const uint64_t nslabs = n_p / 32 / kSlabWords;
+  const size_t smem = kG8Uint2 * sizeof(uint2) + 64 * kPad * sizeof(uint32_t);
+  decode64_kernel<<<grid_for(nslabs, 4), 256, smem, s>>>(ev, nslabs, n_p / 32, dt.dec_g8, poly);
   FPM_LAUNCH_CHECK();
 }
 

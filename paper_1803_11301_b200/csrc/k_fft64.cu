@@ -1,0 +1,389 @@
+// k_fft64.cu -- LCH butterflies and pointwise products over GF(2^64) on sm_100a: the reference's
+// auto-field pipeline (plan_mul picks m = 64 whenever the field supports the size, polymul.cpp:
+// 203-205; run_pipeline<gf64>, polymul.cpp:78-135, 235).
+//
+// Same schedule as k_fft.cu (see there for the layer/twiddle algebra):
+//     w(i, b) = C2P((base >> i) ^ 2b) = layer[i] ^ C2P(2b),  base = e_{l+32}  (butterfly.cpp:45-49)
+// with 8-byte elements and 32 KiB G8 twiddle tables (gf64.cuh):
+//  * fft64_top4_kernel: layers (i+1, i) per HBM round trip, three G8 tables per CTA.
+//  * fft64_top_kernel:  one layer (odd top-layer count).
+//  * fft64_tile_kernel / fft64_tile_fused_kernel: layers [0, T) in shared-memory tiles (generic
+//    gf64_mul below layer 8, one G8 table at a time above); the fused one also does the pointwise
+//    product with operand a and the inverse tile layers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "fpm_internal.h"
+#include "gf64.cuh"
+
+namespace fpm {
+namespace {
+
+constexpr int kTileMax64 = 12;  // 2^12 x 8 B = 32 KiB tile
+
+__device__ __forceinline__ uint2 c2p2_64(const uint2* __restrict__ c2p, uint64_t b) {  // C2P(2b)
+  uint2 r = c2p[b & 511];
+  if (b >> 9) r = x2(r, c2p[512 + ((b >> 9) & 511)]);
+  if (b >> 18) r = x2(r, c2p[1024 + ((b >> 18) & 511)]);
+  if (b >> 27) r = x2(r, c2p[1536 + ((b >> 27) & 511)]);
+  return r;
+}
+
+__device__ __forceinline__ uint2 twiddle64(const TwiddleSrc64& tw, unsigned i, uint64_t b) {
+  return x2(tw.layer[i], c2p2_64(tw.c2p, b));
+}
+
+// ------------------------------------------------------------------ one top layer
+template <bool INV>
+__global__ void __launch_bounds__(256) fft64_top_kernel(uint2* __restrict__ ev, unsigned i, int ppc, TwiddleSrc64 tw) {
+  extern __shared__ uint2 tab64[];  // kG8Uint2
+  __shared__ uint2 rows[kG8Rows];
+  const uint64_t half = (uint64_t)1 << i;
+  const uint64_t pair0 = (uint64_t)blockIdx.x * ppc;  // ppc <= 2^i: a CTA stays inside one block
+  const uint64_t b = pair0 >> i;
+  g8_build(tab64, rows, twiddle64(tw, i, b), threadIdx.x);
+  const int lane = threadIdx.x & 31;
+  uint2* base = ev + (b << (i + 1));
+#pragma unroll 4
+  for (int k = threadIdx.x; k < ppc; k += blockDim.x) {
+    const uint64_t j = (pair0 & (half - 1)) + k;
+    uint2 u0 = base[j], u1 = base[j + half];
+    if (!INV) {
+      u0 = x2(u0, g8_mul(tab64, u1, lane));
+      u1 = x2(u1, u0);
+    } else {
+      u1 = x2(u1, u0);
+      u0 = x2(u0, g8_mul(tab64, u1, lane));
+    }
+    base[j] = u0;
+    base[j + half] = u1;
+  }
+}
+
+// ------------------------------------------------------------------ two top layers per pass
+// 384 threads (three 128-thread table builders), two CTAs per SM: one CTA's table build overlaps
+// the other's streaming.
+constexpr int kTop4Threads64 = 384;
+constexpr size_t kTop4Smem64 = (3 * (size_t)kG8Uint2 + 3 * kG8Rows) * sizeof(uint2);
+
+template <bool INV>
+__global__ void __launch_bounds__(kTop4Threads64, 2) fft64_top4_kernel(uint2* __restrict__ ev, unsigned i, int qpc,
+                                                                       TwiddleSrc64 tw) {
+  extern __shared__ uint2 sm64[];
+  uint2* t1 = sm64;                    // w(i+1, B)
+  uint2* t0a = sm64 + kG8Uint2;        // w(i, 2B)
+  uint2* t0b = sm64 + 2 * kG8Uint2;    // w(i, 2B+1)
+  uint2* rows = sm64 + 3 * kG8Uint2;   // 3 x kG8Rows
+  const uint64_t h = (uint64_t)1 << i;
+  const uint64_t quad0 = (uint64_t)blockIdx.x * qpc;  // qpc <= h
+  const uint64_t B = quad0 >> i;
+  const int tid = threadIdx.x, grp = tid >> 7, lt = tid & 127;
+  {
+    const uint2 w = grp == 0 ? twiddle64(tw, i + 1, B) : twiddle64(tw, i, 2 * B + (grp - 1));
+    uint2* tab = sm64 + grp * kG8Uint2;
+    uint2* rs = rows + grp * kG8Rows;
+    if (lt < 64) rs[lt + (lt >> 3)] = gf64_mul_xk(w, (unsigned)lt);
+    __syncthreads();
+    const int c = lt & 7;
+    uint2 r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = rs[9 * c + j];
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int sv = (lt >> 3) + 16 * half;
+      uint2 t[8];
+      t[0] = make_uint2(0, 0);
+#pragma unroll
+      for (int j = 0; j < 5; ++j)
+        if (sv >> j & 1) t[0] = x2(t[0], r[3 + j]);
+#pragma unroll
+      for (int u = 1; u < 8; ++u) t[u] = x2(t[u & (u - 1)], r[(u & 1) ? 0 : (u & 2) ? 1 : 2]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        uint2* e = tab + (8 * sv + u) * 16 + c;
+        e[0] = t[u];
+        e[8] = t[u];
+      }
+    }
+    __syncthreads();
+  }
+  const int lane = tid & 31;
+  uint2* base = ev + (B << (i + 2));
+  const uint64_t j0 = quad0 & (h - 1);
+  // Each thread transforms two adjacent quads with 16-byte accesses (512 B per warp per quarter
+  // stream: the eight streams of a CTA stay DRAM-page friendly).
+  auto bfly = [&](uint2& a0, uint2& a1, uint2& a2, uint2& a3) {
+    if (!INV) {
+      a0 = x2(a0, g8_mul(t1, a2, lane));
+      a1 = x2(a1, g8_mul(t1, a3, lane));
+      a2 = x2(a2, a0);
+      a3 = x2(a3, a1);
+      a0 = x2(a0, g8_mul(t0a, a1, lane));
+      a2 = x2(a2, g8_mul(t0b, a3, lane));
+      a1 = x2(a1, a0);
+      a3 = x2(a3, a2);
+    } else {
+      a1 = x2(a1, a0);
+      a3 = x2(a3, a2);
+      a0 = x2(a0, g8_mul(t0a, a1, lane));
+      a2 = x2(a2, g8_mul(t0b, a3, lane));
+      a2 = x2(a2, a0);
+      a3 = x2(a3, a1);
+      a0 = x2(a0, g8_mul(t1, a2, lane));
+      a1 = x2(a1, g8_mul(t1, a3, lane));
+    }
+  };
+#pragma unroll 1
+  for (int k = 2 * tid; k < qpc; k += 2 * kTop4Threads64) {
+    uint4* p = reinterpret_cast<uint4*>(base + j0 + k);
+    const uint64_t h2 = h / 2;
+    uint4 v0 = p[0], v1 = p[h2], v2 = p[2 * h2], v3 = p[3 * h2];
+    uint2 a0 = make_uint2(v0.x, v0.y), a1 = make_uint2(v1.x, v1.y), a2 = make_uint2(v2.x, v2.y),
+          a3 = make_uint2(v3.x, v3.y);
+    uint2 b0 = make_uint2(v0.z, v0.w), b1 = make_uint2(v1.z, v1.w), b2 = make_uint2(v2.z, v2.w),
+          b3 = make_uint2(v3.z, v3.w);
+    bfly(a0, a1, a2, a3);
+    bfly(b0, b1, b2, b3);
+    p[0] = make_uint4(a0.x, a0.y, b0.x, b0.y);
+    p[h2] = make_uint4(a1.x, a1.y, b1.x, b1.y);
+    p[2 * h2] = make_uint4(a2.x, a2.y, b2.x, b2.y);
+    p[3 * h2] = make_uint4(a3.x, a3.y, b3.x, b3.y);
+  }
+}
+
+// ------------------------------------------------------------------ tile layers (i < T)
+constexpr unsigned kTabLayer64 = 8;  // layers >= 8 of a 256-thread tile: <= 8 twiddles, G8 tables
+template <bool INV>
+__device__ __forceinline__ void tile_layers64(uint2* __restrict__ s, unsigned T, uint64_t tile_idx,
+                                              const TwiddleSrc64& tw, uint2* __restrict__ tab) {
+  const int npairs = 1 << (T - 1);
+  const int lane = threadIdx.x & 31;
+  for (unsigned step = 0; step < T; ++step) {
+    const unsigned i = INV ? step : T - 1 - step;
+    const uint64_t bhi = tile_idx << (T - 1 - i);
+    const uint2 Z = twiddle64(tw, i, bhi);  // w = Z ^ C2P(2 blk) (disjoint bit ranges, C2P linear)
+    if (tab && i >= kTabLayer64) {
+      for (int blk = 0; blk < (npairs >> i); ++blk) {
+        g8_build(tab, tab + kG8Uint2, x2(Z, c2p2_64(tw.c2p, (uint64_t)blk)), threadIdx.x);
+        for (int j = threadIdx.x; j < (1 << i); j += blockDim.x) {
+          const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+          uint2 u0 = s[i0], u1 = s[i1];
+          if (!INV) {
+            u0 = x2(u0, g8_mul(tab, u1, lane));
+            u1 = x2(u1, u0);
+          } else {
+            u1 = x2(u1, u0);
+            u0 = x2(u0, g8_mul(tab, u1, lane));
+          }
+          s[i0] = u0;
+          s[i1] = u1;
+        }
+      }
+      __syncthreads();
+      continue;
+    }
+    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+      const int blk = p >> i, j = p & ((1 << i) - 1);
+      const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+      const uint2 w = x2(Z, c2p2_64(tw.c2p, (uint64_t)blk));
+      uint2 u0 = s[i0], u1 = s[i1];
+      if (!INV) {
+        u0 = x2(u0, gf64_mul(w, u1));
+        u1 = x2(u1, u0);
+      } else {
+        u1 = x2(u1, u0);
+        u0 = x2(u0, gf64_mul(w, u1));
+      }
+      s[i0] = u0;
+      s[i1] = u1;
+    }
+    __syncthreads();
+  }
+}
+
+template <bool INV>
+__global__ void __launch_bounds__(256) fft64_tile_kernel(uint2* __restrict__ ev, unsigned l, unsigned T,
+                                                         TwiddleSrc64 tw, int use_tab) {
+  extern __shared__ uint2 s64[];
+  const int n = 1 << T;
+  uint2* tab = use_tab ? s64 + n : nullptr;
+  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint2* g = ev + (t << T);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) s64[k] = g[k];
+    __syncthreads();
+    tile_layers64<INV>(s64, T, t, tw, tab);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) g[k] = s64[k];
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) fft64_tile_fused_kernel(const uint2* __restrict__ ea, uint2* __restrict__ eb,
+                                                               unsigned l, unsigned T, TwiddleSrc64 tw, int use_tab) {
+  extern __shared__ uint2 s64[];
+  const int n = 1 << T;
+  uint2* tab = use_tab ? s64 + n : nullptr;
+  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint2* g = eb + (t << T);
+    const uint2* ga = ea + (t << T);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) s64[k] = g[k];
+    __syncthreads();
+    tile_layers64<false>(s64, T, t, tw, tab);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) s64[k] = gf64_mul(ga[k], s64[k]);
+    __syncthreads();
+    tile_layers64<true>(s64, T, t, tw, tab);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) g[k] = s64[k];
+    __syncthreads();
+  }
+}
+
+__global__ void pointwise64_kernel(const uint2* __restrict__ u, const uint2* __restrict__ v, uint2* __restrict__ out,
+                                   uint64_t n) {
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
+    out[k] = gf64_mul(u[k], v[k]);
+}
+
+int sms64() {
+  int dev, n;
+  FPM_CUDA(cudaGetDevice(&dev));
+  FPM_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  return n;
+}
+
+template <class K>
+void set_smem64(K kernel, size_t bytes) {
+  FPM_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+int tile_threads64(unsigned T) { return T >= 9 ? 256 : std::max(32, 1 << (T - 1)); }
+
+struct TileCfg64 {
+  int threads, use_tab, grid;
+  size_t smem;
+};
+TileCfg64 tile_cfg64(unsigned l, unsigned T) {
+  TileCfg64 c;
+  c.threads = tile_threads64(T);
+  c.use_tab = T > kTabLayer64 && c.threads == 256;
+  c.smem = ((size_t)1 << T) * sizeof(uint2) + (c.use_tab ? (kG8Uint2 + kG8Rows) * sizeof(uint2) : 0);
+  const int per_sm = c.use_tab ? 3 : 768 / c.threads;
+  c.grid = (int)std::min<uint64_t>(((uint64_t)1 << l) >> T, (uint64_t)sms64() * per_sm);
+  return c;
+}
+constexpr size_t kTileSmemMax64 = ((size_t)1 << kTileMax64) * sizeof(uint2) + (kG8Uint2 + kG8Rows) * sizeof(uint2);
+
+}  // namespace
+
+// Tile depth for the GF(2^64) transforms (tuning override FPM_TILE_LOG2_64).
+unsigned fft64_tile_log2(unsigned l) {
+  static const int knob = [] {
+    const char* e = std::getenv("FPM_TILE_LOG2_64");
+    return e ? std::max(8, std::min(kTileMax64, std::atoi(e))) : 0;
+  }();
+  const unsigned cap = knob ? (unsigned)knob : (l >= 20 ? 12u : l >= 18 ? 10u : 8u);
+  return l < cap ? l : cap;
+}
+
+TwiddleSrc64 make_twiddle_src64(int device, unsigned l, uint64_t base) {
+  if (l > (unsigned)kMaxLayers) throw Error(kInvalid, "butterfly: too many layers");
+  TwiddleSrc64 tw{};
+  tw.c2p = device_tables(device).c2p64;
+  const FieldTables& ft = field_tables64();
+  for (unsigned i = 0; i < l; ++i) {
+    const U128 p = host_cantor_to_poly64(ft, base >> i);
+    tw.layer[i] = make_uint2((uint32_t)p.lo, (uint32_t)(p.lo >> 32));
+  }
+  return tw;
+}
+
+void butterfly64_top_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s) {
+  if (l <= T) return;
+  const size_t smem = kG8Uint2 * sizeof(uint2);
+  static bool attr = false;
+  if (!attr) {
+    set_smem64(fft64_top_kernel<false>, smem);
+    set_smem64(fft64_top_kernel<true>, smem);
+    set_smem64(fft64_top4_kernel<false>, kTop4Smem64);
+    set_smem64(fft64_top4_kernel<true>, kTop4Smem64);
+    attr = true;
+  }
+  if (T < 8) throw Error(kInvalid, "butterfly_top: layer too small for the table layer kernel");
+  const uint64_t pairs = ((uint64_t)1 << l) / 2;
+  uint64_t ppc = 4096;
+  while (ppc > 256 && pairs / ppc < (uint64_t)sms64() * 2) ppc /= 2;
+  auto radix2 = [&](unsigned i) {
+    const uint64_t p = std::min<uint64_t>(ppc, (uint64_t)1 << i);
+    if (!inverse) fft64_top_kernel<false><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, i, (int)p, tw);
+    else fft64_top_kernel<true><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, i, (int)p, tw);
+    FPM_LAUNCH_CHECK();
+  };
+  const uint64_t quads = ((uint64_t)1 << l) / 4;
+  uint64_t qpc = 8192;
+  while (qpc > 1024 && quads / qpc < (uint64_t)sms64() * 4) qpc /= 2;
+  auto radix4 = [&](unsigned i) {
+    const unsigned q = (unsigned)std::min<uint64_t>(qpc, (uint64_t)1 << i);
+    if (!inverse)
+      fft64_top4_kernel<false><<<(unsigned)(quads / q), kTop4Threads64, kTop4Smem64, s>>>(ev, i, (int)q, tw);
+    else
+      fft64_top4_kernel<true><<<(unsigned)(quads / q), kTop4Threads64, kTop4Smem64, s>>>(ev, i, (int)q, tw);
+    FPM_LAUNCH_CHECK();
+  };
+  const unsigned n = l - T;
+  const bool odd = n & 1;
+  if (!inverse) {
+    for (unsigned k = 0; k + 1 < n; k += 2) radix4(l - 2 - k);
+    if (odd) radix2(T);
+  } else {
+    if (odd) radix2(T);
+    for (unsigned i = T + (odd ? 1 : 0); i + 1 < l; i += 2) radix4(i);
+  }
+}
+
+void butterfly64_tile_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s) {
+  if (T == 0) return;
+  static bool attr = false;
+  if (!attr) {
+    set_smem64(fft64_tile_kernel<false>, kTileSmemMax64);
+    set_smem64(fft64_tile_kernel<true>, kTileSmemMax64);
+    attr = true;
+  }
+  const TileCfg64 c = tile_cfg64(l, T);
+  if (!inverse) fft64_tile_kernel<false><<<c.grid, c.threads, c.smem, s>>>(ev, l, T, tw, c.use_tab);
+  else fft64_tile_kernel<true><<<c.grid, c.threads, c.smem, s>>>(ev, l, T, tw, c.use_tab);
+  FPM_LAUNCH_CHECK();
+}
+
+void butterfly64_tile_fused_device(const uint2* ea, uint2* eb, unsigned l, unsigned T, const TwiddleSrc64& tw,
+                                   cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) { set_smem64(fft64_tile_fused_kernel, kTileSmemMax64); attr = true; }
+  const TileCfg64 c = tile_cfg64(l, T);
+  fft64_tile_fused_kernel<<<c.grid, c.threads, c.smem, s>>>(ea, eb, l, T, tw, c.use_tab);
+  FPM_LAUNCH_CHECK();
+}
+
+void butterfly64_device(uint2* ev, unsigned l, uint64_t base, bool inverse, cudaStream_t s) {
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  const TwiddleSrc64 tw = make_twiddle_src64(dev, l, base);
+  const unsigned T = fft64_tile_log2(l);
+  if (!inverse) {
+    butterfly64_top_device(ev, l, T, false, tw, s);
+    butterfly64_tile_device(ev, l, T, false, tw, s);
+  } else {
+    butterfly64_tile_device(ev, l, T, true, tw, s);
+    butterfly64_top_device(ev, l, T, true, tw, s);
+  }
+}
+
+void pointwise64_device(const uint2* u, const uint2* v, uint2* out, size_t n, cudaStream_t s) {
+  if (!n) return;
+  const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms64() * 16);
+  pointwise64_kernel<<<grid, 256, 0, s>>>(u, v, out, n);
+  FPM_LAUNCH_CHECK();
+}
+
+}  // namespace fpm

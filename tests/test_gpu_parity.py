@@ -102,6 +102,24 @@ def test_polymul_shapes(gpu, checker, port, la, lb):
     assert np.array_equal(got, checker.polymul(a, la, b, lb))
 
 
+@pytest.mark.parametrize("la,lb", SHAPES)
+def test_polymul_shapes_gf64(gpu, checker, port, la, lb):
+    """The GF(2^64) pipeline (run_pipeline<gf64>, the reference's auto field) gives the same product."""
+    a = port.random_bitpoly(la, 3000 + la)
+    b = port.random_bitpoly(lb, 4000 + lb)
+    want = checker.polymul(a, la, b, lb)
+    assert np.array_equal(gpu.fp_polymul(a, la, b, lb, field=gpu.FIELD_GF64), want)
+    assert np.array_equal(gpu.fp_polymul(a, la, b, lb, field=gpu.FIELD_AUTO), want)
+
+
+@pytest.mark.parametrize("lg", [21, 23, 24])
+def test_polymul_gf64_large(gpu, checker, port, lg):
+    la = 1 << lg
+    a = port.random_bitpoly(la, 5000 + lg)
+    b = port.random_bitpoly(la - 3, 6000 + lg)
+    assert np.array_equal(gpu.fp_polymul(a, la, b, la - 3, field=gpu.FIELD_GF64), checker.polymul(a, la, b, la - 3))
+
+
 def test_polymul_edge_values(gpu, port):
     # identity, monomial shift, zero, empty (test_polymul.cpp:50-66)
     one = np.array([1], np.uint64)

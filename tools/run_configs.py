@@ -15,6 +15,7 @@ import paper_1803_11301_b200 as pkg  # noqa: E402
 P = oracle.port()
 cfgs = [int(x) for x in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["20", "24", "28"])]
 check = len(sys.argv) > 2 and sys.argv[2] == "check"
+FIELD = int(__import__("os").environ.get("FPM_FIELD", "128"))  # 128, 64 or 0 (auto)
 out = {}
 for lg in cfgs:
     n = 1 << lg
@@ -27,7 +28,7 @@ for lg in cfgs:
     wc = (2 * n - 1 + 63) // 64
     dc = torch.zeros(wc, dtype=torch.int64, device="cuda")
     st = [0.0] * 7
-    pkg.fp_polymul_dev(da, n, db, n, dc, field=128, stage_seconds=st)  # warm
+    pkg.fp_polymul_dev(da, n, db, n, dc, field=FIELD, stage_seconds=st)  # warm
     torch.cuda.synchronize()
     reps = 3 if lg >= 30 else 5
     st = [0.0] * 7
@@ -35,12 +36,12 @@ for lg in cfgs:
     times = []
     for _ in range(reps):
         e0.record()
-        pkg.fp_polymul_dev(da, n, db, n, dc, field=128)
+        pkg.fp_polymul_dev(da, n, db, n, dc, field=FIELD)
         e1.record()
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1))
     st = [0.0] * 7
-    pkg.fp_polymul_dev(da, n, db, n, dc, field=128, stage_seconds=st)
+    pkg.fp_polymul_dev(da, n, db, n, dc, field=FIELD, stage_seconds=st)
     torch.cuda.synchronize()
     c = dc.cpu().numpy().view(np.uint64)
     h = hashlib.blake2b(c.tobytes(), digest_size=16).hexdigest()
