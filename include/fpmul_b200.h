@@ -144,6 +144,21 @@ fpm_status fpm_gf128_mul(const uint64_t* a, const uint64_t* b, uint64_t* out, si
  * inv_row): each 128 elements x {lo, hi}.  Host-only, no GPU needed. */
 fpm_status fpm_tables128(uint64_t* cantor, uint64_t* rows, uint64_t* inv_rows);
 
+/* ---- GF(2^64) stages (the reference's auto field; encode.hpp:84-91, butterfly.hpp:58-68,
+ * polymul.hpp:78-80 instantiated for gf64, FPMUL_INSTANTIATE_*(gf64)).  Elements are one uint64
+ * word (FieldElem<gf64>); the partition matrix has 64 rows of 2^l bits; l < 32 (PartitionSpec). */
+fpm_status fpm_encode64_dev(const uint64_t* d_poly, unsigned l, uint64_t* d_ev, void* stream);
+fpm_status fpm_decode64_dev(const uint64_t* d_ev, unsigned l, uint64_t* d_poly, void* stream);
+/* base: Cantor coordinates of plan_butterflies<gf64>(l, base). */
+fpm_status fpm_lch_butterfly64_dev(uint64_t* d_ev, unsigned l, uint64_t base, int inverse, void* stream);
+fpm_status fpm_pointwise64_dev(const uint64_t* d_u, const uint64_t* d_v, uint64_t* d_out, size_t n, void* stream);
+fpm_status fpm_encode64(const uint64_t* poly, unsigned l, uint64_t* ev, int device);
+fpm_status fpm_decode64(const uint64_t* ev, unsigned l, uint64_t* poly, int device);
+fpm_status fpm_lch_butterfly64(uint64_t* ev, unsigned l, uint64_t base, int inverse, int device);
+fpm_status fpm_pointwise64(const uint64_t* u, const uint64_t* v, uint64_t* out, size_t n, int device);
+/* CantorField<gf64>::basis, EncodeMatrix<gf64> rows / inverse rows: 64 words each (host only). */
+fpm_status fpm_tables64(uint64_t* cantor, uint64_t* rows, uint64_t* inv_rows);
+
 /* Number of kernel launches issued by this library on the calling thread since the last reset
  * (for the bench's gpu_launches accounting). */
 uint64_t fpm_launch_count(int reset);

@@ -159,6 +159,11 @@ class _Ref:
         L.ref_gf128_mul.argtypes = [_u64p, _u64p, _u64p]
         L.ref_tables128.argtypes = [_u64p, _u64p, _u64p]
         L.ref_twiddles128.argtypes = [C.c_uint, _u64p]
+        L.ref_encode64.argtypes = [_u64p, C.c_uint, _u64p]
+        L.ref_decode64.argtypes = [_u64p, C.c_uint, _u64p]
+        L.ref_butterfly64.argtypes = [_u64p, C.c_uint, C.c_uint64, C.c_int]
+        L.ref_pointwise64.argtypes = [_u64p, _u64p, _u64p, C.c_size_t]
+        L.ref_tables64.argtypes = [_u64p, _u64p, _u64p]
         L.ref_last_error.restype = C.c_char_p
         L.ref_set_threads.argtypes = [C.c_int]
         self.L = L
@@ -252,6 +257,33 @@ class _Ref:
         r = np.zeros(256, np.uint64)
         i = np.zeros(256, np.uint64)
         self.L.ref_tables128(_ptr(c), _ptr(r), _ptr(i))
+        return c, r, i
+
+    # gf64 stages (the reference's auto field)
+    def encode64(self, a, l):
+        ev = np.zeros(1 << l, np.uint64)
+        self._chk(self.L.ref_encode64(_ptr(np.ascontiguousarray(a, np.uint64)), l, _ptr(ev)))
+        return ev
+
+    def decode64(self, ev, l):
+        a = np.zeros(max(1, (64 << l) // 64), np.uint64)
+        self._chk(self.L.ref_decode64(_ptr(np.ascontiguousarray(ev, np.uint64)), l, _ptr(a)))
+        return a
+
+    def butterfly64(self, ev, l, base=None, inverse=False):
+        ev = np.ascontiguousarray(ev, np.uint64).copy()
+        b = (1 << (l + 32)) if base is None else base
+        self._chk(self.L.ref_butterfly64(_ptr(ev), l, b, int(inverse)))
+        return ev
+
+    def pointwise64(self, u, v):
+        out = np.zeros_like(u)
+        self._chk(self.L.ref_pointwise64(_ptr(u), _ptr(v), _ptr(out), u.size))
+        return out
+
+    def tables64(self):
+        c, r, i = (np.zeros(64, np.uint64) for _ in range(3))
+        self.L.ref_tables64(_ptr(c), _ptr(r), _ptr(i))
         return c, r, i
 
     def twiddles128(self, l):

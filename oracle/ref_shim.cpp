@@ -71,6 +71,14 @@ void store_ev(const EvalVec<gf128>& v, uint64_t* w) {
     w[2 * i + 1] = v[i].v.hi;
   }
 }
+EvalVec<gf64> load_ev64(const uint64_t* w, size_t n) {
+  EvalVec<gf64> v(n);
+  for (size_t i = 0; i < n; ++i) v[i].v = w[i];
+  return v;
+}
+void store_ev64(const EvalVec<gf64>& v, uint64_t* w) {
+  for (size_t i = 0; i < v.size(); ++i) w[i] = v[i].v;
+}
 }  // namespace
 
 extern "C" {
@@ -211,6 +219,46 @@ void ref_tables128(uint64_t* cantor, uint64_t* rows, uint64_t* inv_rows) {
     cantor[2 * i] = f.basis(i).v.lo; cantor[2 * i + 1] = f.basis(i).v.hi;
     rows[2 * i] = m.row(i).v.lo; rows[2 * i + 1] = m.row(i).v.hi;
     inv_rows[2 * i] = m.inv_row(i).v.lo; inv_rows[2 * i + 1] = m.inv_row(i).v.hi;
+  }
+}
+// gf64 stage APIs (the reference's auto field); an EvalVec<gf64> is n_p x uint64.
+int ref_encode64(const uint64_t* w, unsigned l, uint64_t* ev) {
+  return guard([&] {
+    const auto spec = make_partition_spec<gf64>(l);
+    BitPoly p = make_poly(w, size_t{64} << l);
+    store_ev64(encode<gf64>(p, spec, EncodeMatrix<gf64>::get(), ExecPolicy::kParallel), ev);
+  });
+}
+int ref_decode64(const uint64_t* ev, unsigned l, uint64_t* w) {
+  return guard([&] {
+    const auto spec = make_partition_spec<gf64>(l);
+    auto v = load_ev64(ev, (size_t)1 << l);
+    BitPoly p = decode<gf64>(std::span<const FieldElem<gf64>>(v), spec, EncodeMatrix<gf64>::get(), ExecPolicy::kParallel);
+    store_poly(p, w, ((size_t{64} << l) + 63) / 64);
+  });
+}
+int ref_butterfly64(uint64_t* ev, unsigned l, uint64_t base, int inverse) {
+  return guard([&] {
+    const auto plan = plan_butterflies<gf64>(l, CantorVec<gf64>{base});
+    auto v = load_ev64(ev, (size_t)1 << l);
+    if (inverse) i_lch_butterfly<gf64>(std::span<FieldElem<gf64>>(v), plan, ExecPolicy::kParallel);
+    else lch_butterfly<gf64>(std::span<FieldElem<gf64>>(v), plan, ExecPolicy::kParallel);
+    store_ev64(v, ev);
+  });
+}
+int ref_pointwise64(const uint64_t* u, const uint64_t* v, uint64_t* out, size_t n) {
+  return guard([&] {
+    auto a = load_ev64(u, n), b = load_ev64(v, n);
+    store_ev64(pointwise_mul<gf64>(a, b, ExecPolicy::kSerial), out);
+  });
+}
+void ref_tables64(uint64_t* cantor, uint64_t* rows, uint64_t* inv_rows) {
+  const auto& f = CantorField<gf64>::get();
+  const auto& m = EncodeMatrix<gf64>::get();
+  for (unsigned i = 0; i < 64; ++i) {
+    cantor[i] = f.basis(i).v;
+    rows[i] = m.row(i).v;
+    inv_rows[i] = m.inv_row(i).v;
   }
 }
 int ref_twiddles128(unsigned l, uint64_t* out) {

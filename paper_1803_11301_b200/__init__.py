@@ -33,7 +33,12 @@ from ._lib import (  # noqa: F401
     launch_count,
     lch_butterfly,
     lib,
+    decode64,
+    encode64,
     fft_tile_log2,
+    lch_butterfly64,
+    pointwise64,
+    tables64,
     plan_mul,
     pointwise_mul,
     stage_dev,

@@ -68,6 +68,11 @@ def lib():
         L.fpm_pointwise.argtypes = [_u64p, _u64p, _u64p, sz, C.c_int]
         L.fpm_gf128_mul.argtypes = [_u64p, _u64p, _u64p, sz, C.c_int]
         L.fpm_tables128.argtypes = [_u64p, _u64p, _u64p]
+        L.fpm_tables64.argtypes = [_u64p, _u64p, _u64p]
+        L.fpm_encode64.argtypes = [_u64p, C.c_uint, _u64p, C.c_int]
+        L.fpm_decode64.argtypes = [_u64p, C.c_uint, _u64p, C.c_int]
+        L.fpm_lch_butterfly64.argtypes = [_u64p, C.c_uint, C.c_uint64, C.c_int, C.c_int]
+        L.fpm_pointwise64.argtypes = [_u64p, _u64p, _u64p, sz, C.c_int]
         L.fpm_lch_butterfly_dev.argtypes = [vp, C.c_uint, _u64p, C.c_int, vp]
         L.fpm_lch_butterfly.argtypes = [_u64p, C.c_uint, _u64p, C.c_int, C.c_int]
         L.fpm_encode_cols_dev.argtypes = [vp, C.c_uint, sz, sz, C.c_int, vp, vp]
@@ -168,6 +173,56 @@ def i_basis_cvt(w, n_bits: int, device: int = 0) -> np.ndarray:
         raise ValueError("i_basis_cvt: word array shorter than n_bits")
     _check(lib().fpm_i_basis_cvt(_ptr(w), n_bits, device))
     return w
+
+
+def tables64():
+    """(cantor, rows, inv_rows) of CantorField<gf64> / EncodeMatrix<gf64>, 64 words each."""
+    out = [np.zeros(64, np.uint64) for _ in range(3)]
+    _check(lib().fpm_tables64(*[_ptr(o) for o in out]))
+    return tuple(out)
+
+
+def encode64(poly, l: int, device: int = 0) -> np.ndarray:
+    """encode<gf64> with make_partition_spec<gf64>(l): 64 rows of 2^l bits -> 2^l uint64 elements."""
+    poly = _as_u64(poly)
+    if l >= 32:
+        raise ValueError("PartitionSpec: l must satisfy l < m/2")
+    if poly.size != max(1, (64 << l) // 64):
+        raise ValueError("encode: input length must be m * n_p bits")
+    ev = np.zeros(1 << l, np.uint64)
+    _check(lib().fpm_encode64(_ptr(poly), l, _ptr(ev), device))
+    return ev
+
+
+def decode64(ev, l: int, device: int = 0) -> np.ndarray:
+    ev = _as_u64(ev)
+    if l >= 32:
+        raise ValueError("PartitionSpec: l must satisfy l < m/2")
+    if ev.size != (1 << l):
+        raise ValueError("decode: length must equal n_p")
+    poly = np.zeros(max(1, (64 << l) // 64), np.uint64)
+    _check(lib().fpm_decode64(_ptr(ev), l, _ptr(poly), device))
+    return poly
+
+
+def lch_butterfly64(ev, l: int, base: int | None = None, inverse: bool = False, device: int = 0) -> np.ndarray:
+    """lch_butterfly<gf64> / i_lch_butterfly<gf64> with plan_butterflies(l, base); base defaults to
+    the partition base e_{l+32}."""
+    ev = _as_u64(ev).copy()
+    if ev.size != (1 << l):
+        raise ValueError("lch_butterfly: vector length does not match plan")
+    b = (1 << (l + 32)) if base is None else base
+    _check(lib().fpm_lch_butterfly64(_ptr(ev), l, b, int(inverse), device))
+    return ev
+
+
+def pointwise64(u, v, device: int = 0) -> np.ndarray:
+    u, v = _as_u64(u), _as_u64(v)
+    if u.size != v.size:
+        raise ValueError("pointwise_mul: length mismatch")
+    out = np.zeros_like(u)
+    _check(lib().fpm_pointwise64(_ptr(u), _ptr(v), _ptr(out), u.size, device))
+    return out
 
 
 def encode(poly, l: int, device: int = 0) -> np.ndarray:

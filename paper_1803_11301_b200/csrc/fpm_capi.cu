@@ -727,4 +727,100 @@ fpm_status fpm_gf128_mul(const uint64_t* a, const uint64_t* b, uint64_t* out, si
   return fpm_pointwise(a, b, out, n, device);
 }
 
+// ---- GF(2^64) stages
+fpm_status fpm_tables64(uint64_t* cantor, uint64_t* rows, uint64_t* inv_rows) {
+  return guard([&] {
+    const FieldTables& t = field_tables64();
+    for (int i = 0; i < 64; ++i) {
+      if (cantor) cantor[i] = t.cantor[i].lo;
+      if (rows) rows[i] = t.enc_rows[i].lo;
+      if (inv_rows) inv_rows[i] = t.inv_rows[i].lo;
+    }
+  });
+}
+
+static void check_l64(unsigned l) {
+  if (l >= 32) throw Error(kInvalid, "PartitionSpec: l must satisfy l < m/2");
+}
+
+fpm_status fpm_encode64_dev(const uint64_t* d_poly, unsigned l, uint64_t* d_ev, void* stream) {
+  return guard([&] {
+    require_device();
+    check_l64(l);
+    encode64_device(reinterpret_cast<const uint32_t*>(d_poly), l, reinterpret_cast<uint2*>(d_ev), 64,
+                    (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_decode64_dev(const uint64_t* d_ev, unsigned l, uint64_t* d_poly, void* stream) {
+  return guard([&] {
+    require_device();
+    check_l64(l);
+    decode64_device(reinterpret_cast<const uint2*>(d_ev), l, reinterpret_cast<uint32_t*>(d_poly), (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_lch_butterfly64_dev(uint64_t* d_ev, unsigned l, uint64_t base, int inverse, void* stream) {
+  return guard([&] {
+    require_device();
+    if (l > 63) throw Error(kInvalid, "lch_butterfly: at most 63 layers");
+    if (l == 0) return;
+    butterfly64_device(reinterpret_cast<uint2*>(d_ev), l, base, inverse != 0, (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_pointwise64_dev(const uint64_t* d_u, const uint64_t* d_v, uint64_t* d_out, size_t n, void* stream) {
+  return guard([&] {
+    require_device();
+    pointwise64_device(reinterpret_cast<const uint2*>(d_u), reinterpret_cast<const uint2*>(d_v),
+                       reinterpret_cast<uint2*>(d_out), n, (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_encode64(const uint64_t* poly, unsigned l, uint64_t* ev, int device) {
+  return host_call(device, [&](cudaStream_t s) {
+    check_l64(l);
+    const size_t pb = ((size_t)64 << l) / 8, eb = ((size_t)8 << l);
+    DevBuf P(pb < 8 ? 8 : pb, s), E(eb, s);
+    FPM_CUDA(cudaMemcpyAsync(P.p, poly, (pb + 7) / 8 * 8, cudaMemcpyHostToDevice, s));
+    encode64_device(P.as<uint32_t>(), l, E.as<uint2>(), 64, s);
+    FPM_CUDA(cudaMemcpyAsync(ev, E.p, eb, cudaMemcpyDeviceToHost, s));
+  });
+}
+
+fpm_status fpm_decode64(const uint64_t* ev, unsigned l, uint64_t* poly, int device) {
+  return host_call(device, [&](cudaStream_t s) {
+    check_l64(l);
+    const size_t pb = ((size_t)64 << l) / 8, eb = ((size_t)8 << l);
+    DevBuf P(pb < 8 ? 8 : pb, s), E(eb, s);
+    FPM_CUDA(cudaMemcpyAsync(E.p, ev, eb, cudaMemcpyHostToDevice, s));
+    FPM_CUDA(cudaMemsetAsync(P.p, 0, pb < 8 ? 8 : pb, s));
+    decode64_device(E.as<uint2>(), l, P.as<uint32_t>(), s);
+    FPM_CUDA(cudaMemcpyAsync(poly, P.p, (pb + 7) / 8 * 8, cudaMemcpyDeviceToHost, s));
+  });
+}
+
+fpm_status fpm_lch_butterfly64(uint64_t* ev, unsigned l, uint64_t base, int inverse, int device) {
+  return host_call(device, [&](cudaStream_t s) {
+    if (l > 63) throw Error(kInvalid, "lch_butterfly: at most 63 layers");
+    if (l == 0) return;
+    const size_t eb = ((size_t)8 << l);
+    DevBuf E(eb, s);
+    FPM_CUDA(cudaMemcpyAsync(E.p, ev, eb, cudaMemcpyHostToDevice, s));
+    butterfly64_device(E.as<uint2>(), l, base, inverse != 0, s);
+    FPM_CUDA(cudaMemcpyAsync(ev, E.p, eb, cudaMemcpyDeviceToHost, s));
+  });
+}
+
+fpm_status fpm_pointwise64(const uint64_t* u, const uint64_t* v, uint64_t* out, size_t n, int device) {
+  return host_call(device, [&](cudaStream_t s) {
+    if (!n) return;
+    DevBuf U(n * 8, s), V(n * 8, s);
+    FPM_CUDA(cudaMemcpyAsync(U.p, u, n * 8, cudaMemcpyHostToDevice, s));
+    FPM_CUDA(cudaMemcpyAsync(V.p, v, n * 8, cudaMemcpyHostToDevice, s));
+    pointwise64_device(U.as<uint2>(), V.as<uint2>(), U.as<uint2>(), n, s);
+    FPM_CUDA(cudaMemcpyAsync(out, U.p, n * 8, cudaMemcpyDeviceToHost, s));
+  });
+}
+
 }  // extern "C"

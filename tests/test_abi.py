@@ -54,3 +54,17 @@ def test_no_cpu_fallback_without_device():
     a = np.ones(4, np.uint64)
     with pytest.raises(pkg.FpmError, match="no CUDA device"):
         pkg.fp_polymul(a, 256, a, 256)
+
+
+def test_gf64_tables_host_side(port):
+    """CantorField<gf64> / EncodeMatrix<gf64> as built by the library (host only) equal the port's,
+    and the reference's when it is built here."""
+    import oracle
+    import paper_1803_11301_b200 as pkg
+    c, r, i = pkg.tables64()
+    assert np.array_equal(c, port.cantor_basis(64)[0::2])
+    pr, pi = port.encode_matrix(64)
+    assert np.array_equal(r, pr[0::2]) and np.array_equal(i, pi[0::2])
+    if oracle.have_ref():
+        rc, rr, ri = oracle.ref().tables64()
+        assert np.array_equal(c, rc) and np.array_equal(r, rr) and np.array_equal(i, ri)

@@ -150,3 +150,65 @@ def test_batch(gpu, port, checker):
     C = dC.cpu().numpy().view(np.uint64)
     for k in (0, 1, count - 1):
         assert np.array_equal(C[k], checker.polymul(A[k], la, B[k], lb)), k
+
+
+# ---------------------------------------------------------------- GF(2^64) stages (auto field)
+def _ref64_or_port(port):
+    import oracle
+    if oracle.have_ref():
+        R = oracle.ref()
+
+        class _R:
+            encode = staticmethod(lambda a, l: R.encode64(a, l))
+            decode = staticmethod(lambda e, l: R.decode64(e, l))
+            butterfly = staticmethod(lambda e, l, base=None, inv=False: R.butterfly64(e, l, base, inv))
+            pointwise = staticmethod(lambda u, v: R.pointwise64(u, v))
+        return _R()
+
+    class _P:  # the port keeps GF(2^64) elements as {lo, hi = 0}
+        encode = staticmethod(lambda a, l: port.encode(64, a, l)[0::2].copy())
+        decode = staticmethod(lambda e, l: port.decode(64, np.stack([e, np.zeros_like(e)], 1).ravel(), l))
+        butterfly = staticmethod(lambda e, l, base=None, inv=False: port.butterfly(
+            64, np.stack([e, np.zeros_like(e)], 1).ravel(), l, inv)[0::2].copy())
+        pointwise = staticmethod(lambda u, v: port.pointwise(
+            64, np.stack([u, np.zeros_like(u)], 1).ravel(), np.stack([v, np.zeros_like(v)], 1).ravel())[0::2].copy())
+    return _P()
+
+
+@pytest.mark.parametrize("l", [0, 3, 9, 10, 14, 16])
+def test_encode_decode64(gpu, port, l):
+    chk = _ref64_or_port(port)
+    rng = np.random.default_rng(900 + l)
+    a = rnd_words(rng, 64 << l)
+    ev = gpu.encode64(a, l)
+    assert np.array_equal(ev, chk.encode(a, l))
+    assert np.array_equal(gpu.decode64(ev, l), a)
+    assert np.array_equal(gpu.decode64(ev, l), chk.decode(ev, l))
+
+
+@pytest.mark.parametrize("l", [1, 4, 7, 8, 9, 12, 13, 16, 19])
+def test_butterfly64(gpu, port, l):
+    chk = _ref64_or_port(port)
+    rng = np.random.default_rng(950 + l)
+    ev = rnd_words(rng, 64 << l)
+    f = gpu.lch_butterfly64(ev, l)
+    assert np.array_equal(f, chk.butterfly(ev, l)), "forward"
+    assert np.array_equal(gpu.lch_butterfly64(f, l, inverse=True), ev), "inverse"
+
+
+def test_butterfly64_any_base(gpu, ref):
+    rng = np.random.default_rng(77)
+    l = 13
+    ev = rnd_words(rng, 64 << l)
+    base = (1 << 45) | (0x1234 << 20)  # an arbitrary coset of a sub-FFT
+    assert np.array_equal(gpu.lch_butterfly64(ev, l, base=base), ref.butterfly64(ev, l, base=base))
+    assert np.array_equal(gpu.lch_butterfly64(ev, l, base=base, inverse=True),
+                          ref.butterfly64(ev, l, base=base, inverse=True))
+
+
+def test_pointwise64(gpu, port):
+    chk = _ref64_or_port(port)
+    rng = np.random.default_rng(31)
+    u = rnd_words(rng, 64 * 5000)
+    v = rnd_words(rng, 64 * 5000)
+    assert np.array_equal(gpu.pointwise64(u, v), chk.pointwise(u, v))
