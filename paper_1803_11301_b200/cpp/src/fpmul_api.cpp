@@ -2,8 +2,8 @@
 // implemented over the B200 C-ABI (include/fpmul_b200.h).  Bulk work -- basis conversion,
 // encode/decode, butterflies, pointwise products, whole products -- runs on the GPU for the
 // north-star field GF(2^128); scalar field arithmetic and init-time tables stay on the host, as
-// in the reference.  GF(2^16)/GF(2^64) stage calls are not built on this backend and throw
-// std::invalid_argument (GF(2^64) is a "next" row).  Errors follow the reference:
+// in the reference.  GF(2^128) and GF(2^64) stages run on the GPU; the GF(2^16) test field's stage
+// calls are not built on this backend and throw std::invalid_argument.  Errors follow the reference:
 // std::invalid_argument for shape/length problems, std::runtime_error otherwise.
 #include <atomic>
 #include <mutex>
@@ -33,12 +33,16 @@ void check(fpm_status st) {
 }
 
 [[noreturn]] void not_built(const char* what) {
-  throw std::invalid_argument(std::string(what) + ": only GF(2^128) is built on the B200 backend");
+  throw std::invalid_argument(std::string(what) + ": the GF(2^16) test field is not built on the B200 backend");
 }
 
 template <class F>
 constexpr bool is128() {
   return F::kDegree == 128;
+}
+template <class F>
+constexpr bool is64() {
+  return F::kDegree == 64;
 }
 
 using detail::test_bit;
@@ -290,8 +294,13 @@ const EncodeMatrix<F>& EncodeMatrix<F>::get() {
 template <class F>
 EvalVec<F> encode(const BitPoly& a, const PartitionSpec<F>& spec, const EncodeMatrix<F>&, ExecPolicy) {
   if (a.bit_length() != size_t{F::kDegree} * spec.n_p) throw std::invalid_argument("encode: input length must be m * n_p bits");
-  if constexpr (!is128<F>()) not_built("encode");
-  else {
+  if constexpr (is64<F>()) {
+    EvalVec<F> out(spec.n_p);
+    check(fpm_encode64(a.word_data(), spec.l, reinterpret_cast<uint64_t*>(out.data()), current_device()));
+    return out;
+  } else if constexpr (!is128<F>()) {
+    not_built("encode");
+  } else {
     EvalVec<F> out(spec.n_p);
     check(fpm_encode(a.word_data(), spec.l, reinterpret_cast<uint64_t*>(out.data()), current_device()));
     return out;
@@ -301,8 +310,13 @@ EvalVec<F> encode(const BitPoly& a, const PartitionSpec<F>& spec, const EncodeMa
 template <class F>
 BitPoly decode(std::span<const FieldElem<F>> v, const PartitionSpec<F>& spec, const EncodeMatrix<F>&, ExecPolicy) {
   if (v.size() != spec.n_p) throw std::invalid_argument("decode: length must equal n_p");
-  if constexpr (!is128<F>()) not_built("decode");
-  else {
+  if constexpr (is64<F>()) {
+    BitPoly a(size_t{F::kDegree} * spec.n_p);
+    check(fpm_decode64(reinterpret_cast<const uint64_t*>(v.data()), spec.l, a.word_data(), current_device()));
+    return a;
+  } else if constexpr (!is128<F>()) {
+    not_built("decode");
+  } else {
     BitPoly a(size_t{F::kDegree} * spec.n_p);
     check(fpm_decode(reinterpret_cast<const uint64_t*>(v.data()), spec.l, a.word_data(), current_device()));
     return a;
@@ -368,8 +382,13 @@ namespace {
 template <class F>
 void run_butterfly(std::span<FieldElem<F>> v, const ButterflyPlan<F>& plan, bool inverse) {
   if (v.size() != size_t{1} << plan.layers) throw std::invalid_argument("lch_butterfly: vector length does not match plan");
-  if constexpr (!is128<F>()) not_built("lch_butterfly");
-  else {
+  if constexpr (is64<F>()) {
+    if (!plan.layers) return;
+    check(fpm_lch_butterfly64(reinterpret_cast<uint64_t*>(v.data()), plan.layers, plan.base.bits, inverse ? 1 : 0,
+                              current_device()));
+  } else if constexpr (!is128<F>()) {
+    not_built("lch_butterfly");
+  } else {
     if (!plan.layers) return;
     const uint64_t base[2] = {plan.base.bits.lo, plan.base.bits.hi};
     check(fpm_lch_butterfly(reinterpret_cast<uint64_t*>(v.data()), plan.layers, base, inverse ? 1 : 0, current_device()));
@@ -443,11 +462,11 @@ BitPoly fp_polymul(const BitPoly& a, const BitPoly& b) { return fp_polymul(a, b,
 
 BitPoly fp_polymul(const BitPoly& a, const BitPoly& b, const MulOptions& opts) {
   if (!a.bit_length() || !b.bit_length()) return BitPoly{};
-  if (opts.field == FieldChoice::kGF64) {
-    (void)plan_mul(a.bit_length(), b.bit_length(), opts.field);  // same argument checks as the reference
-    not_built("fp_polymul(kGF64)");
-  }
-  return gpu_product(a, b, FPM_FIELD_GF128, opts.stage_seconds);
+  // The reference's field choice (plan_mul, polymul.cpp:203-205): kAuto runs GF(2^64) when it
+  // supports the size; the product is the same in every field.
+  const int f = opts.field == FieldChoice::kGF64 ? FPM_FIELD_GF64
+              : opts.field == FieldChoice::kGF128 ? FPM_FIELD_GF128 : FPM_FIELD_AUTO;
+  return gpu_product(a, b, f, opts.stage_seconds);
 }
 
 BitPoly naive_mul(const BitPoly& a, const BitPoly& b) { return gpu_product(a, b, FPM_FIELD_GF128, nullptr); }
@@ -456,8 +475,15 @@ BitPoly karatsuba_mul(const BitPoly& a, const BitPoly& b) { return gpu_product(a
 template <class F>
 EvalVec<F> pointwise_mul(std::span<const FieldElem<F>> u, std::span<const FieldElem<F>> v, ExecPolicy) {
   if (u.size() != v.size()) throw std::invalid_argument("pointwise_mul: length mismatch");
-  if constexpr (!is128<F>()) not_built("pointwise_mul");
-  else {
+  if constexpr (is64<F>()) {
+    EvalVec<F> out(u.size());
+    if (!u.empty())
+      check(fpm_pointwise64(reinterpret_cast<const uint64_t*>(u.data()), reinterpret_cast<const uint64_t*>(v.data()),
+                            reinterpret_cast<uint64_t*>(out.data()), u.size(), current_device()));
+    return out;
+  } else if constexpr (!is128<F>()) {
+    not_built("pointwise_mul");
+  } else {
     EvalVec<F> out(u.size());
     if (!u.empty())
       check(fpm_pointwise(reinterpret_cast<const uint64_t*>(u.data()), reinterpret_cast<const uint64_t*>(v.data()),

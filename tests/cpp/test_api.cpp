@@ -167,9 +167,25 @@ static void gpu_tests() {
   }
   check_throws<std::invalid_argument>([&] { encode<gf128>(BitPoly(100), make_partition_spec<gf128>(3), mat); },
                                       "encode(bad length)");
+  // gf64 (the auto field): encode == row combination, decode inverts (encode_suite<gf64>, selftest.cpp:485)
+  for (unsigned l : {0u, 5u, 11u}) {
+    const auto& m64 = EncodeMatrix<gf64>::get();
+    const auto spec = make_partition_spec<gf64>(l);
+    const BitPoly a = random_bitpoly(64 * spec.n_p, rng);
+    const auto ev = encode<gf64>(a, spec, m64);
+    bool ok64 = true;
+    for (size_t i = 0; i < spec.n_p; ++i) {
+      FieldElem<gf64> acc{};
+      for (unsigned j = 0; j < 64; ++j)
+        if (a.bit(j * spec.n_p + i)) acc = gf_add(acc, m64.row(j));
+      ok64 &= ev[i] == acc;
+    }
+    CHECK(ok64);
+    CHECK(decode<gf64>(std::span<const FieldElem<gf64>>(ev), spec, m64) == a);
+  }
   check_throws<std::invalid_argument>([&] {
-    encode<gf64>(BitPoly(64 * 8), make_partition_spec<gf64>(3), EncodeMatrix<gf64>::get());
-  }, "encode<gf64>");
+    encode<gf16>(BitPoly(16 * 8), make_partition_spec<gf16>(3), EncodeMatrix<gf16>::get());
+  }, "encode<gf16>");
   // butterflies == direct evaluation for random bases (test_butterfly.cpp:28-47, 104-108)
   for (unsigned l = 0; l <= 8; ++l) {
     const CantorVec<gf128> base{u128{rng(), rng()}};
@@ -208,6 +224,31 @@ static void gpu_tests() {
     lch_butterfly<gf128>(std::span<FieldElem<gf128>>(v), plan);
     CHECK(v == ref);
   }
+  // gf64 butterflies == direct evaluation, inverse restores (butterfly_suite<gf64>)
+  for (unsigned l : {3u, 9u, 12u}) {
+    const CantorVec<gf64> base{rng() & ~((uint64_t{1} << l) - 1)};
+    const auto plan = plan_butterflies<gf64>(l, base);
+    EvalVec<gf64> coeffs(size_t{1} << l);
+    for (auto& e : coeffs) e.v = rng();
+    EvalVec<gf64> v = coeffs;
+    lch_butterfly<gf64>(std::span<FieldElem<gf64>>(v), plan);
+    bool ok64 = true;
+    for (size_t idx = 0; idx < v.size(); idx += 1 + v.size() / 64) {
+      const CantorVec<gf64> pt{base.bits ^ idx};
+      ok64 &= direct_eval<gf64>(std::span<const FieldElem<gf64>>(coeffs), pt) == v[idx];
+    }
+    CHECK(ok64);
+    i_lch_butterfly<gf64>(std::span<FieldElem<gf64>>(v), plan);
+    CHECK(v == coeffs);
+  }
+  {
+    EvalVec<gf64> u64(257), w64(257);
+    for (size_t i = 0; i < u64.size(); ++i) { u64[i].v = rng(); w64[i].v = rng(); }
+    const auto p64 = pointwise_mul<gf64>(u64, w64);
+    bool ok64 = true;
+    for (size_t i = 0; i < u64.size(); ++i) ok64 &= p64[i].v == gf64::mul(u64[i].v, w64[i].v);
+    CHECK(ok64);
+  }
   // pointwise (test_polymul.cpp:136-152)
   EvalVec<gf128> u(300), w(300);
   for (size_t i = 0; i < u.size(); ++i) { u[i].v = u128{rng(), rng()}; w[i].v = u128{rng(), rng()}; }
@@ -231,16 +272,16 @@ static void gpu_tests() {
     const size_t la = 1 + rng() % 70000, lb = 1 + rng() % 70000;
     const BitPoly a = random_bitpoly(la, rng), c = random_bitpoly(lb, rng);
     MulOptions o;
-    o.field = (t & 1) ? FieldChoice::kGF128 : FieldChoice::kAuto;
+    o.field = t % 3 == 0 ? FieldChoice::kGF128 : t % 3 == 1 ? FieldChoice::kGF64 : FieldChoice::kAuto;
     StageSeconds st;
     o.stage_seconds = &st;
     CHECK(fp_polymul(a, c, o) == schoolbook(a, c));
   }
-  check_throws<std::invalid_argument>([&] {
+  check_throws<std::invalid_argument>([&] {  // beyond GF(2^64)'s bound (field_supports, polymul.cpp:45-49)
     MulOptions o;
     o.field = FieldChoice::kGF64;
-    fp_polymul(b, b, o);
-  }, "fp_polymul(kGF64)");
+    (void)plan_mul(size_t{1} << 40, 8, o.field);
+  }, "plan_mul(kGF64, 2^40)");
 }
 
 int main(int argc, char** argv) {
