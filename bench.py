@@ -161,14 +161,17 @@ def run_reference(args, ws, rank):
     P = oracle.port()
     a = P.random_bitpoly(bits, 20261020)
     b = P.random_bitpoly(bits, 20261021)
+    # Same field as our arm's config (GF(2^128), the north-star transform); --ref-field 0 times the
+    # reference's default auto field (GF(2^64)) instead.
+    field = args.ref_field
     for _ in range(min(args.warmup, 1)):  # cold call builds the twiddle plan (polymul.cpp:63-74)
-        R.polymul(a, bits, b, bits, field=0)
+        R.polymul(a, bits, b, bits, field=field)
     times = []
     budget = args.ref_budget_s
     t_all = time.perf_counter()
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        R.polymul(a, bits, b, bits, field=0)
+        R.polymul(a, bits, b, bits, field=field)
         times.append((time.perf_counter() - t0) * 1e3)
         if time.perf_counter() - t_all > budget:
             break
@@ -179,7 +182,9 @@ def run_reference(args, ws, rank):
         "ms_per_step": round(v, 3), "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "u64", "data": "synthetic (mt19937_64 seeded, random_bitpoly)",
         "config": {"workload": f"cfg{args.config}: 2^{bits.bit_length()-1} x 2^{bits.bit_length()-1}-bit product",
-                   "field": "auto (m=64, the reference default)", "library": os.path.basename(R.path)},
+                   "field": {128: "GF(2^128) (FieldChoice::kGF128, as our arm)", 64: "GF(2^64)",
+                             0: "auto (m=64, the reference default)"}[field],
+                   "library": os.path.basename(R.path)},
         "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": threads, "kind": "reference",
                          "sample": f"{len(times)} warm full products (ExecPolicy::kParallel, {threads} OpenMP "
                                    f"threads) after {min(args.warmup, 1)} cold call(s)"},
@@ -216,6 +221,8 @@ def main():
     ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
+    ap.add_argument("--ref-field", type=int, default=128, choices=[0, 64, 128],
+                    help="--impl reference: the reference's field (default GF(2^128), as our arm)")
     ap.add_argument("--mode", default="shard", choices=["shard", "replicas"],
                     help="N>1: shard one product over the GPUs (default) or run independent replicas")
     args = ap.parse_args()
@@ -352,6 +359,27 @@ def main():
     roof["step_frac"] = round(t_roof / (sum(stages.values())), 4)
     roof["stage_ms"] = {k: round(v * 1e3, 3) for k, v in stages.items()}
 
+    # ---- the reference's default (auto) field, GF(2^64): same product, device-resident
+    auto_field = None
+    if mode == "single":
+        for _ in range(2):
+            pkg.fp_polymul_dev(a, bits, b, bits, c, field=pkg.FIELD_AUTO)
+        k2 = max(1, min(args.steps, 5))
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(k2):
+            pkg.fp_polymul_dev(a, bits, b, bits, c, field=pkg.FIELD_AUTO)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        auto_ms = e0.elapsed_time(e1) / k2
+        st = [0.0] * pkg.NUM_STAGES
+        pkg.fp_polymul_dev(a, bits, b, bits, c, field=pkg.FIELD_AUTO, stage_seconds=st)
+        torch.cuda.synchronize()
+        auto_field = {"field": f"GF(2^{pkg.plan_mul(bits, bits)['field_degree']}) (plan_mul auto, the reference default)",
+                      "value": round(auto_ms, 3), "unit": "ms", "steps": k2,
+                      "same_product": bool(np.array_equal(c.cpu().numpy().view(np.uint64), dev_result)),
+                      "stage_ms": {k: round(v * 1e3, 3) for k, v in zip(pkg.STAGE_NAMES, st)}}
+
     line = {
         "metric": METRIC, "value": round(ms_max / ws if mode == "replicas" else ms_max, 3), "unit": "ms",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 3),
@@ -370,6 +398,8 @@ def main():
         "roofline": roof,
         "clocks": clocks,
     }
+    if auto_field:
+        line["auto_field"] = auto_field
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_baseline(bits)
