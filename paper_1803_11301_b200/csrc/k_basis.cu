@@ -296,6 +296,181 @@ __global__ void __launch_bounds__(256) slab_kernel(uint32_t* __restrict__ data, 
   }
 }
 
+// ------------------------------------------------------------------ conv(256) over units, by L1(16, 16)
+// conv(256) of 256 units (8 KiB rows; unit u = 16 d + v) evaluated per bit column by the same
+// recursion as the whole conversion one level down: C_rows(conv16 over v) o C_cols(conv16 over d)
+// o L1(16, 16), with the L1 skew in units.  A CTA of 512 threads owns 32 consecutive words of each
+// of the 256 units; thread (r = tid >> 5, c = tid & 31).  Three register-local phases (zeta over d,
+// conv16 over k, conv16 over v) with shared-memory exchanges between them: 28 B of shared traffic
+// per word instead of the ~80 B of the 12 row passes.  Skewed rows Z[d][s] (s < 32 unit slots):
+// Z[d][v + d] = F_d[v].
+constexpr int kC256Threads = 512;
+constexpr size_t kC256Smem = 16 * 32 * 32 * sizeof(uint32_t);  // Z[16][32][32]
+
+// conv16 over 16 register values (build_schedule(16): (16,6), (8,3), (16,4), (4,1)); increasing q
+// reads every source before it is overwritten (sources sit above their targets).
+template <int S, int D, bool INV>
+__device__ __forceinline__ void conv_pass16(uint32_t (&x)[16]) {
+#pragma unroll
+  for (int base = 0; base < 16; base += S)
+#pragma unroll
+    for (int q = S / 2 - D; q < S - D; ++q) {
+      uint32_t v = x[base + q + D];
+      if (!INV && q + 2 * D < S) v ^= x[base + q + 2 * D];
+      x[base + q] ^= v;
+    }
+}
+template <bool INV>
+__device__ __forceinline__ void conv16_vals(uint32_t (&x)[16]) {
+  if (!INV) {
+    conv_pass16<16, 6, false>(x);
+    conv_pass16<8, 3, false>(x);
+    conv_pass16<16, 4, false>(x);
+    conv_pass16<4, 1, false>(x);
+  } else {
+    conv_pass16<4, 1, true>(x);
+    conv_pass16<16, 4, true>(x);
+    conv_pass16<8, 3, true>(x);
+    conv_pass16<16, 6, true>(x);
+  }
+}
+
+// zeta over the 4 digit bits (superset sums): x[d] ^= x[d | 2^b] for d without bit b.
+__device__ __forceinline__ void zeta16_vals(uint32_t (&x)[16]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int d = 0; d < 16; ++d)
+      if (!(d >> j & 1)) x[d] ^= x[d | (1 << j)];
+}
+
+// Units of CTA slab `blk`: unit u of group `grp` is row grp_base + u * ustride (rows of kTWords
+// words); the CTA takes word columns [c0, c0 + 32).
+struct UnitMap {
+  uint64_t ustride, gstride, ngroups;  // group g's unit u at row g_row(g) + u * ustride
+  __device__ __forceinline__ uint64_t row(uint64_t grp, int u) const {
+    // groups: (ngroups) groups; group index -> base row = (grp % gstride) + (grp / gstride) * 256 * gstride
+    return (grp % gstride) + (grp / gstride) * 256 * gstride + (uint64_t)u * ustride;
+  }
+};
+
+// Optional fused input stage (forward only): the units are the unit-level L1 carry of a
+// unit-skewed zeta output gs (digit rows of gs_pitch words, 256 + 256 units):
+//   unit kh of group v = gs[kh][v+kh] ^ [v>=1] gs[kh][255+v+kh] ^ [kh>=1] gs[kh-1][255+v+kh]
+// (the last two only while 255 + v + kh < 512, the stored width; digit count 256)
+struct CarrySrc {
+  const uint32_t* gs = nullptr;
+  uint64_t gs_pitch = 0;
+};
+
+template <bool INV>
+__global__ void __launch_bounds__(kC256Threads, 1) conv256_units_kernel(uint32_t* __restrict__ data, UnitMap um,
+                                                                        uint64_t nitems, CarrySrc cs) {
+  extern __shared__ uint32_t Z[];  // [d][s][c], d < 16, s < 32, c < 32
+  const int tid = threadIdx.x, c = tid & 31, r = tid >> 5;
+  constexpr int kCols = kTWords / 32;  // 32-word column blocks per unit
+  auto zi = [](int d, int s, int cc) { return (d * 32 + s) * 32 + cc; };
+  for (uint64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const uint64_t grp = it / kCols;
+    const uint64_t colw = (it % kCols) * 32 + c;
+    uint32_t* const gbase = data + um.row(grp, 0) * kTWords + colw;
+    const uint32_t ustep = (uint32_t)(um.ustride * kTWords);  // 256 units x ustep < 2^32 words
+    auto at = [&](int u) -> uint32_t* { return gbase + (uint32_t)u * ustep; };
+    auto src = [&](int u) -> uint32_t {  // input unit u of this group
+      if (!cs.gs) return *at(u);
+      const uint64_t v = grp;  // group = offset v within the digit, unit = digit kh
+      const uint32_t* rk = cs.gs + (uint64_t)u * cs.gs_pitch + colw;
+      uint32_t g = rk[(v + u) * kTWords];
+      if (v + u < 257) {  // units >= 256 + 256 of a skewed digit row are zero (not stored)
+        if (v >= 1) g ^= rk[(255 + v + u) * kTWords];
+        if (u >= 1) g ^= rk[(255 + v + u) * kTWords - cs.gs_pitch];
+      }
+      return g;
+    };
+    uint32_t x[16];
+    if (!INV) {
+      // ---- skewed load (thread = slot pair {r, r+16}) + zeta over d
+      uint32_t y[16];
+#pragma unroll
+      for (int d = 0; d < 16; ++d) {
+        const int v0 = r - d, v1 = r + 16 - d;
+        x[d] = v0 >= 0 ? src(16 * d + v0) : 0u;
+        y[d] = v1 < 16 ? src(16 * d + v1) : 0u;
+      }
+      zeta16_vals(x);
+      zeta16_vals(y);
+      __syncthreads();  // previous item's readers of Z are done
+#pragma unroll
+      for (int d = 0; d < 16; ++d) {
+        Z[zi(d, r, c)] = x[d];
+        Z[zi(d, r + 16, c)] = y[d];
+      }
+      __syncthreads();
+      // ---- carry + unskew (thread = v = r): g_k[v] = Z[k][v+k] ^ Z[k][15+v+k] ^ Z[k-1][15+v+k]
+      const int v = r;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        uint32_t g = Z[zi(k, v + k, c)];
+        if (v >= 1 && 15 + v + k < 31) g ^= Z[zi(k, 15 + v + k, c)];
+        if (k >= 1 && 15 + v + k < 31) g ^= Z[zi(k - 1, 15 + v + k, c)];
+        x[k] = g;
+      }
+      conv16_vals<false>(x);  // C_cols: conv16 over k
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) Z[zi(k, v, c)] = x[k];
+      __syncthreads();
+      // ---- C_rows: conv16 over v (thread = k = r)
+#pragma unroll
+      for (int vv = 0; vv < 16; ++vv) x[vv] = Z[zi(r, vv, c)];
+      conv16_vals<false>(x);
+#pragma unroll
+      for (int vv = 0; vv < 16; ++vv) *at(16 * r + vv) = x[vv];
+    } else {
+      // ---- C_rows^-1 over v (thread = k = r)
+#pragma unroll
+      for (int vv = 0; vv < 16; ++vv) x[vv] = *at(16 * r + vv);
+      conv16_vals<true>(x);
+      __syncthreads();
+#pragma unroll
+      for (int vv = 0; vv < 16; ++vv) Z[zi(r, vv, c)] = x[vv];
+      __syncthreads();
+      // ---- C_cols^-1 over k (thread = v = r), then skew: Z[k][v + k]
+      const int v = r;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) x[k] = Z[zi(k, v, c)];
+      conv16_vals<true>(x);
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) Z[zi(k, v + k, c)] = x[k];
+      __syncthreads();
+      // ---- zeta over k on the skewed rows (thread = slot pair {r, r+16}); row k holds slots k..k+15
+      uint32_t y[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        x[k] = (r >= k) ? Z[zi(k, r, c)] : 0u;
+        y[k] = (r + 16 < k + 16) ? Z[zi(k, r + 16, c)] : 0u;
+      }
+      zeta16_vals(x);
+      zeta16_vals(y);
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        Z[zi(k, r, c)] = x[k];
+        Z[zi(k, r + 16, c)] = y[k];
+      }
+      __syncthreads();
+      // ---- overflow + unskew (thread = d = r): F_d[v] = Z[d][v+d] ^ Z[d-1][15+v+d]
+#pragma unroll
+      for (int vv = 0; vv < 16; ++vv) {
+        uint32_t f = Z[zi(r, vv + r, c)];
+        if (r >= 1 && 15 + vv + r < 31) f ^= Z[zi(r - 1, 15 + vv + r, c)];
+        *at(16 * r + vv) = f;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ unit-level L1 carry + C_cols
 // Rows of t bits are units; row d = 256 * dh + v (digit dh, offset v).  After the unit-skewed zeta,
 // Gs[kh] holds units u = 0 .. 256+Dd-1 (pitch gs_pitch words).  Output unit (kh, v):
@@ -399,6 +574,23 @@ void zeta(const uint32_t* src, uint64_t src_pitch, uint32_t* dst, uint64_t dst_p
 
 constexpr size_t kSlabSmem = 256 * kRowPitchW<kSlabW> * sizeof(uint32_t);
 // nslabs counts 8-word columns (callers' unit); the kernels take kSlabW of them per slab.
+// conv(256) over groups of 256 units: group g's unit u is row base(g) + u * ustride, base(g) =
+// (g % gstride) + (g / gstride) * 256 * gstride.
+void conv256_units(uint32_t* w, uint64_t ngroups, uint64_t ustride, uint64_t gstride, bool inv, cudaStream_t s,
+                   CarrySrc cs = CarrySrc{}) {
+  static bool attr = false;
+  if (!attr) {
+    FPM_CUDA(cudaFuncSetAttribute(conv256_units_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC256Smem));
+    FPM_CUDA(cudaFuncSetAttribute(conv256_units_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC256Smem));
+    attr = true;
+  }
+  UnitMap um{ustride, gstride, ngroups};
+  const uint64_t items = ngroups * (kTWords / 32);
+  if (inv) conv256_units_kernel<true><<<grid_cap(items, 2), kC256Threads, kC256Smem, s>>>(w, um, items, cs);
+  else conv256_units_kernel<false><<<grid_cap(items, 2), kC256Threads, kC256Smem, s>>>(w, um, items, cs);
+  FPM_LAUNCH_CHECK();
+}
+
 void slab(uint32_t* w, int g, uint64_t rstride, uint64_t nslabs, bool inv, cudaStream_t s) {
   static_assert(kSlabSmem <= 48 * 1024, "slab tile fits the default dynamic smem limit");
   nslabs /= kSlabW;
@@ -443,11 +635,19 @@ void conv_cols(uint32_t* w, uint32_t* scratch, int lgD, bool inv, cudaStream_t s
   unit_skew.log = kTLog2;
   if (!inv) {
     zeta(w, 256 * (uint64_t)kTWords, scratch, sk_pitch, Dd, 0, gd, unit_skew, windows, s, 256 * (uint64_t)kTWords);
-    unit_carry_cols(scratch, sk_pitch, w, gd, s);
-    slab(w, 8, 1, (Dd * 256 / 256) * (kTWords / 8), false, s);   // C_rows: conv(256) over consecutive rows
+    if (gd == 8) {  // carry fused into the conv(256) over the high digit (row stride 256)
+      CarrySrc cs;
+      cs.gs = scratch;
+      cs.gs_pitch = sk_pitch;
+      conv256_units(w, 256, 256, 256, false, s, cs);
+    } else {
+      unit_carry_cols(scratch, sk_pitch, w, gd, s);
+    }
+    conv256_units(w, Dd, 1, 1, false, s);                         // C_rows: conv(256) over consecutive rows
   } else {
-    slab(w, 8, 1, (Dd * 256 / 256) * (kTWords / 8), true, s);
-    slab(w, gd, 256, 256 * (kTWords / 8), true, s);               // C_cols^-1: conv(Dd) at row stride 256
+    conv256_units(w, Dd, 1, 1, true, s);
+    if (gd == 8) conv256_units(w, 256, 256, 256, true, s);        // C_cols^-1: conv(Dd) at row stride 256
+    else slab(w, gd, 256, 256 * (kTWords / 8), true, s);
     zeta(w, 256 * (uint64_t)kTWords, scratch, sk_pitch, Dd, 0, gd, unit_skew, windows, s, 256 * (uint64_t)kTWords);
     unit_overflow(scratch, sk_pitch, w, Dd, s);
   }
