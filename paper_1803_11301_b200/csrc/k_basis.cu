@@ -119,7 +119,10 @@ struct Skew {
 };
 constexpr int kZW = 32;
 constexpr int kZP = 36;  // shared row pitch (16 B aligned, conflict-free for both mappings)
-__global__ void __launch_bounds__(256, 2) zeta_kernel(const uint32_t* __restrict__ src, uint64_t src_pitch,
+// BITSKEW: the bit-granular skew path (neighbour words by shuffle) needs the registers of 2 CTAs/SM;
+// word-aligned or no skew runs at 3 CTAs/SM.
+template <bool BITSKEW>
+__global__ void __launch_bounds__(256, BITSKEW ? 2 : 3) zeta_kernel(const uint32_t* __restrict__ src, uint64_t src_pitch,
                                                    uint32_t* __restrict__ dst, uint64_t dst_pitch, uint64_t D,
                                                    int b0, int nb, Skew skew, uint64_t src_row_words,
                                                    uint64_t windows) {
@@ -136,7 +139,7 @@ __global__ void __launch_bounds__(256, 2) zeta_kernel(const uint32_t* __restrict
     // ---- mapping A: load, stages on tile-row bits 3..7
     const int c = tid & 31;
     uint32_t a[32];
-    if (skew.mask && skew.log >= 5) {  // word-aligned skew: plain coalesced loads
+    if (!BITSKEW && skew.mask) {  // word-aligned skew: plain coalesced loads
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         const int R = (tid >> 5) + 8 * k;
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(256, 2) zeta_kernel(const uint32_t* __restrict
         const int64_t iw = (int64_t)(wi * kZW) - (int64_t)((((d >> skew.lo) & skew.mask) << skew.log) >> 5) + c;
         a[k] = (wi < windows && iw >= 0 && iw < (int64_t)src_row_words) ? __ldg(src + d * src_pitch + iw) : 0u;
       }
-    } else if (skew.mask) {
+    } else if (BITSKEW) {
       // R (so d, wi, the shift) is warp-uniform: one coalesced word per lane and row, all rows'
       // loads in flight at once (lane 31 also fetches the word after the window), then the
       // neighbour word comes by shuffle and a funnel shift aligns the window.
@@ -567,8 +570,12 @@ void zeta(const uint32_t* src, uint64_t src_pitch, uint32_t* dst, uint64_t dst_p
   if (nb <= 0) return;
   const int wpc = 256 >> nb;
   const uint64_t items = (D >> nb) * ((windows + wpc - 1) / wpc);
-  zeta_kernel<<<grid_cap(items, 4), 256, 256 * kZP * sizeof(uint32_t), s>>>(
-      src, src_pitch, dst, dst_pitch, D, b0, nb, skew, src_row_words, windows);
+  if (skew.mask && skew.log < 5)
+    zeta_kernel<true><<<grid_cap(items, 4), 256, 256 * kZP * sizeof(uint32_t), s>>>(
+        src, src_pitch, dst, dst_pitch, D, b0, nb, skew, src_row_words, windows);
+  else
+    zeta_kernel<false><<<grid_cap(items, 4), 256, 256 * kZP * sizeof(uint32_t), s>>>(
+        src, src_pitch, dst, dst_pitch, D, b0, nb, skew, src_row_words, windows);
   FPM_LAUNCH_CHECK();
 }
 
