@@ -225,18 +225,43 @@ __global__ void __launch_bounds__(256) carry_rows_kernel(const uint32_t* __restr
   uint32_t* tile = smem;
   uint32_t* sc = smem + kTileRows * kRowPitchW<1>;
   const int tid = threadIdx.x;
+  // Staging (aliases the conversion tile): the two source spans of the row, word w at w + w/8 so
+  // that thread t's 9-word window starting at 8t is bank-conflict free.
+  uint32_t* sa = smem;                    // Gs[k] words a0 .. a0 + 2048      (L part, bit offset k)
+  uint32_t* sh = smem + 2312;             // Gs[k] ^ Gs[k-1], words b0 ..     (H parts, t + k - 1)
+  auto pad = [](int w) { return w + (w >> 3); };
   for (uint64_t k = blockIdx.x; k < D; k += gridDim.x) {
     const uint32_t* rk = gs + k * gs_pitch;
     const uint32_t* rk1 = k ? gs + (k - 1) * gs_pitch : nullptr;
+    const uint64_t a0 = k >> 5, b0 = (kT + k - 1) >> 5;
+    const int sA = (int)(k & 31), sB = (int)((kT + k - 1) & 31);
+    __syncthreads();  // the previous row's conversion is done with the shared tile
+    for (int w = tid; w <= kTWords; w += 256) {  // coalesced: 2049 words per span
+      sa[pad(w)] = __ldg(rk + a0 + w);
+      const uint64_t wb = b0 + w;
+      uint32_t h = 0;
+      if (wb < gs_pitch) {
+        h = __ldg(rk + wb);
+        if (k) h ^= __ldg(rk1 + wb);
+      }
+      sh[pad(w)] = h;
+    }
+    __syncthreads();
     uint32_t m[8];
+    {
+      uint32_t wa[9], wh[9];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int64_t p = (int64_t)(tid * 8 + i) * 32;
-      uint32_t v = g_get32(rk, gs_pitch, p + (int64_t)k);
-      uint32_t hi = g_get32(rk, gs_pitch, (int64_t)kT + p - 1 + (int64_t)k);
-      if (p == 0) hi &= ~1u;
-      if (k) hi ^= g_get32(rk1, gs_pitch, (int64_t)kT + p + (int64_t)k - 1);
-      m[i] = v ^ hi;
+      for (int j = 0; j < 9; ++j) {
+        wa[j] = sa[pad(8 * tid + j)];
+        wh[j] = sh[pad(8 * tid + j)];
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) m[i] = __funnelshift_r(wa[i], wa[i + 1], sA) ^ __funnelshift_r(wh[i], wh[i + 1], sB);
+    }
+    if (tid == 0) {  // g_k[0] takes no x * H_k term ([p >= 1]): undo bit 0 of Gs[k]'s H contribution
+      const uint64_t pos = kT + k - 1;
+      m[0] ^= __funnelshift_r(__ldg(rk + (pos >> 5)), (pos >> 5) + 1 < gs_pitch ? __ldg(rk + (pos >> 5) + 1) : 0u,
+                              (int)(pos & 31)) & 1u;
     }
     conv_tile<false>(m, tile, sc, kTLog2);
     uint4* o = reinterpret_cast<uint4*>(out + k * kTWords + tid * 8);
