@@ -31,18 +31,42 @@ __device__ __forceinline__ uint32_t sm_get32(const uint32_t* row, int nwords, in
   return __funnelshift_r(lo, hi, s);
 }
 
+// 16-word registers shifted by whole words (ws < 16), left (towards higher words) or right, by
+// three/four conditional stages: no local memory, no shared-memory round trip.  ws is
+// warp-uniform in the callers (d >> 5 with 32 consecutive rows per warp).
+__device__ __forceinline__ void words_shl16(uint32_t (&t)[16], int ws) {
+#pragma unroll
+  for (int st = 8; st >= 1; st >>= 1)
+    if (ws & st) {
+#pragma unroll
+      for (int i = 15; i >= 0; --i) t[i] = i >= st ? t[i - st] : 0u;
+    }
+}
+__device__ __forceinline__ void words_shr16(uint32_t (&t)[16], int ws) {
+#pragma unroll
+  for (int st = 8; st >= 1; st >>= 1)
+    if (ws & st) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) t[i] = i + st < 16 ? t[i + st] : 0u;
+    }
+}
+
 // L1(256, 2^g) forward (carry) or inverse (overflow) on the chunk rows; m = this thread's row.
 template <bool INV>
 __device__ __forceinline__ void l1_tile(uint32_t (&m)[8], uint32_t* sc, int g, int d) {
   const int tid = threadIdx.x;
   uint32_t* my = sc + tid * kScPitch;
   uint32_t W[16];
-  __syncthreads();
+  const int ws = d >> 5, bs = d & 31;
+  // skew: W = m << d, in registers
+  {
+    uint32_t t[16];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) my[i] = m[i];
-  // skew: W = m << d  (own row only: no barrier needed)
+    for (int i = 0; i < 16; ++i) t[i] = i < 8 ? m[i] : 0u;
+    words_shl16(t, ws);
 #pragma unroll
-  for (int i = 0; i < 16; ++i) W[i] = sm_get32(my, 8, 32 * i - d);
+    for (int i = 0; i < 16; ++i) W[i] = __funnelshift_l(i ? t[i - 1] : 0u, t[i], bs);
+  }
   // subset-zeta over the g row bits: rows with bit b clear ^= row | 2^b
   for (int b = 0; b < g; ++b) {
     const bool lower = !((d >> b) & 1);
@@ -64,13 +88,11 @@ __device__ __forceinline__ void l1_tile(uint32_t (&m)[8], uint32_t* sc, int g, i
       }
     }
   }
-  // unskew: G = W >> d
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < 16; ++i) my[i] = W[i];
+  // unskew: G = W >> d, in registers
   uint32_t G[16];
+  words_shr16(W, ws);
 #pragma unroll
-  for (int i = 0; i < 16; ++i) G[i] = sm_get32(my, 16, 32 * i + d);
+  for (int i = 0; i < 16; ++i) G[i] = __funnelshift_r(W[i], i < 15 ? W[i + 1] : 0u, bs);
   // carry (forward) / overflow (inverse) with the previous row's high half H_{d-1}
   __syncthreads();
 #pragma unroll
