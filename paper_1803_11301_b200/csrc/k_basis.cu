@@ -41,16 +41,6 @@ int sm_count() {
   return n;
 }
 
-__device__ __forceinline__ uint32_t g_get32(const uint32_t* __restrict__ row, uint64_t nwords, int64_t pos) {
-  if (pos <= -32) return 0u;
-  const int64_t iw = pos >> 5;
-  const uint32_t s = (uint32_t)(pos & 31);
-  const uint32_t lo = (iw >= 0 && (uint64_t)iw < nwords) ? __ldg(row + iw) : 0u;
-  if (!s) return lo;
-  const uint32_t hi = (iw + 1 >= 0 && (uint64_t)(iw + 1) < nwords) ? __ldg(row + iw + 1) : 0u;
-  return __funnelshift_r(lo, hi, s);
-}
-
 // ------------------------------------------------------------------ generic in-place pass (K > 32)
 __global__ void bc_pass_kernel(uint32_t* __restrict__ w, uint64_t nwords, uint64_t S, uint64_t D, int inverse,
                                uint64_t w_first, uint64_t nw_span, uint64_t nspans, uint64_t rlo, uint64_t rhi,
@@ -274,12 +264,25 @@ __global__ void __launch_bounds__(256) carry_rows_kernel(const uint32_t* __restr
 // F_d[p] = Gs[d][p+d] ^ (d >= 1 ? Gs[d-1][t+p+d-1] : 0)
 __global__ void overflow_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch, uint32_t* __restrict__ out,
                                 uint64_t D) {
+  // A warp covers 32 consecutive output words of one row: both bit offsets are warp-uniform, so each
+  // span is one coalesced load per lane, the neighbour word comes by shuffle (lane 31 loads it).
   const uint64_t total = D * kTWords;
+  const int lane = threadIdx.x & 31;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t d = k / kTWords, w = k % kTWords;
-    const int64_t p = (int64_t)w * 32;
-    uint32_t v = g_get32(gs + d * gs_pitch, gs_pitch, p + (int64_t)d);
-    if (d) v ^= g_get32(gs + (d - 1) * gs_pitch, gs_pitch, (int64_t)kT + p + (int64_t)d - 1);
+    const uint32_t* r0 = gs + d * gs_pitch;
+    const uint64_t ia = w + (d >> 5);
+    uint32_t x = __ldg(r0 + ia), y = __shfl_down_sync(0xFFFFFFFFu, x, 1);
+    if (lane == 31) y = ia + 1 < gs_pitch ? __ldg(r0 + ia + 1) : 0u;
+    uint32_t v = __funnelshift_r(x, y, (int)(d & 31));
+    if (d) {
+      const uint32_t* r1 = r0 - gs_pitch;
+      const uint64_t pos = kT + d - 1, ib = w + (pos >> 5);
+      uint32_t xb = ib < gs_pitch ? __ldg(r1 + ib) : 0u;
+      uint32_t yb = __shfl_down_sync(0xFFFFFFFFu, xb, 1);
+      if (lane == 31) yb = ib + 1 < gs_pitch ? __ldg(r1 + ib + 1) : 0u;
+      v ^= __funnelshift_r(xb, yb, (int)(pos & 31));
+    }
     out[k] = v;
   }
 }
