@@ -226,15 +226,25 @@ __global__ void __launch_bounds__(256) carry_rows_kernel(const uint32_t* __restr
     const uint64_t a0 = k >> 5, b0 = (kT + k - 1) >> 5;
     const int sA = (int)(k & 31), sB = (int)((kT + k - 1) & 31);
     __syncthreads();  // the previous row's conversion is done with the shared tile
-    for (int w = tid; w <= kTWords; w += 256) {  // coalesced: 2049 words per span
-      sa[pad(w)] = __ldg(rk + a0 + w);
-      const uint64_t wb = b0 + w;
-      uint32_t h = 0;
-      if (wb < gs_pitch) {
-        h = __ldg(rk + wb);
-        if (k) h ^= __ldg(rk1 + wb);
+    {  // coalesced: 2049 words per span, every load of the thread issued before any store
+      uint32_t va[9], vb[9], vc[9];
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        const int w = tid + 256 * j;
+        const uint64_t wb = b0 + w;
+        const bool in = w <= kTWords;
+        va[j] = in ? __ldg(rk + a0 + w) : 0u;
+        vb[j] = in && wb < gs_pitch ? __ldg(rk + wb) : 0u;
+        vc[j] = in && wb < gs_pitch && k ? __ldg(rk1 + wb) : 0u;
       }
-      sh[pad(w)] = h;
+#pragma unroll
+      for (int j = 0; j < 9; ++j) {
+        const int w = tid + 256 * j;
+        if (w <= kTWords) {
+          sa[pad(w)] = va[j];
+          sh[pad(w)] = vb[j] ^ vc[j];
+        }
+      }
     }
     __syncthreads();
     uint32_t m[8];
@@ -587,8 +597,8 @@ int grid_cap(uint64_t items, int per_sm) {
 
 void conv_rows(uint32_t* data, uint64_t nwords, int r, bool inv, cudaStream_t s) {
   const uint64_t tiles = nwords < 2048 ? 1 : nwords / 2048;
-  if (inv) conv_rows_kernel<true><<<grid_cap(tiles, 4), 256, kTileSmem, s>>>(data, nwords, r);
-  else conv_rows_kernel<false><<<grid_cap(tiles, 4), 256, kTileSmem, s>>>(data, nwords, r);
+  if (inv) conv_rows_kernel<true><<<grid_cap(tiles, 7), 256, kTileSmem, s>>>(data, nwords, r);
+  else conv_rows_kernel<false><<<grid_cap(tiles, 7), 256, kTileSmem, s>>>(data, nwords, r);
   FPM_LAUNCH_CHECK();
 }
 
@@ -710,7 +720,7 @@ void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s) {
   };
   if (!inv) {
     l1_zeta(w);
-    carry_rows_kernel<<<grid_cap(D, 4), 256, kTileSmem, s>>>(scratch, wsk, w, D);
+    carry_rows_kernel<<<grid_cap(D, 7), 256, kTileSmem, s>>>(scratch, wsk, w, D);
     FPM_LAUNCH_CHECK();
     conv_cols(w, scratch, lgD, false, s);
   } else {
