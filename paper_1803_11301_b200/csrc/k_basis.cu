@@ -112,7 +112,7 @@ constexpr int kZP = 36;  // shared row pitch (16 B aligned, conflict-free for bo
 // BITSKEW: the bit-granular skew path (neighbour words by shuffle) needs the registers of 2 CTAs/SM;
 // word-aligned or no skew runs at 3 CTAs/SM.
 template <bool BITSKEW>
-__global__ void __launch_bounds__(256, BITSKEW ? 2 : 3) zeta_kernel(const uint32_t* __restrict__ src, uint64_t src_pitch,
+__global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32_t* __restrict__ src, uint64_t src_pitch,
                                                    uint32_t* __restrict__ dst, uint64_t dst_pitch, uint64_t D,
                                                    int b0, int nb, Skew skew, uint64_t src_row_words,
                                                    uint64_t windows) {
@@ -129,7 +129,16 @@ __global__ void __launch_bounds__(256, BITSKEW ? 2 : 3) zeta_kernel(const uint32
     // ---- mapping A: load, stages on tile-row bits 3..7
     const int c = tid & 31;
     uint32_t a[32];
-    if (!BITSKEW && skew.mask) {  // word-aligned skew: plain coalesced loads
+    if (!BITSKEW && nb == 8) {  // full 256-row groups: one window per CTA, rows at a fixed stride
+      const uint64_t dstep = (uint64_t)8 << b0;
+      uint64_t d = base + ((uint64_t)(tid >> 5) << b0);
+      const int64_t w0 = (int64_t)(wb * kZW) + c;
+#pragma unroll
+      for (int k = 0; k < 32; ++k, d += dstep) {
+        const int64_t iw = skew.mask ? w0 - (int64_t)((((d >> skew.lo) & skew.mask) << skew.log) >> 5) : w0;
+        a[k] = (iw >= 0 && iw < (int64_t)src_row_words) ? __ldg(src + d * src_pitch + iw) : 0u;
+      }
+    } else if (!BITSKEW && skew.mask) {  // word-aligned skew: plain coalesced loads
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         const int R = (tid >> 5) + 8 * k;
