@@ -153,11 +153,13 @@ __global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32
       // neighbour word comes by shuffle and a funnel shift aligns the window.
       uint32_t e[32];
       int sh[32];
+      const bool full = nb == 8;  // one window per CTA: wi = wb, rows at stride 8 << b0
+      uint64_t dfull = base + ((uint64_t)(tid >> 5) << b0);
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
+      for (int k = 0; k < 32; ++k, dfull += (uint64_t)8 << b0) {
         const int R = (tid >> 5) + 8 * k;
-        const uint64_t d = base + ((uint64_t)(R & ((1 << nb) - 1)) << b0);
-        const uint64_t wi = wb * wpc + (R >> nb);
+        const uint64_t d = full ? dfull : base + ((uint64_t)(R & ((1 << nb) - 1)) << b0);
+        const uint64_t wi = full ? wb : wb * wpc + (R >> nb);
         const uint32_t* row = src + d * src_pitch;
         const int64_t pos0 = (int64_t)(wi * 32 * kZW) - (int64_t)(((d >> skew.lo) & skew.mask) << skew.log);
         const int64_t iw = (pos0 >> 5) + c;
@@ -206,12 +208,19 @@ __global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32
                                                    bq[k].z ^ bq[k | (1 << b)].z, bq[k].w ^ bq[k | (1 << b)].w);
       }
     }
+    if (nb == 8) {  // one window, rows base + (R0 + k) << b0
+      uint32_t* p = dst + (base + ((uint64_t)R0 << b0)) * dst_pitch + wb * kZW + 4 * q;
+      const uint64_t step = ((uint64_t)1 << b0) * dst_pitch;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int R = R0 + k;
-      const uint64_t d = base + ((uint64_t)(R & ((1 << nb) - 1)) << b0);
-      const uint64_t wi = wb * wpc + (R >> nb);
-      if (wi < windows) *reinterpret_cast<uint4*>(dst + d * dst_pitch + wi * kZW + 4 * q) = bq[k];
+      for (int k = 0; k < 8; ++k) *reinterpret_cast<uint4*>(p + k * step) = bq[k];
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int R = R0 + k;
+        const uint64_t d = base + ((uint64_t)(R & ((1 << nb) - 1)) << b0);
+        const uint64_t wi = wb * wpc + (R >> nb);
+        if (wi < windows) *reinterpret_cast<uint4*>(dst + d * dst_pitch + wi * kZW + 4 * q) = bq[k];
+      }
     }
     __syncthreads();
   }
