@@ -358,13 +358,16 @@ __global__ void __launch_bounds__(256) slab_kernel(uint32_t* __restrict__ data, 
 // ------------------------------------------------------------------ conv(256) over units, by L1(16, 16)
 // conv(256) of 256 units (8 KiB rows; unit u = 16 d + v) evaluated per bit column by the same
 // recursion as the whole conversion one level down: C_rows(conv16 over v) o C_cols(conv16 over d)
-// o L1(16, 16), with the L1 skew in units.  A CTA of 512 threads owns 32 consecutive words of each
-// of the 256 units; thread (r = tid >> 5, c = tid & 31).  Three register-local phases (zeta over d,
+// o L1(16, 16), with the L1 skew in units.  A CTA of 16 x kC256Cols threads owns kC256Cols words of each
+// of the 256 units; thread (r = tid / cols, c = tid % cols).  Three register-local phases (zeta over d,
 // conv16 over k, conv16 over v) with shared-memory exchanges between them: 28 B of shared traffic
 // per word instead of the ~80 B of the 12 row passes.  Skewed rows Z[d][s] (s < 32 unit slots):
 // Z[d][v + d] = F_d[v].
-constexpr int kC256Threads = 512;
-constexpr size_t kC256Smem = 16 * 32 * 32 * sizeof(uint32_t);  // Z[16][32][32]
+// kC256Cols words of each unit per CTA (16 x kC256Cols threads, 2 CTAs/SM: one CTA's load phase
+// overlaps the other's shared-memory phases).
+constexpr int kC256Cols = 16;
+constexpr int kC256Threads = 16 * kC256Cols;
+constexpr size_t kC256Smem = 16 * 32 * kC256Cols * sizeof(uint32_t);  // Z[16][32][cols]
 
 // conv16 over 16 register values (build_schedule(16): (16,6), (8,3), (16,4), (4,1)); increasing q
 // reads every source before it is overwritten (sources sit above their targets).
@@ -423,15 +426,15 @@ struct CarrySrc {
 };
 
 template <bool INV>
-__global__ void __launch_bounds__(kC256Threads, 1) conv256_units_kernel(uint32_t* __restrict__ data, UnitMap um,
+__global__ void __launch_bounds__(kC256Threads, 2) conv256_units_kernel(uint32_t* __restrict__ data, UnitMap um,
                                                                         uint64_t nitems, CarrySrc cs) {
   extern __shared__ uint32_t Z[];  // [d][s][c], d < 16, s < 32, c < 32
-  const int tid = threadIdx.x, c = tid & 31, r = tid >> 5;
-  constexpr int kCols = kTWords / 32;  // 32-word column blocks per unit
-  auto zi = [](int d, int s, int cc) { return (d * 32 + s) * 32 + cc; };
+  const int tid = threadIdx.x, c = tid % kC256Cols, r = tid / kC256Cols;
+  constexpr int kCols = kTWords / kC256Cols;  // column blocks per unit
+  auto zi = [](int d, int s, int cc) { return (d * 32 + s) * kC256Cols + cc; };
   for (uint64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
     const uint64_t grp = it / kCols;
-    const uint64_t colw = (it % kCols) * 32 + c;
+    const uint64_t colw = (it % kCols) * kC256Cols + c;
     uint32_t* const gbase = data + um.row(grp, 0) * kTWords + colw;
     const uint32_t ustep = (uint32_t)(um.ustride * kTWords);  // 256 units x ustep < 2^32 words
     auto at = [&](int u) -> uint32_t* { return gbase + (uint32_t)u * ustep; };
@@ -648,7 +651,7 @@ void conv256_units(uint32_t* w, uint64_t ngroups, uint64_t ustride, uint64_t gst
     attr = true;
   }
   UnitMap um{ustride, gstride, ngroups};
-  const uint64_t items = ngroups * (kTWords / 32);
+  const uint64_t items = ngroups * (kTWords / kC256Cols);
   if (inv) conv256_units_kernel<true><<<grid_cap(items, 2), kC256Threads, kC256Smem, s>>>(w, um, items, cs);
   else conv256_units_kernel<false><<<grid_cap(items, 2), kC256Threads, kC256Smem, s>>>(w, um, items, cs);
   FPM_LAUNCH_CHECK();
