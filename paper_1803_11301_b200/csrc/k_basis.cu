@@ -130,14 +130,20 @@ __global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32
     const int c = tid & 31;
     uint32_t a[32];
     if (!BITSKEW && nb == 8) {  // full 256-row groups: one window per CTA, rows at a fixed stride
+      // Within a full group the skew is affine in the row (its digit never wraps): the word offset
+      // advances by a constant per 8 rows, so addresses are one add per load.
       const uint64_t dstep = (uint64_t)8 << b0;
-      uint64_t d = base + ((uint64_t)(tid >> 5) << b0);
-      const int64_t w0 = (int64_t)(wb * kZW) + c;
+      const uint64_t d0 = base + ((uint64_t)(tid >> 5) << b0);
+      auto skw = [&](uint64_t d) -> int64_t {
+        return skew.mask ? (int64_t)((((d >> skew.lo) & skew.mask) << skew.log) >> 5) : 0;
+      };
+      const int64_t s0 = skw(d0), sstep = skw(d0 + dstep) - s0;
+      const uint32_t* p = src + d0 * src_pitch + wb * kZW + c - s0;   // row d0, word iw
+      int64_t iw = (int64_t)(wb * kZW) + c - s0;
+      const int64_t pstep = (int64_t)(dstep * src_pitch) - sstep;
 #pragma unroll
-      for (int k = 0; k < 32; ++k, d += dstep) {
-        const int64_t iw = skew.mask ? w0 - (int64_t)((((d >> skew.lo) & skew.mask) << skew.log) >> 5) : w0;
-        a[k] = (iw >= 0 && iw < (int64_t)src_row_words) ? __ldg(src + d * src_pitch + iw) : 0u;
-      }
+      for (int k = 0; k < 32; ++k, p += pstep, iw -= sstep)
+        a[k] = (iw >= 0 && iw < (int64_t)src_row_words) ? __ldg(p) : 0u;
     } else if (!BITSKEW && skew.mask) {  // word-aligned skew: plain coalesced loads
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
