@@ -159,13 +159,28 @@ __global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32
       // neighbour word comes by shuffle and a funnel shift aligns the window.
       uint32_t e[32];
       int sh[32];
-      const bool full = nb == 8;  // one window per CTA: wi = wb, rows at stride 8 << b0
-      uint64_t dfull = base + ((uint64_t)(tid >> 5) << b0);
+      if (nb == 8) {
+        // full group: skew bits affine in the row (d & 255 = R, base 256-aligned): per load one add
+        const uint64_t dstep = (uint64_t)8 << b0;
+        const uint64_t d0 = base + ((uint64_t)(tid >> 5) << b0);
+        const int64_t s0 = (int64_t)(((d0 >> skew.lo) & skew.mask) << skew.log);
+        const int64_t sstep = (int64_t)((((d0 + dstep) >> skew.lo) & skew.mask) << skew.log) - s0;
+        int64_t pos = (int64_t)(wb * 32 * kZW) - s0;      // bit position of this row's window
+        const uint32_t* row = src + d0 * src_pitch;
+        const uint64_t rstep = dstep * src_pitch;
 #pragma unroll
-      for (int k = 0; k < 32; ++k, dfull += (uint64_t)8 << b0) {
+        for (int k = 0; k < 32; ++k, pos -= sstep, row += rstep) {
+          const int64_t iw = (pos >> 5) + c;
+          sh[k] = (int)(pos & 31);
+          a[k] = (iw >= 0 && iw < (int64_t)src_row_words) ? __ldg(row + iw) : 0u;
+          e[k] = (c == 31 && iw + 1 >= 0 && iw + 1 < (int64_t)src_row_words) ? __ldg(row + iw + 1) : 0u;
+        }
+      } else {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
         const int R = (tid >> 5) + 8 * k;
-        const uint64_t d = full ? dfull : base + ((uint64_t)(R & ((1 << nb) - 1)) << b0);
-        const uint64_t wi = full ? wb : wb * wpc + (R >> nb);
+        const uint64_t d = base + ((uint64_t)(R & ((1 << nb) - 1)) << b0);
+        const uint64_t wi = wb * wpc + (R >> nb);
         const uint32_t* row = src + d * src_pitch;
         const int64_t pos0 = (int64_t)(wi * 32 * kZW) - (int64_t)(((d >> skew.lo) & skew.mask) << skew.log);
         const int64_t iw = (pos0 >> 5) + c;
@@ -173,6 +188,7 @@ __global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32
         const bool ok = wi < windows;
         a[k] = (ok && iw >= 0 && iw < (int64_t)src_row_words) ? __ldg(row + iw) : 0u;
         e[k] = (ok && c == 31 && iw + 1 >= 0 && iw + 1 < (int64_t)src_row_words) ? __ldg(row + iw + 1) : 0u;
+      }
       }
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
