@@ -448,7 +448,7 @@ struct CarrySrc {
 };
 
 template <bool INV>
-__global__ void __launch_bounds__(kC256Threads, 2) conv256_units_kernel(uint32_t* __restrict__ data, UnitMap um,
+__global__ void __launch_bounds__(kC256Threads, INV ? 3 : 4) conv256_units_kernel(uint32_t* __restrict__ data, UnitMap um,
                                                                         uint64_t nitems, CarrySrc cs) {
   extern __shared__ uint32_t Z[];  // [d][s][c], d < 16, s < 32, c < 32
   const int tid = threadIdx.x, c = tid % kC256Cols, r = tid / kC256Cols;
@@ -674,8 +674,8 @@ void conv256_units(uint32_t* w, uint64_t ngroups, uint64_t ustride, uint64_t gst
   }
   UnitMap um{ustride, gstride, ngroups};
   const uint64_t items = ngroups * (kTWords / kC256Cols);
-  if (inv) conv256_units_kernel<true><<<grid_cap(items, 2), kC256Threads, kC256Smem, s>>>(w, um, items, cs);
-  else conv256_units_kernel<false><<<grid_cap(items, 2), kC256Threads, kC256Smem, s>>>(w, um, items, cs);
+  if (inv) conv256_units_kernel<true><<<grid_cap(items, 3), kC256Threads, kC256Smem, s>>>(w, um, items, cs);
+  else conv256_units_kernel<false><<<grid_cap(items, 4), kC256Threads, kC256Smem, s>>>(w, um, items, cs);
   FPM_LAUNCH_CHECK();
 }
 
