@@ -169,4 +169,42 @@ __device__ __forceinline__ uint4 m4r_mul(const uint4* __restrict__ tab, uint4 x,
   return x4(acc0, acc1);
 }
 
+// ---------------------------------------------------------------- rotated 4-bit tables, 8 at a time
+// For tile layers whose twiddles are shared by only 2^5..2^7 butterflies: 32 nibble-chunk tables of
+// w*(v << 4c), 8 KiB per twiddle, entry (c, v) at uint4 index v*32 + c (16-byte bank group c & 7);
+// lane q visits chunks (k + q) & 31, so a quarter-warp's LDS.128 never conflicts.  Building 8
+// tables costs what one M8 table does (4096 stores), lookups are 32 per product.
+constexpr int kM4TabUint4 = 512;
+
+// 256 threads build tables t = 0..7; thread (table t = tid >> 5, chunk tid & 31) passes w = w_t.
+__device__ __forceinline__ void m4s_build8(uint4* __restrict__ tab, uint4 w, int tid) {
+  const int t = tid >> 5, c = tid & 31;
+  uint4 r[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) r[j] = gf_mul_xk(w, (unsigned)(4 * c + j));
+  uint4* dst = tab + t * kM4TabUint4 + c;
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  dst[0] = acc;
+#pragma unroll
+  for (int v = 1; v < 16; ++v) {  // gray-code walk: one XOR per entry
+    const int g = v ^ (v >> 1), gp = (v - 1) ^ ((v - 1) >> 1);
+    const int bit = __ffs(g ^ gp) - 1;
+    acc = x4(acc, r[bit]);
+    dst[g * 32] = acc;
+  }
+}
+
+__device__ __forceinline__ uint4 m4s_mul(const uint4* __restrict__ tab, uint4 x, int q) {
+  uint4 acc0 = make_uint4(0, 0, 0, 0), acc1 = make_uint4(0, 0, 0, 0);
+  auto word = [&](int c) { return c < 16 ? (c < 8 ? x.x : x.y) : (c < 24 ? x.z : x.w); };
+#pragma unroll
+  for (int k = 0; k < 32; k += 2) {
+    const int c0 = (k + q) & 31, c1 = (k + 1 + q) & 31;
+    const uint32_t n0 = (word(c0) >> (4 * (c0 & 7))) & 15u, n1 = (word(c1) >> (4 * (c1 & 7))) & 15u;
+    acc0 = x4(acc0, tab[n0 * 32 + c0]);
+    acc1 = x4(acc1, tab[n1 * 32 + c1]);
+  }
+  return x4(acc0, acc1);
+}
+
 }  // namespace fpm

@@ -156,6 +156,8 @@ __global__ void __launch_bounds__(kTop4Threads, 1) fft_top4_kernel(uint4* __rest
 // butterflies: those use an M8 table built in shared memory (tab != nullptr: 64 KiB + 144 rows
 // after the tile) instead of the generic multiply.
 constexpr unsigned kTabLayer = 8;
+// Layers [kM4Layer, kTabLayer): rotated 4-bit tables for 8 twiddles at a time (gf128.cuh m4s_*).
+constexpr unsigned kM4Layer = 6;
 template <bool INV>
 __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, unsigned l, uint64_t tile_idx,
                                             const TwiddleSrc& tw, uint4* __restrict__ tab) {
@@ -165,6 +167,34 @@ __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, u
     const uint64_t bhi = tile_idx << (T - 1 - i);  // global block index of the tile's first block
     // w = v_{l+64-i} ^ C2P(2*(bhi + blk)) = Z ^ C2P(2*blk)  (bit ranges disjoint, C2P linear)
     const uint4 Z = twiddle(tw, l, i, bhi);
+    if (tab && i >= kM4Layer && i < kTabLayer && (npairs >> i) % 8 == 0) {
+      // 2^(T-1-i) twiddles of 2^i butterflies each: rotated 4-bit tables, 8 twiddles per round
+      const int q = threadIdx.x & 7;
+      const int nblk = npairs >> i;
+      for (int b0 = 0; b0 < nblk; b0 += 8) {
+        const uint4 w = x4(Z, c2p2(tw.c2p, (uint64_t)(b0 + (threadIdx.x >> 5))));
+        __syncthreads();  // previous round's lookups done
+        m4s_build8(tab, w, threadIdx.x);
+        __syncthreads();
+        for (int p = threadIdx.x; p < (8 << i); p += blockDim.x) {
+          const int t = p >> i, j = p & ((1 << i) - 1), blk = b0 + t;
+          const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+          const uint4* tb = tab + t * kM4TabUint4;
+          uint4 u0 = s[i0], u1 = s[i1];
+          if (!INV) {
+            u0 = x4(u0, m4s_mul(tb, u1, q));
+            u1 = x4(u1, u0);
+          } else {
+            u1 = x4(u1, u0);
+            u0 = x4(u0, m4s_mul(tb, u1, q));
+          }
+          s[i0] = u0;
+          s[i1] = u1;
+        }
+      }
+      __syncthreads();
+      continue;
+    }
     if (tab && i >= kTabLayer) {
       const int q = threadIdx.x & 7;
       for (int blk = 0; blk < (npairs >> i); ++blk) {
