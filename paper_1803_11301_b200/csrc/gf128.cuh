@@ -187,9 +187,8 @@ __device__ __forceinline__ void m4s_build8(uint4* __restrict__ tab, uint4 w, int
   dst[0] = acc;
 #pragma unroll
   for (int v = 1; v < 16; ++v) {  // gray-code walk: one XOR per entry
-    const int g = v ^ (v >> 1), gp = (v - 1) ^ ((v - 1) >> 1);
-    const int bit = __ffs(g ^ gp) - 1;
-    acc = x4(acc, r[bit]);
+    const int g = v ^ (v >> 1);  // Gray code: step v flips bit ctz(v)
+    acc = x4(acc, r[(v & 1) ? 0 : (v & 2) ? 1 : (v & 4) ? 2 : 3]);
     dst[g * 32] = acc;
   }
 }

@@ -84,4 +84,41 @@ __device__ __forceinline__ uint2 g8_mul(const uint2* __restrict__ tab, uint2 x, 
   return x2(acc0, acc1);
 }
 
+// ---------------------------------------------------------------- 4-bit tables, 16 at a time
+// For tile layers whose twiddles are shared by only 2^4..2^7 butterflies: 16 nibble-chunk tables of
+// w*(v << 4c), 2 KiB per twiddle, entry (c, v) at uint2 index v*16 + c (8-byte slot c of a 128-byte
+// row); lane L visits chunks (k + L) & 15, so the 16 lanes of a half-warp hit 16 distinct slots:
+// 16 conflict-free LDS.64 per product.
+constexpr int kG4TabUint2 = 256;
+
+// 256 threads build tables t = 0..15 (thread: table tid >> 4, chunk tid & 15; it passes w = w_t).
+__device__ __forceinline__ void g4_build16(uint2* __restrict__ tab, uint2 w, int tid) {
+  const int t = tid >> 4, c = tid & 15;
+  uint2 r[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) r[j] = gf64_mul_xk(w, (unsigned)(4 * c + j));
+  uint2* dst = tab + t * kG4TabUint2 + c;
+  uint2 acc = make_uint2(0, 0);
+  dst[0] = acc;
+#pragma unroll
+  for (int v = 1; v < 16; ++v) {  // gray-code walk
+    const int g = v ^ (v >> 1);  // Gray code: step v flips bit ctz(v)
+    acc = x2(acc, r[(v & 1) ? 0 : (v & 2) ? 1 : (v & 4) ? 2 : 3]);
+    dst[g * 16] = acc;
+  }
+}
+
+__device__ __forceinline__ uint2 g4_mul(const uint2* __restrict__ tab, uint2 x, int lane) {
+  uint2 acc0 = make_uint2(0, 0), acc1 = make_uint2(0, 0);
+#pragma unroll
+  for (int k = 0; k < 16; k += 2) {
+    const int c0 = (k + lane) & 15, c1 = (k + 1 + lane) & 15;
+    const uint32_t n0 = ((c0 < 8 ? x.x : x.y) >> (4 * (c0 & 7))) & 15u;
+    const uint32_t n1 = ((c1 < 8 ? x.x : x.y) >> (4 * (c1 & 7))) & 15u;
+    acc0 = x2(acc0, tab[n0 * 16 + c0]);
+    acc1 = x2(acc1, tab[n1 * 16 + c1]);
+  }
+  return x2(acc0, acc1);
+}
+
 }  // namespace fpm

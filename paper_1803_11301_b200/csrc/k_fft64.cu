@@ -155,6 +155,8 @@ __global__ void __launch_bounds__(kTop4Threads64, 2) fft64_top4_kernel(uint2* __
 
 // ------------------------------------------------------------------ tile layers (i < T)
 constexpr unsigned kTabLayer64 = 8;  // layers >= 8 of a 256-thread tile: <= 8 twiddles, G8 tables
+// Layers [kG4Layer, kTabLayer64): 4-bit tables for 16 twiddles per round (gf64.cuh g4_*).
+constexpr unsigned kG4Layer = 6;
 template <bool INV>
 __device__ __forceinline__ void tile_layers64(uint2* __restrict__ s, unsigned T, uint64_t tile_idx,
                                               const TwiddleSrc64& tw, uint2* __restrict__ tab) {
@@ -164,6 +166,32 @@ __device__ __forceinline__ void tile_layers64(uint2* __restrict__ s, unsigned T,
     const unsigned i = INV ? step : T - 1 - step;
     const uint64_t bhi = tile_idx << (T - 1 - i);
     const uint2 Z = twiddle64(tw, i, bhi);  // w = Z ^ C2P(2 blk) (disjoint bit ranges, C2P linear)
+    if (tab && i >= kG4Layer && i < kTabLayer64 && (npairs >> i) % 16 == 0) {
+      const int nblk = npairs >> i;
+      for (int b0 = 0; b0 < nblk; b0 += 16) {
+        const uint2 w = x2(Z, c2p2_64(tw.c2p, (uint64_t)(b0 + (threadIdx.x >> 4))));
+        __syncthreads();  // previous round's lookups done
+        g4_build16(tab, w, threadIdx.x);
+        __syncthreads();
+        for (int p = threadIdx.x; p < (16 << i); p += blockDim.x) {
+          const int t = p >> i, j = p & ((1 << i) - 1), blk = b0 + t;
+          const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+          const uint2* tb = tab + t * kG4TabUint2;
+          uint2 u0 = s[i0], u1 = s[i1];
+          if (!INV) {
+            u0 = x2(u0, g4_mul(tb, u1, lane));
+            u1 = x2(u1, u0);
+          } else {
+            u1 = x2(u1, u0);
+            u0 = x2(u0, g4_mul(tb, u1, lane));
+          }
+          s[i0] = u0;
+          s[i1] = u1;
+        }
+      }
+      __syncthreads();
+      continue;
+    }
     if (tab && i >= kTabLayer64) {
       for (int blk = 0; blk < (npairs >> i); ++blk) {
         g8_build(tab, tab + kG8Uint2, x2(Z, c2p2_64(tw.c2p, (uint64_t)blk)), threadIdx.x);
