@@ -151,7 +151,9 @@ enum { kStBasis = 0, kStEncode, kStBfly, kStPointwise, kStIBfly, kStDecode, kStI
 struct DevBuf {
   void* p = nullptr;
   cudaStream_t s;
-  DevBuf(size_t bytes, cudaStream_t st) : s(st) { FPM_CUDA(cudaMallocAsync(&p, bytes, st)); }
+  DevBuf(size_t bytes, cudaStream_t st) : s(st) {
+    if (bytes) FPM_CUDA(cudaMallocAsync(&p, bytes, st));
+  }
   ~DevBuf() { if (p) cudaFreeAsync(p, s); }
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
@@ -240,7 +242,12 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
   FPM_CUDA(cudaGetDevice(&dev));
   const typename F::Tw tw = F::twiddles(dev, l);
   const size_t n = p.n_bits, n_p = p.n_p;
-  DevBuf P(n / 8, s), EA(n_p * sizeof(E), s), EB(n_p * sizeof(E), s);
+  // The n-bit work array: the product buffer itself when it spans exactly n bits (equal-length
+  // power-of-two operands: out_bits = n - 1), else a scratch array trimmed into d_c at the end.
+  const bool in_place = out_words * 64 == n;
+  DevBuf P(in_place ? 0 : n / 8, s), EA(n_p * sizeof(E), s), EB(n_p * sizeof(E), s);
+  uint64_t* const work = in_place ? d_c : P.as<uint64_t>();
+  uint32_t* const work32 = reinterpret_cast<uint32_t*>(work);
   const uint64_t* xs[2] = {d_a, d_b};
   const size_t xbits[2] = {a_bits, b_bits};
   E* es[2] = {EA.as<E>(), EB.as<E>()};
@@ -248,13 +255,13 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     wait_operand(k);
     clk.mark(kStBasis);
     const uint64_t half_words = n / 128;  // n/2 bits in uint64 words
-    load_operand_kernel<<<grid_1d(half_words), 256, 0, s>>>(P.as<uint64_t>(), half_words, xs[k], xbits[k]);
+    load_operand_kernel<<<grid_1d(half_words), 256, 0, s>>>(work, half_words, xs[k], xbits[k]);
     FPM_LAUNCH_CHECK();
     size_t count = (size_t)1 << log2_ceil(xbits[k]);
     if (count < 32) count = 32;
-    basis_cvt_device(P.as<uint32_t>(), count, xbits[k], false, s);
+    basis_cvt_device(work32, count, xbits[k], false, s);
     clk.mark(kStEncode);
-    F::encode(P.as<uint32_t>(), l, es[k], s);
+    F::encode(work32, l, es[k], s);
     clk.mark(kStBfly);
     F::top(es[k], l, T, false, tw, s);
     if (k == 0) F::tile(es[k], l, T, false, tw, s);
@@ -264,7 +271,7 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
   clk.mark(kStIBfly);
   F::top(EB.as<E>(), l, T, true, tw, s);
   clk.mark(kStDecode);
-  F::decode(EB.as<E>(), l, P.as<uint32_t>(), s);
+  F::decode(EB.as<E>(), l, work32, s);
   clk.mark(kStIBasis);
   // Each finished range of the product is trimmed into d_c (and copied out) right away.
   const FinalFn on_final = [&](uint64_t w0, uint64_t w1) {  // 32-bit word range of P
@@ -272,11 +279,13 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     // partition and only ever copies a word once both of its halves are final.
     const uint64_t q0 = std::min<uint64_t>((w0 + 1) / 2, out_words), q1 = std::min<uint64_t>((w1 + 1) / 2, out_words);
     if (q0 >= q1) return;
-    store_product_kernel<<<grid_1d(q1 - q0), 256, 0, s>>>(d_c, P.as<uint64_t>(), out_bits, q0, q1);
-    FPM_LAUNCH_CHECK();
+    if (!in_place) {  // (in place, bit n-1 is the product's, which is zero: deg < out_bits)
+      store_product_kernel<<<grid_1d(q1 - q0), 256, 0, s>>>(d_c, work, out_bits, q0, q1);
+      FPM_LAUNCH_CHECK();
+    }
     copy_out(q0, q1);
   };
-  basis_cvt_device(P.as<uint32_t>(), n, n, true, s, &on_final);
+  basis_cvt_device(work32, n, n, true, s, &on_final);
   clk.finish();
 }
 
