@@ -255,11 +255,16 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     wait_operand(k);
     clk.mark(kStBasis);
     const uint64_t half_words = n / 128;  // n/2 bits in uint64 words
-    load_operand_kernel<<<grid_1d(half_words), 256, 0, s>>>(work, half_words, xs[k], xbits[k]);
-    FPM_LAUNCH_CHECK();
     size_t count = (size_t)1 << log2_ceil(xbits[k]);
     if (count < 32) count = 32;
-    basis_cvt_device(work32, count, xbits[k], false, s);
+    if (xbits[k] == n / 2 && count == n / 2 && count >= ((size_t)1 << 17) && count <= ((size_t)1 << 32)) {
+      // the operand fills the conversion exactly: convert straight from the caller's buffer
+      basis_cvt_device(work32, count, xbits[k], false, s, nullptr, reinterpret_cast<const uint32_t*>(xs[k]));
+    } else {
+      load_operand_kernel<<<grid_1d(half_words), 256, 0, s>>>(work, half_words, xs[k], xbits[k]);
+      FPM_LAUNCH_CHECK();
+      basis_cvt_device(work32, count, xbits[k], false, s);
+    }
     clk.mark(kStEncode);
     F::encode(work32, l, es[k], s);
     clk.mark(kStBfly);

@@ -84,8 +84,10 @@ const DeviceTables& device_tables(int device);
 // as the work enqueued on s so far leaves them final, so callers can start copying them out while
 // the rest of the conversion runs; every word is reported exactly once.
 using FinalFn = std::function<void(uint64_t w0, uint64_t w1)>;
+// src (forward, 2^17..2^32 bits only; may be null): the unconverted array is read from src and the
+// result written to w (w's prior contents are ignored).
 void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s,
-                      const FinalFn* on_final = nullptr);
+                      const FinalFn* on_final = nullptr, const uint32_t* src = nullptr);
 
 // Encode / decode (k_codec.cu).  poly has 128 * 2^l bits; ev has 2^l uint4.
 void encode_device(const uint32_t* poly, unsigned l, uint4* ev, cudaStream_t s);

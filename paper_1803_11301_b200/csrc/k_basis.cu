@@ -742,7 +742,9 @@ void conv_cols(uint32_t* w, uint32_t* scratch, int lgD, bool inv, cudaStream_t s
 }
 
 // conv(2^K) for 17 <= K <= 32 on w (2^K bits).  scratch >= 2^(K-16) * (2^16 + max(2^(K-16), 1024)) bits.
-void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s) {
+// src (forward only, may be null): read the unconverted rows from src instead of w (w is first
+// written by the carry pass, so an input buffer need not be copied into w beforehand).
+void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s, const uint32_t* src = nullptr) {
   const int lgD = K - kTLog2;
   const uint64_t D = (uint64_t)1 << lgD;
   const uint64_t wsk_bits = kT + std::max<uint64_t>(D, 32 * kZW);
@@ -762,7 +764,7 @@ void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s) {
     if (nb_hi) zeta(s1, w1, scratch, wsk, D, 8, nb_hi, hi_skew, windows, s, w1);
   };
   if (!inv) {
-    l1_zeta(w);
+    l1_zeta(src ? src : w);
     carry_rows_kernel<<<grid_cap(D, 7), 256, kTileSmem, s>>>(scratch, wsk, w, D);
     FPM_LAUNCH_CHECK();
     conv_cols(w, scratch, lgD, false, s);
@@ -801,7 +803,7 @@ struct Scratch {
 }  // namespace
 
 void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s,
-                      const FinalFn* on_final) {
+                      const FinalFn* on_final, const uint32_t* src) {
   if (n_bits < 4 || (n_bits & (n_bits - 1))) throw Error(kInvalid, "basis_cvt: length must be a power of two >= 4");
   set_smem_attr();
   int K = 0;
@@ -819,6 +821,8 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
     if (inverse && on_final) (*on_final)(0, nwords);
     return;
   }
+  if (src && (inverse || K <= kTLog2 || K > 32))
+    throw Error(kInvalid, "basis_cvt: a separate source is supported for forward 2^17..2^32-bit arrays");
   if (K <= kTLog2) {
     conv_rows(w, nwords, K, inverse, s);
     if (inverse && on_final) (*on_final)(0, nwords);
@@ -845,7 +849,7 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
     for (const Pass& p : top) run_big_pass(w, nwords, p, false, live_bits, s);
     for (uint64_t b = 0; b < nblocks; ++b) {
       if (b * block_words * 32 >= live_bits) continue;  // all-zero block stays zero
-      conv2d(w + b * block_words, Kb, inverse, scratch, s);
+      conv2d(w + b * block_words, Kb, inverse, scratch, s, src ? src + b * block_words : nullptr);
     }
     return;
   }
