@@ -212,3 +212,37 @@ def test_pointwise64(gpu, port):
     u = rnd_words(rng, 64 * 5000)
     v = rnd_words(rng, 64 * 5000)
     assert np.array_equal(gpu.pointwise64(u, v), chk.pointwise(u, v))
+
+
+def test_largest_shapes_fields_agree(gpu):
+    """2^33-bit x (2^33 - 337)-bit product (n = 2^34: two top basis-conversion passes, 28/27 FFT
+    layers): the GF(2^64) and GF(2^128) transforms give the same product; an all-ones-by-x^k probe
+    checks the same path against a closed form."""
+    import torch
+    n = 1 << 33
+    g = torch.Generator(device="cuda").manual_seed(3)
+    a = torch.randint(-(1 << 62), 1 << 62, (n // 64,), generator=g, device="cuda", dtype=torch.int64)
+    nb = n - 5 * 64 - 17
+    b = torch.randint(-(1 << 62), 1 << 62, ((nb + 63) // 64,), generator=g, device="cuda", dtype=torch.int64)
+    b[-1] &= (1 << (nb % 64)) - 1
+    out = (n + nb - 1 + 63) // 64
+    c1 = torch.empty(out, dtype=torch.int64, device="cuda")
+    c2 = torch.empty(out, dtype=torch.int64, device="cuda")
+    gpu.fp_polymul_dev(a, n, b, nb, c1, field=gpu.FIELD_GF128)
+    gpu.fp_polymul_dev(a, n, b, nb, c2, field=gpu.FIELD_GF64)
+    torch.cuda.synchronize()
+    assert torch.equal(c1, c2)
+    # (x^k) * b = b shifted by k bits, through the same 2^34-bit transform
+    k = 3 * 64 + 5
+    xk = torch.zeros((k + 1 + 63) // 64, dtype=torch.int64, device="cuda")
+    xk[k // 64] = 1 << (k % 64)
+    c3 = torch.empty((k + 1 + nb - 1 + 63) // 64, dtype=torch.int64, device="cuda")
+    gpu.fp_polymul_dev(b, nb, xk, k + 1, c3, field=gpu.FIELD_GF128)
+    torch.cuda.synchronize()
+    bb = b.cpu().numpy().view(np.uint64)
+    got = c3.cpu().numpy().view(np.uint64)
+    want = np.zeros(got.size + 1, np.uint64)
+    q, r = k // 64, np.uint64(k % 64)
+    want[q: q + bb.size] ^= bb << r
+    want[q + 1: q + 1 + bb.size] ^= bb >> (np.uint64(64) - r)
+    assert np.array_equal(got, want[: got.size]) and not want[got.size:].any()
