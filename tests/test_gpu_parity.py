@@ -246,3 +246,57 @@ def test_largest_shapes_fields_agree(gpu):
     want[q: q + bb.size] ^= bb << r
     want[q + 1: q + 1 + bb.size] ^= bb >> (np.uint64(64) - r)
     assert np.array_equal(got, want[: got.size]) and not want[got.size:].any()
+
+
+# ---------------------------------------------------------------- BASELINE configs vs the reference
+def _meta():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_meta.json")) as f:
+        return json.load(f)["configs"]
+
+
+@pytest.mark.parametrize("key", ["1048576x1048576", "16777216x16777216", "16777216x8400953",
+                                 "268435456x268435456", "4294967296x4294967296"])
+def test_baseline_config_products_match_reference_hashes(gpu, port, key):
+    """BASELINE configs 1, 3 (equal and unequal), 4 and 5 on the seeded inputs: blake2b-128 of the
+    GPU product (both fields) equals the hash of the reference library's product
+    (tests/golden/make_golden.py; config 5 with the F4-patched reference build)."""
+    import hashlib
+    import torch
+    c = _meta()[key]
+    a = port.random_bitpoly(c["a_bits"], c["seed_a"])
+    b = port.random_bitpoly(c["b_bits"], c["seed_b"])
+    da = torch.from_numpy(a.view(np.int64)).cuda()
+    db = torch.from_numpy(b.view(np.int64)).cuda()
+    dc = torch.empty((c["product_bits"] + 63) // 64, dtype=torch.int64, device="cuda")
+    for field in (gpu.FIELD_GF128, gpu.FIELD_GF64):
+        gpu.fp_polymul_dev(da, c["a_bits"], db, c["b_bits"], dc, field=field)
+        torch.cuda.synchronize()
+        got = hashlib.blake2b(dc.cpu().numpy().view(np.uint64).tobytes(), digest_size=16).hexdigest()
+        assert got == c["blake2b128"], field
+
+
+def _edge_operand(port, kind, bits, seed):
+    w = port.random_bitpoly(bits, seed)
+    if kind == "sparse":  # density 1/64: AND of six uniform words (SURVEY 8(d), config 3)
+        for k in range(1, 6):
+            w &= port.random_bitpoly(bits, seed + 1000 * k)
+    elif kind == "ones":
+        w[:] = np.uint64(0xFFFFFFFFFFFFFFFF)
+        if bits % 64:
+            w[-1] = np.uint64((1 << (bits % 64)) - 1)
+    elif kind == "top":  # exact degree: bit N-1 forced
+        w[(bits - 1) // 64] |= np.uint64(1) << np.uint64((bits - 1) % 64)
+    return w
+
+
+@pytest.mark.parametrize("kind", ["sparse", "ones", "top"])
+def test_config3_edge_shapes_vs_reference(gpu, ref, port, kind):
+    """Config 3's edge shapes at ~2^24 bits, bit-exact against the reference library."""
+    la, lb = 1 << 24, (1 << 23) + 12345
+    a = _edge_operand(port, kind, la, 71)
+    b = _edge_operand(port, kind, lb, 72)
+    want = ref.polymul(a, la, b, lb, field=0)
+    for field in (gpu.FIELD_GF128, gpu.FIELD_GF64):
+        assert np.array_equal(gpu.fp_polymul(a, la, b, lb, field=field), want), (kind, field)
