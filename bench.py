@@ -30,8 +30,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "ms per 2^k-bit GF(2)[x] multiply (k=20..32); fraction of per-pass roofline"
 CONFIGS = {  # BASELINE.json configs by index (1-based); operand bits
-    1: 1 << 20, 3: 1 << 24, 4: 1 << 28, 5: 1 << 32,
+    1: 1 << 20, 2: 1 << 16, 3: 1 << 24, 4: 1 << 28, 5: 1 << 32,
 }
+BATCH = 4096  # config 2: independent 2^16 x 2^16 products per batch (split across ranks)
 
 
 def peaks():
@@ -146,6 +147,116 @@ def algorithmic(stage: str, bits: int, T: int):
     raise KeyError(stage)
 
 
+def run_batch(args, ws, rank, local):
+    """Config 2: a batch of 4096 independent 2^16 x 2^16 products (fpm_polymul_batch_dev: one CTA
+    per product, everything in shared memory), split across ranks with no exchange (strong scaling
+    over the fixed batch); one step = the whole batch."""
+    import numpy as np
+    import torch
+
+    import paper_1803_11301_b200 as pkg
+
+    dev = torch.device("cuda", local)
+    bits = CONFIGS[2]
+    wa = bits // 64
+    wc = (2 * bits - 1 + 63) // 64
+    per = BATCH // ws
+    a = rand_words(torch, per * wa, 3000 + rank, dev)
+    b = rand_words(torch, per * wa, 4000 + rank, dev)
+    c = torch.empty(per * wc, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(x, y):
+        pkg.fp_polymul_batch_dev(x, bits, wa, y, bits, wa, c, wc, per)
+        return c
+
+    for _ in range(args.warmup):
+        step(a, b)
+    torch.cuda.synchronize()
+    pkg.launch_count(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(a, b)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+    launches = pkg.launch_count(reset=True)
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    dev_result = c.cpu().numpy().view(np.uint64).copy()
+    # e2e: pinned host operands in, products out, every step
+    ha = torch.empty(per * wa, dtype=torch.int64, pin_memory=True)
+    hb = torch.empty(per * wa, dtype=torch.int64, pin_memory=True)
+    hc = torch.empty(per * wc, dtype=torch.int64, pin_memory=True)
+    ha.copy_(a)
+    hb.copy_(b)
+    def e2e_step():
+        step(ha.to(dev, non_blocking=True), hb.to(dev, non_blocking=True))
+        hc.copy_(c)
+        torch.cuda.synchronize()
+    e2e_step()
+    k2 = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(k2):
+        e2e_step()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / k2
+    t = torch.tensor([e2e_ms], device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    same = bool(np.array_equal(hc.numpy().view(np.uint64), dev_result))
+    clocks = clk.summary()
+    mhz = clocks.get("sm_mhz") or 1965.0
+    peak_tops = LOP3_OPS_PER_CLK_SM * 148 * mhz * 1e6 / 1e12
+    ops = 1.02e7 * BATCH  # SURVEY 8(d): ops per config-2 product (l = 10 transform + pointwise)
+    achieved = ops / (ms * 1e-3) / 1e12
+    line = {
+        "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (uniform random bits, seeded)",
+        "config": {"workload": f"cfg2: batch of {BATCH} independent 2^16 x 2^16-bit products (one step = the batch)",
+                   "parallelism": f"batch split over {ws} GPU(s), no exchange", "l2": "batch operands 64 MiB (fit in L2)"},
+        "e2e": {"value": round(e2e_ms, 3), "unit": "ms", "steps": k2, "h2d_bytes_per_step": 2 * per * wa * 8 * ws,
+                "d2h_bytes_per_step": per * wc * 8 * ws, "matches_device_result": same},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "int", "kernel": "batch_kernel", "achieved": round(achieved, 2),
+                     "peak": round(peak_tops, 2), "unit": "Tops/s", "frac": round(achieved / peak_tops, 4),
+                     "traffic": None, "peak_source": "LOP3 microbenchmark 63 ops/clk/SM at the sampled SM clock",
+                     "op_convention": "SURVEY 8(d): 1.02e7 int32 ops per 2^16 x 2^16 product"},
+        "clocks": clocks,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle
+            R = oracle.ref()
+            P = oracle.port()
+            x = P.random_bitpoly(bits, 1)
+            y = P.random_bitpoly(bits, 2)
+            R.polymul(x, bits, y, bits, field=0, parallel=False)
+            nsample = 64
+            t0 = time.perf_counter()
+            for _ in range(nsample):
+                R.polymul(x, bits, y, bits, field=0, parallel=False)
+            per_prod = (time.perf_counter() - t0) / nsample
+            line["cpu_baseline"] = {"value": round(per_prod * BATCH * 1e3, 1), "unit": "ms", "cores": 1,
+                                    "kind": "reference",
+                                    "sample": f"{nsample} serial products (ExecPolicy::kSerial, auto field) on 1 core, "
+                                              f"scaled to the {BATCH}-product batch"}
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "unit": "ms", "cores": 1, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def run_reference(args, ws, rank):
     """--impl reference: the reference's own CPU fp_polymul (oracle/_ref) on this host's cores."""
     if rank != 0:
@@ -158,6 +269,30 @@ def run_reference(args, ws, rank):
     f4 = 2 * bits >= (1 << 33)
     R = oracle.ref(f4=f4)
     threads = R.max_threads()
+    if args.config == 2:  # batch: each step times a bounded sample of serial products, scaled
+        P = oracle.port()
+        x = P.random_bitpoly(bits, 1)
+        y = P.random_bitpoly(bits, 2)
+        R.polymul(x, bits, y, bits, field=args.ref_field, parallel=False)
+        nsample, times = 256, []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            for _ in range(nsample):
+                R.polymul(x, bits, y, bits, field=args.ref_field, parallel=False)
+            times.append((time.perf_counter() - t0) * 1e3 * BATCH / nsample)
+        v = statistics.mean(times)
+        line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": ws,
+                "steps": len(times), "warmup": 1, "ms_per_step": round(v, 3), "higher_is_better": False,
+                "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+                "data": "synthetic (mt19937_64 seeded, random_bitpoly)",
+                "config": {"workload": f"cfg2: batch of {BATCH} independent 2^16 x 2^16-bit products",
+                           "library": os.path.basename(R.path)},
+                "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": 1, "kind": "reference",
+                                 "sample": f"{nsample} serial products per step (ExecPolicy::kSerial, 1 core), "
+                                           f"scaled to the {BATCH}-product batch"},
+                "e2e": {"value": round(v, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     P = oracle.port()
     a = P.random_bitpoly(bits, 20261020)
     b = P.random_bitpoly(bits, 20261021)
@@ -218,7 +353,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS),
+                    help="BASELINE config: 1, 3, 4, 5 = one product of 2^20/2^24/2^28/2^32 bits; 2 = the 4096-product batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
     ap.add_argument("--ref-field", type=int, default=128, choices=[0, 64, 128],
@@ -248,6 +384,9 @@ def main():
         if ws > 1:
             torch.distributed.barrier()
 
+    if args.config == 2:
+        run_batch(args, ws, rank, local)
+        return
     bits = CONFIGS[args.config]
     words = bits // 64
     out_words = (2 * bits - 1 + 63) // 64
