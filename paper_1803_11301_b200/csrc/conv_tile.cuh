@@ -22,15 +22,6 @@ namespace fpm {
 constexpr int kTileRows = 256;
 constexpr int kScPitch = 17;  // scratch row pitch (words) for 512-bit widened rows
 
-__device__ __forceinline__ uint32_t sm_get32(const uint32_t* row, int nwords, int pos) {
-  // 32 bits of `row` (nwords words) starting at bit pos (may be negative / past the end: zeros)
-  const int iw = pos >> 5, s = pos & 31;
-  const uint32_t lo = (iw >= 0 && iw < nwords) ? row[iw] : 0u;
-  if (!s) return lo;
-  const uint32_t hi = (iw + 1 >= 0 && iw + 1 < nwords) ? row[iw + 1] : 0u;
-  return __funnelshift_r(lo, hi, s);
-}
-
 // 16-word registers shifted by whole words (ws < 16), left (towards higher words) or right, by
 // three/four conditional stages: no local memory, no shared-memory round trip.  ws is
 // warp-uniform in the callers (d >> 5 with 32 consecutive rows per warp).

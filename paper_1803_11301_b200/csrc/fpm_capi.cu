@@ -348,21 +348,8 @@ const DeviceTables& device_tables(int dev) {
   if (dev < 0 || dev >= 64) throw Error(kInvalid, "device ordinal out of range");
   if (have[dev]) return tabs[dev];
   const FieldTables& ft = field_tables();
-  std::vector<uint4> cantor(128), rows(128), inv(128), enc(kM4RUint4), dec(kM4RUint4), c2p(4 * 512);
+  std::vector<uint4> cantor(128), rows(128), inv(128), c2p(4 * 512);
   for (int i = 0; i < 128; ++i) { cantor[i] = to4(ft.cantor[i]); rows[i] = to4(ft.enc_rows[i]); inv[i] = to4(ft.inv_rows[i]); }
-  for (int c = 0; c < kM4RChunks; ++c)
-    for (int v = 0; v < 16; ++v) {
-      U128 e, d;
-      for (int j = 0; j < 4; ++j)
-        if (v >> j & 1) {
-          e.lo ^= ft.enc_rows[4 * c + j].lo; e.hi ^= ft.enc_rows[4 * c + j].hi;
-          d.lo ^= ft.inv_rows[4 * c + j].lo; d.hi ^= ft.inv_rows[4 * c + j].hi;
-        }
-      for (int r = 0; r < kM4RCopies; ++r) {
-        enc[(c * 16 + v) * kM4RCopies + r] = to4(e);
-        dec[(c * 16 + v) * kM4RCopies + r] = to4(d);
-      }
-    }
   // rotated 8-bit tables (gf128.cuh m8 layout): entry (c, v) at (c >> 3) * 2048 + v * 8 + (c & 7)
   std::vector<uint4> enc8(kM8Uint4), dec8(kM8Uint4);
   for (int c = 0; c < 16; ++c)
@@ -421,7 +408,7 @@ const DeviceTables& device_tables(int dev) {
     FPM_CUDA(cudaMemcpy(*dst, v.data(), v.size() * sizeof(uint4), cudaMemcpyHostToDevice));
   };
   up(&t.cantor, cantor); up(&t.enc_rows, rows); up(&t.inv_rows, inv);
-  up(&t.enc_m4r, enc); up(&t.dec_m4r, dec); up(&t.c2p, c2p);
+  up(&t.c2p, c2p);
   up(&t.enc_m8, enc8); up(&t.dec_m8, dec8);
   auto up2 = [](uint2** dst, const std::vector<uint2>& v) {
     FPM_CUDA(cudaMalloc(dst, v.size() * sizeof(uint2)));

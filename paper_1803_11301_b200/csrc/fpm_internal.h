@@ -41,8 +41,6 @@ struct DeviceTables {
   uint4* cantor = nullptr;    // 128 x v_i
   uint4* enc_rows = nullptr;  // 128 x r_j
   uint4* inv_rows = nullptr;  // 128 rows of E^{-1}
-  uint4* enc_m4r = nullptr;   // 32 chunks x 16 x 8 copies (x*E by nibbles)
-  uint4* dec_m4r = nullptr;   // 32 chunks x 16 x 8 copies (x*E^{-1})
   uint4* enc_m8 = nullptr;    // rotated 8-bit tables (gf128.cuh m8 layout) of x*E
   uint4* dec_m8 = nullptr;    // ... of x*E^{-1}
   uint4* c2p = nullptr;       // 4 x 512: part p entry e = C2P(2 * (e << 9p))
@@ -105,7 +103,7 @@ void decode_device(const uint4* ev, unsigned l, uint32_t* poly, cudaStream_t s);
 // Butterflies (k_fft.cu).
 void butterfly_device(uint4* ev, unsigned l, U128 base, bool inverse, cudaStream_t s);
 void pointwise_device(const uint4* u, const uint4* v, uint4* out, size_t n, cudaStream_t s);
-// Pipeline helpers exposing the split between top (global, M4R) and bottom (tile) layers.
+// Pipeline helpers exposing the split between top (radix-4 table passes) and bottom (tile) layers.
 unsigned fft_tile_log2(unsigned l);
 void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s);
 void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s);

@@ -4,14 +4,15 @@
 // uint4 {x,y,z,w} = 32-bit limbs, bit k of the element is bit (k%32) of limb k/32 -- byte-identical
 // to the reference u128 {lo, hi} (gf.hpp:24-52) so device EvalVecs are reference EvalVecs.
 //
-// Two multipliers, chosen per call site by measurement (profiles/r01_ubench_gf128_mul.log):
+// Multipliers, chosen per call site by measurement (profiles/):
 //  * gf_mul():      generic a*b.  Karatsuba 128 -> 3x64 -> 9x32; each 32x32 carry-less product is
 //                   16 IMAD.WIDE.U32 on "holed" operands (every 4th bit), whose digit sums stay < 16 so
 //                   bit 4k+r of the integer product is the GF(2) coefficient; XOR-combine, mask.
-//                   IMAD runs on the FMA pipe, the masks/XORs on the ALU pipe (7.0 clk/mul/SM measured).
-//  * M4R tables:    w*x for a twiddle w shared by a whole butterfly block: 32 nibble-chunk tables of
-//                   w*(v << 4c), replicated 8x so a quarter-warp's LDS.128 never bank-conflicts
-//                   (4.2 clk/mul/SM measured).  Replaces PCLMULQDQ (reference gf_pclmul.cpp:25-30).
+//                   IMAD runs on the FMA pipe, the masks/XORs on the ALU pipe (~7-8 clk/mul/SM).
+//  * M8 tables:     w*x for a twiddle w shared by a whole butterfly block: 16 byte-chunk tables of
+//                   w*(v << 8c) in a lane-rotated layout (16 conflict-free LDS.128 per product).
+//  * M4 tables:     8 twiddles at a time for blocks of 64..128 butterflies (32 lookups, 8 KiB each).
+//  These replace PCLMULQDQ (reference gf_pclmul.cpp:25-30).
 #pragma once
 #include <cstdint>
 
@@ -67,7 +68,7 @@ __device__ __forceinline__ uint4 gf_mul(uint4 a, uint4 b) {
   return gf_reduce(c0l, c0h ^ c1l, c2l ^ c1h, c2h);
 }
 
-// w * x^k mod P for 0 <= k < 128 (shift then fold), used to build M4R rows.
+// w * x^k mod P for 0 <= k < 128 (shift then fold), used to build table rows.
 __device__ __forceinline__ uint4 gf_mul_xk(uint4 w, unsigned k) {
   uint64_t lo = w.x | ((uint64_t)w.y << 32), hi = w.z | ((uint64_t)w.w << 32);
   uint64_t r0, r1, r2, r3;
@@ -78,36 +79,7 @@ __device__ __forceinline__ uint4 gf_mul_xk(uint4 w, unsigned k) {
   return gf_reduce(r0, r1, r2, r3);
 }
 
-// ---------------------------------------------------------------- M4R twiddle tables
-// Layout: entry (chunk c in [0,32), nibble v in [0,16)) replicated 8x; copy r of entry e at
-// uint4 index e*8 + r.  A lane always reads copy (lane & 7): the 8 lanes of a quarter-warp hit
-// 8 distinct 16-byte bank groups -> conflict-free LDS.128.
-constexpr int kM4RChunks = 32;
-constexpr int kM4REntries = kM4RChunks * 16;   // 512
-constexpr int kM4RCopies = 8;
-constexpr int kM4RUint4 = kM4REntries * kM4RCopies;  // 4096 uint4 = 64 KiB
-
-// Cooperative build of the table for twiddle w by the whole CTA (nthreads threads, tid).
-// rows_scratch: 128 uint4 of shared memory.
-__device__ __forceinline__ void m4r_build(uint4* __restrict__ tab, uint4* __restrict__ rows_scratch, uint4 w,
-                                          int tid, int nthreads) {
-  for (int k = tid; k < 128; k += nthreads) rows_scratch[k] = gf_mul_xk(w, (unsigned)k);
-  __syncthreads();
-  // Flat slot order (consecutive threads -> consecutive 16 B slots): conflict-free STS.128; the
-  // 8 threads writing one entry's copies each recompute it (<= 3 uint4 XORs, cheaper than a
-  // 32-way bank conflict on strided stores).
-  for (int f = tid; f < kM4RUint4; f += nthreads) {
-    const int e = f >> 3, c = e >> 4, v = e & 15;
-    uint4 acc = make_uint4(0, 0, 0, 0);
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (v >> j & 1) acc = x4(acc, rows_scratch[4 * c + j]);
-    tab[f] = acc;
-  }
-  __syncthreads();
-}
-
-// ---------------------------------------------------------------- rotated 8-bit M4R tables
+// ---------------------------------------------------------------- rotated 8-bit (M8) tables
 // 16 byte-chunk tables of w*(v << 8c), 256 entries each, 64 KiB total, no replication: entry
 // (c, v) lives at uint4 index (c >> 3) * 2048 + v * 8 + (c & 7), i.e. in 16-byte bank group c & 7.
 // Lane q (= lane & 7) of a quarter-warp visits chunks in the rotated order (k + q) & 7, so at
@@ -153,21 +125,6 @@ __device__ __forceinline__ uint4 m8_mul(const uint4* __restrict__ tab, uint4 x, 
   return x4(acc0, acc1);
 }
 
-__device__ __forceinline__ uint4 m4r_mul(const uint4* __restrict__ tab, uint4 x, int copy) {
-  uint4 acc0 = make_uint4(0, 0, 0, 0), acc1 = make_uint4(0, 0, 0, 0);
-  const uint32_t wds[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-#pragma unroll
-    for (int s = 0; s < 8; s += 2) {
-      const uint32_t n0 = (wds[q] >> (4 * s)) & 15u, n1 = (wds[q] >> (4 * s + 4)) & 15u;
-      const int c0 = q * 8 + s;
-      acc0 = x4(acc0, tab[((c0 * 16 + n0) << 3) + copy]);
-      acc1 = x4(acc1, tab[(((c0 + 1) * 16 + n1) << 3) + copy]);
-    }
-  }
-  return x4(acc0, acc1);
-}
 
 // ---------------------------------------------------------------- rotated 4-bit tables, 8 at a time
 // For tile layers whose twiddles are shared by only 2^5..2^7 butterflies: 32 nibble-chunk tables of

@@ -8,8 +8,8 @@
 // element, so 32 consecutive elements are one 32-bit word per row.  A CTA stages a 1024-element
 // slab (32 words x 64|128 rows, coalesced 128 B row segments) in padded shared memory, each warp
 // turns 32x32 bit blocks into per-lane column words with a 5-step __shfl_xor_sync transpose, and
-// the 128-bit matrix product x*E runs as M4R lookups in an 8x-replicated, bank-conflict-free
-// shared table.  Decode runs the same steps in reverse.
+// the matrix product x*E runs as byte-chunk lookups in a lane-rotated, bank-conflict-free shared
+// table (gf128.cuh M8 layout; GF(2^64): gf64.cuh G8 layout).  Decode runs the same steps in reverse.
 #include <cuda_runtime.h>
 
 #include "fpm_internal.h"

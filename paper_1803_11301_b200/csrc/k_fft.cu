@@ -8,12 +8,12 @@
 // 2^l - 1 entry plan (1 GiB at l = 26) never exists on the GPU.
 //   forward  p0 ^= w*p1; p1 ^= p0          inverse  p1 ^= p0; p0 ^= w*p1
 //
-// Kernels:
-//  * fft_top_kernel: one layer i >= T per launch.  Each CTA owns <= 4096 pairs of ONE block, builds
-//    the 64 KiB M4R table of that block's twiddle in shared memory, then streams its pairs
-//    (4.2 clk/mul/SM, bank-conflict free).
-//  * fft_tile_kernel: layers [0, T) of a 2^T-element tile held in shared memory (one HBM read and
-//    write for T layers); twiddles vary per block there, so products use the generic IMAD gf_mul.
+// Kernels (T = fft_tile_log2(l): layers >= T are "top" layers, < T run in shared-memory tiles):
+//  * fft_top4_kernel: top layers (i+1, i) per HBM round trip; the three twiddles of a block as M8
+//    tables (gf128.cuh), one 768-thread CTA per SM; fft_top_kernel: a single top layer.
+//  * fft_tile_kernel: layers [0, T) of a 2^T-element tile (one HBM read and write for T layers):
+//    layers >= 8 via one M8 table per twiddle, layers 6-7 via M4 tables 8 twiddles at a time, lower
+//    layers (twiddles vary per block) via the generic IMAD-hole gf_mul.
 //  * fft_tile_fused_kernel: forward layers [0,T) of operand b, the pointwise product with operand
 //    a (subsystem 3, kernels_impl.hpp:116-123), and inverse layers [0,T) in one tile pass.
 #include <cuda_runtime.h>
@@ -46,7 +46,7 @@ __device__ __forceinline__ uint4 twiddle(const TwiddleSrc& tw, unsigned l, unsig
 // ------------------------------------------------------------------ top layers (i >= T)
 template <bool INV>
 __global__ void __launch_bounds__(256) fft_top_kernel(uint4* __restrict__ ev, unsigned l, unsigned i, int ppc, TwiddleSrc tw) {
-  extern __shared__ uint4 tab[];            // kM4RUint4
+  extern __shared__ uint4 tab[];            // kM8Uint4
   __shared__ uint4 rows[144];
   const uint64_t half = (uint64_t)1 << i;
   const uint64_t pair0 = (uint64_t)blockIdx.x * ppc;   // ppc <= 2^i: CTA pairs never straddle a block
@@ -345,7 +345,7 @@ TwiddleSrc make_twiddle_src(int device, unsigned l, U128 base) {
 
 void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s) {
   if (l <= T) return;
-  const size_t smem = kM4RUint4 * sizeof(uint4);
+  const size_t smem = kM8Uint4 * sizeof(uint4);
   static bool attr = false;
   if (!attr) { set_smem(fft_top_kernel<false>, smem); set_smem(fft_top_kernel<true>, smem); attr = true; }
   // Pairs per CTA: 4096 amortise the 64 KiB table build; smaller layers still fill 2 CTAs/SM.
@@ -359,7 +359,7 @@ void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const
   uint64_t ppc = 4096;
   while (ppc > 256 && pairs / ppc < (uint64_t)sms() * 2) ppc /= 2;
   const uint64_t ctas = pairs / ppc;
-  if (T < 8 || ctas == 0) throw Error(kInvalid, "butterfly_top: layer too small for the M4R layer kernel");
+  if (T < 8 || ctas == 0) throw Error(kInvalid, "butterfly_top: layer too small for the table layer kernel");
   auto radix2 = [&](unsigned i) {
     const uint64_t p = std::min<uint64_t>(ppc, (uint64_t)1 << i);  // a CTA stays inside one block
     if (!inverse) fft_top_kernel<false><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, l, i, (int)p, tw);
@@ -452,7 +452,7 @@ void butterfly_device(uint4* ev, unsigned l, U128 base, bool inverse, cudaStream
 
 void bfly_pair_device(uint4* mine, const uint4* theirs, uint64_t n, U128 w, int side, bool inverse, cudaStream_t s) {
   if (!n) return;
-  const size_t smem = kM4RUint4 * sizeof(uint4);
+  const size_t smem = kM8Uint4 * sizeof(uint4);
   static bool attr = false;
   if (!attr) { set_smem(fft_pair_kernel<false>, smem); set_smem(fft_pair_kernel<true>, smem); attr = true; }
   uint64_t ppc = 4096;
