@@ -12,8 +12,10 @@
 #include <vector>
 
 #include "basis_dev.cuh"
+#include "conv_tile.cuh"
 #include "fpm_internal.h"
 #include "gf128.cuh"
+#include "warp_bits.cuh"
 
 namespace fpm {
 
@@ -28,22 +30,55 @@ __device__ __forceinline__ uint4 c2p2b(const uint4* __restrict__ c2p, uint64_t b
   return r;
 }
 
-__device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
-  const uint32_t masks[5] = {0xFFFF0000u, 0xFF00FF00u, 0xF0F0F0F0u, 0xCCCCCCCCu, 0xAAAAAAAAu};
+
+// Basis conversion of a <= 2^16-bit array W (2^K bits) in place, as one conversion tile
+// (conv_tile.cuh: L1 + row passes + register passes; zero-padded to the 8 KiB tile).
+// scratch: >= kTileRows * (kRowPitchW<1> + kScPitch) words, disjoint from W.
+template <bool INV>
+__device__ __forceinline__ void conv_small(uint32_t* W, int K, uint32_t* scratch) {
+  const int tid = threadIdx.x;
+  const int words = K >= 5 ? 1 << (K - 5) : 1;
+  uint32_t m[8];
 #pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    const int s = 16 >> k;
-    const uint32_t m = masks[k];
-    const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, x, s);
-    if (lane & s) x = (x & m) | ((y >> s) & ~m);
-    else x = (x & ~m) | ((y << s) & m);
+  for (int j = 0; j < 8; ++j) m[j] = 8 * tid + j < words ? W[8 * tid + j] : 0u;
+  conv_tile<INV>(m, scratch, scratch + kTileRows * kRowPitchW<1>, K);
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    if (8 * tid + j < words) W[8 * tid + j] = m[j];
+  __syncthreads();
+}
+
+// Inverse conversion of the 2^17-bit product array: conv(2^16)^-1 of both halves, then the inverse
+// of the single top pass (S = 2^17, D = 2^16 - 1: bits [1, 2^16] ^= bits [2^16, 2^17 - 1], from the
+// pre-pass values; build_schedule at 2^17, basis_convert.cpp:53-67).
+__device__ __forceinline__ void i_conv_17(uint32_t* W, uint32_t* scratch) {
+  conv_small<true>(W, 16, scratch);
+  conv_small<true>(W + 2048, 16, scratch);
+  const int tid = threadIdx.x;
+  uint32_t t[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    const int w = tid + 256 * k;  // target words 0 .. 2048
+    t[k] = 0;
+    if (w <= 2048) {
+      const uint32_t lo = W[w + 2047], hi = w + 2048 < 4096 ? W[w + 2048] : 0u;
+      t[k] = __funnelshift_r(lo, hi, 31);
+      if (w == 0) t[k] &= ~1u;
+      if (w == 2048) t[k] &= 1u;
+    }
   }
-  return x;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    const int w = tid + 256 * k;
+    if (w <= 2048) W[w] ^= t[k];
+  }
+  __syncthreads();
 }
 
 // Forward transform of one operand: W0 <- x (n/2 bits), basis conversion, encode into E, butterflies.
-__device__ void transform_operand(const uint64_t* __restrict__ x, uint64_t x_bits, uint32_t* W0, uint32_t* W1,
-                                  uint4* E, unsigned l, int half_words, const PassList& pl_half,
+__device__ void transform_operand(const uint64_t* __restrict__ x, uint64_t x_bits, uint32_t* W0, uint32_t* scratch,
+                                  uint4* E, unsigned l, int half_words, const uint4* __restrict__ enc_m8,
                                   const uint4* __restrict__ enc_rows, const TwiddleSrc& tw) {
   const int tid = threadIdx.x;
   const uint32_t* x32 = reinterpret_cast<const uint32_t*>(x);
@@ -57,19 +92,26 @@ __device__ void transform_operand(const uint64_t* __restrict__ x, uint64_t x_bit
     W0[i] = v;
   }
   __syncthreads();
-  const uint32_t* P = smem_passes(W0, W1, half_words, pl_half, false);
-  // encode: f_i = sum_j a_{j n_p + i} r_j, rows j < 64 (the upper half is zero padding)
+  const int Kh = l + 6;  // the operand half: 2^(l+6) bits
+  conv_small<false>(W0, Kh, scratch);
+  const uint32_t* P = W0;
+  // encode: f_i = sum_j a_{j n_p + i} r_j, rows j < 64 (the upper half is zero padding): 8 byte
+  // lookups in the rotated 8-bit table of x*E (read through L1)
   const int n_p = 1 << l;
   const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   if (n_p >= 32) {
+    const Transpose32 tr(lane);
+    const int q8 = lane & 7;
     const int row_words = n_p / 32;
     for (int col = warp; col < row_words; col += nwarps) {
-      const uint32_t lo = transpose32(P[lane * row_words + col], lane);
-      const uint32_t hi = transpose32(P[(lane + 32) * row_words + col], lane);
+      const uint32_t lo = tr(P[lane * row_words + col]);
+      const uint32_t hi = tr(P[(lane + 32) * row_words + col]);
       uint4 f = make_uint4(0, 0, 0, 0);
-      for (int j = 0; j < 32; ++j) {
-        if (lo >> j & 1u) f = x4(f, enc_rows[j]);
-        if (hi >> j & 1u) f = x4(f, enc_rows[32 + j]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int c = (k + q8) & 7;
+        const uint32_t byte = __byte_perm(c < 4 ? lo : hi, 0, 0x4440u | (uint32_t)(c & 3));
+        f = x4(f, __ldg(enc_m8 + byte * 8 + c));
       }
       E[col * 32 + lane] = f;
     }
@@ -101,24 +143,29 @@ __device__ void transform_operand(const uint64_t* __restrict__ x, uint64_t x_bit
   }
 }
 
+// Shared memory (fixed l = 10 layout, 64 KiB): EA | EB | W0 | W1, 16 KiB each.  The bit arrays
+// (operand halves, then the product) live in W1; EB..W0 (32 KiB, contiguous) is the conversion
+// tile's scratch whenever it is not holding data (EB is only written by the second encode, after
+// that operand's conversion).
+constexpr int kBatchSmemUint4 = 4 * 1024;
 __global__ void __launch_bounds__(256) batch_kernel(const uint64_t* __restrict__ a, uint64_t a_bits, uint64_t a_stride,
                                                     const uint64_t* __restrict__ b, uint64_t b_bits, uint64_t b_stride,
                                                     uint64_t* __restrict__ c, uint64_t c_stride, unsigned l,
-                                                    PassList pl_half, PassList pl_full_inv,
+                                                    const uint4* __restrict__ enc_m8, const uint4* __restrict__ dec_m8,
                                                     const uint4* __restrict__ enc_rows,
                                                     const uint4* __restrict__ inv_rows, TwiddleSrc tw) {
   extern __shared__ uint4 sm[];
   const int n_p = 1 << l;
   const int n_words = n_p * 4;  // n = 128 n_p bits
   uint4* EA = sm;
-  uint4* EB = sm + n_p;
-  uint32_t* W0 = reinterpret_cast<uint32_t*>(sm + 2 * n_p);
-  uint32_t* W1 = W0 + n_words;
+  uint4* EB = sm + 1024;
+  uint32_t* W1 = reinterpret_cast<uint32_t*>(sm + 3 * 1024);
+  uint32_t* scratch = reinterpret_cast<uint32_t*>(EB);  // EB + W0: 8192 words
   const uint64_t prod = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
 
-  transform_operand(a + prod * a_stride, a_bits, W0, W1, EA, l, n_words / 2, pl_half, enc_rows, tw);
-  transform_operand(b + prod * b_stride, b_bits, W0, W1, EB, l, n_words / 2, pl_half, enc_rows, tw);
+  transform_operand(a + prod * a_stride, a_bits, W1, scratch, EA, l, n_words / 2, enc_m8, enc_rows, tw);
+  transform_operand(b + prod * b_stride, b_bits, W1, scratch, EB, l, n_words / 2, enc_m8, enc_rows, tw);
   for (int i = tid; i < n_p; i += blockDim.x) EA[i] = gf_mul(EA[i], EB[i]);
   __syncthreads();
   // inverse butterflies, layers 0 .. l-1 (kernels_impl.hpp:48-61)
@@ -136,45 +183,57 @@ __global__ void __launch_bounds__(256) batch_kernel(const uint64_t* __restrict__
     }
     __syncthreads();
   }
-  // decode: y_i = f_i E^{-1}; bit j of y_i -> c_{j n_p + i}  (encode.cpp:195-220)
-  for (int i = tid; i < n_p; i += blockDim.x) {
-    const uint4 f = EA[i];
-    const uint32_t fw[4] = {f.x, f.y, f.z, f.w};
-    uint4 y = make_uint4(0, 0, 0, 0);
-    for (int t = 0; t < 128; ++t)
-      if ((fw[t >> 5] >> (t & 31)) & 1u) y = x4(y, inv_rows[t]);
-    EB[i] = y;  // EB is free now
-  }
-  __syncthreads();
+  // decode: y_i = f_i E^{-1} (16 byte lookups in the rotated table, through L1); bit j of y_i ->
+  // c_{j n_p + i} by warp transposes (encode.cpp:195-220)
   if (n_p >= 32) {
+    const Transpose32 tr(lane);
+    const int q8 = lane & 7;
     const int row_words = n_p / 32;
     for (int col = warp; col < row_words; col += nwarps) {
-      const uint4 y = EB[col * 32 + lane];
-      W0[(0 * 32 + lane) * row_words + col] = transpose32(y.x, lane);
-      W0[(1 * 32 + lane) * row_words + col] = transpose32(y.y, lane);
-      W0[(2 * 32 + lane) * row_words + col] = transpose32(y.z, lane);
-      W0[(3 * 32 + lane) * row_words + col] = transpose32(y.w, lane);
+      const uint4 f = EA[col * 32 + lane];
+      uint4 y = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int cc = (k + q8) & 7;
+        const uint32_t lo = __byte_perm(cc < 4 ? f.x : f.y, 0, 0x4440u | (uint32_t)(cc & 3));
+        const uint32_t hi = __byte_perm(cc < 4 ? f.z : f.w, 0, 0x4440u | (uint32_t)(cc & 3));
+        y = x4(y, __ldg(dec_m8 + lo * 8 + cc));
+        y = x4(y, __ldg(dec_m8 + 2048 + hi * 8 + cc));
+      }
+      W1[(0 * 32 + lane) * row_words + col] = tr(y.x);
+      W1[(1 * 32 + lane) * row_words + col] = tr(y.y);
+      W1[(2 * 32 + lane) * row_words + col] = tr(y.z);
+      W1[(3 * 32 + lane) * row_words + col] = tr(y.w);
     }
   } else {
     for (int wi = tid; wi < n_words; wi += blockDim.x) {
       uint32_t out = 0;
       for (int bb = 0; bb < 32; ++bb) {
         const int k = wi * 32 + bb, j = k / n_p, i = k % n_p;
-        const uint4 y = EB[i];
-        const uint32_t yw[4] = {y.x, y.y, y.z, y.w};
-        out |= ((yw[j >> 5] >> (j & 31)) & 1u) << bb;
+        const uint4 f = EA[i];
+        const uint32_t fw[4] = {f.x, f.y, f.z, f.w};
+        uint32_t acc = 0;  // bit j of f E^{-1}
+        for (int t = 0; t < 128; ++t)
+          if ((fw[t >> 5] >> (t & 31)) & 1u) {
+            const uint4 r = inv_rows[t];
+            const uint32_t rw[4] = {r.x, r.y, r.z, r.w};
+            acc ^= (rw[j >> 5] >> (j & 31)) & 1u;
+          }
+        out |= acc << bb;
       }
-      W0[wi] = out;
+      W1[wi] = out;
     }
   }
   __syncthreads();
-  const uint32_t* C = smem_passes(W0, W1, n_words, pl_full_inv, true);
+  // inverse basis conversion of the n-bit product (n = 2^(l+7))
+  if (l + 7 <= 16) conv_small<true>(W1, l + 7, scratch);
+  else i_conv_17(W1, scratch);
   // trim to len_a + len_b - 1 bits and write 64-bit words
   const uint64_t out_bits = a_bits + b_bits - 1;
   const uint64_t out_words = (out_bits + 63) / 64;
   uint64_t* cc = c + prod * c_stride;
   for (uint64_t k = tid; k < out_words; k += blockDim.x) {
-    uint64_t v = (uint64_t)C[2 * k] | ((uint64_t)C[2 * k + 1] << 32);
+    uint64_t v = (uint64_t)W1[2 * k] | ((uint64_t)W1[2 * k + 1] << 32);
     if (k == out_words - 1 && (out_bits & 63)) v &= (((uint64_t)1) << (out_bits & 63)) - 1;
     cc[k] = v;
   }
@@ -193,30 +252,20 @@ void polymul_batch_device(const uint64_t* a, size_t a_bits, size_t a_stride_word
   while (((size_t)1 << logn) < n) ++logn;
   if (logn > (unsigned)kBatchMaxLog2N) throw Error(kInvalid, "polymul_batch: product longer than 2^17 bits");
   const unsigned l = logn - 7;
-  Pass sched[128];
-  size_t np = 0;
-  build_schedule(sched, &np, n / 2, 1);
-  const PassList pl_half = make_passlist(std::vector<Pass>(sched, sched + np), false);
-  np = 0;
-  build_schedule(sched, &np, n, 1);
-  std::vector<Pass> inv(sched, sched + np);
-  std::vector<Pass> rinv(inv.rbegin(), inv.rend());
-  const PassList pl_full_inv = make_passlist(rinv, true);
   int dev;
   FPM_CUDA(cudaGetDevice(&dev));
   const DeviceTables& dt = device_tables(dev);
-  const size_t n_p = (size_t)1 << l;
-  const size_t smem = 2 * n_p * sizeof(uint4) + 2 * (n / 8);
+  const size_t smem = kBatchSmemUint4 * sizeof(uint4);
   static bool attr = false;
   if (!attr) {
-    FPM_CUDA(cudaFuncSetAttribute(batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 1024 * 16 + 2 * (1 << 14)));
+    FPM_CUDA(cudaFuncSetAttribute(batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   for (size_t off = 0; off < count; off += 65535u * 16u) {
     const size_t cnt = std::min<size_t>(count - off, 65535u * 16u);
     batch_kernel<<<(unsigned)cnt, 256, smem, s>>>(a + off * a_stride_words, a_bits, a_stride_words,
                                                   b + off * b_stride_words, b_bits, b_stride_words,
-                                                  c + off * c_stride_words, c_stride_words, l, pl_half, pl_full_inv,
+                                                  c + off * c_stride_words, c_stride_words, l, dt.enc_m8, dt.dec_m8,
                                                   dt.enc_rows, dt.inv_rows, make_twiddle_src(dev, l, partition_base(l)));
     FPM_LAUNCH_CHECK();
   }
