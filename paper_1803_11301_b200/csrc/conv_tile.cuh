@@ -58,26 +58,46 @@ __device__ __forceinline__ void l1_tile(uint32_t (&m)[8], uint32_t* sc, int g, i
 #pragma unroll
     for (int i = 0; i < 16; ++i) W[i] = __funnelshift_l(i ? t[i - 1] : 0u, t[i], bs);
   }
-  // subset-zeta over the g row bits: rows with bit b clear ^= row | 2^b
-  for (int b = 0; b < g; ++b) {
-    const bool lower = !((d >> b) & 1);
-    if ((1 << b) < 32) {
+  // subset-zeta over the g low row bits (rows with bit b clear ^= row | 2^b), as register-local
+  // stages in two transposed mappings with shared-memory exchanges (row-major sc, pitch 17):
+  //   A: thread (c = tid & 15, r0 = tid >> 4) holds word c of rows r0 + 16k -> row bits 4..7 local
+  //   B: thread (c, r1 = tid >> 4) holds word c of rows 16 r1 + k         -> row bits 0..3 local
+  // Chunk boundaries (2^g rows) are respected by running only stages b < g.
+  {
+    const int c = tid & 15, rr = tid >> 4;
+    uint32_t v[16];
+    __syncthreads();
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const uint32_t y = __shfl_xor_sync(0xFFFFFFFFu, W[i], 1 << b);
-        if (lower) W[i] ^= y;
-      }
-    } else {
+    for (int i = 0; i < 16; ++i) my[i] = W[i];
+    __syncthreads();
+    if (g > 4) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = sc[(rr + 16 * k) * kScPitch + c];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (4 + j < g) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (!(k >> j & 1)) v[k] ^= v[k | (1 << j)];
+        }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) sc[(rr + 16 * k) * kScPitch + c] = v[k];
       __syncthreads();
-#pragma unroll
-      for (int i = 0; i < 16; ++i) my[i] = W[i];
-      __syncthreads();
-      if (lower) {
-        const uint32_t* pr = sc + (tid + (1 << b)) * kScPitch;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) W[i] ^= pr[i];
-      }
     }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = sc[(16 * rr + k) * kScPitch + c];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j < g) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (!(k >> j & 1)) v[k] ^= v[k | (1 << j)];
+      }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) sc[(16 * rr + k) * kScPitch + c] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) W[i] = my[i];
   }
   // unskew: G = W >> d, in registers
   uint32_t G[16];
