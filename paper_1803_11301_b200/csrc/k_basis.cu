@@ -312,8 +312,10 @@ __global__ void __launch_bounds__(256) carry_rows_kernel(const uint32_t* __restr
 
 // ------------------------------------------------------------------ O: overflow + unskew (inverse)
 // F_d[p] = Gs[d][p+d] ^ (d >= 1 ? Gs[d-1][t+p+d-1] : 0)
+// top (optional): the single inverse top pass of a 2^33-bit array fused in when `out` is the lower
+// 2^32-bit block: out bit q (q >= 1) ^= top bit q - 1, top = the (final) upper block.
 __global__ void overflow_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch, uint32_t* __restrict__ out,
-                                uint64_t D) {
+                                uint64_t D, const uint32_t* __restrict__ top) {
   // A warp covers 32 consecutive output words of one row: both bit offsets are warp-uniform, so each
   // span is one coalesced load per lane, the neighbour word comes by shuffle (lane 31 loads it).
   const uint64_t total = D * kTWords;
@@ -333,8 +335,14 @@ __global__ void overflow_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pit
       if (lane == 31) yb = ib + 1 < gs_pitch ? __ldg(r1 + ib + 1) : 0u;
       v ^= __funnelshift_r(xb, yb, (int)(pos & 31));
     }
+    if (top) v ^= (top[k] << 1) | (k ? top[k - 1] >> 31 : 0u);
     out[k] = v;
   }
+}
+
+// Bit 0 of the upper 2^32-bit block ^= its last bit (the fused 2^33-bit top pass's target 2^32).
+__global__ void top_bit_fix_kernel(uint32_t* __restrict__ hi_block, uint64_t block_words) {
+  if (threadIdx.x == 0) hi_block[0] ^= hi_block[block_words - 1] >> 31;
 }
 
 // ------------------------------------------------------------------ C_D for D <= 256: slab tiles
@@ -744,7 +752,9 @@ void conv_cols(uint32_t* w, uint32_t* scratch, int lgD, bool inv, cudaStream_t s
 // conv(2^K) for 17 <= K <= 32 on w (2^K bits).  scratch >= 2^(K-16) * (2^16 + max(2^(K-16), 1024)) bits.
 // src (forward only, may be null): read the unconverted rows from src instead of w (w is first
 // written by the carry pass, so an input buffer need not be copied into w beforehand).
-void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s, const uint32_t* src = nullptr) {
+// top (inverse only): fuse the 2^33-bit top pass into this (lower) block's last kernel.
+void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s, const uint32_t* src = nullptr,
+            const uint32_t* top = nullptr) {
   const int lgD = K - kTLog2;
   const uint64_t D = (uint64_t)1 << lgD;
   const uint64_t wsk_bits = kT + std::max<uint64_t>(D, 32 * kZW);
@@ -772,7 +782,7 @@ void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s, con
     conv_rows(w, D * kTWords, kTLog2, true, s);
     conv_cols(w, scratch, lgD, true, s);
     l1_zeta(w);
-    overflow_kernel<<<grid_cap(D * kTWords / 256, 32), 256, 0, s>>>(scratch, wsk, w, D);
+    overflow_kernel<<<grid_cap(D * kTWords / 256, 32), 256, 0, s>>>(scratch, wsk, w, D, top);
     FPM_LAUNCH_CHECK();
   }
 }
@@ -861,12 +871,20 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
     const uint64_t hi_bit = top[0].span - top[0].shift;  // exclusive end of the rewritten bits
     early_from = (hi_bit + 31) / 32;
   }
+  // 2^33 bits: that single pass is fused into the lower block's overflow kernel (bits [1, 2^32)),
+  // and its last target bit 2^32 (= upper bit 0 ^= bit 2^33 - 1) is one word fixed afterwards.
+  const bool fuse_top = top.size() == 1 && nblocks == 2 && top[0].shift == block_words * 32 - 1;
   for (uint64_t b = nblocks; b-- > 0;) {
-    conv2d(w + b * block_words, Kb, inverse, scratch, s);
+    conv2d(w + b * block_words, Kb, inverse, scratch, s, nullptr, fuse_top && b == 0 ? w + block_words : nullptr);
     const uint64_t w0 = std::max(b * block_words, early_from), w1 = (b + 1) * block_words;
     if (on_final && w0 < w1) (*on_final)(w0, w1);
   }
-  for (size_t k = top.size(); k-- > 0;) run_big_pass(w, nwords, top[k], true, n_bits, s);
+  if (fuse_top) {
+    top_bit_fix_kernel<<<1, 32, 0, s>>>(w + block_words, block_words);
+    FPM_LAUNCH_CHECK();
+  } else {
+    for (size_t k = top.size(); k-- > 0;) run_big_pass(w, nwords, top[k], true, n_bits, s);
+  }
   if (on_final) (*on_final)(0, std::min<uint64_t>(early_from, nwords));
 }
 
