@@ -300,3 +300,22 @@ def test_config3_edge_shapes_vs_reference(gpu, ref, port, kind):
     want = ref.polymul(a, la, b, lb, field=0)
     for field in (gpu.FIELD_GF128, gpu.FIELD_GF64):
         assert np.array_equal(gpu.fp_polymul(a, la, b, lb, field=field), want), (kind, field)
+
+
+@pytest.mark.parametrize("lg", [28, 32, 33, 34])
+def test_basis_cvt_large_roundtrip_and_linearity(gpu, lg):
+    """Conversions beyond the oracle's reach (the 2D tile path, the fused 2^33 top pass, the generic
+    top passes above it): inverse(forward(x)) = x and forward is GF(2)-linear."""
+    import torch
+    n = 1 << lg
+    g = torch.Generator(device="cuda").manual_seed(lg)
+    x = torch.randint(-(1 << 62), 1 << 62, (n // 64,), generator=g, device="cuda", dtype=torch.int64)
+    y = torch.randint(-(1 << 62), 1 << 62, (n // 64,), generator=g, device="cuda", dtype=torch.int64)
+    fx, fy, fs = x.clone(), y.clone(), x ^ y
+    for t in (fx, fy, fs):
+        gpu.stage_dev("basis_cvt", t, n, n)
+    torch.cuda.synchronize()
+    assert torch.equal(fx ^ fy, fs), "linearity"
+    gpu.stage_dev("i_basis_cvt", fx, n)
+    torch.cuda.synchronize()
+    assert torch.equal(fx, x), "round trip"
