@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <functional>
@@ -34,6 +35,22 @@ void note_launch();
     ::fpm::note_launch();              \
     FPM_CUDA(cudaGetLastError());      \
   } while (0)
+
+// Runs an initialisation (e.g. cudaFuncSetAttribute of a kernel's dynamic shared memory) once per
+// device: kernel attributes belong to a device context, so a process driving several GPUs must set
+// them on each one.  Thread-safe; devices 0..63.
+struct PerDeviceOnce {
+  std::atomic<uint64_t> done{0};
+  template <class Fn>
+  void run(Fn&& fn) {
+    int dev = 0;
+    FPM_CUDA(cudaGetDevice(&dev));
+    const uint64_t bit = uint64_t{1} << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    fn();
+    done.fetch_or(bit, std::memory_order_acq_rel);
+  }
+};
 
 // Per-device immutable tables (uploaded once, lazily, under a mutex -- the reference's
 // thread-safe singletons CantorField::get / EncodeMatrix::get, cantor.cpp:136-140).

@@ -674,12 +674,11 @@ constexpr size_t kSlabSmem = 256 * kRowPitchW<kSlabW> * sizeof(uint32_t);
 // (g % gstride) + (g / gstride) * 256 * gstride.
 void conv256_units(uint32_t* w, uint64_t ngroups, uint64_t ustride, uint64_t gstride, bool inv, cudaStream_t s,
                    CarrySrc cs = CarrySrc{}) {
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  attr.run([&] {
     FPM_CUDA(cudaFuncSetAttribute(conv256_units_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC256Smem));
     FPM_CUDA(cudaFuncSetAttribute(conv256_units_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC256Smem));
-    attr = true;
-  }
+  });
   UnitMap um{ustride, gstride, ngroups};
   const uint64_t items = ngroups * (kTWords / kC256Cols);
   if (inv) conv256_units_kernel<true><<<grid_cap(items, 3), kC256Threads, kC256Smem, s>>>(w, um, items, cs);

@@ -256,11 +256,10 @@ void polymul_batch_device(const uint64_t* a, size_t a_bits, size_t a_stride_word
   FPM_CUDA(cudaGetDevice(&dev));
   const DeviceTables& dt = device_tables(dev);
   const size_t smem = kBatchSmemUint4 * sizeof(uint4);
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  attr.run([&] {
     FPM_CUDA(cudaFuncSetAttribute(batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  });
   for (size_t off = 0; off < count; off += 65535u * 16u) {
     const size_t cnt = std::min<size_t>(count - off, 65535u * 16u);
     batch_kernel<<<(unsigned)cnt, 256, smem, s>>>(a + off * a_stride_words, a_bits, a_stride_words,

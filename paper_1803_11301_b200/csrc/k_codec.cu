@@ -294,13 +294,13 @@ void encode_cols_device(const uint32_t* poly, unsigned l, uint64_t col0, uint64_
   const uint64_t nslabs = ncols / 32 / kSlabWords;
   if (rows_live == 64) {
     const size_t smem = kM8Uint4 / 2 * sizeof(uint4) + 64 * kPad * sizeof(uint32_t);
-    static bool attr = false;
-    if (!attr) { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); attr = true; }
+    static PerDeviceOnce attr;
+    attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
     encode_kernel<64><<<grid_for(nslabs, 4), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, dt.enc_m8, ev);
   } else {
     const size_t smem = kM8Uint4 * sizeof(uint4) + 128 * kPad * sizeof(uint32_t);
-    static bool attr = false;
-    if (!attr) { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); attr = true; }
+    static PerDeviceOnce attr;
+    attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
     encode_kernel<128><<<grid_for(nslabs, 2), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, dt.enc_m8, ev);
   }
   FPM_LAUNCH_CHECK();
@@ -328,8 +328,8 @@ void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaSt
   if (ncols % 1024) throw Error(kInvalid, "decode: column count not 1024-aligned");
   const DeviceTables& dt = device_tables(dev);
   const size_t smem = kM8Uint4 * sizeof(uint4) + 128 * kPad * sizeof(uint32_t);
-  static bool attr = false;
-  if (!attr) { FPM_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); attr = true; }
+  static PerDeviceOnce attr;
+  attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
   const uint64_t nslabs = ncols / 32 / kSlabWords;
   decode_kernel<<<grid_for(nslabs, 2), 256, smem, s>>>(ev, nslabs, ncols / 32, dt.dec_m8, slice);
   FPM_LAUNCH_CHECK();

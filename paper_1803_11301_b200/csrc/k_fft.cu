@@ -346,15 +346,14 @@ TwiddleSrc make_twiddle_src(int device, unsigned l, U128 base) {
 void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s) {
   if (l <= T) return;
   const size_t smem = kM8Uint4 * sizeof(uint4);
-  static bool attr = false;
-  if (!attr) { set_smem(fft_top_kernel<false>, smem); set_smem(fft_top_kernel<true>, smem); attr = true; }
+  static PerDeviceOnce attr;
+  attr.run([&] { set_smem(fft_top_kernel<false>, smem); set_smem(fft_top_kernel<true>, smem); });
   // Pairs per CTA: 4096 amortise the 64 KiB table build; smaller layers still fill 2 CTAs/SM.
-  static bool attr4 = false;
-  if (!attr4) {
+  static PerDeviceOnce attr4;
+  attr4.run([&] {
     set_smem(fft_top4_kernel<false>, kTop4Smem);
     set_smem(fft_top4_kernel<true>, kTop4Smem);
-    attr4 = true;
-  }
+  });
   const uint64_t pairs = ((uint64_t)1 << l) / 2;
   uint64_t ppc = 4096;
   while (ppc > 256 && pairs / ppc < (uint64_t)sms() * 2) ppc /= 2;
@@ -415,12 +414,11 @@ constexpr size_t kTileSmemMax = ((size_t)1 << kTileMax << 4) + (kM8Uint4 + 144) 
 
 void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s) {
   if (T == 0) return;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  attr.run([&] {
     set_smem(fft_tile_kernel<false>, kTileSmemMax);
     set_smem(fft_tile_kernel<true>, kTileSmemMax);
-    attr = true;
-  }
+  });
   const TileCfg c = tile_cfg(l, T);
   if (!inverse) fft_tile_kernel<false><<<c.grid, c.threads, c.smem, s>>>(ev, l, T, tw, c.use_tab);
   else fft_tile_kernel<true><<<c.grid, c.threads, c.smem, s>>>(ev, l, T, tw, c.use_tab);
@@ -429,8 +427,8 @@ void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, cons
 
 void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
                                  cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) { set_smem(fft_tile_fused_kernel, kTileSmemMax); attr = true; }
+  static PerDeviceOnce attr;
+  attr.run([&] { set_smem(fft_tile_fused_kernel, kTileSmemMax); });
   const TileCfg c = tile_cfg(l, T);
   fft_tile_fused_kernel<<<c.grid, c.threads, c.smem, s>>>(ea, eb, l, T, tw, c.use_tab);
   FPM_LAUNCH_CHECK();
@@ -453,8 +451,8 @@ void butterfly_device(uint4* ev, unsigned l, U128 base, bool inverse, cudaStream
 void bfly_pair_device(uint4* mine, const uint4* theirs, uint64_t n, U128 w, int side, bool inverse, cudaStream_t s) {
   if (!n) return;
   const size_t smem = kM8Uint4 * sizeof(uint4);
-  static bool attr = false;
-  if (!attr) { set_smem(fft_pair_kernel<false>, smem); set_smem(fft_pair_kernel<true>, smem); attr = true; }
+  static PerDeviceOnce attr;
+  attr.run([&] { set_smem(fft_pair_kernel<false>, smem); set_smem(fft_pair_kernel<true>, smem); });
   uint64_t ppc = 4096;
   while (ppc > 256 && n / ppc < (uint64_t)sms() * 2) ppc /= 2;
   const unsigned ctas = (unsigned)((n + ppc - 1) / ppc);

@@ -330,14 +330,13 @@ TwiddleSrc64 make_twiddle_src64(int device, unsigned l, uint64_t base) {
 void butterfly64_top_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s) {
   if (l <= T) return;
   const size_t smem = kG8Uint2 * sizeof(uint2);
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  attr.run([&] {
     set_smem64(fft64_top_kernel<false>, smem);
     set_smem64(fft64_top_kernel<true>, smem);
     set_smem64(fft64_top4_kernel<false>, kTop4Smem64);
     set_smem64(fft64_top4_kernel<true>, kTop4Smem64);
-    attr = true;
-  }
+  });
   if (T < 8) throw Error(kInvalid, "butterfly_top: layer too small for the table layer kernel");
   const uint64_t pairs = ((uint64_t)1 << l) / 2;
   uint64_t ppc = 4096;
@@ -372,12 +371,11 @@ void butterfly64_top_device(uint2* ev, unsigned l, unsigned T, bool inverse, con
 
 void butterfly64_tile_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s) {
   if (T == 0) return;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  attr.run([&] {
     set_smem64(fft64_tile_kernel<false>, kTileSmemMax64);
     set_smem64(fft64_tile_kernel<true>, kTileSmemMax64);
-    attr = true;
-  }
+  });
   const TileCfg64 c = tile_cfg64(l, T);
   if (!inverse) fft64_tile_kernel<false><<<c.grid, c.threads, c.smem, s>>>(ev, l, T, tw, c.use_tab);
   else fft64_tile_kernel<true><<<c.grid, c.threads, c.smem, s>>>(ev, l, T, tw, c.use_tab);
@@ -386,8 +384,8 @@ void butterfly64_tile_device(uint2* ev, unsigned l, unsigned T, bool inverse, co
 
 void butterfly64_tile_fused_device(const uint2* ea, uint2* eb, unsigned l, unsigned T, const TwiddleSrc64& tw,
                                    cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) { set_smem64(fft64_tile_fused_kernel, kTileSmemMax64); attr = true; }
+  static PerDeviceOnce attr;
+  attr.run([&] { set_smem64(fft64_tile_fused_kernel, kTileSmemMax64); });
   const TileCfg64 c = tile_cfg64(l, T);
   fft64_tile_fused_kernel<<<c.grid, c.threads, c.smem, s>>>(ea, eb, l, T, tw, c.use_tab);
   FPM_LAUNCH_CHECK();
