@@ -68,6 +68,55 @@ __device__ __forceinline__ uint4 gf_mul(uint4 a, uint4 b) {
   return gf_reduce(c0l, c0h ^ c1l, c2l ^ c1h, c2h);
 }
 
+// ---------------------------------------------------------------- prepared-operand multiply
+// gf_mul(w, x) splits both operands into the 9 Karatsuba 32-bit limbs and masks each limb four
+// ways (4-bit holes).  When one twiddle w multiplies many x, its 9 x 4 masked limbs are computed
+// once (GfPrep, 144 B) and the product costs only x's side: ~14% fewer ALU ops.
+struct GfPrep {
+  uint4 m[9];  // limb k (al.lo, al.hi, al.lo^hi, ah.lo, ..., (al^ah).lo^hi): {& M, & M<<1, & M<<2, & M<<3}
+};
+__device__ __forceinline__ uint4 mask4(uint32_t a) {
+  const uint32_t m = 0x11111111u;
+  return make_uint4(a & m, a & (m << 1), a & (m << 2), a & (m << 3));
+}
+__device__ __forceinline__ GfPrep gf_prep(uint4 w) {
+  GfPrep p;
+  const uint32_t l0 = w.x, l1 = w.y, h0 = w.z, h1 = w.w;
+  const uint32_t s0 = l0 ^ h0, s1 = l1 ^ h1;
+  p.m[0] = mask4(l0); p.m[1] = mask4(l1); p.m[2] = mask4(l0 ^ l1);
+  p.m[3] = mask4(h0); p.m[4] = mask4(h1); p.m[5] = mask4(h0 ^ h1);
+  p.m[6] = mask4(s0); p.m[7] = mask4(s1); p.m[8] = mask4(s0 ^ s1);
+  return p;
+}
+__device__ __forceinline__ uint64_t clmul32_p(uint4 a, uint32_t b) {  // a = mask4(limb)
+  const uint32_t m = 0x11111111u;
+  const uint32_t b0 = b & m, b1 = b & (m << 1), b2 = b & (m << 2), b3 = b & (m << 3);
+  const uint64_t r0 = (uint64_t)a.x * b0 ^ (uint64_t)a.y * b3 ^ (uint64_t)a.z * b2 ^ (uint64_t)a.w * b1;
+  const uint64_t r1 = (uint64_t)a.x * b1 ^ (uint64_t)a.y * b0 ^ (uint64_t)a.z * b3 ^ (uint64_t)a.w * b2;
+  const uint64_t r2 = (uint64_t)a.x * b2 ^ (uint64_t)a.y * b1 ^ (uint64_t)a.z * b0 ^ (uint64_t)a.w * b3;
+  const uint64_t r3 = (uint64_t)a.x * b3 ^ (uint64_t)a.y * b2 ^ (uint64_t)a.z * b1 ^ (uint64_t)a.w * b0;
+  const uint64_t M = 0x1111111111111111ull;
+  return (r0 & M) | (r1 & (M << 1)) | (r2 & (M << 2)) | (r3 & (M << 3));
+}
+__device__ __forceinline__ void clmul64_p(uint4 a0, uint4 a1, uint4 a01, uint64_t b, uint64_t& lo, uint64_t& hi) {
+  const uint32_t b0 = (uint32_t)b, b1 = (uint32_t)(b >> 32);
+  const uint64_t p0 = clmul32_p(a0, b0), p2 = clmul32_p(a1, b1);
+  const uint64_t p1 = clmul32_p(a01, b0 ^ b1) ^ p0 ^ p2;
+  lo = p0 ^ (p1 << 32);
+  hi = p2 ^ (p1 >> 32);
+}
+// == gf_mul(w, x) for p = gf_prep(w)
+__device__ __forceinline__ uint4 gf_mul_prep(const GfPrep& p, uint4 x) {
+  const uint64_t bl = x.x | ((uint64_t)x.y << 32), bh = x.z | ((uint64_t)x.w << 32);
+  uint64_t c0l, c0h, c2l, c2h, c1l, c1h;
+  clmul64_p(p.m[0], p.m[1], p.m[2], bl, c0l, c0h);
+  clmul64_p(p.m[3], p.m[4], p.m[5], bh, c2l, c2h);
+  clmul64_p(p.m[6], p.m[7], p.m[8], bl ^ bh, c1l, c1h);
+  c1l ^= c0l ^ c2l;
+  c1h ^= c0h ^ c2h;
+  return gf_reduce(c0l, c0h ^ c1l, c2l ^ c1h, c2h);
+}
+
 // w * x^k mod P for 0 <= k < 128 (shift then fold), used to build table rows.
 __device__ __forceinline__ uint4 gf_mul_xk(uint4 w, unsigned k) {
   uint64_t lo = w.x | ((uint64_t)w.y << 32), hi = w.z | ((uint64_t)w.w << 32);

@@ -158,6 +158,8 @@ __global__ void __launch_bounds__(kTop4Threads, 1) fft_top4_kernel(uint4* __rest
 constexpr unsigned kTabLayer = 8;
 // Layers [kM4Layer, kTabLayer): rotated 4-bit tables for 8 twiddles at a time (gf128.cuh m4s_*).
 constexpr unsigned kM4Layer = 6;
+// Layers [kPrepLayer, kM4Layer): generic multiplies with the twiddle's limbs prepared once per block.
+constexpr unsigned kPrepLayer = 1;
 template <bool INV>
 __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, unsigned l, uint64_t tile_idx,
                                             const TwiddleSrc& tw, uint4* __restrict__ tab) {
@@ -212,6 +214,31 @@ __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, u
           s[i0] = u0;
           s[i1] = u1;
         }
+      }
+      __syncthreads();
+      continue;
+    }
+    if (tab && i >= kPrepLayer && (npairs >> i) * (int)sizeof(GfPrep) <= kM8Uint4 * (int)sizeof(uint4)) {
+      // each twiddle serves 2^i butterflies: its masked Karatsuba limbs are prepared once, in the
+      // (otherwise idle) table area
+      GfPrep* prep = reinterpret_cast<GfPrep*>(tab);
+      const int nblk = npairs >> i;
+      for (int b = threadIdx.x; b < nblk; b += blockDim.x) prep[b] = gf_prep(x4(Z, c2p2(tw.c2p, (uint64_t)b)));
+      __syncthreads();
+      for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+        const int blk = p >> i, j = p & ((1 << i) - 1);
+        const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+        const GfPrep w = prep[blk];
+        uint4 u0 = s[i0], u1 = s[i1];
+        if (!INV) {
+          u0 = x4(u0, gf_mul_prep(w, u1));
+          u1 = x4(u1, u0);
+        } else {
+          u1 = x4(u1, u0);
+          u0 = x4(u0, gf_mul_prep(w, u1));
+        }
+        s[i0] = u0;
+        s[i1] = u1;
       }
       __syncthreads();
       continue;
