@@ -35,6 +35,23 @@ __device__ __forceinline__ uint2 gf64_mul(uint2 a, uint2 b) {
   return as_u2(gf64_reduce(lo, hi));
 }
 
+// Prepared operand (cf. gf128.cuh GfPrep): the 3 Karatsuba limbs of w, each masked four ways.
+struct Gf64Prep {
+  uint4 m[3];
+};
+__device__ __forceinline__ Gf64Prep gf64_prep(uint2 w) {
+  Gf64Prep p;
+  p.m[0] = mask4(w.x);
+  p.m[1] = mask4(w.y);
+  p.m[2] = mask4(w.x ^ w.y);
+  return p;
+}
+__device__ __forceinline__ uint2 gf64_mul_prep(const Gf64Prep& p, uint2 x) {
+  uint64_t lo, hi;
+  clmul64_p(p.m[0], p.m[1], p.m[2], as_u64(x), lo, hi);
+  return as_u2(gf64_reduce(lo, hi));
+}
+
 // w * x^k mod P for 0 <= k < 64 (table rows).
 __device__ __forceinline__ uint2 gf64_mul_xk(uint2 w, unsigned k) {
   const uint64_t v = as_u64(w);

@@ -212,6 +212,30 @@ __device__ __forceinline__ void tile_layers64(uint2* __restrict__ s, unsigned T,
       __syncthreads();
       continue;
     }
+    if (tab && i >= 1 && (npairs >> i) * (int)sizeof(Gf64Prep) <= kG8Uint2 * (int)sizeof(uint2)) {
+      // twiddle limbs prepared once per block in the idle table area (cf. k_fft.cu)
+      Gf64Prep* prep = reinterpret_cast<Gf64Prep*>(tab);
+      const int nblk = npairs >> i;
+      for (int b = threadIdx.x; b < nblk; b += blockDim.x) prep[b] = gf64_prep(x2(Z, c2p2_64(tw.c2p, (uint64_t)b)));
+      __syncthreads();
+      for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+        const int blk = p >> i, j = p & ((1 << i) - 1);
+        const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+        const Gf64Prep w = prep[blk];
+        uint2 u0 = s[i0], u1 = s[i1];
+        if (!INV) {
+          u0 = x2(u0, gf64_mul_prep(w, u1));
+          u1 = x2(u1, u0);
+        } else {
+          u1 = x2(u1, u0);
+          u0 = x2(u0, gf64_mul_prep(w, u1));
+        }
+        s[i0] = u0;
+        s[i1] = u1;
+      }
+      __syncthreads();
+      continue;
+    }
     for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
       const int blk = p >> i, j = p & ((1 << i) - 1);
       const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
