@@ -81,12 +81,26 @@ __global__ void __launch_bounds__(256) decode_kernel(const uint4* __restrict__ e
   const int q8 = lane & 7;
   const Transpose32 tr(lane);
   __syncthreads();
+  // The warp's four elements of the next slab are loaded while this slab is transformed and
+  // stored (software pipelining across slabs).
+  constexpr int kCols = kSlabWords / 8;
+  uint4 nx[kCols];
+  auto fetch = [&](uint64_t sl) {
+#pragma unroll
+    for (int k = 0; k < kCols; ++k)
+      nx[k] = sl < nslabs ? __ldg(ev + (sl * kSlabWords + warp * kCols + k) * 32 + lane) : make_uint4(0, 0, 0, 0);
+  };
+  fetch(blockIdx.x);
   for (uint64_t sl = blockIdx.x; sl < nslabs; sl += gridDim.x) {
     const uint64_t w0 = sl * kSlabWords;
-#pragma unroll 1
-    for (int k = 0; k < kSlabWords / 8; ++k) {
-      const int col = warp * (kSlabWords / 8) + k;
-      const uint4 y = m8_mul(tab, ev[(w0 + col) * 32 + lane], q8);
+    uint4 cur[kCols];
+#pragma unroll
+    for (int k = 0; k < kCols; ++k) cur[k] = nx[k];
+    fetch(sl + gridDim.x);
+#pragma unroll
+    for (int k = 0; k < kCols; ++k) {
+      const int col = warp * kCols + k;
+      const uint4 y = m8_mul(tab, cur[k], q8);
       slab[(0 * 32 + lane) * kPad + col] = tr(y.x);
       slab[(1 * 32 + lane) * kPad + col] = tr(y.y);
       slab[(2 * 32 + lane) * kPad + col] = tr(y.z);
