@@ -36,14 +36,28 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint32_t* __restrict_
   for (int i = tid; i < kTab; i += blockDim.x) tab[i] = tab_g[i];
   const int q8 = lane & 7;
   const Transpose32 tr(lane);
+  // Each thread's share of the next slab is loaded into registers while the current one is
+  // transformed (software pipelining across slabs).
+  constexpr int kPer = ROWS * kSlabWords / 256;
+  uint32_t nx[kPer];
+  auto fetch = [&](uint64_t sl) {
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = tid + 256 * j, r = i / kSlabWords, c = i % kSlabWords;
+      nx[j] = sl < nslabs ? __ldg(poly + (uint64_t)r * row_words + col0_words + sl * kSlabWords + c) : 0u;
+    }
+  };
+  fetch(blockIdx.x);
   for (uint64_t sl = blockIdx.x; sl < nslabs; sl += gridDim.x) {
     const uint64_t w0 = sl * kSlabWords;
     __syncthreads();
-    for (int i = tid; i < ROWS * kSlabWords; i += blockDim.x) {
-      const int r = i / kSlabWords, c = i % kSlabWords;
-      slab[r * kPad + c] = poly[(uint64_t)r * row_words + col0_words + w0 + c];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = tid + 256 * j, r = i / kSlabWords, c = i % kSlabWords;
+      slab[r * kPad + c] = nx[j];
     }
     __syncthreads();
+    fetch(sl + gridDim.x);
 #pragma unroll 1
     for (int k = 0; k < kSlabWords / 8; ++k) {
       const int col = warp * (kSlabWords / 8) + k;
@@ -169,14 +183,26 @@ __global__ void __launch_bounds__(256) encode64_kernel(const uint32_t* __restric
   for (int i = tid; i < kG8Uint2; i += blockDim.x) tab[i] = tab_g[i];
   const Transpose32 tr(lane);
   const int q = lane & 7, h8 = lane & 8;
+  constexpr int kPer = ROWS * kSlabWords / 256;  // next-slab register prefetch, as encode_kernel
+  uint32_t nx[kPer];
+  auto fetch = [&](uint64_t sl) {
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = tid + 256 * j, r = i / kSlabWords, c = i % kSlabWords;
+      nx[j] = sl < nslabs ? __ldg(poly + (uint64_t)r * row_words + sl * kSlabWords + c) : 0u;
+    }
+  };
+  fetch(blockIdx.x);
   for (uint64_t sl = blockIdx.x; sl < nslabs; sl += gridDim.x) {
     const uint64_t w0 = sl * kSlabWords;
     __syncthreads();
-    for (int i = tid; i < ROWS * kSlabWords; i += blockDim.x) {
-      const int r = i / kSlabWords, c = i % kSlabWords;
-      slab[r * kPad + c] = poly[(uint64_t)r * row_words + w0 + c];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = tid + 256 * j, r = i / kSlabWords, c = i % kSlabWords;
+      slab[r * kPad + c] = nx[j];
     }
     __syncthreads();
+    fetch(sl + gridDim.x);
 #pragma unroll 1
     for (int k = 0; k < kSlabWords / 8; ++k) {
       const int col = warp * (kSlabWords / 8) + k;
@@ -208,12 +234,24 @@ __global__ void __launch_bounds__(256) decode64_kernel(const uint2* __restrict__
   for (int i = tid; i < kG8Uint2; i += blockDim.x) tab[i] = tab_g[i];
   const Transpose32 tr(lane);
   __syncthreads();
+  constexpr int kCols = kSlabWords / 8;  // next-slab register prefetch, as decode_kernel
+  uint2 nx[kCols];
+  auto fetch = [&](uint64_t sl) {
+#pragma unroll
+    for (int k = 0; k < kCols; ++k)
+      nx[k] = sl < nslabs ? __ldg(ev + (sl * kSlabWords + warp * kCols + k) * 32 + lane) : make_uint2(0, 0);
+  };
+  fetch(blockIdx.x);
   for (uint64_t sl = blockIdx.x; sl < nslabs; sl += gridDim.x) {
     const uint64_t w0 = sl * kSlabWords;
-#pragma unroll 1
-    for (int k = 0; k < kSlabWords / 8; ++k) {
-      const int col = warp * (kSlabWords / 8) + k;
-      const uint2 y = g8_mul(tab, ev[(w0 + col) * 32 + lane], lane);
+    uint2 cur[kCols];
+#pragma unroll
+    for (int k = 0; k < kCols; ++k) cur[k] = nx[k];
+    fetch(sl + gridDim.x);
+#pragma unroll
+    for (int k = 0; k < kCols; ++k) {
+      const int col = warp * kCols + k;
+      const uint2 y = g8_mul(tab, cur[k], lane);
       slab[lane * kPad + col] = tr(y.x);
       slab[(32 + lane) * kPad + col] = tr(y.y);
     }
