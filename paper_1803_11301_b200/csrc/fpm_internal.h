@@ -52,6 +52,20 @@ struct PerDeviceOnce {
   }
 };
 
+// Grid of a persistent (grid-stride) kernel: as many CTAs as are co-resident on the device
+// (occupancy query for the actual threads / dynamic shared memory), capped at the work items --
+// a grid that is not a multiple of the resident slots leaves a half-empty last wave.
+template <class K>
+int resident_grid(K kernel, int threads, size_t smem, uint64_t work) {
+  int dev = 0, sms = 0, per_sm = 0;
+  FPM_CUDA(cudaGetDevice(&dev));
+  FPM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  FPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+  if (per_sm < 1) per_sm = 1;
+  const uint64_t g = (uint64_t)sms * per_sm;
+  return (int)(work < g ? (work ? work : 1) : g);
+}
+
 // Per-device immutable tables (uploaded once, lazily, under a mutex -- the reference's
 // thread-safe singletons CantorField::get / EncodeMatrix::get, cantor.cpp:136-140).
 struct DeviceTables {

@@ -318,14 +318,6 @@ const RowTables& row_tables(int dev) {
   return t[dev];
 }
 
-int grid_for(uint64_t work, int per_sm) {
-  int dev, sms;
-  FPM_CUDA(cudaGetDevice(&dev));
-  FPM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const uint64_t g = std::min<uint64_t>(work, (uint64_t)sms * per_sm);
-  return (int)(g ? g : 1);
-}
-
 }  // namespace
 
 // Column range [col0, col0 + ncols) of the 128-row partition matrix (row pitch n_p bits) -> ncols
@@ -348,12 +340,12 @@ void encode_cols_device(const uint32_t* poly, unsigned l, uint64_t col0, uint64_
     const size_t smem = kM8Uint4 / 2 * sizeof(uint4) + 64 * kPad * sizeof(uint32_t);
     static PerDeviceOnce attr;
     attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
-    encode_kernel<64><<<grid_for(nslabs, 4), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, dt.enc_m8, ev);
+    encode_kernel<64><<<resident_grid(encode_kernel<64>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, dt.enc_m8, ev);
   } else {
     const size_t smem = kM8Uint4 * sizeof(uint4) + 128 * kPad * sizeof(uint32_t);
     static PerDeviceOnce attr;
     attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
-    encode_kernel<128><<<grid_for(nslabs, 2), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, dt.enc_m8, ev);
+    encode_kernel<128><<<resident_grid(encode_kernel<128>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, dt.enc_m8, ev);
   }
   FPM_LAUNCH_CHECK();
 }
@@ -383,7 +375,7 @@ void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaSt
   static PerDeviceOnce attr;
   attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
   const uint64_t nslabs = ncols / 32 / kSlabWords;
-  decode_kernel<<<grid_for(nslabs, 2), 256, smem, s>>>(ev, nslabs, ncols / 32, dt.dec_m8, slice);
+  decode_kernel<<<resident_grid(decode_kernel, 256, smem, nslabs), 256, smem, s>>>(ev, nslabs, ncols / 32, dt.dec_m8, slice);
   FPM_LAUNCH_CHECK();
 }
 
@@ -400,10 +392,10 @@ void encode64_device(const uint32_t* poly, unsigned l, uint2* ev, int rows_live,
   const uint64_t nslabs = n_p / 32 / kSlabWords;
   if (rows_live <= 32) {
     const size_t smem = kG8Uint2 * sizeof(uint2) + 32 * kPad * sizeof(uint32_t);
-    encode64_kernel<32><<<grid_for(nslabs, 4), 256, smem, s>>>(poly, n_p / 32, nslabs, dt.enc_g8, ev);
+    encode64_kernel<32><<<resident_grid(encode64_kernel<32>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, nslabs, dt.enc_g8, ev);
   } else {
     const size_t smem = kG8Uint2 * sizeof(uint2) + 64 * kPad * sizeof(uint32_t);
-    encode64_kernel<64><<<grid_for(nslabs, 4), 256, smem, s>>>(poly, n_p / 32, nslabs, dt.enc_g8, ev);
+    encode64_kernel<64><<<resident_grid(encode64_kernel<64>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, nslabs, dt.enc_g8, ev);
   }
   FPM_LAUNCH_CHECK();
 }
@@ -421,7 +413,7 @@ void decode64_device(const uint2* ev, unsigned l, uint32_t* poly, cudaStream_t s
   }
   const uint64_t nslabs = n_p / 32 / kSlabWords;
   const size_t smem = kG8Uint2 * sizeof(uint2) + 64 * kPad * sizeof(uint32_t);
-  decode64_kernel<<<grid_for(nslabs, 4), 256, smem, s>>>(ev, nslabs, n_p / 32, dt.dec_g8, poly);
+  decode64_kernel<<<resident_grid(decode64_kernel, 256, smem, nslabs), 256, smem, s>>>(ev, nslabs, n_p / 32, dt.dec_g8, poly);
   FPM_LAUNCH_CHECK();
 }
 

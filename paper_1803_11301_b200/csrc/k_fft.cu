@@ -421,7 +421,7 @@ int tile_threads(unsigned T) { return T >= 9 ? 256 : std::max(32, 1 << (T - 1));
 // Tile launch geometry: tables for layers >= kTabLayer when the tile runs 256 threads (T >= 9;
 // FPM_TILE_TABLES=0 disables them for comparison).
 struct TileCfg {
-  int threads, use_tab, grid;
+  int threads, use_tab;
   size_t smem;
 };
 TileCfg tile_cfg(unsigned l, unsigned T) {
@@ -433,8 +433,6 @@ TileCfg tile_cfg(unsigned l, unsigned T) {
   c.threads = tile_threads(T);
   c.use_tab = tables && T > kTabLayer && c.threads == 256;
   c.smem = ((size_t)1 << T) * sizeof(uint4) + (c.use_tab ? (kM8Uint4 + 144) * sizeof(uint4) : 0);
-  const int per_sm = c.use_tab ? 2 : 768 / c.threads;
-  c.grid = (int)std::min<uint64_t>(((uint64_t)1 << l) >> T, (uint64_t)sms() * per_sm);
   return c;
 }
 constexpr size_t kTileSmemMax = ((size_t)1 << kTileMax << 4) + (kM8Uint4 + 144) * sizeof(uint4);
@@ -447,8 +445,13 @@ void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, cons
     set_smem(fft_tile_kernel<true>, kTileSmemMax);
   });
   const TileCfg c = tile_cfg(l, T);
-  if (!inverse) fft_tile_kernel<false><<<c.grid, c.threads, c.smem, s>>>(ev, l, T, tw, c.use_tab);
-  else fft_tile_kernel<true><<<c.grid, c.threads, c.smem, s>>>(ev, l, T, tw, c.use_tab);
+  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
+  if (!inverse)
+    fft_tile_kernel<false><<<resident_grid(fft_tile_kernel<false>, c.threads, c.smem, ntiles), c.threads, c.smem, s>>>(
+        ev, l, T, tw, c.use_tab);
+  else
+    fft_tile_kernel<true><<<resident_grid(fft_tile_kernel<true>, c.threads, c.smem, ntiles), c.threads, c.smem, s>>>(
+        ev, l, T, tw, c.use_tab);
   FPM_LAUNCH_CHECK();
 }
 
@@ -457,7 +460,8 @@ void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigne
   static PerDeviceOnce attr;
   attr.run([&] { set_smem(fft_tile_fused_kernel, kTileSmemMax); });
   const TileCfg c = tile_cfg(l, T);
-  fft_tile_fused_kernel<<<c.grid, c.threads, c.smem, s>>>(ea, eb, l, T, tw, c.use_tab);
+  const int grid = resident_grid(fft_tile_fused_kernel, c.threads, c.smem, ((uint64_t)1 << l) >> T);
+  fft_tile_fused_kernel<<<grid, c.threads, c.smem, s>>>(ea, eb, l, T, tw, c.use_tab);
   FPM_LAUNCH_CHECK();
 }
 

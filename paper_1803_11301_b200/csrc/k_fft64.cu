@@ -313,7 +313,7 @@ void set_smem64(K kernel, size_t bytes) {
 int tile_threads64(unsigned T) { return T >= 9 ? 256 : std::max(32, 1 << (T - 1)); }
 
 struct TileCfg64 {
-  int threads, use_tab, grid;
+  int threads, use_tab;
   size_t smem;
 };
 TileCfg64 tile_cfg64(unsigned l, unsigned T) {
@@ -321,8 +321,6 @@ TileCfg64 tile_cfg64(unsigned l, unsigned T) {
   c.threads = tile_threads64(T);
   c.use_tab = T > kTabLayer64 && c.threads == 256;
   c.smem = ((size_t)1 << T) * sizeof(uint2) + (c.use_tab ? (kG8Uint2 + kG8Rows) * sizeof(uint2) : 0);
-  const int per_sm = c.use_tab ? 3 : 768 / c.threads;
-  c.grid = (int)std::min<uint64_t>(((uint64_t)1 << l) >> T, (uint64_t)sms64() * per_sm);
   return c;
 }
 constexpr size_t kTileSmemMax64 = ((size_t)1 << kTileMax64) * sizeof(uint2) + (kG8Uint2 + kG8Rows) * sizeof(uint2);
@@ -401,8 +399,13 @@ void butterfly64_tile_device(uint2* ev, unsigned l, unsigned T, bool inverse, co
     set_smem64(fft64_tile_kernel<true>, kTileSmemMax64);
   });
   const TileCfg64 c = tile_cfg64(l, T);
-  if (!inverse) fft64_tile_kernel<false><<<c.grid, c.threads, c.smem, s>>>(ev, l, T, tw, c.use_tab);
-  else fft64_tile_kernel<true><<<c.grid, c.threads, c.smem, s>>>(ev, l, T, tw, c.use_tab);
+  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
+  if (!inverse)
+    fft64_tile_kernel<false><<<resident_grid(fft64_tile_kernel<false>, c.threads, c.smem, ntiles), c.threads, c.smem, s>>>(
+        ev, l, T, tw, c.use_tab);
+  else
+    fft64_tile_kernel<true><<<resident_grid(fft64_tile_kernel<true>, c.threads, c.smem, ntiles), c.threads, c.smem, s>>>(
+        ev, l, T, tw, c.use_tab);
   FPM_LAUNCH_CHECK();
 }
 
@@ -411,7 +414,8 @@ void butterfly64_tile_fused_device(const uint2* ea, uint2* eb, unsigned l, unsig
   static PerDeviceOnce attr;
   attr.run([&] { set_smem64(fft64_tile_fused_kernel, kTileSmemMax64); });
   const TileCfg64 c = tile_cfg64(l, T);
-  fft64_tile_fused_kernel<<<c.grid, c.threads, c.smem, s>>>(ea, eb, l, T, tw, c.use_tab);
+  const int grid = resident_grid(fft64_tile_fused_kernel, c.threads, c.smem, ((uint64_t)1 << l) >> T);
+  fft64_tile_fused_kernel<<<grid, c.threads, c.smem, s>>>(ea, eb, l, T, tw, c.use_tab);
   FPM_LAUNCH_CHECK();
 }
 
