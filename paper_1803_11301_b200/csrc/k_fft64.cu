@@ -256,7 +256,7 @@ __device__ __forceinline__ void tile_layers64(uint2* __restrict__ s, unsigned T,
 }
 
 template <bool INV>
-__global__ void __launch_bounds__(256) fft64_tile_kernel(uint2* __restrict__ ev, unsigned l, unsigned T,
+__global__ void __launch_bounds__(256, 3) fft64_tile_kernel(uint2* __restrict__ ev, unsigned l, unsigned T,
                                                          TwiddleSrc64 tw, int use_tab) {
   extern __shared__ uint2 s64[];
   const int n = 1 << T;
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(256) fft64_tile_kernel(uint2* __restrict__ ev,
   }
 }
 
-__global__ void __launch_bounds__(256) fft64_tile_fused_kernel(const uint2* __restrict__ ea, uint2* __restrict__ eb,
+__global__ void __launch_bounds__(256, 3) fft64_tile_fused_kernel(const uint2* __restrict__ ea, uint2* __restrict__ eb,
                                                                unsigned l, unsigned T, TwiddleSrc64 tw, int use_tab) {
   extern __shared__ uint2 s64[];
   const int n = 1 << T;
