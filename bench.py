@@ -108,6 +108,17 @@ def rand_words(torch, words, seed, device):
     return lo | (hi << 32)
 
 
+def stage_pipes(stage: str, bits: int):
+    """ncu pipe utilisation (percent of peak, duration-weighted over the stage's launches) from the
+    committed --set full capture (profiles/pipes.json, tools/ncu_traffic.py), or None: SURVEY 8(d)
+    asks for the ALU-pipe utilisation beside an int-bound roofline."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "pipes.json")) as f:
+            return json.load(f).get(f"{bits}:{stage}")
+    except (OSError, ValueError):
+        return None
+
+
 def stage_traffic(stage: str, bits: int):
     """DRAM bytes (read + write) per launch of the stage's kernel from the committed ncu capture
     (profiles/traffic.json, written by tools/ncu_traffic.py), or None."""
@@ -490,6 +501,7 @@ def main():
                       "ibutterfly": "fft_top4_kernel<inverse>"}.get(dom, dom)
     roof["stage"] = dom
     roof["traffic"] = stage_traffic(dom, bits)
+    roof["ncu_pipes"] = stage_pipes(dom, bits)
     # whole step against the sum of per-stage roofline times (slower of bytes and ops per stage)
     t_roof = 0.0
     for k in stages:
