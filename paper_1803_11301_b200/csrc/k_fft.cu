@@ -12,7 +12,7 @@
 //  * fft_top4_kernel: top layers (i+1, i) per HBM round trip; the three twiddles of a block as M8
 //    tables (gf128.cuh), one 768-thread CTA per SM; fft_top_kernel: a single top layer.
 //  * fft_tile_kernel: layers [0, T) of a 2^T-element tile (one HBM read and write for T layers):
-//    layers >= 8 via one M8 table per twiddle, layers 6-7 via M4 tables 8 twiddles at a time, lower
+//    layers >= 9 via one M8 table per twiddle, layers 6-8 via M4 tables 8 twiddles at a time, lower
 //    layers (twiddles vary per block) via the generic IMAD-hole gf_mul.
 //  * fft_tile_fused_kernel: forward layers [0,T) of operand b, the pointwise product with operand
 //    a (subsystem 3, kernels_impl.hpp:116-123), and inverse layers [0,T) in one tile pass.
@@ -152,11 +152,15 @@ __global__ void __launch_bounds__(kTop4Threads, 1) fft_top4_kernel(uint4* __rest
 }
 
 // ------------------------------------------------------------------ tile layers (i < T)
-// Layers i >= kTabLayer of a 256-thread tile have <= 2 twiddles per tile, each shared by >= 256
+// Layers i >= kTabLayer of a 256-thread tile have <= 2 twiddles per tile, each shared by >= 512
 // butterflies: those use an M8 table built in shared memory (tab != nullptr: 64 KiB + 144 rows
-// after the tile) instead of the generic multiply.
-constexpr unsigned kTabLayer = 8;
-// Layers [kM4Layer, kTabLayer): rotated 4-bit tables for 8 twiddles at a time (gf128.cuh m4s_*).
+// after the tile) instead of the generic multiply.  (Layer 8's four twiddles per 2^11 tile: M4
+// tables, 57.8 vs 58.3 ms at 2^32 bits; all tile layers on M4: 63.3 ms.)
+#ifndef FPM_M8_LAYER
+#define FPM_M8_LAYER 9
+#endif
+constexpr unsigned kTabLayer = FPM_M8_LAYER;
+// Layers [kM4Layer, kTabLayer): rotated 4-bit tables for up to 8 twiddles at a time (gf128.cuh m4s_*).
 constexpr unsigned kM4Layer = 6;
 // Layers [kPrepLayer, kM4Layer): generic multiplies with the twiddle's limbs prepared once per block.
 constexpr unsigned kPrepLayer = 1;
@@ -169,16 +173,16 @@ __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, u
     const uint64_t bhi = tile_idx << (T - 1 - i);  // global block index of the tile's first block
     // w = v_{l+64-i} ^ C2P(2*(bhi + blk)) = Z ^ C2P(2*blk)  (bit ranges disjoint, C2P linear)
     const uint4 Z = twiddle(tw, l, i, bhi);
-    if (tab && i >= kM4Layer && i < kTabLayer && (npairs >> i) % 8 == 0) {
-      // 2^(T-1-i) twiddles of 2^i butterflies each: rotated 4-bit tables, 8 twiddles per round
+    if (tab && i >= kM4Layer && i < kTabLayer) {
+      // 2^(T-1-i) twiddles of 2^i butterflies each: rotated 4-bit tables, up to 8 twiddles per round
       const int q = threadIdx.x & 7;
-      const int nblk = npairs >> i;
-      for (int b0 = 0; b0 < nblk; b0 += 8) {
+      const int nblk = npairs >> i, G = nblk < 8 ? nblk : 8;
+      for (int b0 = 0; b0 < nblk; b0 += G) {
         const uint4 w = x4(Z, c2p2(tw.c2p, (uint64_t)(b0 + (threadIdx.x >> 5))));
         __syncthreads();  // previous round's lookups done
-        m4s_build8(tab, w, threadIdx.x);
+        if (threadIdx.x < 32 * G) m4s_build8(tab, w, threadIdx.x);
         __syncthreads();
-        for (int p = threadIdx.x; p < (8 << i); p += blockDim.x) {
+        for (int p = threadIdx.x; p < (G << i); p += blockDim.x) {
           const int t = p >> i, j = p & ((1 << i) - 1), blk = b0 + t;
           const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
           const uint4* tb = tab + t * kM4TabUint4;
