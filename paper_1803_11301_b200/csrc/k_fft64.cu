@@ -154,8 +154,11 @@ __global__ void __launch_bounds__(kTop4Threads64, 2) fft64_top4_kernel(uint2* __
 }
 
 // ------------------------------------------------------------------ tile layers (i < T)
-constexpr unsigned kTabLayer64 = 8;  // layers >= 8 of a 256-thread tile: <= 8 twiddles, G8 tables
-// Layers [kG4Layer, kTabLayer64): 4-bit tables for 16 twiddles per round (gf64.cuh g4_*).
+#ifndef FPM_G8_LAYER
+#define FPM_G8_LAYER 9
+#endif
+constexpr unsigned kTabLayer64 = FPM_G8_LAYER;  // layers >= 9: G8 tables (layer 8 on G4: 48.3 vs 49.0 ms)
+// Layers [kG4Layer, kTabLayer64): 4-bit tables for up to 16 twiddles per round (gf64.cuh g4_*).
 constexpr unsigned kG4Layer = 6;
 template <bool INV>
 __device__ __forceinline__ void tile_layers64(uint2* __restrict__ s, unsigned T, uint64_t tile_idx,
@@ -166,14 +169,14 @@ __device__ __forceinline__ void tile_layers64(uint2* __restrict__ s, unsigned T,
     const unsigned i = INV ? step : T - 1 - step;
     const uint64_t bhi = tile_idx << (T - 1 - i);
     const uint2 Z = twiddle64(tw, i, bhi);  // w = Z ^ C2P(2 blk) (disjoint bit ranges, C2P linear)
-    if (tab && i >= kG4Layer && i < kTabLayer64 && (npairs >> i) % 16 == 0) {
-      const int nblk = npairs >> i;
-      for (int b0 = 0; b0 < nblk; b0 += 16) {
+    if (tab && i >= kG4Layer && i < kTabLayer64) {
+      const int nblk = npairs >> i, G = nblk < 16 ? nblk : 16;
+      for (int b0 = 0; b0 < nblk; b0 += G) {
         const uint2 w = x2(Z, c2p2_64(tw.c2p, (uint64_t)(b0 + (threadIdx.x >> 4))));
         __syncthreads();  // previous round's lookups done
-        g4_build16(tab, w, threadIdx.x);
+        if (threadIdx.x < 16 * G) g4_build16(tab, w, threadIdx.x);
         __syncthreads();
-        for (int p = threadIdx.x; p < (16 << i); p += blockDim.x) {
+        for (int p = threadIdx.x; p < (G << i); p += blockDim.x) {
           const int t = p >> i, j = p & ((1 << i) - 1), blk = b0 + t;
           const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
           const uint2* tb = tab + t * kG4TabUint2;
