@@ -8,7 +8,8 @@
 // and its inverse  F'_d = sum_{k superset of d} x^(k-d) g_k ,  F_d = (F'_d mod x^256) + (F'_{d-1} div x^256).
 // Skewing row d left by d bits turns the shifted subset sums into plain XOR butterflies over the row
 // index (shuffles for row distances < 32, shared memory above).  C_cols is conv(D) with whole rows
-// as units (pure row XORs, kRowSched*), C_rows is conv(256) in registers (conv_regs_gen.cuh).
+// as units (pure row XORs), run as conv_regs on the columns of the transposed tile; C_rows is
+// conv(256) in registers (conv_regs_gen.cuh).
 //
 // Tile layout: 256 rows x 8 words (row-major); thread t owns row t.  A tile holds 2^(16-r)
 // independent chunks (r >= 8) or 256 rows each holding 2^(8-r) chunks (r < 8).
@@ -16,6 +17,7 @@
 #include <cstdint>
 
 #include "conv_regs_gen.cuh"
+#include "warp_bits.cuh"
 
 namespace fpm {
 
@@ -163,6 +165,34 @@ __device__ __forceinline__ void rowpasses_w(uint32_t (&m)[W][8], uint32_t* tile,
   }
 }
 
+// 256 x 256-bit tile transpose (an involution): thread t's row t <-> thread c's column c (word w
+// of a column = rows 32w .. 32w+31).  Each warp transposes its eight 32 x 32 blocks in registers
+// (Transpose32), then the blocks change warps through shared memory (pitch 9: conflict-free).
+// sm: >= 256 x 9 words; all 256 threads call it (two barriers).
+__device__ __forceinline__ void tile_transpose(uint32_t (&m)[8], uint32_t* sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Transpose32 tr(lane);
+  uint32_t x[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) x[j] = tr(m[j]);  // lane l: column 32j + l of rows 32 warp ..
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 8; ++j) sm[(32 * j + lane) * 9 + warp] = x[j];
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < 8; ++w) m[w] = sm[tid * 9 + w];
+}
+
+// conv(2^g) over the tile's rows as units (C_cols): a GF(2)-linear map applied identically to
+// every bit column, so in the transposed tile it is conv_regs on each column word -- two
+// transposes instead of kRowSchedN[g] shared-memory row passes (12 passes, 24 barriers at g = 8).
+template <bool INV>
+__device__ __forceinline__ void colconv_tile(uint32_t (&m)[8], uint32_t* sm, int g) {
+  tile_transpose(m, sm);
+  conv_regs<INV>(g, m);
+  tile_transpose(m, sm);
+}
+
 // Converts every aligned 2^r-bit chunk of the tile (thread t's row in m), r in [1, 16].
 // tile: 256 x kRowPitchW<1> words of shared memory; sc: 256 x kScPitch words of shared memory.
 // All 256 threads must call it (barriers inside when r > 8).
@@ -175,11 +205,11 @@ __device__ __forceinline__ void conv_tile(uint32_t (&m)[8], uint32_t* tile, uint
   const int g = r - 8, d = threadIdx.x & ((1 << g) - 1);
   if (!INV) {
     l1_tile<false>(m, sc, g, d);
-    rowpasses_w<false, 1>(*reinterpret_cast<uint32_t(*)[1][8]>(&m), tile, g, d);
+    colconv_tile<false>(m, tile, g);
     conv_regs<false>(8, m);
   } else {
     conv_regs<true>(8, m);
-    rowpasses_w<true, 1>(*reinterpret_cast<uint32_t(*)[1][8]>(&m), tile, g, d);
+    colconv_tile<true>(m, tile, g);
     l1_tile<true>(m, sc, g, d);
   }
 }

@@ -161,7 +161,10 @@ __global__ void __launch_bounds__(kTop4Threads, 1) fft_top4_kernel(uint4* __rest
 #endif
 constexpr unsigned kTabLayer = FPM_M8_LAYER;
 // Layers [kM4Layer, kTabLayer): rotated 4-bit tables for up to 8 twiddles at a time (gf128.cuh m4s_*).
-constexpr unsigned kM4Layer = 6;
+#ifndef FPM_M4_LAYER
+#define FPM_M4_LAYER 6
+#endif
+constexpr unsigned kM4Layer = FPM_M4_LAYER;
 // Layers [kPrepLayer, kM4Layer): generic multiplies with the twiddle's limbs prepared once per block.
 constexpr unsigned kPrepLayer = 1;
 template <bool INV>

@@ -159,7 +159,10 @@ __global__ void __launch_bounds__(kTop4Threads64, 2) fft64_top4_kernel(uint2* __
 #endif
 constexpr unsigned kTabLayer64 = FPM_G8_LAYER;  // layers >= 9: G8 tables (layer 8 on G4: 48.3 vs 49.0 ms)
 // Layers [kG4Layer, kTabLayer64): 4-bit tables for up to 16 twiddles per round (gf64.cuh g4_*).
-constexpr unsigned kG4Layer = 6;
+#ifndef FPM_G4_LAYER
+#define FPM_G4_LAYER 6
+#endif
+constexpr unsigned kG4Layer = FPM_G4_LAYER;
 template <bool INV>
 __device__ __forceinline__ void tile_layers64(uint2* __restrict__ s, unsigned T, uint64_t tile_idx,
                                               const TwiddleSrc64& tw, uint2* __restrict__ tab) {
