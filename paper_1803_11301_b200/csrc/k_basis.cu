@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32
 }
 // ------------------------------------------------------------------ C: carry + unskew + conv(2^16)
 // g_k[p] = Gs[k][p+k] ^ (p >= 1 ? Gs[k][t+p-1+k] : 0) ^ (k >= 1 ? Gs[k-1][t+p+k-1] : 0), then conv(g_k).
-__global__ void __launch_bounds__(256) carry_rows_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch,
+__global__ void __launch_bounds__(256, 4) carry_rows_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch,
                                                          uint32_t* __restrict__ out, uint64_t D) {
   extern __shared__ uint32_t smem[];
   uint32_t* tile = smem;
@@ -260,32 +260,41 @@ __global__ void __launch_bounds__(256) carry_rows_kernel(const uint32_t* __restr
   uint32_t* sa = smem;                    // Gs[k] words a0 .. a0 + 2048      (L part, bit offset k)
   uint32_t* sh = smem + 2312;             // Gs[k] ^ Gs[k-1], words b0 ..     (H parts, t + k - 1)
   auto pad = [](int w) { return w + (w >> 3); };
+  // coalesced: 2049 words per span; the next row's spans are loaded (into registers) while this
+  // row converts
+  uint32_t va[9], vh[9];
+  auto fetch = [&](uint64_t k) {
+    if (k >= D) return;
+    const uint32_t* rk = gs + k * gs_pitch;
+    const uint32_t* rk1 = gs + (k - (k ? 1 : 0)) * gs_pitch;
+    const uint64_t a0 = k >> 5, b0 = (kT + k - 1) >> 5;
+    uint32_t vb[9], vc[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      const int w = tid + 256 * j;
+      const uint64_t wb = b0 + w;
+      const bool in = w <= kTWords;
+      va[j] = in ? __ldg(rk + a0 + w) : 0u;
+      vb[j] = in && wb < gs_pitch ? __ldg(rk + wb) : 0u;
+      vc[j] = in && wb < gs_pitch && k ? __ldg(rk1 + wb) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 9; ++j) vh[j] = vb[j] ^ vc[j];
+  };
+  fetch(blockIdx.x);
   for (uint64_t k = blockIdx.x; k < D; k += gridDim.x) {
     const uint32_t* rk = gs + k * gs_pitch;
-    const uint32_t* rk1 = k ? gs + (k - 1) * gs_pitch : nullptr;
-    const uint64_t a0 = k >> 5, b0 = (kT + k - 1) >> 5;
     const int sA = (int)(k & 31), sB = (int)((kT + k - 1) & 31);
     __syncthreads();  // the previous row's conversion is done with the shared tile
-    {  // coalesced: 2049 words per span, every load of the thread issued before any store
-      uint32_t va[9], vb[9], vc[9];
 #pragma unroll
-      for (int j = 0; j < 9; ++j) {
-        const int w = tid + 256 * j;
-        const uint64_t wb = b0 + w;
-        const bool in = w <= kTWords;
-        va[j] = in ? __ldg(rk + a0 + w) : 0u;
-        vb[j] = in && wb < gs_pitch ? __ldg(rk + wb) : 0u;
-        vc[j] = in && wb < gs_pitch && k ? __ldg(rk1 + wb) : 0u;
-      }
-#pragma unroll
-      for (int j = 0; j < 9; ++j) {
-        const int w = tid + 256 * j;
-        if (w <= kTWords) {
-          sa[pad(w)] = va[j];
-          sh[pad(w)] = vb[j] ^ vc[j];
-        }
+    for (int j = 0; j < 9; ++j) {
+      const int w = tid + 256 * j;
+      if (w <= kTWords) {
+        sa[pad(w)] = va[j];
+        sh[pad(w)] = vh[j];
       }
     }
+    fetch(k + gridDim.x);
     __syncthreads();
     uint32_t m[8];
     {

@@ -1,7 +1,7 @@
 // Microbenchmark: register-resident GF(2^128) multiply throughput on sm_100a (clk/product/SM).
 #include <cstdio>
 #include <cuda_runtime.h>
-#include "../../paper_1803_11301_b200/csrc/gf128.cuh"
+#include "../../paper_1803_11301_b200/csrc/gf128.cuh"  // from tools/microbench/
 using namespace fpm;
 template <int CH>
 __global__ void __launch_bounds__(256) prep_kernel(uint4* out, int iters, uint4 w0) {
