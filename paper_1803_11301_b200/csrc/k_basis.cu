@@ -640,14 +640,12 @@ __global__ void unit_overflow_kernel(const uint32_t* __restrict__ gs, uint64_t g
 
 // ------------------------------------------------------------------ host orchestration
 void set_smem_attr() {
-  static bool done[64];
-  int dev;
-  FPM_CUDA(cudaGetDevice(&dev));
-  if (done[dev]) return;
-  FPM_CUDA(cudaFuncSetAttribute(conv_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
-  FPM_CUDA(cudaFuncSetAttribute(conv_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
-  FPM_CUDA(cudaFuncSetAttribute(carry_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
-  done[dev] = true;
+  static PerDeviceOnce once;
+  once.run([] {
+    FPM_CUDA(cudaFuncSetAttribute(conv_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
+    FPM_CUDA(cudaFuncSetAttribute(conv_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
+    FPM_CUDA(cudaFuncSetAttribute(carry_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem));
+  });
 }
 
 int grid_cap(uint64_t items, int per_sm) {

@@ -12,6 +12,8 @@
 // table (gf128.cuh M8 layout; GF(2^64): gf64.cuh G8 layout).  Decode runs the same steps in reverse.
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include "fpm_internal.h"
 #include "gf128.cuh"
 #include "gf64.cuh"
@@ -305,8 +307,11 @@ struct RowTables {
   uint4* inv = nullptr;
 };
 const RowTables& row_tables(int dev) {
+  static std::mutex mu;
   static RowTables t[64];
   static bool have[64];
+  if (dev < 0 || dev >= 64) throw Error(kInvalid, "device ordinal out of range");
+  std::lock_guard<std::mutex> lock(mu);
   if (!have[dev]) {
     const FieldTables& ft = field_tables();
     FPM_CUDA(cudaMalloc(&t[dev].rows, 128 * 16));

@@ -319,3 +319,23 @@ def test_basis_cvt_large_roundtrip_and_linearity(gpu, lg):
     gpu.stage_dev("i_basis_cvt", fx, n)
     torch.cuda.synchronize()
     assert torch.equal(fx, x), "round trip"
+
+
+def test_concurrent_host_calls(gpu, checker):
+    """The reference's fp_polymul is safe to call from several threads (its per-field singletons and
+    the twiddle-plan cache are mutex-guarded, cantor.cpp:136-140, polymul.cpp:63-74); so is ours:
+    four host threads, mixed sizes (tiny shapes use the lazily uploaded row tables) and fields,
+    every product checked."""
+    import concurrent.futures as cf
+    rng = np.random.default_rng(77)
+    jobs = []
+    for k in range(24):
+        la = int(rng.choice([7, 300, 4096, 70000, 1 << 20]))
+        lb = int(rng.choice([5, 129, 4096, 1 << 18]))
+        a, b = rnd_words(rng, la), rnd_words(rng, lb)
+        field = [gpu.FIELD_GF128, gpu.FIELD_GF64, gpu.FIELD_AUTO][k % 3]
+        jobs.append((a, la, b, lb, field))
+    with cf.ThreadPoolExecutor(4) as ex:
+        got = list(ex.map(lambda j: gpu.fp_polymul(j[0], j[1], j[2], j[3], field=j[4]), jobs))
+    for (a, la, b, lb, _), g in zip(jobs, got):
+        assert np.array_equal(g, checker.polymul(a, la, b, lb)), (la, lb)
