@@ -67,15 +67,15 @@ int fpm_device_count(void);
  * passes.  Used by bench.py to attribute work to kernels; never fails. */
 unsigned fpm_fft_tile_log2(unsigned l);
 
-/* plan_mul (proj/src/polymul.cpp:187-219).  field: FPM_FIELD_*.  The GPU pipeline always runs
- * GF(2^128); plan_mul still reports the reference's choice for the requested field. */
+/* plan_mul (proj/src/polymul.cpp:187-219).  field: FPM_FIELD_*; the pipeline runs the field the
+ * plan reports (GF(2^64) for FPM_FIELD_AUTO whenever it supports the size). */
 fpm_status fpm_plan_mul(size_t a_bits, size_t b_bits, int field, fpm_plan* out);
 
 /* fp_polymul (polymul.hpp:74-75, polymul.cpp:223-239) on host buffers.
  * c receives ceil((a_bits+b_bits-1)/64) words (bits >= a_bits+b_bits-1 cleared); nothing is
- * written when either length is 0.  field: FPM_FIELD_AUTO or FPM_FIELD_GF128 (GF(2^64) is not
- * built yet -> FPM_EINVAL).  stage_seconds: NULL or double[FPM_NUM_STAGES] (accumulated).
- * device: CUDA ordinal. */
+ * written when either length is 0.  field: FPM_FIELD_AUTO (short inputs: karatsuba_mul, else
+ * plan_mul's field), FPM_FIELD_GF64 or FPM_FIELD_GF128.  stage_seconds: NULL or
+ * double[FPM_NUM_STAGES] (accumulated).  device: CUDA ordinal. */
 fpm_status fpm_polymul(const uint64_t* a, size_t a_bits, const uint64_t* b, size_t b_bits, uint64_t* c,
                        int field, int device, double* stage_seconds);
 
@@ -90,6 +90,18 @@ fpm_status fpm_polymul_dev(const uint64_t* d_a, size_t a_bits, const uint64_t* d
 fpm_status fpm_polymul_batch_dev(const uint64_t* d_a, size_t a_bits, size_t a_stride_words, const uint64_t* d_b,
                                  size_t b_bits, size_t b_stride_words, uint64_t* d_c, size_t c_stride_words,
                                  size_t count, void* stream);
+
+/* karatsuba_mul (proj/include/fpmul/polymul.hpp:85-87, polymul.cpp:268-282) on host buffers: the
+ * exact product by word-level carry-less multiplication (no FFT), c as for fpm_polymul.  Also what
+ * fpm_polymul / fpm_polymul_dev run in FPM_FIELD_AUTO when max(a_bits, b_bits) < 4096, the
+ * reference's fft_threshold_bits default (polymul.cpp:226-231, polymul.hpp:65).  It is the
+ * independent cross-check of the FFT path, as in the reference. */
+fpm_status fpm_karatsuba_mul(const uint64_t* a, size_t a_bits, const uint64_t* b, size_t b_bits, uint64_t* c,
+                             int device);
+/* naive_mul_words_kernel (proj/include/fpmul/detail/kernels.hpp:115-118) on device buffers, except
+ * that d_out[0 .. wa+wb) is overwritten (not accumulated): d_out = d_a * d_b carry-less. */
+fpm_status fpm_clmul_words_dev(const uint64_t* d_a, size_t wa, const uint64_t* d_b, size_t wb, uint64_t* d_out,
+                               void* stream);
 
 /* ---- stage entry points on device buffers, field GF(2^128) ---- */
 

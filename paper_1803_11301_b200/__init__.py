@@ -25,6 +25,9 @@ from ._lib import (  # noqa: F401
     device_count,
     encode,
     fp_polymul,
+    karatsuba_mul,
+    naive_mul,
+    clmul_words_dev,
     fp_polymul_batch_dev,
     fp_polymul_dev,
     gf128_mul,

@@ -79,6 +79,8 @@ def lib():
         L.fpm_decode_cols_dev.argtypes = [vp, sz, vp, vp]
         L.fpm_bfly_pair_dev.argtypes = [vp, vp, sz, _u64p, C.c_int, C.c_int, vp]
         L.fpm_twiddle128.argtypes = [C.c_uint, C.c_uint64, _u64p, _u64p]
+        L.fpm_karatsuba_mul.argtypes = [_u64p, sz, _u64p, sz, _u64p, C.c_int]
+        L.fpm_clmul_words_dev.argtypes = [vp, sz, vp, sz, vp, vp]
         _LIB = L
     return _LIB
 
@@ -155,6 +157,22 @@ def fp_polymul(a, a_bits: int, b, b_bits: int, field: int = FIELD_AUTO, device: 
     if stage_seconds is not None:
         stage_seconds[:] = list(st)
     return c
+
+
+def karatsuba_mul(a, a_bits: int, b, b_bits: int, device: int = 0) -> np.ndarray:
+    """karatsuba_mul (proj/src/polymul.cpp:268-282): the exact product by word-level carry-less
+    multiplication on the GPU, no FFT -- the independent cross-check of fp_polymul."""
+    a, b = _as_u64(a), _as_u64(b)
+    if a.size < _words(a_bits) or b.size < _words(b_bits):
+        raise ValueError("karatsuba_mul: word arrays shorter than the declared bit lengths")
+    if a_bits == 0 or b_bits == 0:
+        return np.zeros(0, np.uint64)
+    c = np.zeros(_words(a_bits + b_bits - 1), np.uint64)
+    _check(lib().fpm_karatsuba_mul(_ptr(a), a_bits, _ptr(b), b_bits, _ptr(c), device))
+    return c
+
+
+naive_mul = karatsuba_mul  # polymul.hpp:83: the same exact product
 
 
 def basis_cvt(w, n_bits: int, content_bits: int | None = None, device: int = 0) -> np.ndarray:
@@ -293,6 +311,14 @@ def _stream(stream):
         return stream
     import torch
     return torch.cuda.current_stream().cuda_stream
+
+
+def clmul_words_dev(a, b, out, stream=None) -> None:
+    """naive_mul_words_kernel (detail/kernels.hpp:115-118) on device tensors: out[0 .. a.numel() +
+    b.numel()) = a * b carry-less (overwritten)."""
+    if out.numel() < a.numel() + b.numel():
+        raise ValueError("clmul_words_dev: output shorter than a + b words")
+    _check(lib().fpm_clmul_words_dev(_dptr(a), a.numel(), _dptr(b), b.numel(), _dptr(out), _stream(stream)))
 
 
 def fp_polymul_dev(a, a_bits: int, b, b_bits: int, c, field: int = FIELD_AUTO, stream=None,

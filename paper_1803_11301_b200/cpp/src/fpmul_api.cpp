@@ -5,6 +5,7 @@
 // in the reference.  GF(2^128) and GF(2^64) stages run on the GPU; the GF(2^16) test field's stage
 // calls are not built on this backend and throw std::invalid_argument.  Errors follow the reference:
 // std::invalid_argument for shape/length problems, std::runtime_error otherwise.
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <stdexcept>
@@ -460,17 +461,31 @@ BitPoly gpu_product(const BitPoly& a, const BitPoly& b, int field, StageSeconds*
 
 BitPoly fp_polymul(const BitPoly& a, const BitPoly& b) { return fp_polymul(a, b, MulOptions{}); }
 
-BitPoly fp_polymul(const BitPoly& a, const BitPoly& b, const MulOptions& opts) {
+BitPoly karatsuba_mul(const BitPoly& a, const BitPoly& b) {
   if (!a.bit_length() || !b.bit_length()) return BitPoly{};
-  // The reference's field choice (plan_mul, polymul.cpp:203-205): kAuto runs GF(2^64) when it
-  // supports the size; the product is the same in every field.
-  const int f = opts.field == FieldChoice::kGF64 ? FPM_FIELD_GF64
-              : opts.field == FieldChoice::kGF128 ? FPM_FIELD_GF128 : FPM_FIELD_AUTO;
-  return gpu_product(a, b, f, opts.stage_seconds);
+  BitPoly c(a.bit_length() + b.bit_length() - 1);
+  check(fpm_karatsuba_mul(a.word_data(), a.bit_length(), b.word_data(), b.bit_length(), c.word_data(),
+                          current_device()));
+  return c;
 }
 
-BitPoly naive_mul(const BitPoly& a, const BitPoly& b) { return gpu_product(a, b, FPM_FIELD_GF128, nullptr); }
-BitPoly karatsuba_mul(const BitPoly& a, const BitPoly& b) { return gpu_product(a, b, FPM_FIELD_GF128, nullptr); }
+// polymul.hpp:83: schoolbook and Karatsuba give the same words; both run the GPU word product.
+BitPoly naive_mul(const BitPoly& a, const BitPoly& b) { return karatsuba_mul(a, b); }
+
+BitPoly fp_polymul(const BitPoly& a, const BitPoly& b, const MulOptions& opts) {
+  if (!a.bit_length() || !b.bit_length()) return BitPoly{};
+  const size_t max_len = std::max(a.bit_length(), b.bit_length());
+  // polymul.cpp:226-231: in auto mode short inputs take karatsuba_mul
+  if (opts.field == FieldChoice::kAuto && max_len < opts.fft_threshold_bits) return karatsuba_mul(a, b);
+  // The reference's field choice (plan_mul, polymul.cpp:203-205): kAuto runs GF(2^64) when it
+  // supports the size.  Resolved here so that a caller-chosen fft_threshold_bits below the C-ABI's
+  // default is honoured (the C-ABI applies the default threshold only to FPM_FIELD_AUTO).
+  fpm_plan p{};
+  const int req = opts.field == FieldChoice::kGF64 ? FPM_FIELD_GF64
+                : opts.field == FieldChoice::kGF128 ? FPM_FIELD_GF128 : FPM_FIELD_AUTO;
+  check(fpm_plan_mul(a.bit_length(), b.bit_length(), req, &p));
+  return gpu_product(a, b, p.field_degree == 64 ? FPM_FIELD_GF64 : FPM_FIELD_GF128, opts.stage_seconds);
+}
 
 template <class F>
 EvalVec<F> pointwise_mul(std::span<const FieldElem<F>> u, std::span<const FieldElem<F>> v, ExecPolicy) {

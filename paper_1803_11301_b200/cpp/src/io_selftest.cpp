@@ -246,9 +246,19 @@ SelftestReport run_selftest(const SelftestOptions& opts, std::ostream& log) {
     return fp_polymul(one, b) == b && p.max_degree_plus_one() == 1000 + 4096 + 1;
   });
   c.guarded("polymul.fp_polymul vs schoolbook", [&] {
+    MulOptions fft;  // short inputs: auto mode takes karatsuba_mul, kGF128 forces the FFT pipeline
+    fft.field = FieldChoice::kGF128;
     for (int k = 0; k < (full ? 12 : 4); ++k) {
       const BitPoly a = random_bitpoly(1 + rng() % 3000, rng), b = random_bitpoly(1 + rng() % 3000, rng);
-      if (fp_polymul(a, b) != schoolbook(a, b)) return false;
+      const BitPoly want = schoolbook(a, b);
+      if (fp_polymul(a, b) != want || fp_polymul(a, b, fft) != want) return false;
+    }
+    return true;
+  });
+  c.guarded("polymul.FFT pipeline vs karatsuba_mul (independent GPU paths)", [&] {
+    for (size_t lg : {size_t{14}, full ? size_t{20} : size_t{17}}) {
+      const BitPoly a = random_bitpoly((size_t{1} << lg) + 5, rng), b = random_bitpoly(size_t{1} << lg, rng);
+      if (fp_polymul(a, b) != karatsuba_mul(a, b)) return false;
     }
     return true;
   });

@@ -11,6 +11,7 @@
 // device every entry point returns FPM_ECUDA.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstring>
@@ -294,9 +295,45 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
   clk.finish();
 }
 
+// karatsuba_mul (polymul.cpp:268-282) on device buffers: the word product of the masked operands,
+// trimmed to a_bits + b_bits - 1 bits.
+void karatsuba_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_t b_bits, uint64_t* d_c,
+                      cudaStream_t s) {
+  const uint64_t wa = (a_bits + 63) / 64, wb = (b_bits + 63) / 64;
+  const size_t out_bits = a_bits + b_bits - 1;
+  DevBuf X(wa * 8, s), Y(wb * 8, s), P((wa + wb) * 8, s);
+  load_operand_kernel<<<grid_1d(wa), 256, 0, s>>>(X.as<uint64_t>(), wa, d_a, a_bits);
+  FPM_LAUNCH_CHECK();
+  load_operand_kernel<<<grid_1d(wb), 256, 0, s>>>(Y.as<uint64_t>(), wb, d_b, b_bits);
+  FPM_LAUNCH_CHECK();
+  clmul_words_device(X.as<uint64_t>(), wa, Y.as<uint64_t>(), wb, P.as<uint64_t>(), s);
+  const uint64_t out_words = (out_bits + 63) / 64;
+  store_product_kernel<<<grid_1d(out_words), 256, 0, s>>>(d_c, P.as<uint64_t>(), out_bits, 0, out_words);
+  FPM_LAUNCH_CHECK();
+}
+
 void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_t b_bits, uint64_t* d_c,
                     int field, cudaStream_t s, double* stages, const HostIO* io = nullptr) {
   if (!a_bits || !b_bits) return;
+  if (field == FPM_FIELD_AUTO && std::max(a_bits, b_bits) < kFftThresholdBits) {
+    // the reference's auto-mode bypass (polymul.cpp:226-231): short inputs take karatsuba_mul
+    if (io && io->ready[0]) FPM_CUDA(cudaStreamWaitEvent(s, io->ready[0], 0));
+    if (io && io->ready[1]) FPM_CUDA(cudaStreamWaitEvent(s, io->ready[1], 0));
+    StageClock clk(s, stages);
+    clk.mark(kStPointwise);
+    karatsuba_device(d_a, a_bits, d_b, b_bits, d_c, s);
+    clk.finish();
+    if (io && io->h_out) {
+      const uint64_t out_words = (a_bits + b_bits - 1 + 63) / 64;
+      cudaEvent_t done;
+      FPM_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      FPM_CUDA(cudaEventRecord(done, s));
+      FPM_CUDA(cudaStreamWaitEvent(io->d2h, done, 0));
+      FPM_CUDA(cudaEventDestroy(done));  // released once the wait is satisfied
+      FPM_CUDA(cudaMemcpyAsync(io->h_out, d_c, out_words * 8, cudaMemcpyDeviceToHost, io->d2h));
+    }
+    return;
+  }
   const fpm_plan p = plan_mul(a_bits, b_bits, field);  // validates the field and the size bound
   if (p.field_degree == 64) run_pipeline<Gf64Ops>(d_a, a_bits, d_b, b_bits, d_c, p, s, stages, io);
   else run_pipeline<Gf128Ops>(d_a, a_bits, d_b, b_bits, d_c, p, s, stages, io);
@@ -524,6 +561,30 @@ fpm_status fpm_polymul_batch_dev(const uint64_t* d_a, size_t a_bits, size_t a_st
     if (!a_bits || !b_bits || !count) return;
     polymul_batch_device(d_a, a_bits, a_stride_words, d_b, b_bits, b_stride_words, d_c, c_stride_words, count,
                          (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_clmul_words_dev(const uint64_t* d_a, size_t wa, const uint64_t* d_b, size_t wb, uint64_t* d_out,
+                               void* stream) {
+  return guard([&] {
+    require_device();
+    clmul_words_device(d_a, wa, d_b, wb, d_out, (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_karatsuba_mul(const uint64_t* a, size_t a_bits, const uint64_t* b, size_t b_bits, uint64_t* c,
+                             int device) {
+  return guard([&] {
+    if (!a_bits || !b_bits) return;
+    DeviceGuard g(device);
+    cudaStream_t s = host_stream(device);
+    const size_t wa = (a_bits + 63) / 64, wb = (b_bits + 63) / 64, wc = (a_bits + b_bits - 1 + 63) / 64;
+    DevBuf A(wa * 8, s), B(wb * 8, s), C(wc * 8, s);
+    FPM_CUDA(cudaMemcpyAsync(A.p, a, wa * 8, cudaMemcpyHostToDevice, s));
+    FPM_CUDA(cudaMemcpyAsync(B.p, b, wb * 8, cudaMemcpyHostToDevice, s));
+    karatsuba_device(A.as<uint64_t>(), a_bits, B.as<uint64_t>(), b_bits, C.as<uint64_t>(), s);
+    FPM_CUDA(cudaMemcpyAsync(c, C.p, wc * 8, cudaMemcpyDeviceToHost, s));
+    FPM_CUDA(cudaStreamSynchronize(s));
   });
 }
 

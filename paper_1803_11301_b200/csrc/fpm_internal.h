@@ -155,6 +155,11 @@ void encode64_device(const uint32_t* poly, unsigned l, uint2* ev, int rows_live,
 void decode64_device(const uint2* ev, unsigned l, uint32_t* poly, cudaStream_t s);
 
 // Whole small products in one CTA each (k_batch.cu); n_bits = padded product length <= 2^17.
+// Carry-less word product out[0 .. wa + wb) = a * b (k_clmul.cu; polymul.cpp:156-183, 268-282).
+void clmul_words_device(const uint64_t* a, uint64_t wa, const uint64_t* b, uint64_t wb, uint64_t* out,
+                        cudaStream_t s);
+// fp_polymul's auto-mode threshold (MulOptions::fft_threshold_bits default, polymul.hpp:65).
+constexpr size_t kFftThresholdBits = size_t{1} << 12;
 void polymul_batch_device(const uint64_t* a, size_t a_bits, size_t a_stride_words,
                           const uint64_t* b, size_t b_bits, size_t b_stride_words, uint64_t* c,
                           size_t c_stride_words, size_t count, cudaStream_t s);

@@ -339,3 +339,42 @@ def test_concurrent_host_calls(gpu, checker):
         got = list(ex.map(lambda j: gpu.fp_polymul(j[0], j[1], j[2], j[3], field=j[4]), jobs))
     for (a, la, b, lb, _), g in zip(jobs, got):
         assert np.array_equal(g, checker.polymul(a, la, b, lb)), (la, lb)
+
+
+@pytest.mark.parametrize("la,lb", [(1, 1), (63, 64), (64, 65), (4095, 4095), (4096, 100), (700, 9000),
+                                   (100_000, 77_777), (1 << 20, (1 << 19) + 3)])
+def test_karatsuba_mul(gpu, checker, la, lb):
+    """karatsuba_mul / naive_mul (polymul.cpp:268-282, polymul.hpp:83-87): the word-level GPU
+    product, an algorithm independent of the FFT path, equals the reference product."""
+    rng = np.random.default_rng(la * 7 + lb)
+    a, b = rnd_words(rng, la), rnd_words(rng, lb)
+    want = checker.polymul(a, la, b, lb)
+    assert np.array_equal(gpu.karatsuba_mul(a, la, b, lb), want)
+    if la < 4096 and lb < 4096:  # the reference's auto-mode bypass (polymul.cpp:226-231)
+        assert np.array_equal(gpu.fp_polymul(a, la, b, lb, field=gpu.FIELD_AUTO), want)
+    # garbage above the declared length is ignored, as for fp_polymul
+    ga, gb = a.copy(), b.copy()
+    if la % 64:
+        ga[-1] |= np.uint64(~((1 << (la % 64)) - 1) & (2**64 - 1))
+    if lb % 64:
+        gb[-1] |= np.uint64(~((1 << (lb % 64)) - 1) & (2**64 - 1))
+    assert np.array_equal(gpu.karatsuba_mul(ga, la, gb, lb), want)
+
+
+def test_clmul_words_dev(gpu, checker):
+    """naive_mul_words_kernel (detail/kernels.hpp:115-118) on device tensors: full words, out
+    overwritten (stale contents must not leak in)."""
+    import torch
+    rng = np.random.default_rng(5)
+    for wa, wb in [(1, 1), (3, 700), (256, 256), (257, 255), (1000, 3000)]:
+        a, b = rnd_words(rng, 64 * wa), rnd_words(rng, 64 * wb)
+        ta = torch.from_numpy(a.view(np.int64)).cuda()
+        tb = torch.from_numpy(b.view(np.int64)).cuda()
+        out = torch.full((wa + wb,), -1, dtype=torch.int64, device="cuda")
+        gpu.clmul_words_dev(ta, tb, out)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy().view(np.uint64)
+        want = np.zeros(wa + wb, np.uint64)
+        w = checker.polymul(a, 64 * wa, b, 64 * wb)
+        want[: w.size] = w
+        assert np.array_equal(got, want), (wa, wb)
