@@ -130,7 +130,7 @@ def stage_traffic(stage: str, bits: int):
         return None
 
 
-def algorithmic(stage: str, bits: int, T: int):
+def algorithmic(stage: str, bits: int, T: int, fused_ab: bool = False):
     """SURVEY.md 8(d) per-unit algorithmic work of one product with equal operands of `bits` bits,
     per pipeline stage (each stage is one kernel class).
     Returns (bytes, int32 ops): HBM bytes a perfect kernel moves, and 552 ops per GF(2^128)
@@ -147,10 +147,14 @@ def algorithmic(stage: str, bits: int, T: int):
         return 2 * (bits // 8 + V), 0
     if stage == "decode":
         return V + n // 8, 0
-    if stage == "butterfly":            # radix-4 passes over layers [T, l) of both operands + tile pass of a
+    if stage == "butterfly":            # radix-4 passes over layers [T, l) of both operands (+ tile pass of a)
         passes = (l - T + 1) // 2
+        if fused_ab:
+            return 2 * passes * 2 * V, 552 * (l - T) * n_p
         return 2 * passes * 2 * V + 2 * V, 552 * ((l - T) * n_p + T * n_p // 2)
-    if stage == "pointwise":            # fft_tile_fused_kernel: b's tile layers, a*b, inverse tile layers
+    if stage == "pointwise":            # fused tile pass: b's (and a's) tile layers, a*b, inverse tile layers
+        if fused_ab:
+            return 3 * V, 552 * (3 * T * n_p // 2 + n_p)
         return 3 * V, 552 * (T * n_p + n_p)
     if stage == "ibutterfly":
         passes = (l - T + 1) // 2
@@ -480,7 +484,8 @@ def main():
     dom = max(stages, key=stages.get)
     l_fft = (2 * bits // 128).bit_length() - 1
     T = pkg.fft_tile_log2(l_fft)
-    nbytes, ops = algorithmic(dom, bits, T)
+    fab = pkg.pipeline_fuses_operands(l_fft)
+    nbytes, ops = algorithmic(dom, bits, T, fab)
     clocks = clk.summary()
     hbm, peak_kind = peaks()
     mhz = clocks.get("sm_mhz") or 1965.0
@@ -497,7 +502,8 @@ def main():
         achieved = nbytes / stages[dom] / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "peak_source": peak_kind}
-    roof["kernel"] = {"pointwise": "fft_tile_fused_kernel", "butterfly": "fft_top4_kernel + fft_tile_kernel",
+    roof["kernel"] = {"pointwise": "fft_tile_fused2_kernel" if fab else "fft_tile_fused_kernel",
+                      "butterfly": "fft_top4_kernel" if fab else "fft_top4_kernel + fft_tile_kernel",
                       "ibutterfly": "fft_top4_kernel<inverse>"}.get(dom, dom)
     roof["stage"] = dom
     roof["traffic"] = stage_traffic(dom, bits)
@@ -505,7 +511,7 @@ def main():
     # whole step against the sum of per-stage roofline times (slower of bytes and ops per stage)
     t_roof = 0.0
     for k in stages:
-        nb, op = algorithmic(k, bits, T)
+        nb, op = algorithmic(k, bits, T, fab)
         t_roof += max(nb / (hbm * 1e9), op / (peak_tops * 1e12))
     roof["step_frac"] = round(t_roof / (sum(stages.values())), 4)
     roof["stage_ms"] = {k: round(v * 1e3, 3) for k, v in stages.items()}

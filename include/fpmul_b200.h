@@ -62,10 +62,13 @@ const char* fpm_version(void);
 /* Number of CUDA devices visible (0 when none); never fails. */
 int fpm_device_count(void);
 
-/* Schedule introspection (no reference counterpart): the butterfly layers [0, T) of a 2^l-element
- * transform run in shared-memory tiles (one launch per operand pass), layers [T, l) in radix-4
- * passes.  Used by bench.py to attribute work to kernels; never fails. */
+/* Schedule introspection (no reference counterpart): in the product pipeline the butterfly layers
+ * [0, T) of a 2^l-element transform run in shared-memory tiles, layers [T, l) in radix-4 passes;
+ * fpm_pipeline_fuses_operands(l) = 1 when both operands' tile layers run inside the fused
+ * pointwise pass (else operand a has its own tile pass).  Used by bench.py to attribute work to
+ * kernels; never fail. */
 unsigned fpm_fft_tile_log2(unsigned l);
+int fpm_pipeline_fuses_operands(unsigned l);
 
 /* plan_mul (proj/src/polymul.cpp:187-219).  field: FPM_FIELD_*; the pipeline runs the field the
  * plan reports (GF(2^64) for FPM_FIELD_AUTO whenever it supports the size). */

@@ -39,6 +39,7 @@ from ._lib import (  # noqa: F401
     decode64,
     encode64,
     fft_tile_log2,
+    pipeline_fuses_operands,
     lch_butterfly64,
     pointwise64,
     tables64,

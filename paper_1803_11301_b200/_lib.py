@@ -48,6 +48,7 @@ def lib():
         L.fpm_version.restype = C.c_char_p
         L.fpm_fft_tile_log2.restype = C.c_uint
         L.fpm_fft_tile_log2.argtypes = [C.c_uint]
+        L.fpm_pipeline_fuses_operands.argtypes = [C.c_uint]
         L.fpm_launch_count.restype = C.c_uint64
         L.fpm_launch_count.argtypes = [C.c_int]
         L.fpm_plan_mul.argtypes = [sz, sz, C.c_int, C.POINTER(_Plan)]
@@ -117,8 +118,14 @@ def launch_count(reset: bool = False) -> int:
 
 
 def fft_tile_log2(l: int) -> int:
-    """Butterfly layers below this run in shared-memory tiles, the rest in radix-4 passes."""
+    """Product pipeline: butterfly layers below this run in shared-memory tiles, the rest in
+    radix-4 passes."""
     return int(lib().fpm_fft_tile_log2(l))
+
+
+def pipeline_fuses_operands(l: int) -> bool:
+    """Whether both operands' tile layers run inside the fused pointwise pass."""
+    return bool(lib().fpm_pipeline_fuses_operands(l))
 
 
 def plan_mul(a_bits: int, b_bits: int, field: int = FIELD_AUTO) -> dict:

@@ -175,7 +175,7 @@ struct Gf128Ops {
   using Tw = TwiddleSrc;
   static constexpr int kLiveRows = 64;  // rows >= m/2 of a padded operand are zero
   static Tw twiddles(int dev, unsigned l) { return make_twiddle_src(dev, l, partition_base(l)); }
-  static unsigned tile_log2(unsigned l) { return fft_tile_log2(l); }
+  static unsigned tile_log2(unsigned l) { return pipeline_tile_log2(l); }
   static void encode(const uint32_t* p, unsigned l, E* ev, cudaStream_t s) { encode_device_rows(p, l, ev, kLiveRows, s); }
   static void decode(const E* ev, unsigned l, uint32_t* p, cudaStream_t s) { decode_device(ev, l, p, s); }
   static void top(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s) {
@@ -186,6 +186,11 @@ struct Gf128Ops {
   }
   static void fused(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s) {
     butterfly_tile_fused_device(ea, eb, l, T, tw, s);
+  }
+  // both operands' tile layers in the fused pass (no separate tile pass of operand a)
+  static bool fuse_ab(unsigned T) { return tile_fused2_enabled(T); }
+  static void fused2(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s) {
+    butterfly_tile_fused2_device(ea, eb, l, T, tw, s);
   }
 };
 struct Gf64Ops {
@@ -205,6 +210,8 @@ struct Gf64Ops {
   static void fused(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s) {
     butterfly64_tile_fused_device(ea, eb, l, T, tw, s);
   }
+  static bool fuse_ab(unsigned) { return false; }
+  static void fused2(const E*, E*, unsigned, unsigned, const Tw&, cudaStream_t) {}
 };
 
 // fp_polymul on device buffers.  field: FPM_FIELD_GF128, FPM_FIELD_GF64, or FPM_FIELD_AUTO (the
@@ -239,6 +246,7 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     return;
   }
   const unsigned l = p.l, T = F::tile_log2(l);
+  const bool fuse_ab = T > 0 && F::fuse_ab(T);
   int dev;
   FPM_CUDA(cudaGetDevice(&dev));
   const typename F::Tw tw = F::twiddles(dev, l);
@@ -270,10 +278,11 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     F::encode(work32, l, es[k], s);
     clk.mark(kStBfly);
     F::top(es[k], l, T, false, tw, s);
-    if (k == 0) F::tile(es[k], l, T, false, tw, s);
+    if (k == 0 && !fuse_ab) F::tile(es[k], l, T, false, tw, s);
   }
-  clk.mark(kStPointwise);  // + operand b's bottom T forward and the bottom T inverse layers (fused)
-  F::fused(EA.as<E>(), EB.as<E>(), l, T, tw, s);
+  clk.mark(kStPointwise);  // + operand b's (and a's) bottom T forward and the bottom T inverse layers (fused)
+  if (fuse_ab) F::fused2(EA.as<E>(), EB.as<E>(), l, T, tw, s);
+  else F::fused(EA.as<E>(), EB.as<E>(), l, T, tw, s);
   clk.mark(kStIBfly);
   F::top(EB.as<E>(), l, T, true, tw, s);
   clk.mark(kStDecode);
@@ -487,7 +496,11 @@ extern "C" {
 const char* fpm_last_error(void) { return g_err.c_str(); }
 const char* fpm_version(void) { return "fpmul_b200 0.1 (sm_100a)"; }
 
-unsigned fpm_fft_tile_log2(unsigned l) { return fpm::fft_tile_log2(l); }
+unsigned fpm_fft_tile_log2(unsigned l) { return fpm::pipeline_tile_log2(l); }
+int fpm_pipeline_fuses_operands(unsigned l) {
+  const unsigned T = fpm::pipeline_tile_log2(l);
+  return l >= 18 && T > 0 && fpm::tile_fused2_enabled(T) ? 1 : 0;
+}
 int fpm_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;

@@ -139,6 +139,10 @@ unsigned fft_tile_log2(unsigned l);
 void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s);
 void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s);
 // Fused: forward layers [0, T) of b's tiles, pointwise * a, inverse layers [0, T).
+bool tile_fused2_enabled(unsigned T);
+unsigned pipeline_tile_log2(unsigned l);
+void butterfly_tile_fused2_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
+                                  cudaStream_t s);
 void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
                                  cudaStream_t s);
 

@@ -136,13 +136,14 @@ __device__ __forceinline__ uint4 gf_mul_xk(uint4 w, unsigned k) {
 // 16 lookups per product (2 clk/mul/SM of shared-memory bandwidth).
 constexpr int kM8Uint4 = 4096;
 
-// Build by exactly 256 threads: thread (c = tid & 15, s = tid >> 4) writes entries v = 16s..16s+15
+// Build by threads tid < 256: thread (c = tid & 15, s = tid >> 4) writes entries v = 16s..16s+15
 // of chunk c -- the high nibble s once from rows 8c+4..8c+7, the 16 low-nibble combinations
 // incrementally in registers; stores are conflict-free (a quarter-warp covers 8 bank groups).
 // rows_scratch: 144 uint4 of shared memory (row k padded to k + k/8).
 __device__ __forceinline__ void m8_build(uint4* __restrict__ tab, uint4* __restrict__ rows_scratch, uint4 w, int tid) {
   if (tid < 128) rows_scratch[tid + (tid >> 3)] = gf_mul_xk(w, (unsigned)tid);
   __syncthreads();
+  if (tid < 256) {  // larger CTAs: the other threads only join the barriers
   const int c = tid & 15, s = tid >> 4;
   uint4 r[8];
 #pragma unroll
@@ -157,6 +158,7 @@ __device__ __forceinline__ void m8_build(uint4* __restrict__ tab, uint4* __restr
   uint4* dst = tab + (c >> 3) * 2048 + 16 * s * 8 + (c & 7);
 #pragma unroll
   for (int u = 0; u < 16; ++u) dst[u * 8] = t[u];
+  }
   __syncthreads();
 }
 

@@ -30,6 +30,10 @@ namespace fpm {
 namespace {
 
 constexpr int kTileMax = 12;         // 2^12 elements x 16 B = 64 KiB tile
+#ifndef FPM_TILE2_THREADS
+#define FPM_TILE2_THREADS 256
+#endif
+constexpr int kTile2Threads = FPM_TILE2_THREADS;  // fft_tile_fused2_kernel
 
 __device__ __forceinline__ uint4 c2p2(const uint4* __restrict__ c2p, uint64_t b) {  // C2P(2b)
   uint4 r = c2p[b & 511];
@@ -167,10 +171,12 @@ constexpr unsigned kTabLayer = FPM_M8_LAYER;
 constexpr unsigned kM4Layer = FPM_M4_LAYER;
 // Layers [kPrepLayer, kM4Layer): generic multiplies with the twiddle's limbs prepared once per block.
 constexpr unsigned kPrepLayer = 1;
-template <bool INV>
+// NT tiles that share twiddles (operands a and b at the same position) lie at s, s + 2^T, ...:
+// every table or prepared twiddle serves the butterflies of all of them.
+template <bool INV, int NT = 1>
 __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, unsigned l, uint64_t tile_idx,
                                             const TwiddleSrc& tw, uint4* __restrict__ tab) {
-  const int npairs = 1 << (T - 1);
+  const int npairs = 1 << (T - 1), n = 1 << T;
   for (unsigned step = 0; step < T; ++step) {
     const unsigned i = INV ? step : T - 1 - step;
     const uint64_t bhi = tile_idx << (T - 1 - i);  // global block index of the tile's first block
@@ -180,14 +186,16 @@ __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, u
       // 2^(T-1-i) twiddles of 2^i butterflies each: rotated 4-bit tables, up to 8 twiddles per round
       const int q = threadIdx.x & 7;
       const int nblk = npairs >> i, G = nblk < 8 ? nblk : 8;
+      const int gi = i + (G >= 8 ? 3 : G >= 4 ? 2 : G >= 2 ? 1 : 0);  // log2(G << i)
       for (int b0 = 0; b0 < nblk; b0 += G) {
         const uint4 w = x4(Z, c2p2(tw.c2p, (uint64_t)(b0 + (threadIdx.x >> 5))));
         __syncthreads();  // previous round's lookups done
         if (threadIdx.x < 32 * G) m4s_build8(tab, w, threadIdx.x);
         __syncthreads();
-        for (int p = threadIdx.x; p < (G << i); p += blockDim.x) {
+        for (int pp = threadIdx.x; pp < (NT << gi); pp += blockDim.x) {
+          const int p = pp & ((1 << gi) - 1), tt = pp >> gi;
           const int t = p >> i, j = p & ((1 << i) - 1), blk = b0 + t;
-          const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+          const int i0 = (blk << (i + 1)) + j + tt * n, i1 = i0 + (1 << i);
           const uint4* tb = tab + t * kM4TabUint4;
           uint4 u0 = s[i0], u1 = s[i1];
           if (!INV) {
@@ -208,8 +216,9 @@ __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, u
       const int q = threadIdx.x & 7;
       for (int blk = 0; blk < (npairs >> i); ++blk) {
         m8_build(tab, tab + kM8Uint4, x4(Z, c2p2(tw.c2p, (uint64_t)blk)), threadIdx.x);
-        for (int j = threadIdx.x; j < (1 << i); j += blockDim.x) {
-          const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+        for (int jj = threadIdx.x; jj < (NT << i); jj += blockDim.x) {
+          const int j = jj & ((1 << i) - 1), tt = jj >> i;
+          const int i0 = (blk << (i + 1)) + j + tt * n, i1 = i0 + (1 << i);
           uint4 u0 = s[i0], u1 = s[i1];
           if (!INV) {
             u0 = x4(u0, m8_mul(tab, u1, q));
@@ -232,9 +241,10 @@ __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, u
       const int nblk = npairs >> i;
       for (int b = threadIdx.x; b < nblk; b += blockDim.x) prep[b] = gf_prep(x4(Z, c2p2(tw.c2p, (uint64_t)b)));
       __syncthreads();
-      for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+      for (int pp = threadIdx.x; pp < NT * npairs; pp += blockDim.x) {
+        const int p = pp & (npairs - 1), tt = pp >> (T - 1);
         const int blk = p >> i, j = p & ((1 << i) - 1);
-        const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+        const int i0 = (blk << (i + 1)) + j + tt * n, i1 = i0 + (1 << i);
         const GfPrep w = prep[blk];
         uint4 u0 = s[i0], u1 = s[i1];
         if (!INV) {
@@ -250,9 +260,10 @@ __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, u
       __syncthreads();
       continue;
     }
-    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+    for (int pp = threadIdx.x; pp < NT * npairs; pp += blockDim.x) {
+      const int p = pp & (npairs - 1), tt = pp >> (T - 1);
       const int blk = p >> i, j = p & ((1 << i) - 1);
-      const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+      const int i0 = (blk << (i + 1)) + j + tt * n, i1 = i0 + (1 << i);
       const uint4 w = x4(Z, c2p2(tw.c2p, (uint64_t)blk));
       uint4 u0 = s[i0], u1 = s[i1];
       if (!INV) {
@@ -306,6 +317,34 @@ __global__ void __launch_bounds__(256) fft_tile_fused_kernel(const uint4* __rest
   }
 }
 
+// Both operands' tile layers in one CTA: the a and b tiles at the same position share every
+// twiddle, so each M8/M4 table and prepared twiddle is built once for two butterflies; then the
+// pointwise product and the inverse tile layers, as fft_tile_fused_kernel.  Saves operand a's
+// separate tile pass (one HBM round trip of EvalVec a).
+__global__ void __launch_bounds__(kTile2Threads, 512 / kTile2Threads) fft_tile_fused2_kernel(const uint4* __restrict__ ea,
+                                                                          uint4* __restrict__ eb, unsigned l,
+                                                                          unsigned T, TwiddleSrc tw) {
+  extern __shared__ uint4 s[];
+  const int n = 1 << T;
+  uint4* tab = s + 2 * n;
+  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint4* g = eb + (t << T);
+    const uint4* ga = ea + (t << T);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      s[k] = ga[k];
+      s[n + k] = g[k];
+    }
+    __syncthreads();
+    tile_layers<false, 2>(s, T, l, t, tw, tab);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) s[k] = gf_mul(s[k], s[n + k]);
+    __syncthreads();
+    tile_layers<true, 1>(s, T, l, t, tw, tab);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) g[k] = s[k];
+    __syncthreads();
+  }
+}
+
 // Exchanged layer of the sharded FFT: all local elements share one twiddle w.
 template <bool INV>
 __global__ void __launch_bounds__(256) fft_pair_kernel(uint4* __restrict__ mine, const uint4* __restrict__ theirs,
@@ -353,13 +392,28 @@ void set_smem(K kernel, size_t bytes) {
 // >= kTabLayer), layers >= T in radix-4 M8-table passes.  B200 sweeps (ms, T = 10 / 11):
 // 2^26-bit 1.269 / 1.262, 2^28 4.375 / 4.320, 2^30 17.14 / 16.93, 2^32 73.0 / 71.8; 2^24 0.457 /
 // 0.470; below 2^18 elements T = 8 keeps >= 2^10 tiles in flight.
-unsigned fft_tile_log2(unsigned l) {
+bool tile_fused2_enabled(unsigned T);
+
+int tile_log2_knob() {
   static const int knob = [] {
     const char* e = std::getenv("FPM_TILE_LOG2");  // tuning override (8..12)
     return e ? std::max(8, std::min(kTileMax, std::atoi(e))) : 0;
   }();
+  return knob;
+}
+
+unsigned fft_tile_log2(unsigned l) {
+  const int knob = tile_log2_knob();
   const unsigned cap = knob ? (unsigned)knob : (l >= 20 ? 11u : l >= 18 ? 10u : 8u);
   return l < cap ? l : cap;
+}
+
+// The product pipeline's tile depth: with both operands' tile layers fused (fft_tile_fused2_kernel,
+// two 2^T tiles + tables per CTA) T = 10 keeps two CTAs per SM (2^32-bit product: 57.5 ms, vs
+// 57.7 unfused at T = 11 and 60.1 fused at T = 11 with one CTA per SM).
+unsigned pipeline_tile_log2(unsigned l) {
+  if (!tile_log2_knob() && l >= 20 && tile_fused2_enabled(10)) return 10;
+  return fft_tile_log2(l);
 }
 
 TwiddleSrc make_twiddle_src(int device, unsigned l, U128 base) {
@@ -469,6 +523,26 @@ void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigne
   const TileCfg c = tile_cfg(l, T);
   const int grid = resident_grid(fft_tile_fused_kernel, c.threads, c.smem, ((uint64_t)1 << l) >> T);
   fft_tile_fused_kernel<<<grid, c.threads, c.smem, s>>>(ea, eb, l, T, tw, c.use_tab);
+  FPM_LAUNCH_CHECK();
+}
+
+// Both operands' tile layers + pointwise + inverse tile layers in one pass (fft_tile_fused2_kernel);
+// T >= 10 (tables), FPM_FUSE_AB=0 disables it.
+bool tile_fused2_enabled(unsigned T) {
+  static const bool on = [] {
+    const char* e = std::getenv("FPM_FUSE_AB");
+    return !(e && e[0] == '0');
+  }();
+  return on && T >= 10 && T <= 11;
+}
+
+void butterfly_tile_fused2_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
+                                  cudaStream_t s) {
+  const size_t smem = (2 * ((size_t)1 << T) + kM8Uint4 + 144) * sizeof(uint4);
+  static PerDeviceOnce attr;
+  attr.run([&] { set_smem(fft_tile_fused2_kernel, (2 * ((size_t)1 << 11) + kM8Uint4 + 144) * sizeof(uint4)); });
+  const int grid = resident_grid(fft_tile_fused2_kernel, kTile2Threads, smem, ((uint64_t)1 << l) >> T);
+  fft_tile_fused2_kernel<<<grid, kTile2Threads, smem, s>>>(ea, eb, l, T, tw);
   FPM_LAUNCH_CHECK();
 }
 

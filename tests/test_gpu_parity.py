@@ -89,6 +89,35 @@ def test_butterfly_tile_depths(tile):
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("env", [{}, {"FPM_FUSE_AB": "0"}, {"FPM_TILE_LOG2": "11"},
+                                 {"FPM_TILE_LOG2": "10", "FPM_FUSE_AB": "0"}, {"FPM_TILE_LOG2": "12"}])
+def test_pipeline_schedules(checker, port, env):
+    """Every tile schedule of the product pipeline -- both operands' tile layers fused into the
+    pointwise pass (default), operand a in its own tile pass, other depths -- gives the reference
+    product (child process per environment; l = 18 and 20)."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+    shapes = [(1 << 24, (1 << 24) - 3), ((1 << 26) - 5, 1 << 25)]
+    code = (
+        "import hashlib, oracle, paper_1803_11301_b200 as g\n"
+        "P = oracle.port()\n"
+        f"for la, lb in {shapes!r}:\n"
+        "    a, b = P.random_bitpoly(la, 11 + la), P.random_bitpoly(lb, 13 + lb)\n"
+        "    c = g.fp_polymul(a, la, b, lb, field=g.FIELD_GF128)\n"
+        "    print(hashlib.blake2b(c.tobytes(), digest_size=16).hexdigest())\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, **env))
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = r.stdout.split()
+    for (la, lb), h in zip(shapes, got):
+        a, b = port.random_bitpoly(la, 11 + la), port.random_bitpoly(lb, 13 + lb)
+        want = hashlib.blake2b(checker.polymul(a, la, b, lb).tobytes(), digest_size=16).hexdigest()
+        assert h == want, (env, la, lb)
+
+
 SHAPES = [(1, 1), (1, 5), (63, 64), (64, 64), (100, 3000), (4095, 4096), (5000, 3000), (1 << 12, 1 << 12),
           (1 << 14, (1 << 14) - 17), (1 << 16, 1 << 16), ((1 << 16) + 1, 9), ((1 << 17) - 3, (1 << 16) + 5),
           (1 << 18, 1 << 18), (300000, 1 << 19), (1 << 20, 1 << 20), ((1 << 20) + 77, 12345)]
