@@ -34,6 +34,15 @@ constexpr int kTileMax = 12;         // 2^12 elements x 16 B = 64 KiB tile
 #define FPM_TILE2_THREADS 256
 #endif
 constexpr int kTile2Threads = FPM_TILE2_THREADS;  // fft_tile_fused2_kernel
+// M8 tables from this layer on in fft_tile_fused2_kernel (a table then serves both operands'
+// butterflies in the forward layers): 57.27 ms at 2^32 bits vs 57.48 from layer 9.
+#ifndef FPM_M8_LAYER2
+#define FPM_M8_LAYER2 8
+#endif
+#ifndef FPM_M8_LAYER2_INV
+#define FPM_M8_LAYER2_INV 8
+#endif
+constexpr unsigned kTabLayer2 = FPM_M8_LAYER2, kTabLayer2Inv = FPM_M8_LAYER2_INV;
 
 __device__ __forceinline__ uint4 c2p2(const uint4* __restrict__ c2p, uint64_t b) {  // C2P(2b)
   uint4 r = c2p[b & 511];
@@ -173,7 +182,7 @@ constexpr unsigned kM4Layer = FPM_M4_LAYER;
 constexpr unsigned kPrepLayer = 1;
 // NT tiles that share twiddles (operands a and b at the same position) lie at s, s + 2^T, ...:
 // every table or prepared twiddle serves the butterflies of all of them.
-template <bool INV, int NT = 1>
+template <bool INV, int NT = 1, unsigned kTabLayer = kTabLayer>
 __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, unsigned l, uint64_t tile_idx,
                                             const TwiddleSrc& tw, uint4* __restrict__ tab) {
   const int npairs = 1 << (T - 1), n = 1 << T;
@@ -336,10 +345,10 @@ __global__ void __launch_bounds__(kTile2Threads, 512 / kTile2Threads) fft_tile_f
       s[n + k] = g[k];
     }
     __syncthreads();
-    tile_layers<false, 2>(s, T, l, t, tw, tab);
+    tile_layers<false, 2, kTabLayer2>(s, T, l, t, tw, tab);
     for (int k = threadIdx.x; k < n; k += blockDim.x) s[k] = gf_mul(s[k], s[n + k]);
     __syncthreads();
-    tile_layers<true, 1>(s, T, l, t, tw, tab);
+    tile_layers<true, 1, kTabLayer2Inv>(s, T, l, t, tw, tab);
     for (int k = threadIdx.x; k < n; k += blockDim.x) g[k] = s[k];
     __syncthreads();
   }
