@@ -198,7 +198,7 @@ struct Gf64Ops {
   using Tw = TwiddleSrc64;
   static constexpr int kLiveRows = 32;
   static Tw twiddles(int dev, unsigned l) { return make_twiddle_src64(dev, l, partition_base64(l)); }
-  static unsigned tile_log2(unsigned l) { return fft64_tile_log2(l); }
+  static unsigned tile_log2(unsigned l) { return pipeline64_tile_log2(l); }
   static void encode(const uint32_t* p, unsigned l, E* ev, cudaStream_t s) { encode64_device(p, l, ev, kLiveRows, s); }
   static void decode(const E* ev, unsigned l, uint32_t* p, cudaStream_t s) { decode64_device(ev, l, p, s); }
   static void top(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s) {
@@ -210,8 +210,10 @@ struct Gf64Ops {
   static void fused(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s) {
     butterfly64_tile_fused_device(ea, eb, l, T, tw, s);
   }
-  static bool fuse_ab(unsigned) { return false; }
-  static void fused2(const E*, E*, unsigned, unsigned, const Tw&, cudaStream_t) {}
+  static bool fuse_ab(unsigned T) { return tile64_fused2_enabled(T); }
+  static void fused2(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s) {
+    butterfly64_tile_fused2_device(ea, eb, l, T, tw, s);
+  }
 };
 
 // fp_polymul on device buffers.  field: FPM_FIELD_GF128, FPM_FIELD_GF64, or FPM_FIELD_AUTO (the

@@ -140,6 +140,10 @@ void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const
 void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s);
 // Fused: forward layers [0, T) of b's tiles, pointwise * a, inverse layers [0, T).
 bool tile_fused2_enabled(unsigned T);
+bool tile64_fused2_enabled(unsigned T);
+unsigned pipeline64_tile_log2(unsigned l);
+void butterfly64_tile_fused2_device(const uint2* ea, uint2* eb, unsigned l, unsigned T, const TwiddleSrc64& tw,
+                                    cudaStream_t s);
 unsigned pipeline_tile_log2(unsigned l);
 void butterfly_tile_fused2_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
                                   cudaStream_t s);

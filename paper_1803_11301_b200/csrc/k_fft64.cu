@@ -163,10 +163,15 @@ constexpr unsigned kTabLayer64 = FPM_G8_LAYER;  // layers >= 9: G8 tables (layer
 #define FPM_G4_LAYER 6
 #endif
 constexpr unsigned kG4Layer = FPM_G4_LAYER;
-template <bool INV>
+#ifndef FPM_G8_LAYER2
+#define FPM_G8_LAYER2 8
+#endif
+constexpr unsigned kTabLayer64_2 = FPM_G8_LAYER2;  // fft64_tile_fused2_kernel
+// NT tiles sharing twiddles (both operands at one position) at s, s + 2^T (cf. k_fft.cu).
+template <bool INV, int NT = 1, unsigned kTabLayer64 = kTabLayer64>
 __device__ __forceinline__ void tile_layers64(uint2* __restrict__ s, unsigned T, uint64_t tile_idx,
                                               const TwiddleSrc64& tw, uint2* __restrict__ tab) {
-  const int npairs = 1 << (T - 1);
+  const int npairs = 1 << (T - 1), n = 1 << T;
   const int lane = threadIdx.x & 31;
   for (unsigned step = 0; step < T; ++step) {
     const unsigned i = INV ? step : T - 1 - step;
@@ -174,14 +179,16 @@ __device__ __forceinline__ void tile_layers64(uint2* __restrict__ s, unsigned T,
     const uint2 Z = twiddle64(tw, i, bhi);  // w = Z ^ C2P(2 blk) (disjoint bit ranges, C2P linear)
     if (tab && i >= kG4Layer && i < kTabLayer64) {
       const int nblk = npairs >> i, G = nblk < 16 ? nblk : 16;
+      const int gi = i + (G >= 16 ? 4 : G >= 8 ? 3 : G >= 4 ? 2 : G >= 2 ? 1 : 0);  // log2(G << i)
       for (int b0 = 0; b0 < nblk; b0 += G) {
         const uint2 w = x2(Z, c2p2_64(tw.c2p, (uint64_t)(b0 + (threadIdx.x >> 4))));
         __syncthreads();  // previous round's lookups done
         if (threadIdx.x < 16 * G) g4_build16(tab, w, threadIdx.x);
         __syncthreads();
-        for (int p = threadIdx.x; p < (G << i); p += blockDim.x) {
+        for (int pp = threadIdx.x; pp < (NT << gi); pp += blockDim.x) {
+          const int p = NT == 1 ? pp : pp & ((1 << gi) - 1), tt = NT == 1 ? 0 : pp >> gi;
           const int t = p >> i, j = p & ((1 << i) - 1), blk = b0 + t;
-          const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+          const int i0 = (blk << (i + 1)) + j + tt * n, i1 = i0 + (1 << i);
           const uint2* tb = tab + t * kG4TabUint2;
           uint2 u0 = s[i0], u1 = s[i1];
           if (!INV) {
@@ -201,8 +208,9 @@ __device__ __forceinline__ void tile_layers64(uint2* __restrict__ s, unsigned T,
     if (tab && i >= kTabLayer64) {
       for (int blk = 0; blk < (npairs >> i); ++blk) {
         g8_build(tab, tab + kG8Uint2, x2(Z, c2p2_64(tw.c2p, (uint64_t)blk)), threadIdx.x);
-        for (int j = threadIdx.x; j < (1 << i); j += blockDim.x) {
-          const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+        for (int jj = threadIdx.x; jj < (NT << i); jj += blockDim.x) {
+          const int j = NT == 1 ? jj : jj & ((1 << i) - 1), tt = NT == 1 ? 0 : jj >> i;
+          const int i0 = (blk << (i + 1)) + j + tt * n, i1 = i0 + (1 << i);
           uint2 u0 = s[i0], u1 = s[i1];
           if (!INV) {
             u0 = x2(u0, g8_mul(tab, u1, lane));
@@ -224,9 +232,10 @@ __device__ __forceinline__ void tile_layers64(uint2* __restrict__ s, unsigned T,
       const int nblk = npairs >> i;
       for (int b = threadIdx.x; b < nblk; b += blockDim.x) prep[b] = gf64_prep(x2(Z, c2p2_64(tw.c2p, (uint64_t)b)));
       __syncthreads();
-      for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+      for (int pp = threadIdx.x; pp < NT * npairs; pp += blockDim.x) {
+        const int p = NT == 1 ? pp : pp & (npairs - 1), tt = NT == 1 ? 0 : pp >> (T - 1);
         const int blk = p >> i, j = p & ((1 << i) - 1);
-        const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+        const int i0 = (blk << (i + 1)) + j + tt * n, i1 = i0 + (1 << i);
         const Gf64Prep w = prep[blk];
         uint2 u0 = s[i0], u1 = s[i1];
         if (!INV) {
@@ -242,9 +251,10 @@ __device__ __forceinline__ void tile_layers64(uint2* __restrict__ s, unsigned T,
       __syncthreads();
       continue;
     }
-    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+    for (int pp = threadIdx.x; pp < NT * npairs; pp += blockDim.x) {
+      const int p = NT == 1 ? pp : pp & (npairs - 1), tt = NT == 1 ? 0 : pp >> (T - 1);
       const int blk = p >> i, j = p & ((1 << i) - 1);
-      const int i0 = (blk << (i + 1)) + j, i1 = i0 + (1 << i);
+      const int i0 = (blk << (i + 1)) + j + tt * n, i1 = i0 + (1 << i);
       const uint2 w = x2(Z, c2p2_64(tw.c2p, (uint64_t)blk));
       uint2 u0 = s[i0], u1 = s[i1];
       if (!INV) {
@@ -298,6 +308,32 @@ __global__ void __launch_bounds__(256, 3) fft64_tile_fused_kernel(const uint2* _
   }
 }
 
+// Both operands' tile layers in one CTA (shared tables / prepared twiddles), the pointwise product
+// and the inverse tile layers (cf. k_fft.cu fft_tile_fused2_kernel).
+__global__ void __launch_bounds__(256, 3) fft64_tile_fused2_kernel(const uint2* __restrict__ ea,
+                                                                   uint2* __restrict__ eb, unsigned l, unsigned T,
+                                                                   TwiddleSrc64 tw) {
+  extern __shared__ uint2 s64[];
+  const int n = 1 << T;
+  uint2* tab = s64 + 2 * n;
+  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint2* g = eb + (t << T);
+    const uint2* ga = ea + (t << T);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      s64[k] = ga[k];
+      s64[n + k] = g[k];
+    }
+    __syncthreads();
+    tile_layers64<false, 2, kTabLayer64_2>(s64, T, t, tw, tab);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) s64[k] = gf64_mul(s64[k], s64[n + k]);
+    __syncthreads();
+    tile_layers64<true, 1, kTabLayer64_2>(s64, T, t, tw, tab);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) g[k] = s64[k];
+    __syncthreads();
+  }
+}
+
 __global__ void pointwise64_kernel(const uint2* __restrict__ u, const uint2* __restrict__ v, uint2* __restrict__ out,
                                    uint64_t n) {
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
@@ -334,13 +370,45 @@ constexpr size_t kTileSmemMax64 = ((size_t)1 << kTileMax64) * sizeof(uint2) + (k
 }  // namespace
 
 // Tile depth for the GF(2^64) transforms (tuning override FPM_TILE_LOG2_64).
-unsigned fft64_tile_log2(unsigned l) {
+int tile_log2_knob64() {
   static const int knob = [] {
     const char* e = std::getenv("FPM_TILE_LOG2_64");
     return e ? std::max(8, std::min(kTileMax64, std::atoi(e))) : 0;
   }();
+  return knob;
+}
+
+unsigned fft64_tile_log2(unsigned l) {
+  const int knob = tile_log2_knob64();
   const unsigned cap = knob ? (unsigned)knob : (l >= 20 ? 12u : l >= 18 ? 10u : 8u);
   return l < cap ? l : cap;
+}
+
+// Both operands' tile layers in the fused pass (FPM_FUSE_AB=0 disables it).
+bool tile64_fused2_enabled(unsigned T) {
+  static const bool on = [] {
+    const char* e = std::getenv("FPM_FUSE_AB");
+    return !(e && e[0] == '0');
+  }();
+  return on && T >= 10 && T <= 12;
+}
+
+#ifndef FPM_TILE2_LOG2_64
+#define FPM_TILE2_LOG2_64 11
+#endif
+unsigned pipeline64_tile_log2(unsigned l) {
+  if (!tile_log2_knob64() && l >= 20 && tile64_fused2_enabled(FPM_TILE2_LOG2_64)) return FPM_TILE2_LOG2_64;
+  return fft64_tile_log2(l);
+}
+
+void butterfly64_tile_fused2_device(const uint2* ea, uint2* eb, unsigned l, unsigned T, const TwiddleSrc64& tw,
+                                    cudaStream_t s) {
+  const size_t smem = (2 * ((size_t)1 << T) + kG8Uint2 + kG8Rows) * sizeof(uint2);
+  static PerDeviceOnce attr;
+  attr.run([&] { set_smem64(fft64_tile_fused2_kernel, (2 * ((size_t)1 << 12) + kG8Uint2 + kG8Rows) * sizeof(uint2)); });
+  const int grid = resident_grid(fft64_tile_fused2_kernel, 256, smem, ((uint64_t)1 << l) >> T);
+  fft64_tile_fused2_kernel<<<grid, 256, smem, s>>>(ea, eb, l, T, tw);
+  FPM_LAUNCH_CHECK();
 }
 
 TwiddleSrc64 make_twiddle_src64(int device, unsigned l, uint64_t base) {

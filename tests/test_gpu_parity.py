@@ -89,9 +89,11 @@ def test_butterfly_tile_depths(tile):
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("env", [{}, {"FPM_FUSE_AB": "0"}, {"FPM_TILE_LOG2": "11"},
-                                 {"FPM_TILE_LOG2": "10", "FPM_FUSE_AB": "0"}, {"FPM_TILE_LOG2": "12"}])
-def test_pipeline_schedules(checker, port, env):
+@pytest.mark.parametrize("env", [{}, {"FPM_FUSE_AB": "0"}, {"FPM_TILE_LOG2": "11", "FPM_TILE_LOG2_64": "12"},
+                                 {"FPM_TILE_LOG2": "10", "FPM_TILE_LOG2_64": "10", "FPM_FUSE_AB": "0"},
+                                 {"FPM_TILE_LOG2": "12", "FPM_TILE_LOG2_64": "11"}])
+@pytest.mark.parametrize("field", [128, 64])
+def test_pipeline_schedules(checker, port, env, field):
     """Every tile schedule of the product pipeline -- both operands' tile layers fused into the
     pointwise pass (default), operand a in its own tile pass, other depths -- gives the reference
     product (child process per environment; l = 18 and 20)."""
@@ -105,7 +107,7 @@ def test_pipeline_schedules(checker, port, env):
         "P = oracle.port()\n"
         f"for la, lb in {shapes!r}:\n"
         "    a, b = P.random_bitpoly(la, 11 + la), P.random_bitpoly(lb, 13 + lb)\n"
-        "    c = g.fp_polymul(a, la, b, lb, field=g.FIELD_GF128)\n"
+        f"    c = g.fp_polymul(a, la, b, lb, field={field})\n"
         "    print(hashlib.blake2b(c.tobytes(), digest_size=16).hexdigest())\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=900,
