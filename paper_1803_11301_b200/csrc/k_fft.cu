@@ -16,6 +16,9 @@
 //    layers (twiddles vary per block) via the generic IMAD-hole gf_mul.
 //  * fft_tile_fused_kernel: forward layers [0,T) of operand b, the pointwise product with operand
 //    a (subsystem 3, kernels_impl.hpp:116-123), and inverse layers [0,T) in one tile pass.
+//  * fft_tile_fused2_kernel (the product pipeline): forward layers [0,T) of BOTH operands (their
+//    tiles share every twiddle, so each table serves both), the pointwise product and the inverse
+//    layers [0,T) in one pass -- no separate tile pass for operand a.
 #include <cuda_runtime.h>
 
 #include <algorithm>
