@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfpmul_b200.so")
+LIB_PATH = os.environ.get("FPM_LIB") or os.path.join(HERE, "libfpmul_b200.so")  # FPM_LIB: experiment builds
 
 FIELD_AUTO, FIELD_GF64, FIELD_GF128 = 0, 64, 128
 NUM_STAGES = 7

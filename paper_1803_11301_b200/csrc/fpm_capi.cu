@@ -176,10 +176,15 @@ struct Gf128Ops {
   static constexpr int kLiveRows = 64;  // rows >= m/2 of a padded operand are zero
   static Tw twiddles(int dev, unsigned l) { return make_twiddle_src(dev, l, partition_base(l)); }
   static unsigned tile_log2(unsigned l) { return pipeline_tile_log2(l); }
-  static void encode(const uint32_t* p, unsigned l, E* ev, cudaStream_t s) { encode_device_rows(p, l, ev, kLiveRows, s); }
-  static void decode(const E* ev, unsigned l, uint32_t* p, cudaStream_t s) { decode_device(ev, l, p, s); }
-  static void top(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s) {
-    butterfly_top_device(ev, l, T, inv, tw, s);
+  // The fused pass on tower-representation tiles (tower.cuh); then encode, the top passes and
+  // decode work in R as well.
+  static bool tower(unsigned T) { return tile_fused2_enabled(T) && tile_tower_enabled(T); }
+  static void encode(const uint32_t* p, unsigned l, E* ev, cudaStream_t s, bool r) {
+    encode_device_rows(p, l, ev, kLiveRows, s, r);
+  }
+  static void decode(const E* ev, unsigned l, uint32_t* p, cudaStream_t s, bool r) { decode_device(ev, l, p, s, r); }
+  static void top(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s, bool r) {
+    butterfly_top_device(ev, l, T, inv, tw, s, r);
   }
   static void tile(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s) {
     butterfly_tile_device(ev, l, T, inv, tw, s);
@@ -189,8 +194,9 @@ struct Gf128Ops {
   }
   // both operands' tile layers in the fused pass (no separate tile pass of operand a)
   static bool fuse_ab(unsigned T) { return tile_fused2_enabled(T); }
-  static void fused2(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s) {
-    butterfly_tile_fused2_device(ea, eb, l, T, tw, s);
+  static void fused2(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s, bool r) {
+    if (r) butterfly_tile_tower_device(ea, eb, l, T, tw, s);
+    else butterfly_tile_fused2_device(ea, eb, l, T, tw, s);
   }
 };
 struct Gf64Ops {
@@ -199,9 +205,10 @@ struct Gf64Ops {
   static constexpr int kLiveRows = 32;
   static Tw twiddles(int dev, unsigned l) { return make_twiddle_src64(dev, l, partition_base64(l)); }
   static unsigned tile_log2(unsigned l) { return pipeline64_tile_log2(l); }
-  static void encode(const uint32_t* p, unsigned l, E* ev, cudaStream_t s) { encode64_device(p, l, ev, kLiveRows, s); }
-  static void decode(const E* ev, unsigned l, uint32_t* p, cudaStream_t s) { decode64_device(ev, l, p, s); }
-  static void top(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s) {
+  static bool tower(unsigned) { return false; }
+  static void encode(const uint32_t* p, unsigned l, E* ev, cudaStream_t s, bool) { encode64_device(p, l, ev, kLiveRows, s); }
+  static void decode(const E* ev, unsigned l, uint32_t* p, cudaStream_t s, bool) { decode64_device(ev, l, p, s); }
+  static void top(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s, bool) {
     butterfly64_top_device(ev, l, T, inv, tw, s);
   }
   static void tile(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s) {
@@ -211,7 +218,7 @@ struct Gf64Ops {
     butterfly64_tile_fused_device(ea, eb, l, T, tw, s);
   }
   static bool fuse_ab(unsigned T) { return tile64_fused2_enabled(T); }
-  static void fused2(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s) {
+  static void fused2(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s, bool) {
     butterfly64_tile_fused2_device(ea, eb, l, T, tw, s);
   }
 };
@@ -249,6 +256,7 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
   }
   const unsigned l = p.l, T = F::tile_log2(l);
   const bool fuse_ab = T > 0 && F::fuse_ab(T);
+  const bool rep = fuse_ab && F::tower(T);  // EvalVecs in the tower representation
   int dev;
   FPM_CUDA(cudaGetDevice(&dev));
   const typename F::Tw tw = F::twiddles(dev, l);
@@ -277,18 +285,18 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
       basis_cvt_device(work32, count, xbits[k], false, s);
     }
     clk.mark(kStEncode);
-    F::encode(work32, l, es[k], s);
+    F::encode(work32, l, es[k], s, rep);
     clk.mark(kStBfly);
-    F::top(es[k], l, T, false, tw, s);
+    F::top(es[k], l, T, false, tw, s, rep);
     if (k == 0 && !fuse_ab) F::tile(es[k], l, T, false, tw, s);
   }
   clk.mark(kStPointwise);  // + operand b's (and a's) bottom T forward and the bottom T inverse layers (fused)
-  if (fuse_ab) F::fused2(EA.as<E>(), EB.as<E>(), l, T, tw, s);
+  if (fuse_ab) F::fused2(EA.as<E>(), EB.as<E>(), l, T, tw, s, rep);
   else F::fused(EA.as<E>(), EB.as<E>(), l, T, tw, s);
   clk.mark(kStIBfly);
-  F::top(EB.as<E>(), l, T, true, tw, s);
+  F::top(EB.as<E>(), l, T, true, tw, s, rep);
   clk.mark(kStDecode);
-  F::decode(EB.as<E>(), l, work32, s);
+  F::decode(EB.as<E>(), l, work32, s, rep);
   clk.mark(kStIBasis);
   // Each finished range of the product is trimmed into d_c (and copied out) right away.
   const FinalFn on_final = [&](uint64_t w0, uint64_t w1) {  // 32-bit word range of P
@@ -399,18 +407,37 @@ const DeviceTables& device_tables(int dev) {
   std::vector<uint4> cantor(128), rows(128), inv(128), c2p(4 * 512);
   for (int i = 0; i < 128; ++i) { cantor[i] = to4(ft.cantor[i]); rows[i] = to4(ft.enc_rows[i]); inv[i] = to4(ft.inv_rows[i]); }
   // rotated 8-bit tables (gf128.cuh m8 layout): entry (c, v) at (c >> 3) * 2048 + v * 8 + (c & 7)
-  std::vector<uint4> enc8(kM8Uint4), dec8(kM8Uint4);
-  for (int c = 0; c < 16; ++c)
-    for (int v = 0; v < 256; ++v) {
-      U128 e, d;
-      for (int j = 0; j < 8; ++j)
-        if (v >> j & 1) {
-          e.lo ^= ft.enc_rows[8 * c + j].lo; e.hi ^= ft.enc_rows[8 * c + j].hi;
-          d.lo ^= ft.inv_rows[8 * c + j].lo; d.hi ^= ft.inv_rows[8 * c + j].hi;
-        }
-      enc8[(c >> 3) * 2048 + v * 8 + (c & 7)] = to4(e);
-      dec8[(c >> 3) * 2048 + v * 8 + (c & 7)] = to4(d);
-    }
+  // tower representation (fpm_tables.h): encode writes R(x*E); decode reads R, i.e. its row k is
+  // the decode of e_k = poly(R basis vector k)
+  const TowerTables& tt = tower_tables();
+  std::vector<uint4> to_r(128), to_poly(128);
+  U128 enc_rows_r[128], inv_rows_r[128];
+  for (int k = 0; k < 128; ++k) {
+    to_r[k] = to4(tt.to_r[k]);
+    to_poly[k] = to4(tt.to_poly[k]);
+    enc_rows_r[k] = host_to_r(ft.enc_rows[k]);
+    U128 d;
+    for (int m = 0; m < 128; ++m)
+      if ((m < 64 ? tt.to_poly[k].lo >> m : tt.to_poly[k].hi >> (m - 64)) & 1) {
+        d.lo ^= ft.inv_rows[m].lo;
+        d.hi ^= ft.inv_rows[m].hi;
+      }
+    inv_rows_r[k] = d;
+  }
+  std::vector<uint4> enc8(kM8Uint4), dec8(kM8Uint4), enc8r(kM8Uint4), dec8r(kM8Uint4);
+  auto m8_entries = [](std::vector<uint4>& tab, const U128* rows) {
+    for (int c = 0; c < 16; ++c)
+      for (int v = 0; v < 256; ++v) {
+        U128 e;
+        for (int j = 0; j < 8; ++j)
+          if (v >> j & 1) { e.lo ^= rows[8 * c + j].lo; e.hi ^= rows[8 * c + j].hi; }
+        tab[(c >> 3) * 2048 + v * 8 + (c & 7)] = to4(e);
+      }
+  };
+  m8_entries(enc8, ft.enc_rows);
+  m8_entries(dec8, ft.inv_rows);
+  m8_entries(enc8r, enc_rows_r);
+  m8_entries(dec8r, inv_rows_r);
   for (int part = 0; part < 4; ++part)
     for (int e = 0; e < 512; ++e) {
       U128 acc;
@@ -458,6 +485,7 @@ const DeviceTables& device_tables(int dev) {
   up(&t.cantor, cantor); up(&t.enc_rows, rows); up(&t.inv_rows, inv);
   up(&t.c2p, c2p);
   up(&t.enc_m8, enc8); up(&t.dec_m8, dec8);
+  up(&t.to_r, to_r); up(&t.to_poly, to_poly); up(&t.enc_m8r, enc8r); up(&t.dec_m8r, dec8r);
   auto up2 = [](uint2** dst, const std::vector<uint2>& v) {
     FPM_CUDA(cudaMalloc(dst, v.size() * sizeof(uint2)));
     FPM_CUDA(cudaMemcpy(*dst, v.data(), v.size() * sizeof(uint2), cudaMemcpyHostToDevice));

@@ -75,6 +75,11 @@ struct DeviceTables {
   uint4* enc_m8 = nullptr;    // rotated 8-bit tables (gf128.cuh m8 layout) of x*E
   uint4* dec_m8 = nullptr;    // ... of x*E^{-1}
   uint4* c2p = nullptr;       // 4 x 512: part p entry e = C2P(2 * (e << 9p))
+  // Tower representation R (fpm_tables.h TowerTables), used inside the product pipeline's FFT:
+  uint4* to_r = nullptr;      // 128 x R(x^k): rows of the poly -> R map
+  uint4* to_poly = nullptr;   // 128 x e_k in poly: rows of the R -> poly map
+  uint4* enc_m8r = nullptr;   // M8 tables of x -> R(x*E)
+  uint4* dec_m8r = nullptr;   // M8 tables of x_R -> poly(x)*E^{-1}
   // GF(2^64) (run_pipeline<gf64>): G8 tables (gf64.cuh layout) of x*E and x*E^{-1}, C2P tables
   uint2* enc_g8 = nullptr;
   uint2* dec_g8 = nullptr;
@@ -89,6 +94,9 @@ struct DeviceTables {
 constexpr int kMaxLayers = 64;
 struct TwiddleSrc {
   const uint4* c2p;          // device: 4 x 512 C2P(2 * (e << 9p)) tables
+  const uint4* to_r;         // device: DeviceTables::to_r (tower-representation table rows)
+  const uint4* to_poly;      // device: DeviceTables::to_poly
+  uint64_t tau;              // TowerTables::tau, byte b = R(v_{b+1}) (subfield twiddle parts)
   uint4 layer[kMaxLayers];   // C2P(base >> i)
 };
 // Host: twiddle source for plan_butterflies(l, base) (base in Cantor coordinates).
@@ -121,22 +129,25 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
 // Encode / decode (k_codec.cu).  poly has 128 * 2^l bits; ev has 2^l uint4.
 void encode_device(const uint32_t* poly, unsigned l, uint4* ev, cudaStream_t s);
 // rows_live = 64: rows >= 64 of poly are known zero (pipeline operands) and not read.
-void encode_device_rows(const uint32_t* poly, unsigned l, uint4* ev, int rows_live, cudaStream_t s);
+// tower: write the elements in the tower representation R (product pipeline; n_p >= 1024).
+void encode_device_rows(const uint32_t* poly, unsigned l, uint4* ev, int rows_live, cudaStream_t s, bool tower = false);
 // Column (element) range of the partition matrix; used by the sharded multi-GPU product.
 void encode_cols_device(const uint32_t* poly, unsigned l, uint64_t col0, uint64_t ncols, uint4* ev, int rows_live,
-                        cudaStream_t s);
-void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaStream_t s);
+                        cudaStream_t s, bool tower = false);
+void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaStream_t s, bool tower = false);
 // One exchanged butterfly layer (sharded FFT): this rank holds `mine` (side 0 = p0 half, 1 = p1 half),
 // the partner's half arrived in `theirs`; uniform twiddle w.  Result replaces `mine`.
 void bfly_pair_device(uint4* mine, const uint4* theirs, uint64_t n, U128 w, int side, bool inverse, cudaStream_t s);
-void decode_device(const uint4* ev, unsigned l, uint32_t* poly, cudaStream_t s);
+void decode_device(const uint4* ev, unsigned l, uint32_t* poly, cudaStream_t s, bool tower = false);
 
 // Butterflies (k_fft.cu).
 void butterfly_device(uint4* ev, unsigned l, U128 base, bool inverse, cudaStream_t s);
 void pointwise_device(const uint4* u, const uint4* v, uint4* out, size_t n, cudaStream_t s);
 // Pipeline helpers exposing the split between top (radix-4 table passes) and bottom (tile) layers.
 unsigned fft_tile_log2(unsigned l);
-void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s);
+// tower: the elements are in the tower representation R (tables built in R).
+void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s,
+                          bool tower = false);
 void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s);
 // Fused: forward layers [0, T) of b's tiles, pointwise * a, inverse layers [0, T).
 bool tile_fused2_enabled(unsigned T);
@@ -147,6 +158,11 @@ void butterfly64_tile_fused2_device(const uint2* ea, uint2* eb, unsigned l, unsi
 unsigned pipeline_tile_log2(unsigned l);
 void butterfly_tile_fused2_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
                                   cudaStream_t s);
+// The same pass on tower-representation tiles (fft_tile_tower_kernel): every tile layer as one M8
+// table of the tile's twiddle plus a GF(2^8)-scalar product for the per-block part; T in [10, 11].
+bool tile_tower_enabled(unsigned T);
+void butterfly_tile_tower_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
+                                 cudaStream_t s);
 void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
                                  cudaStream_t s);
 

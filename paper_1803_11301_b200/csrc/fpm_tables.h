@@ -25,6 +25,22 @@ const FieldTables& field_tables();
 // GF(2^64) (CantorField<gf64>, EncodeMatrix<gf64>): entries 0..63 used, hi words zero.
 const FieldTables& field_tables64();
 
+// Internal "tower" representation R of GF(2^128) for the product pipeline's FFT (not visible at any
+// API boundary): GF(2^128) as a 16-dimensional vector space over its subfield GF(2^8) =
+// span(v_0..v_7) (Cantor basis), basis e_{8j+s} = x^j t^s where t is a root of
+// y^8 + y^4 + y^3 + y + 1 in GF(2^128).  Byte j of an R element holds the GF(2^8) coordinate of x^j in
+// the basis 1, t, ..., t^7, so multiplying by a subfield element is 16 independent byte products
+// (xtime mod 0x11B), while M8 tables work unchanged (any GF(2)-basis).
+struct TowerTables {
+  U128 t;             // the root t (polynomial representation)
+  U128 to_poly[128];  // e_k in polynomial representation (R -> poly rows)
+  U128 to_r[128];     // x^k in R coordinates (poly -> R rows)
+  uint8_t tau[8];     // tau[b] = R byte 0 of v_{b+1} (b < 7): C2P(2d) for d < 128 is byte sum_b d_b tau[b]
+};
+const TowerTables& tower_tables();
+U128 host_to_r(U128 poly);
+U128 host_from_r(U128 r);
+
 U128 host_gf128_mul(U128 a, U128 b);
 U128 host_gf64_mul(U128 a, U128 b);                      // lo words only
 U128 host_cantor_to_poly(const FieldTables& t, U128 c);  // bitmat.hpp:29-35

@@ -140,9 +140,8 @@ constexpr int kM8Uint4 = 4096;
 // of chunk c -- the high nibble s once from rows 8c+4..8c+7, the 16 low-nibble combinations
 // incrementally in registers; stores are conflict-free (a quarter-warp covers 8 bank groups).
 // rows_scratch: 144 uint4 of shared memory (row k padded to k + k/8).
-__device__ __forceinline__ void m8_build(uint4* __restrict__ tab, uint4* __restrict__ rows_scratch, uint4 w, int tid) {
-  if (tid < 128) rows_scratch[tid + (tid >> 3)] = gf_mul_xk(w, (unsigned)tid);
-  __syncthreads();
+// Expansion of 128 rows (rows_scratch[k + k/8] = image of basis vector k) into the 16 chunk tables.
+__device__ __forceinline__ void m8_expand(uint4* __restrict__ tab, const uint4* __restrict__ rows_scratch, int tid) {
   if (tid < 256) {  // larger CTAs: the other threads only join the barriers
   const int c = tid & 15, s = tid >> 4;
   uint4 r[8];
@@ -159,6 +158,12 @@ __device__ __forceinline__ void m8_build(uint4* __restrict__ tab, uint4* __restr
 #pragma unroll
   for (int u = 0; u < 16; ++u) dst[u * 8] = t[u];
   }
+}
+
+__device__ __forceinline__ void m8_build(uint4* __restrict__ tab, uint4* __restrict__ rows_scratch, uint4 w, int tid) {
+  if (tid < 128) rows_scratch[tid + (tid >> 3)] = gf_mul_xk(w, (unsigned)tid);
+  __syncthreads();
+  m8_expand(tab, rows_scratch, tid);
   __syncthreads();
 }
 
@@ -176,6 +181,43 @@ __device__ __forceinline__ uint4 m8_mul(const uint4* __restrict__ tab, uint4 x, 
   return x4(acc0, acc1);
 }
 
+
+// m8_mul with the lane rotation applied to the operand once: the 64-bit halves are rotated right by
+// 8q bits, so lookup k reads byte k at a constant position (one PRMT) of chunk (k + q) & 7, and the
+// entry address is base[k] + 128 * byte with base[k] = tab + ((k + q) & 7) (one IMAD).
+struct M8Base {
+  uint32_t b[8];  // shared-memory byte addresses of tab + ((k + q) & 7)
+};
+__device__ __forceinline__ M8Base m8_base(const uint4* tab, int q) {
+  M8Base m;
+  const uint32_t t = (uint32_t)__cvta_generic_to_shared(tab);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) m.b[k] = t + 16u * (uint32_t)((k + q) & 7);
+  return m;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint4 m8_mul_r(const M8Base& mb, uint4 x, int q) {
+  // rotate (x.y:x.x) and (x.w:x.z) right by 8q bits
+  const bool sw = q & 4;
+  const uint32_t s = 8u * (uint32_t)(q & 3);
+  const uint32_t a0 = sw ? x.y : x.x, a1 = sw ? x.x : x.y, b0 = sw ? x.w : x.z, b1 = sw ? x.z : x.w;
+  const uint32_t lo0 = __funnelshift_r(a0, a1, s), lo1 = __funnelshift_r(a1, a0, s);
+  const uint32_t hi0 = __funnelshift_r(b0, b1, s), hi1 = __funnelshift_r(b1, b0, s);
+  uint4 acc0 = make_uint4(0, 0, 0, 0), acc1 = make_uint4(0, 0, 0, 0);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t sel = 0x4440u | (uint32_t)(k & 3);
+    const uint32_t lo = __byte_perm(k < 4 ? lo0 : lo1, 0, sel);
+    const uint32_t hi = __byte_perm(k < 4 ? hi0 : hi1, 0, sel);
+    acc0 = x4(acc0, lds128(mb.b[k] + 128u * lo));
+    acc1 = x4(acc1, lds128(mb.b[k] + 128u * hi + 2048u * 16u));
+  }
+  return x4(acc0, acc1);
+}
 
 // ---------------------------------------------------------------- rotated 4-bit tables, 8 at a time
 // For tile layers whose twiddles are shared by only 2^5..2^7 butterflies: 32 nibble-chunk tables of

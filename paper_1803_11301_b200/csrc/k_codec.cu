@@ -328,35 +328,36 @@ const RowTables& row_tables(int dev) {
 // Column range [col0, col0 + ncols) of the 128-row partition matrix (row pitch n_p bits) -> ncols
 // elements.  rows_live: 64 when rows >= 64 are known zero (pipeline operands), else 128.
 void encode_cols_device(const uint32_t* poly, unsigned l, uint64_t col0, uint64_t ncols, uint4* ev, int rows_live,
-                        cudaStream_t s) {
+                        cudaStream_t s, bool tower) {
   int dev;
   FPM_CUDA(cudaGetDevice(&dev));
   const uint64_t n_p = (uint64_t)1 << l;
   if (n_p < 1024) {
-    if (col0 != 0 || ncols != n_p) throw Error(kInvalid, "encode: column ranges need n_p >= 1024");
+    if (col0 != 0 || ncols != n_p || tower) throw Error(kInvalid, "encode: column ranges need n_p >= 1024");
     encode_small_kernel<<<(unsigned)((n_p + 127) / 128), 128, 0, s>>>(poly, n_p, row_tables(dev).rows, ev);
     FPM_LAUNCH_CHECK();
     return;
   }
   if (col0 % 1024 || ncols % 1024 || col0 + ncols > n_p) throw Error(kInvalid, "encode: column range not 1024-aligned");
   const DeviceTables& dt = device_tables(dev);
+  const uint4* tab = tower ? dt.enc_m8r : dt.enc_m8;
   const uint64_t nslabs = ncols / 32 / kSlabWords;
   if (rows_live == 64) {
     const size_t smem = kM8Uint4 / 2 * sizeof(uint4) + 64 * kPad * sizeof(uint32_t);
     static PerDeviceOnce attr;
     attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
-    encode_kernel<64><<<resident_grid(encode_kernel<64>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, dt.enc_m8, ev);
+    encode_kernel<64><<<resident_grid(encode_kernel<64>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, tab, ev);
   } else {
     const size_t smem = kM8Uint4 * sizeof(uint4) + 128 * kPad * sizeof(uint32_t);
     static PerDeviceOnce attr;
     attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
-    encode_kernel<128><<<resident_grid(encode_kernel<128>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, dt.enc_m8, ev);
+    encode_kernel<128><<<resident_grid(encode_kernel<128>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, tab, ev);
   }
   FPM_LAUNCH_CHECK();
 }
 
-void encode_device_rows(const uint32_t* poly, unsigned l, uint4* ev, int rows_live, cudaStream_t s) {
-  encode_cols_device(poly, l, 0, (uint64_t)1 << l, ev, rows_live, s);
+void encode_device_rows(const uint32_t* poly, unsigned l, uint4* ev, int rows_live, cudaStream_t s, bool tower) {
+  encode_cols_device(poly, l, 0, (uint64_t)1 << l, ev, rows_live, s, tower);
 }
 
 void encode_device(const uint32_t* poly, unsigned l, uint4* ev, cudaStream_t s) {
@@ -364,11 +365,11 @@ void encode_device(const uint32_t* poly, unsigned l, uint4* ev, cudaStream_t s) 
 }
 
 // ncols elements -> a 128-row x ncols-bit slice (row pitch ncols bits).
-void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaStream_t s) {
+void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaStream_t s, bool tower) {
   int dev;
   FPM_CUDA(cudaGetDevice(&dev));
   if (ncols < 1024) {
-    if (ncols & (ncols - 1)) throw Error(kInvalid, "decode: element count must be a power of two");
+    if ((ncols & (ncols - 1)) || tower) throw Error(kInvalid, "decode: element count must be a power of two");
     const uint64_t nwords = (128 * ncols + 31) / 32;
     decode_small_kernel<<<(unsigned)((nwords + 127) / 128), 128, 0, s>>>(ev, ncols, row_tables(dev).inv, slice);
     FPM_LAUNCH_CHECK();
@@ -380,7 +381,7 @@ void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaSt
   static PerDeviceOnce attr;
   attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
   const uint64_t nslabs = ncols / 32 / kSlabWords;
-  decode_kernel<<<resident_grid(decode_kernel, 256, smem, nslabs), 256, smem, s>>>(ev, nslabs, ncols / 32, dt.dec_m8, slice);
+  decode_kernel<<<resident_grid(decode_kernel, 256, smem, nslabs), 256, smem, s>>>(ev, nslabs, ncols / 32, tower ? dt.dec_m8r : dt.dec_m8, slice);
   FPM_LAUNCH_CHECK();
 }
 
@@ -422,8 +423,8 @@ void decode64_device(const uint2* ev, unsigned l, uint32_t* poly, cudaStream_t s
   FPM_LAUNCH_CHECK();
 }
 
-void decode_device(const uint4* ev, unsigned l, uint32_t* poly, cudaStream_t s) {
-  decode_cols_device(ev, (uint64_t)1 << l, poly, s);
+void decode_device(const uint4* ev, unsigned l, uint32_t* poly, cudaStream_t s, bool tower) {
+  decode_cols_device(ev, (uint64_t)1 << l, poly, s, tower);
 }
 
 }  // namespace fpm

@@ -26,6 +26,7 @@
 
 #include "fpm_internal.h"
 #include "gf128.cuh"
+#include "tower.cuh"
 
 namespace fpm {
 
@@ -60,7 +61,8 @@ __device__ __forceinline__ uint4 twiddle(const TwiddleSrc& tw, unsigned l, unsig
 }
 
 // ------------------------------------------------------------------ top layers (i >= T)
-template <bool INV>
+// R: elements in the tower representation (tower.cuh), the table built in R.
+template <bool INV, bool R>
 __global__ void __launch_bounds__(256) fft_top_kernel(uint4* __restrict__ ev, unsigned l, unsigned i, int ppc, TwiddleSrc tw) {
   extern __shared__ uint4 tab[];            // kM8Uint4
   __shared__ uint4 rows[144];
@@ -68,7 +70,14 @@ __global__ void __launch_bounds__(256) fft_top_kernel(uint4* __restrict__ ev, un
   const uint64_t pair0 = (uint64_t)blockIdx.x * ppc;   // ppc <= 2^i: CTA pairs never straddle a block
   const uint64_t b = pair0 >> i;
   const uint4 w = twiddle(tw, l, i, b);
-  m8_build(tab, rows, w, threadIdx.x);
+  if (R) {
+    rows_r<false>(rows, w, threadIdx.x, tw.to_r);
+    __syncthreads();
+    m8_expand(tab, rows, threadIdx.x);
+    __syncthreads();
+  } else {
+    m8_build(tab, rows, w, threadIdx.x);
+  }
   const int copy = threadIdx.x & 7;
   uint4* base = ev + (b << (i + 1));
 #pragma unroll 4
@@ -93,9 +102,9 @@ __global__ void __launch_bounds__(256) fft_top_kernel(uint4* __restrict__ ev, un
 // w(i, 2B) and (q2,q3) with w(i, 2B+1).  The three M8 tables (192 KiB) are built by three groups of
 // 256 threads; one 768-thread CTA per SM then streams its quads.
 constexpr int kTop4Threads = 768;
-constexpr size_t kTop4Smem = (3 * (size_t)kM8Uint4 + 3 * 144) * sizeof(uint4);
+constexpr size_t kTop4Smem = (3 * (size_t)kM8Uint4 + 3 * 144 + 136) * sizeof(uint4);  // + to_r (tower)
 
-template <bool INV>
+template <bool INV, bool R>
 __global__ void __launch_bounds__(kTop4Threads, 1) fft_top4_kernel(uint4* __restrict__ ev, unsigned l, unsigned i,
                                                                    int qpc, TwiddleSrc tw) {
   extern __shared__ uint4 sm4[];
@@ -103,10 +112,15 @@ __global__ void __launch_bounds__(kTop4Threads, 1) fft_top4_kernel(uint4* __rest
   uint4* t0a = sm4 + kM8Uint4;       // w(i, 2B)
   uint4* t0b = sm4 + 2 * kM8Uint4;   // w(i, 2B+1)
   uint4* rows = sm4 + 3 * kM8Uint4;  // 3 x 144
+  uint4* to_r = rows + 3 * 144;      // tower: the conversion rows, to_r_pad layout
   const uint64_t h = (uint64_t)1 << i;
   const uint64_t quad0 = (uint64_t)blockIdx.x * qpc;  // qpc <= h: a CTA never straddles a block
   const uint64_t B = quad0 >> i;
   const int tid = threadIdx.x, grp = tid >> 8, lt = tid & 255;
+  if (R) {
+    if (tid < 128) to_r[to_r_pad(tid)] = __ldg(tw.to_r + tid);
+    __syncthreads();
+  }
   {
     uint4 w = make_uint4(0, 0, 0, 0);
     if (grp == 0) w = twiddle(tw, l, i + 1, B);
@@ -114,7 +128,11 @@ __global__ void __launch_bounds__(kTop4Threads, 1) fft_top4_kernel(uint4* __rest
     else if (grp == 2) w = twiddle(tw, l, i, 2 * B + 1);
     uint4* tab = sm4 + grp * kM8Uint4;
     uint4* rs = rows + grp * 144;
-    if (grp < 3 && lt < 128) rs[lt + (lt >> 3)] = gf_mul_xk(w, (unsigned)lt);
+    if (R) {
+      if (grp < 3) rows_r<true>(rs, w, lt, to_r);
+    } else if (grp < 3 && lt < 128) {
+      rs[lt + (lt >> 3)] = gf_mul_xk(w, (unsigned)lt);
+    }
     __syncthreads();
     if (grp < 3) {
       const int c = lt & 15, sv = lt >> 4;
@@ -357,6 +375,157 @@ __global__ void __launch_bounds__(kTile2Threads, 512 / kTile2Threads) fft_tile_f
   }
 }
 
+// ------------------------------------------------------------------ tower-representation tiles
+// Tile layers on R elements (tower.cuh).  Layer i's twiddle for tile block blk is
+//   w = Z ^ C2P(2 (blk & ~127)) ^ C2P(2 (blk & 127)),  Z = twiddle(i, tile's first block);
+// the first two terms are one M8 table per 128 blocks (layers 0 and 1 of a 2^10 tile need 4 and 2,
+// every other layer one), the last is the subfield scalar d(blk & 127), applied by smul_t (byte permutes, tower.cuh).
+// A table build is latency-bound (twiddle -> conversion -> shuffles -> xtimes -> 4096 stores), so:
+// the tile's table twiddles are computed once per tile (wz, shared by both directions), the
+// conversion rows stay in shared memory, and the rows of table k+1 are computed by warps 0-3 before
+// their butterflies with table k (double-buffered rows), overlapping the other warps' work.
+__host__ __device__ constexpr int tower_groups(unsigned T, unsigned i) {  // tables of layer i
+  return (1 << (T - 1 - i)) > 128 ? (1 << (T - 1 - i)) >> 7 : 1;
+}
+__host__ __device__ constexpr int tower_tables(unsigned T) {
+  int n = 0;
+  for (unsigned i = 0; i < T; ++i) n += tower_groups(T, i);
+  return n;
+}
+constexpr int kTowerMaxTables = tower_tables(11);  // 22
+
+struct TowerSmem {  // after the 2^(T+1) tile elements
+  uint4 tab[kM8Uint4];
+  uint4 rows[2][144];
+  uint4 to_r[128 + 8];        // rows_r conversion source, to_r_pad layout
+  uint4 rows_to_r[144];       // m8 rows of poly -> R
+  uint4 rows_to_poly[144];    // m8 rows of R -> poly
+  uint4 wz[kTowerMaxTables];  // table twiddles of the current tile, layer-ascending, h ascending
+  SmulTab stab[128];          // subfield twiddle parts d(b) = R(C2P(2b)), b < 128 (tower.cuh)
+};
+
+// Index in wz of (layer i, group g): layers ascending.
+__device__ __forceinline__ int tower_wz_index(unsigned T, unsigned i, int g) {
+  int k = 0;
+  for (unsigned u = 0; u < i; ++u) k += tower_groups(T, u);
+  return k + g;
+}
+
+template <bool INV, int NT>
+__device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, unsigned T, TowerSmem& sm) {
+  const int npairs = 1 << (T - 1), n = 1 << T, tid = threadIdx.x, q = tid & 7;
+  const int ntab = tower_tables(T);
+  // table sequence k = 0..ntab-1: forward = wz descending by layer (h ascending within a layer),
+  // inverse = wz ascending
+  auto wz_of = [&](int k) -> int {
+    if (INV) return k;
+    int kk = 0;
+    for (int i = (int)T - 1; i >= 0; --i) {
+      const int g = tower_groups(T, (unsigned)i);
+      if (k < kk + g) return tower_wz_index(T, (unsigned)i, k - kk);
+      kk += g;
+    }
+    return 0;
+  };
+  rows_r<true>(sm.rows[0], sm.wz[wz_of(0)], tid, sm.to_r);
+  __syncthreads();
+  m8_expand(sm.tab, sm.rows[0], tid);
+  __syncthreads();
+  int k = 0;
+  for (unsigned step = 0; step < T; ++step) {
+    const unsigned i = INV ? step : T - 1 - step;
+    const int nblk = npairs >> i;
+    const int lg = (nblk < 128 ? T - 1 : 7 + i);  // log2(pairs per table per tile)
+    for (int h = 0; h < nblk; h += 128, ++k) {
+      if (k + 1 < ntab) rows_r<true>(sm.rows[(k + 1) & 1], sm.wz[wz_of(k + 1)], tid, sm.to_r);
+      const M8Base mb = m8_base(sm.tab, q);
+      for (int pp = tid; pp < (NT << lg); pp += blockDim.x) {
+        const int p = pp & ((1 << lg) - 1), tt = pp >> lg;
+        const int blk = h + (p >> i), j = p & ((1 << i) - 1);
+        const int i0 = (blk << (i + 1)) + j + tt * n, i1 = i0 + (1 << i);
+        const int d = blk & 127;  // subfield part of the twiddle (zero iff d == 0)
+        uint4 u0 = s[i0], u1 = s[i1];
+        if (!INV) {
+          uint4 m = m8_mul_r(mb, u1, q);
+#ifndef FPM_EXP_NO_SMUL
+          if (d) m = x4(m, smul_t(u1, sm.stab[d]));
+#endif
+          u0 = x4(u0, m);
+          u1 = x4(u1, u0);
+        } else {
+          u1 = x4(u1, u0);
+          uint4 m = m8_mul_r(mb, u1, q);
+#ifndef FPM_EXP_NO_SMUL
+          if (d) m = x4(m, smul_t(u1, sm.stab[d]));
+#endif
+          u0 = x4(u0, m);
+        }
+        s[i0] = u0;
+        s[i1] = u1;
+      }
+      __syncthreads();  // lookups of table k and this layer's butterflies done; rows of k+1 ready
+      if (k + 1 < ntab) {
+#ifndef FPM_EXP_NO_BUILD
+        m8_expand(sm.tab, sm.rows[(k + 1) & 1], tid);
+#endif
+        __syncthreads();
+      }
+    }
+  }
+}
+
+#ifndef FPM_TOWER_THREADS
+#define FPM_TOWER_THREADS 256
+#endif
+constexpr int kTowerThreads = FPM_TOWER_THREADS;
+size_t tower_smem(unsigned T) { return 2 * ((size_t)1 << T) * sizeof(uint4) + sizeof(TowerSmem); }
+
+// fft_tile_fused2_kernel on R tiles: forward layers [0, T) of both operands (one table per layer
+// serves both tiles), the pointwise product (R -> poly by an M8 table of to_poly, gf_mul, poly -> R
+// by an M8 table of to_r) and the inverse layers [0, T).
+__global__ void __launch_bounds__(kTowerThreads, 512 / kTowerThreads) fft_tile_tower_kernel(const uint4* __restrict__ ea,
+                                                                          uint4* __restrict__ eb, unsigned l,
+                                                                          unsigned T, TwiddleSrc tw) {
+  extern __shared__ uint4 s[];
+  const int n = 1 << T, tid = threadIdx.x, q = tid & 7;
+  TowerSmem& sm = *reinterpret_cast<TowerSmem*>(s + 2 * n);
+  smul_tabs_build(sm.stab, tw.tau, tid);
+  if (tid < 128) {
+    sm.to_r[to_r_pad(tid)] = __ldg(tw.to_r + tid);
+    sm.rows_to_r[tid + (tid >> 3)] = __ldg(tw.to_r + tid);
+    sm.rows_to_poly[tid + (tid >> 3)] = __ldg(tw.to_poly + tid);
+  }
+  const int ntab = tower_tables(T);
+  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint4* g = eb + (t << T);
+    const uint4* ga = ea + (t << T);
+    if (tid < ntab) {  // wz[k]: layer i, group h of this tile: Z(i) ^ C2P(2 * 128 h)
+      int i = 0, kk = tid;
+      while (kk >= tower_groups(T, (unsigned)i)) kk -= tower_groups(T, (unsigned)i++);
+      sm.wz[tid] = x4(twiddle(tw, l, (unsigned)i, t << (T - 1 - i)), c2p2(tw.c2p, (uint64_t)kk << 7));
+    }
+    for (int k = tid; k < n; k += blockDim.x) {
+      s[k] = ga[k];
+      s[n + k] = g[k];
+    }
+    __syncthreads();
+    tile_layers_r<false, 2>(s, T, sm);
+    m8_expand(sm.tab, sm.rows_to_poly, tid);
+    __syncthreads();
+    const M8Base mb = m8_base(sm.tab, q);
+    for (int k = tid; k < n; k += blockDim.x) s[k] = gf_mul(m8_mul_r(mb, s[k], q), m8_mul_r(mb, s[n + k], q));
+    __syncthreads();
+    m8_expand(sm.tab, sm.rows_to_r, tid);
+    __syncthreads();
+    for (int k = tid; k < n; k += blockDim.x) s[k] = m8_mul_r(mb, s[k], q);
+    // (tile_layers_r's first barrier orders these stores before its butterflies)
+    tile_layers_r<true, 1>(s, T, sm);
+    for (int k = tid; k < n; k += blockDim.x) g[k] = s[k];
+    __syncthreads();
+  }
+}
+
 // Exchanged layer of the sharded FFT: all local elements share one twiddle w.
 template <bool INV>
 __global__ void __launch_bounds__(256) fft_pair_kernel(uint4* __restrict__ mine, const uint4* __restrict__ theirs,
@@ -431,7 +600,12 @@ unsigned pipeline_tile_log2(unsigned l) {
 TwiddleSrc make_twiddle_src(int device, unsigned l, U128 base) {
   if (l > (unsigned)kMaxLayers) throw Error(kInvalid, "butterfly: too many layers");
   TwiddleSrc tw{};
-  tw.c2p = device_tables(device).c2p;
+  const DeviceTables& dt = device_tables(device);
+  tw.c2p = dt.c2p;
+  tw.to_r = dt.to_r;
+  tw.to_poly = dt.to_poly;
+  const TowerTables& tt = tower_tables();
+  for (int b = 0; b < 8; ++b) tw.tau |= (uint64_t)tt.tau[b] << (8 * b);
   const FieldTables& ft = field_tables();
   for (unsigned i = 0; i < l; ++i) {
     U128 c;  // base >> i (Cantor coordinates)
@@ -443,16 +617,16 @@ TwiddleSrc make_twiddle_src(int device, unsigned l, U128 base) {
   return tw;
 }
 
-void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s) {
-  if (l <= T) return;
+template <bool R>
+void top_passes(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s) {
   const size_t smem = kM8Uint4 * sizeof(uint4);
   static PerDeviceOnce attr;
-  attr.run([&] { set_smem(fft_top_kernel<false>, smem); set_smem(fft_top_kernel<true>, smem); });
+  attr.run([&] { set_smem(fft_top_kernel<false, R>, smem); set_smem(fft_top_kernel<true, R>, smem); });
   // Pairs per CTA: 4096 amortise the 64 KiB table build; smaller layers still fill 2 CTAs/SM.
   static PerDeviceOnce attr4;
   attr4.run([&] {
-    set_smem(fft_top4_kernel<false>, kTop4Smem);
-    set_smem(fft_top4_kernel<true>, kTop4Smem);
+    set_smem(fft_top4_kernel<false, R>, kTop4Smem);
+    set_smem(fft_top4_kernel<true, R>, kTop4Smem);
   });
   const uint64_t pairs = ((uint64_t)1 << l) / 2;
   uint64_t ppc = 4096;
@@ -461,8 +635,8 @@ void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const
   if (T < 8 || ctas == 0) throw Error(kInvalid, "butterfly_top: layer too small for the table layer kernel");
   auto radix2 = [&](unsigned i) {
     const uint64_t p = std::min<uint64_t>(ppc, (uint64_t)1 << i);  // a CTA stays inside one block
-    if (!inverse) fft_top_kernel<false><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, l, i, (int)p, tw);
-    else fft_top_kernel<true><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, l, i, (int)p, tw);
+    if (!inverse) fft_top_kernel<false, R><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, l, i, (int)p, tw);
+    else fft_top_kernel<true, R><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, l, i, (int)p, tw);
     FPM_LAUNCH_CHECK();
   };
   // layer pairs (i+1, i) from the top down (forward) / bottom up (inverse); an odd count leaves
@@ -472,8 +646,8 @@ void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const
   while (qpc > 1024 && quads / qpc < (uint64_t)sms() * 4) qpc /= 2;
   auto radix4 = [&](unsigned i) {
     const unsigned q = (unsigned)std::min<uint64_t>(qpc, (uint64_t)1 << i);
-    if (!inverse) fft_top4_kernel<false><<<(unsigned)(quads / q), kTop4Threads, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
-    else fft_top4_kernel<true><<<(unsigned)(quads / q), kTop4Threads, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
+    if (!inverse) fft_top4_kernel<false, R><<<(unsigned)(quads / q), kTop4Threads, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
+    else fft_top4_kernel<true, R><<<(unsigned)(quads / q), kTop4Threads, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
     FPM_LAUNCH_CHECK();
   };
   const unsigned n = l - T;
@@ -485,6 +659,13 @@ void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const
     if (odd) radix2(T);
     for (unsigned i = T + (odd ? 1 : 0); i + 1 < l; i += 2) radix4(i);
   }
+}
+
+void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s,
+                          bool tower) {
+  if (l <= T) return;
+  if (tower) top_passes<true>(ev, l, T, inverse, tw, s);
+  else top_passes<false>(ev, l, T, inverse, tw, s);
 }
 
 // One thread per butterfly of a tile layer (2^(T-1) pairs), at most 256: small tiles run more CTAs
@@ -555,6 +736,26 @@ void butterfly_tile_fused2_device(const uint4* ea, uint4* eb, unsigned l, unsign
   attr.run([&] { set_smem(fft_tile_fused2_kernel, (2 * ((size_t)1 << 11) + kM8Uint4 + 144) * sizeof(uint4)); });
   const int grid = resident_grid(fft_tile_fused2_kernel, kTile2Threads, smem, ((uint64_t)1 << l) >> T);
   fft_tile_fused2_kernel<<<grid, kTile2Threads, smem, s>>>(ea, eb, l, T, tw);
+  FPM_LAUNCH_CHECK();
+}
+
+// The tower tile pass (fft_tile_tower_kernel) for the product pipeline; FPM_TOWER=0 disables it.
+bool tile_tower_enabled(unsigned T) {
+  static const bool on = [] {
+    const char* e = std::getenv("FPM_TOWER");
+    return !(e && e[0] == '0');
+  }();
+  return on && T >= 10 && T <= 11;
+}
+
+void butterfly_tile_tower_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
+                                 cudaStream_t s) {
+  if (T < 10 || T > 11 || l < T) throw Error(kInvalid, "tower tile pass: T must be 10 or 11");
+  static PerDeviceOnce attr;
+  attr.run([&] { set_smem(fft_tile_tower_kernel, tower_smem(11)); });
+  const size_t smem = tower_smem(T);
+  const int grid = resident_grid(fft_tile_tower_kernel, kTowerThreads, smem, ((uint64_t)1 << l) >> T);
+  fft_tile_tower_kernel<<<grid, kTowerThreads, smem, s>>>(ea, eb, l, T, tw);
   FPM_LAUNCH_CHECK();
 }
 

@@ -89,13 +89,14 @@ def test_butterfly_tile_depths(tile):
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("env", [{}, {"FPM_FUSE_AB": "0"}, {"FPM_TILE_LOG2": "11", "FPM_TILE_LOG2_64": "12"},
+@pytest.mark.parametrize("env", [{}, {"FPM_FUSE_AB": "0"}, {"FPM_TOWER": "0"}, {"FPM_TILE_LOG2": "11", "FPM_TILE_LOG2_64": "12"},
                                  {"FPM_TILE_LOG2": "10", "FPM_TILE_LOG2_64": "10", "FPM_FUSE_AB": "0"},
                                  {"FPM_TILE_LOG2": "12", "FPM_TILE_LOG2_64": "11"}])
 @pytest.mark.parametrize("field", [128, 64])
 def test_pipeline_schedules(checker, port, env, field):
     """Every tile schedule of the product pipeline -- both operands' tile layers fused into the
-    pointwise pass (default), operand a in its own tile pass, other depths -- gives the reference
+    pointwise pass on tower-representation tiles (default), the same on polynomial-representation
+    tiles, operand a in its own tile pass, other depths -- gives the reference
     product (child process per environment; l = 18 and 20)."""
     import hashlib
     import os
