@@ -200,7 +200,8 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
-__device__ __forceinline__ uint4 m8_mul_r(const M8Base& mb, uint4 x, int q) {
+// off: byte offset of another table laid out after the one mb was made for (folded into the LDS).
+__device__ __forceinline__ uint4 m8_mul_r(const M8Base& mb, uint4 x, int q, uint32_t off = 0) {
   // rotate (x.y:x.x) and (x.w:x.z) right by 8q bits
   const bool sw = q & 4;
   const uint32_t s = 8u * (uint32_t)(q & 3);
@@ -213,8 +214,8 @@ __device__ __forceinline__ uint4 m8_mul_r(const M8Base& mb, uint4 x, int q) {
     const uint32_t sel = 0x4440u | (uint32_t)(k & 3);
     const uint32_t lo = __byte_perm(k < 4 ? lo0 : lo1, 0, sel);
     const uint32_t hi = __byte_perm(k < 4 ? hi0 : hi1, 0, sel);
-    acc0 = x4(acc0, lds128(mb.b[k] + 128u * lo));
-    acc1 = x4(acc1, lds128(mb.b[k] + 128u * hi + 2048u * 16u));
+    acc0 = x4(acc0, lds128(mb.b[k] + 128u * lo + off));
+    acc1 = x4(acc1, lds128(mb.b[k] + 128u * hi + 2048u * 16u + off));
   }
   return x4(acc0, acc1);
 }
