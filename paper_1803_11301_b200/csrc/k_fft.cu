@@ -403,8 +403,13 @@ struct TowerSmem {  // after the 2^(T+1) tile elements
   uint4 rows_to_r[144];       // m8 rows of poly -> R
   uint4 rows_to_poly[144];    // m8 rows of R -> poly
   uint4 wz[kTowerMaxTables];  // table twiddles of the current tile, layer-ascending, h ascending
-  SmulTab stab[128];          // subfield twiddle parts d(b) = R(C2P(2b)), b < 128 (tower.cuh)
+  SmulTabs stab;              // subfield twiddle parts d(b) = R(C2P(2b)), b < 128 (tower.cuh)
 };
+
+// Tile element k lives at tsw(k) = k ^ 7 [bit 3 of k]: the butterflies of layers 0-2 (pairs at
+// distance 1, 2, 4) then reach eight distinct 16-byte bank groups per quarter-warp (2-way bank
+// conflicts otherwise); contiguous runs of 8 stay contiguous.
+__device__ __forceinline__ int tsw(int k) { return k ^ (((k >> 3) & 1) * 7); }
 
 // Index in wz of (layer i, group g): layers ascending.
 __device__ __forceinline__ int tower_wz_index(unsigned T, unsigned i, int g) {
@@ -413,16 +418,17 @@ __device__ __forceinline__ int tower_wz_index(unsigned T, unsigned i, int g) {
   return k + g;
 }
 
+// Layers [P, T) of the tile on R elements (forward: T-1 down to P; inverse: P up to T-1).
 template <bool INV, int NT>
-__device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, unsigned T, TowerSmem& sm) {
+__device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, unsigned T, unsigned P, TowerSmem& sm) {
   const int npairs = 1 << (T - 1), n = 1 << T, tid = threadIdx.x, q = tid & 7;
-  const int ntab = tower_tables(T);
+  const int first = tower_wz_index(T, P, 0), ntab = tower_tables(T) - first;
   // table sequence k = 0..ntab-1: forward = wz descending by layer (h ascending within a layer),
   // inverse = wz ascending
   auto wz_of = [&](int k) -> int {
-    if (INV) return k;
+    if (INV) return first + k;
     int kk = 0;
-    for (int i = (int)T - 1; i >= 0; --i) {
+    for (int i = (int)T - 1; i >= (int)P; --i) {
       const int g = tower_groups(T, (unsigned)i);
       if (k < kk + g) return tower_wz_index(T, (unsigned)i, k - kk);
       kk += g;
@@ -434,8 +440,8 @@ __device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, unsigned T,
   m8_expand(sm.tab, sm.rows[0], tid);
   __syncthreads();
   int k = 0;
-  for (unsigned step = 0; step < T; ++step) {
-    const unsigned i = INV ? step : T - 1 - step;
+  for (unsigned step = 0; step < T - P; ++step) {
+    const unsigned i = INV ? P + step : T - 1 - step;
     const int nblk = npairs >> i;
     const int lg = (nblk < 128 ? T - 1 : 7 + i);  // log2(pairs per table per tile)
     for (int h = 0; h < nblk; h += 128, ++k) {
@@ -446,11 +452,11 @@ __device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, unsigned T,
         const int blk = h + (p >> i), j = p & ((1 << i) - 1);
         const int i0 = (blk << (i + 1)) + j + tt * n, i1 = i0 + (1 << i);
         const int d = blk & 127;  // subfield part of the twiddle (zero iff d == 0)
-        uint4 u0 = s[i0], u1 = s[i1];
+        uint4 u0 = s[tsw(i0)], u1 = s[tsw(i1)];
         if (!INV) {
           uint4 m = m8_mul_r(mb, u1, q);
 #ifndef FPM_EXP_NO_SMUL
-          if (d) m = x4(m, smul_t(u1, sm.stab[d]));
+          if (d) m = x4(m, smul_t(u1, smul_tab(sm.stab, d)));
 #endif
           u0 = x4(u0, m);
           u1 = x4(u1, u0);
@@ -458,12 +464,12 @@ __device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, unsigned T,
           u1 = x4(u1, u0);
           uint4 m = m8_mul_r(mb, u1, q);
 #ifndef FPM_EXP_NO_SMUL
-          if (d) m = x4(m, smul_t(u1, sm.stab[d]));
+          if (d) m = x4(m, smul_t(u1, smul_tab(sm.stab, d)));
 #endif
           u0 = x4(u0, m);
         }
-        s[i0] = u0;
-        s[i1] = u1;
+        s[tsw(i0)] = u0;
+        s[tsw(i1)] = u1;
       }
       __syncthreads();  // lookups of table k and this layer's butterflies done; rows of k+1 ready
       if (k + 1 < ntab) {
@@ -476,9 +482,49 @@ __device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, unsigned T,
   }
 }
 
+// Layers [0, P) of the tile in POLYNOMIAL representation with the IMAD-hole gf_mul (FMA pipe): these
+// layers would need 2^(T-8-i) tables each in R, while the shared-memory pipe is the tower pass's
+// bottleneck.  Forward: both tiles, one prepared twiddle per butterfly pair.
+template <bool INV>
+__device__ __forceinline__ void tile_layers_poly(uint4* __restrict__ s, unsigned T, unsigned P, unsigned l,
+                                                 uint64_t t, const TwiddleSrc& tw) {
+  const int npairs = 1 << (T - 1), n = 1 << T;
+  for (unsigned step = 0; step < P; ++step) {
+    const unsigned i = INV ? step : P - 1 - step;
+    const uint4 Z = twiddle(tw, l, i, t << (T - 1 - i));
+    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+      const int blk = p >> i, j = p & ((1 << i) - 1);
+      const int i0 = tsw((blk << (i + 1)) + j), i1 = tsw((blk << (i + 1)) + j + (1 << i));
+      const uint4 w = x4(Z, c2p2(tw.c2p, (uint64_t)blk));
+      if (!INV) {
+        const GfPrep wp = gf_prep(w);
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+          uint4 u0 = s[i0 + tt * n], u1 = s[i1 + tt * n];
+          u0 = x4(u0, gf_mul_prep(wp, u1));
+          u1 = x4(u1, u0);
+          s[i0 + tt * n] = u0;
+          s[i1 + tt * n] = u1;
+        }
+      } else {
+        uint4 u0 = s[i0], u1 = s[i1];
+        u1 = x4(u1, u0);
+        u0 = x4(u0, gf_mul(w, u1));
+        s[i0] = u0;
+        s[i1] = u1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 #ifndef FPM_TOWER_THREADS
 #define FPM_TOWER_THREADS 256
 #endif
+#ifndef FPM_TOWER_POLY
+#define FPM_TOWER_POLY 1
+#endif
+constexpr unsigned kPolyLayers = FPM_TOWER_POLY;  // bottom tile layers in polynomial representation
 constexpr int kTowerThreads = FPM_TOWER_THREADS;
 size_t tower_smem(unsigned T) { return 2 * ((size_t)1 << T) * sizeof(uint4) + sizeof(TowerSmem); }
 
@@ -508,22 +554,31 @@ __global__ void __launch_bounds__(kTowerThreads, 512 / kTowerThreads) fft_tile_t
       sm.wz[tid] = x4(twiddle(tw, l, (unsigned)i, t << (T - 1 - i)), c2p2(tw.c2p, (uint64_t)kk << 7));
     }
     for (int k = tid; k < n; k += blockDim.x) {
-      s[k] = ga[k];
-      s[n + k] = g[k];
+      s[tsw(k)] = ga[k];
+      s[n + tsw(k)] = g[k];
     }
     __syncthreads();
-    tile_layers_r<false, 2>(s, T, sm);
+    tile_layers_r<false, 2>(s, T, kPolyLayers, sm);
     m8_expand(sm.tab, sm.rows_to_poly, tid);
     __syncthreads();
     const M8Base mb = m8_base(sm.tab, q);
-    for (int k = tid; k < n; k += blockDim.x) s[k] = gf_mul(m8_mul_r(mb, s[k], q), m8_mul_r(mb, s[n + k], q));
-    __syncthreads();
+    if (kPolyLayers) {
+      for (int k = tid; k < 2 * n; k += blockDim.x) s[k] = m8_mul_r(mb, s[k], q);
+      __syncthreads();
+      tile_layers_poly<false>(s, T, kPolyLayers, l, t, tw);
+      for (int k = tid; k < n; k += blockDim.x) s[k] = gf_mul(s[k], s[n + k]);
+      __syncthreads();
+      tile_layers_poly<true>(s, T, kPolyLayers, l, t, tw);
+    } else {
+      for (int k = tid; k < n; k += blockDim.x) s[k] = gf_mul(m8_mul_r(mb, s[k], q), m8_mul_r(mb, s[n + k], q));
+      __syncthreads();
+    }
     m8_expand(sm.tab, sm.rows_to_r, tid);
     __syncthreads();
     for (int k = tid; k < n; k += blockDim.x) s[k] = m8_mul_r(mb, s[k], q);
     // (tile_layers_r's first barrier orders these stores before its butterflies)
-    tile_layers_r<true, 1>(s, T, sm);
-    for (int k = tid; k < n; k += blockDim.x) g[k] = s[k];
+    tile_layers_r<true, 1>(s, T, kPolyLayers, sm);
+    for (int k = tid; k < n; k += blockDim.x) g[k] = s[tsw(k)];
     __syncthreads();
   }
 }

@@ -76,8 +76,18 @@ struct SmulTab {
   uint32_t lo0, lo1;  // M(0..3), M(4..7)
   uint32_t hi0, hi1;  // M(0x00, 0x10, 0x20, 0x30), M(0x40, 0x50, 0x60, 0x70)
   uint32_t m8, m80;   // M(0x08), M(0x80), replicated to 4 bytes
-  uint32_t pad0, pad1;
 };
+// Shared-memory layout: the four table words of d at a[d] (16 B: eight consecutive d of a
+// quarter-warp hit eight bank groups), the two sign-term words at b[d].
+struct SmulTabs {
+  uint4 a[128];
+  uint2 b[128];
+};
+__device__ __forceinline__ SmulTab smul_tab(const SmulTabs& t, int d) {
+  const uint4 a = t.a[d];
+  const uint2 b = t.b[d];
+  return SmulTab{a.x, a.y, a.z, a.w, b.x, b.y};
+}
 // PTX prmt in its default mode: a selector nibble with bit 3 set replicates the sign bit of the
 // selected byte (__byte_perm ignores that bit, so this needs the instruction itself).
 __device__ __forceinline__ uint32_t prmt_sign(uint32_t a, uint32_t sel) {
@@ -104,7 +114,7 @@ __device__ __forceinline__ uint32_t gf8_mul(uint32_t a, uint32_t b) {  // mod t^
   return r;
 }
 // Threads tid < 128 build the table of d = R(C2P(2 tid)) = sum over bits b of tid of tau byte b.
-__device__ __forceinline__ void smul_tabs_build(SmulTab* __restrict__ tabs, uint64_t tau, int tid) {
+__device__ __forceinline__ void smul_tabs_build(SmulTabs& tabs, uint64_t tau, int tid) {
   if (tid < 128) {
     uint32_t d = 0;
 #pragma unroll
@@ -120,9 +130,8 @@ __device__ __forceinline__ void smul_tabs_build(SmulTab* __restrict__ tabs, uint
     }
     t.m8 = gf8_mul(8, d) * 0x01010101u;
     t.m80 = gf8_mul(0x80, d) * 0x01010101u;
-    t.pad0 = d;
-    t.pad1 = 0;
-    tabs[tid] = t;
+    tabs.a[tid] = make_uint4(t.lo0, t.lo1, t.hi0, t.hi1);
+    tabs.b[tid] = make_uint2(t.m8, t.m80);
   }
 }
 
