@@ -502,7 +502,9 @@ def main():
         achieved = nbytes / stages[dom] / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "peak_source": peak_kind}
-    roof["kernel"] = {"pointwise": "fft_tile_fused2_kernel" if fab else "fft_tile_fused_kernel",
+    tower = fab and os.environ.get("FPM_TOWER", "1") != "0"  # tower-representation tile pass (k_fft.cu)
+    roof["kernel"] = {"pointwise": ("fft_tile_tower_kernel" if tower else "fft_tile_fused2_kernel") if fab
+                      else "fft_tile_fused_kernel",
                       "butterfly": "fft_top4_kernel" if fab else "fft_top4_kernel + fft_tile_kernel",
                       "ibutterfly": "fft_top4_kernel<inverse>"}.get(dom, dom)
     roof["stage"] = dom

@@ -13,9 +13,10 @@ import os
 import subprocess
 import sys
 
-STAGE_OF = [("fft_tile_fused_kernel", "pointwise"), ("fft_tile_fused2_kernel", "pointwise"), ("fft_top4_kernel<1>", "ibutterfly"),
-            ("fft_top_kernel<1>", "ibutterfly"), ("fft_top4_kernel<0>", "butterfly"),
-            ("fft_top_kernel<0>", "butterfly"), ("fft_tile_kernel<0>", "butterfly"),
+STAGE_OF = [("fft_tile_fused_kernel", "pointwise"), ("fft_tile_fused2_kernel", "pointwise"),
+            ("fft_tile_tower_kernel", "pointwise"), ("fft_top4_kernel<1", "ibutterfly"),
+            ("fft_top_kernel<1", "ibutterfly"), ("fft_top4_kernel<0", "butterfly"),
+            ("fft_top_kernel<0", "butterfly"), ("fft_tile_kernel<0>", "butterfly"),
             ("encode_kernel", "encode"), ("decode_kernel", "decode")]
 
 
