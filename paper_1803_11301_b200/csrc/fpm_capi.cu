@@ -205,11 +205,13 @@ struct Gf64Ops {
   static constexpr int kLiveRows = 32;
   static Tw twiddles(int dev, unsigned l) { return make_twiddle_src64(dev, l, partition_base64(l)); }
   static unsigned tile_log2(unsigned l) { return pipeline64_tile_log2(l); }
-  static bool tower(unsigned) { return false; }
-  static void encode(const uint32_t* p, unsigned l, E* ev, cudaStream_t s, bool) { encode64_device(p, l, ev, kLiveRows, s); }
-  static void decode(const E* ev, unsigned l, uint32_t* p, cudaStream_t s, bool) { decode64_device(ev, l, p, s); }
-  static void top(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s, bool) {
-    butterfly64_top_device(ev, l, T, inv, tw, s);
+  static bool tower(unsigned T) { return tile64_fused2_enabled(T) && tile64_tower_enabled(T); }
+  static void encode(const uint32_t* p, unsigned l, E* ev, cudaStream_t s, bool r) {
+    encode64_device(p, l, ev, kLiveRows, s, r);
+  }
+  static void decode(const E* ev, unsigned l, uint32_t* p, cudaStream_t s, bool r) { decode64_device(ev, l, p, s, r); }
+  static void top(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s, bool r) {
+    butterfly64_top_device(ev, l, T, inv, tw, s, r);
   }
   static void tile(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s) {
     butterfly64_tile_device(ev, l, T, inv, tw, s);
@@ -218,8 +220,9 @@ struct Gf64Ops {
     butterfly64_tile_fused_device(ea, eb, l, T, tw, s);
   }
   static bool fuse_ab(unsigned T) { return tile64_fused2_enabled(T); }
-  static void fused2(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s, bool) {
-    butterfly64_tile_fused2_device(ea, eb, l, T, tw, s);
+  static void fused2(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s, bool r) {
+    if (r) butterfly64_tile_tower_device(ea, eb, l, T, tw, s);
+    else butterfly64_tile_fused2_device(ea, eb, l, T, tw, s);
   }
 };
 
@@ -474,6 +477,31 @@ const DeviceTables& device_tables(int dev) {
       c2p64[part * 512 + e] = u2(acc);
     }
   for (int j = 0; j < 64; ++j) { rows64[j] = u2(f64.enc_rows[j].lo); inv64[j] = u2(f64.inv_rows[j].lo); }
+  // GF(2^64) tower representation: encode writes R, decode reads R (cf. the GF(2^128) tables)
+  const TowerTables& t64 = tower_tables64();
+  std::vector<uint2> to_r64(64), to_poly64(64), enc64r(4096), dec64r(4096);
+  uint64_t enc_r[64], inv_r[64];
+  for (int k = 0; k < 64; ++k) {
+    to_r64[k] = u2(t64.to_r[k].lo);
+    to_poly64[k] = u2(t64.to_poly[k].lo);
+    uint64_t e = 0, d = 0;
+    for (int m = 0; m < 64; ++m) {
+      if (f64.enc_rows[k].lo >> m & 1) e ^= t64.to_r[m].lo;
+      if (t64.to_poly[k].lo >> m & 1) d ^= f64.inv_rows[m].lo;
+    }
+    enc_r[k] = e;
+    inv_r[k] = d;
+  }
+  for (int c = 0; c < 8; ++c)
+    for (int v = 0; v < 256; ++v) {
+      uint64_t e = 0, d = 0;
+      for (int j = 0; j < 8; ++j)
+        if (v >> j & 1) { e ^= enc_r[8 * c + j]; d ^= inv_r[8 * c + j]; }
+      for (int h = 0; h < 2; ++h) {
+        enc64r[v * 16 + 8 * h + c] = u2(e);
+        dec64r[v * 16 + 8 * h + c] = u2(d);
+      }
+    }
   int prev;
   FPM_CUDA(cudaGetDevice(&prev));
   FPM_CUDA(cudaSetDevice(dev));
@@ -491,6 +519,7 @@ const DeviceTables& device_tables(int dev) {
     FPM_CUDA(cudaMemcpy(*dst, v.data(), v.size() * sizeof(uint2), cudaMemcpyHostToDevice));
   };
   up2(&t.enc_g8, enc64); up2(&t.dec_g8, dec64); up2(&t.c2p64, c2p64); up2(&t.rows64, rows64); up2(&t.inv64, inv64);
+  up2(&t.to_r64, to_r64); up2(&t.to_poly64, to_poly64); up2(&t.enc_g8r, enc64r); up2(&t.dec_g8r, dec64r);
   // Keep freed pool memory cached: the pipeline allocates its scratch per call (reentrant).
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {

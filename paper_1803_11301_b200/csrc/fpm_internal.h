@@ -86,6 +86,11 @@ struct DeviceTables {
   uint2* c2p64 = nullptr;     // 4 x 512, as c2p
   uint2* rows64 = nullptr;    // 64 x r_j
   uint2* inv64 = nullptr;     // 64 rows of E^{-1}
+  // GF(2^64) tower representation (fpm_tables.h tower_tables64): as the GF(2^128) fields above
+  uint2* to_r64 = nullptr;
+  uint2* to_poly64 = nullptr;
+  uint2* enc_g8r = nullptr;
+  uint2* dec_g8r = nullptr;
 };
 
 // Twiddle generator inputs (passed by value as a kernel parameter):
@@ -103,6 +108,9 @@ struct TwiddleSrc {
 TwiddleSrc make_twiddle_src(int device, unsigned l, U128 base);
 struct TwiddleSrc64 {
   const uint2* c2p;
+  const uint2* to_r;     // DeviceTables::to_r64
+  const uint2* to_poly;  // DeviceTables::to_poly64
+  uint64_t tau;          // tower_tables64().tau
   uint2 layer[kMaxLayers];
 };
 TwiddleSrc64 make_twiddle_src64(int device, unsigned l, uint64_t base);
@@ -169,14 +177,19 @@ void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigne
 // GF(2^64) stages (k_fft64.cu, k_codec.cu): 64-row partition matrix, 8-byte elements.
 unsigned fft64_tile_log2(unsigned l);
 void butterfly64_device(uint2* ev, unsigned l, uint64_t base, bool inverse, cudaStream_t s);
-void butterfly64_top_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s);
+void butterfly64_top_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s,
+                            bool tower = false);
+bool tile64_tower_enabled(unsigned T);
+void butterfly64_tile_tower_device(const uint2* ea, uint2* eb, unsigned l, unsigned T, const TwiddleSrc64& tw,
+                                   cudaStream_t s);
 void butterfly64_tile_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s);
 void butterfly64_tile_fused_device(const uint2* ea, uint2* eb, unsigned l, unsigned T, const TwiddleSrc64& tw,
                                    cudaStream_t s);
 void pointwise64_device(const uint2* u, const uint2* v, uint2* out, size_t n, cudaStream_t s);
 // rows_live = 32: rows >= 32 known zero (pipeline operands); 64: general.
-void encode64_device(const uint32_t* poly, unsigned l, uint2* ev, int rows_live, cudaStream_t s);
-void decode64_device(const uint2* ev, unsigned l, uint32_t* poly, cudaStream_t s);
+// tower: elements in the GF(2^64) tower representation (product pipeline; n_p >= 1024).
+void encode64_device(const uint32_t* poly, unsigned l, uint2* ev, int rows_live, cudaStream_t s, bool tower = false);
+void decode64_device(const uint2* ev, unsigned l, uint32_t* poly, cudaStream_t s, bool tower = false);
 
 // Whole small products in one CTA each (k_batch.cu); n_bits = padded product length <= 2^17.
 // Carry-less word product out[0 .. wa + wb) = a * b (k_clmul.cu; polymul.cpp:156-183, 268-282).

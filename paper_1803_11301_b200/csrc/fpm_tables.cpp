@@ -141,11 +141,12 @@ const FieldTables& field_tables64() {
 }
 
 namespace {
-void build_tower(TowerTables& tt) {
-  const FieldTables& f = field_tables();
-  auto pw = [](U128 a, int e) {
+void build_tower(TowerTables& tt, unsigned m) {
+  const FieldTables& f = m == 128 ? field_tables() : field_tables64();
+  auto mul = [m](U128 a, U128 b) { return m == 128 ? host_gf128_mul(a, b) : host_gf64_mul(a, b); };
+  auto pw = [&](U128 a, int e) {
     U128 r = unit(0);
-    for (int k = 0; k < e; ++k) r = host_gf128_mul(r, a);
+    for (int k = 0; k < e; ++k) r = mul(r, a);
     return r;
   };
   bool found = false;
@@ -153,21 +154,21 @@ void build_tower(TowerTables& tt) {
     U128 e;
     for (unsigned b = 0; b < 8; ++b)
       if (v >> b & 1) e = x(e, f.cantor[b]);
-    const U128 m = x(x(x(pw(e, 8), pw(e, 4)), x(pw(e, 3), e)), unit(0));  // e^8 + e^4 + e^3 + e + 1
-    if (!nz(m)) { tt.t = e; found = true; }
+    const U128 r = x(x(x(pw(e, 8), pw(e, 4)), x(pw(e, 3), e)), unit(0));  // e^8 + e^4 + e^3 + e + 1
+    if (!nz(r)) { tt.t = e; found = true; }
   }
   if (!found) throw std::runtime_error("tower: no root of y^8+y^4+y^3+y+1 in span(v_0..v_7)");
   U128 ts[8];
   ts[0] = unit(0);
-  for (int s = 1; s < 8; ++s) ts[s] = host_gf128_mul(ts[s - 1], tt.t);
+  for (int s = 1; s < 8; ++s) ts[s] = mul(ts[s - 1], tt.t);
   U128 xj = unit(0);
-  for (int j = 0; j < 16; ++j) {
-    for (int s = 0; s < 8; ++s) tt.to_poly[8 * j + s] = host_gf128_mul(xj, ts[s]);
-    xj = host_gf128_mul(xj, unit(1));
+  for (unsigned j = 0; j < m / 8; ++j) {
+    for (int s = 0; s < 8; ++s) tt.to_poly[8 * j + s] = mul(xj, ts[s]);
+    xj = mul(xj, unit(1));
   }
-  if (!invert(tt.to_poly, tt.to_r, 128)) throw std::runtime_error("tower: x^j t^s is not a basis");
+  if (!invert(tt.to_poly, tt.to_r, m)) throw std::runtime_error("tower: x^j t^s is not a basis");
   for (int b = 0; b < 8; ++b) {
-    const U128 r = row_mul(f.cantor[b < 7 ? b + 1 : 0], tt.to_r);
+    const U128 r = row_mul(f.cantor[b < 7 ? b + 1 : 0], tt.to_r, m);
     if (r.hi || (r.lo >> 8)) throw std::runtime_error("tower: Cantor subfield element outside GF(2^8)");
     tt.tau[b] = b < 7 ? (uint8_t)r.lo : 0;
   }
@@ -177,7 +178,13 @@ void build_tower(TowerTables& tt) {
 const TowerTables& tower_tables() {
   static TowerTables tables;
   static std::once_flag once;
-  std::call_once(once, [] { build_tower(tables); });
+  std::call_once(once, [] { build_tower(tables, 128); });
+  return tables;
+}
+const TowerTables& tower_tables64() {
+  static TowerTables tables;
+  static std::once_flag once;
+  std::call_once(once, [] { build_tower(tables, 64); });
   return tables;
 }
 U128 host_to_r(U128 poly) { return row_mul(poly, tower_tables().to_r); }

@@ -38,6 +38,8 @@ struct TowerTables {
   uint8_t tau[8];     // tau[b] = R byte 0 of v_{b+1} (b < 7): C2P(2d) for d < 128 is byte sum_b d_b tau[b]
 };
 const TowerTables& tower_tables();
+// The same for GF(2^64) (8 coordinates, basis x^j t^s, j < 8): entries 0..63 used, hi words zero.
+const TowerTables& tower_tables64();
 U128 host_to_r(U128 poly);
 U128 host_from_r(U128 r);
 

@@ -63,9 +63,8 @@ constexpr int kG8Rows = 72;     // 64 rows, row k at k + k/8 (conflict-free row 
 
 // Build by exactly 256 threads (thread c = tid & 7, s = tid >> 3 writes v = 8s .. 8s+7 of chunk c);
 // rows_scratch: kG8Rows uint2 of shared memory.  Ends with a barrier.
-__device__ __forceinline__ void g8_build(uint2* __restrict__ tab, uint2* __restrict__ rows_scratch, uint2 w, int tid) {
-  if (tid < 64) rows_scratch[tid + (tid >> 3)] = gf64_mul_xk(w, (unsigned)tid);
-  __syncthreads();
+// Expansion of the 64 rows (rows_scratch[k + k/8]) into the table; exactly 256 threads.
+__device__ __forceinline__ void g8_expand(uint2* __restrict__ tab, const uint2* __restrict__ rows_scratch, int tid) {
   const int c = tid & 7, s = tid >> 3;
   uint2 r[8];
 #pragma unroll
@@ -83,6 +82,12 @@ __device__ __forceinline__ void g8_build(uint2* __restrict__ tab, uint2* __restr
     e[0] = t[u];
     e[8] = t[u];
   }
+}
+
+__device__ __forceinline__ void g8_build(uint2* __restrict__ tab, uint2* __restrict__ rows_scratch, uint2 w, int tid) {
+  if (tid < 64) rows_scratch[tid + (tid >> 3)] = gf64_mul_xk(w, (unsigned)tid);
+  __syncthreads();
+  g8_expand(tab, rows_scratch, tid);
   __syncthreads();
 }
 

@@ -385,12 +385,13 @@ void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaSt
   FPM_LAUNCH_CHECK();
 }
 
-void encode64_device(const uint32_t* poly, unsigned l, uint2* ev, int rows_live, cudaStream_t s) {
+void encode64_device(const uint32_t* poly, unsigned l, uint2* ev, int rows_live, cudaStream_t s, bool tower) {
   int dev;
   FPM_CUDA(cudaGetDevice(&dev));
   const DeviceTables& dt = device_tables(dev);
   const uint64_t n_p = (uint64_t)1 << l;
   if (n_p < 1024) {
+    if (tower) throw Error(kInvalid, "encode64: the tower representation needs n_p >= 1024");
     encode64_small_kernel<<<(unsigned)((n_p + 127) / 128), 128, 0, s>>>(poly, n_p, dt.rows64, ev);
     FPM_LAUNCH_CHECK();
     return;
@@ -398,20 +399,21 @@ void encode64_device(const uint32_t* poly, unsigned l, uint2* ev, int rows_live,
   const uint64_t nslabs = n_p / 32 / kSlabWords;
   if (rows_live <= 32) {
     const size_t smem = kG8Uint2 * sizeof(uint2) + 32 * kPad * sizeof(uint32_t);
-    encode64_kernel<32><<<resident_grid(encode64_kernel<32>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, nslabs, dt.enc_g8, ev);
+    encode64_kernel<32><<<resident_grid(encode64_kernel<32>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, nslabs, tower ? dt.enc_g8r : dt.enc_g8, ev);
   } else {
     const size_t smem = kG8Uint2 * sizeof(uint2) + 64 * kPad * sizeof(uint32_t);
-    encode64_kernel<64><<<resident_grid(encode64_kernel<64>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, nslabs, dt.enc_g8, ev);
+    encode64_kernel<64><<<resident_grid(encode64_kernel<64>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, nslabs, tower ? dt.enc_g8r : dt.enc_g8, ev);
   }
   FPM_LAUNCH_CHECK();
 }
 
-void decode64_device(const uint2* ev, unsigned l, uint32_t* poly, cudaStream_t s) {
+void decode64_device(const uint2* ev, unsigned l, uint32_t* poly, cudaStream_t s, bool tower) {
   int dev;
   FPM_CUDA(cudaGetDevice(&dev));
   const DeviceTables& dt = device_tables(dev);
   const uint64_t n_p = (uint64_t)1 << l;
   if (n_p < 1024) {
+    if (tower) throw Error(kInvalid, "decode64: the tower representation needs n_p >= 1024");
     const uint64_t nwords = (64 * n_p + 31) / 32;
     decode64_small_kernel<<<(unsigned)((nwords + 127) / 128), 128, 0, s>>>(ev, n_p, dt.inv64, poly);
     FPM_LAUNCH_CHECK();
@@ -419,7 +421,7 @@ void decode64_device(const uint2* ev, unsigned l, uint32_t* poly, cudaStream_t s
   }
   const uint64_t nslabs = n_p / 32 / kSlabWords;
   const size_t smem = kG8Uint2 * sizeof(uint2) + 64 * kPad * sizeof(uint32_t);
-  decode64_kernel<<<resident_grid(decode64_kernel, 256, smem, nslabs), 256, smem, s>>>(ev, nslabs, n_p / 32, dt.dec_g8, poly);
+  decode64_kernel<<<resident_grid(decode64_kernel, 256, smem, nslabs), 256, smem, s>>>(ev, nslabs, n_p / 32, tower ? dt.dec_g8r : dt.dec_g8, poly);
   FPM_LAUNCH_CHECK();
 }
 

@@ -531,7 +531,10 @@ size_t tower_smem(unsigned T) { return 2 * ((size_t)1 << T) * sizeof(uint4) + si
 // fft_tile_fused2_kernel on R tiles: forward layers [0, T) of both operands (one table per layer
 // serves both tiles), the pointwise product (R -> poly by an M8 table of to_poly, gf_mul, poly -> R
 // by an M8 table of to_r) and the inverse layers [0, T).
-__global__ void __launch_bounds__(kTowerThreads, 512 / kTowerThreads) fft_tile_tower_kernel(const uint4* __restrict__ ea,
+#ifndef FPM_TOWER_MINB
+#define FPM_TOWER_MINB 2
+#endif
+__global__ void __launch_bounds__(kTowerThreads, FPM_TOWER_MINB) fft_tile_tower_kernel(const uint4* __restrict__ ea,
                                                                           uint4* __restrict__ eb, unsigned l,
                                                                           unsigned T, TwiddleSrc tw) {
   extern __shared__ uint4 s[];

@@ -17,6 +17,7 @@
 
 #include "fpm_internal.h"
 #include "gf64.cuh"
+#include "tower.cuh"
 
 namespace fpm {
 namespace {
@@ -36,14 +37,25 @@ __device__ __forceinline__ uint2 twiddle64(const TwiddleSrc64& tw, unsigned i, u
 }
 
 // ------------------------------------------------------------------ one top layer
-template <bool INV>
+// R: elements in the tower representation (tower.cuh), the table built in R.
+template <bool INV, bool R>
 __global__ void __launch_bounds__(256) fft64_top_kernel(uint2* __restrict__ ev, unsigned i, int ppc, TwiddleSrc64 tw) {
   extern __shared__ uint2 tab64[];  // kG8Uint2
   __shared__ uint2 rows[kG8Rows];
+  __shared__ uint2 to_r[72];
   const uint64_t half = (uint64_t)1 << i;
   const uint64_t pair0 = (uint64_t)blockIdx.x * ppc;  // ppc <= 2^i: a CTA stays inside one block
   const uint64_t b = pair0 >> i;
-  g8_build(tab64, rows, twiddle64(tw, i, b), threadIdx.x);
+  if (R) {
+    if (threadIdx.x < 64) to_r[to_r64_pad(threadIdx.x)] = __ldg(tw.to_r + threadIdx.x);
+    __syncthreads();
+    rows_r64(rows, twiddle64(tw, i, b), threadIdx.x, to_r);
+    __syncthreads();
+    g8_expand(tab64, rows, threadIdx.x);
+    __syncthreads();
+  } else {
+    g8_build(tab64, rows, twiddle64(tw, i, b), threadIdx.x);
+  }
   const int lane = threadIdx.x & 31;
   uint2* base = ev + (b << (i + 1));
 #pragma unroll 4
@@ -66,9 +78,9 @@ __global__ void __launch_bounds__(256) fft64_top_kernel(uint2* __restrict__ ev, 
 // 384 threads (three 128-thread table builders), two CTAs per SM: one CTA's table build overlaps
 // the other's streaming.
 constexpr int kTop4Threads64 = 384;
-constexpr size_t kTop4Smem64 = (3 * (size_t)kG8Uint2 + 3 * kG8Rows) * sizeof(uint2);
+constexpr size_t kTop4Smem64 = (3 * (size_t)kG8Uint2 + 3 * kG8Rows + 72) * sizeof(uint2);  // + to_r (tower)
 
-template <bool INV>
+template <bool INV, bool R>
 __global__ void __launch_bounds__(kTop4Threads64, 2) fft64_top4_kernel(uint2* __restrict__ ev, unsigned i, int qpc,
                                                                        TwiddleSrc64 tw) {
   extern __shared__ uint2 sm64[];
@@ -76,15 +88,21 @@ __global__ void __launch_bounds__(kTop4Threads64, 2) fft64_top4_kernel(uint2* __
   uint2* t0a = sm64 + kG8Uint2;        // w(i, 2B)
   uint2* t0b = sm64 + 2 * kG8Uint2;    // w(i, 2B+1)
   uint2* rows = sm64 + 3 * kG8Uint2;   // 3 x kG8Rows
+  uint2* to_r = rows + 3 * kG8Rows;    // tower: conversion rows, to_r64_pad layout
   const uint64_t h = (uint64_t)1 << i;
   const uint64_t quad0 = (uint64_t)blockIdx.x * qpc;  // qpc <= h
   const uint64_t B = quad0 >> i;
   const int tid = threadIdx.x, grp = tid >> 7, lt = tid & 127;
+  if (R) {
+    if (tid < 64) to_r[to_r64_pad(tid)] = __ldg(tw.to_r + tid);
+    __syncthreads();
+  }
   {
     const uint2 w = grp == 0 ? twiddle64(tw, i + 1, B) : twiddle64(tw, i, 2 * B + (grp - 1));
     uint2* tab = sm64 + grp * kG8Uint2;
     uint2* rs = rows + grp * kG8Rows;
-    if (lt < 64) rs[lt + (lt >> 3)] = gf64_mul_xk(w, (unsigned)lt);
+    if (R) rows_r64(rs, w, lt, to_r);
+    else if (lt < 64) rs[lt + (lt >> 3)] = gf64_mul_xk(w, (unsigned)lt);
     __syncthreads();
     const int c = lt & 7;
     uint2 r[8];
@@ -334,6 +352,181 @@ __global__ void __launch_bounds__(256, 3) fft64_tile_fused2_kernel(const uint2* 
   }
 }
 
+// ------------------------------------------------------------------ tower-representation tiles
+// fft64_tile_fused2_kernel on tiles in the GF(2^64) tower representation (tower.cuh; the algebra
+// is k_fft.cu's fft_tile_tower_kernel): tile layers [P, T) as one G8 table per 128 blocks plus a
+// GF(2^8)-scalar product by byte permutes, layers [0, P), the pointwise product and the inverse
+// layers [0, P) in polynomial representation (gf64_mul), conversions by G8 tables of to_poly/to_r.
+__host__ __device__ constexpr int tower64_groups(unsigned T, unsigned i) {
+  return (1 << (T - 1 - i)) > 128 ? (1 << (T - 1 - i)) >> 7 : 1;
+}
+__host__ __device__ constexpr int tower64_tables(unsigned T) {
+  int n = 0;
+  for (unsigned i = 0; i < T; ++i) n += tower64_groups(T, i);
+  return n;
+}
+__device__ __forceinline__ int tower64_wz_index(unsigned T, unsigned i, int g) {
+  int k = 0;
+  for (unsigned u = 0; u < i; ++u) k += tower64_groups(T, u);
+  return k + g;
+}
+constexpr int kTower64MaxTables = tower64_tables(12);
+struct TowerSmem64 {  // after the 2^(T+1) tile elements
+  uint2 tab[kG8Uint2];
+  uint2 rows[2][kG8Rows];
+  uint2 to_r[72];              // rows_r64 conversion source, to_r64_pad layout
+  uint2 rows_to_r[kG8Rows];    // g8 rows of poly -> R
+  uint2 rows_to_poly[kG8Rows]; // g8 rows of R -> poly
+  uint2 wz[kTower64MaxTables]; // table twiddles of the current tile (layer-ascending, groups ascending)
+  SmulTabs stab;
+};
+// Tile element k at k ^ 15 [bit 4 of k]: a half-warp's 8-byte accesses at layers 0-3 reach 16
+// distinct bank pairs.
+__device__ __forceinline__ int tsw64(int k) { return k ^ (((k >> 4) & 1) * 15); }
+
+template <bool INV, int NT>
+__device__ __forceinline__ void tile_layers_r64(uint2* __restrict__ s, unsigned T, unsigned P, TowerSmem64& sm) {
+  const int npairs = 1 << (T - 1), n = 1 << T, tid = threadIdx.x, lane = tid & 31;
+  const int first = tower64_wz_index(T, P, 0), ntab = tower64_tables(T) - first;
+  auto wz_of = [&](int k) -> int {
+    if (INV) return first + k;
+    int kk = 0;
+    for (int i = (int)T - 1; i >= (int)P; --i) {
+      const int g = tower64_groups(T, (unsigned)i);
+      if (k < kk + g) return tower64_wz_index(T, (unsigned)i, k - kk);
+      kk += g;
+    }
+    return 0;
+  };
+  rows_r64(sm.rows[0], sm.wz[wz_of(0)], tid, sm.to_r);
+  __syncthreads();
+  g8_expand(sm.tab, sm.rows[0], tid);
+  __syncthreads();
+  int k = 0;
+  for (unsigned step = 0; step < T - P; ++step) {
+    const unsigned i = INV ? P + step : T - 1 - step;
+    const int nblk = npairs >> i;
+    const int lg = (nblk < 128 ? T - 1 : 7 + i);
+    for (int h = 0; h < nblk; h += 128, ++k) {
+      if (k + 1 < ntab) rows_r64(sm.rows[(k + 1) & 1], sm.wz[wz_of(k + 1)], tid, sm.to_r);
+      for (int pp = tid; pp < (NT << lg); pp += blockDim.x) {
+        const int p = pp & ((1 << lg) - 1), tt = pp >> lg;
+        const int blk = h + (p >> i), j = p & ((1 << i) - 1);
+        const int i0 = (blk << (i + 1)) + j + tt * n, i1 = i0 + (1 << i);
+        const int d = blk & 127;
+        uint2 u0 = s[tsw64(i0)], u1 = s[tsw64(i1)];
+        if (!INV) {
+          uint2 m = g8_mul(sm.tab, u1, lane);
+          if (d) m = x2(m, smul_t2(u1, smul_tab(sm.stab, d)));
+          u0 = x2(u0, m);
+          u1 = x2(u1, u0);
+        } else {
+          u1 = x2(u1, u0);
+          uint2 m = g8_mul(sm.tab, u1, lane);
+          if (d) m = x2(m, smul_t2(u1, smul_tab(sm.stab, d)));
+          u0 = x2(u0, m);
+        }
+        s[tsw64(i0)] = u0;
+        s[tsw64(i1)] = u1;
+      }
+      __syncthreads();
+      if (k + 1 < ntab) {
+        g8_expand(sm.tab, sm.rows[(k + 1) & 1], tid);
+        __syncthreads();
+      }
+    }
+  }
+}
+
+template <bool INV>
+__device__ __forceinline__ void tile_layers_poly64(uint2* __restrict__ s, unsigned T, unsigned P, uint64_t t,
+                                                   const TwiddleSrc64& tw) {
+  const int npairs = 1 << (T - 1), n = 1 << T;
+  for (unsigned step = 0; step < P; ++step) {
+    const unsigned i = INV ? step : P - 1 - step;
+    const uint2 Z = twiddle64(tw, i, t << (T - 1 - i));
+    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+      const int blk = p >> i, j = p & ((1 << i) - 1);
+      const int i0 = tsw64((blk << (i + 1)) + j), i1 = tsw64((blk << (i + 1)) + j + (1 << i));
+      const uint2 w = x2(Z, c2p2_64(tw.c2p, (uint64_t)blk));
+      if (!INV) {
+        const Gf64Prep wp = gf64_prep(w);
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+          uint2 u0 = s[i0 + tt * n], u1 = s[i1 + tt * n];
+          u0 = x2(u0, gf64_mul_prep(wp, u1));
+          u1 = x2(u1, u0);
+          s[i0 + tt * n] = u0;
+          s[i1 + tt * n] = u1;
+        }
+      } else {
+        uint2 u0 = s[i0], u1 = s[i1];
+        u1 = x2(u1, u0);
+        u0 = x2(u0, gf64_mul(w, u1));
+        s[i0] = u0;
+        s[i1] = u1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+#ifndef FPM_TOWER64_POLY
+#define FPM_TOWER64_POLY 2  // P = 1: 46.0 ms, 2: 45.34, 3: 45.39, 4: 45.86 (2^32-bit product)
+#endif
+constexpr unsigned kPolyLayers64 = FPM_TOWER64_POLY;
+size_t tower64_smem(unsigned T) { return 2 * ((size_t)1 << T) * sizeof(uint2) + sizeof(TowerSmem64); }
+
+__global__ void __launch_bounds__(256, 3) fft64_tile_tower_kernel(const uint2* __restrict__ ea, uint2* __restrict__ eb,
+                                                                  unsigned l, unsigned T, TwiddleSrc64 tw) {
+  extern __shared__ uint2 s64[];
+  const int n = 1 << T, tid = threadIdx.x, lane = tid & 31;
+  TowerSmem64& sm = *reinterpret_cast<TowerSmem64*>(s64 + 2 * n);
+  smul_tabs_build(sm.stab, tw.tau, tid);
+  if (tid < 64) {
+    sm.to_r[to_r64_pad(tid)] = __ldg(tw.to_r + tid);
+    sm.rows_to_r[tid + (tid >> 3)] = __ldg(tw.to_r + tid);
+    sm.rows_to_poly[tid + (tid >> 3)] = __ldg(tw.to_poly + tid);
+  }
+  const int ntab = tower64_tables(T);
+  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    uint2* g = eb + (t << T);
+    const uint2* ga = ea + (t << T);
+    for (int k = tid; k < ntab; k += blockDim.x) {
+      int i = 0, kk = k;
+      while (kk >= tower64_groups(T, (unsigned)i)) kk -= tower64_groups(T, (unsigned)i++);
+      sm.wz[k] = x2(twiddle64(tw, (unsigned)i, t << (T - 1 - i)), c2p2_64(tw.c2p, (uint64_t)kk << 7));
+    }
+    for (int k = tid; k < n; k += blockDim.x) {
+      s64[tsw64(k)] = ga[k];
+      s64[n + tsw64(k)] = g[k];
+    }
+    __syncthreads();
+    tile_layers_r64<false, 2>(s64, T, kPolyLayers64, sm);
+    g8_expand(sm.tab, sm.rows_to_poly, tid);
+    __syncthreads();
+    if (kPolyLayers64) {
+      for (int k = tid; k < 2 * n; k += blockDim.x) s64[k] = g8_mul(sm.tab, s64[k], lane);
+      __syncthreads();
+      tile_layers_poly64<false>(s64, T, kPolyLayers64, t, tw);
+      for (int k = tid; k < n; k += blockDim.x) s64[k] = gf64_mul(s64[k], s64[n + k]);
+      __syncthreads();
+      tile_layers_poly64<true>(s64, T, kPolyLayers64, t, tw);
+    } else {
+      for (int k = tid; k < n; k += blockDim.x)
+        s64[k] = gf64_mul(g8_mul(sm.tab, s64[k], lane), g8_mul(sm.tab, s64[n + k], lane));
+      __syncthreads();
+    }
+    g8_expand(sm.tab, sm.rows_to_r, tid);
+    __syncthreads();
+    for (int k = tid; k < n; k += blockDim.x) s64[k] = g8_mul(sm.tab, s64[k], lane);
+    tile_layers_r64<true, 1>(s64, T, kPolyLayers64, sm);
+    for (int k = tid; k < n; k += blockDim.x) g[k] = s64[tsw64(k)];
+    __syncthreads();
+  }
+}
+
 __global__ void pointwise64_kernel(const uint2* __restrict__ u, const uint2* __restrict__ v, uint2* __restrict__ out,
                                    uint64_t n) {
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
@@ -411,10 +604,35 @@ void butterfly64_tile_fused2_device(const uint2* ea, uint2* eb, unsigned l, unsi
   FPM_LAUNCH_CHECK();
 }
 
+// The tower tile pass for the GF(2^64) product pipeline (FPM_TOWER=0 disables it, as for GF(2^128)).
+bool tile64_tower_enabled(unsigned T) {
+  static const bool on = [] {
+    const char* e = std::getenv("FPM_TOWER");
+    return !(e && e[0] == '0');
+  }();
+  return on && T >= 10 && T <= 12;
+}
+
+void butterfly64_tile_tower_device(const uint2* ea, uint2* eb, unsigned l, unsigned T, const TwiddleSrc64& tw,
+                                   cudaStream_t s) {
+  if (T < 10 || T > 12 || l < T) throw Error(kInvalid, "tower tile pass (GF(2^64)): T must be 10..12");
+  static PerDeviceOnce attr;
+  attr.run([&] { set_smem64(fft64_tile_tower_kernel, tower64_smem(12)); });
+  const size_t smem = tower64_smem(T);
+  const int grid = resident_grid(fft64_tile_tower_kernel, 256, smem, ((uint64_t)1 << l) >> T);
+  fft64_tile_tower_kernel<<<grid, 256, smem, s>>>(ea, eb, l, T, tw);
+  FPM_LAUNCH_CHECK();
+}
+
 TwiddleSrc64 make_twiddle_src64(int device, unsigned l, uint64_t base) {
   if (l > (unsigned)kMaxLayers) throw Error(kInvalid, "butterfly: too many layers");
   TwiddleSrc64 tw{};
-  tw.c2p = device_tables(device).c2p64;
+  const DeviceTables& dt = device_tables(device);
+  tw.c2p = dt.c2p64;
+  tw.to_r = dt.to_r64;
+  tw.to_poly = dt.to_poly64;
+  const TowerTables& tt = tower_tables64();
+  for (int b = 0; b < 8; ++b) tw.tau |= (uint64_t)tt.tau[b] << (8 * b);
   const FieldTables& ft = field_tables64();
   for (unsigned i = 0; i < l; ++i) {
     const U128 p = host_cantor_to_poly64(ft, base >> i);
@@ -423,15 +641,15 @@ TwiddleSrc64 make_twiddle_src64(int device, unsigned l, uint64_t base) {
   return tw;
 }
 
-void butterfly64_top_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s) {
-  if (l <= T) return;
+template <bool R>
+void top_passes64(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s) {
   const size_t smem = kG8Uint2 * sizeof(uint2);
   static PerDeviceOnce attr;
   attr.run([&] {
-    set_smem64(fft64_top_kernel<false>, smem);
-    set_smem64(fft64_top_kernel<true>, smem);
-    set_smem64(fft64_top4_kernel<false>, kTop4Smem64);
-    set_smem64(fft64_top4_kernel<true>, kTop4Smem64);
+    set_smem64(fft64_top_kernel<false, R>, smem);
+    set_smem64(fft64_top_kernel<true, R>, smem);
+    set_smem64(fft64_top4_kernel<false, R>, kTop4Smem64);
+    set_smem64(fft64_top4_kernel<true, R>, kTop4Smem64);
   });
   if (T < 8) throw Error(kInvalid, "butterfly_top: layer too small for the table layer kernel");
   const uint64_t pairs = ((uint64_t)1 << l) / 2;
@@ -439,8 +657,8 @@ void butterfly64_top_device(uint2* ev, unsigned l, unsigned T, bool inverse, con
   while (ppc > 256 && pairs / ppc < (uint64_t)sms64() * 2) ppc /= 2;
   auto radix2 = [&](unsigned i) {
     const uint64_t p = std::min<uint64_t>(ppc, (uint64_t)1 << i);
-    if (!inverse) fft64_top_kernel<false><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, i, (int)p, tw);
-    else fft64_top_kernel<true><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, i, (int)p, tw);
+    if (!inverse) fft64_top_kernel<false, R><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, i, (int)p, tw);
+    else fft64_top_kernel<true, R><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, i, (int)p, tw);
     FPM_LAUNCH_CHECK();
   };
   const uint64_t quads = ((uint64_t)1 << l) / 4;
@@ -449,9 +667,9 @@ void butterfly64_top_device(uint2* ev, unsigned l, unsigned T, bool inverse, con
   auto radix4 = [&](unsigned i) {
     const unsigned q = (unsigned)std::min<uint64_t>(qpc, (uint64_t)1 << i);
     if (!inverse)
-      fft64_top4_kernel<false><<<(unsigned)(quads / q), kTop4Threads64, kTop4Smem64, s>>>(ev, i, (int)q, tw);
+      fft64_top4_kernel<false, R><<<(unsigned)(quads / q), kTop4Threads64, kTop4Smem64, s>>>(ev, i, (int)q, tw);
     else
-      fft64_top4_kernel<true><<<(unsigned)(quads / q), kTop4Threads64, kTop4Smem64, s>>>(ev, i, (int)q, tw);
+      fft64_top4_kernel<true, R><<<(unsigned)(quads / q), kTop4Threads64, kTop4Smem64, s>>>(ev, i, (int)q, tw);
     FPM_LAUNCH_CHECK();
   };
   const unsigned n = l - T;
@@ -463,6 +681,13 @@ void butterfly64_top_device(uint2* ev, unsigned l, unsigned T, bool inverse, con
     if (odd) radix2(T);
     for (unsigned i = T + (odd ? 1 : 0); i + 1 < l; i += 2) radix4(i);
   }
+}
+
+void butterfly64_top_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s,
+                            bool tower) {
+  if (l <= T) return;
+  if (tower) top_passes64<true>(ev, l, T, inverse, tw, s);
+  else top_passes64<false>(ev, l, T, inverse, tw, s);
 }
 
 void butterfly64_tile_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s) {

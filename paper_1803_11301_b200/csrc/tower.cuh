@@ -12,6 +12,7 @@
 #include <cstdint>
 
 #include "gf128.cuh"
+#include "gf64.cuh"
 
 namespace fpm {
 
@@ -60,6 +61,35 @@ __device__ __forceinline__ void rows_r(uint4* __restrict__ rows, uint4 w, int ti
   rows[tid + (tid >> 3)] = acc;
 }
 
+// GF(2^64) (8 coordinates): rows of the G8 table of "multiply by w" (w polynomial) in R, row 8j+s =
+// R(w x^j) * t^s, by threads tid < 64 (two whole warps): thread (j, s) converts bits [8s, 8s+8) of
+// w x^j, shuffle-XOR over the 8 lanes of j, then s xtimes.  to_r: 64 rows at to_r64_pad(k)
+// (the 8 lanes s = 0..7 read 8 distinct bank pairs).  Writes rows[k + k/8].
+__device__ __forceinline__ int to_r64_pad(int k) { return k + (k >> 3); }
+__device__ __forceinline__ void rows_r64(uint2* __restrict__ rows, uint2 w, int tid, const uint2* __restrict__ to_r) {
+  if (tid >= 64) return;
+  const int j = tid >> 3, s = tid & 7;
+  const uint2 p = gf64_mul_xk(w, (unsigned)j);
+  const uint32_t bits = ((s < 4 ? p.x : p.y) >> (8 * (s & 3))) & 0xFFu;
+  uint2 acc = make_uint2(0, 0);
+  const uint2* src = to_r + to_r64_pad(8 * s);
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const uint32_t m = 0u - ((bits >> b) & 1u);
+    acc.x ^= src[b].x & m;
+    acc.y ^= src[b].y & m;
+  }
+#pragma unroll
+  for (int m = 1; m < 8; m <<= 1) {
+    acc.x ^= __shfl_xor_sync(0xffffffffu, acc.x, m);
+    acc.y ^= __shfl_xor_sync(0xffffffffu, acc.y, m);
+  }
+#pragma unroll
+  for (int r = 0; r < 7; ++r)
+    if (r < s) acc = make_uint2(xt32(acc.x), xt32(acc.y));
+  rows[tid + (tid >> 3)] = acc;
+}
+
 // Rows of a constant linear map (to_r / to_poly) into the m8 row scratch.
 __device__ __forceinline__ void rows_const(uint4* __restrict__ rows, const uint4* __restrict__ src, int tid) {
   if (tid < 128) rows[tid + (tid >> 3)] = __ldg(src + tid);
@@ -104,6 +134,7 @@ __device__ __forceinline__ uint32_t smul_w(uint32_t w, const SmulTab& t) {
 __device__ __forceinline__ uint4 smul_t(uint4 u, const SmulTab& t) {
   return make_uint4(smul_w(u.x, t), smul_w(u.y, t), smul_w(u.z, t), smul_w(u.w, t));
 }
+__device__ __forceinline__ uint2 smul_t2(uint2 u, const SmulTab& t) { return make_uint2(smul_w(u.x, t), smul_w(u.y, t)); }
 __device__ __forceinline__ uint32_t gf8_mul(uint32_t a, uint32_t b) {  // mod t^8 + t^4 + t^3 + t + 1
   uint32_t r = 0;
   for (int i = 0; i < 8; ++i) {
