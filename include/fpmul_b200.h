@@ -174,6 +174,14 @@ fpm_status fpm_pointwise64(const uint64_t* u, const uint64_t* v, uint64_t* out, 
 /* CantorField<gf64>::basis, EncodeMatrix<gf64> rows / inverse rows: 64 words each (host only). */
 fpm_status fpm_tables64(uint64_t* cantor, uint64_t* rows, uint64_t* inv_rows);
 
+/* Diagnostic, not a reference interface: the tower representation the product pipeline's FFT uses
+ * internally (paper_1803_11301_b200/csrc/tower.cuh) for field_degree 128 or 64 -- GF(2^m) as a
+ * vector space over its subfield GF(2^8) with basis x^j t^s.  t: 2 words; to_poly / to_r: m
+ * entries x 2 words (basis vector k in polynomial form / x^k in tower coordinates); tau: 8 bytes
+ * (tower byte 0 of Cantor basis vectors v_1..v_7).  Host only; lets the CPU tests check the
+ * construction against the oracle's field arithmetic. */
+fpm_status fpm_tower_tables(int field_degree, uint64_t* t, uint64_t* to_poly, uint64_t* to_r, uint8_t* tau);
+
 /* Number of kernel launches issued by this library on the calling thread since the last reset
  * (for the bench's gpu_launches accounting). */
 uint64_t fpm_launch_count(int reset);

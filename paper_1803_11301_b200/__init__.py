@@ -47,6 +47,7 @@ from ._lib import (  # noqa: F401
     pointwise_mul,
     stage_dev,
     tables128,
+    tower_tables,
 )
 
 __all__ = [n for n in dir() if not n.startswith("_")]

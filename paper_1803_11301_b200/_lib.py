@@ -70,6 +70,7 @@ def lib():
         L.fpm_gf128_mul.argtypes = [_u64p, _u64p, _u64p, sz, C.c_int]
         L.fpm_tables128.argtypes = [_u64p, _u64p, _u64p]
         L.fpm_tables64.argtypes = [_u64p, _u64p, _u64p]
+        L.fpm_tower_tables.argtypes = [C.c_int, _u64p, _u64p, _u64p, C.POINTER(C.c_uint8)]
         L.fpm_encode64.argtypes = [_u64p, C.c_uint, _u64p, C.c_int]
         L.fpm_decode64.argtypes = [_u64p, C.c_uint, _u64p, C.c_int]
         L.fpm_lch_butterfly64.argtypes = [_u64p, C.c_uint, C.c_uint64, C.c_int, C.c_int]
@@ -205,6 +206,17 @@ def tables64():
     out = [np.zeros(64, np.uint64) for _ in range(3)]
     _check(lib().fpm_tables64(*[_ptr(o) for o in out]))
     return tuple(out)
+
+
+def tower_tables(field_degree: int):
+    """(t, to_poly, to_r, tau) of the pipeline's internal tower representation (fpm_tower_tables):
+    t as 2 words, to_poly / to_r as (m, 2) word arrays, tau as 8 bytes.  Host only."""
+    t = np.zeros(2, np.uint64)
+    tp = np.zeros(2 * field_degree, np.uint64)
+    tr = np.zeros(2 * field_degree, np.uint64)
+    tau = np.zeros(8, np.uint8)
+    _check(lib().fpm_tower_tables(field_degree, _ptr(t), _ptr(tp), _ptr(tr), tau.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return t, tp.reshape(-1, 2), tr.reshape(-1, 2), tau
 
 
 def encode64(poly, l: int, device: int = 0) -> np.ndarray:

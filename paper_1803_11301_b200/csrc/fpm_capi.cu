@@ -587,6 +587,20 @@ fpm_status fpm_tables128(uint64_t* cantor, uint64_t* rows, uint64_t* inv_rows) {
   });
 }
 
+fpm_status fpm_tower_tables(int field_degree, uint64_t* t, uint64_t* to_poly, uint64_t* to_r, uint8_t* tau) {
+  return guard([&] {
+    if (field_degree != 128 && field_degree != 64) throw Error(kInvalid, "tower tables: field degree must be 128 or 64");
+    const TowerTables& tt = field_degree == 128 ? tower_tables() : tower_tables64();
+    if (t) { t[0] = tt.t.lo; t[1] = tt.t.hi; }
+    for (int k = 0; k < field_degree; ++k) {
+      if (to_poly) { to_poly[2 * k] = tt.to_poly[k].lo; to_poly[2 * k + 1] = tt.to_poly[k].hi; }
+      if (to_r) { to_r[2 * k] = tt.to_r[k].lo; to_r[2 * k + 1] = tt.to_r[k].hi; }
+    }
+    if (tau)
+      for (int b = 0; b < 8; ++b) tau[b] = tt.tau[b];
+  });
+}
+
 fpm_status fpm_polymul_dev(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_t b_bits, uint64_t* d_c,
                            int field, void* stream, double* stage_seconds) {
   return guard([&] {

@@ -68,3 +68,75 @@ def test_gf64_tables_host_side(port):
     if oracle.have_ref():
         rc, rr, ri = oracle.ref().tables64()
         assert np.array_equal(c, rc) and np.array_equal(r, rr) and np.array_equal(i, ri)
+
+
+@pytest.mark.parametrize("m", [128, 64])
+def test_tower_representation_host_side(port, m):
+    """The product pipeline's internal tower representation (csrc/tower.cuh; fpm_tower_tables):
+    GF(2^m) over its subfield GF(2^8) with basis x^j t^s.  Checked with the oracle port's field
+    arithmetic: t is a root of y^8+y^4+y^3+y+1 inside span(v_0..v_7), to_poly[8j+s] = x^j t^s,
+    to_r inverts it, tau are the tower coordinates of v_1..v_7, and multiplying by a subfield
+    element is the byte-wise GF(2^8) product in tower coordinates (what smul_w computes)."""
+    import paper_1803_11301_b200 as pkg
+    t, to_poly, to_r, tau = pkg.tower_tables(m)
+    mul = lambda a, b: port.pointwise(m, np.asarray(a, np.uint64), np.asarray(b, np.uint64))  # noqa: E731
+    one, x = np.array([1, 0], np.uint64), np.array([2, 0], np.uint64)
+
+    def pw(a, e):
+        r = one
+        for _ in range(e):
+            r = mul(r, a)
+        return r
+    assert not np.any(pw(t, 8) ^ pw(t, 4) ^ pw(t, 3) ^ t ^ one)
+    cantor = port.cantor_basis(m).reshape(-1, 2)
+
+    sub = {0}  # span(v_0..v_7) = GF(2^8)
+    for c in cantor[:8]:
+        sub |= {e ^ (int(c[0]) | int(c[1]) << 64) for e in sub}
+    assert len(sub) == 256 and (int(t[0]) | int(t[1]) << 64) in sub
+    xj = one
+    for j in range(m // 8):
+        ts = one
+        for s in range(8):
+            assert np.array_equal(to_poly[8 * j + s], ts if j == 0 else mul(xj, ts)), (j, s)
+            ts = mul(ts, t)
+        xj = mul(xj, x)
+
+    def conv(v, rows):  # row-vector times matrix over GF(2)
+        acc = np.zeros(2, np.uint64)
+        bits = int(v[0]) | int(v[1]) << 64
+        for k in range(m):
+            if bits >> k & 1:
+                acc ^= rows[k]
+        return acc
+    for k in range(m):
+        unit = np.zeros(2, np.uint64)
+        unit[k // 64] = np.uint64(1) << np.uint64(k % 64)
+        assert np.array_equal(conv(to_poly[k], to_r), unit)
+    for b in range(7):
+        r = conv(cantor[b + 1], to_r)
+        assert int(r[1]) == 0 and int(r[0]) == int(tau[b])
+
+    def gf8(a, b):
+        r = 0
+        for i in range(8):
+            if b >> i & 1:
+                r ^= a
+            a <<= 1
+            if a & 0x100:
+                a ^= 0x11B
+        return r
+    rng = np.random.default_rng(m)
+    for _ in range(8):
+        u = rng.integers(0, 2**63, 2, dtype=np.uint64)
+        if m == 64:
+            u[1] = 0
+        d = int(rng.integers(1, 128))
+        dpoly = np.zeros(2, np.uint64)
+        for b in range(7):
+            if d >> b & 1:
+                dpoly ^= cantor[b + 1]
+        ur = conv(u, to_r)
+        dr = int(conv(dpoly, to_r)[0])
+        want = bytes(gf8(c, dr) for c in ur.tobytes()[: m // 8])
+        assert conv(mul(u, dpoly), to_r).tobytes()[: m // 8] == want
