@@ -141,6 +141,20 @@ fpm_status fpm_decode_cols_dev(const uint64_t* d_ev, size_t ncols, uint64_t* d_s
  * twiddle for this block.  Forward: p0' = p0 + w p1, p1' = p1 + p0'; inverse undoes it. */
 fpm_status fpm_bfly_pair_dev(uint64_t* d_mine, const uint64_t* d_theirs, size_t n, const uint64_t* w, int side,
                              int inverse, void* stream);
+/* The same building blocks in the product pipeline's internal tower representation (tower.cuh),
+ * so that each rank's coset runs the single-GPU fast path: fpm_shard_tower(l) says whether a coset
+ * of 2^l elements takes it (l >= 18); encode/decode/pair as above but with tower-representation
+ * elements; fpm_shard_local_product_dev multiplies two encoded, exchanged cosets (base in Cantor
+ * coordinates: the partition base ^ the coset's first element): the local forward layers of both,
+ * the pointwise product and the local inverse layers, result in d_eb. */
+int fpm_shard_tower(unsigned l);
+fpm_status fpm_encode_cols_r_dev(const uint64_t* d_poly, unsigned l, size_t col0, size_t ncols, int rows_live,
+                                 uint64_t* d_ev, void* stream);
+fpm_status fpm_decode_cols_r_dev(const uint64_t* d_ev, size_t ncols, uint64_t* d_slice, void* stream);
+fpm_status fpm_bfly_pair_r_dev(uint64_t* d_mine, const uint64_t* d_theirs, size_t n, const uint64_t* w, int side,
+                               int inverse, void* stream);
+fpm_status fpm_shard_local_product_dev(uint64_t* d_ea, uint64_t* d_eb, unsigned l, const uint64_t* base,
+                                       void* stream);
 /* Host: the twiddle C2P((base >> i) ^ 2b) of layer i, block b (butterfly.cpp:45-49); base in
  * Cantor coordinates {lo, hi}; out = {lo, hi} polynomial representation. */
 fpm_status fpm_twiddle128(unsigned i, uint64_t b, const uint64_t* base, uint64_t* out);

@@ -81,6 +81,12 @@ def lib():
         L.fpm_decode_cols_dev.argtypes = [vp, sz, vp, vp]
         L.fpm_bfly_pair_dev.argtypes = [vp, vp, sz, _u64p, C.c_int, C.c_int, vp]
         L.fpm_twiddle128.argtypes = [C.c_uint, C.c_uint64, _u64p, _u64p]
+        L.fpm_shard_tower.argtypes = [C.c_uint]
+        L.fpm_shard_tower.restype = C.c_int
+        L.fpm_encode_cols_r_dev.argtypes = [vp, C.c_uint, sz, sz, C.c_int, vp, vp]
+        L.fpm_decode_cols_r_dev.argtypes = [vp, sz, vp, vp]
+        L.fpm_bfly_pair_r_dev.argtypes = [vp, vp, sz, _u64p, C.c_int, C.c_int, vp]
+        L.fpm_shard_local_product_dev.argtypes = [vp, vp, C.c_uint, _u64p, vp]
         L.fpm_karatsuba_mul.argtypes = [_u64p, sz, _u64p, sz, _u64p, C.c_int]
         L.fpm_clmul_words_dev.argtypes = [vp, sz, vp, sz, vp, vp]
         _LIB = L

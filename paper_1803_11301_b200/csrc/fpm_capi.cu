@@ -749,6 +749,65 @@ fpm_status fpm_decode_cols_dev(const uint64_t* d_ev, size_t ncols, uint64_t* d_s
   });
 }
 
+int fpm_shard_tower(unsigned l) {
+  const unsigned T = pipeline_tile_log2(l);
+  return l >= 18 && l < 64 && tile_fused2_enabled(T) && tile_tower_enabled(T) ? 1 : 0;
+}
+
+fpm_status fpm_encode_cols_r_dev(const uint64_t* d_poly, unsigned l, size_t col0, size_t ncols, int rows_live,
+                                 uint64_t* d_ev, void* stream) {
+  return guard([&] {
+    require_device();
+    if (l >= 64) throw Error(kInvalid, "PartitionSpec: l must satisfy l < m/2");
+    encode_cols_device(reinterpret_cast<const uint32_t*>(d_poly), l, col0, ncols, reinterpret_cast<uint4*>(d_ev),
+                       rows_live == 64 ? 64 : 128, (cudaStream_t)stream, true);
+  });
+}
+
+fpm_status fpm_decode_cols_r_dev(const uint64_t* d_ev, size_t ncols, uint64_t* d_slice, void* stream) {
+  return guard([&] {
+    require_device();
+    decode_cols_device(reinterpret_cast<const uint4*>(d_ev), ncols, reinterpret_cast<uint32_t*>(d_slice),
+                       (cudaStream_t)stream, true);
+  });
+}
+
+fpm_status fpm_bfly_pair_r_dev(uint64_t* d_mine, const uint64_t* d_theirs, size_t n, const uint64_t* w, int side,
+                               int inverse, void* stream) {
+  return guard([&] {
+    require_device();
+    if (!w || (side != 0 && side != 1)) throw Error(kInvalid, "bfly_pair: bad twiddle or side");
+    U128 t;
+    t.lo = w[0];
+    t.hi = w[1];
+    bfly_pair_device(reinterpret_cast<uint4*>(d_mine), reinterpret_cast<const uint4*>(d_theirs), n, t, side,
+                     inverse != 0, (cudaStream_t)stream, true);
+  });
+}
+
+fpm_status fpm_shard_local_product_dev(uint64_t* d_ea, uint64_t* d_eb, unsigned l, const uint64_t* base,
+                                       void* stream) {
+  return guard([&] {
+    require_device();
+    if (!base) throw Error(kInvalid, "local product: null base");
+    if (!fpm_shard_tower(l)) throw Error(kInvalid, "local product: the coset needs 2^18 or more elements");
+    int dev;
+    FPM_CUDA(cudaGetDevice(&dev));
+    U128 b;
+    b.lo = base[0];
+    b.hi = base[1];
+    const TwiddleSrc tw = make_twiddle_src(dev, l, b);
+    const unsigned T = pipeline_tile_log2(l);
+    const cudaStream_t s = (cudaStream_t)stream;
+    uint4* ea = reinterpret_cast<uint4*>(d_ea);
+    uint4* eb = reinterpret_cast<uint4*>(d_eb);
+    butterfly_top_device(ea, l, T, false, tw, s, true);
+    butterfly_top_device(eb, l, T, false, tw, s, true);
+    butterfly_tile_tower_device(ea, eb, l, T, tw, s);
+    butterfly_top_device(eb, l, T, true, tw, s, true);
+  });
+}
+
 fpm_status fpm_bfly_pair_dev(uint64_t* d_mine, const uint64_t* d_theirs, size_t n, const uint64_t* w, int side,
                              int inverse, void* stream) {
   return guard([&] {

@@ -586,13 +586,21 @@ __global__ void __launch_bounds__(kTowerThreads, FPM_TOWER_MINB) fft_tile_tower_
   }
 }
 
-// Exchanged layer of the sharded FFT: all local elements share one twiddle w.
-template <bool INV>
+// Exchanged layer of the sharded FFT: all local elements share one twiddle w (polynomial form);
+// R: elements in the tower representation (table built in R).
+template <bool INV, bool R>
 __global__ void __launch_bounds__(256) fft_pair_kernel(uint4* __restrict__ mine, const uint4* __restrict__ theirs,
-                                                       uint64_t n, uint4 w, int side, int ppc) {
+                                                       uint64_t n, uint4 w, int side, int ppc, const uint4* to_r) {
   extern __shared__ uint4 tab[];
   __shared__ uint4 rows[144];
-  m8_build(tab, rows, w, threadIdx.x);
+  if (R) {
+    rows_r<false>(rows, w, threadIdx.x, to_r);
+    __syncthreads();
+    m8_expand(tab, rows, threadIdx.x);
+    __syncthreads();
+  } else {
+    m8_build(tab, rows, w, threadIdx.x);
+  }
   const int copy = threadIdx.x & 7;
   const uint64_t k0 = (uint64_t)blockIdx.x * ppc;
   for (int k = threadIdx.x; k < ppc; k += blockDim.x) {
@@ -833,17 +841,31 @@ void butterfly_device(uint4* ev, unsigned l, U128 base, bool inverse, cudaStream
   }
 }
 
-void bfly_pair_device(uint4* mine, const uint4* theirs, uint64_t n, U128 w, int side, bool inverse, cudaStream_t s) {
+void bfly_pair_device(uint4* mine, const uint4* theirs, uint64_t n, U128 w, int side, bool inverse, cudaStream_t s,
+                      bool tower) {
   if (!n) return;
   const size_t smem = kM8Uint4 * sizeof(uint4);
   static PerDeviceOnce attr;
-  attr.run([&] { set_smem(fft_pair_kernel<false>, smem); set_smem(fft_pair_kernel<true>, smem); });
+  attr.run([&] {
+    set_smem(fft_pair_kernel<false, false>, smem);
+    set_smem(fft_pair_kernel<true, false>, smem);
+    set_smem(fft_pair_kernel<false, true>, smem);
+    set_smem(fft_pair_kernel<true, true>, smem);
+  });
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  const uint4* to_r = device_tables(dev).to_r;
   uint64_t ppc = 4096;
   while (ppc > 256 && n / ppc < (uint64_t)sms() * 2) ppc /= 2;
   const unsigned ctas = (unsigned)((n + ppc - 1) / ppc);
   const uint4 w4 = make_uint4((uint32_t)w.lo, (uint32_t)(w.lo >> 32), (uint32_t)w.hi, (uint32_t)(w.hi >> 32));
-  if (!inverse) fft_pair_kernel<false><<<ctas, 256, smem, s>>>(mine, theirs, n, w4, side, (int)ppc);
-  else fft_pair_kernel<true><<<ctas, 256, smem, s>>>(mine, theirs, n, w4, side, (int)ppc);
+  if (tower) {
+    if (!inverse) fft_pair_kernel<false, true><<<ctas, 256, smem, s>>>(mine, theirs, n, w4, side, (int)ppc, to_r);
+    else fft_pair_kernel<true, true><<<ctas, 256, smem, s>>>(mine, theirs, n, w4, side, (int)ppc, to_r);
+  } else {
+    if (!inverse) fft_pair_kernel<false, false><<<ctas, 256, smem, s>>>(mine, theirs, n, w4, side, (int)ppc, to_r);
+    else fft_pair_kernel<true, false><<<ctas, 256, smem, s>>>(mine, theirs, n, w4, side, (int)ppc, to_r);
+  }
   FPM_LAUNCH_CHECK();
 }
 

@@ -13,6 +13,11 @@ SURVEY.md 8(e): rank g of P owns elements [g*m, (g+1)*m), m = n_p / P, of every 
 * decode: local columns -> a 128 x m-bit slice; all_gather + column interleave -> the n-bit
   product array; inverse basis conversion (replicated); trim.
 
+Cosets of 2^18 or more elements take the single-GPU fast path (backend.tower(l') true): operands
+encoded straight into the tower representation, exchanged layers on tower tables, and the local
+forward layers of both operands + pointwise product + local inverse layers as ONE call
+(local_product: the radix-4 top passes and the fused tower tile pass of k_fft.cu).
+
 Exchange volume per top layer: m * 16 B per rank (config 5, P = 8: 128 MiB).  The compute goes
 through a `backend` (GpuBackend here: the CUDA C-ABI; the gloo CPU tests plug in an oracle
 backend), so the partition / exchange logic is one piece of code tested on CPU and run on GPUs.
@@ -86,21 +91,27 @@ def polymul_sharded(a, a_bits: int, b, b_bits: int, backend, plan: ShardPlan | N
     every rank returns the full product words."""
     P, rank = backend.world()
     plan = plan or make_plan(a_bits, b_bits, P, rank)
+    r = hasattr(backend, "tower") and backend.tower(plan.lp)           # coset on the fast path
+    kw = {"tower": True} if r else {}
     evs = []
     for x, bits in ((a, a_bits), (b, b_bits)):
         poly = backend.convert_operand(x, bits, plan.n_bits)          # basis_cvt, replicated
-        ev = backend.encode_cols(poly, plan.l, plan.col0, plan.m)      # local columns
+        ev = backend.encode_cols(poly, plan.l, plan.col0, plan.m, **kw)  # local columns
         for i in plan.top_layers(inverse=False):                       # exchanged layers
             theirs = backend.exchange(ev, plan.partner(i))
-            backend.pair(ev, theirs, backend.twiddle(i, plan.block(i), plan.base), plan.side(i), inverse=False)
-        backend.butterfly(ev, plan.lp, plan.base ^ plan.col0, inverse=False)
+            backend.pair(ev, theirs, backend.twiddle(i, plan.block(i), plan.base), plan.side(i), inverse=False, **kw)
+        if not r:
+            backend.butterfly(ev, plan.lp, plan.base ^ plan.col0, inverse=False)
         evs.append(ev)
-    c = backend.pointwise(evs[0], evs[1])
-    backend.butterfly(c, plan.lp, plan.base ^ plan.col0, inverse=True)
+    if r:  # local forward layers of both, pointwise, local inverse layers: one call
+        c = backend.local_product(evs[0], evs[1], plan.lp, plan.base ^ plan.col0)
+    else:
+        c = backend.pointwise(evs[0], evs[1])
+        backend.butterfly(c, plan.lp, plan.base ^ plan.col0, inverse=True)
     for i in plan.top_layers(inverse=True):
         theirs = backend.exchange(c, plan.partner(i))
-        backend.pair(c, theirs, backend.twiddle(i, plan.block(i), plan.base), plan.side(i), inverse=True)
-    slice_ = backend.decode_cols(c, plan.m)                             # 128 rows x m bits
+        backend.pair(c, theirs, backend.twiddle(i, plan.block(i), plan.base), plan.side(i), inverse=True, **kw)
+    slice_ = backend.decode_cols(c, plan.m, **kw)                       # 128 rows x m bits
     full = backend.gather_columns(slice_, plan)                         # 128 rows x n_p bits
     return backend.finish(full, plan.n_bits, a_bits + b_bits - 1)       # i_basis_cvt + trim
 
@@ -140,9 +151,13 @@ class GpuBackend:
         self.L.stage_dev("basis_cvt", poly, count, bits, stream=self._s())
         return poly
 
-    def encode_cols(self, poly, l: int, col0: int, ncols: int):
+    def tower(self, l: int) -> bool:
+        return bool(self.L.lib().fpm_shard_tower(l))
+
+    def encode_cols(self, poly, l: int, col0: int, ncols: int, tower: bool = False):
         ev = self.torch.empty(2 * ncols, dtype=self.torch.int64, device=poly.device)
-        self.L._check(self.L.lib().fpm_encode_cols_dev(poly.data_ptr(), l, col0, ncols, 64, ev.data_ptr(), self._s()))
+        f = self.L.lib().fpm_encode_cols_r_dev if tower else self.L.lib().fpm_encode_cols_dev
+        self.L._check(f(poly.data_ptr(), l, col0, ncols, 64, ev.data_ptr(), self._s()))
         return ev
 
     def exchange(self, t, partner: int):
@@ -162,9 +177,17 @@ class GpuBackend:
         self.L._check(self.L.lib().fpm_twiddle128(i, b, bb.ctypes.data_as(self.L._u64p), out.ctypes.data_as(self.L._u64p)))
         return out
 
-    def pair(self, mine, theirs, w, side: int, inverse: bool):
-        self.L._check(self.L.lib().fpm_bfly_pair_dev(mine.data_ptr(), theirs.data_ptr(), mine.numel() // 2,
-                                                     w.ctypes.data_as(self.L._u64p), side, int(inverse), self._s()))
+    def pair(self, mine, theirs, w, side: int, inverse: bool, tower: bool = False):
+        f = self.L.lib().fpm_bfly_pair_r_dev if tower else self.L.lib().fpm_bfly_pair_dev
+        self.L._check(f(mine.data_ptr(), theirs.data_ptr(), mine.numel() // 2, w.ctypes.data_as(self.L._u64p), side,
+                        int(inverse), self._s()))
+
+    def local_product(self, ea, eb, l: int, base: int):
+        import numpy as np
+        bb = np.array([base & (2**64 - 1), base >> 64], np.uint64)
+        self.L._check(self.L.lib().fpm_shard_local_product_dev(ea.data_ptr(), eb.data_ptr(), l,
+                                                               bb.ctypes.data_as(self.L._u64p), self._s()))
+        return eb
 
     def butterfly(self, ev, l: int, base: int, inverse: bool):
         import numpy as np
@@ -178,9 +201,10 @@ class GpuBackend:
         self.L.stage_dev("pointwise", u, v, u, u.numel() // 2, stream=self._s())
         return u
 
-    def decode_cols(self, ev, ncols: int):
+    def decode_cols(self, ev, ncols: int, tower: bool = False):
         out = self.torch.empty(128 * ncols // 64, dtype=self.torch.int64, device=ev.device)
-        self.L._check(self.L.lib().fpm_decode_cols_dev(ev.data_ptr(), ncols, out.data_ptr(), self._s()))
+        f = self.L.lib().fpm_decode_cols_r_dev if tower else self.L.lib().fpm_decode_cols_dev
+        self.L._check(f(ev.data_ptr(), ncols, out.data_ptr(), self._s()))
         return out
 
     def gather_columns(self, slice_, plan: ShardPlan):

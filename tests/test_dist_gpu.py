@@ -47,7 +47,9 @@ def _make_backend(shared, rank):
     return ThreadBackend()
 
 
-@pytest.mark.parametrize("P,la,lb", [(2, 1 << 18, 1 << 18), (4, 1 << 20, (1 << 20) - 333), (8, 1 << 22, 1 << 21)])
+# the last two shapes give cosets of 2^18 elements: the tower fast path (fpm_shard_local_product_dev)
+@pytest.mark.parametrize("P,la,lb", [(2, 1 << 18, 1 << 18), (4, 1 << 20, (1 << 20) - 333), (8, 1 << 22, 1 << 21),
+                                     (2, 1 << 25, (1 << 25) - 99), (4, 1 << 26, 1 << 25)])
 def test_sharded_on_one_gpu(gpu, port, checker, P, la, lb):
     from paper_1803_11301_b200.dist import make_plan, polymul_sharded
 
