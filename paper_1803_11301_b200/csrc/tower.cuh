@@ -31,70 +31,6 @@ __device__ __forceinline__ uint4 smul(uint4 u, uint32_t d) {
   return acc;
 }
 
-// Rows of the M8 table of "multiply by w" (w in POLYNOMIAL representation) in R: row 8j+s =
-// R(w x^j) * t^s.  Threads tid < 128 (four whole warps): thread (j, s) converts bits [16s, 16s+16)
-// of w x^j with the to_r rows, the 8 partial sums of a j meet by shuffle-XOR, then s xtimes.
-// Writes rows[k + k/8] (m8 padding).  to_r: 128 rows, row k at index k + k/16 (TO_R_PAD) when
-// staged in shared memory, so the 8 lanes (s = 0..7) of a quarter-warp read distinct bank groups.
-__device__ __forceinline__ int to_r_pad(int k) { return k + (k >> 4); }
-template <bool SMEM>
-__device__ __forceinline__ void rows_r(uint4* __restrict__ rows, uint4 w, int tid, const uint4* __restrict__ to_r) {
-  if (tid >= 128) return;
-  const int j = tid >> 3, s = tid & 7;
-  const uint4 p = gf_mul_xk(w, (unsigned)j);
-  const uint32_t word = s < 2 ? p.x : s < 4 ? p.y : s < 6 ? p.z : p.w;
-  const uint32_t bits = (word >> (16 * (s & 1))) & 0xFFFFu;
-  uint4 acc = make_uint4(0, 0, 0, 0);
-  const uint4* src = to_r + (SMEM ? to_r_pad(16 * s) : 16 * s);
-#pragma unroll
-  for (int b = 0; b < 16; ++b) acc = x4(acc, and4(SMEM ? src[b] : __ldg(src + b), 0u - ((bits >> b) & 1u)));
-#pragma unroll
-  for (int m = 1; m < 8; m <<= 1) {
-    acc.x ^= __shfl_xor_sync(0xffffffffu, acc.x, m);
-    acc.y ^= __shfl_xor_sync(0xffffffffu, acc.y, m);
-    acc.z ^= __shfl_xor_sync(0xffffffffu, acc.z, m);
-    acc.w ^= __shfl_xor_sync(0xffffffffu, acc.w, m);
-  }
-#pragma unroll
-  for (int r = 0; r < 7; ++r)
-    if (r < s) acc = xt(acc);
-  rows[tid + (tid >> 3)] = acc;
-}
-
-// GF(2^64) (8 coordinates): rows of the G8 table of "multiply by w" (w polynomial) in R, row 8j+s =
-// R(w x^j) * t^s, by threads tid < 64 (two whole warps): thread (j, s) converts bits [8s, 8s+8) of
-// w x^j, shuffle-XOR over the 8 lanes of j, then s xtimes.  to_r: 64 rows at to_r64_pad(k)
-// (the 8 lanes s = 0..7 read 8 distinct bank pairs).  Writes rows[k + k/8].
-__device__ __forceinline__ int to_r64_pad(int k) { return k + (k >> 3); }
-__device__ __forceinline__ void rows_r64(uint2* __restrict__ rows, uint2 w, int tid, const uint2* __restrict__ to_r) {
-  if (tid >= 64) return;
-  const int j = tid >> 3, s = tid & 7;
-  const uint2 p = gf64_mul_xk(w, (unsigned)j);
-  const uint32_t bits = ((s < 4 ? p.x : p.y) >> (8 * (s & 3))) & 0xFFu;
-  uint2 acc = make_uint2(0, 0);
-  const uint2* src = to_r + to_r64_pad(8 * s);
-#pragma unroll
-  for (int b = 0; b < 8; ++b) {
-    const uint32_t m = 0u - ((bits >> b) & 1u);
-    acc.x ^= src[b].x & m;
-    acc.y ^= src[b].y & m;
-  }
-#pragma unroll
-  for (int m = 1; m < 8; m <<= 1) {
-    acc.x ^= __shfl_xor_sync(0xffffffffu, acc.x, m);
-    acc.y ^= __shfl_xor_sync(0xffffffffu, acc.y, m);
-  }
-#pragma unroll
-  for (int r = 0; r < 7; ++r)
-    if (r < s) acc = make_uint2(xt32(acc.x), xt32(acc.y));
-  rows[tid + (tid >> 3)] = acc;
-}
-
-// Rows of a constant linear map (to_r / to_poly) into the m8 row scratch.
-__device__ __forceinline__ void rows_const(uint4* __restrict__ rows, const uint4* __restrict__ src, int tid) {
-  if (tid < 128) rows[tid + (tid >> 3)] = __ldg(src + tid);
-}
-
 // u * d by byte permutes: "times d" is GF(2)-linear on each byte, so byte v maps to
 // M(v & 7) ^ [v & 8] M(8) ^ M(v & 0x70) ^ [v & 0x80] M(0x80).  The eight products M(0..7) and
 // M(0x00..0x70) sit in two register pairs, and one PRMT looks up four bytes at once: the selector
@@ -135,6 +71,88 @@ __device__ __forceinline__ uint4 smul_t(uint4 u, const SmulTab& t) {
   return make_uint4(smul_w(u.x, t), smul_w(u.y, t), smul_w(u.z, t), smul_w(u.w, t));
 }
 __device__ __forceinline__ uint2 smul_t2(uint2 u, const SmulTab& t) { return make_uint2(smul_w(u.x, t), smul_w(u.y, t)); }
+// SmulTabs of the powers t^s (t-basis byte 1 << s), s < 8: field constants of GF(2^8) mod 0x11B
+// (independent of the embedding), so rows_r multiplies by t^s with one smul_t instead of s xtimes.
+constexpr uint32_t gf8c(uint32_t a, uint32_t b) {
+  uint32_t r = 0;
+  for (int i = 0; i < 8; ++i) {
+    if (b >> i & 1) r ^= a;
+    a <<= 1;
+    if (a & 0x100) a ^= 0x11B;
+  }
+  return r;
+}
+constexpr uint32_t gf8c4(uint32_t k0, uint32_t step, uint32_t d) {
+  return gf8c(k0, d) | gf8c(k0 + step, d) << 8 | gf8c(k0 + 2 * step, d) << 16 | gf8c(k0 + 3 * step, d) << 24;
+}
+#define FPM_TPOW(s) {gf8c4(0, 1, 1u << s), gf8c4(4, 1, 1u << s), gf8c4(0, 16, 1u << s), gf8c4(64, 16, 1u << s)}, \
+                    {gf8c(8, 1u << s) * 0x01010101u, gf8c(0x80, 1u << s) * 0x01010101u, 0u, 0u}
+static __device__ const uint4 g_tpow[16] = {FPM_TPOW(0), FPM_TPOW(1), FPM_TPOW(2), FPM_TPOW(3),
+                                            FPM_TPOW(4), FPM_TPOW(5), FPM_TPOW(6), FPM_TPOW(7)};
+#undef FPM_TPOW
+__device__ __forceinline__ SmulTab tpow_tab(int s) {
+  const uint4 a = g_tpow[2 * s], b = g_tpow[2 * s + 1];
+  return SmulTab{a.x, a.y, a.z, a.w, b.x, b.y};
+}
+
+// Rows of the M8 table of "multiply by w" (w in POLYNOMIAL representation) in R: row 8j+s =
+// R(w x^j) * t^s.  Threads tid < 128 (four whole warps): thread (j, s) converts bits [16s, 16s+16)
+// of w x^j with the to_r rows, the 8 partial sums of a j meet by shuffle-XOR, then times t^s.
+// Writes rows[k + k/8] (m8 padding).  to_r: 128 rows, row k at index k + k/16 (TO_R_PAD) when
+// staged in shared memory, so the 8 lanes (s = 0..7) of a quarter-warp read distinct bank groups.
+__device__ __forceinline__ int to_r_pad(int k) { return k + (k >> 4); }
+template <bool SMEM>
+__device__ __forceinline__ void rows_r(uint4* __restrict__ rows, uint4 w, int tid, const uint4* __restrict__ to_r) {
+  if (tid >= 128) return;
+  const int j = tid >> 3, s = tid & 7;
+  const uint4 p = gf_mul_xk(w, (unsigned)j);
+  const uint32_t word = s < 2 ? p.x : s < 4 ? p.y : s < 6 ? p.z : p.w;
+  const uint32_t bits = (word >> (16 * (s & 1))) & 0xFFFFu;
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  const uint4* src = to_r + (SMEM ? to_r_pad(16 * s) : 16 * s);
+#pragma unroll
+  for (int b = 0; b < 16; ++b) acc = x4(acc, and4(SMEM ? src[b] : __ldg(src + b), 0u - ((bits >> b) & 1u)));
+#pragma unroll
+  for (int m = 1; m < 8; m <<= 1) {
+    acc.x ^= __shfl_xor_sync(0xffffffffu, acc.x, m);
+    acc.y ^= __shfl_xor_sync(0xffffffffu, acc.y, m);
+    acc.z ^= __shfl_xor_sync(0xffffffffu, acc.z, m);
+    acc.w ^= __shfl_xor_sync(0xffffffffu, acc.w, m);
+  }
+  rows[tid + (tid >> 3)] = smul_t(acc, tpow_tab(s));
+}
+
+// GF(2^64) (8 coordinates): rows of the G8 table of "multiply by w" (w polynomial) in R, row 8j+s =
+// R(w x^j) * t^s, by threads tid < 64 (two whole warps): thread (j, s) converts bits [8s, 8s+8) of
+// w x^j, shuffle-XOR over the 8 lanes of j, then s xtimes.  to_r: 64 rows at to_r64_pad(k)
+// (the 8 lanes s = 0..7 read 8 distinct bank pairs).  Writes rows[k + k/8].
+__device__ __forceinline__ int to_r64_pad(int k) { return k + (k >> 3); }
+__device__ __forceinline__ void rows_r64(uint2* __restrict__ rows, uint2 w, int tid, const uint2* __restrict__ to_r) {
+  if (tid >= 64) return;
+  const int j = tid >> 3, s = tid & 7;
+  const uint2 p = gf64_mul_xk(w, (unsigned)j);
+  const uint32_t bits = ((s < 4 ? p.x : p.y) >> (8 * (s & 3))) & 0xFFu;
+  uint2 acc = make_uint2(0, 0);
+  const uint2* src = to_r + to_r64_pad(8 * s);
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const uint32_t m = 0u - ((bits >> b) & 1u);
+    acc.x ^= src[b].x & m;
+    acc.y ^= src[b].y & m;
+  }
+#pragma unroll
+  for (int m = 1; m < 8; m <<= 1) {
+    acc.x ^= __shfl_xor_sync(0xffffffffu, acc.x, m);
+    acc.y ^= __shfl_xor_sync(0xffffffffu, acc.y, m);
+  }
+  rows[tid + (tid >> 3)] = smul_t2(acc, tpow_tab(s));
+}
+
+// Rows of a constant linear map (to_r / to_poly) into the m8 row scratch.
+__device__ __forceinline__ void rows_const(uint4* __restrict__ rows, const uint4* __restrict__ src, int tid) {
+  if (tid < 128) rows[tid + (tid >> 3)] = __ldg(src + tid);
+}
+
 __device__ __forceinline__ uint32_t gf8_mul(uint32_t a, uint32_t b) {  // mod t^8 + t^4 + t^3 + t + 1
   uint32_t r = 0;
   for (int i = 0; i < 8; ++i) {
