@@ -579,6 +579,14 @@ __global__ void __launch_bounds__(kTowerThreads, FPM_TOWER_MINB) fft_tile_tower_
     m8_expand(sm.tab, sm.rows_to_r, tid);
     __syncthreads();
     for (int k = tid; k < n; k += blockDim.x) s[k] = m8_mul_r(mb, s[k], q);
+    {  // the next tile's operands into L2 while this tile's inverse layers run (128-byte lines)
+      const uint64_t tn = t + gridDim.x;
+      if (tn < ntiles) {
+        const int lines = n * 16 / 128;
+        const char* p = reinterpret_cast<const char*>((tid < lines ? ea : eb) + (tn << T)) + 128 * (tid % lines);
+        if (tid < 2 * lines) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+      }
+    }
     // (tile_layers_r's first barrier orders these stores before its butterflies)
     tile_layers_r<true, 1>(s, T, kPolyLayers, sm);
     for (int k = tid; k < n; k += blockDim.x) g[k] = s[tsw(k)];

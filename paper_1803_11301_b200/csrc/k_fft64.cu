@@ -521,6 +521,15 @@ __global__ void __launch_bounds__(256, 3) fft64_tile_tower_kernel(const uint2* _
     g8_expand(sm.tab, sm.rows_to_r, tid);
     __syncthreads();
     for (int k = tid; k < n; k += blockDim.x) s64[k] = g8_mul(sm.tab, s64[k], lane);
+    {  // the next tile's operands into L2 while this tile's inverse layers run
+      const uint64_t tn = t + gridDim.x;
+      const int lines = n * 8 / 128;
+      if (tn < ntiles)
+        for (int k = tid; k < 2 * lines; k += blockDim.x) {
+          const char* p = reinterpret_cast<const char*>((k < lines ? ea : eb) + (tn << T)) + 128 * (k % lines);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        }
+    }
     tile_layers_r64<true, 1>(s64, T, kPolyLayers64, sm);
     for (int k = tid; k < n; k += blockDim.x) g[k] = s64[tsw64(k)];
     __syncthreads();
