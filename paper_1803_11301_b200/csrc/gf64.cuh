@@ -106,6 +106,41 @@ __device__ __forceinline__ uint2 g8_mul(const uint2* __restrict__ tab, uint2 x, 
   return x2(acc0, acc1);
 }
 
+// g8_mul with the lane rotation applied to the operand once (cf. gf128.cuh m8_mul_r): x rotated
+// right by 8q bits puts chunk (k + q) & 7 at byte k, so each lookup is one PRMT (constant selector)
+// and one IMAD on a per-lane base address.
+struct G8Base {
+  uint32_t b[8];  // shared-memory byte address of entry (0, chunk (k + q) & 7, copy h)
+};
+__device__ __forceinline__ G8Base g8_base(const uint2* tab, int lane) {
+  G8Base g;
+  const uint32_t t = (uint32_t)__cvta_generic_to_shared(tab) + 8u * (uint32_t)(lane & 8);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) g.b[k] = t + 8u * (uint32_t)((k + lane) & 7);
+  return g;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint2 g8_mul_r(const G8Base& gb, uint2 x, int lane, uint32_t off = 0) {
+  const int q = lane & 7;
+  const bool sw = q & 4;
+  const uint32_t s = 8u * (uint32_t)(q & 3);
+  const uint32_t a0 = sw ? x.y : x.x, a1 = sw ? x.x : x.y;
+  const uint32_t r0 = __funnelshift_r(a0, a1, s), r1 = __funnelshift_r(a1, a0, s);
+  uint2 acc0 = make_uint2(0, 0), acc1 = make_uint2(0, 0);
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) {
+    const uint32_t b0 = __byte_perm(k < 4 ? r0 : r1, 0, 0x4440u | (uint32_t)(k & 3));
+    const uint32_t b1 = __byte_perm(k < 4 ? r0 : r1, 0, 0x4440u | (uint32_t)((k + 1) & 3));
+    acc0 = x2(acc0, lds64(gb.b[k] + 128u * b0 + off));
+    acc1 = x2(acc1, lds64(gb.b[k + 1] + 128u * b1 + off));
+  }
+  return x2(acc0, acc1);
+}
+
 // ---------------------------------------------------------------- 4-bit tables, 16 at a time
 // For tile layers whose twiddles are shared by only 2^4..2^7 butterflies: 16 nibble-chunk tables of
 // w*(v << 4c), 2 KiB per twiddle, entry (c, v) at uint2 index v*16 + c (8-byte slot c of a 128-byte

@@ -132,25 +132,27 @@ __global__ void __launch_bounds__(kTop4Threads64, 2) fft64_top4_kernel(uint2* __
   const uint64_t j0 = quad0 & (h - 1);
   // Each thread transforms two adjacent quads with 16-byte accesses (512 B per warp per quarter
   // stream: the eight streams of a CTA stay DRAM-page friendly).
+  const G8Base gb = g8_base(t1, lane);
+  constexpr uint32_t kA = kG8Uint2 * 8u, kB = 2u * kG8Uint2 * 8u;  // t0a, t0b after t1
   auto bfly = [&](uint2& a0, uint2& a1, uint2& a2, uint2& a3) {
     if (!INV) {
-      a0 = x2(a0, g8_mul(t1, a2, lane));
-      a1 = x2(a1, g8_mul(t1, a3, lane));
+      a0 = x2(a0, g8_mul_r(gb, a2, lane));
+      a1 = x2(a1, g8_mul_r(gb, a3, lane));
       a2 = x2(a2, a0);
       a3 = x2(a3, a1);
-      a0 = x2(a0, g8_mul(t0a, a1, lane));
-      a2 = x2(a2, g8_mul(t0b, a3, lane));
+      a0 = x2(a0, g8_mul_r(gb, a1, lane, kA));
+      a2 = x2(a2, g8_mul_r(gb, a3, lane, kB));
       a1 = x2(a1, a0);
       a3 = x2(a3, a2);
     } else {
       a1 = x2(a1, a0);
       a3 = x2(a3, a2);
-      a0 = x2(a0, g8_mul(t0a, a1, lane));
-      a2 = x2(a2, g8_mul(t0b, a3, lane));
+      a0 = x2(a0, g8_mul_r(gb, a1, lane, kA));
+      a2 = x2(a2, g8_mul_r(gb, a3, lane, kB));
       a2 = x2(a2, a0);
       a3 = x2(a3, a1);
-      a0 = x2(a0, g8_mul(t1, a2, lane));
-      a1 = x2(a1, g8_mul(t1, a3, lane));
+      a0 = x2(a0, g8_mul_r(gb, a2, lane));
+      a1 = x2(a1, g8_mul_r(gb, a3, lane));
     }
   };
 #pragma unroll 1
@@ -409,6 +411,7 @@ __device__ __forceinline__ void tile_layers_r64(uint2* __restrict__ s, unsigned 
     const int lg = (nblk < 128 ? T - 1 : 7 + i);
     for (int h = 0; h < nblk; h += 128, ++k) {
       if (k + 1 < ntab) rows_r64(sm.rows[(k + 1) & 1], sm.wz[wz_of(k + 1)], tid, sm.to_r);
+      const G8Base gb = g8_base(sm.tab, lane);
       for (int pp = tid; pp < (NT << lg); pp += blockDim.x) {
         const int p = pp & ((1 << lg) - 1), tt = pp >> lg;
         const int blk = h + (p >> i), j = p & ((1 << i) - 1);
@@ -416,13 +419,13 @@ __device__ __forceinline__ void tile_layers_r64(uint2* __restrict__ s, unsigned 
         const int d = blk & 127;
         uint2 u0 = s[tsw64(i0)], u1 = s[tsw64(i1)];
         if (!INV) {
-          uint2 m = g8_mul(sm.tab, u1, lane);
+          uint2 m = g8_mul_r(gb, u1, lane);
           if (d) m = x2(m, smul_t2(u1, smul_tab(sm.stab, d)));
           u0 = x2(u0, m);
           u1 = x2(u1, u0);
         } else {
           u1 = x2(u1, u0);
-          uint2 m = g8_mul(sm.tab, u1, lane);
+          uint2 m = g8_mul_r(gb, u1, lane);
           if (d) m = x2(m, smul_t2(u1, smul_tab(sm.stab, d)));
           u0 = x2(u0, m);
         }
