@@ -376,6 +376,8 @@ def main():
                     help="--impl reference: the reference's field (default GF(2^128), as our arm)")
     ap.add_argument("--mode", default="shard", choices=["shard", "replicas"],
                     help="N>1: shard one product over the GPUs (default) or run independent replicas")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="shard mode: exchanged FFT layers over peer memory (default) or NCCL send/recv")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     ws, rank, local = dist_env()
@@ -412,8 +414,26 @@ def main():
     c = torch.empty(out_words, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
     from paper_1803_11301_b200 import dist as pdist
-    backend = pdist.GpuBackend() if mode == "shard" else None
     plan = pdist.make_plan(bits, bits, ws, rank) if mode == "shard" else None
+    backend, exchange = None, None
+    if mode == "shard":
+        # exchanged layers over peer memory (NVLink loads fused into the pair kernel, dist.PeerBackend),
+        # or NCCL send/recv + pair kernel; a peer setup failure on any rank falls back to NCCL on all
+        ok = 0
+        if args.exchange == "peer":
+            try:
+                backend = pdist.PeerBackend()
+                backend.begin(plan)
+                ok = 1
+            except Exception as e:  # noqa: BLE001 - reported in the JSON line
+                exchange = f"nccl (peer setup failed: {str(e)[:120]})"
+        flag = torch.tensor([ok], device=dev)
+        torch.distributed.all_reduce(flag, op=torch.distributed.ReduceOp.MIN)
+        if int(flag.item()) == 1:
+            exchange = "peer"
+        else:
+            backend = pdist.GpuBackend()
+            exchange = exchange or "nccl"
 
     def step(x, y):
         if mode == "shard":
@@ -548,7 +568,7 @@ def main():
                                f"l={(2*bits//128).bit_length()-1})",
                    "parallelism": {"single": "single GPU", "replicas": f"{ws} independent products (replicas)",
                                    "shard": f"one product sharded over {ws} GPUs: top {ws.bit_length() - 1} butterfly "
-                                            "layers exchanged over NCCL P2P, basis conversions replicated"}[mode],
+                                            f"layers exchanged ({exchange}), basis conversions replicated"}[mode],
                    "l2": "inputs >= 2x L2 per operand at cfg4/5 (no flush needed)" if bits >= 1 << 28 else "inputs fit in L2"},
         "e2e": {"value": round(e2e_ms / ws if mode == "replicas" else e2e_ms, 3), "unit": "ms", "steps": e2e_steps,
                 "h2d_bytes_per_step": 2 * words * 8, "d2h_bytes_per_step": out_words * 8,

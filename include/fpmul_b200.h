@@ -155,6 +155,20 @@ fpm_status fpm_bfly_pair_r_dev(uint64_t* d_mine, const uint64_t* d_theirs, size_
                                int inverse, void* stream);
 fpm_status fpm_shard_local_product_dev(uint64_t* d_ea, uint64_t* d_eb, unsigned l, const uint64_t* base,
                                        void* stream);
+/* The exchanged layer with the exchange fused in (peer memory over NVLink instead of an NCCL copy):
+ * d_theirs is the partner's half in the PARTNER GPU's memory (a pointer from fpm_ipc_open), read
+ * directly by the kernel; the result goes to d_out, a third local buffer, so neither input is
+ * overwritten while the partner may still be reading this rank's half (ping-pong buffers; one
+ * barrier per layer).  tower: elements in the tower representation. */
+fpm_status fpm_bfly_pair_peer_dev(const uint64_t* d_mine, const uint64_t* d_theirs, uint64_t* d_out, size_t n,
+                                  const uint64_t* w, int side, int inverse, int tower, void* stream);
+/* Peer-shareable device buffers: cudaMalloc + cudaIpcGetMemHandle (64-byte handle) / open a peer's
+ * handle in this process (cudaIpcMemLazyEnablePeerAccess) / close / free. */
+#define FPM_IPC_HANDLE_BYTES 64
+fpm_status fpm_ipc_alloc(size_t bytes, void** d_ptr, uint8_t* handle);
+fpm_status fpm_ipc_open(const uint8_t* handle, void** d_peer);
+fpm_status fpm_ipc_close(void* d_peer);
+fpm_status fpm_ipc_free(void* d_ptr);
 /* Host: the twiddle C2P((base >> i) ^ 2b) of layer i, block b (butterfly.cpp:45-49); base in
  * Cantor coordinates {lo, hi}; out = {lo, hi} polynomial representation. */
 fpm_status fpm_twiddle128(unsigned i, uint64_t b, const uint64_t* base, uint64_t* out);

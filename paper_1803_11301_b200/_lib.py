@@ -12,6 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+IPC_HANDLE_BYTES = 64  # FPM_IPC_HANDLE_BYTES (include/fpmul_b200.h)
 LIB_PATH = os.environ.get("FPM_LIB") or os.path.join(HERE, "libfpmul_b200.so")  # FPM_LIB: experiment builds
 
 FIELD_AUTO, FIELD_GF64, FIELD_GF128 = 0, 64, 128
@@ -87,6 +88,11 @@ def lib():
         L.fpm_decode_cols_r_dev.argtypes = [vp, sz, vp, vp]
         L.fpm_bfly_pair_r_dev.argtypes = [vp, vp, sz, _u64p, C.c_int, C.c_int, vp]
         L.fpm_shard_local_product_dev.argtypes = [vp, vp, C.c_uint, _u64p, vp]
+        L.fpm_bfly_pair_peer_dev.argtypes = [vp, vp, vp, sz, _u64p, C.c_int, C.c_int, C.c_int, vp]
+        L.fpm_ipc_alloc.argtypes = [sz, C.POINTER(vp), C.POINTER(C.c_uint8)]
+        L.fpm_ipc_open.argtypes = [C.POINTER(C.c_uint8), C.POINTER(vp)]
+        L.fpm_ipc_close.argtypes = [vp]
+        L.fpm_ipc_free.argtypes = [vp]
         L.fpm_karatsuba_mul.argtypes = [_u64p, sz, _u64p, sz, _u64p, C.c_int]
         L.fpm_clmul_words_dev.argtypes = [vp, sz, vp, sz, vp, vp]
         _LIB = L

@@ -785,6 +785,55 @@ fpm_status fpm_bfly_pair_r_dev(uint64_t* d_mine, const uint64_t* d_theirs, size_
   });
 }
 
+fpm_status fpm_bfly_pair_peer_dev(const uint64_t* d_mine, const uint64_t* d_theirs, uint64_t* d_out, size_t n,
+                                  const uint64_t* w, int side, int inverse, int tower, void* stream) {
+  return guard([&] {
+    require_device();
+    if (!w || (side != 0 && side != 1)) throw Error(kInvalid, "bfly_pair: bad twiddle or side");
+    if (d_out == d_mine || d_out == d_theirs) throw Error(kInvalid, "bfly_pair_peer: the output must be a third buffer");
+    U128 t;
+    t.lo = w[0];
+    t.hi = w[1];
+    bfly_pair_device(const_cast<uint4*>(reinterpret_cast<const uint4*>(d_mine)), reinterpret_cast<const uint4*>(d_theirs),
+                     n, t, side, inverse != 0, (cudaStream_t)stream, tower != 0, reinterpret_cast<uint4*>(d_out));
+  });
+}
+
+fpm_status fpm_ipc_alloc(size_t bytes, void** d_ptr, uint8_t* handle) {
+  return guard([&] {
+    require_device();
+    if (!d_ptr || !handle || !bytes) throw Error(kInvalid, "ipc_alloc: null argument or size");
+    FPM_CUDA(cudaMalloc(d_ptr, bytes));
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, *d_ptr);
+    if (e != cudaSuccess) {
+      cudaFree(*d_ptr);
+      *d_ptr = nullptr;
+      throw Error(kCuda, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+    }
+    static_assert(sizeof(h) == FPM_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle, &h, sizeof(h));
+  });
+}
+
+fpm_status fpm_ipc_open(const uint8_t* handle, void** d_peer) {
+  return guard([&] {
+    require_device();
+    if (!handle || !d_peer) throw Error(kInvalid, "ipc_open: null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    FPM_CUDA(cudaIpcOpenMemHandle(d_peer, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+fpm_status fpm_ipc_close(void* d_peer) {
+  return guard([&] { FPM_CUDA(cudaIpcCloseMemHandle(d_peer)); });
+}
+
+fpm_status fpm_ipc_free(void* d_ptr) {
+  return guard([&] { FPM_CUDA(cudaFree(d_ptr)); });
+}
+
 fpm_status fpm_shard_local_product_dev(uint64_t* d_ea, uint64_t* d_eb, unsigned l, const uint64_t* base,
                                        void* stream) {
   return guard([&] {

@@ -145,8 +145,10 @@ void encode_cols_device(const uint32_t* poly, unsigned l, uint64_t col0, uint64_
 void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaStream_t s, bool tower = false);
 // One exchanged butterfly layer (sharded FFT): this rank holds `mine` (side 0 = p0 half, 1 = p1 half),
 // the partner's half arrived in `theirs`; uniform twiddle w.  Result replaces `mine`.
+// out (optional): write the result there instead of over `mine` (then `theirs` may be a peer GPU's
+// memory that the partner reads concurrently: nothing of `mine` or `theirs` is overwritten).
 void bfly_pair_device(uint4* mine, const uint4* theirs, uint64_t n, U128 w, int side, bool inverse, cudaStream_t s,
-                      bool tower = false);
+                      bool tower = false, uint4* out = nullptr);
 void decode_device(const uint4* ev, unsigned l, uint32_t* poly, cudaStream_t s, bool tower = false);
 
 // Butterflies (k_fft.cu).

@@ -597,8 +597,12 @@ __global__ void __launch_bounds__(kTowerThreads, FPM_TOWER_MINB) fft_tile_tower_
 // Exchanged layer of the sharded FFT: all local elements share one twiddle w (polynomial form);
 // R: elements in the tower representation (table built in R).
 template <bool INV, bool R>
-__global__ void __launch_bounds__(256) fft_pair_kernel(uint4* __restrict__ mine, const uint4* __restrict__ theirs,
-                                                       uint64_t n, uint4 w, int side, int ppc, const uint4* to_r) {
+// out: where the result goes -- `mine` itself after an NCCL exchange, or the other buffer of a
+// ping-pong pair when `theirs` is the partner GPU's memory read over NVLink (fpm_bfly_pair_peer_dev:
+// the exchange is these loads, fused with the butterfly; nothing is staged).
+__global__ void __launch_bounds__(256) fft_pair_kernel(const uint4* mine, const uint4* __restrict__ theirs,
+                                                       uint4* out, uint64_t n, uint4 w, int side, int ppc,
+                                                       const uint4* to_r) {
   extern __shared__ uint4 tab[];
   __shared__ uint4 rows[144];
   if (R) {
@@ -621,7 +625,7 @@ __global__ void __launch_bounds__(256) fft_pair_kernel(uint4* __restrict__ mine,
     } else {     // p1' = p1 + p0 ; p0' = p0 + w p1'
       r = side == 0 ? x4(a, m8_mul(tab, x4(a, b), copy)) : x4(a, b);
     }
-    mine[e] = r;
+    out[e] = r;
   }
 }
 
@@ -850,7 +854,8 @@ void butterfly_device(uint4* ev, unsigned l, U128 base, bool inverse, cudaStream
 }
 
 void bfly_pair_device(uint4* mine, const uint4* theirs, uint64_t n, U128 w, int side, bool inverse, cudaStream_t s,
-                      bool tower) {
+                      bool tower, uint4* out) {
+  if (!out) out = mine;
   if (!n) return;
   const size_t smem = kM8Uint4 * sizeof(uint4);
   static PerDeviceOnce attr;
@@ -868,11 +873,11 @@ void bfly_pair_device(uint4* mine, const uint4* theirs, uint64_t n, U128 w, int 
   const unsigned ctas = (unsigned)((n + ppc - 1) / ppc);
   const uint4 w4 = make_uint4((uint32_t)w.lo, (uint32_t)(w.lo >> 32), (uint32_t)w.hi, (uint32_t)(w.hi >> 32));
   if (tower) {
-    if (!inverse) fft_pair_kernel<false, true><<<ctas, 256, smem, s>>>(mine, theirs, n, w4, side, (int)ppc, to_r);
-    else fft_pair_kernel<true, true><<<ctas, 256, smem, s>>>(mine, theirs, n, w4, side, (int)ppc, to_r);
+    if (!inverse) fft_pair_kernel<false, true><<<ctas, 256, smem, s>>>(mine, theirs, out, n, w4, side, (int)ppc, to_r);
+    else fft_pair_kernel<true, true><<<ctas, 256, smem, s>>>(mine, theirs, out, n, w4, side, (int)ppc, to_r);
   } else {
-    if (!inverse) fft_pair_kernel<false, false><<<ctas, 256, smem, s>>>(mine, theirs, n, w4, side, (int)ppc, to_r);
-    else fft_pair_kernel<true, false><<<ctas, 256, smem, s>>>(mine, theirs, n, w4, side, (int)ppc, to_r);
+    if (!inverse) fft_pair_kernel<false, false><<<ctas, 256, smem, s>>>(mine, theirs, out, n, w4, side, (int)ppc, to_r);
+    else fft_pair_kernel<true, false><<<ctas, 256, smem, s>>>(mine, theirs, out, n, w4, side, (int)ppc, to_r);
   }
   FPM_LAUNCH_CHECK();
 }

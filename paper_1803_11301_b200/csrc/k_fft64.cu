@@ -84,9 +84,7 @@ template <bool INV, bool R>
 __global__ void __launch_bounds__(kTop4Threads64, 2) fft64_top4_kernel(uint2* __restrict__ ev, unsigned i, int qpc,
                                                                        TwiddleSrc64 tw) {
   extern __shared__ uint2 sm64[];
-  uint2* t1 = sm64;                    // w(i+1, B)
-  uint2* t0a = sm64 + kG8Uint2;        // w(i, 2B)
-  uint2* t0b = sm64 + 2 * kG8Uint2;    // w(i, 2B+1)
+  uint2* t1 = sm64;                    // w(i+1, B); then w(i, 2B) at + kG8Uint2, w(i, 2B+1) at + 2 kG8Uint2
   uint2* rows = sm64 + 3 * kG8Uint2;   // 3 x kG8Rows
   uint2* to_r = rows + 3 * kG8Rows;    // tower: conversion rows, to_r64_pad layout
   const uint64_t h = (uint64_t)1 << i;

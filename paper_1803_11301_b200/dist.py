@@ -93,13 +93,23 @@ def polymul_sharded(a, a_bits: int, b, b_bits: int, backend, plan: ShardPlan | N
     plan = plan or make_plan(a_bits, b_bits, P, rank)
     r = hasattr(backend, "tower") and backend.tower(plan.lp)           # coset on the fast path
     kw = {"tower": True} if r else {}
+    if hasattr(backend, "begin"):
+        backend.begin(plan)
+
+    def exchanged(ev, i, inverse):
+        w = backend.twiddle(i, plan.block(i), plan.base)
+        if hasattr(backend, "exchange_pair"):  # exchange fused into the butterfly (peer memory)
+            return backend.exchange_pair(ev, plan.partner(i), w, plan.side(i), inverse, **kw)
+        theirs = backend.exchange(ev, plan.partner(i))
+        backend.pair(ev, theirs, w, plan.side(i), inverse=inverse, **kw)
+        return ev
+
     evs = []
     for x, bits in ((a, a_bits), (b, b_bits)):
         poly = backend.convert_operand(x, bits, plan.n_bits)          # basis_cvt, replicated
         ev = backend.encode_cols(poly, plan.l, plan.col0, plan.m, **kw)  # local columns
         for i in plan.top_layers(inverse=False):                       # exchanged layers
-            theirs = backend.exchange(ev, plan.partner(i))
-            backend.pair(ev, theirs, backend.twiddle(i, plan.block(i), plan.base), plan.side(i), inverse=False, **kw)
+            ev = exchanged(ev, i, False)
         if not r:
             backend.butterfly(ev, plan.lp, plan.base ^ plan.col0, inverse=False)
         evs.append(ev)
@@ -109,8 +119,7 @@ def polymul_sharded(a, a_bits: int, b, b_bits: int, backend, plan: ShardPlan | N
         c = backend.pointwise(evs[0], evs[1])
         backend.butterfly(c, plan.lp, plan.base ^ plan.col0, inverse=True)
     for i in plan.top_layers(inverse=True):
-        theirs = backend.exchange(c, plan.partner(i))
-        backend.pair(c, theirs, backend.twiddle(i, plan.block(i), plan.base), plan.side(i), inverse=True, **kw)
+        c = exchanged(c, i, True)
     slice_ = backend.decode_cols(c, plan.m, **kw)                       # 128 rows x m bits
     full = backend.gather_columns(slice_, plan)                         # 128 rows x n_p bits
     return backend.finish(full, plan.n_bits, a_bits + b_bits - 1)       # i_basis_cvt + trim
@@ -226,3 +235,102 @@ class GpuBackend:
         if out_bits % 64:
             out[w - 1] &= (1 << (out_bits % 64)) - 1
         return out
+
+
+class DevBuf:
+    """A raw device buffer with the two tensor methods the backend's C-ABI calls use."""
+
+    def __init__(self, ptr: int, numel: int, device=None):
+        self.ptr, self.n, self.device = ptr, numel, device
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+    def numel(self) -> int:
+        return self.n
+
+
+class PeerBackend(GpuBackend):
+    """GpuBackend with the exchanged layers fused into their butterflies over peer memory (NVLink):
+    each rank keeps both operands' evaluation slices in ping-pong pairs of peer-shareable buffers
+    (fpm_ipc_alloc; handles exchanged once per plan with all_gather_object, partners' buffers opened
+    with fpm_ipc_open), and an exchanged layer is ONE kernel (fpm_bfly_pair_peer_dev) that reads the
+    partner's current buffer directly and writes this rank's other one.  A barrier before each
+    exchanged layer orders it after every rank's previous step (inputs written, old reads done);
+    the local product only touches the buffers partners do not read.  Across products the final
+    column all_gather (stream-ordered after every rank's last pair kernel) orders the reuse.
+    No NCCL data-path transfer remains except that gather."""
+
+    def __init__(self, group=None):
+        super().__init__(group)
+        self.key = None
+
+    # -- hooks (the single-GPU thread test overrides these)
+    def _alloc(self, nbytes: int):
+        import ctypes as C
+        import numpy as np
+        p = C.c_void_p()
+        h = np.zeros(self.L.IPC_HANDLE_BYTES, np.uint8)
+        self.L._check(self.L.lib().fpm_ipc_alloc(nbytes, C.byref(p), h.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return p.value, bytes(h)
+
+    def _publish(self, handles):
+        out = [None] * self.world()[0]
+        self.dist.all_gather_object(out, handles, group=self.group)
+        return out
+
+    def _open(self, handle):
+        import ctypes as C
+        import numpy as np
+        p = C.c_void_p()
+        h = np.frombuffer(handle, np.uint8).copy()
+        self.L._check(self.L.lib().fpm_ipc_open(h.ctypes.data_as(C.POINTER(C.c_uint8)), C.byref(p)))
+        return p.value
+
+    def _barrier(self):
+        self.torch.cuda.current_stream().synchronize()
+        self.dist.barrier(group=self.group)
+
+    # -- plan setup: 2 operands x ping/pong of m elements, partners' buffers opened once
+    def begin(self, plan):
+        P, rank = self.world()
+        key = (plan.m, P, rank)
+        if self.key != key:
+            nbytes = plan.m * 16
+            mine = [self._alloc(nbytes) for _ in range(4)]
+            allh = self._publish([h for _, h in mine])
+            dev = self.torch.device("cuda", self.torch.cuda.current_device())
+            self.mine = [DevBuf(p, 2 * plan.m, dev) for p, _ in mine]
+            self.peer = {}
+            for i in range(plan.lp, plan.l):
+                g = plan.partner(i)
+                if g not in self.peer:
+                    self.peer[g] = [self._open(h) for h in allh[g]]
+            self.key = key
+        self.n_enc = 0
+        self.cur = [0, 0]
+
+    def encode_cols(self, poly, l: int, col0: int, ncols: int, tower: bool = False):
+        k = self.n_enc
+        self.n_enc += 1
+        ev = self.mine[2 * k]
+        f = self.L.lib().fpm_encode_cols_r_dev if tower else self.L.lib().fpm_encode_cols_dev
+        self.L._check(f(poly.data_ptr(), l, col0, ncols, 64, ev.data_ptr(), self._s()))
+        self.cur[k] = 0
+        return ev
+
+    def exchange_pair(self, ev, partner: int, w, side: int, inverse: bool, tower: bool = False):
+        k = next(j for j in (0, 1) if self.mine[2 * j + self.cur[j]].ptr == ev.ptr)
+        c = self.cur[k]
+        out = self.mine[2 * k + 1 - c]
+        self._barrier()  # every rank's buffer c is final; nobody still reads buffer 1 - c
+        self.L._check(self.L.lib().fpm_bfly_pair_peer_dev(ev.data_ptr(), self.peer[partner][2 * k + c], out.data_ptr(),
+                                                          ev.numel() // 2, w.ctypes.data_as(self.L._u64p), side,
+                                                          int(inverse), int(tower), self._s()))
+        self.cur[k] = 1 - c
+        return out
+
+    def pointwise(self, u, v):
+        self.L._check(self.L.lib().fpm_pointwise_dev(u.data_ptr(), v.data_ptr(), u.data_ptr(), u.numel() // 2,
+                                                     self._s()))
+        return u

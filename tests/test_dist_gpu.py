@@ -80,3 +80,106 @@ def test_sharded_on_one_gpu(gpu, port, checker, P, la, lb):
     assert not errs, errs
     for r in range(P):
         assert np.array_equal(out[r], want), r
+
+
+def _make_peer_backend(shared, rank, keep):
+    """PeerBackend with the IPC hooks replaced by same-process pointers: the exchanged layers read the
+    partner thread's buffer directly (as over NVLink), the barriers are host barriers."""
+    from paper_1803_11301_b200.dist import PeerBackend
+
+    class ThreadPeerBackend(PeerBackend):
+        def world(self):
+            return shared.P, rank
+
+        def _alloc(self, nbytes):
+            t = torch.empty(nbytes // 8, dtype=torch.int64, device="cuda")
+            keep.append(t)
+            return t.data_ptr(), t.data_ptr()
+
+        def _publish(self, handles):
+            shared.slots[("h", rank)] = handles
+            shared.barrier.wait()
+            out = [shared.slots[("h", r)] for r in range(shared.P)]
+            shared.barrier.wait()
+            return out
+
+        def _open(self, handle):
+            return handle
+
+        def _barrier(self):
+            torch.cuda.synchronize()
+            shared.barrier.wait()
+
+        def gather_columns(self, slice_, plan):
+            torch.cuda.synchronize()
+            shared.slots[rank] = slice_
+            shared.barrier.wait()
+            parts = [shared.slots[r].clone() for r in range(shared.P)]
+            torch.cuda.synchronize()
+            shared.barrier.wait()
+            stacked = torch.stack([p.view(128, plan.m // 64) for p in parts], dim=1)
+            return stacked.reshape(-1).contiguous()
+
+    return ThreadPeerBackend()
+
+
+@pytest.mark.parametrize("P,la,lb", [(2, 1 << 20, 1 << 19), (4, 1 << 25, (1 << 25) - 5), (2, 1 << 26, 1 << 26)])
+def test_sharded_peer_exchange_on_one_gpu(gpu, port, checker, P, la, lb):
+    """The peer-memory exchange (PeerBackend, fpm_bfly_pair_peer_dev: ping-pong buffers, the
+    partner's half read directly by the pair kernel), both for small cosets (stand-alone stage
+    kernels) and for >= 2^18-element cosets (tower fast path); two products per backend so the
+    buffers are reused."""
+    from paper_1803_11301_b200.dist import make_plan, polymul_sharded
+
+    a = port.random_bitpoly(la, 41)
+    b = port.random_bitpoly(lb, 42)
+    want = checker.polymul(a, la, b, lb)
+    shared = _Shared(P)
+    out, errs, keep = {}, [], []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            da = torch.from_numpy(a.view(np.int64).copy()).cuda()
+            db = torch.from_numpy(b.view(np.int64).copy()).cuda()
+            be = _make_peer_backend(shared, rank, keep)
+            plan = make_plan(la, lb, P, rank)
+            for _ in range(2):
+                res = polymul_sharded(da, la, db, lb, be, plan)
+            torch.cuda.synchronize()
+            out[rank] = res.cpu().numpy().view(np.uint64)
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append((rank, repr(e)))
+            shared.barrier.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    for r in range(P):
+        assert np.array_equal(out[r], want), r
+
+
+def test_pair_peer_matches_in_place_pair(gpu):
+    """fpm_bfly_pair_peer_dev (out-of-place, partner half from another buffer) equals the in-place
+    fpm_bfly_pair_dev for both sides and directions, polynomial and tower representation."""
+    import paper_1803_11301_b200._lib as L
+    n = 1 << 16
+    g = torch.Generator(device="cuda").manual_seed(5)
+    mine = torch.randint(-(1 << 62), 1 << 62, (2 * n,), generator=g, device="cuda", dtype=torch.int64)
+    theirs = torch.randint(-(1 << 62), 1 << 62, (2 * n,), generator=g, device="cuda", dtype=torch.int64)
+    w = np.array([0x0123456789ABCDEF, 0x0FEDCBA987654321], np.uint64)
+    s = torch.cuda.current_stream().cuda_stream
+    for tower in (0, 1):
+        for side in (0, 1):
+            for inv in (0, 1):
+                ref = mine.clone()
+                f = L.lib().fpm_bfly_pair_r_dev if tower else L.lib().fpm_bfly_pair_dev
+                L._check(f(ref.data_ptr(), theirs.data_ptr(), n, w.ctypes.data_as(L._u64p), side, inv, s))
+                out = torch.empty_like(mine)
+                L._check(L.lib().fpm_bfly_pair_peer_dev(mine.data_ptr(), theirs.data_ptr(), out.data_ptr(), n,
+                                                        w.ctypes.data_as(L._u64p), side, inv, tower, s))
+                torch.cuda.synchronize()
+                assert torch.equal(out, ref), (tower, side, inv)
