@@ -11,8 +11,9 @@ Contract (one JSON line on rank 0):
   --impl reference   times the reference's own CPU implementation instead (rank 0 only)
 
 Multi-GPU (torchrun, N>1): by default ONE product is sharded over the N GPUs
-(paper_1803_11301_b200/dist.py: the top log2 N butterfly layers exchange halves over NCCL P2P;
-"scaling": "strong"); --mode replicas runs N independent products instead ("weak").
+(paper_1803_11301_b200/dist.py: the top log2 N butterfly layers exchange halves -- over peer memory,
+the partner's half read inside the butterfly kernel (--exchange peer, default), or NCCL send/recv
+(--exchange nccl); "scaling": "strong"); --mode replicas runs N independent products ("weak").
 """
 from __future__ import annotations
 
