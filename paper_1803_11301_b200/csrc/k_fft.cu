@@ -104,9 +104,11 @@ __global__ void __launch_bounds__(256) fft_top_kernel(uint4* __restrict__ ev, un
 constexpr int kTop4Threads = 768;
 constexpr size_t kTop4Smem = (3 * (size_t)kM8Uint4 + 3 * 144 + 136) * sizeof(uint4);  // + to_r (tower)
 
-template <bool INV, bool R>
-__global__ void __launch_bounds__(kTop4Threads, 1) fft_top4_kernel(uint4* __restrict__ ev, unsigned l, unsigned i,
-                                                                   int qpc, TwiddleSrc tw) {
+// NT: 768 threads (80 registers; three table groups at once) or 512 (128 registers: the
+// pre-rotated lookups in both directions; the third table in a second build round).
+template <bool INV, bool R, int NT = kTop4Threads>
+__global__ void __launch_bounds__(NT, 1) fft_top4_kernel(uint4* __restrict__ ev, unsigned l, unsigned i,
+                                                          int qpc, TwiddleSrc tw) {
   extern __shared__ uint4 sm4[];
   uint4* t1 = sm4;                   // w(i+1, B)
   uint4* t0a = sm4 + kM8Uint4;       // w(i, 2B)
@@ -121,20 +123,21 @@ __global__ void __launch_bounds__(kTop4Threads, 1) fft_top4_kernel(uint4* __rest
     if (tid < 128) to_r[to_r_pad(tid)] = __ldg(tw.to_r + tid);
     __syncthreads();
   }
-  {
+  for (int g0 = 0; g0 < 3; g0 += NT / 256) {
+    const int g = g0 + grp;
     uint4 w = make_uint4(0, 0, 0, 0);
-    if (grp == 0) w = twiddle(tw, l, i + 1, B);
-    else if (grp == 1) w = twiddle(tw, l, i, 2 * B);
-    else if (grp == 2) w = twiddle(tw, l, i, 2 * B + 1);
-    uint4* tab = sm4 + grp * kM8Uint4;
-    uint4* rs = rows + grp * 144;
+    if (g == 0) w = twiddle(tw, l, i + 1, B);
+    else if (g == 1) w = twiddle(tw, l, i, 2 * B);
+    else if (g == 2) w = twiddle(tw, l, i, 2 * B + 1);
+    uint4* tab = sm4 + g * kM8Uint4;
+    uint4* rs = rows + g * 144;
     if (R) {
-      if (grp < 3) rows_r<true>(rs, w, lt, to_r);
-    } else if (grp < 3 && lt < 128) {
+      if (g < 3) rows_r<true>(rs, w, lt, to_r);
+    } else if (g < 3 && lt < 128) {
       rs[lt + (lt >> 3)] = gf_mul_xk(w, (unsigned)lt);
     }
     __syncthreads();
-    if (grp < 3) {
+    if (g < 3) {
       const int c = lt & 15, sv = lt >> 4;
       uint4 r[8];
 #pragma unroll
@@ -158,16 +161,25 @@ __global__ void __launch_bounds__(kTop4Threads, 1) fft_top4_kernel(uint4* __rest
   const M8Base mb = m8_base(t1, q);  // (inverse only)
   constexpr uint32_t kA = kM8Uint4 * 16u, kB = 2u * kM8Uint4 * 16u;  // t0a, t0b after t1
 #pragma unroll 1
-  for (int k = tid; k < qpc; k += kTop4Threads) {
+  for (int k = tid; k < qpc; k += NT) {
     uint4* p = base + j0 + k;
     uint4 a0 = p[0], a1 = p[h], a2 = p[2 * h], a3 = p[3 * h];
-    if (!INV) {  // (m8_mul_r here spills at the 80 registers of a 768-thread CTA: 12.8 vs 11.3 ms)
+    if (!INV && NT == 768) {  // (m8_mul_r here spills at the 80 registers of a 768-thread CTA: 12.8 vs 11.3 ms)
       a0 = x4(a0, m8_mul(t1, a2, q));
       a1 = x4(a1, m8_mul(t1, a3, q));
       a2 = x4(a2, a0);
       a3 = x4(a3, a1);
       a0 = x4(a0, m8_mul(t0a, a1, q));
       a2 = x4(a2, m8_mul(t0b, a3, q));
+      a1 = x4(a1, a0);
+      a3 = x4(a3, a2);
+    } else if (!INV) {
+      a0 = x4(a0, m8_mul_r(mb, a2, q));
+      a1 = x4(a1, m8_mul_r(mb, a3, q));
+      a2 = x4(a2, a0);
+      a3 = x4(a3, a1);
+      a0 = x4(a0, m8_mul_r(mb, a1, q, kA));
+      a2 = x4(a2, m8_mul_r(mb, a3, q, kB));
       a1 = x4(a1, a0);
       a3 = x4(a3, a2);
     } else {
@@ -707,6 +719,8 @@ void top_passes(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSr
   attr4.run([&] {
     set_smem(fft_top4_kernel<false, R>, kTop4Smem);
     set_smem(fft_top4_kernel<true, R>, kTop4Smem);
+    set_smem(fft_top4_kernel<false, R, 512>, kTop4Smem);
+    set_smem(fft_top4_kernel<true, R, 512>, kTop4Smem);
   });
   const uint64_t pairs = ((uint64_t)1 << l) / 2;
   uint64_t ppc = 4096;
@@ -726,8 +740,20 @@ void top_passes(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSr
   while (qpc > 1024 && quads / qpc < (uint64_t)sms() * 4) qpc /= 2;
   auto radix4 = [&](unsigned i) {
     const unsigned q = (unsigned)std::min<uint64_t>(qpc, (uint64_t)1 << i);
-    if (!inverse) fft_top4_kernel<false, R><<<(unsigned)(quads / q), kTop4Threads, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
-    else fft_top4_kernel<true, R><<<(unsigned)(quads / q), kTop4Threads, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
+    // forward: 512 threads (pre-rotated lookups without spills; 11.04 vs 11.22 ms at 2^32 bits);
+    // inverse: 768 (5.48 vs 5.51).  FPM_TOP4_THREADS=512/768 forces one width for both.
+    static const int knob = [] {
+      const char* e = std::getenv("FPM_TOP4_THREADS");
+      return e ? std::atoi(e) : 0;
+    }();
+    const int nt = knob == 512 || knob == 768 ? knob : (inverse ? kTop4Threads : 512);
+    if (nt == 512) {
+      if (!inverse) fft_top4_kernel<false, R, 512><<<(unsigned)(quads / q), 512, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
+      else fft_top4_kernel<true, R, 512><<<(unsigned)(quads / q), 512, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
+    } else {
+      if (!inverse) fft_top4_kernel<false, R><<<(unsigned)(quads / q), kTop4Threads, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
+      else fft_top4_kernel<true, R><<<(unsigned)(quads / q), kTop4Threads, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
+    }
     FPM_LAUNCH_CHECK();
   };
   const unsigned n = l - T;
