@@ -119,16 +119,23 @@ __global__ void __launch_bounds__(NT, 1) fft_top4_kernel(uint4* __restrict__ ev,
   const uint64_t quad0 = (uint64_t)blockIdx.x * qpc;  // qpc <= h: a CTA never straddles a block
   const uint64_t B = quad0 >> i;
   const int tid = threadIdx.x, grp = tid >> 8, lt = tid & 255;
+  // the twiddles (global loads) are issued before the to_r staging barrier: one L2 round trip, not two
+  constexpr int kRounds = (3 + NT / 256 - 1) / (NT / 256);
+  uint4 ws[kRounds];
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const int g = r * (NT / 256) + grp;
+    ws[r] = g == 0 ? twiddle(tw, l, i + 1, B)
+                   : g == 1 ? twiddle(tw, l, i, 2 * B) : g == 2 ? twiddle(tw, l, i, 2 * B + 1) : make_uint4(0, 0, 0, 0);
+  }
   if (R) {
     if (tid < 128) to_r[to_r_pad(tid)] = __ldg(tw.to_r + tid);
     __syncthreads();
   }
-  for (int g0 = 0; g0 < 3; g0 += NT / 256) {
-    const int g = g0 + grp;
-    uint4 w = make_uint4(0, 0, 0, 0);
-    if (g == 0) w = twiddle(tw, l, i + 1, B);
-    else if (g == 1) w = twiddle(tw, l, i, 2 * B);
-    else if (g == 2) w = twiddle(tw, l, i, 2 * B + 1);
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const int g = r * (NT / 256) + grp;
+    const uint4 w = ws[r];
     uint4* tab = sm4 + g * kM8Uint4;
     uint4* rs = rows + g * 144;
     if (R) {
