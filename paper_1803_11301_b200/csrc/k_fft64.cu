@@ -91,12 +91,13 @@ __global__ void __launch_bounds__(kTop4Threads64, 2) fft64_top4_kernel(uint2* __
   const uint64_t quad0 = (uint64_t)blockIdx.x * qpc;  // qpc <= h
   const uint64_t B = quad0 >> i;
   const int tid = threadIdx.x, grp = tid >> 7, lt = tid & 127;
+  // twiddle loads issued before the to_r staging barrier (one L2 round trip)
+  const uint2 w = grp == 0 ? twiddle64(tw, i + 1, B) : twiddle64(tw, i, 2 * B + (grp - 1));
   if (R) {
     if (tid < 64) to_r[to_r64_pad(tid)] = __ldg(tw.to_r + tid);
     __syncthreads();
   }
   {
-    const uint2 w = grp == 0 ? twiddle64(tw, i + 1, B) : twiddle64(tw, i, 2 * B + (grp - 1));
     uint2* tab = sm64 + grp * kG8Uint2;
     uint2* rs = rows + grp * kG8Rows;
     if (R) rows_r64(rs, w, lt, to_r);
