@@ -466,7 +466,13 @@ __device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, unsigned T,
     for (int h = 0; h < nblk; h += 128, ++k) {
       if (k + 1 < ntab) rows_r<true>(sm.rows[(k + 1) & 1], sm.wz[wz_of(k + 1)], tid, sm.to_r);
       const M8Base mb = m8_base(sm.tab, q);
-      for (int pp = tid; pp < (NT << lg); pp += blockDim.x) {
+      // warps 0-3 computed the next table's rows: they take one pair fewer than warps 4-7 (c = pairs
+      // per thread: threads 128..255 do c + 1, threads 0..127 do c - 1; consecutive threads keep
+      // consecutive pairs)
+      const int c = (NT << lg) >> 8;
+      const int pp0 = tid >= 128 ? tid - 128 : 128 * (c + 1) + tid, cnt = tid >= 128 ? c + 1 : c - 1;
+      for (int r = 0; r < cnt; ++r) {
+        const int pp = pp0 + 128 * r;
         const int p = pp & ((1 << lg) - 1), tt = pp >> lg;
         const int blk = h + (p >> i), j = p & ((1 << i) - 1);
         const int i0 = (blk << (i + 1)) + j + tt * n, i1 = i0 + (1 << i);
