@@ -140,3 +140,11 @@ def test_tower_representation_host_side(port, m):
         dr = int(conv(dpoly, to_r)[0])
         want = bytes(gf8(c, dr) for c in ur.tobytes()[: m // 8])
         assert conv(mul(u, dpoly), to_r).tobytes()[: m // 8] == want
+
+
+def test_shard_fast_path_threshold_host_side():
+    """fpm_shard_tower: a coset of 2^l elements runs the single-GPU tower pipeline exactly when the
+    product pipeline would (l >= 18: tile depth 10, both operands fused, tower tiles).  Host only."""
+    import paper_1803_11301_b200._lib as L
+    f = L.lib().fpm_shard_tower
+    assert [f(l) for l in (8, 14, 17, 18, 19, 22, 26, 30)] == [0, 0, 0, 1, 1, 1, 1, 1]
