@@ -590,7 +590,28 @@ __global__ void __launch_bounds__(kTowerThreads, FPM_TOWER_MINB) fft_tile_tower_
     m8_expand(sm.tab, sm.rows_to_poly, tid);
     __syncthreads();
     const M8Base mb = m8_base(sm.tab, q);
-    if (kPolyLayers) {
+    if (kPolyLayers == 1) {
+      // layer 0 forward on both operands, the pointwise product and inverse layer 0 act on the same
+      // pair (2p, 2p+1) with the same twiddle: one register pass, one prepared twiddle
+      for (int k = tid; k < 2 * n; k += blockDim.x) s[k] = m8_mul_r(mb, s[k], q);
+      __syncthreads();
+      const uint4 Z = twiddle(tw, l, 0, t << (T - 1));
+      for (int p = tid; p < n / 2; p += blockDim.x) {
+        const int i0 = tsw(2 * p), i1 = tsw(2 * p + 1);
+        const GfPrep wp = gf_prep(x4(Z, c2p2(tw.c2p, (uint64_t)p)));
+        uint4 a0 = s[i0], a1 = s[i1], b0 = s[n + i0], b1 = s[n + i1];
+        a0 = x4(a0, gf_mul_prep(wp, a1));
+        a1 = x4(a1, a0);
+        b0 = x4(b0, gf_mul_prep(wp, b1));
+        b1 = x4(b1, b0);
+        uint4 c0 = gf_mul(a0, b0), c1 = gf_mul(a1, b1);
+        c1 = x4(c1, c0);
+        c0 = x4(c0, gf_mul_prep(wp, c1));
+        s[i0] = c0;
+        s[i1] = c1;
+      }
+      __syncthreads();
+    } else if (kPolyLayers) {
       for (int k = tid; k < 2 * n; k += blockDim.x) s[k] = m8_mul_r(mb, s[k], q);
       __syncthreads();
       tile_layers_poly<false>(s, T, kPolyLayers, l, t, tw);
