@@ -183,3 +183,30 @@ def test_pair_peer_matches_in_place_pair(gpu):
                                                         w.ctypes.data_as(L._u64p), side, inv, tower, s))
                 torch.cuda.synchronize()
                 assert torch.equal(out, ref), (tower, side, inv)
+
+
+def test_tower_encode_decode_columns_match_polynomial(gpu):
+    """fpm_encode_cols_r_dev / fpm_decode_cols_r_dev (tower representation) against the polynomial
+    pair: decode_r(encode_r(x)) == decode(encode(x)) == x's column slice, for a column range and
+    rows >= 64 zero as in the pipeline."""
+    import paper_1803_11301_b200._lib as L
+    l, col0, m = 14, 4096, 8192
+    n_p = 1 << l
+    g = torch.Generator(device="cuda").manual_seed(9)
+    poly = torch.randint(-(1 << 62), 1 << 62, (128 * n_p // 64,), generator=g, device="cuda", dtype=torch.int64)
+    poly[64 * n_p // 64:] = 0  # rows >= 64 zero
+    s = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for r in (False, True):
+        ev = torch.empty(2 * m, dtype=torch.int64, device="cuda")
+        enc = L.lib().fpm_encode_cols_r_dev if r else L.lib().fpm_encode_cols_dev
+        dec = L.lib().fpm_decode_cols_r_dev if r else L.lib().fpm_decode_cols_dev
+        L._check(enc(poly.data_ptr(), l, col0, m, 64, ev.data_ptr(), s))
+        sl = torch.empty(128 * m // 64, dtype=torch.int64, device="cuda")
+        L._check(dec(ev.data_ptr(), m, sl.data_ptr(), s))
+        outs.append((ev.clone(), sl))
+    torch.cuda.synchronize()
+    assert not torch.equal(outs[0][0], outs[1][0])  # the two representations differ ...
+    assert torch.equal(outs[0][1], outs[1][1])      # ... and decode to the same bits
+    want = poly.view(128, n_p // 64)[:, col0 // 64:(col0 + m) // 64].reshape(-1)
+    assert torch.equal(outs[1][1], want)
