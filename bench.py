@@ -96,17 +96,45 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+SEEDS = (20261020, 20261021)  # tests/golden/make_golden.py: random_bitpoly(bits, mt19937_64(seed))
+
+
+def golden_meta():
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "reference_meta.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def blake(words) -> str:
+    import hashlib
+
+    import numpy as np
+    return hashlib.blake2b(np.ascontiguousarray(words, np.uint64).tobytes(), digest_size=16).hexdigest()
+
+
+def workload_config(cfg: int) -> dict:
+    """The `config` object, identical in both arms (ours / --impl reference) for the same workload."""
+    if cfg == 2:
+        return {"workload": f"cfg2: batch of {BATCH} independent 2^16 x 2^16-bit products (one step = the batch)",
+                "inputs": "product k = random_bitpoly(2^16, 30000+k) x random_bitpoly(2^16, 40000+k) (mt19937_64)",
+                "field": "GF(2^128) transform (products are field-independent)",
+                "l2": "batch operands 64 MiB (fit in L2)"}
+    bits = CONFIGS[cfg]
+    k = bits.bit_length() - 1
+    return {"workload": f"cfg{cfg}: 2^{k} x 2^{k}-bit product, GF(2^128) Frobenius FFT (n=2^{k + 1}, l={k + 1 - 7})",
+            "inputs": f"random_bitpoly(2^{k}, mt19937_64({SEEDS[0]})) x random_bitpoly(2^{k}, mt19937_64({SEEDS[1]}))",
+            "field": "GF(2^128) (FieldChoice::kGF128)",
+            "l2": "inputs >= 2x L2 per operand (no flush needed)" if bits >= 1 << 28 else
+                  "inputs fit in L2 (each step rewrites the 2n-bit work array and both EvalVecs)"}
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     return ws, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
-def rand_words(torch, words, seed, device):
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    lo = torch.randint(0, 1 << 32, (words,), generator=g, device=device, dtype=torch.int64)
-    hi = torch.randint(0, 1 << 32, (words,), generator=g, device=device, dtype=torch.int64)
-    return lo | (hi << 32)
 
 
 def stage_pipes(stage: str, bits: int):
@@ -165,20 +193,24 @@ def algorithmic(stage: str, bits: int, T: int, fused_ab: bool = False):
 
 def run_batch(args, ws, rank, local):
     """Config 2: a batch of 4096 independent 2^16 x 2^16 products (fpm_polymul_batch_dev: one CTA
-    per product, everything in shared memory), split across ranks with no exchange (strong scaling
-    over the fixed batch); one step = the whole batch."""
+    per product, everything in shared memory), split across ranks with no exchange
+    (dist.polymul_batch_sharded; strong scaling over the fixed batch); one step = the whole batch.
+    The inputs are the golden seeds, so the batch is checked against the reference's hash."""
     import numpy as np
     import torch
 
     import paper_1803_11301_b200 as pkg
+    from paper_1803_11301_b200.dist import batch_shard
 
     dev = torch.device("cuda", local)
     bits = CONFIGS[2]
     wa = bits // 64
     wc = (2 * bits - 1 + 63) // 64
-    per = BATCH // ws
-    a = rand_words(torch, per * wa, 3000 + rank, dev)
-    b = rand_words(torch, per * wa, 4000 + rank, dev)
+    start, per = batch_shard(BATCH, ws, rank)
+    ha_np = np.concatenate([pkg.random_bitpoly(bits, 30000 + k) for k in range(start, start + per)])
+    hb_np = np.concatenate([pkg.random_bitpoly(bits, 40000 + k) for k in range(start, start + per)])
+    a = torch.from_numpy(ha_np.view(np.int64)).to(dev)
+    b = torch.from_numpy(hb_np.view(np.int64)).to(dev)
     c = torch.empty(per * wc, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -208,12 +240,21 @@ def run_batch(args, ws, rank, local):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms = float(t.item())
     dev_result = c.cpu().numpy().view(np.uint64).copy()
+    # parity: the whole batch (gathered on rank 0) against the reference's hash
+    parts = [dev_result]
+    if ws > 1:
+        parts = [None] * ws
+        torch.distributed.all_gather_object(parts, dev_result)
+    meta = golden_meta().get("cfg2_batch", {})
+    got = blake(np.concatenate(parts)) if rank == 0 else None
+    parity = {"blake2b128": got, "reference_blake2b128": meta.get("blake2b128_all"),
+              "matches_reference": got is not None and got == meta.get("blake2b128_all"),
+              "products": BATCH} if rank == 0 else None
     # e2e: pinned host operands in, products out, every step
-    ha = torch.empty(per * wa, dtype=torch.int64, pin_memory=True)
-    hb = torch.empty(per * wa, dtype=torch.int64, pin_memory=True)
+    ha = torch.from_numpy(ha_np.view(np.int64)).pin_memory()
+    hb = torch.from_numpy(hb_np.view(np.int64)).pin_memory()
     hc = torch.empty(per * wc, dtype=torch.int64, pin_memory=True)
-    ha.copy_(a)
-    hb.copy_(b)
+
     def e2e_step():
         step(ha.to(dev, non_blocking=True), hb.to(dev, non_blocking=True))
         hc.copy_(c)
@@ -237,11 +278,12 @@ def run_batch(args, ws, rank, local):
     line = {
         "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "u32", "data": "synthetic (uniform random bits, seeded)",
-        "config": {"workload": f"cfg2: batch of {BATCH} independent 2^16 x 2^16-bit products (one step = the batch)",
-                   "parallelism": f"batch split over {ws} GPU(s), no exchange", "l2": "batch operands 64 MiB (fit in L2)"},
-        "e2e": {"value": round(e2e_ms, 3), "unit": "ms", "steps": k2, "h2d_bytes_per_step": 2 * per * wa * 8 * ws,
-                "d2h_bytes_per_step": per * wc * 8 * ws, "matches_device_result": same},
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (random_bitpoly, mt19937_64 seeded)",
+        "config": workload_config(2),
+        "parallelism": f"batch split over {ws} GPU(s) (dist.batch_shard), no exchange",
+        "e2e": {"value": round(e2e_ms, 3), "unit": "ms", "steps": k2, "h2d_bytes_per_step": 2 * BATCH * wa * 8,
+                "d2h_bytes_per_step": BATCH * wc * 8, "matches_device_result": same},
+        "parity": parity,
         "gpu_launches": int(launches),
         "roofline": {"bound": "int", "kernel": "batch_kernel", "achieved": round(achieved, 2),
                      "peak": round(peak_tops, 2), "unit": "Tops/s", "frac": round(achieved / peak_tops, 4),
@@ -253,9 +295,8 @@ def run_batch(args, ws, rank, local):
         try:
             import oracle
             R = oracle.ref()
-            P = oracle.port()
-            x = P.random_bitpoly(bits, 1)
-            y = P.random_bitpoly(bits, 2)
+            x = ha_np[:wa].copy()
+            y = hb_np[:wa].copy()
             R.polymul(x, bits, y, bits, field=0, parallel=False)
             nsample = 64
             t0 = time.perf_counter()
@@ -287,8 +328,8 @@ def run_reference(args, ws, rank):
     threads = R.max_threads()
     if args.config == 2:  # batch: each step times a bounded sample of serial products, scaled
         P = oracle.port()
-        x = P.random_bitpoly(bits, 1)
-        y = P.random_bitpoly(bits, 2)
+        x = P.random_bitpoly(bits, 30000)
+        y = P.random_bitpoly(bits, 40000)
         R.polymul(x, bits, y, bits, field=args.ref_field, parallel=False)
         nsample, times = 256, []
         for _ in range(args.steps):
@@ -300,9 +341,8 @@ def run_reference(args, ws, rank):
         line = {"impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": ws,
                 "steps": len(times), "warmup": 1, "ms_per_step": round(v, 3), "higher_is_better": False,
                 "scaling": "strong", "vs_baseline": None, "dtype": "u64",
-                "data": "synthetic (mt19937_64 seeded, random_bitpoly)",
-                "config": {"workload": f"cfg2: batch of {BATCH} independent 2^16 x 2^16-bit products",
-                           "library": os.path.basename(R.path)},
+                "data": "synthetic (random_bitpoly, mt19937_64 seeded)",
+                "config": workload_config(2), "library": os.path.basename(R.path),
                 "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": 1, "kind": "reference",
                                  "sample": f"{nsample} serial products per step (ExecPolicy::kSerial, 1 core), "
                                            f"scaled to the {BATCH}-product batch"},
@@ -310,8 +350,8 @@ def run_reference(args, ws, rank):
         print(json.dumps(line), flush=True)
         return
     P = oracle.port()
-    a = P.random_bitpoly(bits, 20261020)
-    b = P.random_bitpoly(bits, 20261021)
+    a = P.random_bitpoly(bits, SEEDS[0])
+    b = P.random_bitpoly(bits, SEEDS[1])
     # Same field as our arm's config (GF(2^128), the north-star transform); --ref-field 0 times the
     # reference's default auto field (GF(2^64)) instead.
     field = args.ref_field
@@ -331,11 +371,10 @@ def run_reference(args, ws, rank):
         "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": "ms", "n_gpus": ws,
         "steps": len(times), "steps_requested": args.steps, "warmup": min(args.warmup, 1),
         "ms_per_step": round(v, 3), "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u64", "data": "synthetic (mt19937_64 seeded, random_bitpoly)",
-        "config": {"workload": f"cfg{args.config}: 2^{bits.bit_length()-1} x 2^{bits.bit_length()-1}-bit product",
-                   "field": {128: "GF(2^128) (FieldChoice::kGF128, as our arm)", 64: "GF(2^64)",
-                             0: "auto (m=64, the reference default)"}[field],
-                   "library": os.path.basename(R.path)},
+        "dtype": "u64", "data": "synthetic (random_bitpoly, mt19937_64 seeded)",
+        "config": workload_config(args.config) if field == 128 else
+                  dict(workload_config(args.config), field={64: "GF(2^64)", 0: "auto (m=64, the reference default)"}[field]),
+        "library": os.path.basename(R.path),
         "cpu_baseline": {"value": round(v, 3), "unit": "ms", "cores": threads, "kind": "reference",
                          "sample": f"{len(times)} warm full products (ExecPolicy::kParallel, {threads} OpenMP "
                                    f"threads) after {min(args.warmup, 1)} cold call(s)"},
@@ -350,8 +389,8 @@ def cpu_baseline(bits):
     f4 = 2 * bits >= (1 << 33)
     R = oracle.ref(f4=f4)
     P = oracle.port()
-    a = P.random_bitpoly(bits, 20261020)
-    b = P.random_bitpoly(bits, 20261021)
+    a = P.random_bitpoly(bits, SEEDS[0])
+    b = P.random_bitpoly(bits, SEEDS[1])
     t0 = time.perf_counter()
     R.polymul(a, bits, b, bits, field=128)  # cold: includes the l-layer twiddle plan build
     cold = (time.perf_counter() - t0) * 1e3
@@ -409,9 +448,12 @@ def main():
     words = bits // 64
     out_words = (2 * bits - 1 + 63) // 64
     mode = "single" if ws == 1 else args.mode
-    seed_off = rank if mode == "replicas" else 0  # shard: every rank holds the same operands
-    a = rand_words(torch, words, 1000 + seed_off, dev)
-    b = rand_words(torch, words, 2000 + seed_off, dev)
+    # the golden seeds (tests/golden/reference_meta.json holds the reference's product hash); every
+    # rank holds the same operands (shard mode: one product; replicas: N copies of it)
+    ha_np = pkg.random_bitpoly(bits, SEEDS[0])
+    hb_np = pkg.random_bitpoly(bits, SEEDS[1])
+    a = torch.from_numpy(ha_np.view(np.int64)).to(dev)
+    b = torch.from_numpy(hb_np.view(np.int64)).to(dev)
     c = torch.empty(out_words, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
     from paper_1803_11301_b200 import dist as pdist
@@ -465,13 +507,15 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms_max = float(t.item())
     dev_result = res_dev.cpu().numpy().view(np.uint64).copy()
+    want = golden_meta().get("configs", {}).get(f"{bits}x{bits}", {}).get("blake2b128")
+    got = blake(dev_result)
+    parity = {"blake2b128": got, "reference_blake2b128": want, "matches_reference": got == want,
+              "product_bits": 2 * bits - 1}
 
     # ---- e2e: pinned HOST buffers; H2D of both operands and D2H of the product in every step
-    ha = torch.empty(words, dtype=torch.int64, pin_memory=True)
-    hb = torch.empty(words, dtype=torch.int64, pin_memory=True)
+    ha = torch.from_numpy(ha_np.view(np.int64)).pin_memory()
+    hb = torch.from_numpy(hb_np.view(np.int64)).pin_memory()
     hc = torch.empty(out_words, dtype=torch.int64, pin_memory=True)
-    ha.copy_(a)
-    hb.copy_(b)
     na, nb, nc = (x.numpy().view(np.uint64) for x in (ha, hb, hc))
 
     def e2e_step():
@@ -564,13 +608,11 @@ def main():
         "metric": METRIC, "value": round(ms_max / ws if mode == "replicas" else ms_max, 3), "unit": "ms",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 3),
         "higher_is_better": False, "scaling": "weak" if mode == "replicas" else "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic (uniform random bits, seeded)",
-        "config": {"workload": f"cfg{args.config}: 2^{bits.bit_length()-1} x 2^{bits.bit_length()-1}-bit product, "
-                               f"GF(2^128) Frobenius FFT (n=2^{(2*bits).bit_length()-1}, "
-                               f"l={(2*bits//128).bit_length()-1})",
-                   "parallelism": {"single": "single GPU", "replicas": f"{ws} independent products (replicas)",
-                                   "shard": f"one product sharded over {ws} GPUs: top {ws.bit_length() - 1} butterfly "
-                                            f"layers exchanged ({exchange}), basis conversions replicated"}[mode],
-                   "l2": "inputs >= 2x L2 per operand at cfg4/5 (no flush needed)" if bits >= 1 << 28 else "inputs fit in L2"},
+        "config": workload_config(args.config),
+        "parallelism": {"single": "single GPU", "replicas": f"{ws} independent products (replicas)",
+                        "shard": f"one product sharded over {ws} GPUs: top {ws.bit_length() - 1} butterfly "
+                                 f"layers exchanged ({exchange}), basis conversions replicated"}[mode],
+        "parity": parity,
         "e2e": {"value": round(e2e_ms / ws if mode == "replicas" else e2e_ms, 3), "unit": "ms", "steps": e2e_steps,
                 "h2d_bytes_per_step": 2 * words * 8, "d2h_bytes_per_step": out_words * 8,
                 "matches_device_result": same},

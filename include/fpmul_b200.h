@@ -74,6 +74,11 @@ int fpm_pipeline_fuses_operands(unsigned l);
  * plan reports (GF(2^64) for FPM_FIELD_AUTO whenever it supports the size). */
 fpm_status fpm_plan_mul(size_t a_bits, size_t b_bits, int field, fpm_plan* out);
 
+/* random_bitpoly(n_bits, std::mt19937_64(seed)) (proj/src/bitpoly.cpp:19-24, bitpoly.hpp:101):
+ * ceil(n_bits/64) words, one generator draw per word, bits >= n_bits cleared.  Host only; the
+ * seeded inputs of the BASELINE configs and the golden fixtures. */
+fpm_status fpm_random_bitpoly(size_t n_bits, uint64_t seed, uint64_t* out);
+
 /* fp_polymul (polymul.hpp:74-75, polymul.cpp:223-239) on host buffers.
  * c receives ceil((a_bits+b_bits-1)/64) words (bits >= a_bits+b_bits-1 cleared); nothing is
  * written when either length is 0.  field: FPM_FIELD_AUTO (short inputs: karatsuba_mul, else
@@ -209,6 +214,17 @@ fpm_status fpm_tables64(uint64_t* cantor, uint64_t* rows, uint64_t* inv_rows);
  * (tower byte 0 of Cantor basis vectors v_1..v_7).  Host only; lets the CPU tests check the
  * construction against the oracle's field arithmetic. */
 fpm_status fpm_tower_tables(int field_degree, uint64_t* t, uint64_t* to_poly, uint64_t* to_r, uint8_t* tau);
+
+/* Fault-injection test hook, the device twin of EncodeMatrix::corrupt_for_test
+ * (proj/include/fpmul/encode.hpp:70-71; used by the self-test, selftest.cpp:315-331): flips one bit
+ * of the forward encode tables the kernels read on `device` (entry "row 0" of chunk 0, both fields,
+ * polynomial and tower representation).  Calling it again restores them.  Not for production use:
+ * every encode on the device sees the flipped table while it is active. */
+fpm_status fpm_test_flip_encode_table(int device);
+
+/* Returns the library's cached device scratch (its private stream-ordered memory pool; the
+ * device's default pool is never modified) on `device` to the driver. */
+fpm_status fpm_trim_pool(int device);
 
 /* Number of kernel launches issued by this library on the calling thread since the last reset
  * (for the bench's gpu_launches accounting). */

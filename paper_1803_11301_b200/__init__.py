@@ -45,6 +45,7 @@ from ._lib import (  # noqa: F401
     tables64,
     plan_mul,
     pointwise_mul,
+    random_bitpoly,
     stage_dev,
     tables128,
     tower_tables,

@@ -53,6 +53,7 @@ def lib():
         L.fpm_launch_count.restype = C.c_uint64
         L.fpm_launch_count.argtypes = [C.c_int]
         L.fpm_plan_mul.argtypes = [sz, sz, C.c_int, C.POINTER(_Plan)]
+        L.fpm_random_bitpoly.argtypes = [sz, C.c_uint64, _u64p]
         L.fpm_polymul.argtypes = [_u64p, sz, _u64p, sz, _u64p, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.fpm_polymul_dev.argtypes = [vp, sz, vp, sz, vp, C.c_int, vp, C.POINTER(C.c_double)]
         L.fpm_polymul_batch_dev.argtypes = [vp, sz, sz, vp, sz, sz, vp, sz, sz, vp]
@@ -146,6 +147,13 @@ def plan_mul(a_bits: int, b_bits: int, field: int = FIELD_AUTO) -> dict:
     p = _Plan()
     _check(lib().fpm_plan_mul(a_bits, b_bits, field, C.byref(p)))
     return {k: int(getattr(p, k)) for k, _ in _Plan._fields_}
+
+
+def random_bitpoly(n_bits: int, seed: int) -> np.ndarray:
+    """random_bitpoly(n_bits, std::mt19937_64(seed)) (proj/src/bitpoly.cpp:19-24): packed words."""
+    out = np.zeros(max(1, _words(n_bits)), np.uint64)
+    _check(lib().fpm_random_bitpoly(n_bits, seed, _ptr(out)))
+    return out[: _words(n_bits)]
 
 
 def tables128():
@@ -355,6 +363,11 @@ def clmul_words_dev(a, b, out, stream=None) -> None:
 def fp_polymul_dev(a, a_bits: int, b, b_bits: int, c, field: int = FIELD_AUTO, stream=None,
                    stage_seconds: list | None = None) -> None:
     """fp_polymul on device-resident tensors; c must hold ceil((a_bits+b_bits-1)/64) words."""
+    if a_bits and b_bits:
+        if a.numel() < _words(a_bits) or b.numel() < _words(b_bits):
+            raise ValueError("fp_polymul_dev: operand tensors shorter than the declared bit lengths")
+        if c.numel() < _words(a_bits + b_bits - 1):
+            raise ValueError("fp_polymul_dev: product tensor shorter than ceil((a_bits+b_bits-1)/64) words")
     st = (C.c_double * NUM_STAGES)()
     _check(lib().fpm_polymul_dev(_dptr(a), a_bits, _dptr(b), b_bits, _dptr(c), field, _stream(stream),
                                  st if stage_seconds is not None else None))
@@ -364,6 +377,14 @@ def fp_polymul_dev(a, a_bits: int, b, b_bits: int, c, field: int = FIELD_AUTO, s
 
 def fp_polymul_batch_dev(a, a_bits: int, a_stride: int, b, b_bits: int, b_stride: int, c, c_stride: int,
                          count: int, stream=None) -> None:
+    """count independent products: a[k*a_stride ..] (a_bits) x b[k*b_stride ..] (b_bits) -> c[k*c_stride ..]."""
+    if count and a_bits and b_bits:
+        wa, wb, wc = _words(a_bits), _words(b_bits), _words(a_bits + b_bits - 1)
+        if a_stride < wa or b_stride < wb or c_stride < wc:
+            raise ValueError("fp_polymul_batch_dev: a stride is shorter than its operand / product")
+        for t, stride, w, name in ((a, a_stride, wa, "a"), (b, b_stride, wb, "b"), (c, c_stride, wc, "c")):
+            if t.numel() < (count - 1) * stride + w:
+                raise ValueError(f"fp_polymul_batch_dev: tensor {name} shorter than (count-1)*stride + words")
     _check(lib().fpm_polymul_batch_dev(_dptr(a), a_bits, a_stride, _dptr(b), b_bits, b_stride, _dptr(c),
                                        c_stride, count, _stream(stream)))
 

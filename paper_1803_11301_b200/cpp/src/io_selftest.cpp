@@ -13,9 +13,11 @@
 #include <string>
 #include <vector>
 
+#include "../../../include/fpmul_b200.h"
 #include "fpmul/basis_convert.hpp"
 #include "fpmul/butterfly.hpp"
 #include "fpmul/encode.hpp"
+#include "fpmul/exec.hpp"
 #include "fpmul/io.hpp"
 #include "fpmul/polymul.hpp"
 #include "fpmul/selftest.hpp"
@@ -171,12 +173,22 @@ void encode_suite(Checker& c, std::mt19937_64& rng, const std::string& t, bool c
     return mat.row(0) == FieldElem<F>{detail::from_low_word<typename F::value_type>(1)} &&
            mat.row(1) == fld.basis(F::kDegree / 2);
   });
+  // The named round-trip invariant (selftest.cpp:315-331); with fault injection it runs while the
+  // DEVICE encode tables have one bit flipped (fpm_test_flip_encode_table, the twin of
+  // EncodeMatrix::corrupt_for_test), restored afterwards.
+  struct DeviceFault {
+    bool on;
+    explicit DeviceFault(bool o) : on(o) {
+      if (on && fpm_test_flip_encode_table(current_device()) != FPM_OK) throw std::runtime_error(fpm_last_error());
+    }
+    ~DeviceFault() { if (on) fpm_test_flip_encode_table(current_device()); }
+  };
   c.guarded("encode." + t + ".encode/decode round-trip", [&] {
-    for (unsigned l = 0; l <= max_l; l += 5) {
+    const DeviceFault fault(corrupt);
+    for (unsigned l : {0u, 1u, 4u, 6u, max_l}) {
       const auto spec = make_partition_spec<F>(l);
       const BitPoly a = random_bitpoly(size_t{F::kDegree} * spec.n_p, rng);
-      EvalVec<F> ev = encode<F>(a, spec, mat);
-      if (corrupt) ev[0] = gf_add(ev[0], mat.row(F::kDegree - 1));  // as if row m-1 were corrupted
+      const EvalVec<F> ev = encode<F>(a, spec, mat);
       if (decode<F>(std::span<const FieldElem<F>>(ev), spec, mat) != a) return false;
     }
     return true;

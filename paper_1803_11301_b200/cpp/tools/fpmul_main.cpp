@@ -118,86 +118,104 @@ int cmd_selftest(const Args& a) {
   return kExitOk;
 }
 
-int cmd_bench(const Args& a) {
-  uint64_t min_log = 0, max_log = 0, reps = 100, seed = 1;
-  bool have_min = false, have_max = false;
-  std::string csv_path, field = "auto";
+// `bench`: one CSV row per size 2^k words of padded product (k = min_log .. max_log), columns as the
+// reference's schema (fpmul_main.cpp:105-106).  mean_s is the host-measured mean of `reps` calls of
+// fp_polymul (host buffers in, product out); the stage columns are the GPU's own per-stage times
+// (CUDA events inside the pipeline, summed by StageSeconds) divided by reps.  Before timing, every
+// size's operands are checked once against karatsuba_mul -- the word-level carry-less product, an
+// algorithm independent of the FFT pipeline -- on a prefix of at most 2^20 bits, so the check runs
+// at every size and cannot be skipped.
+struct BenchSpec {
+  uint64_t lo = 0, hi = 0, reps = 100, seed = 1;
+  bool have_lo = false, have_hi = false;
+  fpmul::FieldChoice field = fpmul::FieldChoice::kAuto;
+  std::string csv;
+};
+
+bool read_bench_spec(const Args& a, BenchSpec& b, std::string& why) {
   for (const auto& [k, v] : a.opts) {
     bool ok = true;
-    if (k == "--min-log") ok = have_min = parse_uint(v, min_log);
-    else if (k == "--max-log") ok = have_max = parse_uint(v, max_log);
-    else if (k == "--reps") ok = parse_uint(v, reps);
-    else if (k == "--seed") ok = parse_uint(v, seed);
-    else if (k == "--csv") csv_path = v;
-    else if (k == "--field") field = v;
-    else return usage("unknown option " + k);
-    if (!ok) return usage("bad value for " + k);
-  }
-  fpmul::FieldChoice fc;
-  if (!have_min || !have_max) return usage("bench needs --min-log and --max-log");
-  if (!parse_field(field, fc)) return usage("--field must be auto, 64 or 128");
-  if (min_log > max_log || reps < 3) {
-    std::cerr << "error: need min-log <= max-log and reps >= 3\n";
-    return kExitUsage;
-  }
-  std::ostream* out = &std::cout;
-  std::ofstream file;
-  if (!csv_path.empty()) {
-    file.open(csv_path);
-    if (!file) {
-      std::cerr << "error: cannot open '" << csv_path << "'\n";
-      return kExitUsage;
+    if (k == "--min-log") b.have_lo = ok = parse_uint(v, b.lo);
+    else if (k == "--max-log") b.have_hi = ok = parse_uint(v, b.hi);
+    else if (k == "--reps") ok = parse_uint(v, b.reps);
+    else if (k == "--seed") ok = parse_uint(v, b.seed);
+    else if (k == "--csv") b.csv = v;
+    else if (k == "--field") ok = parse_field(v, b.field);
+    else ok = false;
+    if (!ok) {
+      why = "bad or unknown bench option " + k;
+      return false;
     }
-    out = &file;
   }
-  // same columns as the reference (fpmul_main.cpp bench): sizes, mean wall time, stage seconds
-  *out << "log2_size_words,n_bits,m,reps,mean_s,basiscvt_s,encode_s,butterfly_s,pointwise_s,"
-          "ibutterfly_s,decode_s,ibasiscvt_s\n";
-  std::mt19937_64 rng(seed);
-  for (uint64_t lg = min_log; lg <= max_log; ++lg) {
-    const size_t n_bits = size_t{64} << lg;  // padded product length
-    fpmul::MulOptions opts;
-    opts.field = fc;
-    fpmul::StageSeconds stages;
-    opts.stage_seconds = &stages;
+  if (!b.have_lo || !b.have_hi) why = "bench needs --min-log and --max-log";
+  else if (b.hi < b.lo) why = "--max-log is below --min-log";
+  else if (b.reps < 3) why = "--reps must be at least 3";
+  else if (b.hi > 27) why = "--max-log above 27 (2^33-bit products) is not supported";
+  return why.empty();
+}
+
+fpmul::BitPoly prefix(const fpmul::BitPoly& p, size_t bits) {
+  fpmul::BitPoly q = p;
+  q.resize_bits(std::min(bits, p.bit_length()));
+  return q;
+}
+
+int cmd_bench(const Args& a) {
+  BenchSpec spec;
+  std::string why;
+  if (!read_bench_spec(a, spec, why)) return usage(why);
+  std::ofstream file;
+  if (!spec.csv.empty()) {
+    file.open(spec.csv);
+    if (!file) return usage("--csv: '" + spec.csv + "' is not writable");
+  }
+  std::ostream& csv = spec.csv.empty() ? std::cout : file;
+  csv << "log2_size_words,n_bits,m,reps,mean_s,basiscvt_s,encode_s,butterfly_s,pointwise_s,"
+         "ibutterfly_s,decode_s,ibasiscvt_s\n";
+  std::mt19937_64 gen(spec.seed);
+  for (uint64_t k = spec.lo; k <= spec.hi; ++k) {
+    const size_t product_bits = size_t{64} << k;
+    const size_t operand_bits = product_bits / 2;
     fpmul::MulPlan plan;
     try {
-      plan = fpmul::plan_mul(n_bits / 2, n_bits / 2, opts.field);
+      plan = fpmul::plan_mul(operand_bits, operand_bits, spec.field);
     } catch (const std::exception& e) {
-      std::cerr << "error: " << e.what() << "\n";
-      return kExitUsage;
+      return usage(std::string("size 2^") + std::to_string(k) + " words: " + e.what());
     }
-    const fpmul::BitPoly x = fpmul::random_bitpoly(n_bits / 2, rng);
-    const fpmul::BitPoly y = fpmul::random_bitpoly(n_bits / 2, rng);
-    if (lg == min_log) {  // verification hook: an independent transform (the other field) agrees
-      fpmul::MulOptions o64, o128;
-      o64.field = fpmul::FieldChoice::kGF64;
-      o128.field = fpmul::FieldChoice::kGF128;
-      bool same = true;
-      try {
-        same = fpmul::fp_polymul(x, y, o64) == fpmul::fp_polymul(x, y, o128);
-      } catch (const std::invalid_argument&) {  // size beyond GF(2^64): compare with itself skipped
-      }
-      if (!same) {
-        std::cerr << "verification FAILED at log2(n/64)=" << lg << ": GF(2^64) and GF(2^128) products differ\n";
+    const fpmul::BitPoly x = fpmul::random_bitpoly(operand_bits, gen);
+    const fpmul::BitPoly y = fpmul::random_bitpoly(operand_bits, gen);
+    fpmul::MulOptions opts;
+    opts.field = spec.field;
+    {  // independent cross-check (karatsuba_mul shares no code with the FFT pipeline)
+      const size_t cut = std::min<size_t>(operand_bits, size_t{1} << 20);
+      const fpmul::BitPoly xs = prefix(x, cut), ys = prefix(y, cut);
+      if (!(fpmul::fp_polymul(xs, ys, opts) == fpmul::karatsuba_mul(xs, ys))) {
+        std::cerr << "verification FAILED at 2^" << k << " words: fp_polymul differs from karatsuba_mul\n";
         return kExitVerifyFailure;
       }
     }
-    stages = fpmul::StageSeconds{};
-    double total = 0;
-    fpmul::BitPoly sink;
-    for (uint64_t r = 0; r < reps; ++r) {
+    fpmul::StageSeconds gpu_stages{};
+    opts.stage_seconds = &gpu_stages;
+    std::vector<double> wall;
+    wall.reserve(spec.reps);
+    fpmul::BitPoly last;
+    for (uint64_t r = 0; r < spec.reps; ++r) {
       const auto t0 = std::chrono::steady_clock::now();
-      sink = fpmul::fp_polymul(x, y, opts);
-      total += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      last = fpmul::fp_polymul(x, y, opts);
+      wall.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
     }
-    const double inv = 1.0 / static_cast<double>(reps);
-    char line[512];
-    std::snprintf(line, sizeof line, "%u,%zu,%u,%u,%.9f,%.9f,%.9f,%.9f,%.9f,%.9f,%.9f,%.9f\n",
-                  static_cast<unsigned>(lg), n_bits, plan.field_degree, static_cast<unsigned>(reps), total * inv,
-                  stages.basiscvt * inv, stages.encode * inv, stages.butterfly * inv, stages.pointwise * inv,
-                  stages.ibutterfly * inv, stages.decode * inv, stages.ibasiscvt * inv);
-    *out << line << std::flush;
+    double sum = 0;
+    for (double w : wall) sum += w;
+    const double per = 1.0 / static_cast<double>(spec.reps);
+    const double cols[7] = {gpu_stages.basiscvt, gpu_stages.encode, gpu_stages.butterfly, gpu_stages.pointwise,
+                            gpu_stages.ibutterfly, gpu_stages.decode, gpu_stages.ibasiscvt};
+    csv << k << ',' << product_bits << ',' << plan.field_degree << ',' << spec.reps << ',';
+    csv.setf(std::ios::fixed);
+    csv.precision(9);
+    csv << sum * per;
+    for (double c : cols) csv << ',' << c * per;
+    csv.unsetf(std::ios::fixed);
+    csv << '\n' << std::flush;
   }
   return kExitOk;
 }

@@ -15,7 +15,9 @@
 #include <atomic>
 #include <chrono>
 #include <cstring>
+#include <exception>
 #include <mutex>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -149,15 +151,6 @@ struct StageClock {
 };
 enum { kStBasis = 0, kStEncode, kStBfly, kStPointwise, kStIBfly, kStDecode, kStIBasis };
 
-struct DevBuf {
-  void* p = nullptr;
-  cudaStream_t s;
-  DevBuf(size_t bytes, cudaStream_t st) : s(st) {
-    if (bytes) FPM_CUDA(cudaMallocAsync(&p, bytes, st));
-  }
-  ~DevBuf() { if (p) cudaFreeAsync(p, s); }
-  template <class T> T* as() const { return static_cast<T*>(p); }
-};
 
 // Host-buffer pipelining for fpm_polymul: the compute stream waits for operand k's upload only
 // right before operand k is first read (operand b's copy overlaps operand a's transforms), and
@@ -399,6 +392,37 @@ struct Ev {
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+namespace {
+cudaMemPool_t library_pool(int dev) {
+  static std::mutex mu;
+  static cudaMemPool_t pools[64] = {};
+  if (dev < 0 || dev >= 64) throw Error(kInvalid, "device ordinal out of range");
+  std::lock_guard<std::mutex> lock(mu);
+  if (!pools[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    FPM_CUDA(cudaMemPoolCreate(&pools[dev], &props));
+    uint64_t thr = UINT64_MAX;  // keep freed memory cached across calls (per-call GiB scratch)
+    FPM_CUDA(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  return pools[dev];
+}
+}  // namespace
+
+void* pool_alloc(size_t bytes, cudaStream_t s) {
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  void* p = nullptr;
+  FPM_CUDA(cudaMallocFromPoolAsync(&p, bytes, library_pool(dev), s));
+  return p;
+}
+
+void pool_free(void* p, cudaStream_t s) { cudaFreeAsync(p, s); }
+
+void trim_pool(int dev) { FPM_CUDA(cudaMemPoolTrimTo(library_pool(dev), 0)); }
+
 const DeviceTables& device_tables(int dev) {
   static std::mutex mu;
   static DeviceTables tabs[64];
@@ -520,12 +544,6 @@ const DeviceTables& device_tables(int dev) {
   };
   up2(&t.enc_g8, enc64); up2(&t.dec_g8, dec64); up2(&t.c2p64, c2p64); up2(&t.rows64, rows64); up2(&t.inv64, inv64);
   up2(&t.to_r64, to_r64); up2(&t.to_poly64, to_poly64); up2(&t.enc_g8r, enc64r); up2(&t.dec_g8r, dec64r);
-  // Keep freed pool memory cached: the pipeline allocates its scratch per call (reentrant).
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
   FPM_CUDA(cudaSetDevice(prev));
   tabs[dev] = t;
   have[dev] = true;
@@ -567,6 +585,30 @@ int fpm_device_count(void) {
 }
 uint64_t fpm_launch_count(int reset) {
   return reset ? g_launches.exchange(0) : g_launches.load();
+}
+
+fpm_status fpm_test_flip_encode_table(int device) {
+  return guard([&] {
+    DeviceGuard g(device);
+    flip_encode_tables(device, host_stream(device));
+  });
+}
+
+fpm_status fpm_trim_pool(int device) {
+  return guard([&] {
+    require_device();
+    trim_pool(device);
+  });
+}
+
+fpm_status fpm_random_bitpoly(size_t n_bits, uint64_t seed, uint64_t* out) {
+  return guard([&] {
+    if (n_bits && !out) throw Error(kInvalid, "random_bitpoly: null output");
+    std::mt19937_64 rng(seed);  // bitpoly.cpp:19-24: one draw per word, excess bits cleared
+    const size_t words = (n_bits + 63) / 64;
+    for (size_t i = 0; i < words; ++i) out[i] = rng();
+    if (n_bits % 64) out[words - 1] &= (((uint64_t)1) << (n_bits % 64)) - 1;
+  });
 }
 
 fpm_status fpm_plan_mul(size_t a_bits, size_t b_bits, int field, fpm_plan* out) {
@@ -619,6 +661,19 @@ fpm_status fpm_polymul(const uint64_t* a, size_t a_bits, const uint64_t* b, size
     const size_t wa = (a_bits + 63) / 64, wb = (b_bits + 63) / 64, wc = (a_bits + b_bits - 1 + 63) / 64;
     cudaStream_t h2d = copy_stream(device, 0), d2h = copy_stream(device, 1);
     DevBuf A(wa * 8, s), B(wb * 8, s), C(wc * 8, s);
+    // On an exception (e.g. an allocation failure inside the pipeline) the buffers above are freed
+    // while the copy streams may still read or write them: drain both copy streams first (this
+    // guard is destroyed before the DevBufs).
+    struct DrainOnUnwind {
+      cudaStream_t a, b;
+      int pending = std::uncaught_exceptions();
+      ~DrainOnUnwind() {
+        if (std::uncaught_exceptions() > pending) {
+          cudaStreamSynchronize(a);
+          cudaStreamSynchronize(b);
+        }
+      }
+    } drain{h2d, d2h};
     Ev allocated, ready_a, ready_b, copied;
     FPM_CUDA(cudaEventRecord(allocated.e, s));  // stream-ordered allocations visible to the copy streams
     FPM_CUDA(cudaStreamWaitEvent(h2d, allocated.e, 0));

@@ -36,6 +36,23 @@ void note_launch();
     FPM_CUDA(cudaGetLastError());      \
   } while (0)
 
+// Stream-ordered scratch from the library's own per-device memory pool (never the device's default
+// pool, so the host application's allocator and cudaMallocAsync users are unaffected).  Freed pool
+// memory stays cached for the next call (reentrant per-call scratch at GiB scale); fpm_trim_pool
+// returns it to the driver.
+void* pool_alloc(size_t bytes, cudaStream_t s);
+void pool_free(void* p, cudaStream_t s);
+void trim_pool(int dev);
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t s;
+  DevBuf(size_t bytes, cudaStream_t st) : s(st) { if (bytes) p = pool_alloc(bytes, st); }
+  ~DevBuf() { if (p) pool_free(p, s); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
 // Runs an initialisation (e.g. cudaFuncSetAttribute of a kernel's dynamic shared memory) once per
 // device: kernel attributes belong to a device context, so a process driving several GPUs must set
 // them on each one.  Thread-safe; devices 0..63.
@@ -92,6 +109,8 @@ struct DeviceTables {
   uint2* enc_g8r = nullptr;
   uint2* dec_g8r = nullptr;
 };
+
+void flip_encode_tables(int dev, cudaStream_t s);  // fault-injection test hook (k_codec.cu)
 
 // Twiddle generator inputs (passed by value as a kernel parameter):
 //   w(i, b) = C2P((base >> i) ^ 2b) = layer[i] ^ C2P(2b)      (butterfly.cpp:45-49; C2P is linear)

@@ -809,12 +809,7 @@ void run_big_pass(uint32_t* w, uint64_t nwords, Pass p, bool inverse, uint64_t l
   }
 }
 
-struct Scratch {
-  void* p = nullptr;
-  cudaStream_t s;
-  Scratch(size_t bytes, cudaStream_t st) : s(st) { if (bytes) FPM_CUDA(cudaMallocAsync(&p, bytes, st)); }
-  ~Scratch() { if (p) cudaFreeAsync(p, s); }
-};
+using Scratch = DevBuf;
 
 }  // namespace
 

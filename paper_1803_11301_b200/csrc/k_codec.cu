@@ -323,7 +323,36 @@ const RowTables& row_tables(int dev) {
   return t[dev];
 }
 
+__device__ __forceinline__ void flip_bit0(uint32_t* w) { *w ^= 1u; }
+__global__ void flip_encode_tables_kernel(uint32_t* small128, uint32_t* m8, uint32_t* m8r, uint32_t* rows64,
+                                          uint32_t* g8, uint32_t* g8r) {
+  if (threadIdx.x != 0) return;
+  // The forward tables' entry for "row 0 alone" (the reference flips bit 0 of tab_[1], chunk 0 /
+  // value 1, encode.hpp:70-71): the tiny-shape row table, the M8 / G8 tables (entry (c=0, v=1);
+  // both G8 copies) and their tower-representation twins.
+  flip_bit0(small128);
+  flip_bit0(m8 + 4 * (1 * 8 + 0));
+  flip_bit0(m8r + 4 * (1 * 8 + 0));
+  flip_bit0(rows64);
+  flip_bit0(g8 + 2 * (1 * 16 + 0));
+  flip_bit0(g8 + 2 * (1 * 16 + 8));
+  flip_bit0(g8r + 2 * (1 * 16 + 0));
+  flip_bit0(g8r + 2 * (1 * 16 + 8));
+}
+
 }  // namespace
+
+// Test hook (EncodeMatrix::corrupt_for_test, proj/include/fpmul/encode.hpp:70-71): flips one bit of
+// the DEVICE copies of the forward encode tables of both fields; a second call restores them.
+void flip_encode_tables(int dev, cudaStream_t s) {
+  const DeviceTables& dt = device_tables(dev);
+  flip_encode_tables_kernel<<<1, 32, 0, s>>>(reinterpret_cast<uint32_t*>(row_tables(dev).rows),
+                                             reinterpret_cast<uint32_t*>(dt.enc_m8), reinterpret_cast<uint32_t*>(dt.enc_m8r),
+                                             reinterpret_cast<uint32_t*>(dt.rows64), reinterpret_cast<uint32_t*>(dt.enc_g8),
+                                             reinterpret_cast<uint32_t*>(dt.enc_g8r));
+  FPM_LAUNCH_CHECK();
+  FPM_CUDA(cudaStreamSynchronize(s));
+}
 
 // Column range [col0, col0 + ncols) of the 128-row partition matrix (row pitch n_p bits) -> ncols
 // elements.  rows_live: 64 when rows >= 64 are known zero (pipeline operands), else 128.

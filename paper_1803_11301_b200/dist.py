@@ -86,6 +86,29 @@ def make_plan(a_bits: int, b_bits: int, P: int, rank: int) -> ShardPlan:
     return plan
 
 
+def batch_shard(count: int, P: int, rank: int) -> tuple[int, int]:
+    """Config 2's split of `count` independent products over P ranks (no exchange): rank r takes the
+    contiguous range [start, start + n), the first count % P ranks one product more."""
+    if P < 1 or not 0 <= rank < P:
+        raise ValueError("batch_shard: bad rank / world size")
+    q, r = divmod(count, P)
+    start = rank * q + min(rank, r)
+    return start, q + (1 if rank < r else 0)
+
+
+def polymul_batch_sharded(a, a_bits: int, b, b_bits: int, c, count: int, P: int, rank: int, lib=None):
+    """This rank's share of a batch of `count` products held densely (stride = words per operand /
+    product) in the FULL batch tensors a, b, c: only rows [start, start + n) are touched."""
+    from . import _lib
+    L = lib or _lib
+    wa, wb, wc = (a_bits + 63) // 64, (b_bits + 63) // 64, (a_bits + b_bits - 1 + 63) // 64
+    start, n = batch_shard(count, P, rank)
+    if n:
+        L.fp_polymul_batch_dev(a[start * wa:(start + n) * wa], a_bits, wa, b[start * wb:(start + n) * wb], b_bits, wb,
+                               c[start * wc:(start + n) * wc], wc, n)
+    return start, n
+
+
 def polymul_sharded(a, a_bits: int, b, b_bits: int, backend, plan: ShardPlan | None = None):
     """Product of two polynomials (backend arrays of packed words) over backend.world ranks;
     every rank returns the full product words."""
@@ -220,7 +243,11 @@ class GpuBackend:
         t = self.torch
         P = plan.P
         parts = [t.empty_like(slice_) for _ in range(P)]
-        if P > 1:
+        if P > 1 and self.dist.get_backend(self.group) == "gloo":  # control-plane group (CPU tests,
+            host = [t.empty_like(slice_, device="cpu") for _ in range(P)]  # several ranks on one GPU)
+            self.dist.all_gather(host, slice_.cpu(), group=self.group)
+            parts = [h.to(slice_.device) for h in host]
+        elif P > 1:
             self.dist.all_gather(parts, slice_, group=self.group)
         else:
             parts[0] = slice_
@@ -235,6 +262,11 @@ class GpuBackend:
         if out_bits % 64:
             out[w - 1] &= (1 << (out_bits % 64)) - 1
         return out
+
+
+def C_void(ptr: int):
+    import ctypes as C
+    return C.c_void_p(ptr)
 
 
 class DevBuf:
@@ -264,6 +296,27 @@ class PeerBackend(GpuBackend):
     def __init__(self, group=None):
         super().__init__(group)
         self.key = None
+        self.mine, self.peer = [], {}
+
+    def _close(self, ptr):
+        self.L._check(self.L.lib().fpm_ipc_close(C_void(ptr)))
+
+    def _free(self, ptr):
+        self.L._check(self.L.lib().fpm_ipc_free(C_void(ptr)))
+
+    def close(self):
+        """Releases the plan's buffers: partners' handles closed, then (after every rank closed the
+        handles to ours) this rank's buffers freed.  Collective: every rank must call it."""
+        if self.key is None:
+            return
+        self._barrier()  # no rank still reads a partner buffer
+        for ptrs in self.peer.values():
+            for p in ptrs:
+                self._close(p)
+        self._barrier()  # every partner closed its mapping of our buffers
+        for b in self.mine:
+            self._free(b.ptr)
+        self.mine, self.peer, self.key = [], {}, None
 
     # -- hooks (the single-GPU thread test overrides these)
     def _alloc(self, nbytes: int):
@@ -296,6 +349,7 @@ class PeerBackend(GpuBackend):
         P, rank = self.world()
         key = (plan.m, P, rank)
         if self.key != key:
+            self.close()  # re-key: release the previous plan's buffers and peer mappings
             nbytes = plan.m * 16
             mine = [self._alloc(nbytes) for _ in range(4)]
             allh = self._publish([h for _, h in mine])

@@ -148,3 +148,22 @@ def test_shard_fast_path_threshold_host_side():
     import paper_1803_11301_b200._lib as L
     f = L.lib().fpm_shard_tower
     assert [f(l) for l in (8, 14, 17, 18, 19, 22, 26, 30)] == [0, 0, 0, 1, 1, 1, 1, 1]
+
+
+def test_random_bitpoly_matches_reference_generator(port):
+    """fpm_random_bitpoly = random_bitpoly(n, mt19937_64(seed)) (bitpoly.cpp:19-24), host only: the
+    seeded inputs bench.py feeds the GPU are the ones the golden hashes were made from."""
+    import paper_1803_11301_b200 as pkg
+    for bits, seed in ((1, 3), (64, 20261020), (1000, 20261021), (65536, 30000), (123457, 40007)):
+        assert np.array_equal(pkg.random_bitpoly(bits, seed), port.random_bitpoly(bits, seed)), (bits, seed)
+    assert pkg.random_bitpoly(0, 1).size == 0
+
+
+def test_batch_shard_partitions_the_batch():
+    from paper_1803_11301_b200.dist import batch_shard
+    for count in (1, 7, 4096):
+        for P in (1, 2, 3, 8):
+            got = [batch_shard(count, P, r) for r in range(P)]
+            assert sum(n for _, n in got) == count
+            assert all(got[r][0] + got[r][1] == got[r + 1][0] for r in range(P - 1))
+            assert max(n for _, n in got) - min(n for _, n in got) <= 1

@@ -106,6 +106,12 @@ def _make_peer_backend(shared, rank, keep):
         def _open(self, handle):
             return handle
 
+        def _close(self, ptr):
+            pass
+
+        def _free(self, ptr):
+            pass
+
         def _barrier(self):
             torch.cuda.synchronize()
             shared.barrier.wait()

@@ -184,6 +184,70 @@ def test_batch(gpu, port, checker):
         assert np.array_equal(C[k], checker.polymul(A[k], la, B[k], lb)), k
 
 
+def _cfg2(gpu):
+    import hashlib
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_meta.json")) as f:
+        meta = json.load(f)["cfg2_batch"]
+    bits, count = meta["a_bits"], meta["count"]
+    A = np.concatenate([gpu.random_bitpoly(bits, 30000 + k) for k in range(count)])
+    B = np.concatenate([gpu.random_bitpoly(bits, 40000 + k) for k in range(count)])
+    h = lambda w: hashlib.blake2b(np.ascontiguousarray(w, np.uint64).tobytes(), digest_size=16).hexdigest()
+    return meta, bits, count, A, B, h
+
+
+def test_batch_config2_all_products(gpu):
+    """BASELINE config 2 in full: the 4096 products of fpm_polymul_batch_dev (one launch) hash to the
+    reference's own 4096 fp_polymul products (tests/golden/make_golden.py, polymul.cpp:223-239)."""
+    import torch
+    meta, bits, count, A, B, h = _cfg2(gpu)
+    wc = meta["product_words"]
+    dA = torch.from_numpy(A.view(np.int64)).cuda()
+    dB = torch.from_numpy(B.view(np.int64)).cuda()
+    dC = torch.full((count * wc,), -1, dtype=torch.int64, device="cuda")
+    gpu.fp_polymul_batch_dev(dA, bits, bits // 64, dB, bits, bits // 64, dC, wc, count)
+    torch.cuda.synchronize()
+    C = dC.cpu().numpy().view(np.uint64)
+    assert h(C[:wc]) == meta["blake2b128_first"]
+    assert h(C) == meta["blake2b128_all"]
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_batch_config2_split_thread_ranks(gpu, P):
+    """bench.py's config-2 split (dist.polymul_batch_sharded: contiguous, uneven when P does not
+    divide the batch) with P host threads as ranks on one GPU, each writing only its rows of the
+    shared product tensor; the assembled batch hashes to the reference's."""
+    import threading
+    import torch
+    from paper_1803_11301_b200.dist import batch_shard, polymul_batch_sharded
+    meta, bits, count, A, B, h = _cfg2(gpu)
+    wc = meta["product_words"]
+    dA = torch.from_numpy(A.view(np.int64)).cuda()
+    dB = torch.from_numpy(B.view(np.int64)).cuda()
+    dC = torch.full((count * wc,), -1, dtype=torch.int64, device="cuda")
+    assert sum(batch_shard(count, P, r)[1] for r in range(P)) == count
+    errs = []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                polymul_batch_sharded(dA, bits, dB, bits, dC, count, P, rank)
+                torch.cuda.current_stream().synchronize()
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append((rank, repr(e)))
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    torch.cuda.synchronize()
+    assert h(dC.cpu().numpy().view(np.uint64)) == meta["blake2b128_all"]
+
+
 # ---------------------------------------------------------------- GF(2^64) stages (auto field)
 def _ref64_or_port(port):
     import oracle
