@@ -51,12 +51,49 @@ LOP3_OPS_PER_CLK_SM = 63.0
 
 
 class ClockSampler:
+    """SM clock and throttle reasons sampled DURING the timed region: NVML (nvidia-ml-py) every 10 ms
+    on a thread, plus one sample on entry and one on exit so short regions are covered; falls back
+    to `nvidia-smi -lms 100` when NVML is unavailable."""
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
         self.proc = None
+        self.nvml = None
+        self.stop = threading.Event()
+
+    def _nvml_sample(self):
+        n, h = self.nvml, self.handle
+        sm = n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)
+        mx = n.nvmlDeviceGetMaxClockInfo(h, n.NVML_CLOCK_SM)
+        try:
+            rs = n.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except AttributeError:
+            rs = n.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        self.samples.append((float(sm), float(mx), int(rs)))
+
+    def _nvml_loop(self):
+        while not self.stop.wait(0.01):
+            try:
+                self._nvml_sample()
+            except Exception:
+                return
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[self.index]) if vis and vis.split(",")[0].isdigit() else self.index
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            self._nvml_sample()
+            self.t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}",
@@ -72,12 +109,21 @@ class ClockSampler:
         return self
 
     def _read(self):
+        names = list(self.REASONS)
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7:
-                self.samples.append(parts)
+            if len(parts) >= 7 and parts[0].replace(".", "").isdigit():
+                mask = sum(self.REASONS[names[k]] for k in range(4) if parts[3 + k].lower() == "active")
+                self.samples.append((float(parts[0]), float(parts[1]), mask))
 
     def __exit__(self, *a):
+        if self.nvml:
+            self.stop.set()
+            self.t.join(timeout=1)
+            try:
+                self._nvml_sample()
+            except Exception:
+                pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -88,12 +134,9 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[3 + k].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        reasons = sorted({k for _, _, m in self.samples for k, bit in self.REASONS.items() if m & bit})
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples), "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
 SEEDS = (20261020, 20261021)  # tests/golden/make_golden.py: random_bitpoly(bits, mt19937_64(seed))
