@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "basis_dev.cuh"
@@ -249,8 +251,10 @@ __global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32
 }
 // ------------------------------------------------------------------ C: carry + unskew + conv(2^16)
 // g_k[p] = Gs[k][p+k] ^ (p >= 1 ? Gs[k][t+p-1+k] : 0) ^ (k >= 1 ? Gs[k-1][t+p+k-1] : 0), then conv(g_k).
+// kmask: the digit index of row k is k & kmask (all-ones: one Taylor step over all D rows; 255: the
+// chunk-local step L1_inner of conv2d, whose digits restart every 256 rows).
 __global__ void __launch_bounds__(256, 4) carry_rows_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch,
-                                                         uint32_t* __restrict__ out, uint64_t D) {
+                                                         uint32_t* __restrict__ out, uint64_t D, uint64_t kmask) {
   extern __shared__ uint32_t smem[];
   uint32_t* tile = smem;
   uint32_t* sc = smem + kTileRows * kRowPitchW<1>;
@@ -263,10 +267,11 @@ __global__ void __launch_bounds__(256, 4) carry_rows_kernel(const uint32_t* __re
   // coalesced: 2049 words per span; the next row's spans are loaded (into registers) while this
   // row converts
   uint32_t va[9], vh[9];
-  auto fetch = [&](uint64_t k) {
-    if (k >= D) return;
-    const uint32_t* rk = gs + k * gs_pitch;
-    const uint32_t* rk1 = gs + (k - (k ? 1 : 0)) * gs_pitch;
+  auto fetch = [&](uint64_t kr) {
+    if (kr >= D) return;
+    const uint64_t k = kr & kmask;
+    const uint32_t* rk = gs + kr * gs_pitch;
+    const uint32_t* rk1 = gs + (kr - (k ? 1 : 0)) * gs_pitch;
     const uint64_t a0 = k >> 5, b0 = (kT + k - 1) >> 5;
     uint32_t vb[9], vc[9];
 #pragma unroll
@@ -282,8 +287,9 @@ __global__ void __launch_bounds__(256, 4) carry_rows_kernel(const uint32_t* __re
     for (int j = 0; j < 9; ++j) vh[j] = vb[j] ^ vc[j];
   };
   fetch(blockIdx.x);
-  for (uint64_t k = blockIdx.x; k < D; k += gridDim.x) {
-    const uint32_t* rk = gs + k * gs_pitch;
+  for (uint64_t kr = blockIdx.x; kr < D; kr += gridDim.x) {
+    const uint64_t k = kr & kmask;
+    const uint32_t* rk = gs + kr * gs_pitch;
     const int sA = (int)(k & 31), sB = (int)((kT + k - 1) & 31);
     __syncthreads();  // the previous row's conversion is done with the shared tile
 #pragma unroll
@@ -294,7 +300,7 @@ __global__ void __launch_bounds__(256, 4) carry_rows_kernel(const uint32_t* __re
         sh[pad(w)] = vh[j];
       }
     }
-    fetch(k + gridDim.x);
+    fetch(kr + gridDim.x);
     __syncthreads();
     uint32_t m[8];
     {
@@ -313,7 +319,7 @@ __global__ void __launch_bounds__(256, 4) carry_rows_kernel(const uint32_t* __re
                               (int)(pos & 31)) & 1u;
     }
     conv_tile<false>(m, tile, sc, kTLog2);
-    uint4* o = reinterpret_cast<uint4*>(out + k * kTWords + tid * 8);
+    uint4* o = reinterpret_cast<uint4*>(out + kr * kTWords + tid * 8);
     o[0] = make_uint4(m[0], m[1], m[2], m[3]);
     o[1] = make_uint4(m[4], m[5], m[6], m[7]);
   }
@@ -324,14 +330,14 @@ __global__ void __launch_bounds__(256, 4) carry_rows_kernel(const uint32_t* __re
 // top (optional): the single inverse top pass of a 2^33-bit array fused in when `out` is the lower
 // 2^32-bit block: out bit q (q >= 1) ^= top bit q - 1, top = the (final) upper block.
 __global__ void overflow_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch, uint32_t* __restrict__ out,
-                                uint64_t D, const uint32_t* __restrict__ top) {
+                                uint64_t D, const uint32_t* __restrict__ top, uint64_t kmask) {
   // A warp covers 32 consecutive output words of one row: both bit offsets are warp-uniform, so each
   // span is one coalesced load per lane, the neighbour word comes by shuffle (lane 31 loads it).
   const uint64_t total = D * kTWords;
   const int lane = threadIdx.x & 31;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t d = k / kTWords, w = k % kTWords;
-    const uint32_t* r0 = gs + d * gs_pitch;
+    const uint64_t dr = k / kTWords, w = k % kTWords, d = dr & kmask;
+    const uint32_t* r0 = gs + dr * gs_pitch;
     const uint64_t ia = w + (d >> 5);
     uint32_t x = __ldg(r0 + ia), y = __shfl_down_sync(0xFFFFFFFFu, x, 1);
     if (lane == 31) y = ia + 1 < gs_pitch ? __ldg(r0 + ia + 1) : 0u;
@@ -638,6 +644,103 @@ __global__ void unit_overflow_kernel(const uint32_t* __restrict__ gs, uint64_t g
   }
 }
 
+// ------------------------------------------------------------------ L1_outer: Taylor step in z = y^256
+// L1 (the Taylor expansion in y = x^t + x over D = 2^lgD rows, t = 2^16) factors as L1_inner o L1_outer
+// with z = y^256 = x^(2^24) + x^256 (tools/models/bc2_model.py): L1_outer expands the array in z over
+// DA = D / 256 chunks of 2^24 bits (digits c, skew 256 c bits = 8 c words: word aligned, so the
+// absolute-frame windows read and write the same words and the step runs IN PLACE); L1_inner is then
+// the 256-row step inside every chunk (skew < 256 bits).  Generic two-term step, R = 2^nb digits:
+//   forward  G_e = sum_{c superset e} x^(256(c-e)) f_c ;  F_e = (G_e mod x^T) + x^256 (G_e div x^T) + (G_{e-1} div x^T)
+//   inverse  F'_c = sum_{e superset c} x^(256(e-c)) F_e ;  f_c = (F'_c mod x^T) + (F'_{c-1} div x^T)
+// Both are the same superset zeta in the absolute frame (row c read at word offset -8c); every row's
+// part beyond its own 2^19-word window goes to `side` (R rows x 8R words) and is folded into the first
+// 8R words of rows e and e+1 (forward) / c+1 (inverse) by outer_fix_kernel.
+// top (inverse, 2^33-bit arrays): the single top pass fused into the lower block's stores, as in
+// overflow_kernel.
+constexpr uint64_t kChunkWords = (uint64_t)1 << 19;
+__global__ void __launch_bounds__(256, 3) outer_zeta_kernel(const uint32_t* src, uint32_t* dst,
+                                                            int nb, uint32_t* __restrict__ side, uint64_t windows,
+                                                            const uint32_t* __restrict__ top) {
+  extern __shared__ __align__(16) uint32_t sx[];  // 256 x kZP
+  const int tid = threadIdx.x, c = tid & 31;
+  const int R = 1 << nb, wpc = 256 >> nb;
+  const uint64_t side_pitch = 8 * (uint64_t)R;
+  const uint64_t items = (windows + wpc - 1) / wpc;
+  for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    // mapping A: word c of tile rows TR = (tid >> 5) + 8k; TR = slot * R + row
+    uint32_t a[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const int TR = (tid >> 5) + 8 * k, j = TR & (R - 1);
+      const uint64_t wi = it * wpc + (TR >> nb);
+      const int64_t iw = (int64_t)(wi * kZW) + c - 8 * j;
+      a[k] = (wi < windows && iw >= 0 && iw < (int64_t)kChunkWords) ? src[(uint64_t)j * kChunkWords + iw] : 0u;
+    }
+#pragma unroll
+    for (int b = 3; b < 8; ++b) {
+      if (b < nb) {
+        const int kb = 1 << (b - 3);
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (!(k & kb)) a[k] ^= a[k | kb];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 32; ++k) sx[((tid >> 5) + 8 * k) * kZP + c] = a[k];
+    __syncthreads();
+    const int q = tid & 7, R0 = 8 * (tid >> 3);
+    uint4 bq[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) bq[k] = *reinterpret_cast<const uint4*>(sx + (R0 + k) * kZP + 4 * q);
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      if (b < nb) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (!(k & (1 << b))) bq[k] = make_uint4(bq[k].x ^ bq[k | (1 << b)].x, bq[k].y ^ bq[k | (1 << b)].y,
+                                                   bq[k].z ^ bq[k | (1 << b)].z, bq[k].w ^ bq[k | (1 << b)].w);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int TR = R0 + k, j = TR & (R - 1);
+      const uint64_t wi = it * wpc + (TR >> nb);
+      const int64_t iw = (int64_t)(wi * kZW) + 4 * q - 8 * j;  // 4 words, one region (8j, 2^19: multiples of 4)
+      if (wi >= windows || iw < 0) continue;
+      uint4 v = bq[k];
+      if (iw < (int64_t)kChunkWords) {
+        const uint64_t g = (uint64_t)j * kChunkWords + iw;
+        if (top) {
+          const uint4 t4 = *reinterpret_cast<const uint4*>(top + g);
+          const uint32_t tp = g ? top[g - 1] : 0u;
+          v.x ^= (t4.x << 1) | (tp >> 31);
+          v.y ^= (t4.y << 1) | (t4.x >> 31);
+          v.z ^= (t4.z << 1) | (t4.y >> 31);
+          v.w ^= (t4.w << 1) | (t4.z >> 31);
+        }
+        *reinterpret_cast<uint4*>(dst + g) = v;
+      } else if ((uint64_t)iw - kChunkWords < side_pitch) {
+        *reinterpret_cast<uint4*>(side + (uint64_t)j * side_pitch + ((uint64_t)iw - kChunkWords)) = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Folds the beyond-window parts into the first 8R words of the rows (row e's side holds
+// 8(R-1-e) meaningful words): forward F_e[p] ^= side_e[p-8] ^ side_{e-1}[p]; inverse f_c[p] ^= side_{c-1}[p].
+template <bool INV>
+__global__ void outer_fix_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ side, int nb) {
+  const uint64_t R = (uint64_t)1 << nb, P = 8 * R;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < R * P; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = k / P, p = k % P;
+    uint32_t v = 0;
+    if (!INV && p >= 8 && p - 8 < 8 * (R - 1 - e)) v ^= side[e * P + p - 8];
+    if (e >= 1 && p < 8 * (R - e)) v ^= side[(e - 1) * P + p];
+    if (v) dst[e * kChunkWords + p] ^= v;
+  }
+}
+
 // ------------------------------------------------------------------ host orchestration
 void set_smem_attr() {
   static PerDeviceOnce once;
@@ -781,16 +884,70 @@ void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s, con
   };
   if (!inv) {
     l1_zeta(src ? src : w);
-    carry_rows_kernel<<<grid_cap(D, 7), 256, kTileSmem, s>>>(scratch, wsk, w, D);
+    carry_rows_kernel<<<grid_cap(D, 7), 256, kTileSmem, s>>>(scratch, wsk, w, D, ~(uint64_t)0);
     FPM_LAUNCH_CHECK();
     conv_cols(w, scratch, lgD, false, s);
   } else {
     conv_rows(w, D * kTWords, kTLog2, true, s);
     conv_cols(w, scratch, lgD, true, s);
     l1_zeta(w);
-    overflow_kernel<<<grid_cap(D * kTWords / 256, 32), 256, 0, s>>>(scratch, wsk, w, D, top);
+    overflow_kernel<<<grid_cap(D * kTWords / 256, 32), 256, 0, s>>>(scratch, wsk, w, D, top, ~(uint64_t)0);
     FPM_LAUNCH_CHECK();
   }
+}
+
+// conv(2^K), 17 <= K <= 32, with L1 factored as L1_inner o L1_outer (see outer_zeta_kernel):
+//   forward  [K > 24: L1_outer in place + fix-up] -> L1_inner (256-row skewed zeta -> scratch, then
+//            chunk-local carry fused with conv(2^16) of every row) -> C_cols = conv(D) over the rows
+//   inverse  C_cols^-1 -> conv(2^16)^-1 of every row -> L1_inner^-1 (zeta -> scratch, chunk-local
+//            overflow) -> [K > 24: L1_outer^-1 in place (+ the fused 2^33 top pass) + fix-up]
+// No step writes a skewed array wider than t + 1024 bits per row (the single-step L1 of conv2d skews
+// rows by up to D = t bits: 2x the array).  scratch >= D * (t + 1024) bits and the C_cols scratch.
+void conv2d_split(uint32_t* w, int K, bool inv, uint32_t* scratch, uint32_t* side, cudaStream_t s,
+                  const uint32_t* src = nullptr, const uint32_t* top = nullptr) {
+  const int lgD = K - kTLog2;
+  const uint64_t D = (uint64_t)1 << lgD;
+  const int nb_in = std::min(lgD, 8), nb_out = lgD - nb_in;
+  const uint64_t p1 = (kT + 32 * kZW) / 32;  // skewed row pitch of L1_inner (t + 1024 bits)
+  Skew lo_skew;
+  lo_skew.mask = 255;
+  auto outer = [&](const uint32_t* from, const uint32_t* tp) {
+    const uint64_t windows = (kChunkWords + 8 * ((uint64_t)1 << nb_out) + kZW - 1) / kZW;
+    const int wpc = 256 >> nb_out;
+    outer_zeta_kernel<<<grid_cap((windows + wpc - 1) / wpc, 3), 256, 256 * kZP * sizeof(uint32_t), s>>>(
+        from, w, nb_out, side, windows, tp);
+    FPM_LAUNCH_CHECK();
+    const uint64_t fix = ((uint64_t)8 << (2 * nb_out));
+    if (inv) outer_fix_kernel<true><<<grid_cap((fix + 255) / 256, 8), 256, 0, s>>>(w, side, nb_out);
+    else outer_fix_kernel<false><<<grid_cap((fix + 255) / 256, 8), 256, 0, s>>>(w, side, nb_out);
+    FPM_LAUNCH_CHECK();
+  };
+  if (!inv) {
+    const uint32_t* in = src ? src : w;
+    if (nb_out) {
+      outer(in, nullptr);
+      in = w;
+    }
+    zeta(in, kTWords, scratch, p1, D, 0, nb_in, lo_skew, p1 / kZW, s, kTWords);
+    carry_rows_kernel<<<grid_cap(D, 7), 256, kTileSmem, s>>>(scratch, p1, w, D, 255);
+    FPM_LAUNCH_CHECK();
+    conv_cols(w, scratch, lgD, false, s);
+  } else {
+    conv_cols(w, scratch, lgD, true, s);
+    conv_rows(w, D * kTWords, kTLog2, true, s);
+    zeta(w, kTWords, scratch, p1, D, 0, nb_in, lo_skew, p1 / kZW, s, kTWords);
+    overflow_kernel<<<grid_cap(D * kTWords / 256, 32), 256, 0, s>>>(scratch, p1, w, D, nb_out ? nullptr : top, 255);
+    FPM_LAUNCH_CHECK();
+    if (nb_out) outer(w, top);
+  }
+}
+
+bool split_l1_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FPM_BASIS");
+    return !(e && std::string(e) == "single");
+  }();
+  return on;
 }
 
 void run_big_pass(uint32_t* w, uint64_t nwords, Pass p, bool inverse, uint64_t live_bits, cudaStream_t s) {
@@ -841,9 +998,19 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
   }
   const int Kb = std::min(K, 32);
   const uint64_t lgD = Kb - kTLog2, D = (uint64_t)1 << lgD;
-  // skewed rows (t + max(D, 1024) bits) + the first zeta's rows (t + 1024 bits) when D > 256
-  Scratch scr(D * (kT + std::max<uint64_t>(D, 32 * kZW)) / 8 + (D > 256 ? D * (kT + 32 * kZW) / 8 : 0), s);
+  // skewed rows (t + max(D, 1024) bits) + the first zeta's rows (t + 1024 bits) when D > 256; the
+  // split L1 needs the C_cols scratch (2 Dd x (256 + Dd) rows) and the outer step's side rows
+  const bool split = split_l1_enabled();
+  const uint64_t Dd = D > 256 ? D / 256 : 0;
+  const size_t scr_bytes = split ? std::max<uint64_t>(D * (kT + 32 * kZW) / 8, Dd * (256 + Dd) * (kT / 8))
+                                 : D * (kT + std::max<uint64_t>(D, 32 * kZW)) / 8 + (D > 256 ? D * (kT + 32 * kZW) / 8 : 0);
+  Scratch scr(scr_bytes, s), side_buf(split && Dd ? 8 * Dd * Dd * sizeof(uint32_t) : 0, s);
   uint32_t* scratch = static_cast<uint32_t*>(scr.p);
+  uint32_t* side = static_cast<uint32_t*>(side_buf.p);
+  auto conv_block = [&](uint32_t* blk, const uint32_t* from, const uint32_t* tp) {
+    if (split) conv2d_split(blk, Kb, inverse, scratch, side, s, from, tp);
+    else conv2d(blk, Kb, inverse, scratch, s, from, tp);
+  };
   const uint64_t block_words = ((uint64_t)1 << Kb) / 32;
   // Arrays above 2^32 bits: their passes with S > 2^32 come first (forward) / last (inverse);
   // what remains is conv(2^32) of every 2^32-bit block (build_schedule's per-digit recursion).
@@ -860,7 +1027,7 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
     for (const Pass& p : top) run_big_pass(w, nwords, p, false, live_bits, s);
     for (uint64_t b = 0; b < nblocks; ++b) {
       if (b * block_words * 32 >= live_bits) continue;  // all-zero block stays zero
-      conv2d(w + b * block_words, Kb, inverse, scratch, s, src ? src + b * block_words : nullptr);
+      conv_block(w + b * block_words, src ? src + b * block_words : nullptr, nullptr);
     }
     return;
   }
@@ -876,7 +1043,7 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
   // and its last target bit 2^32 (= upper bit 0 ^= bit 2^33 - 1) is one word fixed afterwards.
   const bool fuse_top = top.size() == 1 && nblocks == 2 && top[0].shift == block_words * 32 - 1;
   for (uint64_t b = nblocks; b-- > 0;) {
-    conv2d(w + b * block_words, Kb, inverse, scratch, s, nullptr, fuse_top && b == 0 ? w + block_words : nullptr);
+    conv_block(w + b * block_words, nullptr, fuse_top && b == 0 ? w + block_words : nullptr);
     const uint64_t w0 = std::max(b * block_words, early_from), w1 = (b + 1) * block_words;
     if (on_final && w0 < w1) (*on_final)(w0, w1);
   }

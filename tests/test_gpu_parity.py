@@ -31,7 +31,7 @@ def test_gf128_mul(gpu, checker):
     assert np.array_equal(gpu.gf128_mul(u, one), u)
 
 
-@pytest.mark.parametrize("lg", list(range(2, 27)))
+@pytest.mark.parametrize("lg", list(range(2, 29)))
 def test_basis_cvt_roundtrip(gpu, checker, lg):
     n = 1 << lg
     rng = np.random.default_rng(lg)
