@@ -87,6 +87,22 @@ fpm_status fpm_random_bitpoly(size_t n_bits, uint64_t seed, uint64_t* out);
 fpm_status fpm_polymul(const uint64_t* a, size_t a_bits, const uint64_t* b, size_t b_bits, uint64_t* c,
                        int field, int device, double* stage_seconds);
 
+/* fp_polymul over several GPUs from one process (the n_gpus argument;
+ * reference entry point fp_polymul, proj/include/fpmul/polymul.hpp:74-75): host buffers as
+ * fpm_polymul; the product is sharded over the listed devices as logical ranks (a power of two in
+ * [2, 64]; a device may repeat, e.g. {0, 0, 0, 0} runs 4 logical ranks on GPU 0): rank g owns
+ * evaluation elements [g m, (g+1) m), the top log2 P butterfly layers read the partner rank's half
+ * from its memory over NVLink (peer access is enabled on the listed devices), the operands'
+ * conversions run on ranks 0 and 1, and a 2^33-bit product's two inverse-conversion blocks run on
+ * ranks 0 and 1.  Needs >= 1024 evaluation elements per rank.  n_devices == 1 is fpm_polymul.
+ * The transform is GF(2^128) for every field choice (products are field-independent); `field` is
+ * validated as in fpm_plan_mul. */
+fpm_status fpm_polymul_multi(const uint64_t* a, size_t a_bits, const uint64_t* b, size_t b_bits, uint64_t* c,
+                             int field, const int* devices, int n_devices);
+/* fpm_polymul_multi on devices 0 .. n_gpus-1. */
+fpm_status fpm_polymul_n(const uint64_t* a, size_t a_bits, const uint64_t* b, size_t b_bits, uint64_t* c, int field,
+                         int n_gpus);
+
 /* The same on device-resident buffers (d_c sized as above).  Uses the calling thread's current
  * device.  Synchronizes `stream` only when stage_seconds != NULL. */
 fpm_status fpm_polymul_dev(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_t b_bits, uint64_t* d_c,

@@ -25,6 +25,7 @@ from ._lib import (  # noqa: F401
     device_count,
     encode,
     fp_polymul,
+    fp_polymul_multi,
     karatsuba_mul,
     naive_mul,
     clmul_words_dev,

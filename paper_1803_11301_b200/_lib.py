@@ -56,6 +56,10 @@ def lib():
         L.fpm_random_bitpoly.argtypes = [sz, C.c_uint64, _u64p]
         L.fpm_polymul.argtypes = [_u64p, sz, _u64p, sz, _u64p, C.c_int, C.c_int, C.POINTER(C.c_double)]
         L.fpm_polymul_dev.argtypes = [vp, sz, vp, sz, vp, C.c_int, vp, C.POINTER(C.c_double)]
+        L.fpm_polymul_multi.argtypes = [_u64p, sz, _u64p, sz, _u64p, C.c_int, C.POINTER(C.c_int), C.c_int]
+        L.fpm_polymul_n.argtypes = [_u64p, sz, _u64p, sz, _u64p, C.c_int, C.c_int]
+        L.fpm_trim_pool.argtypes = [C.c_int]
+        L.fpm_test_flip_encode_table.argtypes = [C.c_int]
         L.fpm_polymul_batch_dev.argtypes = [vp, sz, sz, vp, sz, sz, vp, sz, sz, vp]
         L.fpm_basis_cvt_dev.argtypes = [vp, sz, sz, vp]
         L.fpm_i_basis_cvt_dev.argtypes = [vp, sz, vp]
@@ -184,6 +188,23 @@ def fp_polymul(a, a_bits: int, b, b_bits: int, field: int = FIELD_AUTO, device: 
                              st if stage_seconds is not None else None))
     if stage_seconds is not None:
         stage_seconds[:] = list(st)
+    return c
+
+
+def fp_polymul_multi(a, a_bits: int, b, b_bits: int, devices, field: int = FIELD_AUTO,
+                     out: np.ndarray | None = None) -> np.ndarray:
+    """fp_polymul sharded over several GPUs from this process (fpm_polymul_multi): `devices` lists
+    the logical ranks (a power of two; a device may repeat, e.g. [0, 0, 0, 0])."""
+    a, b = _as_u64(a), _as_u64(b)
+    if a.size < _words(a_bits) or b.size < _words(b_bits):
+        raise ValueError("fp_polymul_multi: word arrays shorter than the declared bit lengths")
+    if a_bits == 0 or b_bits == 0:
+        return np.zeros(0, np.uint64)
+    c = out if out is not None else np.zeros(_words(a_bits + b_bits - 1), np.uint64)
+    if c.dtype != np.uint64 or c.size < _words(a_bits + b_bits - 1):
+        raise ValueError("fp_polymul_multi: output buffer too small")
+    devs = (C.c_int * len(devices))(*devices)
+    _check(lib().fpm_polymul_multi(_ptr(a), a_bits, _ptr(b), b_bits, _ptr(c), field, devs, len(devices)))
     return c
 
 

@@ -484,6 +484,18 @@ BitPoly fp_polymul(const BitPoly& a, const BitPoly& b, const MulOptions& opts) {
   const int req = opts.field == FieldChoice::kGF64 ? FPM_FIELD_GF64
                 : opts.field == FieldChoice::kGF128 ? FPM_FIELD_GF128 : FPM_FIELD_AUTO;
   check(fpm_plan_mul(a.bit_length(), b.bit_length(), req, &p));
+  if (opts.devices.size() > 1) {  // sharded over several GPUs (logical ranks), GF(2^128) transform
+    BitPoly c(a.bit_length() + b.bit_length() - 1);
+    check(fpm_polymul_multi(a.word_data(), a.bit_length(), b.word_data(), b.bit_length(), c.word_data(), req,
+                            opts.devices.data(), static_cast<int>(opts.devices.size())));
+    return c;
+  }
+  if (opts.devices.size() == 1) {
+    const int prev = current_device();
+    set_device(opts.devices[0]);
+    struct Restore { int d; ~Restore() { set_device(d); } } restore{prev};
+    return gpu_product(a, b, p.field_degree == 64 ? FPM_FIELD_GF64 : FPM_FIELD_GF128, opts.stage_seconds);
+  }
   return gpu_product(a, b, p.field_degree == 64 ? FPM_FIELD_GF64 : FPM_FIELD_GF128, opts.stage_seconds);
 }
 

@@ -391,6 +391,7 @@ struct Ev {
 }  // namespace
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void set_last_error(const char* msg) { g_err = msg; }
 
 namespace {
 cudaMemPool_t library_pool(int dev) {

@@ -6,6 +6,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <functional>
+#include <new>
 #include <stdexcept>
 #include <string>
 
@@ -28,6 +29,27 @@ struct Error : std::runtime_error {
       throw ::fpm::Error(e_ == cudaErrorMemoryAllocation ? ::fpm::kNoMem : ::fpm::kCuda,        \
                          std::string(#x) + ": " + cudaGetErrorString(e_));                     \
   } while (0)
+// C-ABI error plumbing: runs fn, maps exceptions to status codes and the thread-local
+// fpm_last_error() message.
+void set_last_error(const char* msg);
+template <class Fn>
+int fpm_guard_impl(Fn&& fn) {
+  try {
+    fn();
+    return kOk;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    set_last_error(e.what());
+    return kNoMem;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return kCuda;
+  }
+}
+#define fpm_guard(...) ((fpm_status)::fpm::fpm_guard_impl(__VA_ARGS__))
+
 // Every kernel launch of the library goes through this check; it also feeds fpm_launch_count().
 void note_launch();
 #define FPM_LAUNCH_CHECK()             \
@@ -153,6 +175,13 @@ using FinalFn = std::function<void(uint64_t w0, uint64_t w1)>;
 void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s,
                       const FinalFn* on_final = nullptr, const uint32_t* src = nullptr);
 
+// The halves of a 2^33-bit inverse conversion as separate calls (sharded products: the two 2^32-bit
+// blocks converted on different GPUs).  Upper block: basis_cvt_device(w_hi, 2^32, 2^32, true, s); then
+// the lower block with the fused top pass reading the final upper block (may be peer memory); then
+// top_bit_fix_device on the upper block.
+void basis_cvt_block32_inverse(uint32_t* w_lo, const uint32_t* top, cudaStream_t s);
+void top_bit_fix_device(uint32_t* hi_block, cudaStream_t s);
+
 // Encode / decode (k_codec.cu).  poly has 128 * 2^l bits; ev has 2^l uint4.
 void encode_device(const uint32_t* poly, unsigned l, uint4* ev, cudaStream_t s);
 // rows_live = 64: rows >= 64 of poly are known zero (pipeline operands) and not read.
@@ -162,6 +191,10 @@ void encode_device_rows(const uint32_t* poly, unsigned l, uint4* ev, int rows_li
 void encode_cols_device(const uint32_t* poly, unsigned l, uint64_t col0, uint64_t ncols, uint4* ev, int rows_live,
                         cudaStream_t s, bool tower = false);
 void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaStream_t s, bool tower = false);
+// ncols elements -> columns [col0, col0 + ncols) of a 128-row partition matrix of row pitch row_bits,
+// rows 0..63 written to lo, rows 64..127 to hi (each 64 rows of row_bits; either may be peer memory).
+void decode_cols_split_device(const uint4* ev, uint64_t ncols, uint64_t col0, uint64_t row_bits, uint32_t* lo,
+                              uint32_t* hi, cudaStream_t s, bool tower);
 // One exchanged butterfly layer (sharded FFT): this rank holds `mine` (side 0 = p0 half, 1 = p1 half),
 // the partner's half arrived in `theirs`; uniform twiddle w.  Result replaces `mine`.
 // out (optional): write the result there instead of over `mine` (then `theirs` may be a peer GPU's

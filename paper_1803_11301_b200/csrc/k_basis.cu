@@ -970,6 +970,27 @@ using Scratch = DevBuf;
 
 }  // namespace
 
+// One 2^32-bit block of a 2^33-bit array's inverse conversion, on its own: conv(2^32)^-1 of w, then
+// (top != null: the lower block) the array's single top pass x[q] ^= top[q - 1] fused in -- top is the
+// final upper block, possibly in a peer GPU's memory.  The upper block's own bit 0 fix-up is
+// top_bit_fix_device, to be ordered after the lower block's conversion (it reads the pre-fix bit).
+void basis_cvt_block32_inverse(uint32_t* w, const uint32_t* top, cudaStream_t s) {
+  set_smem_attr();
+  const uint64_t D = (uint64_t)1 << 16;
+  const uint64_t Dd = D / 256;
+  const bool split = split_l1_enabled();
+  const size_t scr_bytes = split ? std::max<uint64_t>(D * (kT + 32 * kZW) / 8, Dd * (256 + Dd) * (kT / 8))
+                                 : D * (kT + std::max<uint64_t>(D, 32 * kZW)) / 8 + D * (kT + 32 * kZW) / 8;
+  Scratch scr(scr_bytes, s), side_buf(split ? 8 * Dd * Dd * sizeof(uint32_t) : 0, s);
+  if (split) conv2d_split(w, 32, true, static_cast<uint32_t*>(scr.p), static_cast<uint32_t*>(side_buf.p), s, nullptr, top);
+  else conv2d(w, 32, true, static_cast<uint32_t*>(scr.p), s, nullptr, top);
+}
+
+void top_bit_fix_device(uint32_t* hi_block, cudaStream_t s) {
+  top_bit_fix_kernel<<<1, 32, 0, s>>>(hi_block, ((uint64_t)1 << 32) / 32);
+  FPM_LAUNCH_CHECK();
+}
+
 void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s,
                       const FinalFn* on_final, const uint32_t* src) {
   if (n_bits < 4 || (n_bits & (n_bits - 1))) throw Error(kInvalid, "basis_cvt: length must be a power of two >= 4");

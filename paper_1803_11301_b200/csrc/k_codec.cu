@@ -86,9 +86,12 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint32_t* __restrict_
   }
 }
 
+// Rows 0..63 go to poly (pitch row_words), rows 64..127 to poly_hi (same pitch); column word offset
+// of slab sl: sl * kSlabWords.
 __global__ void __launch_bounds__(256) decode_kernel(const uint4* __restrict__ ev, uint64_t nslabs,
                                                      uint64_t row_words,
-                                                     const uint4* __restrict__ tab_g, uint32_t* __restrict__ poly) {
+                                                     const uint4* __restrict__ tab_g, uint32_t* __restrict__ poly,
+                                                     uint32_t* __restrict__ poly_hi) {
   extern __shared__ uint4 smem4[];
   uint4* tab = smem4;  // rotated 8-bit table of x*E^-1 (gf128.cuh m8 layout)
   uint32_t* slab = reinterpret_cast<uint32_t*>(smem4 + kM8Uint4);  // 128 x kPad
@@ -125,7 +128,8 @@ __global__ void __launch_bounds__(256) decode_kernel(const uint4* __restrict__ e
     __syncthreads();
     for (int i = tid; i < 128 * kSlabWords; i += blockDim.x) {
       const int r = i / kSlabWords, c = i % kSlabWords;
-      poly[(uint64_t)r * row_words + w0 + c] = slab[r * kPad + c];
+      uint32_t* base = r < 64 ? poly + (uint64_t)r * row_words : poly_hi + (uint64_t)(r - 64) * row_words;
+      base[w0 + c] = slab[r * kPad + c];
     }
     __syncthreads();
   }
@@ -410,7 +414,24 @@ void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaSt
   static PerDeviceOnce attr;
   attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
   const uint64_t nslabs = ncols / 32 / kSlabWords;
-  decode_kernel<<<resident_grid(decode_kernel, 256, smem, nslabs), 256, smem, s>>>(ev, nslabs, ncols / 32, tower ? dt.dec_m8r : dt.dec_m8, slice);
+  decode_kernel<<<resident_grid(decode_kernel, 256, smem, nslabs), 256, smem, s>>>(ev, nslabs, ncols / 32, tower ? dt.dec_m8r : dt.dec_m8, slice,
+                                                                                   slice + 64 * (ncols / 32));
+  FPM_LAUNCH_CHECK();
+}
+
+void decode_cols_split_device(const uint4* ev, uint64_t ncols, uint64_t col0, uint64_t row_bits, uint32_t* lo,
+                              uint32_t* hi, cudaStream_t s, bool tower) {
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  if (ncols % 1024 || col0 % 1024 || row_bits % 1024 || col0 + ncols > row_bits)
+    throw Error(kInvalid, "decode: split column ranges need 1024-aligned columns");
+  const DeviceTables& dt = device_tables(dev);
+  const size_t smem = kM8Uint4 * sizeof(uint4) + 128 * kPad * sizeof(uint32_t);
+  static PerDeviceOnce attr;
+  attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
+  const uint64_t nslabs = ncols / 32 / kSlabWords;
+  decode_kernel<<<resident_grid(decode_kernel, 256, smem, nslabs), 256, smem, s>>>(
+      ev, nslabs, row_bits / 32, tower ? dt.dec_m8r : dt.dec_m8, lo + col0 / 32, hi + col0 / 32);
   FPM_LAUNCH_CHECK();
 }
 

@@ -284,10 +284,42 @@ static void gpu_tests() {
   }, "plan_mul(kGF64, 2^40)");
 }
 
+// fp_polymul sharded over P logical ranks on GPU 0 (MulOptions::devices = {0, ..., 0}: the
+// multi-GPU path, fpm_polymul_multi, with peer pointers that happen to be local): bit-exact against
+// karatsuba_mul (an independent algorithm) on both coset regimes of the sharded FFT, and against the
+// single-GPU pipeline at a size whose cosets take the tower fast path.
+void multi_gpu_tests() {
+  std::mt19937_64 rng(77);
+  for (int P : {2, 4, 8}) {
+    MulOptions o;
+    o.devices.assign(P, 0);
+    const BitPoly a = random_bitpoly((size_t{1} << 19) + 321, rng), b = random_bitpoly(size_t{1} << 19, rng);
+    CHECK(fp_polymul(a, b, o) == karatsuba_mul(a, b));
+    const BitPoly x = random_bitpoly(size_t{1} << 25, rng), y = random_bitpoly((size_t{1} << 25) - 4099, rng);
+    MulOptions single;
+    single.field = FieldChoice::kGF128;
+    CHECK(fp_polymul(x, y, o) == fp_polymul(x, y, single));
+  }
+  check_throws<std::invalid_argument>([&] {
+    MulOptions o;
+    o.devices = {0, 0, 0};  // not a power of two
+    (void)fp_polymul(random_bitpoly(size_t{1} << 20, rng), random_bitpoly(size_t{1} << 20, rng), o);
+  }, "fpm_polymul_multi: 3 ranks");
+}
+
 int main(int argc, char** argv) {
   const bool cpu_only = argc > 1 && std::string(argv[1]) == "cpu";
+  const bool multi_only = argc > 1 && std::string(argv[1]) == "multi";
+  if (multi_only) {
+    multi_gpu_tests();
+    std::printf("%s: %d checks, %d failures\n", g_fail ? "FAIL" : "PASS", g_checks, g_fail);
+    return g_fail ? 1 : 0;
+  }
   host_tests();
-  if (!cpu_only) gpu_tests();
+  if (!cpu_only) {
+    gpu_tests();
+    multi_gpu_tests();
+  }
   std::printf("%s: %d checks, %d failures\n", g_fail ? "FAIL" : "PASS", g_checks, g_fail);
   return g_fail ? 1 : 0;
 }

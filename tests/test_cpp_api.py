@@ -29,3 +29,12 @@ def test_cpp_api_on_gpu(test_api):
     r = subprocess.run([test_api], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
     assert "PASS" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_api_multi_gpu_logical_ranks(test_api):
+    """MulOptions::devices = {0, ..., 0}: fp_polymul sharded over P = 2/4/8 logical ranks through
+    the C++ API (fpm_polymul_multi), against karatsuba_mul and the single-GPU pipeline."""
+    r = subprocess.run([test_api, "multi"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    assert "PASS" in r.stdout

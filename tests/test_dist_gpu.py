@@ -216,3 +216,40 @@ def test_tower_encode_decode_columns_match_polynomial(gpu):
     assert torch.equal(outs[0][1], outs[1][1])      # ... and decode to the same bits
     want = poly.view(128, n_p // 64)[:, col0 // 64:(col0 + m) // 64].reshape(-1)
     assert torch.equal(outs[1][1], want)
+
+
+@pytest.mark.parametrize("P,la,lb", [(2, 1 << 20, (1 << 20) - 13), (8, 1 << 20, 1 << 20), (2, 1 << 25, (1 << 25) - 99),
+                                     (4, 1 << 26, 1 << 25), (8, 1 << 24, 8400953)])
+def test_polymul_multi_logical_ranks(gpu, checker, P, la, lb):
+    """fpm_polymul_multi -- the single-process multi-GPU entry point (C-ABI) -- with P logical ranks
+    on GPU 0: peer-memory exchanges, operand conversions on ranks 0/1, decode into the converting
+    rank's array; both coset regimes (stage kernels below 2^18 elements per rank, tower fast path
+    above).  Bit-exact against the oracle."""
+    a = gpu.random_bitpoly(la, 61)
+    b = gpu.random_bitpoly(lb, 62)
+    assert np.array_equal(gpu.fp_polymul_multi(a, la, b, lb, [0] * P), checker.polymul(a, la, b, lb))
+
+
+@pytest.mark.parametrize("key,P", [("268435456x268435456", 4), ("4294967296x4294967296", 2),
+                                   ("4294967296x4294967296", 8)])
+def test_polymul_multi_baseline_configs(gpu, key, P):
+    """BASELINE configs 4 and 5 through fpm_polymul_multi with P logical ranks on GPU 0 against the
+    reference's product hash (config 5: the two 2^32-bit inverse-conversion blocks on ranks 0 and 1,
+    the top pass reading rank 1's block)."""
+    import hashlib
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_meta.json")) as f:
+        c = json.load(f)["configs"][key]
+    a = gpu.random_bitpoly(c["a_bits"], c["seed_a"])
+    b = gpu.random_bitpoly(c["b_bits"], c["seed_b"])
+    prod = gpu.fp_polymul_multi(a, c["a_bits"], b, c["b_bits"], [0] * P, field=gpu.FIELD_GF128)
+    assert hashlib.blake2b(prod.tobytes(), digest_size=16).hexdigest() == c["blake2b128"]
+
+
+def test_polymul_multi_rejects_bad_rank_counts(gpu):
+    a = gpu.random_bitpoly(1 << 20, 1)
+    with pytest.raises(ValueError):
+        gpu.fp_polymul_multi(a, 1 << 20, a, 1 << 20, [0, 0, 0])
+    with pytest.raises(ValueError):  # 2^7 elements per rank
+        gpu.fp_polymul_multi(a, 1 << 12, a, 1 << 12, [0] * 64, field=gpu.FIELD_GF128)
