@@ -36,6 +36,8 @@ constexpr uint64_t kT = (uint64_t)1 << kTLog2;
 constexpr int kTWords = (int)(kT / 32);     // 2048
 constexpr size_t kTileSmem = (kTileRows * kRowPitchW<1> + kTileRows * kScPitch) * sizeof(uint32_t);
 
+__device__ __forceinline__ uint4 x4v(uint4 a, uint4 b) { return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w); }
+
 int sm_count() {
   int dev, n;
   FPM_CUDA(cudaGetDevice(&dev));
@@ -658,23 +660,37 @@ __global__ void unit_overflow_kernel(const uint32_t* __restrict__ gs, uint64_t g
 // top (inverse, 2^33-bit arrays): the single top pass fused into the lower block's stores, as in
 // overflow_kernel.
 constexpr uint64_t kChunkWords = (uint64_t)1 << 19;
-__global__ void __launch_bounds__(256, 3) outer_zeta_kernel(const uint32_t* src, uint32_t* dst,
-                                                            int nb, uint32_t* __restrict__ side, uint64_t windows,
+// Geometry of one generic two-term step: `groups` independent groups (group_words apart), each of
+// R = 2^nb digit rows of row_words words (rows row_words apart), skew skew_words per digit (a
+// multiple of 4 words); side: per group R rows x R*skew_words words.
+struct StepGeom {
+  uint64_t row_words, skew_words, group_words;
+  int nb;
+  uint64_t side_pitch() const { return skew_words << nb; }
+  uint64_t windows() const { return (row_words + skew_words * (((uint64_t)1 << nb) - 1) + kZW - 1) / kZW; }
+};
+__global__ void __launch_bounds__(256, 3) outer_zeta_kernel(const uint32_t* src, uint32_t* dst, const StepGeom gm,
+                                                            uint64_t windows, uint64_t groups,
+                                                            uint32_t* __restrict__ side,
                                                             const uint32_t* __restrict__ top) {
   extern __shared__ __align__(16) uint32_t sx[];  // 256 x kZP
   const int tid = threadIdx.x, c = tid & 31;
-  const int R = 1 << nb, wpc = 256 >> nb;
-  const uint64_t side_pitch = 8 * (uint64_t)R;
-  const uint64_t items = (windows + wpc - 1) / wpc;
+  const int nb = gm.nb, R = 1 << nb, wpc = 256 >> nb;
+  const uint64_t wblocks = (windows + wpc - 1) / wpc;
+  const uint64_t side_pitch = gm.skew_words << nb;
+  const uint64_t items = wblocks * groups;
   for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const uint64_t grp = it / wblocks, wb = it - grp * wblocks;
+    const uint64_t gbase = grp * gm.group_words;
+    uint32_t* gside = side + grp * (side_pitch << nb);
     // mapping A: word c of tile rows TR = (tid >> 5) + 8k; TR = slot * R + row
     uint32_t a[32];
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
       const int TR = (tid >> 5) + 8 * k, j = TR & (R - 1);
-      const uint64_t wi = it * wpc + (TR >> nb);
-      const int64_t iw = (int64_t)(wi * kZW) + c - 8 * j;
-      a[k] = (wi < windows && iw >= 0 && iw < (int64_t)kChunkWords) ? src[(uint64_t)j * kChunkWords + iw] : 0u;
+      const uint64_t wi = wb * wpc + (TR >> nb);
+      const int64_t iw = (int64_t)(wi * kZW) + c - (int64_t)(gm.skew_words * j);
+      a[k] = (wi < windows && iw >= 0 && iw < (int64_t)gm.row_words) ? src[gbase + (uint64_t)j * gm.row_words + iw] : 0u;
     }
 #pragma unroll
     for (int b = 3; b < 8; ++b) {
@@ -704,12 +720,12 @@ __global__ void __launch_bounds__(256, 3) outer_zeta_kernel(const uint32_t* src,
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int TR = R0 + k, j = TR & (R - 1);
-      const uint64_t wi = it * wpc + (TR >> nb);
-      const int64_t iw = (int64_t)(wi * kZW) + 4 * q - 8 * j;  // 4 words, one region (8j, 2^19: multiples of 4)
+      const uint64_t wi = wb * wpc + (TR >> nb);
+      const int64_t iw = (int64_t)(wi * kZW) + 4 * q - (int64_t)(gm.skew_words * j);  // one region: all multiples of 4
       if (wi >= windows || iw < 0) continue;
       uint4 v = bq[k];
-      if (iw < (int64_t)kChunkWords) {
-        const uint64_t g = (uint64_t)j * kChunkWords + iw;
+      if (iw < (int64_t)gm.row_words) {
+        const uint64_t g = gbase + (uint64_t)j * gm.row_words + iw;
         if (top) {
           const uint4 t4 = *reinterpret_cast<const uint4*>(top + g);
           const uint32_t tp = g ? top[g - 1] : 0u;
@@ -719,25 +735,33 @@ __global__ void __launch_bounds__(256, 3) outer_zeta_kernel(const uint32_t* src,
           v.w ^= (t4.w << 1) | (t4.z >> 31);
         }
         *reinterpret_cast<uint4*>(dst + g) = v;
-      } else if ((uint64_t)iw - kChunkWords < side_pitch) {
-        *reinterpret_cast<uint4*>(side + (uint64_t)j * side_pitch + ((uint64_t)iw - kChunkWords)) = v;
+      } else if ((uint64_t)iw - gm.row_words < side_pitch) {
+        *reinterpret_cast<uint4*>(gside + (uint64_t)j * side_pitch + ((uint64_t)iw - gm.row_words)) = v;
       }
     }
     __syncthreads();
   }
 }
 
-// Folds the beyond-window parts into the first 8R words of the rows (row e's side holds
-// 8(R-1-e) meaningful words): forward F_e[p] ^= side_e[p-8] ^ side_{e-1}[p]; inverse f_c[p] ^= side_{c-1}[p].
+// Folds the beyond-window parts into the first R*skew words of the rows (row e's side holds
+// skew*(R-1-e) meaningful words): forward F_e[p] ^= side_e[p-skew] ^ side_{e-1}[p];
+// inverse f_c[p] ^= side_{c-1}[p].  Four words per thread.
 template <bool INV>
-__global__ void outer_fix_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ side, int nb) {
-  const uint64_t R = (uint64_t)1 << nb, P = 8 * R;
-  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < R * P; k += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t e = k / P, p = k % P;
-    uint32_t v = 0;
-    if (!INV && p >= 8 && p - 8 < 8 * (R - 1 - e)) v ^= side[e * P + p - 8];
-    if (e >= 1 && p < 8 * (R - e)) v ^= side[(e - 1) * P + p];
-    if (v) dst[e * kChunkWords + p] ^= v;
+__global__ void outer_fix_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ side, const StepGeom gm,
+                                 uint64_t groups) {
+  const uint64_t R = (uint64_t)1 << gm.nb, P = gm.skew_words << gm.nb, S = gm.skew_words, per_group = R * P / 4;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < groups * per_group;
+       k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t grp = k / per_group, r = k % per_group;
+    const uint64_t e = r / (P / 4), p = 4 * (r % (P / 4));
+    const uint32_t* gs = side + grp * R * P;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (!INV && p >= S && p - S < S * (R - 1 - e)) v = *reinterpret_cast<const uint4*>(gs + e * P + p - S);
+    if (e >= 1 && p < S * (R - e)) v = x4v(v, *reinterpret_cast<const uint4*>(gs + (e - 1) * P + p));
+    if (v.x | v.y | v.z | v.w) {
+      uint4* d = reinterpret_cast<uint4*>(dst + grp * gm.group_words + e * gm.row_words + p);
+      *d = x4v(*d, v);
+    }
   }
 }
 
@@ -903,6 +927,85 @@ void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s, con
 //            overflow) -> [K > 24: L1_outer^-1 in place (+ the fused 2^33 top pass) + fix-up]
 // No step writes a skewed array wider than t + 1024 bits per row (the single-step L1 of conv2d skews
 // rows by up to D = t bits: 2x the array).  scratch >= D * (t + 1024) bits and the C_cols scratch.
+// One generic two-term step (outer_zeta_kernel + fix-up), in place on w (or from src).
+void two_term_step(const uint32_t* src, uint32_t* w, StepGeom gm, uint64_t groups, uint32_t* side, bool inv,
+                   cudaStream_t s, const uint32_t* top = nullptr) {
+  static PerDeviceOnce attr;
+  attr.run([] {
+    FPM_CUDA(cudaFuncSetAttribute(outer_zeta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * kZP * (int)sizeof(uint32_t)));
+  });
+  const int wpc = 256 >> gm.nb;
+  const uint64_t items = (gm.windows() + wpc - 1) / wpc * groups;
+  outer_zeta_kernel<<<grid_cap(items, 3), 256, 256 * kZP * sizeof(uint32_t), s>>>(src, w, gm, gm.windows(), groups,
+                                                                                    side, top);
+  FPM_LAUNCH_CHECK();
+  const uint64_t fix = groups * (gm.side_pitch() << gm.nb) / 4;
+  if (inv) outer_fix_kernel<true><<<grid_cap((fix + 255) / 256, 8), 256, 0, s>>>(w, side, gm, groups);
+  else outer_fix_kernel<false><<<grid_cap((fix + 255) / 256, 8), 256, 0, s>>>(w, side, gm, groups);
+  FPM_LAUNCH_CHECK();
+}
+
+// Side words the split steps need for D = 2^lgD rows (max over the steps, per call).
+uint64_t split_side_words(int lgD) {
+  uint64_t m = 0;
+  if (lgD > 8) m = std::max<uint64_t>(m, (uint64_t)8 << (2 * (lgD - 8)));  // L1_outer
+  const int gd = lgD - 8;
+  if (gd > 4) {  // T_d's w^(2^k) and w steps
+    const int k = gd / 2;
+    m = std::max<uint64_t>(m, ((uint64_t)kTWords << k) << (2 * (gd - k)));
+    m = std::max<uint64_t>(m, ((uint64_t)kTWords << (2 * k)) << (gd - k));
+  } else if (gd > 0) {
+    m = std::max<uint64_t>(m, (uint64_t)kTWords << (2 * gd));
+  }
+  return m;
+}
+
+// C_cols = conv(D) over the row index (rows of t bits as units), D = 2^lgD, without any skewed copy:
+// lgD <= 8: slab passes; else (digits of 256 rows, Dd = D/256 of them):
+//   L1_d (Taylor in w = y^256 + y over the row index, unit skews) as two in-place steps, w^(2^k)
+//   over Dd/2^k digits of 256*2^k rows (skew 2^k rows) then w inside each chunk (skew 1 row)
+//   (tools/models/bc2_model.py), then conv(Dd) over the digit (rows 256 apart) and conv(256) over
+//   the row within the digit.  The inverse runs the same in reverse.
+void conv_cols_split(uint32_t* w, uint32_t* side, int lgD, bool inv, cudaStream_t s) {
+  if (lgD <= 1) return;
+  if (lgD <= 8) {
+    slab(w, lgD, 1, kTWords / 8, inv, s);
+    return;
+  }
+  const int gd = lgD - 8;
+  const uint64_t Dd = (uint64_t)1 << gd;
+  const uint64_t unit = kTWords;  // words per row
+  auto l1d = [&](bool fwd) {
+    if (gd <= 4) {
+      two_term_step(w, w, StepGeom{256 * unit, unit, 0, gd}, 1, side, !fwd, s);
+      return;
+    }
+    const int k = gd / 2;
+    const StepGeom outer{(256 * unit) << k, unit << k, 0, gd - k};
+    const StepGeom inner{256 * unit, unit, (256 * unit) << k, k};
+    if (fwd) {
+      two_term_step(w, w, outer, 1, side, false, s);
+      two_term_step(w, w, inner, (uint64_t)1 << (gd - k), side, false, s);
+    } else {
+      two_term_step(w, w, inner, (uint64_t)1 << (gd - k), side, true, s);
+      two_term_step(w, w, outer, 1, side, true, s);
+    }
+  };
+  auto over_digit = [&](bool iv) {  // conv(Dd) over rows 256 apart
+    if (gd == 8) conv256_units(w, 256, 256, 256, iv, s);
+    else slab(w, gd, 256, 256 * (kTWords / 8), iv, s);
+  };
+  if (!inv) {
+    l1d(true);
+    over_digit(false);
+    conv256_units(w, Dd, 1, 1, false, s);
+  } else {
+    conv256_units(w, Dd, 1, 1, true, s);
+    over_digit(true);
+    l1d(false);
+  }
+}
+
 void conv2d_split(uint32_t* w, int K, bool inv, uint32_t* scratch, uint32_t* side, cudaStream_t s,
                   const uint32_t* src = nullptr, const uint32_t* top = nullptr) {
   const int lgD = K - kTLog2;
@@ -912,15 +1015,7 @@ void conv2d_split(uint32_t* w, int K, bool inv, uint32_t* scratch, uint32_t* sid
   Skew lo_skew;
   lo_skew.mask = 255;
   auto outer = [&](const uint32_t* from, const uint32_t* tp) {
-    const uint64_t windows = (kChunkWords + 8 * ((uint64_t)1 << nb_out) + kZW - 1) / kZW;
-    const int wpc = 256 >> nb_out;
-    outer_zeta_kernel<<<grid_cap((windows + wpc - 1) / wpc, 3), 256, 256 * kZP * sizeof(uint32_t), s>>>(
-        from, w, nb_out, side, windows, tp);
-    FPM_LAUNCH_CHECK();
-    const uint64_t fix = ((uint64_t)8 << (2 * nb_out));
-    if (inv) outer_fix_kernel<true><<<grid_cap((fix + 255) / 256, 8), 256, 0, s>>>(w, side, nb_out);
-    else outer_fix_kernel<false><<<grid_cap((fix + 255) / 256, 8), 256, 0, s>>>(w, side, nb_out);
-    FPM_LAUNCH_CHECK();
+    two_term_step(from, w, StepGeom{kChunkWords, 8, 0, nb_out}, 1, side, inv, s, tp);
   };
   if (!inv) {
     const uint32_t* in = src ? src : w;
@@ -931,9 +1026,9 @@ void conv2d_split(uint32_t* w, int K, bool inv, uint32_t* scratch, uint32_t* sid
     zeta(in, kTWords, scratch, p1, D, 0, nb_in, lo_skew, p1 / kZW, s, kTWords);
     carry_rows_kernel<<<grid_cap(D, 7), 256, kTileSmem, s>>>(scratch, p1, w, D, 255);
     FPM_LAUNCH_CHECK();
-    conv_cols(w, scratch, lgD, false, s);
+    conv_cols_split(w, side, lgD, false, s);
   } else {
-    conv_cols(w, scratch, lgD, true, s);
+    conv_cols_split(w, side, lgD, true, s);
     conv_rows(w, D * kTWords, kTLog2, true, s);
     zeta(w, kTWords, scratch, p1, D, 0, nb_in, lo_skew, p1 / kZW, s, kTWords);
     overflow_kernel<<<grid_cap(D * kTWords / 256, 32), 256, 0, s>>>(scratch, p1, w, D, nb_out ? nullptr : top, 255);
@@ -977,11 +1072,11 @@ using Scratch = DevBuf;
 void basis_cvt_block32_inverse(uint32_t* w, const uint32_t* top, cudaStream_t s) {
   set_smem_attr();
   const uint64_t D = (uint64_t)1 << 16;
-  const uint64_t Dd = D / 256;
   const bool split = split_l1_enabled();
-  const size_t scr_bytes = split ? std::max<uint64_t>(D * (kT + 32 * kZW) / 8, Dd * (256 + Dd) * (kT / 8))
+  const size_t scr_bytes = split ? D * (kT + 32 * kZW) / 8
                                  : D * (kT + std::max<uint64_t>(D, 32 * kZW)) / 8 + D * (kT + 32 * kZW) / 8;
-  Scratch scr(scr_bytes, s), side_buf(split ? 8 * Dd * Dd * sizeof(uint32_t) : 0, s);
+  Scratch scr(scr_bytes, s), side_buf(split ? split_side_words(16) * sizeof(uint32_t) : 0, s);
+
   if (split) conv2d_split(w, 32, true, static_cast<uint32_t*>(scr.p), static_cast<uint32_t*>(side_buf.p), s, nullptr, top);
   else conv2d(w, 32, true, static_cast<uint32_t*>(scr.p), s, nullptr, top);
 }
@@ -1022,10 +1117,10 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
   // skewed rows (t + max(D, 1024) bits) + the first zeta's rows (t + 1024 bits) when D > 256; the
   // split L1 needs the C_cols scratch (2 Dd x (256 + Dd) rows) and the outer step's side rows
   const bool split = split_l1_enabled();
-  const uint64_t Dd = D > 256 ? D / 256 : 0;
-  const size_t scr_bytes = split ? std::max<uint64_t>(D * (kT + 32 * kZW) / 8, Dd * (256 + Dd) * (kT / 8))
+
+  const size_t scr_bytes = split ? D * (kT + 32 * kZW) / 8
                                  : D * (kT + std::max<uint64_t>(D, 32 * kZW)) / 8 + (D > 256 ? D * (kT + 32 * kZW) / 8 : 0);
-  Scratch scr(scr_bytes, s), side_buf(split && Dd ? 8 * Dd * Dd * sizeof(uint32_t) : 0, s);
+  Scratch scr(scr_bytes, s), side_buf(split ? split_side_words((int)lgD) * sizeof(uint32_t) : 0, s);
   uint32_t* scratch = static_cast<uint32_t*>(scr.p);
   uint32_t* side = static_cast<uint32_t*>(side_buf.p);
   auto conv_block = [&](uint32_t* blk, const uint32_t* from, const uint32_t* tp) {
