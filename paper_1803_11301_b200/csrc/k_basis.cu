@@ -669,32 +669,36 @@ struct StepGeom {
   uint64_t side_pitch() const { return skew_words << nb; }
   uint64_t windows() const { return (row_words + skew_words * (((uint64_t)1 << nb) - 1) + kZW - 1) / kZW; }
 };
+// NB = log2 R (template: the tile-row -> (row, window) split is then compile-time and every load /
+// store address is one add from a per-thread base).
+template <int NB>
 __global__ void __launch_bounds__(256, 3) outer_zeta_kernel(const uint32_t* src, uint32_t* dst, const StepGeom gm,
                                                             uint64_t windows, uint64_t groups,
                                                             uint32_t* __restrict__ side,
                                                             const uint32_t* __restrict__ top) {
   extern __shared__ __align__(16) uint32_t sx[];  // 256 x kZP
-  const int tid = threadIdx.x, c = tid & 31;
-  const int nb = gm.nb, R = 1 << nb, wpc = 256 >> nb;
+  constexpr int R = 1 << NB, wpc = 256 >> NB;
+  const int tid = threadIdx.x, c = tid & 31, w8 = tid >> 5;
   const uint64_t wblocks = (windows + wpc - 1) / wpc;
-  const uint64_t side_pitch = gm.skew_words << nb;
+  const uint64_t side_pitch = gm.skew_words << NB;
+  const int64_t rw = (int64_t)gm.row_words, sk = (int64_t)gm.skew_words;
   const uint64_t items = wblocks * groups;
   for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
     const uint64_t grp = it / wblocks, wb = it - grp * wblocks;
-    const uint64_t gbase = grp * gm.group_words;
-    uint32_t* gside = side + grp * (side_pitch << nb);
-    // mapping A: word c of tile rows TR = (tid >> 5) + 8k; TR = slot * R + row
+    const uint32_t* gsrc = src + grp * gm.group_words;
+    const int64_t wi0 = (int64_t)(wb * wpc);
+    // mapping A: word c of tile rows TR = w8 + 8k; row j = TR % R, window slot TR / R
     uint32_t a[32];
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
-      const int TR = (tid >> 5) + 8 * k, j = TR & (R - 1);
-      const uint64_t wi = wb * wpc + (TR >> nb);
-      const int64_t iw = (int64_t)(wi * kZW) + c - (int64_t)(gm.skew_words * j);
-      a[k] = (wi < windows && iw >= 0 && iw < (int64_t)gm.row_words) ? src[gbase + (uint64_t)j * gm.row_words + iw] : 0u;
+      const int TR = w8 + 8 * k, j = TR & (R - 1), slot = TR >> NB;
+      const int64_t wi = wi0 + slot;
+      const int64_t iw = wi * kZW + c - sk * j;
+      a[k] = (wi < (int64_t)windows && iw >= 0 && iw < rw) ? gsrc[j * rw + iw] : 0u;
     }
 #pragma unroll
     for (int b = 3; b < 8; ++b) {
-      if (b < nb) {
+      if (b < NB) {
         const int kb = 1 << (b - 3);
 #pragma unroll
         for (int k = 0; k < 32; ++k)
@@ -702,7 +706,7 @@ __global__ void __launch_bounds__(256, 3) outer_zeta_kernel(const uint32_t* src,
       }
     }
 #pragma unroll
-    for (int k = 0; k < 32; ++k) sx[((tid >> 5) + 8 * k) * kZP + c] = a[k];
+    for (int k = 0; k < 32; ++k) sx[(w8 + 8 * k) * kZP + c] = a[k];
     __syncthreads();
     const int q = tid & 7, R0 = 8 * (tid >> 3);
     uint4 bq[8];
@@ -710,33 +714,36 @@ __global__ void __launch_bounds__(256, 3) outer_zeta_kernel(const uint32_t* src,
     for (int k = 0; k < 8; ++k) bq[k] = *reinterpret_cast<const uint4*>(sx + (R0 + k) * kZP + 4 * q);
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      if (b < nb) {
+      if (b < NB) {
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           if (!(k & (1 << b))) bq[k] = make_uint4(bq[k].x ^ bq[k | (1 << b)].x, bq[k].y ^ bq[k | (1 << b)].y,
                                                    bq[k].z ^ bq[k | (1 << b)].z, bq[k].w ^ bq[k | (1 << b)].w);
       }
     }
+    uint32_t* gdst = dst + grp * gm.group_words;
+    uint32_t* gside = side + grp * (side_pitch << NB);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int TR = R0 + k, j = TR & (R - 1);
-      const uint64_t wi = wb * wpc + (TR >> nb);
-      const int64_t iw = (int64_t)(wi * kZW) + 4 * q - (int64_t)(gm.skew_words * j);  // one region: all multiples of 4
-      if (wi >= windows || iw < 0) continue;
+      const int TR = R0 + k, j = TR & (R - 1), slot = TR >> NB;
+      const int64_t wi = wi0 + slot;
+      const int64_t iw = wi * kZW + 4 * q - sk * j;  // 4 words, one region (all multiples of 4)
+      if (wi >= (int64_t)windows || iw < 0) continue;
       uint4 v = bq[k];
-      if (iw < (int64_t)gm.row_words) {
-        const uint64_t g = gbase + (uint64_t)j * gm.row_words + iw;
+      if (iw < rw) {
+        const uint64_t g = (uint64_t)(j * rw + iw);
         if (top) {
-          const uint4 t4 = *reinterpret_cast<const uint4*>(top + g);
-          const uint32_t tp = g ? top[g - 1] : 0u;
+          const uint64_t G = grp * gm.group_words + g;
+          const uint4 t4 = *reinterpret_cast<const uint4*>(top + G);
+          const uint32_t tp = G ? top[G - 1] : 0u;
           v.x ^= (t4.x << 1) | (tp >> 31);
           v.y ^= (t4.y << 1) | (t4.x >> 31);
           v.z ^= (t4.z << 1) | (t4.y >> 31);
           v.w ^= (t4.w << 1) | (t4.z >> 31);
         }
-        *reinterpret_cast<uint4*>(dst + g) = v;
-      } else if ((uint64_t)iw - gm.row_words < side_pitch) {
-        *reinterpret_cast<uint4*>(gside + (uint64_t)j * side_pitch + ((uint64_t)iw - gm.row_words)) = v;
+        *reinterpret_cast<uint4*>(gdst + g) = v;
+      } else if ((uint64_t)(iw - rw) < side_pitch) {
+        *reinterpret_cast<uint4*>(gside + (uint64_t)j * side_pitch + (uint64_t)(iw - rw)) = v;
       }
     }
     __syncthreads();
@@ -930,14 +937,17 @@ void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s, con
 // One generic two-term step (outer_zeta_kernel + fix-up), in place on w (or from src).
 void two_term_step(const uint32_t* src, uint32_t* w, StepGeom gm, uint64_t groups, uint32_t* side, bool inv,
                    cudaStream_t s, const uint32_t* top = nullptr) {
-  static PerDeviceOnce attr;
-  attr.run([] {
-    FPM_CUDA(cudaFuncSetAttribute(outer_zeta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * kZP * (int)sizeof(uint32_t)));
-  });
   const int wpc = 256 >> gm.nb;
   const uint64_t items = (gm.windows() + wpc - 1) / wpc * groups;
-  outer_zeta_kernel<<<grid_cap(items, 3), 256, 256 * kZP * sizeof(uint32_t), s>>>(src, w, gm, gm.windows(), groups,
-                                                                                    side, top);
+  const size_t smem = 256 * kZP * sizeof(uint32_t);  // 36 KiB: under the default dynamic limit
+  const int grid = grid_cap(items, 3);
+  switch (gm.nb) {
+#define FPM_OUTER(NB) \
+    case NB: outer_zeta_kernel<NB><<<grid, 256, smem, s>>>(src, w, gm, gm.windows(), groups, side, top); break;
+    FPM_OUTER(1) FPM_OUTER(2) FPM_OUTER(3) FPM_OUTER(4) FPM_OUTER(5) FPM_OUTER(6) FPM_OUTER(7) FPM_OUTER(8)
+#undef FPM_OUTER
+    default: throw Error(kInvalid, "two-term step: 1..8 digit bits");
+  }
   FPM_LAUNCH_CHECK();
   const uint64_t fix = groups * (gm.side_pitch() << gm.nb) / 4;
   if (inv) outer_fix_kernel<true><<<grid_cap((fix + 255) / 256, 8), 256, 0, s>>>(w, side, gm, groups);
