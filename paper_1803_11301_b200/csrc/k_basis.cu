@@ -331,29 +331,43 @@ __global__ void __launch_bounds__(256, 4) carry_rows_kernel(const uint32_t* __re
 // F_d[p] = Gs[d][p+d] ^ (d >= 1 ? Gs[d-1][t+p+d-1] : 0)
 // top (optional): the single inverse top pass of a 2^33-bit array fused in when `out` is the lower
 // 2^32-bit block: out bit q (q >= 1) ^= top bit q - 1, top = the (final) upper block.
-__global__ void overflow_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch, uint32_t* __restrict__ out,
-                                uint64_t D, const uint32_t* __restrict__ top, uint64_t kmask) {
-  // A warp covers 32 consecutive output words of one row: both bit offsets are warp-uniform, so each
-  // span is one coalesced load per lane, the neighbour word comes by shuffle (lane 31 loads it).
-  const uint64_t total = D * kTWords;
-  const int lane = threadIdx.x & 31;
-  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t dr = k / kTWords, w = k % kTWords, d = dr & kmask;
+__global__ void __launch_bounds__(256) overflow_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch,
+                                                       uint32_t* __restrict__ out, uint64_t D,
+                                                       const uint32_t* __restrict__ top, uint64_t kmask) {
+  // One row per CTA iteration: the shifts and row pointers are row-invariant; thread t produces
+  // words t, t + 256, ... (a warp covers 32 consecutive words: one coalesced load per lane, the
+  // funnel's upper word from the next lane, lane 31 loads its own).  Only the first words of a row
+  // receive the previous row's overflow (its skewed row ends t + 1024 bits in).
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (uint64_t dr = blockIdx.x; dr < D; dr += gridDim.x) {
+    const uint32_t d = (uint32_t)(dr & kmask);
     const uint32_t* r0 = gs + dr * gs_pitch;
-    const uint64_t ia = w + (d >> 5);
-    uint32_t x = __ldg(r0 + ia), y = __shfl_down_sync(0xFFFFFFFFu, x, 1);
-    if (lane == 31) y = ia + 1 < gs_pitch ? __ldg(r0 + ia + 1) : 0u;
-    uint32_t v = __funnelshift_r(x, y, (int)(d & 31));
-    if (d) {
-      const uint32_t* r1 = r0 - gs_pitch;
-      const uint64_t pos = kT + d - 1, ib = w + (pos >> 5);
-      uint32_t xb = ib < gs_pitch ? __ldg(r1 + ib) : 0u;
-      uint32_t yb = __shfl_down_sync(0xFFFFFFFFu, xb, 1);
-      if (lane == 31) yb = ib + 1 < gs_pitch ? __ldg(r1 + ib + 1) : 0u;
-      v ^= __funnelshift_r(xb, yb, (int)(pos & 31));
+    const uint32_t sh0 = d & 31, a0 = d >> 5;
+    const uint32_t pos = (uint32_t)kT + d - 1, sh1 = pos & 31, b0 = pos >> 5;
+    uint32_t* o = out + dr * kTWords;
+    const uint32_t* tp = top ? top + dr * kTWords : nullptr;
+    uint32_t x[8], y[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {  // all eight loads in flight
+      const uint32_t ia = tid + 256 * i + a0;
+      x[i] = __ldg(r0 + ia);
+      y[i] = lane == 31 && ia + 1 < gs_pitch ? __ldg(r0 + ia + 1) : 0u;
     }
-    if (top) v ^= (top[k] << 1) | (k ? top[k - 1] >> 31 : 0u);
-    out[k] = v;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t w = tid + 256 * i;
+      const uint32_t nx = __shfl_down_sync(0xFFFFFFFFu, x[i], 1);
+      uint32_t v = __funnelshift_r(x[i], lane == 31 ? y[i] : nx, sh0);
+      if (d && (w - lane) + b0 < gs_pitch) {  // warp-uniform: the previous row's overflow reaches
+        const uint32_t ib = w + b0;               // only the first words of the row
+        const uint32_t xb = ib < gs_pitch ? __ldg(r0 - gs_pitch + ib) : 0u;
+        uint32_t yb = __shfl_down_sync(0xFFFFFFFFu, xb, 1);
+        if (lane == 31) yb = ib + 1 < gs_pitch ? __ldg(r0 - gs_pitch + ib + 1) : 0u;
+        v ^= __funnelshift_r(xb, yb, sh1);
+      }
+      if (tp) v ^= (tp[w] << 1) | ((dr || w) ? tp[(int64_t)w - 1] >> 31 : 0u);
+      o[w] = v;
+    }
   }
 }
 
@@ -922,7 +936,7 @@ void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s, con
     conv_rows(w, D * kTWords, kTLog2, true, s);
     conv_cols(w, scratch, lgD, true, s);
     l1_zeta(w);
-    overflow_kernel<<<grid_cap(D * kTWords / 256, 32), 256, 0, s>>>(scratch, wsk, w, D, top, ~(uint64_t)0);
+    overflow_kernel<<<grid_cap(D, 8), 256, 0, s>>>(scratch, wsk, w, D, top, ~(uint64_t)0);
     FPM_LAUNCH_CHECK();
   }
 }
@@ -1041,7 +1055,7 @@ void conv2d_split(uint32_t* w, int K, bool inv, uint32_t* scratch, uint32_t* sid
     conv_cols_split(w, side, lgD, true, s);
     conv_rows(w, D * kTWords, kTLog2, true, s);
     zeta(w, kTWords, scratch, p1, D, 0, nb_in, lo_skew, p1 / kZW, s, kTWords);
-    overflow_kernel<<<grid_cap(D * kTWords / 256, 32), 256, 0, s>>>(scratch, p1, w, D, nb_out ? nullptr : top, 255);
+    overflow_kernel<<<grid_cap(D, 8), 256, 0, s>>>(scratch, p1, w, D, nb_out ? nullptr : top, 255);
     FPM_LAUNCH_CHECK();
     if (nb_out) outer(w, top);
   }
