@@ -169,15 +169,18 @@ __global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32
         const uint64_t d0 = base + ((uint64_t)(tid >> 5) << b0);
         const int64_t s0 = (int64_t)(((d0 >> skew.lo) & skew.mask) << skew.log);
         const int64_t sstep = (int64_t)((((d0 + dstep) >> skew.lo) & skew.mask) << skew.log) - s0;
-        int64_t pos = (int64_t)(wb * 32 * kZW) - s0;      // bit position of this row's window
+        // 32-bit window arithmetic (rows < 2^31 bits); one unsigned compare bounds a word index
+        const int32_t pos0 = (int32_t)((int64_t)(wb * 32 * kZW) - s0), ss = (int32_t)sstep;
+        const uint32_t rows_w = (uint32_t)src_row_words;
         const uint32_t* row = src + d0 * src_pitch;
         const uint64_t rstep = dstep * src_pitch;
 #pragma unroll
-        for (int k = 0; k < 32; ++k, pos -= sstep, row += rstep) {
-          const int64_t iw = (pos >> 5) + c;
-          sh[k] = (int)(pos & 31);
-          a[k] = (iw >= 0 && iw < (int64_t)src_row_words) ? __ldg(row + iw) : 0u;
-          e[k] = (c == 31 && iw + 1 >= 0 && iw + 1 < (int64_t)src_row_words) ? __ldg(row + iw + 1) : 0u;
+        for (int k = 0; k < 32; ++k, row += rstep) {
+          const int32_t pos = pos0 - k * ss;
+          const uint32_t iw = (uint32_t)((pos >> 5) + c);
+          sh[k] = pos & 31;
+          a[k] = iw < rows_w ? __ldg(row + iw) : 0u;
+          e[k] = (c == 31 && iw + 1 < rows_w) ? __ldg(row + iw + 1) : 0u;
         }
       } else {
 #pragma unroll
@@ -428,7 +431,9 @@ __global__ void __launch_bounds__(256) slab_kernel(uint32_t* __restrict__ data, 
 // overlaps the other's shared-memory phases).
 constexpr int kC256Cols = 16;
 constexpr int kC256Threads = 16 * kC256Cols;
-constexpr size_t kC256Smem = 16 * 32 * kC256Cols * sizeof(uint32_t);  // Z[16][32][cols]
+// Z[16][33][cols]: the digit stride padded by one slot row, so that the two half-warps of a phase
+// that differ in d (512 words apart unpadded) land in different banks.
+constexpr size_t kC256Smem = 16 * 33 * kC256Cols * sizeof(uint32_t);
 
 // conv16 over 16 register values (build_schedule(16): (16,6), (8,3), (16,4), (4,1)); increasing q
 // reads every source before it is overwritten (sources sit above their targets).
@@ -492,7 +497,7 @@ __global__ void __launch_bounds__(kC256Threads, INV ? 3 : 4) conv256_units_kerne
   extern __shared__ uint32_t Z[];  // [d][s][c], d < 16, s < 32, c < 32
   const int tid = threadIdx.x, c = tid % kC256Cols, r = tid / kC256Cols;
   constexpr int kCols = kTWords / kC256Cols;  // column blocks per unit
-  auto zi = [](int d, int s, int cc) { return (d * 32 + s) * kC256Cols + cc; };
+  auto zi = [](int d, int s, int cc) { return (d * 33 + s) * kC256Cols + cc; };
   for (uint64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
     const uint64_t grp = it / kCols;
     const uint64_t colw = (it % kCols) * kC256Cols + c;
