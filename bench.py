@@ -169,8 +169,8 @@ def workload_config(cfg: int) -> dict:
     return {"workload": f"cfg{cfg}: 2^{k} x 2^{k}-bit product, GF(2^128) Frobenius FFT (n=2^{k + 1}, l={k + 1 - 7})",
             "inputs": f"random_bitpoly(2^{k}, mt19937_64({SEEDS[0]})) x random_bitpoly(2^{k}, mt19937_64({SEEDS[1]}))",
             "field": "GF(2^128) (FieldChoice::kGF128)",
-            "l2": "inputs >= 2x L2 per operand (no flush needed)" if bits >= 1 << 28 else
-                  "inputs fit in L2 (each step rewrites the 2n-bit work array and both EvalVecs)"}
+            "l2": "operands 512 MiB each (> L2): no flush needed" if bits >= 1 << 30 else
+                  "operands fit in L2: L2 flushed (512 MiB written) before every timed step, steps timed individually"}
 
 
 def dist_env():
@@ -232,6 +232,70 @@ def algorithmic(stage: str, bits: int, T: int, fused_ab: bool = False):
         passes = (l - T + 1) // 2
         return passes * 2 * V, 552 * (l - T) * n_p // 2
     raise KeyError(stage)
+
+
+GENERIC_CLK_PER_PRODUCT = 6.8  # gf_mul on the FMA/ALU pipes, register operands (tools/microbench/gfmul_rate.cu)
+SMEM_BYTES_PER_CLK_SM = 128.0  # shared-memory bandwidth per SM (32 banks x 4 B)
+
+
+def executed_work(stage: str, bits: int, T: int):
+    """EXECUTED work of one stage of the tower-representation GF(2^128) pipeline (equal operands of
+    `bits` bits), per binding unit:
+      smem_bytes      M8-table products: 16 LDS.128 = 256 B of shared memory each
+      generic         generic products (IMAD-hole Karatsuba, GENERIC_CLK_PER_PRODUCT each per SM)
+      hbm_bytes       one algorithmic sweep of the stage's data
+    butterfly/ibutterfly: radix-4 passes over layers [T, l) of both operands / the product (one M8
+    product per butterfly); pointwise: the fused tower tile pass (per element position: (T-1) tile
+    layers of both operands + (T-1) inverse, one M8 product per butterfly, 3 R<->poly conversions,
+    2.5 generic products for layer 0 of both operands, the pointwise product and inverse layer 0)."""
+    n = 2 * bits
+    n_p = n // 128
+    l = n_p.bit_length() - 1
+    V = 16 * n_p
+    passes = (l - T + 1) // 2
+    w = {"smem_bytes": 0.0, "generic": 0.0, "hbm_bytes": 0.0}
+    if stage == "basiscvt":
+        w["hbm_bytes"] = 2 * 2 * (bits // 8)
+    elif stage == "ibasiscvt":
+        w["hbm_bytes"] = 2 * (n // 8)
+    elif stage == "encode":
+        w["hbm_bytes"] = 2 * (bits // 8 + V)
+    elif stage == "decode":
+        w["hbm_bytes"] = V + n // 8
+    elif stage == "butterfly":
+        w["smem_bytes"] = 256.0 * 2 * (l - T) * n_p / 2
+        w["hbm_bytes"] = 2 * passes * 2 * V
+    elif stage == "ibutterfly":
+        w["smem_bytes"] = 256.0 * (l - T) * n_p / 2
+        w["hbm_bytes"] = passes * 2 * V
+    elif stage == "pointwise":
+        w["smem_bytes"] = 256.0 * ((T - 1) * 1.5 + 3) * n_p
+        w["generic"] = 2.5 * n_p
+        w["hbm_bytes"] = 3 * V
+    else:
+        raise KeyError(stage)
+    return w
+
+
+def stage_roofline(stage: str, bits: int, T: int, seconds: float, mhz: float, hbm_gbs: float):
+    """The stage's roofline time = the slowest of its units at peak; frac = that / measured."""
+    w = executed_work(stage, bits, T)
+    clk = mhz * 1e6
+    smem_peak = SMEM_BYTES_PER_CLK_SM * 148 * clk  # B/s
+    t = {"smem": w["smem_bytes"] / smem_peak, "hbm": w["hbm_bytes"] / (hbm_gbs * 1e9),
+         "generic": w["generic"] * GENERIC_CLK_PER_PRODUCT / (148 * clk)}
+    bound = max(t, key=t.get)
+    if bound == "smem":
+        out = {"bound": "smem", "achieved": round(w["smem_bytes"] / seconds / 1e9, 1), "peak": round(smem_peak / 1e9, 1),
+               "unit": "GB/s"}
+    elif bound == "hbm":
+        out = {"bound": "hbm", "achieved": round(w["hbm_bytes"] / seconds / 1e9, 1), "peak": hbm_gbs, "unit": "GB/s"}
+    else:
+        out = {"bound": "generic", "achieved": round(w["generic"] / seconds / 1e9, 2),
+               "peak": round(148 * clk / GENERIC_CLK_PER_PRODUCT / 1e9, 2), "unit": "Gproducts/s"}
+    out["frac"] = round(t[bound] / seconds, 4)
+    out["t_roof_ms"] = round(t[bound] * 1e3, 3)
+    return out
 
 
 def run_batch(args, ws, rank, local):
@@ -531,20 +595,28 @@ def main():
         step(a, b)
     torch.cuda.synchronize()
 
-    # ---- timed region: device-resident inputs
+    # ---- timed region: device-resident inputs.  Operands that fit in L2 (configs 1, 3, 4): L2 is
+    # flushed (a 512 MiB buffer written) before every step and each step is timed on its own.
+    flush = bits < (1 << 30)
+    scrub = torch.empty(1 << 27, dtype=torch.int32, device=dev) if flush else None
     pkg.launch_count(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         barrier()
         torch.cuda.synchronize()
         e0.record(stream)
-        for _ in range(args.steps):
+        for k in range(args.steps):
+            if flush:
+                scrub.fill_(k)
+            step_ev[k][0].record(stream)
             res_dev = step(a, b)
+            step_ev[k][1].record(stream)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
     launches = pkg.launch_count(reset=True)
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = sum(x.elapsed_time(y) for x, y in step_ev) / args.steps
     t = torch.tensor([ms], device=dev)
     if ws > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -593,23 +665,21 @@ def main():
     l_fft = (2 * bits // 128).bit_length() - 1
     T = pkg.fft_tile_log2(l_fft)
     fab = pkg.pipeline_fuses_operands(l_fft)
-    nbytes, ops = algorithmic(dom, bits, T, fab)
     clocks = clk.summary()
     hbm, peak_kind = peaks()
     mhz = clocks.get("sm_mhz") or 1965.0
+    # executed-work roofline per stage (the unit that binds: SMEM for table products, HBM for sweeps,
+    # the FMA pipe for generic products); the dominant stage is the headline kernel
+    per_stage = {k: stage_roofline(k, bits, T, v, mhz, hbm) for k, v in stages.items() if v > 0}
+    roof = dict(per_stage[dom])
+    roof["peak_source"] = {"smem": "128 B/clk/SM x 148 SMs at the sampled SM clock",
+                           "hbm": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                           "generic": f"{GENERIC_CLK_PER_PRODUCT} clk/product/SM (tools/microbench/gfmul_rate.cu)"}[roof["bound"]]
+    nbytes, ops = algorithmic(dom, bits, T, fab)
     peak_tops = LOP3_OPS_PER_CLK_SM * 148 * mhz * 1e6 / 1e12
-    t_hbm = nbytes / (hbm * 1e9)
-    t_int = ops / (peak_tops * 1e12)
-    if t_int >= t_hbm:
-        achieved = ops / stages[dom] / 1e12
-        roof = {"bound": "int", "achieved": round(achieved, 2), "peak": round(peak_tops, 2), "unit": "Tops/s",
-                "frac": round(achieved / peak_tops, 4),
-                "peak_source": "LOP3 microbenchmark 63 ops/clk/SM at the sampled SM clock",
-                "op_convention": "SURVEY 8(d): 552 int32 ops per GF(2^128) product (schoolbook)"}
-    else:
-        achieved = nbytes / stages[dom] / 1e9
-        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "peak_source": peak_kind}
+    roof["schoolbook_equiv_tops"] = round(ops / stages[dom] / 1e12, 2) if ops else None
+    roof["schoolbook_convention"] = "SURVEY 8(d): 552 int32 ops per GF(2^128) product; LOP3 peak " \
+                                    f"{peak_tops:.2f} Tops/s -- a convention, not executed work"
     tower = fab and os.environ.get("FPM_TOWER", "1") != "0"  # tower-representation tile pass (k_fft.cu)
     roof["kernel"] = {"pointwise": ("fft_tile_tower_kernel" if tower else "fft_tile_fused2_kernel") if fab
                       else "fft_tile_fused_kernel",
@@ -618,12 +688,8 @@ def main():
     roof["stage"] = dom
     roof["traffic"] = stage_traffic(dom, bits)
     roof["ncu_pipes"] = stage_pipes(dom, bits)
-    # whole step against the sum of per-stage roofline times (slower of bytes and ops per stage)
-    t_roof = 0.0
-    for k in stages:
-        nb, op = algorithmic(k, bits, T, fab)
-        t_roof += max(nb / (hbm * 1e9), op / (peak_tops * 1e12))
-    roof["step_frac"] = round(t_roof / (sum(stages.values())), 4)
+    roof["per_stage"] = {k: {kk: v[kk] for kk in ("bound", "frac", "t_roof_ms")} for k, v in per_stage.items()}
+    roof["step_frac"] = round(sum(v["t_roof_ms"] for v in per_stage.values()) / (sum(stages.values()) * 1e3), 4)
     roof["stage_ms"] = {k: round(v * 1e3, 3) for k, v in stages.items()}
 
     # ---- the reference's default (auto) field, GF(2^64): same product, device-resident

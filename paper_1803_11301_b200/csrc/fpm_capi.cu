@@ -14,7 +14,10 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
+#include <map>
+#include <tuple>
 #include <exception>
 #include <mutex>
 #include <random>
@@ -327,6 +330,92 @@ void karatsuba_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, s
   FPM_LAUNCH_CHECK();
 }
 
+// ------------------------------------------------------------------ CUDA graphs for repeated products
+// A product of n <= 2^26 bits is tens of short kernels: launch-bound.  Device-buffer calls
+// (fpm_polymul_dev without stage timing) replay a CUDA graph of the whole pipeline, captured on the
+// second call with the same buffers and shape (the first call runs eagerly: it uploads the device
+// tables and sets kernel attributes, which capture cannot).  Per-call scratch comes from graph
+// memory nodes.  FPM_GRAPHS=0 disables it.
+struct GraphKey {
+  const void* a;
+  size_t a_bits;
+  const void* b;
+  size_t b_bits;
+  void* c;
+  unsigned m;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(a, a_bits, b, b_bits, c, m) < std::tie(o.a, o.a_bits, o.b, o.b_bits, o.c, o.m);
+  }
+};
+bool graph_eligible(const fpm_plan& p) {
+  static const bool on = [] {
+    const char* e = std::getenv("FPM_GRAPHS");
+    return !(e && std::string(e) == "0");
+  }();
+  return on && p.n_bits <= ((uint64_t)1 << 26);
+}
+template <class Run>
+void launch_graph(const GraphKey& key, cudaStream_t s, Run&& run) {
+  struct Entry {
+    int seen = 0;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t kernels = 0;  // kernel nodes: fpm_launch_count() counts them at every replay
+  };
+  static std::mutex mu;
+  static std::map<std::pair<int, GraphKey>, Entry> cache;
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  cudaGraphExec_t exec = nullptr;
+  uint64_t kernels = 0;
+  bool capture = false;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    Entry& e = cache[{dev, key}];
+    exec = e.exec;
+    kernels = e.kernels;
+    if (!exec) capture = ++e.seen >= 2 && cache.size() <= 64;  // first sighting: run eagerly
+  }
+  if (exec) {
+    FPM_CUDA(cudaGraphLaunch(exec, s));
+    g_launches.fetch_add(kernels, std::memory_order_relaxed);
+    return;
+  }
+  if (!capture) {
+    run();
+    return;
+  }
+  cudaGraph_t g = nullptr;
+  const uint64_t n0 = g_launches.load();
+  FPM_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  try {
+    run();
+  } catch (...) {
+    cudaStreamEndCapture(s, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  FPM_CUDA(cudaStreamEndCapture(s, &g));
+  kernels = g_launches.load() - n0;  // captured, not executed (single-threaded capture assumed for the count)
+  g_launches.fetch_sub(kernels, std::memory_order_relaxed);
+  cudaGraphExec_t made = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&made, g, 0);
+  cudaGraphDestroy(g);
+  FPM_CUDA(ie);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    Entry& e = cache[{dev, key}];
+    if (e.exec) {  // another thread won the race
+      cudaGraphExecDestroy(made);
+      made = e.exec;
+    } else {
+      e.exec = made;
+      e.kernels = kernels;
+    }
+  }
+  FPM_CUDA(cudaGraphLaunch(made, s));
+  g_launches.fetch_add(kernels, std::memory_order_relaxed);
+}
+
 void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_t b_bits, uint64_t* d_c,
                     int field, cudaStream_t s, double* stages, const HostIO* io = nullptr) {
   if (!a_bits || !b_bits) return;
@@ -350,8 +439,15 @@ void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, siz
     return;
   }
   const fpm_plan p = plan_mul(a_bits, b_bits, field);  // validates the field and the size bound
-  if (p.field_degree == 64) run_pipeline<Gf64Ops>(d_a, a_bits, d_b, b_bits, d_c, p, s, stages, io);
-  else run_pipeline<Gf128Ops>(d_a, a_bits, d_b, b_bits, d_c, p, s, stages, io);
+  auto run = [&] {
+    if (p.field_degree == 64) run_pipeline<Gf64Ops>(d_a, a_bits, d_b, b_bits, d_c, p, s, stages, io);
+    else run_pipeline<Gf128Ops>(d_a, a_bits, d_b, b_bits, d_c, p, s, stages, io);
+  };
+  if (!stages && !io && graph_eligible(p)) {
+    launch_graph(GraphKey{d_a, a_bits, d_b, b_bits, d_c, p.field_degree}, s, run);
+    return;
+  }
+  run();
 }
 
 struct DeviceGuard {
