@@ -381,20 +381,28 @@ void launch_graph(const GraphKey& key, cudaStream_t s, Run&& run) {
     return;
   }
   if (!capture) {
-    run();
+    run(s);
     return;
   }
+  // Capture on a private stream (capture executes nothing, and the caller's stream may be the
+  // legacy default stream, which cannot capture); the graph is then launched on the caller's stream.
+  static cudaStream_t cap_streams[64] = {};
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!cap_streams[dev]) FPM_CUDA(cudaStreamCreateWithFlags(&cap_streams[dev], cudaStreamNonBlocking));
+  }
+  const cudaStream_t cs = cap_streams[dev];
   cudaGraph_t g = nullptr;
   const uint64_t n0 = g_launches.load();
-  FPM_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  FPM_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   try {
-    run();
+    run(cs);
   } catch (...) {
-    cudaStreamEndCapture(s, &g);
+    cudaStreamEndCapture(cs, &g);
     if (g) cudaGraphDestroy(g);
     throw;
   }
-  FPM_CUDA(cudaStreamEndCapture(s, &g));
+  FPM_CUDA(cudaStreamEndCapture(cs, &g));
   kernels = g_launches.load() - n0;  // captured, not executed (single-threaded capture assumed for the count)
   g_launches.fetch_sub(kernels, std::memory_order_relaxed);
   cudaGraphExec_t made = nullptr;
@@ -439,15 +447,15 @@ void polymul_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, siz
     return;
   }
   const fpm_plan p = plan_mul(a_bits, b_bits, field);  // validates the field and the size bound
-  auto run = [&] {
-    if (p.field_degree == 64) run_pipeline<Gf64Ops>(d_a, a_bits, d_b, b_bits, d_c, p, s, stages, io);
-    else run_pipeline<Gf128Ops>(d_a, a_bits, d_b, b_bits, d_c, p, s, stages, io);
+  auto run = [&](cudaStream_t st) {
+    if (p.field_degree == 64) run_pipeline<Gf64Ops>(d_a, a_bits, d_b, b_bits, d_c, p, st, stages, io);
+    else run_pipeline<Gf128Ops>(d_a, a_bits, d_b, b_bits, d_c, p, st, stages, io);
   };
   if (!stages && !io && graph_eligible(p)) {
     launch_graph(GraphKey{d_a, a_bits, d_b, b_bits, d_c, p.field_degree}, s, run);
     return;
   }
-  run();
+  run(s);
 }
 
 struct DeviceGuard {
