@@ -14,7 +14,8 @@ M = {"dur": "gpu__time_duration.sum", "rd": "dram__bytes_read.sum", "wr": "dram_
      "smem": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
      "L1": "l1tex__throughput.avg.pct_of_peak_sustained_active",
      "occ": "sm__warps_active.avg.pct_of_peak_sustained_active"}
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
+         "ns": 1e-6, "us": 1e-3, "ms": 1.0, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
 
 out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv", "--metrics", ",".join(M.values())],
                      capture_output=True, text=True, check=True).stdout
