@@ -17,6 +17,8 @@
 // HBM traffic at K = 32: ~9 GiB (vs ~70 GiB for 48 separate passes).  Arrays of <= 2^16 bits run in
 // one shared-memory tile; > 2^32 bits run their top passes with the generic in-place pass kernel
 // and recurse per 2^32-bit block.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -599,6 +601,152 @@ __global__ void __launch_bounds__(kC256Threads, INV ? 3 : 4) conv256_units_kerne
   }
 }
 
+// ---- the same conv(256) over units with TMA-fed staging (no fused carry input): 128 B of each of
+// the 256 units per item (a warp = one unit row x 32 words), moved global -> shared by 256
+// cp.async.bulk copies completing on an mbarrier, double-buffered so item k+2's copies run while
+// item k computes; 512 threads, one CTA per SM (2 x 32 KiB staging + 66 KiB of Z).  The register
+// phases are those of conv256_units_kernel.
+constexpr int kCT = 32;                      // words of each unit per item
+constexpr int kCTThreads = 16 * kCT;         // (r, c), r < 16
+constexpr size_t kCTStage = 256 * kCT * 4;   // bytes per staging buffer
+constexpr size_t kCTSmem = 2 * kCTStage + 16 * 33 * kCT * 4 + 16;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+template <bool INV>
+__global__ void __launch_bounds__(kCTThreads, 1) conv256_units_tma_kernel(uint32_t* data, UnitMap um, uint64_t nitems,
+                                                                          const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) uint32_t sm_ct[];
+  auto stage = [&](int st) { return sm_ct + st * (256 * kCT); };
+  uint32_t* Z = sm_ct + 2 * 256 * kCT;  // [d][33][kCT]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Z + 16 * 33 * kCT);
+  const int tid = threadIdx.x, c = tid % kCT, r = tid / kCT;
+  constexpr int kCols = kTWords / kCT;
+  auto zi = [](int d, int s, int cc) { return (d * 33 + s) * kCT + cc; };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // one TMA box per item: 32 words x 1 x 256 units of the (word, group-in-stride, unit-row) view
+  auto issue = [&](uint64_t it, int st) {
+    if (tid != 0 || it >= nitems) return;
+    mbar_expect_tx(&bar[st], (uint32_t)kCTStage);
+    const uint64_t grp = it / kCols;
+    const int c0 = (int)((it % kCols) * kCT), c1 = (int)(grp % um.gstride), c2 = (int)((grp / um.gstride) * 256);
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(stage(st))),
+        "l"(&tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(&bar[st]))
+        : "memory");
+  };
+  uint32_t phases = 0;  // bit st: parity of stage st's next completion
+  issue(blockIdx.x, 0);
+  issue(blockIdx.x + gridDim.x, 1);
+  int st = 0;
+  for (uint64_t it = blockIdx.x; it < nitems; it += gridDim.x, st ^= 1) {
+    const uint64_t grp = it / kCols, colw = (it % kCols) * kCT + c;
+    uint32_t* const gbase = data + um.row(grp, 0) * kTWords + colw;
+    const uint32_t ustep = (uint32_t)(um.ustride * kTWords);
+    auto at = [&](int u) -> uint32_t* { return gbase + (uint32_t)u * ustep; };
+    const uint32_t* sg = stage(st);
+    mbar_wait(&bar[st], (phases >> st) & 1u);
+    phases ^= 1u << st;
+    uint32_t x[16];
+    if (!INV) {
+      uint32_t y[16];
+#pragma unroll
+      for (int d = 0; d < 16; ++d) {
+        const int v0 = r - d, v1 = r + 16 - d;
+        x[d] = v0 >= 0 ? sg[(16 * d + v0) * kCT + c] : 0u;
+        y[d] = v1 < 16 ? sg[(16 * d + v1) * kCT + c] : 0u;
+      }
+      __syncthreads();  // staging consumed: refill it with item + 2 while this item computes
+      if (tid == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(it + 2 * (uint64_t)gridDim.x, st);
+      zeta16_vals(x);
+      zeta16_vals(y);
+#pragma unroll
+      for (int d = 0; d < 16; ++d) {
+        Z[zi(d, r, c)] = x[d];
+        Z[zi(d, r + 16, c)] = y[d];
+      }
+      __syncthreads();
+      const int v = r;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        uint32_t g = Z[zi(k, v + k, c)];
+        if (v >= 1 && 15 + v + k < 31) g ^= Z[zi(k, 15 + v + k, c)];
+        if (k >= 1 && 15 + v + k < 31) g ^= Z[zi(k - 1, 15 + v + k, c)];
+        x[k] = g;
+      }
+      conv16_vals<false>(x);
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) Z[zi(k, v, c)] = x[k];
+      __syncthreads();
+#pragma unroll
+      for (int vv = 0; vv < 16; ++vv) x[vv] = Z[zi(r, vv, c)];
+      conv16_vals<false>(x);
+#pragma unroll
+      for (int vv = 0; vv < 16; ++vv) *at(16 * r + vv) = x[vv];
+    } else {
+#pragma unroll
+      for (int vv = 0; vv < 16; ++vv) x[vv] = sg[(16 * r + vv) * kCT + c];
+      __syncthreads();
+      if (tid == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(it + 2 * (uint64_t)gridDim.x, st);
+      conv16_vals<true>(x);
+#pragma unroll
+      for (int vv = 0; vv < 16; ++vv) Z[zi(r, vv, c)] = x[vv];
+      __syncthreads();
+      const int v = r;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) x[k] = Z[zi(k, v, c)];
+      conv16_vals<true>(x);
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) Z[zi(k, v + k, c)] = x[k];
+      __syncthreads();
+      uint32_t y[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        x[k] = (r >= k) ? Z[zi(k, r, c)] : 0u;
+        y[k] = (r + 16 < k + 16) ? Z[zi(k, r + 16, c)] : 0u;
+      }
+      zeta16_vals(x);
+      zeta16_vals(y);
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        Z[zi(k, r, c)] = x[k];
+        Z[zi(k, r + 16, c)] = y[k];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int vv = 0; vv < 16; ++vv) {
+        uint32_t f = Z[zi(r, vv + r, c)];
+        if (r >= 1 && 15 + vv + r < 31) f ^= Z[zi(r - 1, 15 + vv + r, c)];
+        *at(16 * r + vv) = f;
+      }
+    }
+    __syncthreads();  // Z reuse by the next item
+  }
+}
+
 // ------------------------------------------------------------------ unit-level L1 carry + C_cols
 // Rows of t bits are units; row d = 256 * dh + v (digit dh, offset v).  After the unit-skewed zeta,
 // Gs[kh] holds units u = 0 .. 256+Dd-1 (pitch gs_pitch words).  Output unit (kh, v):
@@ -832,6 +980,41 @@ constexpr size_t kSlabSmem = 256 * kRowPitchW<kSlabW> * sizeof(uint32_t);
 // nslabs counts 8-word columns (callers' unit); the kernels take kSlabW of them per slab.
 // conv(256) over groups of 256 units: group g's unit u is row base(g) + u * ustride, base(g) =
 // (g % gstride) + (g / gstride) * 256 * gstride.
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    FPM_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw Error(kCuda, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// The unit view of conv256_units as a 3-D uint32 tensor: (word of a row, group index within the
+// stride, unit row), box 32 x 1 x 256.
+CUtensorMap unit_tensor_map(uint32_t* w, uint64_t rows, uint64_t gstride) {
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {(cuuint64_t)kTWords, (cuuint64_t)gstride, (cuuint64_t)(rows / gstride)};
+  const cuuint64_t strides[2] = {(cuuint64_t)kTWords * 4, (cuuint64_t)kTWords * 4 * gstride};
+  const cuuint32_t box[3] = {(cuuint32_t)kCT, 1, 256};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, w, dims, strides, box, estr,
+                                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(kCuda, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+bool tma_units_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FPM_TMA_UNITS");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
 void conv256_units(uint32_t* w, uint64_t ngroups, uint64_t ustride, uint64_t gstride, bool inv, cudaStream_t s,
                    CarrySrc cs = CarrySrc{}) {
   static PerDeviceOnce attr;
@@ -840,6 +1023,21 @@ void conv256_units(uint32_t* w, uint64_t ngroups, uint64_t ustride, uint64_t gst
     FPM_CUDA(cudaFuncSetAttribute(conv256_units_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC256Smem));
   });
   UnitMap um{ustride, gstride, ngroups};
+  if (!cs.gs && tma_units_enabled()) {
+    static PerDeviceOnce tattr;
+    tattr.run([&] {
+      FPM_CUDA(cudaFuncSetAttribute(conv256_units_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCTSmem));
+      FPM_CUDA(cudaFuncSetAttribute(conv256_units_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCTSmem));
+    });
+    const uint64_t titems = ngroups * (kTWords / kCT);
+    // groups of 256 units: (ustride, gstride) = (1, 1) consecutive rows, or (g, g) rows g apart
+    if (ustride != gstride) throw Error(kInvalid, "conv256_units: unit stride must equal the group stride");
+    const CUtensorMap tm = unit_tensor_map(w, ngroups * 256, gstride);
+    if (inv) conv256_units_tma_kernel<true><<<grid_cap(titems, 1), kCTThreads, kCTSmem, s>>>(w, um, titems, tm);
+    else conv256_units_tma_kernel<false><<<grid_cap(titems, 1), kCTThreads, kCTSmem, s>>>(w, um, titems, tm);
+    FPM_LAUNCH_CHECK();
+    return;
+  }
   const uint64_t items = ngroups * (kTWords / kC256Cols);
   if (inv) conv256_units_kernel<true><<<grid_cap(items, 3), kC256Threads, kC256Smem, s>>>(w, um, items, cs);
   else conv256_units_kernel<false><<<grid_cap(items, 4), kC256Threads, kC256Smem, s>>>(w, um, items, cs);
