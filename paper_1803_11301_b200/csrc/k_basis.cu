@@ -606,7 +606,11 @@ __global__ void __launch_bounds__(kC256Threads, INV ? 3 : 4) conv256_units_kerne
 // cp.async.bulk copies completing on an mbarrier, double-buffered so item k+2's copies run while
 // item k computes; 512 threads, one CTA per SM (2 x 32 KiB staging + 66 KiB of Z).  The register
 // phases are those of conv256_units_kernel.
-constexpr int kCT = 32;                      // words of each unit per item
+#ifndef FPM_CT_WORDS
+#define FPM_CT_WORDS 32
+#endif
+constexpr int kCT = FPM_CT_WORDS;            // words of each unit per item (16: 3 CTAs/SM, 32: 1)
+constexpr int kCTMinBlocks = kCT == 16 ? 3 : 1;
 constexpr int kCTThreads = 16 * kCT;         // (r, c), r < 16
 constexpr size_t kCTStage = 256 * kCT * 4;   // bytes per staging buffer
 constexpr size_t kCTSmem = 2 * kCTStage + 16 * 33 * kCT * 4 + 16;
@@ -626,7 +630,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 template <bool INV>
-__global__ void __launch_bounds__(kCTThreads, 1) conv256_units_tma_kernel(uint32_t* data, UnitMap um, uint64_t nitems,
+__global__ void __launch_bounds__(kCTThreads, kCTMinBlocks) conv256_units_tma_kernel(uint32_t* data, UnitMap um, uint64_t nitems,
                                                                           const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) uint32_t sm_ct[];
   auto stage = [&](int st) { return sm_ct + st * (256 * kCT); };
@@ -1033,8 +1037,8 @@ void conv256_units(uint32_t* w, uint64_t ngroups, uint64_t ustride, uint64_t gst
     // groups of 256 units: (ustride, gstride) = (1, 1) consecutive rows, or (g, g) rows g apart
     if (ustride != gstride) throw Error(kInvalid, "conv256_units: unit stride must equal the group stride");
     const CUtensorMap tm = unit_tensor_map(w, ngroups * 256, gstride);
-    if (inv) conv256_units_tma_kernel<true><<<grid_cap(titems, 1), kCTThreads, kCTSmem, s>>>(w, um, titems, tm);
-    else conv256_units_tma_kernel<false><<<grid_cap(titems, 1), kCTThreads, kCTSmem, s>>>(w, um, titems, tm);
+    if (inv) conv256_units_tma_kernel<true><<<grid_cap(titems, kCTMinBlocks), kCTThreads, kCTSmem, s>>>(w, um, titems, tm);
+    else conv256_units_tma_kernel<false><<<grid_cap(titems, kCTMinBlocks), kCTThreads, kCTSmem, s>>>(w, um, titems, tm);
     FPM_LAUNCH_CHECK();
     return;
   }
