@@ -168,6 +168,7 @@ struct HostIO {
 // Field plumbing of run_pipeline<F> (polymul.cpp:78-135) for the two fields built on the GPU.
 struct Gf128Ops {
   using E = uint4;
+  static constexpr bool kFusedEncode = true;  // basis_cvt's last step can write the encode
   using Tw = TwiddleSrc;
   static constexpr int kLiveRows = 64;  // rows >= m/2 of a padded operand are zero
   static Tw twiddles(int dev, unsigned l) { return make_twiddle_src(dev, l, partition_base(l)); }
@@ -197,6 +198,7 @@ struct Gf128Ops {
 };
 struct Gf64Ops {
   using E = uint2;
+  static constexpr bool kFusedEncode = false;
   using Tw = TwiddleSrc64;
   static constexpr int kLiveRows = 32;
   static Tw twiddles(int dev, unsigned l) { return make_twiddle_src64(dev, l, partition_base64(l)); }
@@ -275,16 +277,20 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     const uint64_t half_words = n / 128;  // n/2 bits in uint64 words
     size_t count = (size_t)1 << log2_ceil(xbits[k]);
     if (count < 32) count = 32;
+    // a 2^32-bit conversion's last step also encodes (GF(2^128): the converted bits never reach HBM)
+    EncodeSink sink{reinterpret_cast<uint4*>(es[k]), rep};
+    const bool fused = F::kFusedEncode && count == n / 2 && basis_cvt_can_encode(count, rep);
     if (xbits[k] == n / 2 && count == n / 2 && count >= ((size_t)1 << 17) && count <= ((size_t)1 << 32)) {
       // the operand fills the conversion exactly: convert straight from the caller's buffer
-      basis_cvt_device(work32, count, xbits[k], false, s, nullptr, reinterpret_cast<const uint32_t*>(xs[k]));
+      basis_cvt_device(work32, count, xbits[k], false, s, nullptr, reinterpret_cast<const uint32_t*>(xs[k]),
+                       fused ? &sink : nullptr);
     } else {
       load_operand_kernel<<<grid_1d(half_words), 256, 0, s>>>(work, half_words, xs[k], xbits[k]);
       FPM_LAUNCH_CHECK();
-      basis_cvt_device(work32, count, xbits[k], false, s);
+      basis_cvt_device(work32, count, xbits[k], false, s, nullptr, nullptr, fused ? &sink : nullptr);
     }
     clk.mark(kStEncode);
-    F::encode(work32, l, es[k], s, rep);
+    if (!fused) F::encode(work32, l, es[k], s, rep);
     clk.mark(kStBfly);
     F::top(es[k], l, T, false, tw, s, rep);
     if (k == 0 && !fuse_ab) F::tile(es[k], l, T, false, tw, s);

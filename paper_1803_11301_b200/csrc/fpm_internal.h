@@ -172,8 +172,17 @@ const DeviceTables& device_tables(int device);
 using FinalFn = std::function<void(uint64_t w0, uint64_t w1)>;
 // src (forward, 2^17..2^32 bits only; may be null): the unconverted array is read from src and the
 // result written to w (w's prior contents are ignored).
+// enc (forward 2^32-bit conversions only, basis_cvt_can_encode): the conversion's last step writes
+// the GF(2^128) encode of the converted operand (64 live partition rows, l = 26) to enc->ev instead
+// of the converted bits (w is then scratch on exit).
+struct EncodeSink {
+  uint4* ev;
+  bool tower;  // elements in the tower representation R (the product pipeline's FFT)
+};
+bool basis_cvt_can_encode(size_t n_bits, bool tower);
 void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s,
-                      const FinalFn* on_final = nullptr, const uint32_t* src = nullptr);
+                      const FinalFn* on_final = nullptr, const uint32_t* src = nullptr,
+                      const EncodeSink* enc = nullptr);
 
 // The halves of a 2^33-bit inverse conversion as separate calls (sharded products: the two 2^32-bit
 // blocks converted on different GPUs).  Upper block: basis_cvt_device(w_hi, 2^32, 2^32, true, s); then

@@ -28,6 +28,8 @@
 
 #include "basis_dev.cuh"
 #include "conv_tile.cuh"
+#include "gf128.cuh"
+#include "warp_bits.cuh"
 #include "fpm_internal.h"
 
 namespace fpm {
@@ -751,6 +753,120 @@ __global__ void __launch_bounds__(kCTThreads, kCTMinBlocks) conv256_units_tma_ke
   }
 }
 
+// ---- the last step of a forward 2^32-bit conversion fused with the Frobenius-partition encode
+// (encode.cpp:165-193): conv(256) over the digit A of the rows B + 256 A (one item = a fixed B and
+// 32 words of every row), then, instead of writing the converted rows back, the item's 4096 encode
+// elements: element i = a 2^24 + B 2^16 + 1024 cb + e (a < 4, e < 1024) takes bit j < 64 (the
+// operand's live partition rows) from converted row A = 4 j + a, bit 32 col + lane of the item's
+// words -- rows 4j + a of the item are exactly a 64 x 1024-bit encode slab.  The slab goes through
+// the warp transpose and the 8 byte-chunk lookups of encode_kernel<64>; the converted operand never
+// reaches HBM (its write and the separate encode sweep's read disappear).
+constexpr size_t kCTEncSmem = kCTSmem + (size_t)(kM8Uint4 / 2) * sizeof(uint4);
+__global__ void __launch_bounds__(kCTThreads, 1) conv256_a_encode_kernel(const uint32_t* data, UnitMap um,
+                                                                         uint64_t nitems,
+                                                                         const __grid_constant__ CUtensorMap tmap,
+                                                                         const uint4* __restrict__ tab_g,
+                                                                         uint4* __restrict__ ev) {
+  extern __shared__ __align__(128) uint32_t sm_ct[];
+  auto stage = [&](int st) { return sm_ct + st * (256 * kCT); };
+  uint32_t* Z = sm_ct + 2 * 256 * kCT;  // [d][33][kCT]; after the conv: the converted rows [A][33]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Z + 16 * 33 * kCT);
+  uint4* tab = reinterpret_cast<uint4*>(sm_ct + (kCTSmem / 4));  // x*E byte-chunk table (chunks 0..7)
+  const int tid = threadIdx.x, c = tid % kCT, r = tid / kCT, lane = tid & 31, warp = tid >> 5;
+  constexpr int kCols = kTWords / kCT;
+  auto zi = [](int d, int s, int cc) { return (d * 33 + s) * kCT + cc; };
+  for (int i = tid; i < kM8Uint4 / 2; i += kCTThreads) tab[i] = tab_g[i];
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](uint64_t it, int st) {
+    if (tid != 0 || it >= nitems) return;
+    mbar_expect_tx(&bar[st], (uint32_t)kCTStage);
+    const uint64_t grp = it / kCols;
+    const int c0 = (int)((it % kCols) * kCT), c1 = (int)(grp % um.gstride), c2 = (int)((grp / um.gstride) * 256);
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(stage(st))),
+        "l"(&tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(&bar[st]))
+        : "memory");
+  };
+  const int q8 = lane & 7;
+  const Transpose32 tr(lane);
+  uint32_t phases = 0;
+  issue(blockIdx.x, 0);
+  issue(blockIdx.x + gridDim.x, 1);
+  int st = 0;
+  for (uint64_t it = blockIdx.x; it < nitems; it += gridDim.x, st ^= 1) {
+    const uint64_t B = it / kCols, cb = it % kCols;  // groups = B (um.gstride = 256)
+    const uint32_t* sg = stage(st);
+    mbar_wait(&bar[st], (phases >> st) & 1u);
+    phases ^= 1u << st;
+    uint32_t x[16], y[16];
+#pragma unroll
+    for (int d = 0; d < 16; ++d) {
+      const int v0 = r - d, v1 = r + 16 - d;
+      x[d] = v0 >= 0 ? sg[(16 * d + v0) * kCT + c] : 0u;
+      y[d] = v1 < 16 ? sg[(16 * d + v1) * kCT + c] : 0u;
+    }
+    __syncthreads();
+    if (tid == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    issue(it + 2 * (uint64_t)gridDim.x, st);
+    zeta16_vals(x);
+    zeta16_vals(y);
+#pragma unroll
+    for (int d = 0; d < 16; ++d) {
+      Z[zi(d, r, c)] = x[d];
+      Z[zi(d, r + 16, c)] = y[d];
+    }
+    __syncthreads();
+    const int v = r;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      uint32_t g = Z[zi(k, v + k, c)];
+      if (v >= 1 && 15 + v + k < 31) g ^= Z[zi(k, 15 + v + k, c)];
+      if (k >= 1 && 15 + v + k < 31) g ^= Z[zi(k - 1, 15 + v + k, c)];
+      x[k] = g;
+    }
+    conv16_vals<false>(x);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) Z[zi(k, v, c)] = x[k];
+    __syncthreads();
+#pragma unroll
+    for (int vv = 0; vv < 16; ++vv) x[vv] = Z[zi(r, vv, c)];
+    conv16_vals<false>(x);
+    __syncthreads();  // every thread's conv input read from Z: Z now holds the converted rows
+#pragma unroll
+    for (int vv = 0; vv < 16; ++vv) {  // row A = 16 r + vv stored at (A % 4) * 64 + A / 4: the
+      const int A = 16 * r + vv;        // encode's slab rows A = 4 j + a are then consecutive
+      Z[((A & 3) * 64 + (A >> 2)) * 33 + c] = x[vv];
+    }
+    __syncthreads();
+    // encode: (a, col) pairs, 8 per warp; slab row j of sub-slab a is converted row 4 j + a
+    const uint64_t e0 = B * 65536 + cb * 1024;
+#pragma unroll 1
+    for (int k = 0; k < 8; ++k) {
+      const int pair = warp * 8 + k, a = pair >> 5, col = pair & 31;
+      const uint32_t x0 = tr(Z[(a * 64 + lane) * 33 + col]);        // rows j = lane
+      const uint32_t x1 = tr(Z[(a * 64 + 32 + lane) * 33 + col]);   // rows j = 32 + lane
+      uint4 acc0 = make_uint4(0, 0, 0, 0), acc1 = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int kk = 0; kk < 8; kk += 2) {
+        const int k0 = (kk + q8) & 7, k1 = (kk + 1 + q8) & 7;
+        const uint32_t b0 = __byte_perm(k0 < 4 ? x0 : x1, 0, 0x4440u | (uint32_t)(k0 & 3));
+        const uint32_t b1 = __byte_perm(k1 < 4 ? x0 : x1, 0, 0x4440u | (uint32_t)(k1 & 3));
+        acc0 = x4v(acc0, tab[b0 * 8 + k0]);
+        acc1 = x4v(acc1, tab[b1 * 8 + k1]);
+      }
+      ev[(uint64_t)a * (1u << 24) + e0 + 32 * col + lane] = x4v(acc0, acc1);
+    }
+    __syncthreads();  // Z reuse by the next item
+  }
+}
+
 // ------------------------------------------------------------------ unit-level L1 carry + C_cols
 // Rows of t bits are units; row d = 256 * dh + v (digit dh, offset v).  After the unit-skewed zeta,
 // Gs[kh] holds units u = 0 .. 256+Dd-1 (pitch gs_pitch words).  Output unit (kh, v):
@@ -1197,7 +1313,23 @@ uint64_t split_side_words(int lgD) {
 //   over Dd/2^k digits of 256*2^k rows (skew 2^k rows) then w inside each chunk (skew 1 row)
 //   (tools/models/bc2_model.py), then conv(Dd) over the digit (rows 256 apart) and conv(256) over
 //   the row within the digit.  The inverse runs the same in reverse.
-void conv_cols_split(uint32_t* w, uint32_t* side, int lgD, bool inv, cudaStream_t s) {
+void conv256_a_encode(uint32_t* w, const EncodeSink& enc, cudaStream_t s) {
+  static PerDeviceOnce attr;
+  attr.run([] {
+    FPM_CUDA(cudaFuncSetAttribute(conv256_a_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCTEncSmem));
+  });
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  const DeviceTables& dt = device_tables(dev);
+  UnitMap um{256, 256, 256};
+  const uint64_t items = 256 * (kTWords / kCT);
+  const CUtensorMap tm = unit_tensor_map(w, 65536, 256);
+  conv256_a_encode_kernel<<<grid_cap(items, 1), kCTThreads, kCTEncSmem, s>>>(w, um, items, tm,
+                                                                              enc.tower ? dt.enc_m8r : dt.enc_m8, enc.ev);
+  FPM_LAUNCH_CHECK();
+}
+
+void conv_cols_split(uint32_t* w, uint32_t* side, int lgD, bool inv, cudaStream_t s, const EncodeSink* enc = nullptr) {
   if (lgD <= 1) return;
   if (lgD <= 8) {
     slab(w, lgD, 1, kTWords / 8, inv, s);
@@ -1228,6 +1360,11 @@ void conv_cols_split(uint32_t* w, uint32_t* side, int lgD, bool inv, cudaStream_
   };
   if (!inv) {
     l1d(true);
+    if (enc && gd == 8 && tma_units_enabled()) {  // conv over B, then conv over A fused with the encode
+      conv256_units(w, Dd, 1, 1, false, s);
+      conv256_a_encode(w, *enc, s);
+      return;
+    }
     over_digit(false);
     conv256_units(w, Dd, 1, 1, false, s);
   } else {
@@ -1238,7 +1375,7 @@ void conv_cols_split(uint32_t* w, uint32_t* side, int lgD, bool inv, cudaStream_
 }
 
 void conv2d_split(uint32_t* w, int K, bool inv, uint32_t* scratch, uint32_t* side, cudaStream_t s,
-                  const uint32_t* src = nullptr, const uint32_t* top = nullptr) {
+                  const uint32_t* src = nullptr, const uint32_t* top = nullptr, const EncodeSink* enc = nullptr) {
   const int lgD = K - kTLog2;
   const uint64_t D = (uint64_t)1 << lgD;
   const int nb_in = std::min(lgD, 8), nb_out = lgD - nb_in;
@@ -1257,7 +1394,7 @@ void conv2d_split(uint32_t* w, int K, bool inv, uint32_t* scratch, uint32_t* sid
     zeta(in, kTWords, scratch, p1, D, 0, nb_in, lo_skew, p1 / kZW, s, kTWords);
     carry_rows_kernel<<<grid_cap(D, 7), 256, kTileSmem, s>>>(scratch, p1, w, D, 255);
     FPM_LAUNCH_CHECK();
-    conv_cols_split(w, side, lgD, false, s);
+    conv_cols_split(w, side, lgD, false, s, enc);
   } else {
     conv_cols_split(w, side, lgD, true, s);
     conv_rows(w, D * kTWords, kTLog2, true, s);
@@ -1317,8 +1454,15 @@ void top_bit_fix_device(uint32_t* hi_block, cudaStream_t s) {
   FPM_LAUNCH_CHECK();
 }
 
+bool basis_cvt_can_encode(size_t n_bits, bool tower) {
+  (void)tower;
+  return n_bits == ((size_t)1 << 32) && split_l1_enabled() && tma_units_enabled();
+}
+
 void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s,
-                      const FinalFn* on_final, const uint32_t* src) {
+                      const FinalFn* on_final, const uint32_t* src, const EncodeSink* enc) {
+  if (enc && (inverse || !basis_cvt_can_encode(n_bits, enc->tower)))
+    throw Error(kInvalid, "basis_cvt: the fused encode needs a forward 2^32-bit conversion");
   if (n_bits < 4 || (n_bits & (n_bits - 1))) throw Error(kInvalid, "basis_cvt: length must be a power of two >= 4");
   set_smem_attr();
   int K = 0;
@@ -1355,7 +1499,7 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
   uint32_t* scratch = static_cast<uint32_t*>(scr.p);
   uint32_t* side = static_cast<uint32_t*>(side_buf.p);
   auto conv_block = [&](uint32_t* blk, const uint32_t* from, const uint32_t* tp) {
-    if (split) conv2d_split(blk, Kb, inverse, scratch, side, s, from, tp);
+    if (split) conv2d_split(blk, Kb, inverse, scratch, side, s, from, tp, enc);
     else conv2d(blk, Kb, inverse, scratch, s, from, tp);
   };
   const uint64_t block_words = ((uint64_t)1 << Kb) / 32;
