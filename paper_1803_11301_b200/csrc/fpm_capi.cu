@@ -301,7 +301,10 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
   clk.mark(kStIBfly);
   F::top(EB.as<E>(), l, T, true, tw, s, rep);
   clk.mark(kStDecode);
-  F::decode(EB.as<E>(), l, work32, s, rep);
+  // a 2^33-bit product's decode runs inside the inverse conversion's first step (GF(2^128))
+  const bool fused_dec = F::kFusedEncode && basis_cvt_can_decode(n);
+  DecodeSource dsrc{reinterpret_cast<const uint4*>(EB.template as<E>()), rep};
+  if (!fused_dec) F::decode(EB.as<E>(), l, work32, s, rep);
   clk.mark(kStIBasis);
   // Each finished range of the product is trimmed into d_c (and copied out) right away.
   const FinalFn on_final = [&](uint64_t w0, uint64_t w1) {  // 32-bit word range of P
@@ -315,7 +318,7 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     }
     copy_out(q0, q1);
   };
-  basis_cvt_device(work32, n, n, true, s, &on_final);
+  basis_cvt_device(work32, n, n, true, s, &on_final, nullptr, nullptr, fused_dec ? &dsrc : nullptr);
   clk.finish();
 }
 

@@ -180,9 +180,17 @@ struct EncodeSink {
   bool tower;  // elements in the tower representation R (the product pipeline's FFT)
 };
 bool basis_cvt_can_encode(size_t n_bits, bool tower);
+// dec (inverse 2^33-bit conversions only, basis_cvt_can_decode): the GF(2^128) decode of dec->ev
+// (2^26 elements) is the conversion's input -- fused into its first step; w's contents on entry are
+// ignored.
+struct DecodeSource {
+  const uint4* ev;
+  bool tower;
+};
+bool basis_cvt_can_decode(size_t n_bits);
 void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s,
                       const FinalFn* on_final = nullptr, const uint32_t* src = nullptr,
-                      const EncodeSink* enc = nullptr);
+                      const EncodeSink* enc = nullptr, const DecodeSource* dec = nullptr);
 
 // The halves of a 2^33-bit inverse conversion as separate calls (sharded products: the two 2^32-bit
 // blocks converted on different GPUs).  Upper block: basis_cvt_device(w_hi, 2^32, 2^32, true, s); then

@@ -867,6 +867,103 @@ __global__ void __launch_bounds__(kCTThreads, 1) conv256_a_encode_kernel(const u
   }
 }
 
+// ---- the first step of a 2^33-bit inverse conversion fused with the decode (encode.cpp:195-220):
+// one item = a fixed row offset B and 32 words of every row, for BOTH 2^32-bit blocks.  The item's
+// 4096 elements i = a 2^24 + B 2^16 + 1024 cb + e (a < 4) are decoded (16 byte-chunk lookups of
+// x*E^-1, the warp transpose of decode_kernel), which yields, for block b, the rows A = 4 j + a
+// (j = partition row - 64 b) of the item; then conv(256)^-1 over A (the inverse register phases of
+// conv256_units_kernel) runs on each block's 256 rows and the results are stored.  The decoded
+// product array never reaches HBM.
+constexpr size_t kDecRows = 256 * 33;  // one block's rows of an item, [A][33]
+constexpr size_t kDecSmem = (size_t)kM8Uint4 * sizeof(uint4) + (2 * kDecRows + 16 * 33 * kCT) * sizeof(uint32_t);
+__global__ void __launch_bounds__(kCTThreads, 1) decode_conv_a_kernel(const uint4* __restrict__ ev,
+                                                                      const uint4* __restrict__ tab_g,
+                                                                      uint32_t* __restrict__ w_lo,
+                                                                      uint32_t* __restrict__ w_hi, uint64_t nitems) {
+  extern __shared__ __align__(16) uint4 sm_dc[];
+  uint4* tab = sm_dc;  // x*E^-1 byte-chunk tables (gf128.cuh m8 layout, 16 chunks)
+  uint32_t* Rw = reinterpret_cast<uint32_t*>(sm_dc + kM8Uint4);  // [block][A][33]
+  uint32_t* Z = Rw + 2 * kDecRows;                                // [d][33][kCT]
+  const int tid = threadIdx.x, c = tid % kCT, r = tid / kCT, lane = tid & 31, warp = tid >> 5;
+  constexpr int kCols = kTWords / kCT;
+  auto zi = [](int d, int s, int cc) { return (d * 33 + s) * kCT + cc; };
+  for (int i = tid; i < kM8Uint4; i += kCTThreads) tab[i] = tab_g[i];
+  const int q8 = lane & 7;
+  const Transpose32 tr(lane);
+  __syncthreads();
+  for (uint64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const uint64_t B = it / kCols, cb = it % kCols;
+    const uint64_t e0 = B * 65536 + cb * 1024;
+    // ---- decode: (a, col) pairs, 8 per warp; all eight elements' loads first
+    uint4 f[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int pair = warp * 8 + k, a = pair >> 5, col = pair & 31;
+      f[k] = __ldg(ev + (uint64_t)a * (1u << 24) + e0 + 32 * col + lane);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int pair = warp * 8 + k, a = pair >> 5, col = pair & 31;
+      const uint4 y = m8_mul(tab, f[k], q8);
+      // word q of y: partition rows 32q + lane after the transpose; block q >> 1, row A = 4 j + a
+      const uint32_t yw[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = 32 * (q & 1) + lane;
+        Rw[(q >> 1) * kDecRows + (a * 64 + j) * 33 + col] = tr(yw[q]);  // row A = 4 j + a at (A%4)*64 + A/4
+      }
+    }
+    __syncthreads();
+    // ---- conv(256)^-1 over A, each block (inverse phases of conv256_units_kernel)
+#pragma unroll 1
+    for (int blk = 0; blk < 2; ++blk) {
+      const uint32_t* Rb = Rw + blk * kDecRows;
+      uint32_t* const gbase = (blk ? w_hi : w_lo) + B * kTWords + cb * kCT + c;
+      auto at = [&](int u) -> uint32_t* { return gbase + (uint64_t)u * 256 * kTWords; };
+      uint32_t x[16];
+#pragma unroll
+      for (int vv = 0; vv < 16; ++vv) {
+        const int A = 16 * r + vv;
+        x[vv] = Rb[((A & 3) * 64 + (A >> 2)) * 33 + c];
+      }
+      conv16_vals<true>(x);
+#pragma unroll
+      for (int vv = 0; vv < 16; ++vv) Z[zi(r, vv, c)] = x[vv];
+      __syncthreads();
+      const int v = r;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) x[k] = Z[zi(k, v, c)];
+      conv16_vals<true>(x);
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) Z[zi(k, v + k, c)] = x[k];
+      __syncthreads();
+      uint32_t y[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        x[k] = (r >= k) ? Z[zi(k, r, c)] : 0u;
+        y[k] = (r + 16 < k + 16) ? Z[zi(k, r + 16, c)] : 0u;
+      }
+      zeta16_vals(x);
+      zeta16_vals(y);
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        Z[zi(k, r, c)] = x[k];
+        Z[zi(k, r + 16, c)] = y[k];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int vv = 0; vv < 16; ++vv) {
+        uint32_t fv = Z[zi(r, vv + r, c)];
+        if (r >= 1 && 15 + vv + r < 31) fv ^= Z[zi(r - 1, 15 + vv + r, c)];
+        *at(16 * r + vv) = fv;
+      }
+      __syncthreads();  // Z reuse
+    }
+  }
+}
+
 // ------------------------------------------------------------------ unit-level L1 carry + C_cols
 // Rows of t bits are units; row d = 256 * dh + v (digit dh, offset v).  After the unit-skewed zeta,
 // Gs[kh] holds units u = 0 .. 256+Dd-1 (pitch gs_pitch words).  Output unit (kh, v):
@@ -1329,7 +1426,9 @@ void conv256_a_encode(uint32_t* w, const EncodeSink& enc, cudaStream_t s) {
   FPM_LAUNCH_CHECK();
 }
 
-void conv_cols_split(uint32_t* w, uint32_t* side, int lgD, bool inv, cudaStream_t s, const EncodeSink* enc = nullptr) {
+// skip_a (inverse, 2^32-bit blocks): conv(Dd)^-1 over the digit already ran (decode_conv_a_kernel).
+void conv_cols_split(uint32_t* w, uint32_t* side, int lgD, bool inv, cudaStream_t s, const EncodeSink* enc = nullptr,
+                     bool skip_a = false) {
   if (lgD <= 1) return;
   if (lgD <= 8) {
     slab(w, lgD, 1, kTWords / 8, inv, s);
@@ -1368,14 +1467,17 @@ void conv_cols_split(uint32_t* w, uint32_t* side, int lgD, bool inv, cudaStream_
     over_digit(false);
     conv256_units(w, Dd, 1, 1, false, s);
   } else {
+    // (conv over the digit and conv over the row within it commute: the digit one runs first so
+    // that it can be fused with the decode)
+    if (!skip_a) over_digit(true);
     conv256_units(w, Dd, 1, 1, true, s);
-    over_digit(true);
     l1d(false);
   }
 }
 
 void conv2d_split(uint32_t* w, int K, bool inv, uint32_t* scratch, uint32_t* side, cudaStream_t s,
-                  const uint32_t* src = nullptr, const uint32_t* top = nullptr, const EncodeSink* enc = nullptr) {
+                  const uint32_t* src = nullptr, const uint32_t* top = nullptr, const EncodeSink* enc = nullptr,
+                  bool skip_a = false) {
   const int lgD = K - kTLog2;
   const uint64_t D = (uint64_t)1 << lgD;
   const int nb_in = std::min(lgD, 8), nb_out = lgD - nb_in;
@@ -1396,7 +1498,7 @@ void conv2d_split(uint32_t* w, int K, bool inv, uint32_t* scratch, uint32_t* sid
     FPM_LAUNCH_CHECK();
     conv_cols_split(w, side, lgD, false, s, enc);
   } else {
-    conv_cols_split(w, side, lgD, true, s);
+    conv_cols_split(w, side, lgD, true, s, nullptr, skip_a);
     conv_rows(w, D * kTWords, kTLog2, true, s);
     zeta(w, kTWords, scratch, p1, D, 0, nb_in, lo_skew, p1 / kZW, s, kTWords);
     overflow_kernel<<<grid_cap(D, 8), 256, 0, s>>>(scratch, p1, w, D, nb_out ? nullptr : top, 255);
@@ -1454,15 +1556,35 @@ void top_bit_fix_device(uint32_t* hi_block, cudaStream_t s) {
   FPM_LAUNCH_CHECK();
 }
 
+bool basis_cvt_can_decode(size_t n_bits) {
+  return n_bits == ((size_t)1 << 33) && split_l1_enabled();
+}
+
+void decode_conv_a(const DecodeSource& dec, uint32_t* w_lo, uint32_t* w_hi, cudaStream_t s) {
+  static PerDeviceOnce attr;
+  attr.run([] {
+    FPM_CUDA(cudaFuncSetAttribute(decode_conv_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecSmem));
+  });
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  const DeviceTables& dt = device_tables(dev);
+  const uint64_t items = 256 * (kTWords / kCT);
+  decode_conv_a_kernel<<<grid_cap(items, 1), kCTThreads, kDecSmem, s>>>(dec.ev, dec.tower ? dt.dec_m8r : dt.dec_m8,
+                                                                          w_lo, w_hi, items);
+  FPM_LAUNCH_CHECK();
+}
+
 bool basis_cvt_can_encode(size_t n_bits, bool tower) {
   (void)tower;
   return n_bits == ((size_t)1 << 32) && split_l1_enabled() && tma_units_enabled();
 }
 
 void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s,
-                      const FinalFn* on_final, const uint32_t* src, const EncodeSink* enc) {
+                      const FinalFn* on_final, const uint32_t* src, const EncodeSink* enc, const DecodeSource* dec) {
   if (enc && (inverse || !basis_cvt_can_encode(n_bits, enc->tower)))
     throw Error(kInvalid, "basis_cvt: the fused encode needs a forward 2^32-bit conversion");
+  if (dec && (!inverse || !basis_cvt_can_decode(n_bits)))
+    throw Error(kInvalid, "basis_cvt: the fused decode needs an inverse 2^33-bit conversion");
   if (n_bits < 4 || (n_bits & (n_bits - 1))) throw Error(kInvalid, "basis_cvt: length must be a power of two >= 4");
   set_smem_attr();
   int K = 0;
@@ -1499,10 +1621,13 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
   uint32_t* scratch = static_cast<uint32_t*>(scr.p);
   uint32_t* side = static_cast<uint32_t*>(side_buf.p);
   auto conv_block = [&](uint32_t* blk, const uint32_t* from, const uint32_t* tp) {
-    if (split) conv2d_split(blk, Kb, inverse, scratch, side, s, from, tp, enc);
+    if (split) conv2d_split(blk, Kb, inverse, scratch, side, s, from, tp, enc, dec != nullptr);
     else conv2d(blk, Kb, inverse, scratch, s, from, tp);
   };
   const uint64_t block_words = ((uint64_t)1 << Kb) / 32;
+  // fused decode (2^33-bit inverse): decode + conv^-1 over the digit of both blocks in one pass; each
+  // block's conversion then skips that step
+  if (dec) decode_conv_a(*dec, w, w + block_words, s);
   // Arrays above 2^32 bits: their passes with S > 2^32 come first (forward) / last (inverse);
   // what remains is conv(2^32) of every 2^32-bit block (build_schedule's per-digit recursion).
   std::vector<Pass> top;
