@@ -186,6 +186,24 @@ fpm_status fpm_bfly_pair_peer_dev(const uint64_t* d_mine, const uint64_t* d_thei
 /* Peer-shareable device buffers: cudaMalloc + cudaIpcGetMemHandle (64-byte handle) / open a peer's
  * handle in this process (cudaIpcMemLazyEnablePeerAccess) / close / free. */
 #define FPM_IPC_HANDLE_BYTES 64
+/* The sharded product's conversions split over ranks instead of replicated (the
+ * blocks of basis_convert.cpp's schedule, :60-67, that are independent):
+ *  - fpm_load_operand_dev: dst[0 .. dst_words) <- the src_bits-bit operand, zero-padded (the padded
+ *    copy run_pipeline converts, polymul.cpp:86-104);
+ *  - fpm_decode_cols_split_dev: ncols elements (a rank's columns [col0, col0 + ncols)) decoded
+ *    straight into the product matrix of row pitch row_bits -- rows 0..63 to d_lo, 64..127 to d_hi
+ *    (either may be a peer GPU's memory): the all-gather of the columns disappears;
+ *  - a 2^33-bit product's inverse conversion as its two independent 2^32-bit blocks: the upper block
+ *    by fpm_i_basis_cvt_dev(d_hi, 2^32), then fpm_i_basis_cvt_block32_dev(d_lo, d_hi) (the array's
+ *    top pass fused in, reading the final upper block), then fpm_top_bit_fix_dev(d_hi);
+ *  - fpm_copy_dev: cudaMemcpyAsync(cudaMemcpyDefault) (peer / device copies for non-torch callers). */
+fpm_status fpm_load_operand_dev(uint64_t* d_dst, size_t dst_words, const uint64_t* d_src, size_t src_bits, void* stream);
+fpm_status fpm_decode_cols_split_dev(const uint64_t* d_ev, size_t ncols, size_t col0, size_t row_bits, uint64_t* d_lo,
+                                     uint64_t* d_hi, int tower, void* stream);
+fpm_status fpm_i_basis_cvt_block32_dev(uint64_t* d_lo, const uint64_t* d_top, void* stream);
+fpm_status fpm_top_bit_fix_dev(uint64_t* d_hi, void* stream);
+fpm_status fpm_copy_dev(void* d_dst, const void* d_src, size_t bytes, void* stream);
+
 fpm_status fpm_ipc_alloc(size_t bytes, void** d_ptr, uint8_t* handle);
 fpm_status fpm_ipc_open(const uint8_t* handle, void** d_peer);
 fpm_status fpm_ipc_close(void* d_peer);

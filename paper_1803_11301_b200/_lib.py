@@ -94,6 +94,11 @@ def lib():
         L.fpm_bfly_pair_r_dev.argtypes = [vp, vp, sz, _u64p, C.c_int, C.c_int, vp]
         L.fpm_shard_local_product_dev.argtypes = [vp, vp, C.c_uint, _u64p, vp]
         L.fpm_bfly_pair_peer_dev.argtypes = [vp, vp, vp, sz, _u64p, C.c_int, C.c_int, C.c_int, vp]
+        L.fpm_load_operand_dev.argtypes = [vp, sz, vp, sz, vp]
+        L.fpm_decode_cols_split_dev.argtypes = [vp, sz, sz, sz, vp, vp, C.c_int, vp]
+        L.fpm_i_basis_cvt_block32_dev.argtypes = [vp, vp, vp]
+        L.fpm_top_bit_fix_dev.argtypes = [vp, vp]
+        L.fpm_copy_dev.argtypes = [vp, vp, sz, vp]
         L.fpm_ipc_alloc.argtypes = [sz, C.POINTER(vp), C.POINTER(C.c_uint8)]
         L.fpm_ipc_open.argtypes = [C.POINTER(C.c_uint8), C.POINTER(vp)]
         L.fpm_ipc_close.argtypes = [vp]

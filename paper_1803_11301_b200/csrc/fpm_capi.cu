@@ -1026,6 +1026,49 @@ fpm_status fpm_shard_local_product_dev(uint64_t* d_ea, uint64_t* d_eb, unsigned 
   });
 }
 
+fpm_status fpm_decode_cols_split_dev(const uint64_t* d_ev, size_t ncols, size_t col0, size_t row_bits, uint64_t* d_lo,
+                                     uint64_t* d_hi, int tower, void* stream) {
+  return guard([&] {
+    require_device();
+    if (!d_ev || !d_lo || !d_hi) throw Error(kInvalid, "decode_cols_split: null pointer");
+    decode_cols_split_device(reinterpret_cast<const uint4*>(d_ev), ncols, col0, row_bits, reinterpret_cast<uint32_t*>(d_lo),
+                             reinterpret_cast<uint32_t*>(d_hi), (cudaStream_t)stream, tower != 0);
+  });
+}
+
+fpm_status fpm_i_basis_cvt_block32_dev(uint64_t* d_lo, const uint64_t* d_top, void* stream) {
+  return guard([&] {
+    require_device();
+    if (!d_lo) throw Error(kInvalid, "i_basis_cvt_block32: null block");
+    basis_cvt_block32_inverse(reinterpret_cast<uint32_t*>(d_lo), reinterpret_cast<const uint32_t*>(d_top),
+                              (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_top_bit_fix_dev(uint64_t* d_hi, void* stream) {
+  return guard([&] {
+    require_device();
+    if (!d_hi) throw Error(kInvalid, "top_bit_fix: null block");
+    top_bit_fix_device(reinterpret_cast<uint32_t*>(d_hi), (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_load_operand_dev(uint64_t* d_dst, size_t dst_words, const uint64_t* d_src, size_t src_bits, void* stream) {
+  return guard([&] {
+    require_device();
+    if (!dst_words) return;
+    load_operand_kernel<<<grid_1d(dst_words), 256, 0, (cudaStream_t)stream>>>(d_dst, dst_words, d_src, src_bits);
+    FPM_LAUNCH_CHECK();
+  });
+}
+
+fpm_status fpm_copy_dev(void* d_dst, const void* d_src, size_t bytes, void* stream) {
+  return guard([&] {
+    require_device();
+    if (bytes) FPM_CUDA(cudaMemcpyAsync(d_dst, d_src, bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+  });
+}
+
 fpm_status fpm_bfly_pair_dev(uint64_t* d_mine, const uint64_t* d_theirs, size_t n, const uint64_t* w, int side,
                              int inverse, void* stream) {
   return guard([&] {

@@ -2,7 +2,9 @@
 
 SURVEY.md 8(e): rank g of P owns elements [g*m, (g+1)*m), m = n_p / P, of every EvalVec.
 
-* basis conversion of the operands: replicated (every rank holds both inputs);
+* basis conversion of the operands: with PeerBackend (P >= 2) operand a converts on rank 0 and b on
+  rank 1 and every rank encodes its columns straight from the converting rank's memory (CUDA IPC);
+  other backends replicate it (every rank holds both inputs);
 * encode: element-local -- rank g encodes columns [g*m, (g+1)*m) of the partition matrix;
 * forward FFT: layers i >= l' = l - log2 P pair element e with e ^ 2^i, which lives on rank
   g ^ 2^(i - l'): ONE exchange of the rank's whole slice with that partner per layer, then a local
@@ -11,7 +13,11 @@ SURVEY.md 8(e): rank g of P owns elements [g*m, (g+1)*m), m = n_p / P, of every 
   C2P((base >> i) ^ 2b) with b = (g*m >> (i+1)) + b_local equals C2P(((base ^ g*m) >> i) ^ 2 b_local);
 * pointwise: local; inverse FFT mirrors the forward (local layers, then exchanged top layers);
 * decode: local columns -> a 128 x m-bit slice; all_gather + column interleave -> the n-bit
-  product array; inverse basis conversion (replicated); trim.
+  product array; inverse basis conversion (replicated); trim.  PeerBackend instead decodes every
+  rank's columns straight into the product array on rank 0 (or, for a 2^33-bit product, the two
+  independent 2^32-bit blocks on ranks 0 and 1, converted there, the lower block's top pass reading
+  the upper one over peer memory) -- the single-process fpm_polymul_multi's decomposition, over the
+  same C-ABI calls.
 
 Cosets of 2^18 or more elements take the single-GPU fast path (backend.tower(l') true): operands
 encoded straight into the tower representation, exchanged layers on tower tables, and the local
@@ -127,9 +133,13 @@ def polymul_sharded(a, a_bits: int, b, b_bits: int, backend, plan: ShardPlan | N
         backend.pair(ev, theirs, w, plan.side(i), inverse=inverse, **kw)
         return ev
 
+    # backends with split conversions (PeerBackend, P >= 2): operand a converts on rank 0, b on rank 1,
+    # every rank encodes its columns from the converting rank's memory; otherwise replicated
+    split = P >= 2 and hasattr(backend, "convert_operands_split")
+    polys = backend.convert_operands_split(a, a_bits, b, b_bits, plan) if split else None
     evs = []
-    for x, bits in ((a, a_bits), (b, b_bits)):
-        poly = backend.convert_operand(x, bits, plan.n_bits)          # basis_cvt, replicated
+    for k, (x, bits) in enumerate(((a, a_bits), (b, b_bits))):
+        poly = polys[k] if split else backend.convert_operand(x, bits, plan.n_bits)
         ev = backend.encode_cols(poly, plan.l, plan.col0, plan.m, **kw)  # local columns
         for i in plan.top_layers(inverse=False):                       # exchanged layers
             ev = exchanged(ev, i, False)
@@ -143,6 +153,8 @@ def polymul_sharded(a, a_bits: int, b, b_bits: int, backend, plan: ShardPlan | N
         backend.butterfly(c, plan.lp, plan.base ^ plan.col0, inverse=True)
     for i in plan.top_layers(inverse=True):
         c = exchanged(c, i, True)
+    if split:  # decode into the converting ranks' arrays, inverse conversion split by block
+        return backend.finish_split(c, plan, a_bits + b_bits - 1, tower=r)
     slice_ = backend.decode_cols(c, plan.m, **kw)                       # 128 rows x m bits
     full = backend.gather_columns(slice_, plan)                         # 128 rows x n_p bits
     return backend.finish(full, plan.n_bits, a_bits + b_bits - 1)       # i_basis_cvt + trim
@@ -313,10 +325,89 @@ class PeerBackend(GpuBackend):
         for ptrs in self.peer.values():
             for p in ptrs:
                 self._close(p)
+        for p in getattr(self, "opened", []):
+            self._close(p)
         self._barrier()  # every partner closed its mapping of our buffers
         for b in self.mine:
             self._free(b.ptr)
-        self.mine, self.peer, self.key = [], {}, None
+        for p in getattr(self, "owned", []):
+            self._free(p)
+        self.mine, self.peer, self.key, self.opened, self.owned, self.arrays = [], {}, None, [], [], {}
+
+    # -- split conversions (P >= 2)
+    @staticmethod
+    def _shared_sizes(plan, P, rank):
+        if P < 2:
+            return {}
+        n = plan.n_bits
+        out = {}
+        if rank == 0:
+            out["x0"] = n // 16
+            out["y0"] = n // 16 if n == 1 << 33 else n // 8
+        if rank == 1:
+            out["x1"] = n // 16
+            if n == 1 << 33:
+                out["y1"] = n // 16
+        return out
+
+    def convert_operands_split(self, a, a_bits, b, b_bits, plan):
+        """Rank 0 converts operand a, rank 1 operand b (each into its own shared array); every rank
+        then reads both converted operands (peer memory) for its encode."""
+        P, rank = self.world()
+        s = self._s()
+        L = self.L.lib()
+        half_words = plan.n_bits // 128
+        for k, (x, bits) in enumerate(((a, a_bits), (b, b_bits))):
+            if rank == k:
+                dst = self.arrays[f"x{k}"]
+                self.L._check(L.fpm_load_operand_dev(dst, half_words, x.data_ptr(), bits, s))
+                count = 32
+                while count < bits:
+                    count <<= 1
+                self.L._check(L.fpm_basis_cvt_dev(dst, count, bits, s))
+        self._barrier()  # both converted operands final before any rank encodes from them
+        dev = self.torch.device("cuda", self.torch.cuda.current_device())
+        return [DevBuf(self.arrays["x0"], half_words, dev), DevBuf(self.arrays["x1"], half_words, dev)]
+
+    def finish_split(self, c, plan, out_bits, tower=False):
+        """Every rank decodes its columns straight into the product array(s); the inverse conversion
+        runs on rank 0 (n <= 2^32 bits) or as the two 2^32-bit blocks on ranks 1 and 0 (2^33 bits:
+        the lower block's top pass reads rank 1's final block); every rank then copies the product."""
+        P, rank = self.world()
+        s = self._s()
+        L = self.L.lib()
+        n, n_p = plan.n_bits, plan.n_p
+        blocks = n == 1 << 33
+        lo = self.arrays["y0"]
+        hi = self.arrays["y1"] if blocks else lo + 64 * (n_p // 8)  # rows 64.. of the n-bit array (bytes)
+        self.L._check(L.fpm_decode_cols_split_dev(c.data_ptr(), plan.m, plan.col0, n_p, lo, hi, int(tower), s))
+        self._barrier()  # every rank's columns are in place
+        if blocks:
+            if rank == 1:
+                self.L._check(L.fpm_i_basis_cvt_dev(hi, 1 << 32, s))
+            self._barrier()
+            if rank == 0:
+                self.L._check(L.fpm_i_basis_cvt_block32_dev(lo, hi, s))
+            self._barrier()  # rank 0 read rank 1's (pre-fix) bit 0
+            if rank == 1:
+                self.L._check(L.fpm_top_bit_fix_dev(hi, s))
+        elif rank == 0:
+            self.L._check(L.fpm_i_basis_cvt_dev(lo, n, s))
+        self._barrier()  # the product is final
+        t = self.torch
+        w = (out_bits + 63) // 64
+        out = t.empty(w, dtype=t.int64, device=c.device)
+        if blocks:
+            bw = (1 << 32) // 64
+            self.L._check(L.fpm_copy_dev(out.data_ptr(), lo, min(w, bw) * 8, s))
+            if w > bw:
+                self.L._check(L.fpm_copy_dev(out.data_ptr() + bw * 8, hi, (w - bw) * 8, s))
+        else:
+            self.L._check(L.fpm_copy_dev(out.data_ptr(), lo, w * 8, s))
+        if out_bits % 64:
+            out[w - 1] &= (1 << (out_bits % 64)) - 1
+        self._barrier()  # every rank copied out before the arrays are reused
+        return out
 
     # -- hooks (the single-GPU thread test overrides these)
     def _alloc(self, nbytes: int):
@@ -344,28 +435,42 @@ class PeerBackend(GpuBackend):
         self.torch.cuda.current_stream().synchronize()
         self.dist.barrier(group=self.group)
 
-    # -- plan setup: 2 operands x ping/pong of m elements, partners' buffers opened once
+    # -- plan setup: 2 operands x ping/pong of m elements, partners' buffers opened once; with P >= 2
+    # also the split conversions' arrays: converted operand a on rank 0, b on rank 1 (n/2 bits each),
+    # the product array on rank 0 (n bits) -- or, for a 2^33-bit product, its two 2^32-bit blocks on
+    # ranks 0 and 1 -- opened on every rank
     def begin(self, plan):
         P, rank = self.world()
-        key = (plan.m, P, rank)
+        key = (plan.m, plan.n_bits, P, rank)
         if self.key != key:
             self.close()  # re-key: release the previous plan's buffers and peer mappings
             nbytes = plan.m * 16
             mine = [self._alloc(nbytes) for _ in range(4)]
-            allh = self._publish([h for _, h in mine])
+            shared = self._shared_sizes(plan, P, rank)  # name -> bytes of the arrays this rank owns
+            own = {k: self._alloc(v) for k, v in shared.items()}
+            allh = self._publish(([h for _, h in mine], {k: h for k, (_, h) in own.items()}))
             dev = self.torch.device("cuda", self.torch.cuda.current_device())
             self.mine = [DevBuf(p, 2 * plan.m, dev) for p, _ in mine]
             self.peer = {}
             for i in range(plan.lp, plan.l):
                 g = plan.partner(i)
                 if g not in self.peer:
-                    self.peer[g] = [self._open(h) for h in allh[g]]
+                    self.peer[g] = [self._open(h) for h in allh[g][0]]
+            # split-conversion arrays: own pointer or an opened peer mapping (self.opened: to close)
+            self.arrays, self.opened, self.owned = {}, [], [p for p, _ in own.values()]
+            for g in range(P):
+                for name, h in allh[g][1].items():
+                    if g == rank:
+                        self.arrays[name] = own[name][0]
+                    else:
+                        self.arrays[name] = self._open(h)
+                        self.opened.append(self.arrays[name])
             self.key = key
         self.n_enc = 0
         self.cur = [0, 0]
 
     def encode_cols(self, poly, l: int, col0: int, ncols: int, tower: bool = False):
-        k = self.n_enc
+        k = self.n_enc  # (poly: a tensor, or a DevBuf over a peer rank's converted operand)
         self.n_enc += 1
         ev = self.mine[2 * k]
         f = self.L.lib().fpm_encode_cols_r_dev if tower else self.L.lib().fpm_encode_cols_dev

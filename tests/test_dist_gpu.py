@@ -253,3 +253,45 @@ def test_polymul_multi_rejects_bad_rank_counts(gpu):
         gpu.fp_polymul_multi(a, 1 << 20, a, 1 << 20, [0, 0, 0])
     with pytest.raises(ValueError):  # 2^7 elements per rank
         gpu.fp_polymul_multi(a, 1 << 12, a, 1 << 12, [0] * 64, field=gpu.FIELD_GF128)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_sharded_peer_config5_split_conversions(gpu, P):
+    """BASELINE config 5 through dist.polymul_sharded with PeerBackend and thread ranks: the split
+    conversions (operand a on rank 0, b on rank 1, encode from peer memory), the decode straight into
+    the two 2^32-bit blocks on ranks 0 and 1 and their separate inverse conversions with the fused
+    top pass; the product hash against the reference's."""
+    import hashlib
+    import json
+    import os
+    from paper_1803_11301_b200.dist import make_plan, polymul_sharded
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_meta.json")) as f:
+        c = json.load(f)["configs"]["4294967296x4294967296"]
+    a = gpu.random_bitpoly(c["a_bits"], c["seed_a"])
+    b = gpu.random_bitpoly(c["b_bits"], c["seed_b"])
+    shared = _Shared(P)
+    out, errs, keep = {}, [], []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            da = torch.from_numpy(a.view(np.int64)).cuda()
+            db = torch.from_numpy(b.view(np.int64)).cuda()
+            be = _make_peer_backend(shared, rank, keep)
+            res = polymul_sharded(da, c["a_bits"], db, c["b_bits"], be, make_plan(c["a_bits"], c["b_bits"], P, rank))
+            torch.cuda.synchronize()
+            if rank == P - 1:
+                out[rank] = hashlib.blake2b(res.cpu().numpy().view(np.uint64).tobytes(), digest_size=16).hexdigest()
+            del res, da, db
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append((rank, repr(e)))
+            shared.barrier.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    keep.clear()
+    assert not errs, errs
+    assert out[P - 1] == c["blake2b128"]
