@@ -720,7 +720,8 @@ def main():
         "config": workload_config(args.config),
         "parallelism": {"single": "single GPU", "replicas": f"{ws} independent products (replicas)",
                         "shard": f"one product sharded over {ws} GPUs: top {ws.bit_length() - 1} butterfly "
-                                 f"layers exchanged ({exchange}), basis conversions replicated"}[mode],
+                                 f"layers exchanged ({exchange}), basis conversions "
+                                 + ("split over ranks 0/1 (peer memory)" if exchange == "peer" else "replicated")}[mode],
         "parity": parity,
         "e2e": {"value": round(e2e_ms / ws if mode == "replicas" else e2e_ms, 3), "unit": "ms", "steps": e2e_steps,
                 "h2d_bytes_per_step": 2 * words * 8, "d2h_bytes_per_step": out_words * 8,
