@@ -758,7 +758,7 @@ void top_passes(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSr
   });
   const uint64_t pairs = ((uint64_t)1 << l) / 2;
   uint64_t ppc = 4096;
-  while (ppc > 256 && pairs / ppc < (uint64_t)sms() * 2) ppc /= 2;
+  while (ppc > (l >= 16 ? 256u : 128u) && pairs / ppc < (uint64_t)sms() * 2) ppc /= 2;
   const uint64_t ctas = pairs / ppc;
   if (T < 8 || ctas == 0) throw Error(kInvalid, "butterfly_top: layer too small for the table layer kernel");
   auto radix2 = [&](unsigned i) {
@@ -769,9 +769,13 @@ void top_passes(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSr
   };
   // layer pairs (i+1, i) from the top down (forward) / bottom up (inverse); an odd count leaves
   // the lowest top layer T to the one-layer kernel.
+  // Quads per CTA: 8192 amortise the three 64 KiB table builds at 2^32 bits; small transforms go
+  // down to 128 quads so that the pass spreads over the SMs (at l = 14 a 1024-quad floor left 4 CTAs
+  // per pass, ~10 us each, dominated by one CTA's table builds).
   const uint64_t quads = ((uint64_t)1 << l) / 4;
+  const uint64_t qmin = l >= 16 ? 1024 : 128;  // l = 18: 1024 beats 128 (0.104 vs 0.154 ms of passes)
   uint64_t qpc = 8192;
-  while (qpc > 1024 && quads / qpc < (uint64_t)sms() * 4) qpc /= 2;
+  while (qpc > qmin && quads / qpc < (uint64_t)sms() * 4) qpc /= 2;
   auto radix4 = [&](unsigned i) {
     const unsigned q = (unsigned)std::min<uint64_t>(qpc, (uint64_t)1 << i);
     // forward: 512 threads (pre-rotated lookups without spills; 11.04 vs 11.22 ms at 2^32 bits);
