@@ -22,6 +22,10 @@
 namespace fpm {
 
 constexpr int kTileRows = 256;
+#ifndef FPM_UNIT_CONV_TILE
+#define FPM_UNIT_CONV_TILE 0  // measured: forward 2.29 -> 2.23 ms, inverse 1.56 -> 1.92 ms (off)
+#endif
+constexpr bool kUnitConvTile = FPM_UNIT_CONV_TILE;
 constexpr int kScPitch = 17;  // scratch row pitch (words) for 512-bit widened rows
 
 // 16-word registers shifted by whole words (ws < 16), left (towards higher words) or right, by
@@ -165,6 +169,141 @@ __device__ __forceinline__ void rowpasses_w(uint32_t (&m)[W][8], uint32_t* tile,
   }
 }
 
+// conv16 over 16 register values (build_schedule(16): (16,6), (8,3), (16,4), (4,1)); increasing q
+// reads every source before it is overwritten (sources sit above their targets).
+template <int S, int D, bool INV>
+__device__ __forceinline__ void conv_pass16(uint32_t (&x)[16]) {
+#pragma unroll
+  for (int base = 0; base < 16; base += S)
+#pragma unroll
+    for (int q = S / 2 - D; q < S - D; ++q) {
+      uint32_t v = x[base + q + D];
+      if (!INV && q + 2 * D < S) v ^= x[base + q + 2 * D];
+      x[base + q] ^= v;
+    }
+}
+template <bool INV>
+__device__ __forceinline__ void conv16_vals(uint32_t (&x)[16]) {
+  if (!INV) {
+    conv_pass16<16, 6, false>(x);
+    conv_pass16<8, 3, false>(x);
+    conv_pass16<16, 4, false>(x);
+    conv_pass16<4, 1, false>(x);
+  } else {
+    conv_pass16<4, 1, true>(x);
+    conv_pass16<16, 4, true>(x);
+    conv_pass16<8, 3, true>(x);
+    conv_pass16<16, 6, true>(x);
+  }
+}
+
+// zeta over the 4 digit bits (superset sums): x[d] ^= x[d | 2^b] for d without bit b.
+__device__ __forceinline__ void zeta16_vals(uint32_t (&x)[16]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int d = 0; d < 16; ++d)
+      if (!(d >> j & 1)) x[d] ^= x[d | (1 << j)];
+}
+
+// conv(256) over the tile's 256 sub-rows as units (C_cols at g = 8) WITHOUT transposing the tile:
+// the unit-level recursion conv(256) = C_rows(conv16 over v) o C_cols(conv16 over d) o L1(16, 16)
+// (units u = 16 d + v, unit skew), as conv256_units_kernel, on 16-bit half-columns: thread
+// (r = tid / 16, hc = tid % 16) holds half-word hc of 16 units per phase.  tile: >= 2048 words;
+// z: >= 4096 words (16 x 32 slots x 16 half-words).  All 256 threads call it.
+template <bool INV>
+__device__ __forceinline__ void unitconv256_tile(uint32_t (&m)[8], uint32_t* tile, uint32_t* z) {
+  const int tid = threadIdx.x, r = tid >> 4, hc = tid & 15;
+  uint16_t* t16 = reinterpret_cast<uint16_t*>(tile);  // [unit][16 half-words]
+  uint16_t* Z = reinterpret_cast<uint16_t*>(z);       // [d][32 slots][16]
+  auto zi = [&](int d, int s) { return (d * 32 + s) * 16 + hc; };
+  __syncthreads();
+  {
+    uint4* t4 = reinterpret_cast<uint4*>(tile + tid * 8);
+    t4[0] = make_uint4(m[0], m[1], m[2], m[3]);
+    t4[1] = make_uint4(m[4], m[5], m[6], m[7]);
+  }
+  __syncthreads();
+  uint32_t x[16];
+  if (!INV) {
+    uint32_t y[16];
+#pragma unroll
+    for (int d = 0; d < 16; ++d) {
+      const int v0 = r - d, v1 = r + 16 - d;
+      x[d] = v0 >= 0 ? t16[(16 * d + v0) * 16 + hc] : 0u;
+      y[d] = v1 < 16 ? t16[(16 * d + v1) * 16 + hc] : 0u;
+    }
+    zeta16_vals(x);
+    zeta16_vals(y);
+#pragma unroll
+    for (int d = 0; d < 16; ++d) {
+      Z[zi(d, r)] = (uint16_t)x[d];
+      Z[zi(d, r + 16)] = (uint16_t)y[d];
+    }
+    __syncthreads();
+    const int v = r;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      uint32_t g = Z[zi(k, v + k)];
+      if (v >= 1 && 15 + v + k < 31) g ^= Z[zi(k, 15 + v + k)];
+      if (k >= 1 && 15 + v + k < 31) g ^= Z[zi(k - 1, 15 + v + k)];
+      x[k] = g;
+    }
+    conv16_vals<false>(x);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) Z[zi(k, v)] = (uint16_t)x[k];
+    __syncthreads();
+#pragma unroll
+    for (int vv = 0; vv < 16; ++vv) x[vv] = Z[zi(r, vv)];
+    conv16_vals<false>(x);
+#pragma unroll
+    for (int vv = 0; vv < 16; ++vv) t16[(16 * r + vv) * 16 + hc] = (uint16_t)x[vv];
+  } else {
+#pragma unroll
+    for (int vv = 0; vv < 16; ++vv) x[vv] = t16[(16 * r + vv) * 16 + hc];
+    conv16_vals<true>(x);
+#pragma unroll
+    for (int vv = 0; vv < 16; ++vv) Z[zi(r, vv)] = (uint16_t)x[vv];
+    __syncthreads();
+    const int v = r;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = Z[zi(k, v)];
+    conv16_vals<true>(x);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) Z[zi(k, v + k)] = (uint16_t)x[k];
+    __syncthreads();
+    uint32_t y[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      x[k] = (r >= k) ? Z[zi(k, r)] : 0u;
+      y[k] = (r < k) ? Z[zi(k, r + 16)] : 0u;
+    }
+    zeta16_vals(x);
+    zeta16_vals(y);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      Z[zi(k, r)] = (uint16_t)x[k];
+      Z[zi(k, r + 16)] = (uint16_t)y[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int vv = 0; vv < 16; ++vv) {
+      uint32_t f = Z[zi(r, vv + r)];
+      if (r >= 1 && 15 + vv + r < 31) f ^= Z[zi(r - 1, 15 + vv + r)];
+      t16[(16 * r + vv) * 16 + hc] = (uint16_t)f;
+    }
+  }
+  __syncthreads();
+  {
+    const uint4* t4 = reinterpret_cast<const uint4*>(tile + tid * 8);
+    const uint4 a = t4[0], b = t4[1];
+    m[0] = a.x; m[1] = a.y; m[2] = a.z; m[3] = a.w; m[4] = b.x; m[5] = b.y; m[6] = b.z; m[7] = b.w;
+  }
+}
+
 // 256 x 256-bit tile transpose (an involution): thread t's row t <-> thread c's column c (word w
 // of a column = rows 32w .. 32w+31).  Each warp transposes its eight 32 x 32 blocks in registers
 // (Transpose32), then the blocks change warps through shared memory (pitch 9: conflict-free).
@@ -203,13 +342,17 @@ __device__ __forceinline__ void conv_tile(uint32_t (&m)[8], uint32_t* tile, uint
     return;
   }
   const int g = r - 8, d = threadIdx.x & ((1 << g) - 1);
+  // full 2^16-bit rows: the sub-row conversion on 16-bit half-columns (no transposes)
+  const bool units = g == 8 && kUnitConvTile;
   if (!INV) {
     l1_tile<false>(m, sc, g, d);
-    colconv_tile<false>(m, tile, g);
+    if (units) unitconv256_tile<false>(m, tile, sc);
+    else colconv_tile<false>(m, tile, g);
     conv_regs<false>(8, m);
   } else {
     conv_regs<true>(8, m);
-    colconv_tile<true>(m, tile, g);
+    if (units) unitconv256_tile<true>(m, tile, sc);
+    else colconv_tile<true>(m, tile, g);
     l1_tile<true>(m, sc, g, d);
   }
 }

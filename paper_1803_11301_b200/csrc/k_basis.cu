@@ -439,43 +439,6 @@ constexpr int kC256Threads = 16 * kC256Cols;
 // that differ in d (512 words apart unpadded) land in different banks.
 constexpr size_t kC256Smem = 16 * 33 * kC256Cols * sizeof(uint32_t);
 
-// conv16 over 16 register values (build_schedule(16): (16,6), (8,3), (16,4), (4,1)); increasing q
-// reads every source before it is overwritten (sources sit above their targets).
-template <int S, int D, bool INV>
-__device__ __forceinline__ void conv_pass16(uint32_t (&x)[16]) {
-#pragma unroll
-  for (int base = 0; base < 16; base += S)
-#pragma unroll
-    for (int q = S / 2 - D; q < S - D; ++q) {
-      uint32_t v = x[base + q + D];
-      if (!INV && q + 2 * D < S) v ^= x[base + q + 2 * D];
-      x[base + q] ^= v;
-    }
-}
-template <bool INV>
-__device__ __forceinline__ void conv16_vals(uint32_t (&x)[16]) {
-  if (!INV) {
-    conv_pass16<16, 6, false>(x);
-    conv_pass16<8, 3, false>(x);
-    conv_pass16<16, 4, false>(x);
-    conv_pass16<4, 1, false>(x);
-  } else {
-    conv_pass16<4, 1, true>(x);
-    conv_pass16<16, 4, true>(x);
-    conv_pass16<8, 3, true>(x);
-    conv_pass16<16, 6, true>(x);
-  }
-}
-
-// zeta over the 4 digit bits (superset sums): x[d] ^= x[d | 2^b] for d without bit b.
-__device__ __forceinline__ void zeta16_vals(uint32_t (&x)[16]) {
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int d = 0; d < 16; ++d)
-      if (!(d >> j & 1)) x[d] ^= x[d | (1 << j)];
-}
-
 // Units of CTA slab `blk`: unit u of group `grp` is row grp_base + u * ustride (rows of kTWords
 // words); the CTA takes word columns [c0, c0 + 32).
 struct UnitMap {
