@@ -168,7 +168,7 @@ struct HostIO {
 // Field plumbing of run_pipeline<F> (polymul.cpp:78-135) for the two fields built on the GPU.
 struct Gf128Ops {
   using E = uint4;
-  static constexpr bool kFusedEncode = true;  // basis_cvt's last step can write the encode
+  static constexpr int kM = 128;
   using Tw = TwiddleSrc;
   static constexpr int kLiveRows = 64;  // rows >= m/2 of a padded operand are zero
   static Tw twiddles(int dev, unsigned l) { return make_twiddle_src(dev, l, partition_base(l)); }
@@ -198,7 +198,7 @@ struct Gf128Ops {
 };
 struct Gf64Ops {
   using E = uint2;
-  static constexpr bool kFusedEncode = false;
+  static constexpr int kM = 64;
   using Tw = TwiddleSrc64;
   static constexpr int kLiveRows = 32;
   static Tw twiddles(int dev, unsigned l) { return make_twiddle_src64(dev, l, partition_base64(l)); }
@@ -278,8 +278,8 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     size_t count = (size_t)1 << log2_ceil(xbits[k]);
     if (count < 32) count = 32;
     // a 2^32-bit conversion's last step also encodes (GF(2^128): the converted bits never reach HBM)
-    EncodeSink sink{reinterpret_cast<uint4*>(es[k]), rep};
-    const bool fused = F::kFusedEncode && count == n / 2 && basis_cvt_can_encode(count, rep);
+    EncodeSink sink{es[k], rep, F::kM};
+    const bool fused = count == n / 2 && basis_cvt_can_encode(count, rep);
     if (xbits[k] == n / 2 && count == n / 2 && count >= ((size_t)1 << 17) && count <= ((size_t)1 << 32)) {
       // the operand fills the conversion exactly: convert straight from the caller's buffer
       basis_cvt_device(work32, count, xbits[k], false, s, nullptr, reinterpret_cast<const uint32_t*>(xs[k]),
@@ -302,8 +302,8 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
   F::top(EB.as<E>(), l, T, true, tw, s, rep);
   clk.mark(kStDecode);
   // a 2^33-bit product's decode runs inside the inverse conversion's first step (GF(2^128))
-  const bool fused_dec = F::kFusedEncode && basis_cvt_can_decode(n);
-  DecodeSource dsrc{reinterpret_cast<const uint4*>(EB.template as<E>()), rep};
+  const bool fused_dec = basis_cvt_can_decode(n);
+  DecodeSource dsrc{EB.p, rep, F::kM};
   if (!fused_dec) F::decode(EB.as<E>(), l, work32, s, rep);
   clk.mark(kStIBasis);
   // Each finished range of the product is trimmed into d_c (and copied out) right away.

@@ -176,16 +176,18 @@ using FinalFn = std::function<void(uint64_t w0, uint64_t w1)>;
 // the GF(2^128) encode of the converted operand (64 live partition rows, l = 26) to enc->ev instead
 // of the converted bits (w is then scratch on exit).
 struct EncodeSink {
-  uint4* ev;
+  void* ev;    // 2^26 uint4 (m = 128) or 2^27 uint2 (m = 64) elements
   bool tower;  // elements in the tower representation R (the product pipeline's FFT)
+  int m = 128; // field degree
 };
 bool basis_cvt_can_encode(size_t n_bits, bool tower);
 // dec (inverse 2^33-bit conversions only, basis_cvt_can_decode): the GF(2^128) decode of dec->ev
 // (2^26 elements) is the conversion's input -- fused into its first step; w's contents on entry are
 // ignored.
 struct DecodeSource {
-  const uint4* ev;
+  const void* ev;
   bool tower;
+  int m = 128;
 };
 bool basis_cvt_can_decode(size_t n_bits);
 void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s,

@@ -24,11 +24,13 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "basis_dev.cuh"
 #include "conv_tile.cuh"
 #include "gf128.cuh"
+#include "gf64.cuh"
 #include "warp_bits.cuh"
 #include "fpm_internal.h"
 
@@ -724,21 +726,29 @@ __global__ void __launch_bounds__(kCTThreads, kCTMinBlocks) conv256_units_tma_ke
 // words -- rows 4j + a of the item are exactly a 64 x 1024-bit encode slab.  The slab goes through
 // the warp transpose and the 8 byte-chunk lookups of encode_kernel<64>; the converted operand never
 // reaches HBM (its write and the separate encode sweep's read disappear).
-constexpr size_t kCTEncSmem = kCTSmem + (size_t)(kM8Uint4 / 2) * sizeof(uint4);
+// GF(2^64) (M = 64, l = 27): 32 live partition rows of 2^27 bits, so converted row A = 8 j + a
+// (a < 8, j < 32) and 4 byte-chunk G8 lookups per element (encode64_kernel<32>).  Rows of sub-slab
+// a are stored at (A % S) (256 / S) + A / S, S = the number of sub-slabs (4 or 8): consecutive j,
+// conflict-free transposes.
+constexpr size_t kCTEncSmem = kCTSmem + 32768;  // + the x*E table (M8 chunks 0..7 / G8 chunks 0..3)
+template <int M>
 __global__ void __launch_bounds__(kCTThreads, 1) conv256_a_encode_kernel(const uint32_t* data, UnitMap um,
                                                                          uint64_t nitems,
                                                                          const __grid_constant__ CUtensorMap tmap,
-                                                                         const uint4* __restrict__ tab_g,
-                                                                         uint4* __restrict__ ev) {
+                                                                         const void* __restrict__ tab_g,
+                                                                         void* __restrict__ ev_out) {
+  using E = std::conditional_t<M == 128, uint4, uint2>;
+  constexpr int S = M == 128 ? 4 : 8, RPS = 256 / S;  // sub-slabs, rows per sub-slab
+  E* ev = static_cast<E*>(ev_out);
   extern __shared__ __align__(128) uint32_t sm_ct[];
   auto stage = [&](int st) { return sm_ct + st * (256 * kCT); };
   uint32_t* Z = sm_ct + 2 * 256 * kCT;  // [d][33][kCT]; after the conv: the converted rows [A][33]
   uint64_t* bar = reinterpret_cast<uint64_t*>(Z + 16 * 33 * kCT);
-  uint4* tab = reinterpret_cast<uint4*>(sm_ct + (kCTSmem / 4));  // x*E byte-chunk table (chunks 0..7)
+  uint4* tab = reinterpret_cast<uint4*>(sm_ct + (kCTSmem / 4));  // x*E byte-chunk table, 32 KiB
   const int tid = threadIdx.x, c = tid % kCT, r = tid / kCT, lane = tid & 31, warp = tid >> 5;
   constexpr int kCols = kTWords / kCT;
   auto zi = [](int d, int s, int cc) { return (d * 33 + s) * kCT + cc; };
-  for (int i = tid; i < kM8Uint4 / 2; i += kCTThreads) tab[i] = tab_g[i];
+  for (int i = tid; i < 32768 / 16; i += kCTThreads) tab[i] = static_cast<const uint4*>(tab_g)[i];
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -803,28 +813,45 @@ __global__ void __launch_bounds__(kCTThreads, 1) conv256_a_encode_kernel(const u
     conv16_vals<false>(x);
     __syncthreads();  // every thread's conv input read from Z: Z now holds the converted rows
 #pragma unroll
-    for (int vv = 0; vv < 16; ++vv) {  // row A = 16 r + vv stored at (A % 4) * 64 + A / 4: the
-      const int A = 16 * r + vv;        // encode's slab rows A = 4 j + a are then consecutive
-      Z[((A & 3) * 64 + (A >> 2)) * 33 + c] = x[vv];
+    for (int vv = 0; vv < 16; ++vv) {  // row A = 16 r + vv stored at (A % S) RPS + A / S: the
+      const int A = 16 * r + vv;        // encode's slab rows A = S j + a are then consecutive
+      Z[((A % S) * RPS + A / S) * 33 + c] = x[vv];
     }
     __syncthreads();
-    // encode: (a, col) pairs, 8 per warp; slab row j of sub-slab a is converted row 4 j + a
+    // encode: (a, col) pairs, 256 / 16 warps each; slab row j of sub-slab a is converted row S j + a
     const uint64_t e0 = B * 65536 + cb * 1024;
+    constexpr int kPairsPerWarp = S * 32 / 16;
 #pragma unroll 1
-    for (int k = 0; k < 8; ++k) {
-      const int pair = warp * 8 + k, a = pair >> 5, col = pair & 31;
-      const uint32_t x0 = tr(Z[(a * 64 + lane) * 33 + col]);        // rows j = lane
-      const uint32_t x1 = tr(Z[(a * 64 + 32 + lane) * 33 + col]);   // rows j = 32 + lane
-      uint4 acc0 = make_uint4(0, 0, 0, 0), acc1 = make_uint4(0, 0, 0, 0);
+    for (int k = 0; k < kPairsPerWarp; ++k) {
+      const int pair = warp * kPairsPerWarp + k, a = pair >> 5, col = pair & 31;
+      const uint64_t ei = (uint64_t)a * (1u << 24) + e0 + 32 * col + lane;
+      const uint32_t x0 = tr(Z[(a * RPS + lane) * 33 + col]);  // rows j = lane
+      if constexpr (M == 128) {
+        const uint32_t x1 = tr(Z[(a * RPS + 32 + lane) * 33 + col]);  // rows j = 32 + lane
+        uint4 acc0 = make_uint4(0, 0, 0, 0), acc1 = make_uint4(0, 0, 0, 0);
 #pragma unroll
-      for (int kk = 0; kk < 8; kk += 2) {
-        const int k0 = (kk + q8) & 7, k1 = (kk + 1 + q8) & 7;
-        const uint32_t b0 = __byte_perm(k0 < 4 ? x0 : x1, 0, 0x4440u | (uint32_t)(k0 & 3));
-        const uint32_t b1 = __byte_perm(k1 < 4 ? x0 : x1, 0, 0x4440u | (uint32_t)(k1 & 3));
-        acc0 = x4v(acc0, tab[b0 * 8 + k0]);
-        acc1 = x4v(acc1, tab[b1 * 8 + k1]);
+        for (int kk = 0; kk < 8; kk += 2) {
+          const int k0 = (kk + q8) & 7, k1 = (kk + 1 + q8) & 7;
+          const uint32_t b0 = __byte_perm(k0 < 4 ? x0 : x1, 0, 0x4440u | (uint32_t)(k0 & 3));
+          const uint32_t b1 = __byte_perm(k1 < 4 ? x0 : x1, 0, 0x4440u | (uint32_t)(k1 & 3));
+          acc0 = x4v(acc0, tab[b0 * 8 + k0]);
+          acc1 = x4v(acc1, tab[b1 * 8 + k1]);
+        }
+        ev[ei] = x4v(acc0, acc1);
+      } else {  // G8 layout: entry (chunk c, value v, copy h) at v * 16 + 8 h + c (gf64.cuh)
+        const uint2* t2 = reinterpret_cast<const uint2*>(tab);
+        const int h8 = lane & 8;
+        uint2 acc0 = make_uint2(0, 0), acc1 = make_uint2(0, 0);
+#pragma unroll
+        for (int kk = 0; kk < 4; kk += 2) {
+          const int k0 = (kk + q8) & 3, k1 = (kk + 1 + q8) & 3;
+          const uint32_t b0 = __byte_perm(x0, 0, 0x4440u | (uint32_t)k0);
+          const uint32_t b1 = __byte_perm(x0, 0, 0x4440u | (uint32_t)k1);
+          acc0 = x2(acc0, t2[b0 * 16 + h8 + k0]);
+          acc1 = x2(acc1, t2[b1 * 16 + h8 + k1]);
+        }
+        ev[ei] = x2(acc0, acc1);
       }
-      ev[(uint64_t)a * (1u << 24) + e0 + 32 * col + lane] = x4v(acc0, acc1);
     }
     __syncthreads();  // Z reuse by the next item
   }
@@ -837,43 +864,57 @@ __global__ void __launch_bounds__(kCTThreads, 1) conv256_a_encode_kernel(const u
 // (j = partition row - 64 b) of the item; then conv(256)^-1 over A (the inverse register phases of
 // conv256_units_kernel) runs on each block's 256 rows and the results are stored.  The decoded
 // product array never reaches HBM.
+// GF(2^64) (M = 64): 64 partition rows of 2^27 bits, 32 per block; row A = 8 (j % 32) + a (a < 8);
+// 8 G8 lookups per element (decode64_kernel).
 constexpr size_t kDecRows = 256 * 33;  // one block's rows of an item, [A][33]
 constexpr size_t kDecSmem = (size_t)kM8Uint4 * sizeof(uint4) + (2 * kDecRows + 16 * 33 * kCT) * sizeof(uint32_t);
-__global__ void __launch_bounds__(kCTThreads, 1) decode_conv_a_kernel(const uint4* __restrict__ ev,
-                                                                      const uint4* __restrict__ tab_g,
+template <int M>
+__global__ void __launch_bounds__(kCTThreads, 1) decode_conv_a_kernel(const void* __restrict__ ev_in,
+                                                                      const void* __restrict__ tab_g,
                                                                       uint32_t* __restrict__ w_lo,
                                                                       uint32_t* __restrict__ w_hi, uint64_t nitems) {
+  using E = std::conditional_t<M == 128, uint4, uint2>;
+  constexpr int S = M == 128 ? 4 : 8, RPS = 256 / S;
+  constexpr int kTabUint4 = M == 128 ? kM8Uint4 : kG8Uint2 / 2;
+  const E* ev = static_cast<const E*>(ev_in);
   extern __shared__ __align__(16) uint4 sm_dc[];
-  uint4* tab = sm_dc;  // x*E^-1 byte-chunk tables (gf128.cuh m8 layout, 16 chunks)
+  uint4* tab = sm_dc;  // x*E^-1 byte-chunk tables (gf128.cuh m8 / gf64.cuh g8 layout)
   uint32_t* Rw = reinterpret_cast<uint32_t*>(sm_dc + kM8Uint4);  // [block][A][33]
   uint32_t* Z = Rw + 2 * kDecRows;                                // [d][33][kCT]
   const int tid = threadIdx.x, c = tid % kCT, r = tid / kCT, lane = tid & 31, warp = tid >> 5;
   constexpr int kCols = kTWords / kCT;
   auto zi = [](int d, int s, int cc) { return (d * 33 + s) * kCT + cc; };
-  for (int i = tid; i < kM8Uint4; i += kCTThreads) tab[i] = tab_g[i];
+  for (int i = tid; i < kTabUint4; i += kCTThreads) tab[i] = static_cast<const uint4*>(tab_g)[i];
   const int q8 = lane & 7;
   const Transpose32 tr(lane);
   __syncthreads();
+  constexpr int kPairsPerWarp = S * 32 / 16;
   for (uint64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
     const uint64_t B = it / kCols, cb = it % kCols;
     const uint64_t e0 = B * 65536 + cb * 1024;
-    // ---- decode: (a, col) pairs, 8 per warp; all eight elements' loads first
-    uint4 f[8];
+    // ---- decode: (a, col) pairs; all the warp's elements' loads first
+    E f[kPairsPerWarp];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int pair = warp * 8 + k, a = pair >> 5, col = pair & 31;
+    for (int k = 0; k < kPairsPerWarp; ++k) {
+      const int pair = warp * kPairsPerWarp + k, a = pair >> 5, col = pair & 31;
       f[k] = __ldg(ev + (uint64_t)a * (1u << 24) + e0 + 32 * col + lane);
     }
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int pair = warp * 8 + k, a = pair >> 5, col = pair & 31;
-      const uint4 y = m8_mul(tab, f[k], q8);
-      // word q of y: partition rows 32q + lane after the transpose; block q >> 1, row A = 4 j + a
-      const uint32_t yw[4] = {y.x, y.y, y.z, y.w};
+    for (int k = 0; k < kPairsPerWarp; ++k) {
+      const int pair = warp * kPairsPerWarp + k, a = pair >> 5, col = pair & 31;
+      if constexpr (M == 128) {
+        const uint4 y = m8_mul(tab, f[k], q8);
+        // word q of y: partition rows 32q + lane after the transpose; block q >> 1, row A = 4 j + a
+        const uint32_t yw[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int j = 32 * (q & 1) + lane;
-        Rw[(q >> 1) * kDecRows + (a * 64 + j) * 33 + col] = tr(yw[q]);  // row A = 4 j + a at (A%4)*64 + A/4
+        for (int q = 0; q < 4; ++q) {
+          const int j = 32 * (q & 1) + lane;
+          Rw[(q >> 1) * kDecRows + (a * RPS + j) * 33 + col] = tr(yw[q]);  // row A = S j + a
+        }
+      } else {
+        const uint2 y = g8_mul(reinterpret_cast<const uint2*>(tab), f[k], lane);
+        Rw[(a * RPS + lane) * 33 + col] = tr(y.x);             // rows 0..31: block 0
+        Rw[kDecRows + (a * RPS + lane) * 33 + col] = tr(y.y);  // rows 32..63: block 1
       }
     }
     __syncthreads();
@@ -887,7 +928,7 @@ __global__ void __launch_bounds__(kCTThreads, 1) decode_conv_a_kernel(const uint
 #pragma unroll
       for (int vv = 0; vv < 16; ++vv) {
         const int A = 16 * r + vv;
-        x[vv] = Rb[((A & 3) * 64 + (A >> 2)) * 33 + c];
+        x[vv] = Rb[((A % S) * RPS + A / S) * 33 + c];
       }
       conv16_vals<true>(x);
 #pragma unroll
@@ -1376,7 +1417,8 @@ uint64_t split_side_words(int lgD) {
 void conv256_a_encode(uint32_t* w, const EncodeSink& enc, cudaStream_t s) {
   static PerDeviceOnce attr;
   attr.run([] {
-    FPM_CUDA(cudaFuncSetAttribute(conv256_a_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCTEncSmem));
+    FPM_CUDA(cudaFuncSetAttribute(conv256_a_encode_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCTEncSmem));
+    FPM_CUDA(cudaFuncSetAttribute(conv256_a_encode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCTEncSmem));
   });
   int dev;
   FPM_CUDA(cudaGetDevice(&dev));
@@ -1384,8 +1426,13 @@ void conv256_a_encode(uint32_t* w, const EncodeSink& enc, cudaStream_t s) {
   UnitMap um{256, 256, 256};
   const uint64_t items = 256 * (kTWords / kCT);
   const CUtensorMap tm = unit_tensor_map(w, 65536, 256);
-  conv256_a_encode_kernel<<<grid_cap(items, 1), kCTThreads, kCTEncSmem, s>>>(w, um, items, tm,
-                                                                              enc.tower ? dt.enc_m8r : dt.enc_m8, enc.ev);
+  const int grid = grid_cap(items, 1);
+  if (enc.m == 64)
+    conv256_a_encode_kernel<64><<<grid, kCTThreads, kCTEncSmem, s>>>(w, um, items, tm, enc.tower ? dt.enc_g8r : dt.enc_g8,
+                                                                     enc.ev);
+  else
+    conv256_a_encode_kernel<128><<<grid, kCTThreads, kCTEncSmem, s>>>(w, um, items, tm, enc.tower ? dt.enc_m8r : dt.enc_m8,
+                                                                      enc.ev);
   FPM_LAUNCH_CHECK();
 }
 
@@ -1526,14 +1573,20 @@ bool basis_cvt_can_decode(size_t n_bits) {
 void decode_conv_a(const DecodeSource& dec, uint32_t* w_lo, uint32_t* w_hi, cudaStream_t s) {
   static PerDeviceOnce attr;
   attr.run([] {
-    FPM_CUDA(cudaFuncSetAttribute(decode_conv_a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecSmem));
+    FPM_CUDA(cudaFuncSetAttribute(decode_conv_a_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecSmem));
+    FPM_CUDA(cudaFuncSetAttribute(decode_conv_a_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecSmem));
   });
   int dev;
   FPM_CUDA(cudaGetDevice(&dev));
   const DeviceTables& dt = device_tables(dev);
   const uint64_t items = 256 * (kTWords / kCT);
-  decode_conv_a_kernel<<<grid_cap(items, 1), kCTThreads, kDecSmem, s>>>(dec.ev, dec.tower ? dt.dec_m8r : dt.dec_m8,
-                                                                          w_lo, w_hi, items);
+  const int grid = grid_cap(items, 1);
+  if (dec.m == 64)
+    decode_conv_a_kernel<64><<<grid, kCTThreads, kDecSmem, s>>>(dec.ev, dec.tower ? dt.dec_g8r : dt.dec_g8, w_lo, w_hi,
+                                                                items);
+  else
+    decode_conv_a_kernel<128><<<grid, kCTThreads, kDecSmem, s>>>(dec.ev, dec.tower ? dt.dec_m8r : dt.dec_m8, w_lo, w_hi,
+                                                                 items);
   FPM_LAUNCH_CHECK();
 }
 
