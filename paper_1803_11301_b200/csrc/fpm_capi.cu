@@ -65,6 +65,7 @@ inline uint4 to4(U128 v) { return make_uint4((uint32_t)v.lo, (uint32_t)(v.lo >> 
 // dst[0 .. dst_words) <- src bits [0, src_bits), zero above.
 __global__ void load_operand_kernel(uint64_t* __restrict__ dst, uint64_t dst_words, const uint64_t* __restrict__ src,
                                     uint64_t src_bits) {
+  pdl_wait();
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < dst_words; k += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t v = 0;
     if (k * 64 < src_bits) {
@@ -73,16 +74,19 @@ __global__ void load_operand_kernel(uint64_t* __restrict__ dst, uint64_t dst_wor
     }
     dst[k] = v;
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 __global__ void store_product_kernel(uint64_t* __restrict__ dst, const uint64_t* __restrict__ src, uint64_t out_bits,
                                      uint64_t k0, uint64_t k1) {
+  pdl_wait();
   const uint64_t words = (out_bits + 63) / 64;
   for (uint64_t k = k0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < k1; k += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t v = src[k];
     if (k == words - 1 && (out_bits & 63)) v &= (((uint64_t)1) << (out_bits & 63)) - 1;
     dst[k] = v;
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 int grid_1d(uint64_t n, int per_sm = 16) {
@@ -285,7 +289,7 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
       basis_cvt_device(work32, count, xbits[k], false, s, nullptr, reinterpret_cast<const uint32_t*>(xs[k]),
                        fused ? &sink : nullptr);
     } else {
-      load_operand_kernel<<<grid_1d(half_words), 256, 0, s>>>(work, half_words, xs[k], xbits[k]);
+      launch_k(load_operand_kernel, dim3(grid_1d(half_words)), dim3(256), 0, s, work, half_words, xs[k], xbits[k]);
       FPM_LAUNCH_CHECK();
       basis_cvt_device(work32, count, xbits[k], false, s, nullptr, nullptr, fused ? &sink : nullptr);
     }
@@ -313,7 +317,7 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     const uint64_t q0 = std::min<uint64_t>((w0 + 1) / 2, out_words), q1 = std::min<uint64_t>((w1 + 1) / 2, out_words);
     if (q0 >= q1) return;
     if (!in_place) {  // (in place, bit n-1 is the product's, which is zero: deg < out_bits)
-      store_product_kernel<<<grid_1d(q1 - q0), 256, 0, s>>>(d_c, work, out_bits, q0, q1);
+      launch_k(store_product_kernel, dim3(grid_1d(q1 - q0)), dim3(256), 0, s, d_c, work, out_bits, q0, q1);
       FPM_LAUNCH_CHECK();
     }
     copy_out(q0, q1);
@@ -329,13 +333,13 @@ void karatsuba_device(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, s
   const uint64_t wa = (a_bits + 63) / 64, wb = (b_bits + 63) / 64;
   const size_t out_bits = a_bits + b_bits - 1;
   DevBuf X(wa * 8, s), Y(wb * 8, s), P((wa + wb) * 8, s);
-  load_operand_kernel<<<grid_1d(wa), 256, 0, s>>>(X.as<uint64_t>(), wa, d_a, a_bits);
+  launch_k(load_operand_kernel, dim3(grid_1d(wa)), dim3(256), 0, s, X.as<uint64_t>(), wa, d_a, a_bits);
   FPM_LAUNCH_CHECK();
-  load_operand_kernel<<<grid_1d(wb), 256, 0, s>>>(Y.as<uint64_t>(), wb, d_b, b_bits);
+  launch_k(load_operand_kernel, dim3(grid_1d(wb)), dim3(256), 0, s, Y.as<uint64_t>(), wb, d_b, b_bits);
   FPM_LAUNCH_CHECK();
   clmul_words_device(X.as<uint64_t>(), wa, Y.as<uint64_t>(), wb, P.as<uint64_t>(), s);
   const uint64_t out_words = (out_bits + 63) / 64;
-  store_product_kernel<<<grid_1d(out_words), 256, 0, s>>>(d_c, P.as<uint64_t>(), out_bits, 0, out_words);
+  launch_k(store_product_kernel, dim3(grid_1d(out_words)), dim3(256), 0, s, d_c, P.as<uint64_t>(), out_bits, 0, out_words);
   FPM_LAUNCH_CHECK();
 }
 
@@ -505,6 +509,14 @@ struct Ev {
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 void set_last_error(const char* msg) { g_err = msg; }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FPM_PDL");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
 
 namespace {
 cudaMemPool_t library_pool(int dev) {
@@ -1057,7 +1069,7 @@ fpm_status fpm_load_operand_dev(uint64_t* d_dst, size_t dst_words, const uint64_
   return guard([&] {
     require_device();
     if (!dst_words) return;
-    load_operand_kernel<<<grid_1d(dst_words), 256, 0, (cudaStream_t)stream>>>(d_dst, dst_words, d_src, src_bits);
+    launch_k(load_operand_kernel, dim3(grid_1d(dst_words)), dim3(256), 0, (cudaStream_t)stream, d_dst, dst_words, d_src, src_bits);
     FPM_LAUNCH_CHECK();
   });
 }

@@ -9,6 +9,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "fpm_tables.h"
 
@@ -74,6 +75,32 @@ struct DevBuf {
   DevBuf& operator=(const DevBuf&) = delete;
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
+
+// Programmatic dependent launch (sm_90+).  Every library kernel begins with pdl_wait() (the
+// previous kernel of its stream has completed and its writes are visible -- nothing is read before
+// it) and pdl_trigger() (the stream's next kernel may be scheduled now; its CTAs park at their own
+// pdl_wait), and every launch goes through launch_k with the programmatic-serialization attribute:
+// back-to-back kernels overlap their launch latency instead of leaving a gap (graphs keep the edges
+// as programmatic dependencies).  FPM_PDL=0 launches without the attribute (plain serialization).
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
+bool pdl_enabled();
+template <class... KArgs, class... Args>
+void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  (void)cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);  // errors: FPM_LAUNCH_CHECK
+}
 
 // Runs an initialisation (e.g. cudaFuncSetAttribute of a kernel's dynamic shared memory) once per
 // device: kernel attributes belong to a device context, so a process driving several GPUs must set

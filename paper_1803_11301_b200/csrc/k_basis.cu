@@ -55,6 +55,7 @@ int sm_count() {
 __global__ void bc_pass_kernel(uint32_t* __restrict__ w, uint64_t nwords, uint64_t S, uint64_t D, int inverse,
                                uint64_t w_first, uint64_t nw_span, uint64_t nspans, uint64_t rlo, uint64_t rhi,
                                uint64_t live_bits) {
+  pdl_wait();
   const uint64_t total = nw_span * nspans;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t span = k / nw_span;
@@ -63,20 +64,24 @@ __global__ void bc_pass_kernel(uint32_t* __restrict__ w, uint64_t nwords, uint64
     const uint64_t wi = (base >> 5) + w_first + (k - span * nw_span);
     w[wi] = fold_word(w, nwords, wi, S, D, inverse != 0, rlo, rhi);
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ small arrays (< 2^8 bits)
 __global__ void bc_small_kernel(uint32_t* __restrict__ w, int words, PassList pl, int inverse) {
+  pdl_wait();
   extern __shared__ uint32_t sm[];
   for (int i = threadIdx.x; i < words; i += blockDim.x) sm[i] = w[i];
   __syncthreads();
   const uint32_t* a = smem_passes(sm, sm + words, words, pl, inverse != 0);
   for (int i = threadIdx.x; i < words; i += blockDim.x) w[i] = a[i];
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ conv of 2^r-bit chunks, 8 KiB tiles
 template <bool INV>
 __global__ void __launch_bounds__(256) conv_rows_kernel(uint32_t* __restrict__ data, uint64_t nwords, int r) {
+  pdl_wait();
   extern __shared__ uint32_t smem[];
   uint32_t* tile = smem;
   uint32_t* sc = smem + kTileRows * kRowPitchW<1>;
@@ -101,6 +106,7 @@ __global__ void __launch_bounds__(256) conv_rows_kernel(uint32_t* __restrict__ d
       reinterpret_cast<uint4*>(data + off)[1] = make_uint4(m[4], m[5], m[6], m[7]);
     }
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ Z: subset-zeta over row bits
@@ -126,6 +132,7 @@ __global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32
                                                    uint32_t* __restrict__ dst, uint64_t dst_pitch, uint64_t D,
                                                    int b0, int nb, Skew skew, uint64_t src_row_words,
                                                    uint64_t windows) {
+  pdl_wait();
   extern __shared__ __align__(16) uint32_t sx[];  // 256 x kZP
   const int tid = threadIdx.x;
   const int wpc = 256 >> nb;  // windows per CTA
@@ -259,6 +266,7 @@ __global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32
     }
     __syncthreads();
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 // ------------------------------------------------------------------ C: carry + unskew + conv(2^16)
 // g_k[p] = Gs[k][p+k] ^ (p >= 1 ? Gs[k][t+p-1+k] : 0) ^ (k >= 1 ? Gs[k-1][t+p+k-1] : 0), then conv(g_k).
@@ -266,6 +274,7 @@ __global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32
 // chunk-local step L1_inner of conv2d, whose digits restart every 256 rows).
 __global__ void __launch_bounds__(256, 4) carry_rows_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch,
                                                          uint32_t* __restrict__ out, uint64_t D, uint64_t kmask) {
+  pdl_wait();
   extern __shared__ uint32_t smem[];
   uint32_t* tile = smem;
   uint32_t* sc = smem + kTileRows * kRowPitchW<1>;
@@ -334,6 +343,7 @@ __global__ void __launch_bounds__(256, 4) carry_rows_kernel(const uint32_t* __re
     o[0] = make_uint4(m[0], m[1], m[2], m[3]);
     o[1] = make_uint4(m[4], m[5], m[6], m[7]);
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ O: overflow + unskew (inverse)
@@ -343,6 +353,7 @@ __global__ void __launch_bounds__(256, 4) carry_rows_kernel(const uint32_t* __re
 __global__ void __launch_bounds__(256) overflow_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch,
                                                        uint32_t* __restrict__ out, uint64_t D,
                                                        const uint32_t* __restrict__ top, uint64_t kmask) {
+  pdl_wait();
   // One row per CTA iteration: the shifts and row pointers are row-invariant; thread t produces
   // words t, t + 256, ... (a warp covers 32 consecutive words: one coalesced load per lane, the
   // funnel's upper word from the next lane, lane 31 loads its own).  Only the first words of a row
@@ -378,11 +389,14 @@ __global__ void __launch_bounds__(256) overflow_kernel(const uint32_t* __restric
       o[w] = v;
     }
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // Bit 0 of the upper 2^32-bit block ^= its last bit (the fused 2^33-bit top pass's target 2^32).
 __global__ void top_bit_fix_kernel(uint32_t* __restrict__ hi_block, uint64_t block_words) {
+  pdl_wait();
   if (threadIdx.x == 0) hi_block[0] ^= hi_block[block_words - 1] >> 31;
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ C_D for D <= 256: slab tiles
@@ -393,6 +407,7 @@ constexpr int kSlabW = 4;  // 128 B of each row per slab: full lines, 4x fewer b
 template <bool INV>
 __global__ void __launch_bounds__(256) slab_kernel(uint32_t* __restrict__ data, int g, uint64_t rstride,
                                                    uint64_t nslabs) {
+  pdl_wait();
   extern __shared__ __align__(16) uint32_t tile[];  // 256 x kRowPitchW<kSlabW>
   constexpr int W = kSlabW, cpr = kTWords / (8 * W);  // slabs per row
   const int tid = threadIdx.x;
@@ -423,6 +438,7 @@ __global__ void __launch_bounds__(256) slab_kernel(uint32_t* __restrict__ data, 
       }
     }
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ conv(256) over units, by L1(16, 16)
@@ -463,6 +479,7 @@ struct CarrySrc {
 template <bool INV>
 __global__ void __launch_bounds__(kC256Threads, INV ? 3 : 4) conv256_units_kernel(uint32_t* __restrict__ data, UnitMap um,
                                                                         uint64_t nitems, CarrySrc cs) {
+  pdl_wait();
   extern __shared__ uint32_t Z[];  // [d][s][c], d < 16, s < 32, c < 32
   const int tid = threadIdx.x, c = tid % kC256Cols, r = tid / kC256Cols;
   constexpr int kCols = kTWords / kC256Cols;  // column blocks per unit
@@ -566,6 +583,7 @@ __global__ void __launch_bounds__(kC256Threads, INV ? 3 : 4) conv256_units_kerne
       }
     }
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ---- the same conv(256) over units with TMA-fed staging (no fused carry input): 128 B of each of
@@ -599,6 +617,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 template <bool INV>
 __global__ void __launch_bounds__(kCTThreads, kCTMinBlocks) conv256_units_tma_kernel(uint32_t* data, UnitMap um, uint64_t nitems,
                                                                           const __grid_constant__ CUtensorMap tmap) {
+  pdl_wait();
   extern __shared__ __align__(128) uint32_t sm_ct[];
   auto stage = [&](int st) { return sm_ct + st * (256 * kCT); };
   uint32_t* Z = sm_ct + 2 * 256 * kCT;  // [d][33][kCT]
@@ -716,6 +735,7 @@ __global__ void __launch_bounds__(kCTThreads, kCTMinBlocks) conv256_units_tma_ke
     }
     __syncthreads();  // Z reuse by the next item
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ---- the last step of a forward 2^32-bit conversion fused with the Frobenius-partition encode
@@ -737,6 +757,7 @@ __global__ void __launch_bounds__(kCTThreads, 1) conv256_a_encode_kernel(const u
                                                                          const __grid_constant__ CUtensorMap tmap,
                                                                          const void* __restrict__ tab_g,
                                                                          void* __restrict__ ev_out) {
+  pdl_wait();
   using E = std::conditional_t<M == 128, uint4, uint2>;
   constexpr int S = M == 128 ? 4 : 8, RPS = 256 / S;  // sub-slabs, rows per sub-slab
   E* ev = static_cast<E*>(ev_out);
@@ -855,6 +876,7 @@ __global__ void __launch_bounds__(kCTThreads, 1) conv256_a_encode_kernel(const u
     }
     __syncthreads();  // Z reuse by the next item
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ---- the first step of a 2^33-bit inverse conversion fused with the decode (encode.cpp:195-220):
@@ -873,6 +895,7 @@ __global__ void __launch_bounds__(kCTThreads, 1) decode_conv_a_kernel(const void
                                                                       const void* __restrict__ tab_g,
                                                                       uint32_t* __restrict__ w_lo,
                                                                       uint32_t* __restrict__ w_hi, uint64_t nitems) {
+  pdl_wait();
   using E = std::conditional_t<M == 128, uint4, uint2>;
   constexpr int S = M == 128 ? 4 : 8, RPS = 256 / S;
   constexpr int kTabUint4 = M == 128 ? kM8Uint4 : kG8Uint2 / 2;
@@ -966,6 +989,7 @@ __global__ void __launch_bounds__(kCTThreads, 1) decode_conv_a_kernel(const void
       __syncthreads();  // Z reuse
     }
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ unit-level L1 carry + C_cols
@@ -975,6 +999,7 @@ __global__ void __launch_bounds__(kCTThreads, 1) decode_conv_a_kernel(const void
 // followed by conv(Dd) over kh (C_cols, row passes in shared memory).  Item = (v, 8-word column).
 __global__ void __launch_bounds__(256) unit_carry_cols_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch,
                                                               uint32_t* __restrict__ out, int gd, uint64_t items) {
+  pdl_wait();
   extern __shared__ __align__(16) uint32_t tile[];  // 256 x kRowPitchW<kSlabW>
   constexpr int W = kSlabW, cpr = kTWords / (8 * W);
   const int tid = threadIdx.x;
@@ -1015,11 +1040,13 @@ __global__ void __launch_bounds__(256) unit_carry_cols_kernel(const uint32_t* __
       }
     }
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // Unit-level L1 inverse tail: F[256 dh + v] = Gs[dh][v+dh] ^ (dh >= 1 ? Gs[dh-1][256+v+dh-1] : 0).
 __global__ void unit_overflow_kernel(const uint32_t* __restrict__ gs, uint64_t gs_pitch, uint32_t* __restrict__ out,
                                      uint64_t Dd) {
+  pdl_wait();
   const uint64_t q_per_row = kTWords / 4;
   const uint64_t total = Dd * 256 * q_per_row;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (uint64_t)gridDim.x * blockDim.x) {
@@ -1032,6 +1059,7 @@ __global__ void unit_overflow_kernel(const uint32_t* __restrict__ gs, uint64_t g
     }
     reinterpret_cast<uint4*>(out)[k] = a;
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ L1_outer: Taylor step in z = y^256
@@ -1064,6 +1092,7 @@ __global__ void __launch_bounds__(256, 3) outer_zeta_kernel(const uint32_t* src,
                                                             uint64_t windows, uint64_t groups,
                                                             uint32_t* __restrict__ side,
                                                             const uint32_t* __restrict__ top) {
+  pdl_wait();
   extern __shared__ __align__(16) uint32_t sx[];  // 256 x kZP
   constexpr int R = 1 << NB, wpc = 256 >> NB;
   const int tid = threadIdx.x, c = tid & 31, w8 = tid >> 5;
@@ -1136,6 +1165,7 @@ __global__ void __launch_bounds__(256, 3) outer_zeta_kernel(const uint32_t* src,
     }
     __syncthreads();
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // Folds the beyond-window parts into the first R*skew words of the rows (row e's side holds
@@ -1144,6 +1174,7 @@ __global__ void __launch_bounds__(256, 3) outer_zeta_kernel(const uint32_t* src,
 template <bool INV>
 __global__ void outer_fix_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ side, const StepGeom gm,
                                  uint64_t groups) {
+  pdl_wait();
   const uint64_t R = (uint64_t)1 << gm.nb, P = gm.skew_words << gm.nb, S = gm.skew_words, per_group = R * P / 4;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < groups * per_group;
        k += (uint64_t)gridDim.x * blockDim.x) {
@@ -1158,6 +1189,7 @@ __global__ void outer_fix_kernel(uint32_t* __restrict__ dst, const uint32_t* __r
       *d = x4v(*d, v);
     }
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ host orchestration
@@ -1177,8 +1209,8 @@ int grid_cap(uint64_t items, int per_sm) {
 
 void conv_rows(uint32_t* data, uint64_t nwords, int r, bool inv, cudaStream_t s) {
   const uint64_t tiles = nwords < 2048 ? 1 : nwords / 2048;
-  if (inv) conv_rows_kernel<true><<<grid_cap(tiles, 7), 256, kTileSmem, s>>>(data, nwords, r);
-  else conv_rows_kernel<false><<<grid_cap(tiles, 7), 256, kTileSmem, s>>>(data, nwords, r);
+  if (inv) launch_k(conv_rows_kernel<true>, dim3(grid_cap(tiles, 7)), dim3(256), kTileSmem, s, data, nwords, r);
+  else launch_k(conv_rows_kernel<false>, dim3(grid_cap(tiles, 7)), dim3(256), kTileSmem, s, data, nwords, r);
   FPM_LAUNCH_CHECK();
 }
 
@@ -1189,11 +1221,9 @@ void zeta(const uint32_t* src, uint64_t src_pitch, uint32_t* dst, uint64_t dst_p
   const int wpc = 256 >> nb;
   const uint64_t items = (D >> nb) * ((windows + wpc - 1) / wpc);
   if (skew.mask && skew.log < 5)
-    zeta_kernel<true><<<grid_cap(items, 4), 256, 256 * kZP * sizeof(uint32_t), s>>>(
-        src, src_pitch, dst, dst_pitch, D, b0, nb, skew, src_row_words, windows);
+    launch_k(zeta_kernel<true>, dim3(grid_cap(items, 4)), dim3(256), 256 * kZP * sizeof(uint32_t), s, src, src_pitch, dst, dst_pitch, D, b0, nb, skew, src_row_words, windows);
   else
-    zeta_kernel<false><<<grid_cap(items, 4), 256, 256 * kZP * sizeof(uint32_t), s>>>(
-        src, src_pitch, dst, dst_pitch, D, b0, nb, skew, src_row_words, windows);
+    launch_k(zeta_kernel<false>, dim3(grid_cap(items, 4)), dim3(256), 256 * kZP * sizeof(uint32_t), s, src, src_pitch, dst, dst_pitch, D, b0, nb, skew, src_row_words, windows);
   FPM_LAUNCH_CHECK();
 }
 
@@ -1254,14 +1284,14 @@ void conv256_units(uint32_t* w, uint64_t ngroups, uint64_t ustride, uint64_t gst
     // groups of 256 units: (ustride, gstride) = (1, 1) consecutive rows, or (g, g) rows g apart
     if (ustride != gstride) throw Error(kInvalid, "conv256_units: unit stride must equal the group stride");
     const CUtensorMap tm = unit_tensor_map(w, ngroups * 256, gstride);
-    if (inv) conv256_units_tma_kernel<true><<<grid_cap(titems, kCTMinBlocks), kCTThreads, kCTSmem, s>>>(w, um, titems, tm);
-    else conv256_units_tma_kernel<false><<<grid_cap(titems, kCTMinBlocks), kCTThreads, kCTSmem, s>>>(w, um, titems, tm);
+    if (inv) launch_k(conv256_units_tma_kernel<true>, dim3(grid_cap(titems, kCTMinBlocks)), dim3(kCTThreads), kCTSmem, s, w, um, titems, tm);
+    else launch_k(conv256_units_tma_kernel<false>, dim3(grid_cap(titems, kCTMinBlocks)), dim3(kCTThreads), kCTSmem, s, w, um, titems, tm);
     FPM_LAUNCH_CHECK();
     return;
   }
   const uint64_t items = ngroups * (kTWords / kC256Cols);
-  if (inv) conv256_units_kernel<true><<<grid_cap(items, 3), kC256Threads, kC256Smem, s>>>(w, um, items, cs);
-  else conv256_units_kernel<false><<<grid_cap(items, 4), kC256Threads, kC256Smem, s>>>(w, um, items, cs);
+  if (inv) launch_k(conv256_units_kernel<true>, dim3(grid_cap(items, 3)), dim3(kC256Threads), kC256Smem, s, w, um, items, cs);
+  else launch_k(conv256_units_kernel<false>, dim3(grid_cap(items, 4)), dim3(kC256Threads), kC256Smem, s, w, um, items, cs);
   FPM_LAUNCH_CHECK();
 }
 
@@ -1270,21 +1300,21 @@ void slab(uint32_t* w, int g, uint64_t rstride, uint64_t nslabs, bool inv, cudaS
   nslabs /= kSlabW;
   const int spc = 256 >> g;
   const uint64_t ctas = (nslabs + spc - 1) / spc;
-  if (inv) slab_kernel<true><<<grid_cap(ctas, 6), 256, kSlabSmem, s>>>(w, g, rstride, nslabs);
-  else slab_kernel<false><<<grid_cap(ctas, 6), 256, kSlabSmem, s>>>(w, g, rstride, nslabs);
+  if (inv) launch_k(slab_kernel<true>, dim3(grid_cap(ctas, 6)), dim3(256), kSlabSmem, s, w, g, rstride, nslabs);
+  else launch_k(slab_kernel<false>, dim3(grid_cap(ctas, 6)), dim3(256), kSlabSmem, s, w, g, rstride, nslabs);
   FPM_LAUNCH_CHECK();
 }
 
 void unit_carry_cols(const uint32_t* gs, uint64_t gs_pitch, uint32_t* out, int gd, cudaStream_t s) {
   const uint64_t items = 256 * (kTWords / (8 * kSlabW));
   const int spc = 256 >> gd;
-  unit_carry_cols_kernel<<<grid_cap((items + spc - 1) / spc, 6), 256, kSlabSmem, s>>>(gs, gs_pitch, out, gd, items);
+  launch_k(unit_carry_cols_kernel, dim3(grid_cap((items + spc - 1) / spc, 6)), dim3(256), kSlabSmem, s, gs, gs_pitch, out, gd, items);
   FPM_LAUNCH_CHECK();
 }
 
 void unit_overflow(const uint32_t* gs, uint64_t gs_pitch, uint32_t* out, uint64_t Dd, cudaStream_t s) {
   const uint64_t total = Dd * 256 * (kTWords / 4);
-  unit_overflow_kernel<<<grid_cap((total + 255) / 256, 16), 256, 0, s>>>(gs, gs_pitch, out, Dd);
+  launch_k(unit_overflow_kernel, dim3(grid_cap((total + 255) / 256, 16)), dim3(256), 0, s, gs, gs_pitch, out, Dd);
   FPM_LAUNCH_CHECK();
 }
 
@@ -1353,14 +1383,14 @@ void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s, con
   };
   if (!inv) {
     l1_zeta(src ? src : w);
-    carry_rows_kernel<<<grid_cap(D, 7), 256, kTileSmem, s>>>(scratch, wsk, w, D, ~(uint64_t)0);
+    launch_k(carry_rows_kernel, dim3(grid_cap(D, 7)), dim3(256), kTileSmem, s, scratch, wsk, w, D, ~(uint64_t)0);
     FPM_LAUNCH_CHECK();
     conv_cols(w, scratch, lgD, false, s);
   } else {
     conv_rows(w, D * kTWords, kTLog2, true, s);
     conv_cols(w, scratch, lgD, true, s);
     l1_zeta(w);
-    overflow_kernel<<<grid_cap(D, 8), 256, 0, s>>>(scratch, wsk, w, D, top, ~(uint64_t)0);
+    launch_k(overflow_kernel, dim3(grid_cap(D, 8)), dim3(256), 0, s, scratch, wsk, w, D, top, ~(uint64_t)0);
     FPM_LAUNCH_CHECK();
   }
 }
@@ -1381,15 +1411,15 @@ void two_term_step(const uint32_t* src, uint32_t* w, StepGeom gm, uint64_t group
   const int grid = grid_cap(items, 3);
   switch (gm.nb) {
 #define FPM_OUTER(NB) \
-    case NB: outer_zeta_kernel<NB><<<grid, 256, smem, s>>>(src, w, gm, gm.windows(), groups, side, top); break;
+    case NB: launch_k(outer_zeta_kernel<NB>, dim3(grid), dim3(256), smem, s, src, w, gm, gm.windows(), groups, side, top); break;
     FPM_OUTER(1) FPM_OUTER(2) FPM_OUTER(3) FPM_OUTER(4) FPM_OUTER(5) FPM_OUTER(6) FPM_OUTER(7) FPM_OUTER(8)
 #undef FPM_OUTER
     default: throw Error(kInvalid, "two-term step: 1..8 digit bits");
   }
   FPM_LAUNCH_CHECK();
   const uint64_t fix = groups * (gm.side_pitch() << gm.nb) / 4;
-  if (inv) outer_fix_kernel<true><<<grid_cap((fix + 255) / 256, 8), 256, 0, s>>>(w, side, gm, groups);
-  else outer_fix_kernel<false><<<grid_cap((fix + 255) / 256, 8), 256, 0, s>>>(w, side, gm, groups);
+  if (inv) launch_k(outer_fix_kernel<true>, dim3(grid_cap((fix + 255) / 256, 8)), dim3(256), 0, s, w, side, gm, groups);
+  else launch_k(outer_fix_kernel<false>, dim3(grid_cap((fix + 255) / 256, 8)), dim3(256), 0, s, w, side, gm, groups);
   FPM_LAUNCH_CHECK();
 }
 
@@ -1428,10 +1458,10 @@ void conv256_a_encode(uint32_t* w, const EncodeSink& enc, cudaStream_t s) {
   const CUtensorMap tm = unit_tensor_map(w, 65536, 256);
   const int grid = grid_cap(items, 1);
   if (enc.m == 64)
-    conv256_a_encode_kernel<64><<<grid, kCTThreads, kCTEncSmem, s>>>(w, um, items, tm, enc.tower ? dt.enc_g8r : dt.enc_g8,
+    launch_k(conv256_a_encode_kernel<64>, dim3(grid), dim3(kCTThreads), kCTEncSmem, s, w, um, items, tm, enc.tower ? dt.enc_g8r : dt.enc_g8,
                                                                      enc.ev);
   else
-    conv256_a_encode_kernel<128><<<grid, kCTThreads, kCTEncSmem, s>>>(w, um, items, tm, enc.tower ? dt.enc_m8r : dt.enc_m8,
+    launch_k(conv256_a_encode_kernel<128>, dim3(grid), dim3(kCTThreads), kCTEncSmem, s, w, um, items, tm, enc.tower ? dt.enc_m8r : dt.enc_m8,
                                                                       enc.ev);
   FPM_LAUNCH_CHECK();
 }
@@ -1504,14 +1534,14 @@ void conv2d_split(uint32_t* w, int K, bool inv, uint32_t* scratch, uint32_t* sid
       in = w;
     }
     zeta(in, kTWords, scratch, p1, D, 0, nb_in, lo_skew, p1 / kZW, s, kTWords);
-    carry_rows_kernel<<<grid_cap(D, 7), 256, kTileSmem, s>>>(scratch, p1, w, D, 255);
+    launch_k(carry_rows_kernel, dim3(grid_cap(D, 7)), dim3(256), kTileSmem, s, scratch, p1, w, D, 255);
     FPM_LAUNCH_CHECK();
     conv_cols_split(w, side, lgD, false, s, enc);
   } else {
     conv_cols_split(w, side, lgD, true, s, nullptr, skip_a);
     conv_rows(w, D * kTWords, kTLog2, true, s);
     zeta(w, kTWords, scratch, p1, D, 0, nb_in, lo_skew, p1 / kZW, s, kTWords);
-    overflow_kernel<<<grid_cap(D, 8), 256, 0, s>>>(scratch, p1, w, D, nb_out ? nullptr : top, 255);
+    launch_k(overflow_kernel, dim3(grid_cap(D, 8)), dim3(256), 0, s, scratch, p1, w, D, nb_out ? nullptr : top, 255);
     FPM_LAUNCH_CHECK();
     if (nb_out) outer(w, top);
   }
@@ -1535,7 +1565,7 @@ void run_big_pass(uint32_t* w, uint64_t nwords, Pass p, bool inverse, uint64_t l
     const uint64_t w_first = rlo / 32, w_last = (rhi + 31) / 32;
     const uint64_t nw_span = w_last - w_first;
     const uint64_t total = nw_span * nspans;
-    bc_pass_kernel<<<grid_cap((total + 255) / 256, 32), 256, 0, s>>>(w, nwords, S, D, inverse ? 1 : 0, w_first,
+    launch_k(bc_pass_kernel, dim3(grid_cap((total + 255) / 256, 32)), dim3(256), 0, s, w, nwords, S, D, inverse ? 1 : 0, w_first,
                                                                      nw_span, nspans, rlo, rhi, live_bits);
     FPM_LAUNCH_CHECK();
   }
@@ -1562,7 +1592,7 @@ void basis_cvt_block32_inverse(uint32_t* w, const uint32_t* top, cudaStream_t s)
 }
 
 void top_bit_fix_device(uint32_t* hi_block, cudaStream_t s) {
-  top_bit_fix_kernel<<<1, 32, 0, s>>>(hi_block, ((uint64_t)1 << 32) / 32);
+  launch_k(top_bit_fix_kernel, dim3(1), dim3(32), 0, s, hi_block, ((uint64_t)1 << 32) / 32);
   FPM_LAUNCH_CHECK();
 }
 
@@ -1582,10 +1612,10 @@ void decode_conv_a(const DecodeSource& dec, uint32_t* w_lo, uint32_t* w_hi, cuda
   const uint64_t items = 256 * (kTWords / kCT);
   const int grid = grid_cap(items, 1);
   if (dec.m == 64)
-    decode_conv_a_kernel<64><<<grid, kCTThreads, kDecSmem, s>>>(dec.ev, dec.tower ? dt.dec_g8r : dt.dec_g8, w_lo, w_hi,
+    launch_k(decode_conv_a_kernel<64>, dim3(grid), dim3(kCTThreads), kDecSmem, s, dec.ev, dec.tower ? dt.dec_g8r : dt.dec_g8, w_lo, w_hi,
                                                                 items);
   else
-    decode_conv_a_kernel<128><<<grid, kCTThreads, kDecSmem, s>>>(dec.ev, dec.tower ? dt.dec_m8r : dt.dec_m8, w_lo, w_hi,
+    launch_k(decode_conv_a_kernel<128>, dim3(grid), dim3(kCTThreads), kDecSmem, s, dec.ev, dec.tower ? dt.dec_m8r : dt.dec_m8, w_lo, w_hi,
                                                                  items);
   FPM_LAUNCH_CHECK();
 }
@@ -1613,7 +1643,7 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
     std::vector<Pass> v(sched, sched + np);
     if (inverse) v = std::vector<Pass>(sched, sched + np), v = std::vector<Pass>(v.rbegin(), v.rend());
     const PassList pl = make_passlist(v, inverse);
-    bc_small_kernel<<<1, 32, 2 * nwords * sizeof(uint32_t), s>>>(w, (int)nwords, pl, inverse ? 1 : 0);
+    launch_k(bc_small_kernel, dim3(1), dim3(32), 2 * nwords * sizeof(uint32_t), s, w, (int)nwords, pl, inverse ? 1 : 0);
     FPM_LAUNCH_CHECK();
     if (inverse && on_final) (*on_final)(0, nwords);
     return;
@@ -1680,7 +1710,7 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
     if (on_final && w0 < w1) (*on_final)(w0, w1);
   }
   if (fuse_top) {
-    top_bit_fix_kernel<<<1, 32, 0, s>>>(w + block_words, block_words);
+    launch_k(top_bit_fix_kernel, dim3(1), dim3(32), 0, s, w + block_words, block_words);
     FPM_LAUNCH_CHECK();
   } else {
     for (size_t k = top.size(); k-- > 0;) run_big_pass(w, nwords, top[k], true, n_bits, s);

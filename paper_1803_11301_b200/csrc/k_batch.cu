@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(256) batch_kernel(const uint64_t* __restrict__
                                                     const uint4* __restrict__ enc_m8, const uint4* __restrict__ dec_m8,
                                                     const uint4* __restrict__ enc_rows,
                                                     const uint4* __restrict__ inv_rows, TwiddleSrc tw) {
+  pdl_wait();
   extern __shared__ uint4 sm[];
   const int n_p = 1 << l;
   const int n_words = n_p * 4;  // n = 128 n_p bits
@@ -237,6 +238,7 @@ __global__ void __launch_bounds__(256) batch_kernel(const uint64_t* __restrict__
     if (k == out_words - 1 && (out_bits & 63)) v &= (((uint64_t)1) << (out_bits & 63)) - 1;
     cc[k] = v;
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 }  // namespace
@@ -262,7 +264,7 @@ void polymul_batch_device(const uint64_t* a, size_t a_bits, size_t a_stride_word
   });
   for (size_t off = 0; off < count; off += 65535u * 16u) {
     const size_t cnt = std::min<size_t>(count - off, 65535u * 16u);
-    batch_kernel<<<(unsigned)cnt, 256, smem, s>>>(a + off * a_stride_words, a_bits, a_stride_words,
+    launch_k(batch_kernel, dim3((unsigned)cnt), dim3(256), smem, s, a + off * a_stride_words, a_bits, a_stride_words,
                                                   b + off * b_stride_words, b_bits, b_stride_words,
                                                   c + off * c_stride_words, c_stride_words, l, dt.enc_m8, dt.dec_m8,
                                                   dt.enc_rows, dt.inv_rows, make_twiddle_src(dev, l, partition_base(l)));

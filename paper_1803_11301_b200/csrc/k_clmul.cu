@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(kClTile) clmul_words_kernel(const uint64_t* __
                                                                const uint64_t* __restrict__ b, uint64_t wb,
                                                                uint64_t* __restrict__ out, uint64_t wout,
                                                                uint64_t chunks_per_y) {
+  pdl_wait();
   __shared__ uint64_t sa[kClTile];
   __shared__ uint64_t sb[2 * kClTile];
   __shared__ uint64_t carry[kClTile];
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(kClTile) clmul_words_kernel(const uint64_t* __
   if (k < wout && v) atomicXor(reinterpret_cast<unsigned long long*>(out + k), (unsigned long long)v);
   if (t == kClTile - 1 && k + 1 < wout && hi)
     atomicXor(reinterpret_cast<unsigned long long*>(out + k + 1), (unsigned long long)hi);
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 }  // namespace
@@ -97,7 +99,7 @@ void clmul_words_device(const uint64_t* a, uint64_t wa, const uint64_t* b, uint6
   const uint64_t per_y = (nchunks + ys - 1) / ys;
   ys = (nchunks + per_y - 1) / per_y;
   if (tiles > 0x7FFFFFFFull) throw Error(kInvalid, "clmul_words: product too long");
-  clmul_words_kernel<<<dim3((unsigned)tiles, (unsigned)ys), kClTile, 0, s>>>(a, wa, b, wb, out, wout, per_y);
+  launch_k(clmul_words_kernel, dim3(dim3((unsigned)tiles, (unsigned)ys)), dim3(kClTile), 0, s, a, wa, b, wb, out, wout, per_y);
   FPM_LAUNCH_CHECK();
 }
 

@@ -29,6 +29,7 @@ template <int ROWS>  // 64: rows >= 64 are known zero (pipeline); 12
 __global__ void __launch_bounds__(256) encode_kernel(const uint32_t* __restrict__ poly, uint64_t row_words,
                                                      uint64_t col0_words, uint64_t nslabs,
                                                      const uint4* __restrict__ tab_g, uint4* __restrict__ ev) {
+  pdl_wait();
   extern __shared__ uint4 smem4[];
   // rotated 8-bit table of x*E (gf128.cuh m8 layout): chunks 0..7 (ROWS = 64) or all 16
   constexpr int kTab = ROWS == 64 ? kM8Uint4 / 2 : kM8Uint4;
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint32_t* __restrict_
       ev[(w0 + col) * 32 + lane] = f;
     }
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // Rows 0..63 go to poly (pitch row_words), rows 64..127 to poly_hi (same pitch); column word offset
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(256) decode_kernel(const uint4* __restrict__ e
                                                      uint64_t row_words,
                                                      const uint4* __restrict__ tab_g, uint32_t* __restrict__ poly,
                                                      uint32_t* __restrict__ poly_hi) {
+  pdl_wait();
   extern __shared__ uint4 smem4[];
   uint4* tab = smem4;  // rotated 8-bit table of x*E^-1 (gf128.cuh m8 layout)
   uint32_t* slab = reinterpret_cast<uint32_t*>(smem4 + kM8Uint4);  // 128 x kPad
@@ -133,11 +136,13 @@ __global__ void __launch_bounds__(256) decode_kernel(const uint4* __restrict__ e
     }
     __syncthreads();
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // Tiny shapes (n_p < 1024): one thread per element, direct row products (encode.cpp:172-181).
 __global__ void encode_small_kernel(const uint32_t* __restrict__ poly, uint64_t n_p, const uint4* __restrict__ rows,
                                     uint4* __restrict__ ev) {
+  pdl_wait();
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_p) return;
   uint4 acc = make_uint4(0, 0, 0, 0);
@@ -146,10 +151,12 @@ __global__ void encode_small_kernel(const uint32_t* __restrict__ poly, uint64_t 
     if ((poly[k >> 5] >> (k & 31)) & 1u) acc = x4(acc, rows[j]);
   }
   ev[i] = acc;
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 __global__ void decode_small_kernel(const uint4* __restrict__ ev, uint64_t n_p, const uint4* __restrict__ inv_rows,
                                     uint32_t* __restrict__ poly) {
+  pdl_wait();
   // one thread per output word of the 128*n_p-bit polynomial
   const uint64_t wi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nwords = (128 * n_p + 31) / 32;
@@ -172,6 +179,7 @@ __global__ void decode_small_kernel(const uint4* __restrict__ ev, uint64_t n_p, 
     out |= acc << b;
   }
   poly[wi] = out;
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ GF(2^64) (m = 64)
@@ -182,6 +190,7 @@ template <int ROWS>
 __global__ void __launch_bounds__(256) encode64_kernel(const uint32_t* __restrict__ poly, uint64_t row_words,
                                                        uint64_t nslabs, const uint2* __restrict__ tab_g,
                                                        uint2* __restrict__ ev) {
+  pdl_wait();
   extern __shared__ uint2 smem2[];
   uint2* tab = smem2;                                               // kG8Uint2
   uint32_t* slab = reinterpret_cast<uint32_t*>(smem2 + kG8Uint2);  // ROWS x kPad
@@ -228,11 +237,13 @@ __global__ void __launch_bounds__(256) encode64_kernel(const uint32_t* __restric
       ev[(w0 + col) * 32 + lane] = x2(acc0, acc1);
     }
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 __global__ void __launch_bounds__(256) decode64_kernel(const uint2* __restrict__ ev, uint64_t nslabs,
                                                        uint64_t row_words, const uint2* __restrict__ tab_g,
                                                        uint32_t* __restrict__ poly) {
+  pdl_wait();
   extern __shared__ uint2 smem2[];
   uint2* tab = smem2;
   uint32_t* slab = reinterpret_cast<uint32_t*>(smem2 + kG8Uint2);  // 64 x kPad
@@ -268,11 +279,13 @@ __global__ void __launch_bounds__(256) decode64_kernel(const uint2* __restrict__
     }
     __syncthreads();
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // Tiny shapes: one thread per element / output word, direct row products.
 __global__ void encode64_small_kernel(const uint32_t* __restrict__ poly, uint64_t n_p, const uint2* __restrict__ rows,
                                       uint2* __restrict__ ev) {
+  pdl_wait();
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_p) return;
   uint2 acc = make_uint2(0, 0);
@@ -281,10 +294,12 @@ __global__ void encode64_small_kernel(const uint32_t* __restrict__ poly, uint64_
     if ((poly[k >> 5] >> (k & 31)) & 1u) acc = x2(acc, rows[j]);
   }
   ev[i] = acc;
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 __global__ void decode64_small_kernel(const uint2* __restrict__ ev, uint64_t n_p, const uint2* __restrict__ inv_rows,
                                       uint32_t* __restrict__ poly) {
+  pdl_wait();
   const uint64_t wi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t nwords = (64 * n_p + 31) / 32;
   if (wi >= nwords) return;
@@ -303,6 +318,7 @@ __global__ void decode64_small_kernel(const uint2* __restrict__ ev, uint64_t n_p
     out |= acc << b;
   }
   poly[wi] = out;
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // Device copies of the plain row tables for the tiny-shape kernels.
@@ -330,6 +346,7 @@ const RowTables& row_tables(int dev) {
 __device__ __forceinline__ void flip_bit0(uint32_t* w) { *w ^= 1u; }
 __global__ void flip_encode_tables_kernel(uint32_t* small128, uint32_t* m8, uint32_t* m8r, uint32_t* rows64,
                                           uint32_t* g8, uint32_t* g8r) {
+  pdl_wait();
   if (threadIdx.x != 0) return;
   // The forward tables' entry for "row 0 alone" (the reference flips bit 0 of tab_[1], chunk 0 /
   // value 1, encode.hpp:70-71): the tiny-shape row table, the M8 / G8 tables (entry (c=0, v=1);
@@ -342,6 +359,7 @@ __global__ void flip_encode_tables_kernel(uint32_t* small128, uint32_t* m8, uint
   flip_bit0(g8 + 2 * (1 * 16 + 8));
   flip_bit0(g8r + 2 * (1 * 16 + 0));
   flip_bit0(g8r + 2 * (1 * 16 + 8));
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 }  // namespace
@@ -350,7 +368,7 @@ __global__ void flip_encode_tables_kernel(uint32_t* small128, uint32_t* m8, uint
 // the DEVICE copies of the forward encode tables of both fields; a second call restores them.
 void flip_encode_tables(int dev, cudaStream_t s) {
   const DeviceTables& dt = device_tables(dev);
-  flip_encode_tables_kernel<<<1, 32, 0, s>>>(reinterpret_cast<uint32_t*>(row_tables(dev).rows),
+  launch_k(flip_encode_tables_kernel, dim3(1), dim3(32), 0, s, reinterpret_cast<uint32_t*>(row_tables(dev).rows),
                                              reinterpret_cast<uint32_t*>(dt.enc_m8), reinterpret_cast<uint32_t*>(dt.enc_m8r),
                                              reinterpret_cast<uint32_t*>(dt.rows64), reinterpret_cast<uint32_t*>(dt.enc_g8),
                                              reinterpret_cast<uint32_t*>(dt.enc_g8r));
@@ -367,7 +385,7 @@ void encode_cols_device(const uint32_t* poly, unsigned l, uint64_t col0, uint64_
   const uint64_t n_p = (uint64_t)1 << l;
   if (n_p < 1024) {
     if (col0 != 0 || ncols != n_p || tower) throw Error(kInvalid, "encode: column ranges need n_p >= 1024");
-    encode_small_kernel<<<(unsigned)((n_p + 127) / 128), 128, 0, s>>>(poly, n_p, row_tables(dev).rows, ev);
+    launch_k(encode_small_kernel, dim3((unsigned)((n_p + 127) / 128)), dim3(128), 0, s, poly, n_p, row_tables(dev).rows, ev);
     FPM_LAUNCH_CHECK();
     return;
   }
@@ -379,12 +397,12 @@ void encode_cols_device(const uint32_t* poly, unsigned l, uint64_t col0, uint64_
     const size_t smem = kM8Uint4 / 2 * sizeof(uint4) + 64 * kPad * sizeof(uint32_t);
     static PerDeviceOnce attr;
     attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
-    encode_kernel<64><<<resident_grid(encode_kernel<64>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, tab, ev);
+    launch_k(encode_kernel<64>, dim3(resident_grid(encode_kernel<64>, 256, smem, nslabs)), dim3(256), smem, s, poly, n_p / 32, col0 / 32, nslabs, tab, ev);
   } else {
     const size_t smem = kM8Uint4 * sizeof(uint4) + 128 * kPad * sizeof(uint32_t);
     static PerDeviceOnce attr;
     attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
-    encode_kernel<128><<<resident_grid(encode_kernel<128>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, col0 / 32, nslabs, tab, ev);
+    launch_k(encode_kernel<128>, dim3(resident_grid(encode_kernel<128>, 256, smem, nslabs)), dim3(256), smem, s, poly, n_p / 32, col0 / 32, nslabs, tab, ev);
   }
   FPM_LAUNCH_CHECK();
 }
@@ -404,7 +422,7 @@ void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaSt
   if (ncols < 1024) {
     if ((ncols & (ncols - 1)) || tower) throw Error(kInvalid, "decode: element count must be a power of two");
     const uint64_t nwords = (128 * ncols + 31) / 32;
-    decode_small_kernel<<<(unsigned)((nwords + 127) / 128), 128, 0, s>>>(ev, ncols, row_tables(dev).inv, slice);
+    launch_k(decode_small_kernel, dim3((unsigned)((nwords + 127) / 128)), dim3(128), 0, s, ev, ncols, row_tables(dev).inv, slice);
     FPM_LAUNCH_CHECK();
     return;
   }
@@ -414,7 +432,7 @@ void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaSt
   static PerDeviceOnce attr;
   attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
   const uint64_t nslabs = ncols / 32 / kSlabWords;
-  decode_kernel<<<resident_grid(decode_kernel, 256, smem, nslabs), 256, smem, s>>>(ev, nslabs, ncols / 32, tower ? dt.dec_m8r : dt.dec_m8, slice,
+  launch_k(decode_kernel, dim3(resident_grid(decode_kernel, 256, smem, nslabs)), dim3(256), smem, s, ev, nslabs, ncols / 32, tower ? dt.dec_m8r : dt.dec_m8, slice,
                                                                                    slice + 64 * (ncols / 32));
   FPM_LAUNCH_CHECK();
 }
@@ -430,8 +448,7 @@ void decode_cols_split_device(const uint4* ev, uint64_t ncols, uint64_t col0, ui
   static PerDeviceOnce attr;
   attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
   const uint64_t nslabs = ncols / 32 / kSlabWords;
-  decode_kernel<<<resident_grid(decode_kernel, 256, smem, nslabs), 256, smem, s>>>(
-      ev, nslabs, row_bits / 32, tower ? dt.dec_m8r : dt.dec_m8, lo + col0 / 32, hi + col0 / 32);
+  launch_k(decode_kernel, dim3(resident_grid(decode_kernel, 256, smem, nslabs)), dim3(256), smem, s, ev, nslabs, row_bits / 32, tower ? dt.dec_m8r : dt.dec_m8, lo + col0 / 32, hi + col0 / 32);
   FPM_LAUNCH_CHECK();
 }
 
@@ -442,17 +459,17 @@ void encode64_device(const uint32_t* poly, unsigned l, uint2* ev, int rows_live,
   const uint64_t n_p = (uint64_t)1 << l;
   if (n_p < 1024) {
     if (tower) throw Error(kInvalid, "encode64: the tower representation needs n_p >= 1024");
-    encode64_small_kernel<<<(unsigned)((n_p + 127) / 128), 128, 0, s>>>(poly, n_p, dt.rows64, ev);
+    launch_k(encode64_small_kernel, dim3((unsigned)((n_p + 127) / 128)), dim3(128), 0, s, poly, n_p, dt.rows64, ev);
     FPM_LAUNCH_CHECK();
     return;
   }
   const uint64_t nslabs = n_p / 32 / kSlabWords;
   if (rows_live <= 32) {
     const size_t smem = kG8Uint2 * sizeof(uint2) + 32 * kPad * sizeof(uint32_t);
-    encode64_kernel<32><<<resident_grid(encode64_kernel<32>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, nslabs, tower ? dt.enc_g8r : dt.enc_g8, ev);
+    launch_k(encode64_kernel<32>, dim3(resident_grid(encode64_kernel<32>, 256, smem, nslabs)), dim3(256), smem, s, poly, n_p / 32, nslabs, tower ? dt.enc_g8r : dt.enc_g8, ev);
   } else {
     const size_t smem = kG8Uint2 * sizeof(uint2) + 64 * kPad * sizeof(uint32_t);
-    encode64_kernel<64><<<resident_grid(encode64_kernel<64>, 256, smem, nslabs), 256, smem, s>>>(poly, n_p / 32, nslabs, tower ? dt.enc_g8r : dt.enc_g8, ev);
+    launch_k(encode64_kernel<64>, dim3(resident_grid(encode64_kernel<64>, 256, smem, nslabs)), dim3(256), smem, s, poly, n_p / 32, nslabs, tower ? dt.enc_g8r : dt.enc_g8, ev);
   }
   FPM_LAUNCH_CHECK();
 }
@@ -465,13 +482,13 @@ void decode64_device(const uint2* ev, unsigned l, uint32_t* poly, cudaStream_t s
   if (n_p < 1024) {
     if (tower) throw Error(kInvalid, "decode64: the tower representation needs n_p >= 1024");
     const uint64_t nwords = (64 * n_p + 31) / 32;
-    decode64_small_kernel<<<(unsigned)((nwords + 127) / 128), 128, 0, s>>>(ev, n_p, dt.inv64, poly);
+    launch_k(decode64_small_kernel, dim3((unsigned)((nwords + 127) / 128)), dim3(128), 0, s, ev, n_p, dt.inv64, poly);
     FPM_LAUNCH_CHECK();
     return;
   }
   const uint64_t nslabs = n_p / 32 / kSlabWords;
   const size_t smem = kG8Uint2 * sizeof(uint2) + 64 * kPad * sizeof(uint32_t);
-  decode64_kernel<<<resident_grid(decode64_kernel, 256, smem, nslabs), 256, smem, s>>>(ev, nslabs, n_p / 32, tower ? dt.dec_g8r : dt.dec_g8, poly);
+  launch_k(decode64_kernel, dim3(resident_grid(decode64_kernel, 256, smem, nslabs)), dim3(256), smem, s, ev, nslabs, n_p / 32, tower ? dt.dec_g8r : dt.dec_g8, poly);
   FPM_LAUNCH_CHECK();
 }
 

@@ -64,6 +64,7 @@ __device__ __forceinline__ uint4 twiddle(const TwiddleSrc& tw, unsigned l, unsig
 // R: elements in the tower representation (tower.cuh), the table built in R.
 template <bool INV, bool R>
 __global__ void __launch_bounds__(256) fft_top_kernel(uint4* __restrict__ ev, unsigned l, unsigned i, int ppc, TwiddleSrc tw) {
+  pdl_wait();
   extern __shared__ uint4 tab[];            // kM8Uint4
   __shared__ uint4 rows[144];
   const uint64_t half = (uint64_t)1 << i;
@@ -94,6 +95,7 @@ __global__ void __launch_bounds__(256) fft_top_kernel(uint4* __restrict__ ev, un
     base[j] = u0;
     base[j + half] = u1;
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ top layers, two per pass
@@ -109,6 +111,7 @@ constexpr size_t kTop4Smem = (3 * (size_t)kM8Uint4 + 3 * 144 + 136) * sizeof(uin
 template <bool INV, bool R, int NT = kTop4Threads>
 __global__ void __launch_bounds__(NT, 1) fft_top4_kernel(uint4* __restrict__ ev, unsigned l, unsigned i,
                                                           int qpc, TwiddleSrc tw) {
+  pdl_wait();
   extern __shared__ uint4 sm4[];
   uint4* t1 = sm4;                   // w(i+1, B)
   uint4* t0a = sm4 + kM8Uint4;       // w(i, 2B)
@@ -204,6 +207,7 @@ __global__ void __launch_bounds__(NT, 1) fft_top4_kernel(uint4* __restrict__ ev,
     p[2 * h] = a2;
     p[3 * h] = a3;
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ tile layers (i < T)
@@ -334,6 +338,7 @@ __device__ __forceinline__ void tile_layers(uint4* __restrict__ s, unsigned T, u
 template <bool INV>
 __global__ void __launch_bounds__(256) fft_tile_kernel(uint4* __restrict__ ev, unsigned l, unsigned T, TwiddleSrc tw,
                                                        int use_tab) {
+  pdl_wait();
   extern __shared__ uint4 s[];
   const int n = 1 << T;
   uint4* tab = use_tab ? s + n : nullptr;
@@ -346,10 +351,12 @@ __global__ void __launch_bounds__(256) fft_tile_kernel(uint4* __restrict__ ev, u
     for (int k = threadIdx.x; k < n; k += blockDim.x) g[k] = s[k];
     __syncthreads();
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 __global__ void __launch_bounds__(256) fft_tile_fused_kernel(const uint4* __restrict__ ea, uint4* __restrict__ eb,
                                                              unsigned l, unsigned T, TwiddleSrc tw, int use_tab) {
+  pdl_wait();
   extern __shared__ uint4 s[];
   const int n = 1 << T;
   uint4* tab = use_tab ? s + n : nullptr;
@@ -366,6 +373,7 @@ __global__ void __launch_bounds__(256) fft_tile_fused_kernel(const uint4* __rest
     for (int k = threadIdx.x; k < n; k += blockDim.x) g[k] = s[k];
     __syncthreads();
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // Both operands' tile layers in one CTA: the a and b tiles at the same position share every
@@ -375,6 +383,7 @@ __global__ void __launch_bounds__(256) fft_tile_fused_kernel(const uint4* __rest
 __global__ void __launch_bounds__(kTile2Threads, 512 / kTile2Threads) fft_tile_fused2_kernel(const uint4* __restrict__ ea,
                                                                           uint4* __restrict__ eb, unsigned l,
                                                                           unsigned T, TwiddleSrc tw) {
+  pdl_wait();
   extern __shared__ uint4 s[];
   const int n = 1 << T;
   uint4* tab = s + 2 * n;
@@ -394,6 +403,7 @@ __global__ void __launch_bounds__(kTile2Threads, 512 / kTile2Threads) fft_tile_f
     for (int k = threadIdx.x; k < n; k += blockDim.x) g[k] = s[k];
     __syncthreads();
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ tower-representation tiles
@@ -562,6 +572,7 @@ size_t tower_smem(unsigned T) { return 2 * ((size_t)1 << T) * sizeof(uint4) + si
 __global__ void __launch_bounds__(kTowerThreads, FPM_TOWER_MINB) fft_tile_tower_kernel(const uint4* __restrict__ ea,
                                                                           uint4* __restrict__ eb, unsigned l,
                                                                           unsigned T, TwiddleSrc tw) {
+  pdl_wait();
   extern __shared__ uint4 s[];
   const int n = 1 << T, tid = threadIdx.x, q = tid & 7;
   TowerSmem& sm = *reinterpret_cast<TowerSmem*>(s + 2 * n);
@@ -638,6 +649,7 @@ __global__ void __launch_bounds__(kTowerThreads, FPM_TOWER_MINB) fft_tile_tower_
     for (int k = tid; k < n; k += blockDim.x) g[k] = s[tsw(k)];
     __syncthreads();
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // Exchanged layer of the sharded FFT: all local elements share one twiddle w (polynomial form);
@@ -649,6 +661,7 @@ template <bool INV, bool R>
 __global__ void __launch_bounds__(256) fft_pair_kernel(const uint4* mine, const uint4* __restrict__ theirs,
                                                        uint4* out, uint64_t n, uint4 w, int side, int ppc,
                                                        const uint4* to_r) {
+  pdl_wait();
   extern __shared__ uint4 tab[];
   __shared__ uint4 rows[144];
   if (R) {
@@ -673,12 +686,15 @@ __global__ void __launch_bounds__(256) fft_pair_kernel(const uint4* mine, const 
     }
     out[e] = r;
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 __global__ void pointwise_kernel(const uint4* __restrict__ u, const uint4* __restrict__ v, uint4* __restrict__ out,
                                  uint64_t n) {
+  pdl_wait();
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
     out[k] = gf_mul(u[k], v[k]);
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 int sms() {
@@ -763,8 +779,8 @@ void top_passes(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSr
   if (T < 8 || ctas == 0) throw Error(kInvalid, "butterfly_top: layer too small for the table layer kernel");
   auto radix2 = [&](unsigned i) {
     const uint64_t p = std::min<uint64_t>(ppc, (uint64_t)1 << i);  // a CTA stays inside one block
-    if (!inverse) fft_top_kernel<false, R><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, l, i, (int)p, tw);
-    else fft_top_kernel<true, R><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, l, i, (int)p, tw);
+    if (!inverse) launch_k(fft_top_kernel<false, R>, dim3((unsigned)(pairs / p)), dim3(256), smem, s, ev, l, i, (int)p, tw);
+    else launch_k(fft_top_kernel<true, R>, dim3((unsigned)(pairs / p)), dim3(256), smem, s, ev, l, i, (int)p, tw);
     FPM_LAUNCH_CHECK();
   };
   // layer pairs (i+1, i) from the top down (forward) / bottom up (inverse); an odd count leaves
@@ -786,11 +802,11 @@ void top_passes(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSr
     }();
     const int nt = knob == 512 || knob == 768 ? knob : (inverse ? kTop4Threads : 512);
     if (nt == 512) {
-      if (!inverse) fft_top4_kernel<false, R, 512><<<(unsigned)(quads / q), 512, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
-      else fft_top4_kernel<true, R, 512><<<(unsigned)(quads / q), 512, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
+      if (!inverse) launch_k(fft_top4_kernel<false, R, 512>, dim3((unsigned)(quads / q)), dim3(512), kTop4Smem, s, ev, l, i, (int)q, tw);
+      else launch_k(fft_top4_kernel<true, R, 512>, dim3((unsigned)(quads / q)), dim3(512), kTop4Smem, s, ev, l, i, (int)q, tw);
     } else {
-      if (!inverse) fft_top4_kernel<false, R><<<(unsigned)(quads / q), kTop4Threads, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
-      else fft_top4_kernel<true, R><<<(unsigned)(quads / q), kTop4Threads, kTop4Smem, s>>>(ev, l, i, (int)q, tw);
+      if (!inverse) launch_k(fft_top4_kernel<false, R>, dim3((unsigned)(quads / q)), dim3(kTop4Threads), kTop4Smem, s, ev, l, i, (int)q, tw);
+      else launch_k(fft_top4_kernel<true, R>, dim3((unsigned)(quads / q)), dim3(kTop4Threads), kTop4Smem, s, ev, l, i, (int)q, tw);
     }
     FPM_LAUNCH_CHECK();
   };
@@ -845,11 +861,9 @@ void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, cons
   const TileCfg c = tile_cfg(l, T);
   const uint64_t ntiles = ((uint64_t)1 << l) >> T;
   if (!inverse)
-    fft_tile_kernel<false><<<resident_grid(fft_tile_kernel<false>, c.threads, c.smem, ntiles), c.threads, c.smem, s>>>(
-        ev, l, T, tw, c.use_tab);
+    launch_k(fft_tile_kernel<false>, dim3(resident_grid(fft_tile_kernel<false>, c.threads, c.smem, ntiles)), dim3(c.threads), c.smem, s, ev, l, T, tw, c.use_tab);
   else
-    fft_tile_kernel<true><<<resident_grid(fft_tile_kernel<true>, c.threads, c.smem, ntiles), c.threads, c.smem, s>>>(
-        ev, l, T, tw, c.use_tab);
+    launch_k(fft_tile_kernel<true>, dim3(resident_grid(fft_tile_kernel<true>, c.threads, c.smem, ntiles)), dim3(c.threads), c.smem, s, ev, l, T, tw, c.use_tab);
   FPM_LAUNCH_CHECK();
 }
 
@@ -859,7 +873,7 @@ void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigne
   attr.run([&] { set_smem(fft_tile_fused_kernel, kTileSmemMax); });
   const TileCfg c = tile_cfg(l, T);
   const int grid = resident_grid(fft_tile_fused_kernel, c.threads, c.smem, ((uint64_t)1 << l) >> T);
-  fft_tile_fused_kernel<<<grid, c.threads, c.smem, s>>>(ea, eb, l, T, tw, c.use_tab);
+  launch_k(fft_tile_fused_kernel, dim3(grid), dim3(c.threads), c.smem, s, ea, eb, l, T, tw, c.use_tab);
   FPM_LAUNCH_CHECK();
 }
 
@@ -879,7 +893,7 @@ void butterfly_tile_fused2_device(const uint4* ea, uint4* eb, unsigned l, unsign
   static PerDeviceOnce attr;
   attr.run([&] { set_smem(fft_tile_fused2_kernel, (2 * ((size_t)1 << 11) + kM8Uint4 + 144) * sizeof(uint4)); });
   const int grid = resident_grid(fft_tile_fused2_kernel, kTile2Threads, smem, ((uint64_t)1 << l) >> T);
-  fft_tile_fused2_kernel<<<grid, kTile2Threads, smem, s>>>(ea, eb, l, T, tw);
+  launch_k(fft_tile_fused2_kernel, dim3(grid), dim3(kTile2Threads), smem, s, ea, eb, l, T, tw);
   FPM_LAUNCH_CHECK();
 }
 
@@ -899,7 +913,7 @@ void butterfly_tile_tower_device(const uint4* ea, uint4* eb, unsigned l, unsigne
   attr.run([&] { set_smem(fft_tile_tower_kernel, tower_smem(11)); });
   const size_t smem = tower_smem(T);
   const int grid = resident_grid(fft_tile_tower_kernel, kTowerThreads, smem, ((uint64_t)1 << l) >> T);
-  fft_tile_tower_kernel<<<grid, kTowerThreads, smem, s>>>(ea, eb, l, T, tw);
+  launch_k(fft_tile_tower_kernel, dim3(grid), dim3(kTowerThreads), smem, s, ea, eb, l, T, tw);
   FPM_LAUNCH_CHECK();
 }
 
@@ -937,11 +951,11 @@ void bfly_pair_device(uint4* mine, const uint4* theirs, uint64_t n, U128 w, int 
   const unsigned ctas = (unsigned)((n + ppc - 1) / ppc);
   const uint4 w4 = make_uint4((uint32_t)w.lo, (uint32_t)(w.lo >> 32), (uint32_t)w.hi, (uint32_t)(w.hi >> 32));
   if (tower) {
-    if (!inverse) fft_pair_kernel<false, true><<<ctas, 256, smem, s>>>(mine, theirs, out, n, w4, side, (int)ppc, to_r);
-    else fft_pair_kernel<true, true><<<ctas, 256, smem, s>>>(mine, theirs, out, n, w4, side, (int)ppc, to_r);
+    if (!inverse) launch_k(fft_pair_kernel<false, true>, dim3(ctas), dim3(256), smem, s, mine, theirs, out, n, w4, side, (int)ppc, to_r);
+    else launch_k(fft_pair_kernel<true, true>, dim3(ctas), dim3(256), smem, s, mine, theirs, out, n, w4, side, (int)ppc, to_r);
   } else {
-    if (!inverse) fft_pair_kernel<false, false><<<ctas, 256, smem, s>>>(mine, theirs, out, n, w4, side, (int)ppc, to_r);
-    else fft_pair_kernel<true, false><<<ctas, 256, smem, s>>>(mine, theirs, out, n, w4, side, (int)ppc, to_r);
+    if (!inverse) launch_k(fft_pair_kernel<false, false>, dim3(ctas), dim3(256), smem, s, mine, theirs, out, n, w4, side, (int)ppc, to_r);
+    else launch_k(fft_pair_kernel<true, false>, dim3(ctas), dim3(256), smem, s, mine, theirs, out, n, w4, side, (int)ppc, to_r);
   }
   FPM_LAUNCH_CHECK();
 }
@@ -949,7 +963,7 @@ void bfly_pair_device(uint4* mine, const uint4* theirs, uint64_t n, U128 w, int 
 void pointwise_device(const uint4* u, const uint4* v, uint4* out, size_t n, cudaStream_t s) {
   if (!n) return;
   const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms() * 16);
-  pointwise_kernel<<<grid, 256, 0, s>>>(u, v, out, n);
+  launch_k(pointwise_kernel, dim3(grid), dim3(256), 0, s, u, v, out, n);
   FPM_LAUNCH_CHECK();
 }
 

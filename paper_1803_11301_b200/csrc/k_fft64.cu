@@ -40,6 +40,7 @@ __device__ __forceinline__ uint2 twiddle64(const TwiddleSrc64& tw, unsigned i, u
 // R: elements in the tower representation (tower.cuh), the table built in R.
 template <bool INV, bool R>
 __global__ void __launch_bounds__(256) fft64_top_kernel(uint2* __restrict__ ev, unsigned i, int ppc, TwiddleSrc64 tw) {
+  pdl_wait();
   extern __shared__ uint2 tab64[];  // kG8Uint2
   __shared__ uint2 rows[kG8Rows];
   __shared__ uint2 to_r[72];
@@ -72,6 +73,7 @@ __global__ void __launch_bounds__(256) fft64_top_kernel(uint2* __restrict__ ev, 
     base[j] = u0;
     base[j + half] = u1;
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ two top layers per pass
@@ -83,6 +85,7 @@ constexpr size_t kTop4Smem64 = (3 * (size_t)kG8Uint2 + 3 * kG8Rows + 72) * sizeo
 template <bool INV, bool R>
 __global__ void __launch_bounds__(kTop4Threads64, 2) fft64_top4_kernel(uint2* __restrict__ ev, unsigned i, int qpc,
                                                                        TwiddleSrc64 tw) {
+  pdl_wait();
   extern __shared__ uint2 sm64[];
   uint2* t1 = sm64;                    // w(i+1, B); then w(i, 2B) at + kG8Uint2, w(i, 2B+1) at + 2 kG8Uint2
   uint2* rows = sm64 + 3 * kG8Uint2;   // 3 x kG8Rows
@@ -170,6 +173,7 @@ __global__ void __launch_bounds__(kTop4Threads64, 2) fft64_top4_kernel(uint2* __
     p[2 * h2] = make_uint4(a2.x, a2.y, b2.x, b2.y);
     p[3 * h2] = make_uint4(a3.x, a3.y, b3.x, b3.y);
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ tile layers (i < T)
@@ -293,6 +297,7 @@ __device__ __forceinline__ void tile_layers64(uint2* __restrict__ s, unsigned T,
 template <bool INV>
 __global__ void __launch_bounds__(256, 3) fft64_tile_kernel(uint2* __restrict__ ev, unsigned l, unsigned T,
                                                          TwiddleSrc64 tw, int use_tab) {
+  pdl_wait();
   extern __shared__ uint2 s64[];
   const int n = 1 << T;
   uint2* tab = use_tab ? s64 + n : nullptr;
@@ -305,10 +310,12 @@ __global__ void __launch_bounds__(256, 3) fft64_tile_kernel(uint2* __restrict__ 
     for (int k = threadIdx.x; k < n; k += blockDim.x) g[k] = s64[k];
     __syncthreads();
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 __global__ void __launch_bounds__(256, 3) fft64_tile_fused_kernel(const uint2* __restrict__ ea, uint2* __restrict__ eb,
                                                                unsigned l, unsigned T, TwiddleSrc64 tw, int use_tab) {
+  pdl_wait();
   extern __shared__ uint2 s64[];
   const int n = 1 << T;
   uint2* tab = use_tab ? s64 + n : nullptr;
@@ -325,6 +332,7 @@ __global__ void __launch_bounds__(256, 3) fft64_tile_fused_kernel(const uint2* _
     for (int k = threadIdx.x; k < n; k += blockDim.x) g[k] = s64[k];
     __syncthreads();
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // Both operands' tile layers in one CTA (shared tables / prepared twiddles), the pointwise product
@@ -332,6 +340,7 @@ __global__ void __launch_bounds__(256, 3) fft64_tile_fused_kernel(const uint2* _
 __global__ void __launch_bounds__(256, 3) fft64_tile_fused2_kernel(const uint2* __restrict__ ea,
                                                                    uint2* __restrict__ eb, unsigned l, unsigned T,
                                                                    TwiddleSrc64 tw) {
+  pdl_wait();
   extern __shared__ uint2 s64[];
   const int n = 1 << T;
   uint2* tab = s64 + 2 * n;
@@ -351,6 +360,7 @@ __global__ void __launch_bounds__(256, 3) fft64_tile_fused2_kernel(const uint2* 
     for (int k = threadIdx.x; k < n; k += blockDim.x) g[k] = s64[k];
     __syncthreads();
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 // ------------------------------------------------------------------ tower-representation tiles
@@ -481,6 +491,7 @@ size_t tower64_smem(unsigned T) { return 2 * ((size_t)1 << T) * sizeof(uint2) + 
 
 __global__ void __launch_bounds__(256, 3) fft64_tile_tower_kernel(const uint2* __restrict__ ea, uint2* __restrict__ eb,
                                                                   unsigned l, unsigned T, TwiddleSrc64 tw) {
+  pdl_wait();
   extern __shared__ uint2 s64[];
   const int n = 1 << T, tid = threadIdx.x, lane = tid & 31;
   TowerSmem64& sm = *reinterpret_cast<TowerSmem64*>(s64 + 2 * n);
@@ -536,12 +547,15 @@ __global__ void __launch_bounds__(256, 3) fft64_tile_tower_kernel(const uint2* _
     for (int k = tid; k < n; k += blockDim.x) g[k] = s64[tsw64(k)];
     __syncthreads();
   }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 __global__ void pointwise64_kernel(const uint2* __restrict__ u, const uint2* __restrict__ v, uint2* __restrict__ out,
                                    uint64_t n) {
+  pdl_wait();
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
     out[k] = gf64_mul(u[k], v[k]);
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
 int sms64() {
@@ -611,7 +625,7 @@ void butterfly64_tile_fused2_device(const uint2* ea, uint2* eb, unsigned l, unsi
   static PerDeviceOnce attr;
   attr.run([&] { set_smem64(fft64_tile_fused2_kernel, (2 * ((size_t)1 << 12) + kG8Uint2 + kG8Rows) * sizeof(uint2)); });
   const int grid = resident_grid(fft64_tile_fused2_kernel, 256, smem, ((uint64_t)1 << l) >> T);
-  fft64_tile_fused2_kernel<<<grid, 256, smem, s>>>(ea, eb, l, T, tw);
+  launch_k(fft64_tile_fused2_kernel, dim3(grid), dim3(256), smem, s, ea, eb, l, T, tw);
   FPM_LAUNCH_CHECK();
 }
 
@@ -631,7 +645,7 @@ void butterfly64_tile_tower_device(const uint2* ea, uint2* eb, unsigned l, unsig
   attr.run([&] { set_smem64(fft64_tile_tower_kernel, tower64_smem(12)); });
   const size_t smem = tower64_smem(T);
   const int grid = resident_grid(fft64_tile_tower_kernel, 256, smem, ((uint64_t)1 << l) >> T);
-  fft64_tile_tower_kernel<<<grid, 256, smem, s>>>(ea, eb, l, T, tw);
+  launch_k(fft64_tile_tower_kernel, dim3(grid), dim3(256), smem, s, ea, eb, l, T, tw);
   FPM_LAUNCH_CHECK();
 }
 
@@ -668,8 +682,8 @@ void top_passes64(uint2* ev, unsigned l, unsigned T, bool inverse, const Twiddle
   while (ppc > 256 && pairs / ppc < (uint64_t)sms64() * 2) ppc /= 2;
   auto radix2 = [&](unsigned i) {
     const uint64_t p = std::min<uint64_t>(ppc, (uint64_t)1 << i);
-    if (!inverse) fft64_top_kernel<false, R><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, i, (int)p, tw);
-    else fft64_top_kernel<true, R><<<(unsigned)(pairs / p), 256, smem, s>>>(ev, i, (int)p, tw);
+    if (!inverse) launch_k(fft64_top_kernel<false, R>, dim3((unsigned)(pairs / p)), dim3(256), smem, s, ev, i, (int)p, tw);
+    else launch_k(fft64_top_kernel<true, R>, dim3((unsigned)(pairs / p)), dim3(256), smem, s, ev, i, (int)p, tw);
     FPM_LAUNCH_CHECK();
   };
   const uint64_t quads = ((uint64_t)1 << l) / 4;
@@ -678,9 +692,9 @@ void top_passes64(uint2* ev, unsigned l, unsigned T, bool inverse, const Twiddle
   auto radix4 = [&](unsigned i) {
     const unsigned q = (unsigned)std::min<uint64_t>(qpc, (uint64_t)1 << i);
     if (!inverse)
-      fft64_top4_kernel<false, R><<<(unsigned)(quads / q), kTop4Threads64, kTop4Smem64, s>>>(ev, i, (int)q, tw);
+      launch_k(fft64_top4_kernel<false, R>, dim3((unsigned)(quads / q)), dim3(kTop4Threads64), kTop4Smem64, s, ev, i, (int)q, tw);
     else
-      fft64_top4_kernel<true, R><<<(unsigned)(quads / q), kTop4Threads64, kTop4Smem64, s>>>(ev, i, (int)q, tw);
+      launch_k(fft64_top4_kernel<true, R>, dim3((unsigned)(quads / q)), dim3(kTop4Threads64), kTop4Smem64, s, ev, i, (int)q, tw);
     FPM_LAUNCH_CHECK();
   };
   const unsigned n = l - T;
@@ -711,11 +725,9 @@ void butterfly64_tile_device(uint2* ev, unsigned l, unsigned T, bool inverse, co
   const TileCfg64 c = tile_cfg64(l, T);
   const uint64_t ntiles = ((uint64_t)1 << l) >> T;
   if (!inverse)
-    fft64_tile_kernel<false><<<resident_grid(fft64_tile_kernel<false>, c.threads, c.smem, ntiles), c.threads, c.smem, s>>>(
-        ev, l, T, tw, c.use_tab);
+    launch_k(fft64_tile_kernel<false>, dim3(resident_grid(fft64_tile_kernel<false>, c.threads, c.smem, ntiles)), dim3(c.threads), c.smem, s, ev, l, T, tw, c.use_tab);
   else
-    fft64_tile_kernel<true><<<resident_grid(fft64_tile_kernel<true>, c.threads, c.smem, ntiles), c.threads, c.smem, s>>>(
-        ev, l, T, tw, c.use_tab);
+    launch_k(fft64_tile_kernel<true>, dim3(resident_grid(fft64_tile_kernel<true>, c.threads, c.smem, ntiles)), dim3(c.threads), c.smem, s, ev, l, T, tw, c.use_tab);
   FPM_LAUNCH_CHECK();
 }
 
@@ -725,7 +737,7 @@ void butterfly64_tile_fused_device(const uint2* ea, uint2* eb, unsigned l, unsig
   attr.run([&] { set_smem64(fft64_tile_fused_kernel, kTileSmemMax64); });
   const TileCfg64 c = tile_cfg64(l, T);
   const int grid = resident_grid(fft64_tile_fused_kernel, c.threads, c.smem, ((uint64_t)1 << l) >> T);
-  fft64_tile_fused_kernel<<<grid, c.threads, c.smem, s>>>(ea, eb, l, T, tw, c.use_tab);
+  launch_k(fft64_tile_fused_kernel, dim3(grid), dim3(c.threads), c.smem, s, ea, eb, l, T, tw, c.use_tab);
   FPM_LAUNCH_CHECK();
 }
 
@@ -746,7 +758,7 @@ void butterfly64_device(uint2* ev, unsigned l, uint64_t base, bool inverse, cuda
 void pointwise64_device(const uint2* u, const uint2* v, uint2* out, size_t n, cudaStream_t s) {
   if (!n) return;
   const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sms64() * 16);
-  pointwise64_kernel<<<grid, 256, 0, s>>>(u, v, out, n);
+  launch_k(pointwise64_kernel, dim3(grid), dim3(256), 0, s, u, v, out, n);
   FPM_LAUNCH_CHECK();
 }
 
