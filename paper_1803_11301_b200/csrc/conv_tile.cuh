@@ -53,17 +53,12 @@ template <bool INV>
 __device__ __forceinline__ void l1_tile(uint32_t (&m)[8], uint32_t* sc, int g, int d) {
   const int tid = threadIdx.x;
   uint32_t* my = sc + tid * kScPitch;
-  uint32_t W[16];
   const int ws = d >> 5, bs = d & 31;
-  // skew: W = m << d, in registers
-  {
-    uint32_t t[16];
+  // skew: the row m << d -- the bit part (bs) in registers, the word part (ws) as the store offset
+  // into the 16-word shared row (no register shuffling)
+  uint32_t W9[9];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) t[i] = i < 8 ? m[i] : 0u;
-    words_shl16(t, ws);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) W[i] = __funnelshift_l(i ? t[i - 1] : 0u, t[i], bs);
-  }
+  for (int i = 0; i < 9; ++i) W9[i] = __funnelshift_l(i ? m[i - 1] : 0u, i < 8 ? m[i] : 0u, bs);
   // subset-zeta over the g low row bits (rows with bit b clear ^= row | 2^b), as register-local
   // stages in two transposed mappings with shared-memory exchanges (row-major sc, pitch 17):
   //   A: thread (c = tid & 15, r0 = tid >> 4) holds word c of rows r0 + 16k -> row bits 4..7 local
@@ -74,7 +69,9 @@ __device__ __forceinline__ void l1_tile(uint32_t (&m)[8], uint32_t* sc, int g, i
     uint32_t v[16];
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < 16; ++i) my[i] = W[i];
+    for (int i = 0; i < 16; ++i) my[i] = 0u;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) my[ws + i] = W9[i];
     __syncthreads();
     if (g > 4) {
 #pragma unroll
@@ -102,14 +99,16 @@ __device__ __forceinline__ void l1_tile(uint32_t (&m)[8], uint32_t* sc, int g, i
 #pragma unroll
     for (int k = 0; k < 16; ++k) sc[(16 * rr + k) * kScPitch + c] = v[k];
     __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 16; ++i) W[i] = my[i];
   }
-  // unskew: G = W >> d, in registers
+  // unskew: G = (skewed row) >> d -- the word part as the load offset, the bit part in registers
   uint32_t G[16];
-  words_shr16(W, ws);
+  {
+    uint32_t U[17];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) G[i] = __funnelshift_r(W[i], i < 15 ? W[i + 1] : 0u, bs);
+    for (int j = 0; j < 17; ++j) U[j] = j + ws < 16 ? my[j + ws] : 0u;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) G[i] = __funnelshift_r(U[i], U[i + 1], bs);
+  }
   // carry (forward) / overflow (inverse) with the previous row's high half H_{d-1}
   __syncthreads();
 #pragma unroll
