@@ -127,8 +127,8 @@ constexpr int kZW = 32;
 constexpr int kZP = 36;  // shared row pitch (16 B aligned, conflict-free for both mappings)
 // BITSKEW: the bit-granular skew path (neighbour words by shuffle) needs the registers of 2 CTAs/SM;
 // word-aligned or no skew runs at 3 CTAs/SM.
-template <bool BITSKEW>
-__global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32_t* __restrict__ src, uint64_t src_pitch,
+template <bool BITSKEW, bool FULL = false>  // FULL: bit skew over complete 256-row groups (nb = 8)
+__global__ void __launch_bounds__(256, BITSKEW ? (FULL ? 3 : 2) : 4) zeta_kernel(const uint32_t* __restrict__ src, uint64_t src_pitch,
                                                    uint32_t* __restrict__ dst, uint64_t dst_pitch, uint64_t D,
                                                    int b0, int nb, Skew skew, uint64_t src_row_words,
                                                    uint64_t windows) {
@@ -174,10 +174,10 @@ __global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32
       // R (so d, wi, the shift) is warp-uniform: one coalesced word per lane and row, all rows'
       // loads in flight at once (lane 31 also fetches the word after the window), then the
       // neighbour word comes by shuffle and a funnel shift aligns the window.
-      uint32_t e[32];
-      int sh[32];
-      if (nb == 8) {
-        // full group: skew bits affine in the row (d & 255 = R, base 256-aligned): per load one add
+      if (FULL) {
+        // full group: skew bits affine in the row (d & 255 = R, base 256-aligned): per load one add.
+        // The word after row k's window (lane 31's funnel input) is loaded by lane k and
+        // broadcast: one register instead of 32 (and the shifts recomputed), for the occupancy.
         const uint64_t dstep = (uint64_t)8 << b0;
         const uint64_t d0 = base + ((uint64_t)(tid >> 5) << b0);
         const int64_t s0 = (int64_t)(((d0 >> skew.lo) & skew.mask) << skew.log);
@@ -185,17 +185,25 @@ __global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32
         // 32-bit window arithmetic (rows < 2^31 bits); one unsigned compare bounds a word index
         const int32_t pos0 = (int32_t)((int64_t)(wb * 32 * kZW) - s0), ss = (int32_t)sstep;
         const uint32_t rows_w = (uint32_t)src_row_words;
-        const uint32_t* row = src + d0 * src_pitch;
+        const uint32_t* row0 = src + d0 * src_pitch;
         const uint64_t rstep = dstep * src_pitch;
+        const uint32_t* row = row0;
 #pragma unroll
         for (int k = 0; k < 32; ++k, row += rstep) {
-          const int32_t pos = pos0 - k * ss;
-          const uint32_t iw = (uint32_t)((pos >> 5) + c);
-          sh[k] = pos & 31;
+          const uint32_t iw = (uint32_t)(((pos0 - k * ss) >> 5) + c);
           a[k] = iw < rows_w ? __ldg(row + iw) : 0u;
-          e[k] = (c == 31 && iw + 1 < rows_w) ? __ldg(row + iw + 1) : 0u;
+        }
+        const uint32_t iwe = (uint32_t)(((pos0 - c * ss) >> 5) + 32);
+        const uint32_t ext = iwe < rows_w ? __ldg(row0 + c * rstep + iwe) : 0u;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const uint32_t nx = __shfl_down_sync(0xFFFFFFFFu, a[k], 1);
+          const uint32_t ek = __shfl_sync(0xFFFFFFFFu, ext, k);
+          a[k] = __funnelshift_r(a[k], c == 31 ? ek : nx, (pos0 - k * ss) & 31);
         }
       } else {
+      uint32_t e[32];
+      int sh[32];
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         const int R = (tid >> 5) + 8 * k;
@@ -209,11 +217,11 @@ __global__ void __launch_bounds__(256, BITSKEW ? 2 : 4) zeta_kernel(const uint32
         a[k] = (ok && iw >= 0 && iw < (int64_t)src_row_words) ? __ldg(row + iw) : 0u;
         e[k] = (ok && c == 31 && iw + 1 >= 0 && iw + 1 < (int64_t)src_row_words) ? __ldg(row + iw + 1) : 0u;
       }
-      }
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
         const uint32_t nx = __shfl_down_sync(0xFFFFFFFFu, a[k], 1);
         a[k] = __funnelshift_r(a[k], c == 31 ? e[k] : nx, sh[k]);
+      }
       }
     } else {
 #pragma unroll
@@ -1221,7 +1229,10 @@ void zeta(const uint32_t* src, uint64_t src_pitch, uint32_t* dst, uint64_t dst_p
   const int wpc = 256 >> nb;
   const uint64_t items = (D >> nb) * ((windows + wpc - 1) / wpc);
   if (skew.mask && skew.log < 5)
-    launch_k(zeta_kernel<true>, dim3(grid_cap(items, 4)), dim3(256), 256 * kZP * sizeof(uint32_t), s, src, src_pitch, dst, dst_pitch, D, b0, nb, skew, src_row_words, windows);
+    if (nb == 8)
+      launch_k(zeta_kernel<true, true>, dim3(grid_cap(items, 3)), dim3(256), 256 * kZP * sizeof(uint32_t), s, src, src_pitch, dst, dst_pitch, D, b0, nb, skew, src_row_words, windows);
+    else
+      launch_k(zeta_kernel<true>, dim3(grid_cap(items, 4)), dim3(256), 256 * kZP * sizeof(uint32_t), s, src, src_pitch, dst, dst_pitch, D, b0, nb, skew, src_row_words, windows);
   else
     launch_k(zeta_kernel<false>, dim3(grid_cap(items, 4)), dim3(256), 256 * kZP * sizeof(uint32_t), s, src, src_pitch, dst, dst_pitch, D, b0, nb, skew, src_row_words, windows);
   FPM_LAUNCH_CHECK();
