@@ -441,21 +441,24 @@ struct TowerSmem {  // after the 2^(T+1) tile elements
 __device__ __forceinline__ int tsw(int k) { return k ^ (((k >> 3) & 1) * 7); }
 
 // Index in wz of (layer i, group g): layers ascending.
-__device__ __forceinline__ int tower_wz_index(unsigned T, unsigned i, int g) {
+__host__ __device__ constexpr int tower_wz_index(unsigned T, unsigned i, int g) {
   int k = 0;
   for (unsigned u = 0; u < i; ++u) k += tower_groups(T, u);
   return k + g;
 }
 
-// Layers [P, T) of the tile on R elements (forward: T-1 down to P; inverse: P up to T-1).
-template <bool INV, int NT>
-__device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, unsigned T, unsigned P, TowerSmem& sm) {
-  const int npairs = 1 << (T - 1), n = 1 << T, tid = threadIdx.x, q = tid & 7;
-  const int first = tower_wz_index(T, P, 0), ntab = tower_tables(T) - first;
+// Layers [P, T) of the tile on R elements (forward: T-1 down to P; inverse: P up to T-1).  T and P
+// are compile-time constants and the layer / group loops unroll, so every table index, block shift
+// and pair count below folds to an immediate.
+template <bool INV, int NT, unsigned T, unsigned P>
+__device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, TowerSmem& sm) {
+  constexpr int npairs = 1 << (T - 1), n = 1 << T;
+  constexpr int ntab = tower_tables(T) - tower_wz_index(T, P, 0);
+  const int tid = threadIdx.x, q = tid & 7;
   // table sequence k = 0..ntab-1: forward = wz descending by layer (h ascending within a layer),
   // inverse = wz ascending
-  auto wz_of = [&](int k) -> int {
-    if (INV) return first + k;
+  constexpr auto wz_of = [](int k) constexpr -> int {
+    if (INV) return tower_wz_index(T, P, 0) + k;
     int kk = 0;
     for (int i = (int)T - 1; i >= (int)P; --i) {
       const int g = tower_groups(T, (unsigned)i);
@@ -469,10 +472,12 @@ __device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, unsigned T,
   m8_expand(sm.tab, sm.rows[0], tid);
   __syncthreads();
   int k = 0;
+#pragma unroll
   for (unsigned step = 0; step < T - P; ++step) {
     const unsigned i = INV ? P + step : T - 1 - step;
     const int nblk = npairs >> i;
     const int lg = (nblk < 128 ? T - 1 : 7 + i);  // log2(pairs per table per tile)
+#pragma unroll
     for (int h = 0; h < nblk; h += 128, ++k) {
       if (k + 1 < ntab) rows_r<true>(sm.rows[(k + 1) & 1], sm.wz[wz_of(k + 1)], tid, sm.to_r);
       const M8Base mb = m8_base(sm.tab, q);
@@ -569,9 +574,10 @@ size_t tower_smem(unsigned T) { return 2 * ((size_t)1 << T) * sizeof(uint4) + si
 #ifndef FPM_TOWER_MINB
 #define FPM_TOWER_MINB 2
 #endif
+template <unsigned T>
 __global__ void __launch_bounds__(kTowerThreads, FPM_TOWER_MINB) fft_tile_tower_kernel(const uint4* __restrict__ ea,
                                                                           uint4* __restrict__ eb, unsigned l,
-                                                                          unsigned T, TwiddleSrc tw) {
+                                                                          TwiddleSrc tw) {
   pdl_wait();
   extern __shared__ uint4 s[];
   const int n = 1 << T, tid = threadIdx.x, q = tid & 7;
@@ -597,7 +603,7 @@ __global__ void __launch_bounds__(kTowerThreads, FPM_TOWER_MINB) fft_tile_tower_
       s[n + tsw(k)] = g[k];
     }
     __syncthreads();
-    tile_layers_r<false, 2>(s, T, kPolyLayers, sm);
+    tile_layers_r<false, 2, T, kPolyLayers>(s, sm);
     m8_expand(sm.tab, sm.rows_to_poly, tid);
     __syncthreads();
     const M8Base mb = m8_base(sm.tab, q);
@@ -645,7 +651,7 @@ __global__ void __launch_bounds__(kTowerThreads, FPM_TOWER_MINB) fft_tile_tower_
       }
     }
     // (tile_layers_r's first barrier orders these stores before its butterflies)
-    tile_layers_r<true, 1>(s, T, kPolyLayers, sm);
+    tile_layers_r<true, 1, T, kPolyLayers>(s, sm);
     for (int k = tid; k < n; k += blockDim.x) g[k] = s[tsw(k)];
     __syncthreads();
   }
@@ -910,10 +916,14 @@ void butterfly_tile_tower_device(const uint4* ea, uint4* eb, unsigned l, unsigne
                                  cudaStream_t s) {
   if (T < 10 || T > 11 || l < T) throw Error(kInvalid, "tower tile pass: T must be 10 or 11");
   static PerDeviceOnce attr;
-  attr.run([&] { set_smem(fft_tile_tower_kernel, tower_smem(11)); });
+  attr.run([&] {
+    set_smem(fft_tile_tower_kernel<10>, tower_smem(10));
+    set_smem(fft_tile_tower_kernel<11>, tower_smem(11));
+  });
   const size_t smem = tower_smem(T);
-  const int grid = resident_grid(fft_tile_tower_kernel, kTowerThreads, smem, ((uint64_t)1 << l) >> T);
-  launch_k(fft_tile_tower_kernel, dim3(grid), dim3(kTowerThreads), smem, s, ea, eb, l, T, tw);
+  auto kern = T == 10 ? fft_tile_tower_kernel<10> : fft_tile_tower_kernel<11>;
+  const int grid = resident_grid(kern, kTowerThreads, smem, ((uint64_t)1 << l) >> T);
+  launch_k(kern, dim3(grid), dim3(kTowerThreads), smem, s, ea, eb, l, tw);
   FPM_LAUNCH_CHECK();
 }
 
