@@ -179,7 +179,7 @@ struct Gf128Ops {
   static unsigned tile_log2(unsigned l) { return pipeline_tile_log2(l); }
   // The fused pass on tower-representation tiles (tower.cuh); then encode, the top passes and
   // decode work in R as well.
-  static bool tower(unsigned T) { return tile_fused2_enabled(T) && tile_tower_enabled(T); }
+  static bool tower(unsigned T) { return pipeline_tower(T); }
   static void encode(const uint32_t* p, unsigned l, E* ev, cudaStream_t s, bool r) {
     encode_device_rows(p, l, ev, kLiveRows, s, r);
   }
@@ -194,7 +194,7 @@ struct Gf128Ops {
     butterfly_tile_fused_device(ea, eb, l, T, tw, s);
   }
   // both operands' tile layers in the fused pass (no separate tile pass of operand a)
-  static bool fuse_ab(unsigned T) { return tile_fused2_enabled(T); }
+  static bool fuse_ab(unsigned T) { return pipeline_fuses_operands(T); }
   static void fused2(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s, bool r) {
     if (r) butterfly_tile_tower_device(ea, eb, l, T, tw, s);
     else butterfly_tile_fused2_device(ea, eb, l, T, tw, s);
@@ -702,7 +702,7 @@ const char* fpm_version(void) { return "fpmul_b200 0.1 (sm_100a)"; }
 unsigned fpm_fft_tile_log2(unsigned l) { return fpm::pipeline_tile_log2(l); }
 int fpm_pipeline_fuses_operands(unsigned l) {
   const unsigned T = fpm::pipeline_tile_log2(l);
-  return l >= 18 && T > 0 && fpm::tile_fused2_enabled(T) ? 1 : 0;
+  return l >= 18 && T > 0 && fpm::pipeline_fuses_operands(T) ? 1 : 0;
 }
 int fpm_device_count(void) {
   int n = 0;
@@ -932,7 +932,7 @@ fpm_status fpm_decode_cols_dev(const uint64_t* d_ev, size_t ncols, uint64_t* d_s
 
 int fpm_shard_tower(unsigned l) {
   const unsigned T = pipeline_tile_log2(l);
-  return l >= 18 && l < 64 && tile_fused2_enabled(T) && tile_tower_enabled(T) ? 1 : 0;
+  return l >= 18 && l < 64 && pipeline_tower(T) ? 1 : 0;
 }
 
 fpm_status fpm_encode_cols_r_dev(const uint64_t* d_poly, unsigned l, size_t col0, size_t ncols, int rows_live,

@@ -270,6 +270,8 @@ void butterfly_tile_fused2_device(const uint4* ea, uint4* eb, unsigned l, unsign
 // The same pass on tower-representation tiles (fft_tile_tower_kernel): every tile layer as one M8
 // table of the tile's twiddle plus a GF(2^8)-scalar product for the per-block part; T in [10, 11].
 bool tile_tower_enabled(unsigned T);
+bool pipeline_fuses_operands(unsigned T);  // both operands' tile layers in one pass at depth T
+bool pipeline_tower(unsigned T);           // ... on tower-representation tiles
 void butterfly_tile_tower_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
                                  cudaStream_t s);
 void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,

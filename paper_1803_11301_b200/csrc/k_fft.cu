@@ -423,7 +423,7 @@ __host__ __device__ constexpr int tower_tables(unsigned T) {
   for (unsigned i = 0; i < T; ++i) n += tower_groups(T, i);
   return n;
 }
-constexpr int kTowerMaxTables = tower_tables(11);  // 22
+constexpr int kTowerMaxTables = tower_tables(12);  // 38
 
 struct TowerSmem {  // after the 2^(T+1) tile elements
   uint4 tab[kM8Uint4];
@@ -439,6 +439,11 @@ struct TowerSmem {  // after the 2^(T+1) tile elements
 // distance 1, 2, 4) then reach eight distinct 16-byte bank groups per quarter-warp (2-way bank
 // conflicts otherwise); contiguous runs of 8 stay contiguous.
 __device__ __forceinline__ int tsw(int k) { return k ^ (((k >> 3) & 1) * 7); }
+
+// CTA shape per tile depth: T <= 11 -> 256 threads, 2 CTAs/SM (<= 140 KiB of shared memory each at
+// T = 10); T = 12 (two 64 KiB tiles + the 64 KiB table, 207 KiB) -> 512 threads, 1 CTA/SM.
+__host__ __device__ constexpr int tower_threads(unsigned T) { return T >= 12 ? 512 : 256; }
+__host__ __device__ constexpr int tower_min_blocks(unsigned T) { return T >= 12 ? 1 : 2; }
 
 // Index in wz of (layer i, group g): layers ascending.
 __host__ __device__ constexpr int tower_wz_index(unsigned T, unsigned i, int g) {
@@ -481,13 +486,23 @@ __device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, TowerSmem& 
     for (int h = 0; h < nblk; h += 128, ++k) {
       if (k + 1 < ntab) rows_r<true>(sm.rows[(k + 1) & 1], sm.wz[wz_of(k + 1)], tid, sm.to_r);
       const M8Base mb = m8_base(sm.tab, q);
-      // warps 0-3 computed the next table's rows: they take one pair fewer than warps 4-7 (c = pairs
-      // per thread: threads 128..255 do c + 1, threads 0..127 do c - 1; consecutive threads keep
-      // consecutive pairs)
-      const int c = (NT << lg) >> 8;
-      const int pp0 = tid >= 128 ? tid - 128 : 128 * (c + 1) + tid, cnt = tid >= 128 ? c + 1 : c - 1;
+      // warps 0-3 computed the next table's rows: they take one pair fewer (c = pairs per thread:
+      // threads 128..255 do c + 1, threads 0..127 do c - 1, threads >= 256 of a larger CTA do c;
+      // consecutive threads keep consecutive pairs).  Fewer pairs than threads: threads >= 128 only.
+      constexpr int NTH = tower_threads(T);
+      const int total = NT << lg, c = total / NTH;
+      int pp0, cnt, stride;
+      if (c == 0) {
+        pp0 = tid - 128, stride = 0, cnt = tid >= 128 && tid - 128 < total ? 1 : 0;
+      } else if (tid < 128) {
+        pp0 = 128 * (c + 1) + tid, stride = 128, cnt = c - 1;
+      } else if (tid < 256) {
+        pp0 = tid - 128, stride = 128, cnt = c + 1;
+      } else {
+        pp0 = 256 * c + tid - 256, stride = NTH - 256, cnt = c;
+      }
       for (int r = 0; r < cnt; ++r) {
-        const int pp = pp0 + 128 * r;
+        const int pp = pp0 + stride * r;
         const int p = pp & ((1 << lg) - 1), tt = pp >> lg;
         const int blk = h + (p >> i), j = p & ((1 << i) - 1);
         const int i0 = (blk << (i + 1)) + j + tt * n, i1 = i0 + (1 << i);
@@ -558,29 +573,23 @@ __device__ __forceinline__ void tile_layers_poly(uint4* __restrict__ s, unsigned
   }
 }
 
-#ifndef FPM_TOWER_THREADS
-#define FPM_TOWER_THREADS 256
-#endif
 #ifndef FPM_TOWER_POLY
 #define FPM_TOWER_POLY 1
 #endif
 constexpr unsigned kPolyLayers = FPM_TOWER_POLY;  // bottom tile layers in polynomial representation
-constexpr int kTowerThreads = FPM_TOWER_THREADS;
 size_t tower_smem(unsigned T) { return 2 * ((size_t)1 << T) * sizeof(uint4) + sizeof(TowerSmem); }
 
 // fft_tile_fused2_kernel on R tiles: forward layers [0, T) of both operands (one table per layer
 // serves both tiles), the pointwise product (R -> poly by an M8 table of to_poly, gf_mul, poly -> R
 // by an M8 table of to_r) and the inverse layers [0, T).
-#ifndef FPM_TOWER_MINB
-#define FPM_TOWER_MINB 2
-#endif
 template <unsigned T>
-__global__ void __launch_bounds__(kTowerThreads, FPM_TOWER_MINB) fft_tile_tower_kernel(const uint4* __restrict__ ea,
+__global__ void __launch_bounds__(tower_threads(T), tower_min_blocks(T)) fft_tile_tower_kernel(const uint4* __restrict__ ea,
                                                                           uint4* __restrict__ eb, unsigned l,
                                                                           TwiddleSrc tw) {
   pdl_wait();
   extern __shared__ uint4 s[];
-  const int n = 1 << T, tid = threadIdx.x, q = tid & 7;
+  constexpr int n = 1 << T;
+  const int tid = threadIdx.x, q = tid & 7;
   TowerSmem& sm = *reinterpret_cast<TowerSmem*>(s + 2 * n);
   smul_tabs_build(sm.stab, tw.tau, tid);
   if (tid < 128) {
@@ -645,9 +654,11 @@ __global__ void __launch_bounds__(kTowerThreads, FPM_TOWER_MINB) fft_tile_tower_
     {  // the next tile's operands into L2 while this tile's inverse layers run (128-byte lines)
       const uint64_t tn = t + gridDim.x;
       if (tn < ntiles) {
-        const int lines = n * 16 / 128;
-        const char* p = reinterpret_cast<const char*>((tid < lines ? ea : eb) + (tn << T)) + 128 * (tid % lines);
-        if (tid < 2 * lines) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        constexpr int lines = n * 16 / 128;
+        for (int k = tid; k < 2 * lines; k += blockDim.x) {
+          const char* p = reinterpret_cast<const char*>((k < lines ? ea : eb) + (tn << T)) + 128 * (k % lines);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        }
       }
     }
     // (tile_layers_r's first barrier orders these stores before its butterflies)
@@ -740,10 +751,16 @@ unsigned fft_tile_log2(unsigned l) {
 // The product pipeline's tile depth: with both operands' tile layers fused (fft_tile_fused2_kernel,
 // two 2^T tiles + tables per CTA) T = 10 keeps two CTAs per SM (2^32-bit product: 57.5 ms, vs
 // 57.7 unfused at T = 11 and 60.1 fused at T = 11 with one CTA per SM).
+// Round 2: on tower tiles, T = 12 (one 512-thread CTA per SM, 2^10 or more tiles) moves two layers
+// out of the HBM-bound radix-4 passes and shares each layer-(>= 4) table over 4096 positions
+// (2^32-bit product: 49.25 -> 46.97 ms).
 unsigned pipeline_tile_log2(unsigned l) {
+  if (!tile_log2_knob() && l >= 22 && tile_tower_enabled(12)) return 12;
   if (!tile_log2_knob() && l >= 20 && tile_fused2_enabled(10)) return 10;
   return fft_tile_log2(l);
 }
+bool pipeline_fuses_operands(unsigned T) { return tile_fused2_enabled(T) || (T == 12 && tile_tower_enabled(12)); }
+bool pipeline_tower(unsigned T) { return pipeline_fuses_operands(T) && tile_tower_enabled(T); }
 
 TwiddleSrc make_twiddle_src(int device, unsigned l, U128 base) {
   if (l > (unsigned)kMaxLayers) throw Error(kInvalid, "butterfly: too many layers");
@@ -909,21 +926,22 @@ bool tile_tower_enabled(unsigned T) {
     const char* e = std::getenv("FPM_TOWER");
     return !(e && e[0] == '0');
   }();
-  return on && T >= 10 && T <= 11;
+  return on && T >= 10 && T <= 12;
 }
 
 void butterfly_tile_tower_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
                                  cudaStream_t s) {
-  if (T < 10 || T > 11 || l < T) throw Error(kInvalid, "tower tile pass: T must be 10 or 11");
+  if (T < 10 || T > 12 || l < T) throw Error(kInvalid, "tower tile pass: T must be 10, 11 or 12");
   static PerDeviceOnce attr;
   attr.run([&] {
     set_smem(fft_tile_tower_kernel<10>, tower_smem(10));
     set_smem(fft_tile_tower_kernel<11>, tower_smem(11));
+    set_smem(fft_tile_tower_kernel<12>, tower_smem(12));
   });
   const size_t smem = tower_smem(T);
-  auto kern = T == 10 ? fft_tile_tower_kernel<10> : fft_tile_tower_kernel<11>;
-  const int grid = resident_grid(kern, kTowerThreads, smem, ((uint64_t)1 << l) >> T);
-  launch_k(kern, dim3(grid), dim3(kTowerThreads), smem, s, ea, eb, l, tw);
+  auto kern = T == 10 ? fft_tile_tower_kernel<10> : T == 11 ? fft_tile_tower_kernel<11> : fft_tile_tower_kernel<12>;
+  const int grid = resident_grid(kern, tower_threads(T), smem, ((uint64_t)1 << l) >> T);
+  launch_k(kern, dim3(grid), dim3(tower_threads(T)), smem, s, ea, eb, l, tw);
   FPM_LAUNCH_CHECK();
 }
 
