@@ -431,7 +431,8 @@ struct TowerSmem {  // after the 2^(T+1) tile elements
   uint4 to_r[128 + 8];        // rows_r conversion source, to_r_pad layout
   uint4 rows_to_r[144];       // m8 rows of poly -> R
   uint4 rows_to_poly[144];    // m8 rows of R -> poly
-  uint4 wz[kTowerMaxTables];  // table twiddles of the current tile, layer-ascending, h ascending
+  uint4 wz[kTowerMaxTables];   // table twiddles of the current tile, layer-ascending, h ascending
+  uint4 wzf[kTowerMaxTables];  // the same in the forward sequence (layers descending, h ascending)
   SmulTabs stab;              // subfield twiddle parts d(b) = R(C2P(2b)), b < 128 (tower.cuh)
 };
 
@@ -460,19 +461,11 @@ __device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, TowerSmem& 
   constexpr int npairs = 1 << (T - 1), n = 1 << T;
   constexpr int ntab = tower_tables(T) - tower_wz_index(T, P, 0);
   const int tid = threadIdx.x, q = tid & 7;
-  // table sequence k = 0..ntab-1: forward = wz descending by layer (h ascending within a layer),
-  // inverse = wz ascending
-  constexpr auto wz_of = [](int k) constexpr -> int {
-    if (INV) return tower_wz_index(T, P, 0) + k;
-    int kk = 0;
-    for (int i = (int)T - 1; i >= (int)P; --i) {
-      const int g = tower_groups(T, (unsigned)i);
-      if (k < kk + g) return tower_wz_index(T, (unsigned)i, k - kk);
-      kk += g;
-    }
-    return 0;
-  };
-  rows_r<true>(sm.rows[0], sm.wz[wz_of(0)], tid, sm.to_r);
+  // table sequence k = 0..ntab-1: forward = wzf[k] (layers descending, h ascending), inverse =
+  // wz[first + k] (layers ascending)
+  constexpr int first = tower_wz_index(T, P, 0);
+  auto wz_of = [&](int k) -> const uint4& { return INV ? sm.wz[first + k] : sm.wzf[k]; };
+  rows_r<true>(sm.rows[0], wz_of(0), tid, sm.to_r);
   __syncthreads();
   m8_expand(sm.tab, sm.rows[0], tid);
   __syncthreads();
@@ -484,7 +477,7 @@ __device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, TowerSmem& 
     const int lg = (nblk < 128 ? T - 1 : 7 + i);  // log2(pairs per table per tile)
 #pragma unroll
     for (int h = 0; h < nblk; h += 128, ++k) {
-      if (k + 1 < ntab) rows_r<true>(sm.rows[(k + 1) & 1], sm.wz[wz_of(k + 1)], tid, sm.to_r);
+      if (k + 1 < ntab) rows_r<true>(sm.rows[(k + 1) & 1], wz_of(k + 1), tid, sm.to_r);
       const M8Base mb = m8_base(sm.tab, q);
       // warps 0-3 computed the next table's rows: they take one pair fewer (c = pairs per thread:
       // threads 128..255 do c + 1, threads 0..127 do c - 1, threads >= 256 of a larger CTA do c;
@@ -605,7 +598,13 @@ __global__ void __launch_bounds__(tower_threads(T), tower_min_blocks(T)) fft_til
     if (tid < ntab) {  // wz[k]: layer i, group h of this tile: Z(i) ^ C2P(2 * 128 h)
       int i = 0, kk = tid;
       while (kk >= tower_groups(T, (unsigned)i)) kk -= tower_groups(T, (unsigned)i++);
-      sm.wz[tid] = x4(twiddle(tw, l, (unsigned)i, t << (T - 1 - i)), c2p2(tw.c2p, (uint64_t)kk << 7));
+      const uint4 w = x4(twiddle(tw, l, (unsigned)i, t << (T - 1 - i)), c2p2(tw.c2p, (uint64_t)kk << 7));
+      sm.wz[tid] = w;
+      if (i >= (int)kPolyLayers) {  // forward sequence position: the groups of the layers above i first
+        int pos = kk;
+        for (int u = (int)T - 1; u > i; --u) pos += tower_groups(T, (unsigned)u);
+        sm.wzf[pos] = w;
+      }
     }
     for (int k = tid; k < n; k += blockDim.x) {
       s[tsw(k)] = ga[k];
