@@ -400,6 +400,311 @@ __global__ void __launch_bounds__(256) overflow_kernel(const uint32_t* __restric
   pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
+// ------------------------------------------------------------------ L1_inner + T_r, one pipelined pass
+// The chunk-local step L1_inner (256-row skewed zeta, zeta_kernel) and the per-row T_r (carry +
+// conv(2^16), carry_rows_kernel; inverse: conv_rows, zeta, overflow) in ONE persistent kernel whose
+// CTAs claim work items in a fixed order from an atomic counter: per chunk c (256 rows of 2^16
+// bits), Z(c) = its 65 zeta windows and C(c) = its 256 rows, interleaved with a lag of kPipeLag
+// chunks (forward: Z(0) Z(1) [Z(2) C(0)] [Z(3) C(1)] ...; inverse R(c) = the rows' conv^-1 first,
+// then Z, then O = the overflow rows).  A consumer item waits (spinning on a per-chunk counter) for
+// its chunk's producer items, which were all claimed before it: claimed items only ever wait on
+// earlier claims, so the pipeline makes progress with any number of resident CTAs (no co-residency
+// assumption, safe next to other kernels).  The skewed rows live in a ring of kPipeSlots chunk
+// slots (16 MiB instead of a 520 MiB scratch array) that stays in L2: HBM sees one read and one
+// write of the block instead of three of each.
+#ifndef FPM_PIPE_LAG
+#define FPM_PIPE_LAG 8
+#endif
+constexpr int kPipeLag = FPM_PIPE_LAG;  // chunks between a chunk's producer and consumer items
+constexpr int kPipeSlots = 2 * FPM_PIPE_LAG;  // skewed-row ring (chunks); > kPipeLag
+constexpr int kPipeZW = 65;    // zeta windows per skewed row: (2^16 + 1024) / 1024
+constexpr int kPipeORows = 4;  // overflow rows per item (inverse, no T_r^-1)
+constexpr uint64_t kPipeP1 = (kT + 32 * kZW) / 32;  // skewed row pitch (words)
+#ifndef FPM_PIPE_CTAS
+#define FPM_PIPE_CTAS 3
+#endif
+constexpr int kPipeCtas = FPM_PIPE_CTAS;  // CTAs per SM
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// thread 0 waits until *cnt >= target, then the whole CTA proceeds
+__device__ __forceinline__ void pipe_wait(const int* cnt, int target) {
+  if (threadIdx.x == 0)
+    while (ld_acquire(cnt) < target) __nanosleep(64);
+  __syncthreads();
+}
+// after the item's stores (all threads): publish `units` of progress on *cnt (release: the CTA's
+// stores, ordered before it by the barrier, are visible to whoever acquires the count)
+__device__ __forceinline__ void pipe_done(int* cnt, int units = 1) {
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(cnt), "r"(units) : "memory");
+}
+
+// One L1_inner window: rows j < 256 of a chunk (src, pitch kTWords) skewed left by j bits, words
+// [32 wb, 32 wb + 32) of the skewed rows, superset zeta over j -> dst rows (pitch kPipeP1).  The
+// full-group bit-skew path of zeta_kernel<true, true> with the group fixed to one chunk.  CG: load
+// through L2 only (src written by another CTA of the same kernel).
+template <bool CG>
+__device__ __forceinline__ void pipe_zeta_item(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, int wb,
+                                               uint32_t* sx) {
+  const int tid = threadIdx.x, c = tid & 31, j0 = tid >> 5;
+  auto ld = [](const uint32_t* p) { return CG ? __ldcg(p) : __ldg(p); };
+  uint32_t a[32];
+  {
+    const int32_t pos0 = wb * 32 * kZW - j0;  // skew of row j0 + 8k: j0 + 8k bits
+    const uint32_t* row0 = src + (uint64_t)j0 * kTWords;
+    constexpr uint64_t rstep = 8 * (uint64_t)kTWords;
+    const uint32_t* row = row0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k, row += rstep) {
+      const uint32_t iw = (uint32_t)(((pos0 - 8 * k) >> 5) + c);
+      a[k] = iw < (uint32_t)kTWords ? ld(row + iw) : 0u;
+    }
+    const uint32_t iwe = (uint32_t)(((pos0 - 8 * c) >> 5) + 32);
+    const uint32_t ext = iwe < (uint32_t)kTWords ? ld(row0 + c * rstep + iwe) : 0u;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const uint32_t nx = __shfl_down_sync(0xFFFFFFFFu, a[k], 1);
+      const uint32_t ek = __shfl_sync(0xFFFFFFFFu, ext, k);
+      a[k] = __funnelshift_r(a[k], c == 31 ? ek : nx, (pos0 - 8 * k) & 31);
+    }
+  }
+#pragma unroll
+  for (int b = 3; b < 8; ++b) {
+    const int kb = 1 << (b - 3);
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      if (!(k & kb)) a[k] ^= a[k | kb];
+  }
+#pragma unroll
+  for (int k = 0; k < 32; ++k) sx[(j0 + 8 * k) * kZP + c] = a[k];
+  __syncthreads();
+  const int q = tid & 7, R0 = 8 * (tid >> 3);
+  uint4 bq[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) bq[k] = *reinterpret_cast<const uint4*>(sx + (R0 + k) * kZP + 4 * q);
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (!(k & (1 << b))) bq[k] = x4v(bq[k], bq[k | (1 << b)]);
+  uint32_t* p = dst + (uint64_t)R0 * kPipeP1 + wb * kZW + 4 * q;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) *reinterpret_cast<uint4*>(p + k * kPipeP1) = bq[k];
+}
+
+// One forward T_r row: carry from the skewed rows (row k of the chunk and k - 1; carry_rows_kernel's
+// g_k formula) + conv(2^16) of the row in shared memory -> out (kTWords words).
+__device__ __forceinline__ void pipe_carry_row(const uint32_t* __restrict__ gs, int k, uint32_t* __restrict__ out,
+                                               uint32_t* smem) {
+  uint32_t* tile = smem;
+  uint32_t* sc = smem + kTileRows * kRowPitchW<1>;
+  const int tid = threadIdx.x;
+  uint32_t* sa = smem;
+  uint32_t* sh = smem + 2312;
+  auto pad = [](int w) { return w + (w >> 3); };
+  const uint32_t* rk = gs + (uint64_t)k * kPipeP1;
+  const uint32_t* rk1 = gs + (uint64_t)(k ? k - 1 : 0) * kPipeP1;
+  const int a0 = k >> 5, b0 = (int)((kT + k - 1) >> 5);
+  uint32_t va[9], vh[9];
+#pragma unroll
+  for (int j = 0; j < 9; ++j) {
+    const int w = tid + 256 * j;
+    const int wb = b0 + w;
+    const bool in = w <= kTWords;
+    va[j] = in ? __ldcg(rk + a0 + w) : 0u;
+    const uint32_t vb = in && wb < (int)kPipeP1 ? __ldcg(rk + wb) : 0u;
+    const uint32_t vc = in && wb < (int)kPipeP1 && k ? __ldcg(rk1 + wb) : 0u;
+    vh[j] = vb ^ vc;
+  }
+  const int sA = k & 31, sB = (int)((kT + k - 1) & 31);
+#pragma unroll
+  for (int j = 0; j < 9; ++j) {
+    const int w = tid + 256 * j;
+    if (w <= kTWords) {
+      sa[pad(w)] = va[j];
+      sh[pad(w)] = vh[j];
+    }
+  }
+  __syncthreads();
+  uint32_t m[8];
+  {
+    uint32_t wa[9], wh[9];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      wa[j] = sa[pad(8 * tid + j)];
+      wh[j] = sh[pad(8 * tid + j)];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = __funnelshift_r(wa[i], wa[i + 1], sA) ^ __funnelshift_r(wh[i], wh[i + 1], sB);
+  }
+  if (tid == 0) {  // g_k[0] takes no x * H_k term: undo bit 0 of Gs[k]'s H contribution
+    const uint32_t pos = (uint32_t)(kT + k - 1);
+    m[0] ^= __funnelshift_r(__ldcg(rk + (pos >> 5)), (pos >> 5) + 1 < kPipeP1 ? __ldcg(rk + (pos >> 5) + 1) : 0u,
+                            (int)(pos & 31)) & 1u;
+  }
+  conv_tile<false>(m, tile, sc, kTLog2);  // (its first barrier orders the staging reads above)
+  uint4* o = reinterpret_cast<uint4*>(out + tid * 8);
+  o[0] = make_uint4(m[0], m[1], m[2], m[3]);
+  o[1] = make_uint4(m[4], m[5], m[6], m[7]);
+}
+
+// One inverse T_r row in place: conv(2^16)^-1.
+__device__ __forceinline__ void pipe_iconv_row(uint32_t* __restrict__ row, uint32_t* smem) {
+  uint32_t* tile = smem;
+  uint32_t* sc = smem + kTileRows * kRowPitchW<1>;
+  const int tid = threadIdx.x;
+  const uint4 a = reinterpret_cast<const uint4*>(row + tid * 8)[0];
+  const uint4 b = reinterpret_cast<const uint4*>(row + tid * 8)[1];
+  uint32_t m[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  conv_tile<true>(m, tile, sc, kTLog2);
+  reinterpret_cast<uint4*>(row + tid * 8)[0] = make_uint4(m[0], m[1], m[2], m[3]);
+  reinterpret_cast<uint4*>(row + tid * 8)[1] = make_uint4(m[4], m[5], m[6], m[7]);
+}
+
+// One inverse overflow row (overflow_kernel with the chunk-local digit d = row & 255): F_d[p] =
+// Gs[d][p+d] ^ (d >= 1 ? Gs[d-1][t+p+d-1] : 0), gs = the chunk's skewed rows (ring slot).
+__device__ __forceinline__ void pipe_overflow_row(const uint32_t* __restrict__ gs, int d, uint32_t* __restrict__ o,
+                                                  const uint32_t* __restrict__ tp, bool first_row) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t* r0 = gs + (uint64_t)d * kPipeP1;
+  const uint32_t sh0 = d & 31, a0 = d >> 5;
+  const uint32_t pos = (uint32_t)kT + d - 1, sh1 = pos & 31, b0 = pos >> 5;
+  uint32_t x[8], y[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t ia = tid + 256 * i + a0;
+    x[i] = __ldcg(r0 + ia);
+    y[i] = lane == 31 && ia + 1 < kPipeP1 ? __ldcg(r0 + ia + 1) : 0u;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t w = tid + 256 * i;
+    const uint32_t nx = __shfl_down_sync(0xFFFFFFFFu, x[i], 1);
+    uint32_t v = __funnelshift_r(x[i], lane == 31 ? y[i] : nx, sh0);
+    if (d && (w - lane) + b0 < kPipeP1) {
+      const uint32_t ib = w + b0;
+      const uint32_t xb = ib < kPipeP1 ? __ldcg(r0 - kPipeP1 + ib) : 0u;
+      uint32_t yb = __shfl_down_sync(0xFFFFFFFFu, xb, 1);
+      if (lane == 31) yb = ib + 1 < kPipeP1 ? __ldcg(r0 - kPipeP1 + ib + 1) : 0u;
+      v ^= __funnelshift_r(xb, yb, sh1);
+    }
+    if (tp) v ^= (tp[w] << 1) | ((!first_row || w) ? tp[(int64_t)w - 1] >> 31 : 0u);
+    o[w] = v;
+  }
+}
+
+// Work item k of the pipelined pass over nch chunks: (kind, chunk, sub).  Kinds in claim order per
+// step s: [forward] Z(s), C(s - lag); [inverse] R(s), Z(s - lag), O(s - 2 lag).
+struct PipeItem {
+  int kind, chunk, sub;  // kind: 0 = zeta window, 1 = carry / overflow row, 2 = inverse conv row
+};
+template <bool INV, bool ICONV>
+__device__ __forceinline__ PipeItem pipe_item(int k, int nch) {
+  // Step s holds, in order, the items of the kinds j whose chunk s - j * lag is in [0, nch).  The
+  // per-step count only changes at the steps j * lag and nch + j * lag: walk those phases.
+  constexpr int nk = ICONV ? 3 : 2;
+  constexpr int kinds[3] = {ICONV ? 2 : 0, ICONV ? 0 : 1, 1};
+  constexpr int sizes[3] = {ICONV ? 256 : kPipeZW, ICONV ? kPipeZW : (INV ? 256 / kPipeORows : 256), 256};
+  int b[2 * nk];
+#pragma unroll
+  for (int j = 0; j < nk; ++j) {
+    b[j] = j * kPipeLag;
+    b[nk + j] = nch + j * kPipeLag;
+  }
+#pragma unroll
+  for (int i = 1; i < 2 * nk; ++i)  // insertion sort (<= 6 values)
+#pragma unroll
+    for (int j = i; j > 0; --j)
+      if (b[j] < b[j - 1]) {
+        const int t = b[j];
+        b[j] = b[j - 1];
+        b[j - 1] = t;
+      }
+  for (int i = 0; i + 1 < 2 * nk; ++i) {
+    const int s0 = b[i], steps = b[i + 1] - s0;
+    if (steps <= 0) continue;
+    int per = 0;
+#pragma unroll
+    for (int j = 0; j < nk; ++j) {
+      const int ch = s0 - j * kPipeLag;
+      if (ch >= 0 && ch < nch) per += sizes[j];
+    }
+    if (k < per * steps) {
+      const int s = s0 + k / per;
+      int r = k % per;
+#pragma unroll
+      for (int j = 0; j < nk; ++j) {
+        const int ch = s - j * kPipeLag;
+        if (ch < 0 || ch >= nch) continue;
+        if (r < sizes[j]) return PipeItem{kinds[j], ch, r};
+        r -= sizes[j];
+      }
+    }
+    k -= per * steps;
+  }
+  return PipeItem{-1, 0, 0};
+}
+
+// cnt: 3 * nch + 1 zeroed ints: [0, nch) zeta windows done per chunk, [nch, 2 nch) rows done per
+// chunk (carry / overflow), [2 nch, 3 nch) inverse conv rows done per chunk, [3 nch] the claim
+// counter.  w: the block (nch * 256 rows of kTWords words); src: the rows the zeta reads (forward:
+// the unconverted rows, may be w; inverse: w); ring: kPipeSlots chunks of 256 skewed rows (pitch
+// kPipeP1); top: as overflow_kernel.  INV: zeta + overflow (L1_inner^-1); ICONV: with the rows'
+// conv(2^16)^-1 (T_r^-1) first.
+template <bool INV, bool ICONV>
+__global__ void __launch_bounds__(256, kPipeCtas) l1_inner_rows_kernel(const uint32_t* src, uint32_t* w, uint32_t* ring,
+                                                                int nch, int* cnt, const uint32_t* __restrict__ top) {
+  pdl_wait();
+  extern __shared__ __align__(16) uint32_t smem[];  // max(zeta 256 x kZP, row tile kTileSmem)
+  __shared__ int s_item[2];
+  const int total = nch * (kPipeZW + (INV && !ICONV ? 256 / kPipeORows : 256) + (ICONV ? 256 : 0));
+  int* zdone = cnt;
+  int* rdone = cnt + nch;
+  int* idone = cnt + 2 * nch;
+  int* claim = cnt + 3 * nch;
+  if (threadIdx.x == 0) s_item[0] = atomicAdd(claim, 1);
+  __syncthreads();
+  int buf = 0;
+  for (int cur = s_item[0]; cur < total; cur = s_item[buf]) {
+    if (threadIdx.x == 0) s_item[buf ^ 1] = atomicAdd(claim, 1);  // next claim in flight
+    const PipeItem it = pipe_item<INV, ICONV>(cur, nch);
+    const int c = it.chunk;
+    uint32_t* slot = ring + (uint64_t)(c % kPipeSlots) * 256 * kPipeP1;
+    uint32_t* wc = w + (uint64_t)c * 256 * kTWords;
+    if (it.kind == 0) {  // zeta window
+      if (ICONV) pipe_wait(idone + c, 256);                       // the chunk's rows are conv^-1'ed
+      if (c >= kPipeSlots) pipe_wait(rdone + c - kPipeSlots, 256);  // the slot's previous chunk is consumed
+      if (ICONV) pipe_zeta_item<true>(wc, slot, it.sub, smem);
+      else pipe_zeta_item<false>(src + (uint64_t)c * 256 * kTWords, slot, it.sub, smem);
+      pipe_done(zdone + c);
+    } else if (it.kind == 1) {  // carry (forward) / overflow (inverse) row
+      pipe_wait(zdone + c, kPipeZW);
+      if (!INV) {
+        pipe_carry_row(slot, it.sub, wc + (uint64_t)it.sub * kTWords, smem);
+        pipe_done(rdone + c);
+      } else {
+        constexpr int nr = ICONV ? 1 : kPipeORows;
+#pragma unroll 1
+        for (int r = 0; r < nr; ++r) {
+          const int d = it.sub * nr + r;
+          const uint64_t row = (uint64_t)c * 256 + d;
+          pipe_overflow_row(slot, d, wc + (uint64_t)d * kTWords, top ? top + row * kTWords : nullptr, row == 0);
+        }
+        pipe_done(rdone + c, nr);
+      }
+    } else if (it.kind == 2) {  // inverse conv row
+      pipe_iconv_row(wc + (uint64_t)it.sub * kTWords, smem);
+      pipe_done(idone + c);
+    }
+    buf ^= 1;  // (s_item[buf] was written before pipe_done's barrier)
+  }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
+}
+
 // Bit 0 of the upper 2^32-bit block ^= its last bit (the fused 2^33-bit top pass's target 2^32).
 __global__ void top_bit_fix_kernel(uint32_t* __restrict__ hi_block, uint64_t block_words) {
   pdl_wait();
@@ -1526,6 +1831,52 @@ void conv_cols_split(uint32_t* w, uint32_t* side, int lgD, bool inv, cudaStream_
   }
 }
 
+// FPM_L1_PIPE: 0 = separate kernels (zeta -> 520 MiB skewed copy -> carry_rows / overflow); 1
+// (default) = the pipelined pass for the forward zeta + carry/T_r and for the inverse zeta +
+// overflow, T_r^-1 staying a separate conv_rows pass; 2 = T_r^-1 inside the pipelined pass too.
+// Measured at 2^32 bits (two blocks per direction, bench stage times): forward 5.70 (0) / 5.68 ms
+// (1), inverse 5.65 / 5.65 / 6.04 (2: conv^-1 at 3 CTAs/SM instead of 6).  The gain is memory: the
+// skewed rows need a 32 MiB ring instead of a 520 MiB scratch array, and HBM traffic drops by the
+// skewed copy's write + read (ncu: 2.0 -> 1.1 GB per forward block).
+int l1_pipe_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("FPM_L1_PIPE");
+    return e ? std::atoi(e) : 1;
+  }();
+  return m;
+}
+// Skewed-row scratch words the L1_inner step needs for D rows: the pipelined pass keeps a ring of
+// kPipeSlots chunks, the separate kernels a skewed copy of every row.
+uint64_t l1_scratch_words(uint64_t D, bool inverse) {
+  (void)inverse;  // both directions use the ring
+  const bool ring = D >= 256 && l1_pipe_mode() >= 1;
+  const uint64_t rows = ring ? std::min<uint64_t>(D, (uint64_t)kPipeSlots * 256) : D;
+  return rows * kPipeP1;
+}
+
+// L1_inner (+ T_r) as one pipelined pass (l1_inner_rows_kernel) over the D = 256 nch rows of w:
+// mode 0 forward zeta + carry/T_r; 1 inverse zeta + overflow; 2 inverse T_r^-1 + zeta + overflow.
+void l1_inner_rows(const uint32_t* src, uint32_t* w, uint32_t* ring, uint64_t D, int mode, const uint32_t* top,
+                   cudaStream_t s) {
+  static PerDeviceOnce attr;
+  constexpr size_t smem = 256 * kZP * sizeof(uint32_t);
+  static_assert(smem >= kTileSmem, "the zeta tile is the larger shared-memory user");
+  attr.run([] {
+    FPM_CUDA(cudaFuncSetAttribute(l1_inner_rows_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FPM_CUDA(cudaFuncSetAttribute(l1_inner_rows_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FPM_CUDA(cudaFuncSetAttribute(l1_inner_rows_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  });
+  const int nch = (int)(D / 256);
+  DevBuf cnt((3 * nch + 1) * sizeof(int), s);
+  FPM_CUDA(cudaMemsetAsync(cnt.p, 0, (3 * nch + 1) * sizeof(int), s));
+  const int items = nch * (kPipeZW + (mode == 1 ? 256 / kPipeORows : 256) + (mode == 2 ? 256 : 0));
+  const int grid = grid_cap((uint64_t)items, kPipeCtas);
+  if (mode == 2) launch_k(l1_inner_rows_kernel<true, true>, dim3(grid), dim3(256), smem, s, src, w, ring, nch, cnt.as<int>(), top);
+  else if (mode == 1) launch_k(l1_inner_rows_kernel<true, false>, dim3(grid), dim3(256), smem, s, src, w, ring, nch, cnt.as<int>(), top);
+  else launch_k(l1_inner_rows_kernel<false, false>, dim3(grid), dim3(256), smem, s, src, w, ring, nch, cnt.as<int>(), top);
+  FPM_LAUNCH_CHECK();
+}
+
 void conv2d_split(uint32_t* w, int K, bool inv, uint32_t* scratch, uint32_t* side, cudaStream_t s,
                   const uint32_t* src = nullptr, const uint32_t* top = nullptr, const EncodeSink* enc = nullptr,
                   bool skip_a = false) {
@@ -1544,16 +1895,27 @@ void conv2d_split(uint32_t* w, int K, bool inv, uint32_t* scratch, uint32_t* sid
       outer(in, nullptr);
       in = w;
     }
-    zeta(in, kTWords, scratch, p1, D, 0, nb_in, lo_skew, p1 / kZW, s, kTWords);
-    launch_k(carry_rows_kernel, dim3(grid_cap(D, 7)), dim3(256), kTileSmem, s, scratch, p1, w, D, 255);
-    FPM_LAUNCH_CHECK();
+    if (nb_in == 8 && l1_pipe_mode() >= 1) {
+      l1_inner_rows(in, w, scratch, D, 0, nullptr, s);
+    } else {
+      zeta(in, kTWords, scratch, p1, D, 0, nb_in, lo_skew, p1 / kZW, s, kTWords);
+      launch_k(carry_rows_kernel, dim3(grid_cap(D, 7)), dim3(256), kTileSmem, s, scratch, p1, w, D, 255);
+      FPM_LAUNCH_CHECK();
+    }
     conv_cols_split(w, side, lgD, false, s, enc);
   } else {
     conv_cols_split(w, side, lgD, true, s, nullptr, skip_a);
-    conv_rows(w, D * kTWords, kTLog2, true, s);
-    zeta(w, kTWords, scratch, p1, D, 0, nb_in, lo_skew, p1 / kZW, s, kTWords);
-    launch_k(overflow_kernel, dim3(grid_cap(D, 8)), dim3(256), 0, s, scratch, p1, w, D, nb_out ? nullptr : top, 255);
-    FPM_LAUNCH_CHECK();
+    if (nb_in == 8 && l1_pipe_mode() == 2) {
+      l1_inner_rows(w, w, scratch, D, 2, nb_out ? nullptr : top, s);
+    } else if (nb_in == 8 && l1_pipe_mode() == 1) {
+      conv_rows(w, D * kTWords, kTLog2, true, s);
+      l1_inner_rows(w, w, scratch, D, 1, nb_out ? nullptr : top, s);
+    } else {
+      conv_rows(w, D * kTWords, kTLog2, true, s);
+      zeta(w, kTWords, scratch, p1, D, 0, nb_in, lo_skew, p1 / kZW, s, kTWords);
+      launch_k(overflow_kernel, dim3(grid_cap(D, 8)), dim3(256), 0, s, scratch, p1, w, D, nb_out ? nullptr : top, 255);
+      FPM_LAUNCH_CHECK();
+    }
     if (nb_out) outer(w, top);
   }
 }
@@ -1594,7 +1956,7 @@ void basis_cvt_block32_inverse(uint32_t* w, const uint32_t* top, cudaStream_t s)
   set_smem_attr();
   const uint64_t D = (uint64_t)1 << 16;
   const bool split = split_l1_enabled();
-  const size_t scr_bytes = split ? D * (kT + 32 * kZW) / 8
+  const size_t scr_bytes = split ? l1_scratch_words(D, true) * sizeof(uint32_t)
                                  : D * (kT + std::max<uint64_t>(D, 32 * kZW)) / 8 + D * (kT + 32 * kZW) / 8;
   Scratch scr(scr_bytes, s), side_buf(split ? split_side_words(16) * sizeof(uint32_t) : 0, s);
 
@@ -1672,7 +2034,7 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
   // split L1 needs the C_cols scratch (2 Dd x (256 + Dd) rows) and the outer step's side rows
   const bool split = split_l1_enabled();
 
-  const size_t scr_bytes = split ? D * (kT + 32 * kZW) / 8
+  const size_t scr_bytes = split ? l1_scratch_words(D, inverse) * sizeof(uint32_t)
                                  : D * (kT + std::max<uint64_t>(D, 32 * kZW)) / 8 + (D > 256 ? D * (kT + 32 * kZW) / 8 : 0);
   Scratch scr(scr_bytes, s), side_buf(split ? split_side_words((int)lgD) * sizeof(uint32_t) : 0, s);
   uint32_t* scratch = static_cast<uint32_t*>(scr.p);
