@@ -5,6 +5,8 @@
 #include <atomic>
 #include <cstddef>
 #include <cstdint>
+#include <utility>
+#include <vector>
 #include <functional>
 #include <new>
 #include <stdexcept>
@@ -227,6 +229,25 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
 // top_bit_fix_device on the upper block.
 void basis_cvt_block32_inverse(uint32_t* w_lo, const uint32_t* top, cudaStream_t s);
 void top_bit_fix_device(uint32_t* hi_block, cudaStream_t s);
+// The sharded 2^32-bit conversion (k_basis.cu; fpm_multi.cu at P >= 4): phase steps on one rank's
+// full-size replica of a block, Q = 2 or 4 ranks per block.
+enum { kDistWindow = 0, kDistChunk = 1, kDistColumn = 2 };
+struct RankPtrs {
+  uint32_t* p[4];
+};
+void b32_regather(uint32_t* dst, const RankPtrs& src, int from, int to, int q, int Q, cudaStream_t s);
+void b32_l1_outer(const uint32_t* src, uint32_t* w, uint32_t* side, bool inv, int q, int Q, cudaStream_t s);
+void b32_l1_outer_fix(uint32_t* w, const uint32_t* side, bool inv, uint32_t e_lo, uint32_t e_hi, cudaStream_t s);
+void b32_rows(uint32_t* w_rows, uint64_t rows, bool inv, cudaStream_t s);
+void b32_cols(uint32_t* w, bool inv, int q, int Q, cudaStream_t s);
+void b32_top_pass(uint32_t* lo, const RankPtrs& hi, int q, int Q, cudaStream_t s);
+void b32_top_bit_fix(uint32_t* hi0, const uint32_t* hi_last_owner, cudaStream_t s);
+std::vector<std::pair<uint64_t, uint64_t>> b32_window_ranges(int q, int Q);
+void encode_cols_owners(const RankPtrs& polys, int Q, unsigned l, uint64_t col0, uint64_t ncols, uint4* ev,
+                        int rows_live, cudaStream_t s, bool tower);
+void decode_cols_owners(const uint4* ev, uint64_t ncols, uint64_t col0, uint64_t row_bits, const RankPtrs& los,
+                        const RankPtrs& his, int Q, cudaStream_t s, bool tower);
+
 
 // Encode / decode (k_codec.cu).  poly has 128 * 2^l bits; ev has 2^l uint4.
 void encode_device(const uint32_t* poly, unsigned l, uint4* ev, cudaStream_t s);

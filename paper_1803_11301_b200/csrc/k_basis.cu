@@ -774,6 +774,9 @@ constexpr size_t kC256Smem = 16 * 33 * kC256Cols * sizeof(uint32_t);
 // words); the CTA takes word columns [c0, c0 + 32).
 struct UnitMap {
   uint64_t ustride, gstride, ngroups;  // group g's unit u at row g_row(g) + u * ustride
+  // conv256_units_tma_kernel only: column items [col_lo, col_lo + ncols) of every group (ncols = 0:
+  // all kTWords / kCT of them) -- a rank's column share in the sharded conversion
+  uint32_t col_lo = 0, ncols = 0;
   __device__ __forceinline__ uint64_t row(uint64_t grp, int u) const {
     // groups: (ngroups) groups; group index -> base row = (grp % gstride) + (grp / gstride) * 256 * gstride
     return (grp % gstride) + (grp / gstride) * 256 * gstride + (uint64_t)u * ustride;
@@ -937,6 +940,7 @@ __global__ void __launch_bounds__(kCTThreads, kCTMinBlocks) conv256_units_tma_ke
   uint64_t* bar = reinterpret_cast<uint64_t*>(Z + 16 * 33 * kCT);
   const int tid = threadIdx.x, c = tid % kCT, r = tid / kCT;
   constexpr int kCols = kTWords / kCT;
+  const uint64_t nc = um.ncols ? um.ncols : kCols;  // column items per group
   auto zi = [](int d, int s, int cc) { return (d * 33 + s) * kCT + cc; };
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -948,8 +952,8 @@ __global__ void __launch_bounds__(kCTThreads, kCTMinBlocks) conv256_units_tma_ke
   auto issue = [&](uint64_t it, int st) {
     if (tid != 0 || it >= nitems) return;
     mbar_expect_tx(&bar[st], (uint32_t)kCTStage);
-    const uint64_t grp = it / kCols;
-    const int c0 = (int)((it % kCols) * kCT), c1 = (int)(grp % um.gstride), c2 = (int)((grp / um.gstride) * 256);
+    const uint64_t grp = it / nc;
+    const int c0 = (int)((um.col_lo + it % nc) * kCT), c1 = (int)(grp % um.gstride), c2 = (int)((grp / um.gstride) * 256);
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
             smem_u32(stage(st))),
@@ -961,7 +965,7 @@ __global__ void __launch_bounds__(kCTThreads, kCTMinBlocks) conv256_units_tma_ke
   issue(blockIdx.x + gridDim.x, 1);
   int st = 0;
   for (uint64_t it = blockIdx.x; it < nitems; it += gridDim.x, st ^= 1) {
-    const uint64_t grp = it / kCols, colw = (it % kCols) * kCT + c;
+    const uint64_t grp = it / nc, colw = (um.col_lo + it % nc) * kCT + c;
     uint32_t* const gbase = data + um.row(grp, 0) * kTWords + colw;
     const uint32_t ustep = (uint32_t)(um.ustride * kTWords);
     auto at = [&](int u) -> uint32_t* { return gbase + (uint32_t)u * ustep; };
@@ -1400,11 +1404,19 @@ struct StepGeom {
 };
 // NB = log2 R (template: the tile-row -> (row, window) split is then compile-time and every load /
 // store address is one add from a per-thread base).
+// The window blocks (wpc windows each) a launch processes: wb = lo + period (j / n) + first + j % n for
+// j < count, wb < hi -- all of them by default; a contiguous range (L1_outer) or the blocks of one
+// column range (T_d steps: the column of a block is wb mod period) for a rank of the sharded
+// conversion.
+struct WinSel {
+  uint64_t lo = 0, hi = ~(uint64_t)0, count = 0;  // count = 0: every block of [0, wblocks)
+  uint32_t period = 1, first = 0, n = 1;
+};
 template <int NB>
 __global__ void __launch_bounds__(256, 3) outer_zeta_kernel(const uint32_t* src, uint32_t* dst, const StepGeom gm,
                                                             uint64_t windows, uint64_t groups,
                                                             uint32_t* __restrict__ side,
-                                                            const uint32_t* __restrict__ top) {
+                                                            const uint32_t* __restrict__ top, const WinSel sel) {
   pdl_wait();
   extern __shared__ __align__(16) uint32_t sx[];  // 256 x kZP
   constexpr int R = 1 << NB, wpc = 256 >> NB;
@@ -1412,9 +1424,12 @@ __global__ void __launch_bounds__(256, 3) outer_zeta_kernel(const uint32_t* src,
   const uint64_t wblocks = (windows + wpc - 1) / wpc;
   const uint64_t side_pitch = gm.skew_words << NB;
   const int64_t rw = (int64_t)gm.row_words, sk = (int64_t)gm.skew_words;
-  const uint64_t items = wblocks * groups;
+  const uint64_t nsel = sel.count ? sel.count : wblocks;
+  const uint64_t items = nsel * groups;
   for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
-    const uint64_t grp = it / wblocks, wb = it - grp * wblocks;
+    const uint64_t grp = it / nsel, j = it - grp * nsel;
+    const uint64_t wb = sel.count ? sel.lo + sel.period * (j / sel.n) + sel.first + j % sel.n : j;
+    if (wb >= wblocks || wb >= sel.hi) continue;
     const uint32_t* gsrc = src + grp * gm.group_words;
     const int64_t wi0 = (int64_t)(wb * wpc);
     // mapping A: word c of tile rows TR = w8 + 8k; row j = TR % R, window slot TR / R
@@ -1484,15 +1499,21 @@ __global__ void __launch_bounds__(256, 3) outer_zeta_kernel(const uint32_t* src,
 // Folds the beyond-window parts into the first R*skew words of the rows (row e's side holds
 // skew*(R-1-e) meaningful words): forward F_e[p] ^= side_e[p-skew] ^ side_{e-1}[p];
 // inverse f_c[p] ^= side_{c-1}[p].  Four words per thread.
+// FixSel: rows e in [e_lo, e_hi) and words p with (p mod 2048) - col_lo < col_n (a rank's chunks /
+// columns in the sharded conversion; default all).
+struct FixSel {
+  uint32_t e_lo = 0, e_hi = ~0u, col_lo = 0, col_n = 2048;
+};
 template <bool INV>
 __global__ void outer_fix_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ side, const StepGeom gm,
-                                 uint64_t groups) {
+                                 uint64_t groups, const FixSel fs) {
   pdl_wait();
   const uint64_t R = (uint64_t)1 << gm.nb, P = gm.skew_words << gm.nb, S = gm.skew_words, per_group = R * P / 4;
   for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < groups * per_group;
        k += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t grp = k / per_group, r = k % per_group;
     const uint64_t e = r / (P / 4), p = 4 * (r % (P / 4));
+    if (e < fs.e_lo || e >= fs.e_hi || (uint32_t)((p & 2047) - fs.col_lo) >= fs.col_n) continue;
     const uint32_t* gs = side + grp * R * P;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (!INV && p >= S && p - S < S * (R - 1 - e)) v = *reinterpret_cast<const uint4*>(gs + e * P + p - S);
@@ -1583,20 +1604,25 @@ bool tma_units_enabled() {
 }
 
 void conv256_units(uint32_t* w, uint64_t ngroups, uint64_t ustride, uint64_t gstride, bool inv, cudaStream_t s,
-                   CarrySrc cs = CarrySrc{}) {
+                   CarrySrc cs = CarrySrc{}, int q = 0, int Q = 1) {
   static PerDeviceOnce attr;
   attr.run([&] {
     FPM_CUDA(cudaFuncSetAttribute(conv256_units_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC256Smem));
     FPM_CUDA(cudaFuncSetAttribute(conv256_units_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC256Smem));
   });
   UnitMap um{ustride, gstride, ngroups};
+  if (Q > 1) {  // a rank's column items (TMA path only)
+    if (cs.gs || !tma_units_enabled()) throw Error(kInvalid, "conv256_units: column shares need the TMA path");
+    um.ncols = (uint32_t)(kTWords / kCT / Q);
+    um.col_lo = (uint32_t)(q * um.ncols);
+  }
   if (!cs.gs && tma_units_enabled()) {
     static PerDeviceOnce tattr;
     tattr.run([&] {
       FPM_CUDA(cudaFuncSetAttribute(conv256_units_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCTSmem));
       FPM_CUDA(cudaFuncSetAttribute(conv256_units_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCTSmem));
     });
-    const uint64_t titems = ngroups * (kTWords / kCT);
+    const uint64_t titems = ngroups * (um.ncols ? um.ncols : kTWords / kCT);
     // groups of 256 units: (ustride, gstride) = (1, 1) consecutive rows, or (g, g) rows g apart
     if (ustride != gstride) throw Error(kInvalid, "conv256_units: unit stride must equal the group stride");
     const CUtensorMap tm = unit_tensor_map(w, ngroups * 256, gstride);
@@ -1719,24 +1745,56 @@ void conv2d(uint32_t* w, int K, bool inv, uint32_t* scratch, cudaStream_t s, con
 // No step writes a skewed array wider than t + 1024 bits per row (the single-step L1 of conv2d skews
 // rows by up to D = t bits: 2x the array).  scratch >= D * (t + 1024) bits and the C_cols scratch.
 // One generic two-term step (outer_zeta_kernel + fix-up), in place on w (or from src).
-void two_term_step(const uint32_t* src, uint32_t* w, StepGeom gm, uint64_t groups, uint32_t* side, bool inv,
-                   cudaStream_t s, const uint32_t* top = nullptr) {
+void outer_fix(uint32_t* w, const uint32_t* side, StepGeom gm, uint64_t groups, bool inv, cudaStream_t s,
+               FixSel fs = FixSel{}) {
+  const uint64_t fix = groups * (gm.side_pitch() << gm.nb) / 4;
+  if (inv) launch_k(outer_fix_kernel<true>, dim3(grid_cap((fix + 255) / 256, 8)), dim3(256), 0, s, w, side, gm, groups, fs);
+  else launch_k(outer_fix_kernel<false>, dim3(grid_cap((fix + 255) / 256, 8)), dim3(256), 0, s, w, side, gm, groups, fs);
+  FPM_LAUNCH_CHECK();
+}
+
+// The zeta half of a two-term step over the selected window blocks (no fix-up).
+void outer_zeta(const uint32_t* src, uint32_t* w, StepGeom gm, uint64_t groups, uint32_t* side, cudaStream_t s,
+                const uint32_t* top = nullptr, WinSel sel = WinSel{}) {
   const int wpc = 256 >> gm.nb;
-  const uint64_t items = (gm.windows() + wpc - 1) / wpc * groups;
+  const uint64_t wblocks = (gm.windows() + wpc - 1) / wpc;
+  const uint64_t items = (sel.count ? sel.count : wblocks) * groups;
   const size_t smem = 256 * kZP * sizeof(uint32_t);  // 36 KiB: under the default dynamic limit
   const int grid = grid_cap(items, 3);
   switch (gm.nb) {
 #define FPM_OUTER(NB) \
-    case NB: launch_k(outer_zeta_kernel<NB>, dim3(grid), dim3(256), smem, s, src, w, gm, gm.windows(), groups, side, top); break;
+    case NB: launch_k(outer_zeta_kernel<NB>, dim3(grid), dim3(256), smem, s, src, w, gm, gm.windows(), groups, side, top, sel); break;
     FPM_OUTER(1) FPM_OUTER(2) FPM_OUTER(3) FPM_OUTER(4) FPM_OUTER(5) FPM_OUTER(6) FPM_OUTER(7) FPM_OUTER(8)
 #undef FPM_OUTER
     default: throw Error(kInvalid, "two-term step: 1..8 digit bits");
   }
   FPM_LAUNCH_CHECK();
-  const uint64_t fix = groups * (gm.side_pitch() << gm.nb) / 4;
-  if (inv) launch_k(outer_fix_kernel<true>, dim3(grid_cap((fix + 255) / 256, 8)), dim3(256), 0, s, w, side, gm, groups);
-  else launch_k(outer_fix_kernel<false>, dim3(grid_cap((fix + 255) / 256, 8)), dim3(256), 0, s, w, side, gm, groups);
-  FPM_LAUNCH_CHECK();
+}
+
+// Column selection of a T_d step for rank q of Q (Q | 4): window blocks of wpc windows cover
+// 32 wpc words of a 2048-word row; the blocks of columns [q 2048/Q, (q+1) 2048/Q).
+WinSel column_sel(StepGeom gm, int q, int Q) {
+  WinSel sel;
+  if (Q <= 1) return sel;
+  const uint64_t wpc = 256 >> gm.nb, bw = 32 * wpc;  // words per window block
+  if (2048 % bw || (2048 / bw) % (uint64_t)Q) throw Error(kInvalid, "column_sel: unsupported step geometry");
+  const uint64_t per_row = 2048 / bw, wblocks = (gm.windows() + wpc - 1) / wpc;
+  sel.period = (uint32_t)per_row;
+  sel.n = (uint32_t)(per_row / Q);
+  sel.first = (uint32_t)(q * sel.n);
+  sel.count = (wblocks + per_row - 1) / per_row * sel.n;
+  return sel;
+}
+
+void two_term_step(const uint32_t* src, uint32_t* w, StepGeom gm, uint64_t groups, uint32_t* side, bool inv,
+                   cudaStream_t s, const uint32_t* top = nullptr, int q = 0, int Q = 1) {
+  outer_zeta(src, w, gm, groups, side, s, top, column_sel(gm, q, Q));
+  FixSel fs;
+  if (Q > 1) {
+    fs.col_lo = (uint32_t)(q * (2048 / Q));
+    fs.col_n = (uint32_t)(2048 / Q);
+  }
+  outer_fix(w, side, gm, groups, inv, s, fs);
 }
 
 // Side words the split steps need for D = 2^lgD rows (max over the steps, per call).
@@ -1783,8 +1841,11 @@ void conv256_a_encode(uint32_t* w, const EncodeSink& enc, cudaStream_t s) {
 }
 
 // skip_a (inverse, 2^32-bit blocks): conv(Dd)^-1 over the digit already ran (decode_conv_a_kernel).
+// q, Q: only rank q's column share (columns [q 2048/Q, (q+1) 2048/Q) of every row; the sharded
+// conversion, lgD = 16, no fused encode).
 void conv_cols_split(uint32_t* w, uint32_t* side, int lgD, bool inv, cudaStream_t s, const EncodeSink* enc = nullptr,
-                     bool skip_a = false) {
+                     bool skip_a = false, int q = 0, int Q = 1) {
+  if (Q > 1 && (lgD != 16 || enc)) throw Error(kInvalid, "conv_cols_split: column shares for 2^32-bit blocks only");
   if (lgD <= 1) return;
   if (lgD <= 8) {
     slab(w, lgD, 1, kTWords / 8, inv, s);
@@ -1795,22 +1856,22 @@ void conv_cols_split(uint32_t* w, uint32_t* side, int lgD, bool inv, cudaStream_
   const uint64_t unit = kTWords;  // words per row
   auto l1d = [&](bool fwd) {
     if (gd <= 4) {
-      two_term_step(w, w, StepGeom{256 * unit, unit, 0, gd}, 1, side, !fwd, s);
+      two_term_step(w, w, StepGeom{256 * unit, unit, 0, gd}, 1, side, !fwd, s, nullptr, q, Q);
       return;
     }
     const int k = gd / 2;
     const StepGeom outer{(256 * unit) << k, unit << k, 0, gd - k};
     const StepGeom inner{256 * unit, unit, (256 * unit) << k, k};
     if (fwd) {
-      two_term_step(w, w, outer, 1, side, false, s);
-      two_term_step(w, w, inner, (uint64_t)1 << (gd - k), side, false, s);
+      two_term_step(w, w, outer, 1, side, false, s, nullptr, q, Q);
+      two_term_step(w, w, inner, (uint64_t)1 << (gd - k), side, false, s, nullptr, q, Q);
     } else {
-      two_term_step(w, w, inner, (uint64_t)1 << (gd - k), side, true, s);
-      two_term_step(w, w, outer, 1, side, true, s);
+      two_term_step(w, w, inner, (uint64_t)1 << (gd - k), side, true, s, nullptr, q, Q);
+      two_term_step(w, w, outer, 1, side, true, s, nullptr, q, Q);
     }
   };
   auto over_digit = [&](bool iv) {  // conv(Dd) over rows 256 apart
-    if (gd == 8) conv256_units(w, 256, 256, 256, iv, s);
+    if (gd == 8) conv256_units(w, 256, 256, 256, iv, s, CarrySrc{}, q, Q);
     else slab(w, gd, 256, 256 * (kTWords / 8), iv, s);
   };
   if (!inv) {
@@ -1821,12 +1882,12 @@ void conv_cols_split(uint32_t* w, uint32_t* side, int lgD, bool inv, cudaStream_
       return;
     }
     over_digit(false);
-    conv256_units(w, Dd, 1, 1, false, s);
+    conv256_units(w, Dd, 1, 1, false, s, CarrySrc{}, q, Q);
   } else {
     // (conv over the digit and conv over the row within it commute: the digit one runs first so
     // that it can be fused with the decode)
     if (!skip_a) over_digit(true);
-    conv256_units(w, Dd, 1, 1, true, s);
+    conv256_units(w, Dd, 1, 1, true, s, CarrySrc{}, q, Q);
     l1d(false);
   }
 }
@@ -1967,6 +2028,157 @@ void basis_cvt_block32_inverse(uint32_t* w, const uint32_t* top, cudaStream_t s)
 void top_bit_fix_device(uint32_t* hi_block, cudaStream_t s) {
   launch_k(top_bit_fix_kernel, dim3(1), dim3(32), 0, s, hi_block, ((uint64_t)1 << 32) / 32);
   FPM_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------------ the sharded 2^32-bit conversion
+// fpm_polymul_multi at P >= 4 converts each 2^32-bit block (an operand, or a block of the 2^33-bit
+// product) on Q = P/2 ranks holding full-size replicas, one phase of build_schedule's recursion at a
+// time, each phase split the way its data dependencies allow (
+// proj/src/basis_convert.cpp:60-67 the phases, :278-327 the tiling):
+//   L1_outer   (z over the 256 chunks)      by L1_outer window: rank q the windows [q wpr, (q+1) wpr)
+//   L1_inner + T_r (chunk-local)             by chunk: rank q the chunks [q 256/Q, (q+1) 256/Q)
+//   T_d        (conv over the row index)     by column: rank q the words [q 2048/Q, ...) of every row
+// Between two phases every rank pulls the 16-byte groups it owns next from their previous owners'
+// replicas (regather_kernel, peer loads over NVLink); all replicas use the same word offsets.
+namespace {
+
+constexpr uint64_t kB32Words = (uint64_t)1 << 27;                          // 32-bit words per block
+constexpr uint64_t kB32Windows = (kChunkWords + 8 * 255 + kZW - 1) / kZW;  // L1_outer windows (16448)
+
+__device__ __forceinline__ int dist_owner(int dist, uint64_t wi, int lgq, uint64_t wpr) {
+  if (dist == kDistChunk) return (int)((wi >> 19) >> (8 - lgq));
+  if (dist == kDistColumn) return (int)((wi & (kTWords - 1)) >> (11 - lgq));
+  const uint64_t c = wi >> 19, o = wi & (kChunkWords - 1);
+  return (int)(((o + 8 * c) >> 5) / wpr);
+}
+
+// The k-th 16-byte group rank q owns under distribution `dist` (n_owned(dist) of them), or ~0 for a
+// padding index (window ranges are clipped per chunk).
+__device__ __forceinline__ uint64_t dist_group(int dist, uint64_t k, int q, int lgq, uint64_t wpr) {
+  const int Q = 1 << lgq;
+  if (dist == kDistChunk) return ((uint64_t)q << (25 - lgq)) + k;
+  if (dist == kDistColumn) {
+    const uint64_t per = 512 >> lgq;  // of a row's 512 groups
+    return (k / per) * 512 + (uint64_t)q * per + k % per;
+  }
+  const uint64_t span = 8 * wpr, c = k / span, u = k % span;
+  const int64_t lo = (int64_t)(8 * (uint64_t)q * wpr) - 2 * (int64_t)c;
+  const uint64_t whi = q + 1 == Q ? kB32Windows : (uint64_t)(q + 1) * wpr;
+  const int64_t hi = std::min<int64_t>((int64_t)1 << 17, (int64_t)(8 * whi) - 2 * (int64_t)c);
+  const int64_t v = std::max<int64_t>(lo, 0) + (int64_t)u;
+  return v < hi ? (c << 17) + (uint64_t)v : ~(uint64_t)0;
+}
+__host__ __device__ __forceinline__ uint64_t dist_count(int dist, int lgq, uint64_t wpr) {
+  return dist == kDistWindow ? 256 * 8 * wpr : (uint64_t)1 << (25 - lgq);
+}
+
+__global__ void regather_kernel(uint32_t* __restrict__ dst, const RankPtrs src, int from, int to, int q, int lgq,
+                                uint64_t wpr) {
+  pdl_wait();
+  const uint64_t n = dist_count(to, lgq, wpr);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = dist_group(to, k, q, lgq, wpr);
+    if (v == ~(uint64_t)0) continue;
+    const int o = dist_owner(from, 4 * v, lgq, wpr);
+    if (o != q) d4[v] = __ldcg(reinterpret_cast<const uint4*>(src.p[o]) + v);
+  }
+  pdl_trigger();
+}
+
+// The 2^33-bit array's single top pass on rank q's window groups of the lower block: bit b ^= bit
+// b - 1 of the upper block (read from its window owners).
+__global__ void top_pass_windows_kernel(uint32_t* __restrict__ lo, const RankPtrs hi, int q, int lgq, uint64_t wpr) {
+  pdl_wait();
+  const uint64_t n = dist_count(kDistWindow, lgq, wpr);
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = dist_group(kDistWindow, k, q, lgq, wpr);
+    if (v == ~(uint64_t)0) continue;
+    const uint64_t G = 4 * v;
+    const uint4 t4 = __ldcg(reinterpret_cast<const uint4*>(hi.p[dist_owner(kDistWindow, G, lgq, wpr)]) + v);
+    const uint32_t tp = G ? __ldcg(hi.p[dist_owner(kDistWindow, G - 1, lgq, wpr)] + G - 1) : 0u;
+    uint4 x = reinterpret_cast<uint4*>(lo)[v];
+    x.x ^= (t4.x << 1) | (tp >> 31);
+    x.y ^= (t4.y << 1) | (t4.x >> 31);
+    x.z ^= (t4.z << 1) | (t4.y >> 31);
+    x.w ^= (t4.w << 1) | (t4.z >> 31);
+    reinterpret_cast<uint4*>(lo)[v] = x;
+  }
+  pdl_trigger();
+}
+
+__global__ void top_bit_fix_peer_kernel(uint32_t* __restrict__ hi0, const uint32_t* __restrict__ hi_last) {
+  pdl_wait();
+  if (threadIdx.x == 0) hi0[0] ^= __ldcg(hi_last + kB32Words - 1) >> 31;
+  pdl_trigger();
+}
+
+uint64_t b32_wpr(int Q) { return (kB32Windows + Q - 1) / Q; }
+
+}  // namespace
+
+void b32_regather(uint32_t* dst, const RankPtrs& src, int from, int to, int q, int Q, cudaStream_t s) {
+  const int lgq = __builtin_ctz((unsigned)Q);
+  if (Q < 2 || Q > 4 || (Q & (Q - 1))) throw Error(kInvalid, "regather: 2 or 4 ranks per block");
+  const uint64_t n = dist_count(to, lgq, b32_wpr(Q));
+  launch_k(regather_kernel, dim3(grid_cap((n + 255) / 256, 8)), dim3(256), 0, s, dst, src, from, to, q, lgq, b32_wpr(Q));
+  FPM_LAUNCH_CHECK();
+}
+
+void b32_l1_outer(const uint32_t* src, uint32_t* w, uint32_t* side, bool inv, int q, int Q, cudaStream_t s) {
+  const StepGeom gm{kChunkWords, 8, 0, 8};
+  WinSel sel;
+  const uint64_t wpr = b32_wpr(Q);
+  sel.lo = (uint64_t)q * wpr;
+  sel.hi = std::min<uint64_t>(kB32Windows, sel.lo + wpr);
+  sel.count = sel.hi - sel.lo;
+  (void)inv;  // the zeta half is the same superset zeta in both directions
+  outer_zeta(src, w, gm, 1, side, s, nullptr, sel);
+}
+
+void b32_l1_outer_fix(uint32_t* w, const uint32_t* side, bool inv, uint32_t e_lo, uint32_t e_hi, cudaStream_t s) {
+  FixSel fs;
+  fs.e_lo = e_lo;
+  fs.e_hi = e_hi;
+  outer_fix(w, side, StepGeom{kChunkWords, 8, 0, 8}, 1, inv, s, fs);
+}
+
+void b32_rows(uint32_t* w_rows, uint64_t rows, bool inv, cudaStream_t s) {
+  if (rows % 256) throw Error(kInvalid, "b32_rows: whole chunks");
+  set_smem_attr();
+  const uint64_t ring_rows = std::min<uint64_t>(rows, (uint64_t)kPipeSlots * 256);
+  DevBuf ring(ring_rows * kPipeP1 * sizeof(uint32_t), s);
+  if (inv) conv_rows(w_rows, rows * kTWords, kTLog2, true, s);
+  l1_inner_rows(w_rows, w_rows, ring.as<uint32_t>(), rows, inv ? 1 : 0, nullptr, s);
+}
+
+void b32_cols(uint32_t* w, bool inv, int q, int Q, cudaStream_t s) {
+  DevBuf side(split_side_words(16) * sizeof(uint32_t), s);
+  conv_cols_split(w, side.as<uint32_t>(), 16, inv, s, nullptr, false, q, Q);
+}
+
+void b32_top_pass(uint32_t* lo, const RankPtrs& hi, int q, int Q, cudaStream_t s) {
+  const int lgq = __builtin_ctz((unsigned)Q);
+  const uint64_t n = dist_count(kDistWindow, lgq, b32_wpr(Q));
+  launch_k(top_pass_windows_kernel, dim3(grid_cap((n + 255) / 256, 8)), dim3(256), 0, s, lo, hi, q, lgq, b32_wpr(Q));
+  FPM_LAUNCH_CHECK();
+}
+
+void b32_top_bit_fix(uint32_t* hi0, const uint32_t* hi_last_owner, cudaStream_t s) {
+  launch_k(top_bit_fix_peer_kernel, dim3(1), dim3(32), 0, s, hi0, hi_last_owner);
+  FPM_LAUNCH_CHECK();
+}
+
+// Rank q's 32-bit word ranges of a block under the window distribution (for the copy to the host).
+std::vector<std::pair<uint64_t, uint64_t>> b32_window_ranges(int q, int Q) {
+  std::vector<std::pair<uint64_t, uint64_t>> r;
+  const uint64_t wpr = b32_wpr(Q), wlo = (uint64_t)q * wpr, whi = std::min<uint64_t>(kB32Windows, wlo + wpr);
+  for (uint64_t c = 0; c < 256; ++c) {
+    const int64_t lo = std::max<int64_t>(0, (int64_t)(32 * wlo) - (int64_t)(8 * c));
+    const int64_t hi = std::min<int64_t>((int64_t)kChunkWords, (int64_t)(32 * whi) - (int64_t)(8 * c));
+    if (lo < hi) r.emplace_back(c * kChunkWords + (uint64_t)lo, c * kChunkWords + (uint64_t)hi);
+  }
+  return r;
 }
 
 bool basis_cvt_can_decode(size_t n_bits) {

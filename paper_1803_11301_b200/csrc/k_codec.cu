@@ -25,8 +25,10 @@ namespace {
 constexpr int kSlabWords = 32;                 // words per row per CTA slab -> 1024 elements
 constexpr int kPad = kSlabWords + 1;
 
+// polys: the operand, or (sharded conversion) the replicas of the 2^(11 - lgq)-word column owners:
+// a 32-word slab's column (word index mod 2048) selects polys.p[column >> (11 - lgq)].
 template <int ROWS>  // 64: rows >= 64 are known zero (pipeline); 128: general encode
-__global__ void __launch_bounds__(256) encode_kernel(const uint32_t* __restrict__ poly, uint64_t row_words,
+__global__ void __launch_bounds__(256) encode_kernel(const RankPtrs polys, int lgq, uint64_t row_words,
                                                      uint64_t col0_words, uint64_t nslabs,
                                                      const uint4* __restrict__ tab_g, uint4* __restrict__ ev) {
   pdl_wait();
@@ -47,7 +49,9 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint32_t* __restrict_
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
       const int i = tid + 256 * j, r = i / kSlabWords, c = i % kSlabWords;
-      nx[j] = sl < nslabs ? __ldg(poly + (uint64_t)r * row_words + col0_words + sl * kSlabWords + c) : 0u;
+      const uint64_t wc = col0_words + sl * kSlabWords;
+      const uint32_t* poly = polys.p[lgq ? (int)((wc & 2047) >> (11 - lgq)) : 0];
+      nx[j] = sl < nslabs ? __ldg(poly + (uint64_t)r * row_words + wc + c) : 0u;
     }
   };
   fetch(blockIdx.x);
@@ -89,11 +93,12 @@ __global__ void __launch_bounds__(256) encode_kernel(const uint32_t* __restrict_
 }
 
 // Rows 0..63 go to poly (pitch row_words), rows 64..127 to poly_hi (same pitch); column word offset
-// of slab sl: sl * kSlabWords.
+// of slab sl: col0w + sl * kSlabWords.  Sharded conversion (lgq > 0): the slab's column (word index
+// mod 2048) selects the owner replica polys.p / polys_hi.p[column >> (11 - lgq)].
 __global__ void __launch_bounds__(256) decode_kernel(const uint4* __restrict__ ev, uint64_t nslabs,
                                                      uint64_t row_words,
-                                                     const uint4* __restrict__ tab_g, uint32_t* __restrict__ poly,
-                                                     uint32_t* __restrict__ poly_hi) {
+                                                     const uint4* __restrict__ tab_g, const RankPtrs polys,
+                                                     const RankPtrs polys_hi, int lgq, uint64_t col0w) {
   pdl_wait();
   extern __shared__ uint4 smem4[];
   uint4* tab = smem4;  // rotated 8-bit table of x*E^-1 (gf128.cuh m8 layout)
@@ -129,10 +134,14 @@ __global__ void __launch_bounds__(256) decode_kernel(const uint4* __restrict__ e
       slab[(3 * 32 + lane) * kPad + col] = tr(y.w);
     }
     __syncthreads();
+    const uint64_t wc = col0w + w0;
+    const int own = lgq ? (int)((wc & 2047) >> (11 - lgq)) : 0;
+    uint32_t* const poly = polys.p[own];
+    uint32_t* const poly_hi = polys_hi.p[own];
     for (int i = tid; i < 128 * kSlabWords; i += blockDim.x) {
       const int r = i / kSlabWords, c = i % kSlabWords;
       uint32_t* base = r < 64 ? poly + (uint64_t)r * row_words : poly_hi + (uint64_t)(r - 64) * row_words;
-      base[w0 + c] = slab[r * kPad + c];
+      base[wc + c] = slab[r * kPad + c];
     }
     __syncthreads();
   }
@@ -380,6 +389,18 @@ void flip_encode_tables(int dev, cudaStream_t s) {
 // elements.  rows_live: 64 when rows >= 64 are known zero (pipeline operands), else 128.
 void encode_cols_device(const uint32_t* poly, unsigned l, uint64_t col0, uint64_t ncols, uint4* ev, int rows_live,
                         cudaStream_t s, bool tower) {
+  RankPtrs one{};
+  one.p[0] = const_cast<uint32_t*>(poly);
+  encode_cols_owners(one, 1, l, col0, ncols, ev, rows_live, s, tower);
+}
+
+// polys: Q = 1, 2 or 4 replicas, replica q holding the columns [q 2048/Q, (q+1) 2048/Q) of every 2048-word
+// row (the sharded conversion's column owners; Q > 1 needs rows of >= 2048 words).
+void encode_cols_owners(const RankPtrs& polys, int Q, unsigned l, uint64_t col0, uint64_t ncols, uint4* ev,
+                        int rows_live, cudaStream_t s, bool tower) {
+  const uint32_t* poly = polys.p[0];
+  const int lgq = __builtin_ctz((unsigned)Q);
+  if (Q > 1 && (((uint64_t)1 << l) / 32) % 2048) throw Error(kInvalid, "encode: column owners need 2048-word rows");
   int dev;
   FPM_CUDA(cudaGetDevice(&dev));
   const uint64_t n_p = (uint64_t)1 << l;
@@ -397,12 +418,12 @@ void encode_cols_device(const uint32_t* poly, unsigned l, uint64_t col0, uint64_
     const size_t smem = kM8Uint4 / 2 * sizeof(uint4) + 64 * kPad * sizeof(uint32_t);
     static PerDeviceOnce attr;
     attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
-    launch_k(encode_kernel<64>, dim3(resident_grid(encode_kernel<64>, 256, smem, nslabs)), dim3(256), smem, s, poly, n_p / 32, col0 / 32, nslabs, tab, ev);
+    launch_k(encode_kernel<64>, dim3(resident_grid(encode_kernel<64>, 256, smem, nslabs)), dim3(256), smem, s, polys, lgq, n_p / 32, col0 / 32, nslabs, tab, ev);
   } else {
     const size_t smem = kM8Uint4 * sizeof(uint4) + 128 * kPad * sizeof(uint32_t);
     static PerDeviceOnce attr;
     attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
-    launch_k(encode_kernel<128>, dim3(resident_grid(encode_kernel<128>, 256, smem, nslabs)), dim3(256), smem, s, poly, n_p / 32, col0 / 32, nslabs, tab, ev);
+    launch_k(encode_kernel<128>, dim3(resident_grid(encode_kernel<128>, 256, smem, nslabs)), dim3(256), smem, s, polys, lgq, n_p / 32, col0 / 32, nslabs, tab, ev);
   }
   FPM_LAUNCH_CHECK();
 }
@@ -432,13 +453,28 @@ void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaSt
   static PerDeviceOnce attr;
   attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
   const uint64_t nslabs = ncols / 32 / kSlabWords;
-  launch_k(decode_kernel, dim3(resident_grid(decode_kernel, 256, smem, nslabs)), dim3(256), smem, s, ev, nslabs, ncols / 32, tower ? dt.dec_m8r : dt.dec_m8, slice,
-                                                                                   slice + 64 * (ncols / 32));
+  RankPtrs lo{}, hi{};
+  lo.p[0] = slice;
+  hi.p[0] = slice + 64 * (ncols / 32);
+  launch_k(decode_kernel, dim3(resident_grid(decode_kernel, 256, smem, nslabs)), dim3(256), smem, s, ev, nslabs, ncols / 32, tower ? dt.dec_m8r : dt.dec_m8, lo, hi, 0,
+           (uint64_t)0);
   FPM_LAUNCH_CHECK();
 }
 
 void decode_cols_split_device(const uint4* ev, uint64_t ncols, uint64_t col0, uint64_t row_bits, uint32_t* lo,
                               uint32_t* hi, cudaStream_t s, bool tower) {
+  RankPtrs l{}, h{};
+  l.p[0] = lo;
+  h.p[0] = hi;
+  decode_cols_owners(ev, ncols, col0, row_bits, l, h, 1, s, tower);
+}
+
+// The sharded variant: rows 0..63 into the column owners los.p[q], rows 64..127 into his.p[q] (Q
+// replicas as encode_cols_owners).
+void decode_cols_owners(const uint4* ev, uint64_t ncols, uint64_t col0, uint64_t row_bits, const RankPtrs& los,
+                        const RankPtrs& his, int Q, cudaStream_t s, bool tower) {
+  const int lgq = __builtin_ctz((unsigned)Q);
+  if (Q > 1 && (row_bits / 32) % 2048) throw Error(kInvalid, "decode: column owners need 2048-word rows");
   int dev;
   FPM_CUDA(cudaGetDevice(&dev));
   if (ncols % 1024 || col0 % 1024 || row_bits % 1024 || col0 + ncols > row_bits)
@@ -448,7 +484,8 @@ void decode_cols_split_device(const uint4* ev, uint64_t ncols, uint64_t col0, ui
   static PerDeviceOnce attr;
   attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
   const uint64_t nslabs = ncols / 32 / kSlabWords;
-  launch_k(decode_kernel, dim3(resident_grid(decode_kernel, 256, smem, nslabs)), dim3(256), smem, s, ev, nslabs, row_bits / 32, tower ? dt.dec_m8r : dt.dec_m8, lo + col0 / 32, hi + col0 / 32);
+  launch_k(decode_kernel, dim3(resident_grid(decode_kernel, 256, smem, nslabs)), dim3(256), smem, s, ev, nslabs, row_bits / 32, tower ? dt.dec_m8r : dt.dec_m8, los, his, lgq,
+           col0 / 32);
   FPM_LAUNCH_CHECK();
 }
 

@@ -231,11 +231,14 @@ def test_polymul_multi_logical_ranks(gpu, checker, P, la, lb):
 
 
 @pytest.mark.parametrize("key,P", [("268435456x268435456", 4), ("4294967296x4294967296", 2),
-                                   ("4294967296x4294967296", 8)])
+                                   ("4294967296x4294967296", 4), ("4294967296x4294967296", 8)])
 def test_polymul_multi_baseline_configs(gpu, key, P):
     """BASELINE configs 4 and 5 through fpm_polymul_multi with P logical ranks on GPU 0 against the
-    reference's product hash (config 5: the two 2^32-bit inverse-conversion blocks on ranks 0 and 1,
-    the top pass reading rank 1's block)."""
+    reference's product hash.  Config 5 at P = 2: the two 2^32-bit inverse-conversion blocks on ranks
+    0 and 1, the top pass reading rank 1's block; at P = 4 and 8 the sharded conversion -- every
+    2^32-bit block on P/2 ranks phase by phase (L1_outer by window, L1_inner + T_r by chunk, T_d by
+    column, regathered between phases over peer memory), encode reading and decode writing the column
+    owners, the top pass over the window shares."""
     import hashlib
     import json
     import os
