@@ -203,6 +203,46 @@ fpm_status fpm_decode_cols_split_dev(const uint64_t* d_ev, size_t ncols, size_t 
 fpm_status fpm_i_basis_cvt_block32_dev(uint64_t* d_lo, const uint64_t* d_top, void* stream);
 fpm_status fpm_top_bit_fix_dev(uint64_t* d_hi, void* stream);
 fpm_status fpm_copy_dev(void* d_dst, const void* d_src, size_t bytes, void* stream);
+/* The sharded 2^32-bit conversion (P >= 4 ranks, build_schedule's phases
+ * basis_convert.cpp:60-67, their tiling :278-327): a 2^32-bit block (an operand, or a block of the
+ * 2^33-bit product) on Q = 2 or 4 ranks, each holding a full-size replica (d_w, 2^27 32-bit words) in
+ * which it owns, phase by phase:
+ *    FPM_DIST_WINDOW  the L1_outer windows [q wpr, (q+1) wpr) (wpr = ceil(16448 / Q); window w covers
+ *                     words [32 w - 8 c, 32 w - 8 c + 32) of chunk c, a chunk = 2^19 words)
+ *    FPM_DIST_CHUNK   the chunks [q 256/Q, (q+1) 256/Q)
+ *    FPM_DIST_COLUMN  the words with (index mod 2048) in [q 2048/Q, (q+1) 2048/Q)
+ *  - fpm_b32_regather_dev: d_w receives every 16-byte group it owns under `to` from its owner under
+ *    `from` (d_srcs[0..Q): the group's replicas, peer pointers; d_srcs[q] = d_w);
+ *  - fpm_b32_l1_outer_dev: L1_outer (z = x^(2^24) + x^256 over the 256 chunks) on rank q's windows,
+ *    in place; beyond-window parts to d_side (2 MiB; rank Q-1's holds them all);
+ *  - fpm_b32_l1_outer_fix_dev: its fix-up for chunks [e_lo, e_hi) reading d_side (rank Q-1's):
+ *    forward on the chunk owners after the WINDOW -> CHUNK regather, inverse on rank 0 (all chunks);
+ *  - fpm_b32_rows_dev: L1_inner + T_r (forward) / T_r^-1 + L1_inner^-1 of `rows` rows (whole chunks);
+ *  - fpm_b32_cols_dev: T_d (conv over the row index) on rank q's columns;
+ *  - fpm_b32_top_pass_dev / fpm_b32_top_bit_fix_dev: the 2^33-bit array's top pass on rank q's
+ *    windows of the lower block, reading the upper block's window owners d_his[0..Q); then the upper
+ *    block's bit 0 (d_hi0 = its rank 0) ^= its last bit (d_hi_last = its rank Q-1);
+ *  - fpm_encode_cols_owners_dev / fpm_decode_cols_owners_dev: fpm_encode_cols(_r)_dev /
+ *    fpm_decode_cols_split_dev with the operand / product columns at their owners (Q replicas).
+ * Forward: [WINDOW] l1_outer, regather WINDOW->CHUNK, fix, rows, regather CHUNK->COLUMN, cols, encode.
+ * Inverse: decode, cols, regather COLUMN->CHUNK, rows, regather CHUNK->WINDOW, l1_outer, fix (rank 0),
+ * top pass, top bit fix.  Every step on one rank may only start after the group's previous step. */
+#define FPM_DIST_WINDOW 0
+#define FPM_DIST_CHUNK 1
+#define FPM_DIST_COLUMN 2
+fpm_status fpm_b32_regather_dev(uint64_t* d_w, const uint64_t* const* d_srcs, int from, int to, int q, int Q, void* stream);
+fpm_status fpm_b32_l1_outer_dev(uint64_t* d_w, uint64_t* d_side, int inverse, int q, int Q, void* stream);
+fpm_status fpm_b32_l1_outer_fix_dev(uint64_t* d_w, const uint64_t* d_side, int inverse, unsigned e_lo, unsigned e_hi,
+                                    void* stream);
+fpm_status fpm_b32_rows_dev(uint64_t* d_rows, size_t rows, int inverse, void* stream);
+fpm_status fpm_b32_cols_dev(uint64_t* d_w, int inverse, int q, int Q, void* stream);
+fpm_status fpm_b32_top_pass_dev(uint64_t* d_lo, const uint64_t* const* d_his, int q, int Q, void* stream);
+fpm_status fpm_b32_top_bit_fix_dev(uint64_t* d_hi0, const uint64_t* d_hi_last, void* stream);
+fpm_status fpm_encode_cols_owners_dev(const uint64_t* const* d_polys, int Q, unsigned l, size_t col0, size_t ncols,
+                                      int rows_live, uint64_t* d_ev, int tower, void* stream);
+fpm_status fpm_decode_cols_owners_dev(const uint64_t* d_ev, size_t ncols, size_t col0, size_t row_bits,
+                                      const uint64_t* const* d_los, const uint64_t* const* d_his, int Q, int tower,
+                                      void* stream);
 
 fpm_status fpm_ipc_alloc(size_t bytes, void** d_ptr, uint8_t* handle);
 fpm_status fpm_ipc_open(const uint8_t* handle, void** d_peer);

@@ -99,6 +99,16 @@ def lib():
         L.fpm_i_basis_cvt_block32_dev.argtypes = [vp, vp, vp]
         L.fpm_top_bit_fix_dev.argtypes = [vp, vp]
         L.fpm_copy_dev.argtypes = [vp, vp, sz, vp]
+        pp = C.POINTER(C.c_void_p)
+        L.fpm_b32_regather_dev.argtypes = [vp, pp, C.c_int, C.c_int, C.c_int, C.c_int, vp]
+        L.fpm_b32_l1_outer_dev.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, vp]
+        L.fpm_b32_l1_outer_fix_dev.argtypes = [vp, vp, C.c_int, C.c_uint, C.c_uint, vp]
+        L.fpm_b32_rows_dev.argtypes = [vp, sz, C.c_int, vp]
+        L.fpm_b32_cols_dev.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp]
+        L.fpm_b32_top_pass_dev.argtypes = [vp, pp, C.c_int, C.c_int, vp]
+        L.fpm_b32_top_bit_fix_dev.argtypes = [vp, vp, vp]
+        L.fpm_encode_cols_owners_dev.argtypes = [pp, C.c_int, C.c_uint, sz, sz, C.c_int, vp, C.c_int, vp]
+        L.fpm_decode_cols_owners_dev.argtypes = [vp, sz, sz, sz, pp, pp, C.c_int, C.c_int, vp]
         L.fpm_ipc_alloc.argtypes = [sz, C.POINTER(vp), C.POINTER(C.c_uint8)]
         L.fpm_ipc_open.argtypes = [C.POINTER(C.c_uint8), C.POINTER(vp)]
         L.fpm_ipc_close.argtypes = [vp]

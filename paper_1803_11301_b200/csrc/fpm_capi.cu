@@ -694,6 +694,23 @@ fpm_status host_call(int device, Fn&& fn) {
 
 using namespace fpm;
 
+namespace fpm {
+namespace {
+RankPtrs rank_ptrs(const uint64_t* const* p, int Q) {
+  if (!p || Q < 1 || Q > 4 || (Q & (Q - 1))) throw Error(kInvalid, "sharded conversion: 1, 2 or 4 replicas");
+  RankPtrs r{};
+  for (int q = 0; q < Q; ++q) {
+    if (!p[q]) throw Error(kInvalid, "sharded conversion: null replica pointer");
+    r.p[q] = reinterpret_cast<uint32_t*>(const_cast<uint64_t*>(p[q]));
+  }
+  return r;
+}
+void check_q(int q, int Q) {
+  if (Q < 2 || Q > 4 || (Q & (Q - 1)) || q < 0 || q >= Q) throw Error(kInvalid, "sharded conversion: 2 or 4 ranks, 0 <= q < Q");
+}
+}  // namespace
+}  // namespace fpm
+
 extern "C" {
 
 const char* fpm_last_error(void) { return g_err.c_str(); }
@@ -1071,6 +1088,92 @@ fpm_status fpm_load_operand_dev(uint64_t* d_dst, size_t dst_words, const uint64_
     if (!dst_words) return;
     launch_k(load_operand_kernel, dim3(grid_1d(dst_words)), dim3(256), 0, (cudaStream_t)stream, d_dst, dst_words, d_src, src_bits);
     FPM_LAUNCH_CHECK();
+  });
+}
+
+
+fpm_status fpm_b32_regather_dev(uint64_t* d_w, const uint64_t* const* d_srcs, int from, int to, int q, int Q, void* stream) {
+  return guard([&] {
+    require_device();
+    check_q(q, Q);
+    if (!d_w || from < 0 || from > 2 || to < 0 || to > 2 || from == to) throw Error(kInvalid, "regather: bad arguments");
+    b32_regather(reinterpret_cast<uint32_t*>(d_w), rank_ptrs(d_srcs, Q), from, to, q, Q, (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_b32_l1_outer_dev(uint64_t* d_w, uint64_t* d_side, int inverse, int q, int Q, void* stream) {
+  return guard([&] {
+    require_device();
+    check_q(q, Q);
+    if (!d_w || !d_side) throw Error(kInvalid, "b32_l1_outer: null pointer");
+    b32_l1_outer(reinterpret_cast<const uint32_t*>(d_w), reinterpret_cast<uint32_t*>(d_w), reinterpret_cast<uint32_t*>(d_side),
+                 inverse != 0, q, Q, (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_b32_l1_outer_fix_dev(uint64_t* d_w, const uint64_t* d_side, int inverse, unsigned e_lo, unsigned e_hi,
+                                    void* stream) {
+  return guard([&] {
+    require_device();
+    if (!d_w || !d_side || e_lo > e_hi || e_hi > 256) throw Error(kInvalid, "b32_l1_outer_fix: bad arguments");
+    b32_l1_outer_fix(reinterpret_cast<uint32_t*>(d_w), reinterpret_cast<const uint32_t*>(d_side), inverse != 0, e_lo, e_hi,
+                     (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_b32_rows_dev(uint64_t* d_rows, size_t rows, int inverse, void* stream) {
+  return guard([&] {
+    require_device();
+    if (!d_rows || !rows || rows % 256 || rows > 65536) throw Error(kInvalid, "b32_rows: whole chunks of 256 rows");
+    b32_rows(reinterpret_cast<uint32_t*>(d_rows), rows, inverse != 0, (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_b32_cols_dev(uint64_t* d_w, int inverse, int q, int Q, void* stream) {
+  return guard([&] {
+    require_device();
+    check_q(q, Q);
+    if (!d_w) throw Error(kInvalid, "b32_cols: null block");
+    b32_cols(reinterpret_cast<uint32_t*>(d_w), inverse != 0, q, Q, (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_b32_top_pass_dev(uint64_t* d_lo, const uint64_t* const* d_his, int q, int Q, void* stream) {
+  return guard([&] {
+    require_device();
+    check_q(q, Q);
+    if (!d_lo) throw Error(kInvalid, "b32_top_pass: null block");
+    b32_top_pass(reinterpret_cast<uint32_t*>(d_lo), rank_ptrs(d_his, Q), q, Q, (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_b32_top_bit_fix_dev(uint64_t* d_hi0, const uint64_t* d_hi_last, void* stream) {
+  return guard([&] {
+    require_device();
+    if (!d_hi0 || !d_hi_last) throw Error(kInvalid, "b32_top_bit_fix: null pointer");
+    b32_top_bit_fix(reinterpret_cast<uint32_t*>(d_hi0), reinterpret_cast<const uint32_t*>(d_hi_last), (cudaStream_t)stream);
+  });
+}
+
+fpm_status fpm_encode_cols_owners_dev(const uint64_t* const* d_polys, int Q, unsigned l, size_t col0, size_t ncols,
+                                      int rows_live, uint64_t* d_ev, int tower, void* stream) {
+  return guard([&] {
+    require_device();
+    if (!d_ev) throw Error(kInvalid, "encode_cols_owners: null output");
+    if (rows_live != 64 && rows_live != 128) throw Error(kInvalid, "encode_cols_owners: rows_live must be 64 or 128");
+    encode_cols_owners(rank_ptrs(d_polys, Q), Q, l, col0, ncols, reinterpret_cast<uint4*>(d_ev), rows_live,
+                       (cudaStream_t)stream, tower != 0);
+  });
+}
+
+fpm_status fpm_decode_cols_owners_dev(const uint64_t* d_ev, size_t ncols, size_t col0, size_t row_bits,
+                                      const uint64_t* const* d_los, const uint64_t* const* d_his, int Q, int tower,
+                                      void* stream) {
+  return guard([&] {
+    require_device();
+    if (!d_ev) throw Error(kInvalid, "decode_cols_owners: null input");
+    decode_cols_owners(reinterpret_cast<const uint4*>(d_ev), ncols, col0, row_bits, rank_ptrs(d_los, Q), rank_ptrs(d_his, Q), Q,
+                       (cudaStream_t)stream, tower != 0);
   });
 }
 

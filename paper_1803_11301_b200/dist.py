@@ -294,6 +294,13 @@ class DevBuf:
         return self.n
 
 
+class _Owners:
+    """A converted operand held at its column owners (Q peer replicas, a ctypes pointer array)."""
+
+    def __init__(self, ptrs, Q: int):
+        self.ptrs, self.Q = ptrs, Q
+
+
 class PeerBackend(GpuBackend):
     """GpuBackend with the exchanged layers fused into their butterflies over peer memory (NVLink):
     each rank keeps both operands' evaluation slices in ping-pong pairs of peer-shareable buffers
@@ -336,10 +343,20 @@ class PeerBackend(GpuBackend):
 
     # -- split conversions (P >= 2)
     @staticmethod
+    def _sharded(plan) -> bool:
+        """The sharded 2^32-bit conversion (fpm_b32_*; as fpm_polymul_multi): P >= 4 ranks, P/2 <= 4 per
+        block, a 2^33-bit product of two operands that each fill a 2^32-bit conversion."""
+        cnt = lambda bits: max(32, 1 << (bits - 1).bit_length())  # noqa: E731
+        return (4 <= plan.P <= 8 and plan.n_bits == 1 << 33 and cnt(plan.a_bits) == 1 << 32
+                and cnt(plan.b_bits) == 1 << 32)
+
+    @staticmethod
     def _shared_sizes(plan, P, rank):
         if P < 2:
             return {}
         n = plan.n_bits
+        if PeerBackend._sharded(plan):  # every rank: a full-size block replica + L1_outer side rows
+            return {f"r{rank}": n // 16, f"s{rank}": 256 * 2048 * 4}
         out = {}
         if rank == 0:
             out["x0"] = n // 16
@@ -350,9 +367,44 @@ class PeerBackend(GpuBackend):
                 out["y1"] = n // 16
         return out
 
+    def _ptrs(self, names):
+        import ctypes as C
+        return (C.c_void_p * len(names))(*[self.arrays[nm] for nm in names])
+
+    def convert_operands_sharded(self, a, a_bits, b, b_bits, plan):
+        """The sharded conversion: operand k on ranks [kQ, (k+1)Q) (Q = P/2), phase by phase in the
+        ranks' replicas -- L1_outer by window, L1_inner + T_r by chunk, T_d by column -- with a barrier
+        and a peer-memory regather between phases.  Returns, per operand, its column owners."""
+        P, rank = self.world()
+        Q = P // 2
+        k, q = divmod(rank, Q)
+        s = self._s()
+        L = self.L.lib()
+        chk = self.L._check
+        mine, side = self.arrays[f"r{rank}"], self.arrays[f"s{rank}"]
+        group = self._ptrs([f"r{k * Q + j}" for j in range(Q)])
+        x, bits = ((a, a_bits), (b, b_bits))[k]
+        chk(L.fpm_load_operand_dev(mine, plan.n_bits // 128, x.data_ptr(), bits, s))  # every rank holds the inputs
+        chk(L.fpm_b32_l1_outer_dev(mine, side, 0, q, Q, s))
+        self._barrier()
+        chk(L.fpm_b32_regather_dev(mine, group, 0, 1, q, Q, s))  # WINDOW -> CHUNK
+        self._barrier()
+        c0, c1 = q * 256 // Q, (q + 1) * 256 // Q
+        chk(L.fpm_b32_l1_outer_fix_dev(mine, self.arrays[f"s{k * Q + Q - 1}"], 0, c0, c1, s))
+        chk(L.fpm_b32_rows_dev(mine + c0 * 256 * 2048 * 4, (c1 - c0) * 256, 0, s))
+        self._barrier()
+        chk(L.fpm_b32_regather_dev(mine, group, 1, 2, q, Q, s))  # CHUNK -> COLUMN
+        self._barrier()
+        chk(L.fpm_b32_cols_dev(mine, 0, q, Q, s))
+        self._barrier()  # both converted operands final at their column owners
+        return [_Owners(self._ptrs([f"r{kk * Q + j}" for j in range(Q)]), Q) for kk in (0, 1)]
+
     def convert_operands_split(self, a, a_bits, b, b_bits, plan):
         """Rank 0 converts operand a, rank 1 operand b (each into its own shared array); every rank
-        then reads both converted operands (peer memory) for its encode."""
+        then reads both converted operands (peer memory) for its encode.  (P >= 4 with 2^32-bit
+        operands: the sharded conversion.)"""
+        if self._sharded(plan):
+            return self.convert_operands_sharded(a, a_bits, b, b_bits, plan)
         P, rank = self.world()
         s = self._s()
         L = self.L.lib()
@@ -369,10 +421,67 @@ class PeerBackend(GpuBackend):
         dev = self.torch.device("cuda", self.torch.cuda.current_device())
         return [DevBuf(self.arrays["x0"], half_words, dev), DevBuf(self.arrays["x1"], half_words, dev)]
 
+    def finish_sharded(self, c, plan, out_bits, tower=False):
+        """The sharded inverse: decode into the column owners of the lower (ranks [0, Q)) and upper
+        ([Q, 2Q)) 2^32-bit blocks, T_d^-1 by column, T_r^-1 + L1_inner^-1 by chunk, L1_outer^-1 by
+        window (+ fix on rank 0), the top pass, the upper bit fix, a final regather to chunks; then
+        every rank copies the whole product from the chunk owners."""
+        P, rank = self.world()
+        Q = P // 2
+        k, q = divmod(rank, Q)
+        s = self._s()
+        L = self.L.lib()
+        chk = self.L._check
+        mine, side = self.arrays[f"r{rank}"], self.arrays[f"s{rank}"]
+        los = self._ptrs([f"r{j}" for j in range(Q)])
+        his = self._ptrs([f"r{Q + j}" for j in range(Q)])
+        group = los if k == 0 else his
+        chk(L.fpm_decode_cols_owners_dev(c.data_ptr(), plan.m, plan.col0, plan.n_p, los, his, Q, int(tower), s))
+        self._barrier()
+        chk(L.fpm_b32_cols_dev(mine, 1, q, Q, s))
+        self._barrier()
+        chk(L.fpm_b32_regather_dev(mine, group, 2, 1, q, Q, s))  # COLUMN -> CHUNK
+        self._barrier()
+        c0, c1 = q * 256 // Q, (q + 1) * 256 // Q
+        chk(L.fpm_b32_rows_dev(mine + c0 * 256 * 2048 * 4, (c1 - c0) * 256, 1, s))
+        self._barrier()
+        chk(L.fpm_b32_regather_dev(mine, group, 1, 0, q, Q, s))  # CHUNK -> WINDOW
+        self._barrier()
+        chk(L.fpm_b32_l1_outer_dev(mine, side, 1, q, Q, s))
+        self._barrier()
+        if q == 0:
+            chk(L.fpm_b32_l1_outer_fix_dev(mine, self.arrays[f"s{k * Q + Q - 1}"], 1, 0, 256, s))
+        self._barrier()
+        if k == 0:
+            chk(L.fpm_b32_top_pass_dev(mine, his, q, Q, s))
+        self._barrier()  # the lower block read the upper block's (pre-fix) bit 0
+        if rank == Q:
+            chk(L.fpm_b32_top_bit_fix_dev(mine, self.arrays[f"r{2 * Q - 1}"], s))
+        self._barrier()
+        chk(L.fpm_b32_regather_dev(mine, group, 0, 1, q, Q, s))  # WINDOW -> CHUNK
+        self._barrier()  # the product is final at its chunk owners
+        t = self.torch
+        w = (out_bits + 63) // 64
+        out = t.empty(w, dtype=t.int64, device=c.device)
+        per = (1 << 26) // Q  # 64-bit words of a rank's chunks
+        for g in range(P):
+            kk, qq = divmod(g, Q)
+            w0 = kk * (1 << 26) + qq * per
+            w1 = min(w, w0 + per)
+            if w0 < w1:
+                chk(L.fpm_copy_dev(out.data_ptr() + w0 * 8, self.arrays[f"r{g}"] + qq * per * 8, (w1 - w0) * 8, s))
+        if out_bits % 64:
+            out[w - 1] &= (1 << (out_bits % 64)) - 1
+        self._barrier()  # every rank copied out before the replicas are reused
+        return out
+
     def finish_split(self, c, plan, out_bits, tower=False):
         """Every rank decodes its columns straight into the product array(s); the inverse conversion
         runs on rank 0 (n <= 2^32 bits) or as the two 2^32-bit blocks on ranks 1 and 0 (2^33 bits:
-        the lower block's top pass reads rank 1's final block); every rank then copies the product."""
+        the lower block's top pass reads rank 1's final block); every rank then copies the product.
+        (P >= 4 with 2^32-bit operands: the sharded inverse.)"""
+        if self._sharded(plan):
+            return self.finish_sharded(c, plan, out_bits, tower)
         P, rank = self.world()
         s = self._s()
         L = self.L.lib()
@@ -473,8 +582,12 @@ class PeerBackend(GpuBackend):
         k = self.n_enc  # (poly: a tensor, or a DevBuf over a peer rank's converted operand)
         self.n_enc += 1
         ev = self.mine[2 * k]
-        f = self.L.lib().fpm_encode_cols_r_dev if tower else self.L.lib().fpm_encode_cols_dev
-        self.L._check(f(poly.data_ptr(), l, col0, ncols, 64, ev.data_ptr(), self._s()))
+        if isinstance(poly, _Owners):  # the sharded conversion's column owners
+            self.L._check(self.L.lib().fpm_encode_cols_owners_dev(poly.ptrs, poly.Q, l, col0, ncols, 64, ev.data_ptr(),
+                                                                  int(tower), self._s()))
+        else:
+            f = self.L.lib().fpm_encode_cols_r_dev if tower else self.L.lib().fpm_encode_cols_dev
+            self.L._check(f(poly.data_ptr(), l, col0, ncols, 64, ev.data_ptr(), self._s()))
         self.cur[k] = 0
         return ev
 

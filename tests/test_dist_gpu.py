@@ -258,12 +258,13 @@ def test_polymul_multi_rejects_bad_rank_counts(gpu):
         gpu.fp_polymul_multi(a, 1 << 12, a, 1 << 12, [0] * 64, field=gpu.FIELD_GF128)
 
 
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", [2, 4, 8])
 def test_sharded_peer_config5_split_conversions(gpu, P):
-    """BASELINE config 5 through dist.polymul_sharded with PeerBackend and thread ranks: the split
-    conversions (operand a on rank 0, b on rank 1, encode from peer memory), the decode straight into
-    the two 2^32-bit blocks on ranks 0 and 1 and their separate inverse conversions with the fused
-    top pass; the product hash against the reference's."""
+    """BASELINE config 5 through dist.polymul_sharded with PeerBackend and thread ranks: at P = 2 the
+    split conversions (operand a on rank 0, b on rank 1, encode from peer memory), the decode straight
+    into the two 2^32-bit blocks on ranks 0 and 1 and their separate inverse conversions with the
+    fused top pass; at P = 4, 8 the sharded conversion (fpm_b32_*: every block on P/2 ranks phase by
+    phase); the product hash against the reference's."""
     import hashlib
     import json
     import os

@@ -43,3 +43,33 @@ def test_peer_backend_two_processes(gpu, checker, tmp_path, P, la, lb):
         assert p.returncode == 0, f"rank {r} failed:\n{logs[r][-3000:]}"
     for r in range(P):
         assert np.array_equal(np.load(outs[r]), want), r
+
+
+@pytest.mark.parametrize("P", [4])
+def test_peer_backend_processes_config5_sharded_conversion(gpu, tmp_path, P):
+    """BASELINE config 5 over P separate processes (gloo control, CUDA-IPC data): the sharded
+    conversion -- every 2^32-bit block on P/2 processes phase by phase, regathered through the other
+    processes' IPC replicas (fpm_b32_*), encode / decode at the column owners -- bit-exact against the
+    reference's product hash on every rank."""
+    import json
+    with open(os.path.join(HERE, "golden", "reference_meta.json")) as f:
+        c = json.load(f)["configs"]["4294967296x4294967296"]
+    port = _free_port()
+    outs = [str(tmp_path / f"r{r}.hash") for r in range(P)]
+    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "_ipc_rank.py"), str(r), str(P), str(port),
+                               str(c["a_bits"]), str(c["b_bits"]), "1", outs[r], str(c["seed_a"]), str(c["seed_b"])],
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+             for r in range(P)]
+    logs = []
+    try:
+        for p in procs:
+            logs.append(p.communicate(timeout=900)[0])
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    for r, p in enumerate(procs):
+        assert p.returncode == 0, f"rank {r} failed:\n{logs[r][-3000:]}"
+    for r in range(P):
+        with open(outs[r]) as f:
+            assert f.read() == c["blake2b128"], r
