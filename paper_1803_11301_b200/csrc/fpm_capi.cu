@@ -184,8 +184,8 @@ struct Gf128Ops {
     encode_device_rows(p, l, ev, kLiveRows, s, r);
   }
   static void decode(const E* ev, unsigned l, uint32_t* p, cudaStream_t s, bool r) { decode_device(ev, l, p, s, r); }
-  static void top(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s, bool r) {
-    butterfly_top_device(ev, l, T, inv, tw, s, r);
+  static void top(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s, bool r, E* ev2 = nullptr) {
+    butterfly_top_device(ev, l, T, inv, tw, s, r, ev2);
   }
   static void tile(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s) {
     butterfly_tile_device(ev, l, T, inv, tw, s);
@@ -212,8 +212,9 @@ struct Gf64Ops {
     encode64_device(p, l, ev, kLiveRows, s, r);
   }
   static void decode(const E* ev, unsigned l, uint32_t* p, cudaStream_t s, bool r) { decode64_device(ev, l, p, s, r); }
-  static void top(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s, bool r) {
+  static void top(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s, bool r, E* ev2 = nullptr) {
     butterfly64_top_device(ev, l, T, inv, tw, s, r);
+    if (ev2) butterfly64_top_device(ev2, l, T, inv, tw, s, r);
   }
   static void tile(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s) {
     butterfly64_tile_device(ev, l, T, inv, tw, s);
@@ -275,6 +276,10 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
   const uint64_t* xs[2] = {d_a, d_b};
   const size_t xbits[2] = {a_bits, b_bits};
   E* es[2] = {EA.as<E>(), EB.as<E>()};
+  // Device-resident operands: both conversions first, then the top passes of both EvalVecs in one
+  // launch per layer pair (one set of twiddle tables per CTA for both).  Host-buffer calls keep
+  // operand a's transforms ahead of operand b's upload.
+  const bool joint_top = !io && fuse_ab;
   for (int k = 0; k < 2; ++k) {
     wait_operand(k);
     clk.mark(kStBasis);
@@ -295,9 +300,14 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     }
     clk.mark(kStEncode);
     if (!fused) F::encode(work32, l, es[k], s, rep);
+    if (joint_top) continue;
     clk.mark(kStBfly);
     F::top(es[k], l, T, false, tw, s, rep);
     if (k == 0 && !fuse_ab) F::tile(es[k], l, T, false, tw, s);
+  }
+  if (joint_top) {
+    clk.mark(kStBfly);
+    F::top(es[0], l, T, false, tw, s, rep, es[1]);
   }
   clk.mark(kStPointwise);  // + operand b's (and a's) bottom T forward and the bottom T inverse layers (fused)
   if (fuse_ab) F::fused2(EA.as<E>(), EB.as<E>(), l, T, tw, s, rep);

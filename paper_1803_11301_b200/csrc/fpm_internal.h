@@ -277,7 +277,7 @@ void pointwise_device(const uint4* u, const uint4* v, uint4* out, size_t n, cuda
 unsigned fft_tile_log2(unsigned l);
 // tower: the elements are in the tower representation R (tables built in R).
 void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s,
-                          bool tower = false);
+                          bool tower = false, uint4* ev2 = nullptr);
 void butterfly_tile_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s);
 // Fused: forward layers [0, T) of b's tiles, pointwise * a, inverse layers [0, T).
 bool tile_fused2_enabled(unsigned T);

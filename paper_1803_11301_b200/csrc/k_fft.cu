@@ -104,13 +104,27 @@ __global__ void __launch_bounds__(256) fft_top_kernel(uint4* __restrict__ ev, un
 // w(i, 2B) and (q2,q3) with w(i, 2B+1).  The three M8 tables (192 KiB) are built by three groups of
 // 256 threads; one 768-thread CTA per SM then streams its quads.
 constexpr int kTop4Threads = 768;
+#ifndef FPM_TOP4_STREAM
+#define FPM_TOP4_STREAM 1
+#endif
+__device__ __forceinline__ uint4 ld_na(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_cs(uint4* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
 constexpr size_t kTop4Smem = (3 * (size_t)kM8Uint4 + 3 * 144 + 136) * sizeof(uint4);  // + to_r (tower)
 
 // NT: 768 threads (80 registers; three table groups at once) or 512 (128 registers: the
 // pre-rotated lookups in both directions; the third table in a second build round).
+// ev2 (optional): a second evaluation vector at the same layers and twiddles (both operands of a
+// product): every CTA runs its quads of both with one set of tables.
 template <bool INV, bool R, int NT = kTop4Threads>
 __global__ void __launch_bounds__(NT, 1) fft_top4_kernel(uint4* __restrict__ ev, unsigned l, unsigned i,
-                                                          int qpc, TwiddleSrc tw) {
+                                                          int qpc, TwiddleSrc tw, uint4* __restrict__ ev2) {
   pdl_wait();
   extern __shared__ uint4 sm4[];
   uint4* t1 = sm4;                   // w(i+1, B)
@@ -122,6 +136,7 @@ __global__ void __launch_bounds__(NT, 1) fft_top4_kernel(uint4* __restrict__ ev,
   const uint64_t quad0 = (uint64_t)blockIdx.x * qpc;  // qpc <= h: a CTA never straddles a block
   const uint64_t B = quad0 >> i;
   const int tid = threadIdx.x, grp = tid >> 8, lt = tid & 255;
+  const int nq = ev2 ? 2 * qpc : qpc;
   // the twiddles (global loads) are issued before the to_r staging barrier: one L2 round trip, not two
   constexpr int kRounds = (3 + NT / 256 - 1) / (NT / 256);
   uint4 ws[kRounds];
@@ -166,14 +181,18 @@ __global__ void __launch_bounds__(NT, 1) fft_top4_kernel(uint4* __restrict__ ev,
     __syncthreads();
   }
   const int q = tid & 7;
-  uint4* base = ev + (B << (i + 2));
-  const uint64_t j0 = quad0 & (h - 1);
+  const uint64_t off = (B << (i + 2)) + (quad0 & (h - 1));
   const M8Base mb = m8_base(t1, q);  // (inverse only)
   constexpr uint32_t kA = kM8Uint4 * 16u, kB = 2u * kM8Uint4 * 16u;  // t0a, t0b after t1
 #pragma unroll 1
-  for (int k = tid; k < qpc; k += NT) {
-    uint4* p = base + j0 + k;
+  for (int k = tid; k < nq; k += NT) {
+    uint4* p = (k < qpc ? ev + k : ev2 + (k - qpc)) + off;
+#if FPM_TOP4_STREAM
+    // read-once / write-once quads: no L1 allocation (the L1TEX data path is the pass's binding unit)
+    uint4 a0 = ld_na(p), a1 = ld_na(p + h), a2 = ld_na(p + 2 * h), a3 = ld_na(p + 3 * h);
+#else
     uint4 a0 = p[0], a1 = p[h], a2 = p[2 * h], a3 = p[3 * h];
+#endif
     if (!INV && NT == 768) {  // (m8_mul_r here spills at the 80 registers of a 768-thread CTA: 12.8 vs 11.3 ms)
       a0 = x4(a0, m8_mul(t1, a2, q));
       a1 = x4(a1, m8_mul(t1, a3, q));
@@ -202,10 +221,17 @@ __global__ void __launch_bounds__(NT, 1) fft_top4_kernel(uint4* __restrict__ ev,
       a0 = x4(a0, m8_mul_r(mb, a2, q));
       a1 = x4(a1, m8_mul_r(mb, a3, q));
     }
+#if FPM_TOP4_STREAM
+    st_cs(p, a0);
+    st_cs(p + h, a1);
+    st_cs(p + 2 * h, a2);
+    st_cs(p + 3 * h, a3);
+#else
     p[0] = a0;
     p[h] = a1;
     p[2 * h] = a2;
     p[3 * h] = a3;
+#endif
   }
   pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
@@ -782,7 +808,8 @@ TwiddleSrc make_twiddle_src(int device, unsigned l, U128 base) {
 }
 
 template <bool R>
-void top_passes(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s) {
+void top_passes(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s,
+                uint4* ev2 = nullptr) {
   const size_t smem = kM8Uint4 * sizeof(uint4);
   static PerDeviceOnce attr;
   attr.run([&] { set_smem(fft_top_kernel<false, R>, smem); set_smem(fft_top_kernel<true, R>, smem); });
@@ -801,9 +828,12 @@ void top_passes(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSr
   if (T < 8 || ctas == 0) throw Error(kInvalid, "butterfly_top: layer too small for the table layer kernel");
   auto radix2 = [&](unsigned i) {
     const uint64_t p = std::min<uint64_t>(ppc, (uint64_t)1 << i);  // a CTA stays inside one block
-    if (!inverse) launch_k(fft_top_kernel<false, R>, dim3((unsigned)(pairs / p)), dim3(256), smem, s, ev, l, i, (int)p, tw);
-    else launch_k(fft_top_kernel<true, R>, dim3((unsigned)(pairs / p)), dim3(256), smem, s, ev, l, i, (int)p, tw);
-    FPM_LAUNCH_CHECK();
+    for (uint4* e : {ev, ev2}) {
+      if (!e) continue;
+      if (!inverse) launch_k(fft_top_kernel<false, R>, dim3((unsigned)(pairs / p)), dim3(256), smem, s, e, l, i, (int)p, tw);
+      else launch_k(fft_top_kernel<true, R>, dim3((unsigned)(pairs / p)), dim3(256), smem, s, e, l, i, (int)p, tw);
+      FPM_LAUNCH_CHECK();
+    }
   };
   // layer pairs (i+1, i) from the top down (forward) / bottom up (inverse); an odd count leaves
   // the lowest top layer T to the one-layer kernel.
@@ -824,11 +854,11 @@ void top_passes(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSr
     }();
     const int nt = knob == 512 || knob == 768 ? knob : (inverse ? kTop4Threads : 512);
     if (nt == 512) {
-      if (!inverse) launch_k(fft_top4_kernel<false, R, 512>, dim3((unsigned)(quads / q)), dim3(512), kTop4Smem, s, ev, l, i, (int)q, tw);
-      else launch_k(fft_top4_kernel<true, R, 512>, dim3((unsigned)(quads / q)), dim3(512), kTop4Smem, s, ev, l, i, (int)q, tw);
+      if (!inverse) launch_k(fft_top4_kernel<false, R, 512>, dim3((unsigned)(quads / q)), dim3(512), kTop4Smem, s, ev, l, i, (int)q, tw, ev2);
+      else launch_k(fft_top4_kernel<true, R, 512>, dim3((unsigned)(quads / q)), dim3(512), kTop4Smem, s, ev, l, i, (int)q, tw, ev2);
     } else {
-      if (!inverse) launch_k(fft_top4_kernel<false, R>, dim3((unsigned)(quads / q)), dim3(kTop4Threads), kTop4Smem, s, ev, l, i, (int)q, tw);
-      else launch_k(fft_top4_kernel<true, R>, dim3((unsigned)(quads / q)), dim3(kTop4Threads), kTop4Smem, s, ev, l, i, (int)q, tw);
+      if (!inverse) launch_k(fft_top4_kernel<false, R>, dim3((unsigned)(quads / q)), dim3(kTop4Threads), kTop4Smem, s, ev, l, i, (int)q, tw, ev2);
+      else launch_k(fft_top4_kernel<true, R>, dim3((unsigned)(quads / q)), dim3(kTop4Threads), kTop4Smem, s, ev, l, i, (int)q, tw, ev2);
     }
     FPM_LAUNCH_CHECK();
   };
@@ -844,10 +874,10 @@ void top_passes(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSr
 }
 
 void butterfly_top_device(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc& tw, cudaStream_t s,
-                          bool tower) {
+                          bool tower, uint4* ev2) {
   if (l <= T) return;
-  if (tower) top_passes<true>(ev, l, T, inverse, tw, s);
-  else top_passes<false>(ev, l, T, inverse, tw, s);
+  if (tower) top_passes<true>(ev, l, T, inverse, tw, s, ev2);
+  else top_passes<false>(ev, l, T, inverse, tw, s, ev2);
 }
 
 // One thread per butterfly of a tile layer (2^(T-1) pairs), at most 256: small tiles run more CTAs
