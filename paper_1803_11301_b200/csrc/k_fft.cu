@@ -837,12 +837,15 @@ void top_passes(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSr
   };
   // layer pairs (i+1, i) from the top down (forward) / bottom up (inverse); an odd count leaves
   // the lowest top layer T to the one-layer kernel.
-  // Quads per CTA: 8192 amortise the three 64 KiB table builds at 2^32 bits; small transforms go
+  // Quads per CTA: up to 16384 amortise the three 64 KiB table builds at 2^32 bits; small transforms go
   // down to 128 quads so that the pass spreads over the SMs (at l = 14 a 1024-quad floor left 4 CTAs
   // per pass, ~10 us each, dominated by one CTA's table builds).
   const uint64_t quads = ((uint64_t)1 << l) / 4;
   const uint64_t qmin = l >= 16 ? 1024 : 128;  // l = 18: 1024 beats 128 (0.104 vs 0.154 ms of passes)
-  uint64_t qpc = 8192;
+#ifndef FPM_TOP4_QMAX
+#define FPM_TOP4_QMAX 16384  // 2^32-bit product: 46.09 -> 45.72 ms vs 8192 (half the table builds)
+#endif
+  uint64_t qpc = FPM_TOP4_QMAX;
   while (qpc > qmin && quads / qpc < (uint64_t)sms() * 4) qpc /= 2;
   auto radix4 = [&](unsigned i) {
     const unsigned q = (unsigned)std::min<uint64_t>(qpc, (uint64_t)1 << i);
