@@ -279,7 +279,7 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
   // Device-resident operands: both conversions first, then the top passes of both EvalVecs in one
   // launch per layer pair (one set of twiddle tables per CTA for both).  Host-buffer calls keep
   // operand a's transforms ahead of operand b's upload.
-  const bool joint_top = !io && fuse_ab;
+  const bool joint_top = !io;
   for (int k = 0; k < 2; ++k) {
     wait_operand(k);
     clk.mark(kStBasis);
@@ -308,6 +308,7 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
   if (joint_top) {
     clk.mark(kStBfly);
     F::top(es[0], l, T, false, tw, s, rep, es[1]);
+    if (!fuse_ab) F::tile(es[0], l, T, false, tw, s);
   }
   clk.mark(kStPointwise);  // + operand b's (and a's) bottom T forward and the bottom T inverse layers (fused)
   if (fuse_ab) F::fused2(EA.as<E>(), EB.as<E>(), l, T, tw, s, rep);
