@@ -213,8 +213,7 @@ struct Gf64Ops {
   }
   static void decode(const E* ev, unsigned l, uint32_t* p, cudaStream_t s, bool r) { decode64_device(ev, l, p, s, r); }
   static void top(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s, bool r, E* ev2 = nullptr) {
-    butterfly64_top_device(ev, l, T, inv, tw, s, r);
-    if (ev2) butterfly64_top_device(ev2, l, T, inv, tw, s, r);
+    butterfly64_top_device(ev, l, T, inv, tw, s, r, ev2);
   }
   static void tile(E* ev, unsigned l, unsigned T, bool inv, const Tw& tw, cudaStream_t s) {
     butterfly64_tile_device(ev, l, T, inv, tw, s);

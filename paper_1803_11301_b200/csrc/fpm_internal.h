@@ -302,7 +302,7 @@ void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigne
 unsigned fft64_tile_log2(unsigned l);
 void butterfly64_device(uint2* ev, unsigned l, uint64_t base, bool inverse, cudaStream_t s);
 void butterfly64_top_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s,
-                            bool tower = false);
+                            bool tower = false, uint2* ev2 = nullptr);
 bool tile64_tower_enabled(unsigned T);
 void butterfly64_tile_tower_device(const uint2* ea, uint2* eb, unsigned l, unsigned T, const TwiddleSrc64& tw,
                                    cudaStream_t s);

@@ -82,9 +82,10 @@ __global__ void __launch_bounds__(256) fft64_top_kernel(uint2* __restrict__ ev, 
 constexpr int kTop4Threads64 = 384;
 constexpr size_t kTop4Smem64 = (3 * (size_t)kG8Uint2 + 3 * kG8Rows + 72) * sizeof(uint2);  // + to_r (tower)
 
+// ev2 (optional): the other operand at the same layers and twiddles (one set of tables for both).
 template <bool INV, bool R>
 __global__ void __launch_bounds__(kTop4Threads64, 2) fft64_top4_kernel(uint2* __restrict__ ev, unsigned i, int qpc,
-                                                                       TwiddleSrc64 tw) {
+                                                                       TwiddleSrc64 tw, uint2* __restrict__ ev2) {
   pdl_wait();
   extern __shared__ uint2 sm64[];
   uint2* t1 = sm64;                    // w(i+1, B); then w(i, 2B) at + kG8Uint2, w(i, 2B+1) at + 2 kG8Uint2
@@ -157,9 +158,11 @@ __global__ void __launch_bounds__(kTop4Threads64, 2) fft64_top4_kernel(uint2* __
       a1 = x2(a1, g8_mul_r(gb, a3, lane));
     }
   };
+  const int nq = ev2 ? 2 * qpc : qpc;
+  const uint64_t off = (uint64_t)(base - ev) + j0;
 #pragma unroll 1
-  for (int k = 2 * tid; k < qpc; k += 2 * kTop4Threads64) {
-    uint4* p = reinterpret_cast<uint4*>(base + j0 + k);
+  for (int k = 2 * tid; k < nq; k += 2 * kTop4Threads64) {
+    uint4* p = reinterpret_cast<uint4*>((k < qpc ? ev + k : ev2 + (k - qpc)) + off);
     const uint64_t h2 = h / 2;
     uint4 v0 = p[0], v1 = p[h2], v2 = p[2 * h2], v3 = p[3 * h2];
     uint2 a0 = make_uint2(v0.x, v0.y), a1 = make_uint2(v1.x, v1.y), a2 = make_uint2(v2.x, v2.y),
@@ -667,7 +670,8 @@ TwiddleSrc64 make_twiddle_src64(int device, unsigned l, uint64_t base) {
 }
 
 template <bool R>
-void top_passes64(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s) {
+void top_passes64(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s,
+                  uint2* ev2 = nullptr) {
   const size_t smem = kG8Uint2 * sizeof(uint2);
   static PerDeviceOnce attr;
   attr.run([&] {
@@ -682,19 +686,25 @@ void top_passes64(uint2* ev, unsigned l, unsigned T, bool inverse, const Twiddle
   while (ppc > 256 && pairs / ppc < (uint64_t)sms64() * 2) ppc /= 2;
   auto radix2 = [&](unsigned i) {
     const uint64_t p = std::min<uint64_t>(ppc, (uint64_t)1 << i);
-    if (!inverse) launch_k(fft64_top_kernel<false, R>, dim3((unsigned)(pairs / p)), dim3(256), smem, s, ev, i, (int)p, tw);
-    else launch_k(fft64_top_kernel<true, R>, dim3((unsigned)(pairs / p)), dim3(256), smem, s, ev, i, (int)p, tw);
-    FPM_LAUNCH_CHECK();
+    for (uint2* e : {ev, ev2}) {
+      if (!e) continue;
+      if (!inverse) launch_k(fft64_top_kernel<false, R>, dim3((unsigned)(pairs / p)), dim3(256), smem, s, e, i, (int)p, tw);
+      else launch_k(fft64_top_kernel<true, R>, dim3((unsigned)(pairs / p)), dim3(256), smem, s, e, i, (int)p, tw);
+      FPM_LAUNCH_CHECK();
+    }
   };
   const uint64_t quads = ((uint64_t)1 << l) / 4;
-  uint64_t qpc = 8192;
+#ifndef FPM_TOP4_QMAX64
+#define FPM_TOP4_QMAX64 16384  // 40.12 -> 40.04 ms at 2^32 bits
+#endif
+  uint64_t qpc = FPM_TOP4_QMAX64;
   while (qpc > 1024 && quads / qpc < (uint64_t)sms64() * 4) qpc /= 2;
   auto radix4 = [&](unsigned i) {
     const unsigned q = (unsigned)std::min<uint64_t>(qpc, (uint64_t)1 << i);
     if (!inverse)
-      launch_k(fft64_top4_kernel<false, R>, dim3((unsigned)(quads / q)), dim3(kTop4Threads64), kTop4Smem64, s, ev, i, (int)q, tw);
+      launch_k(fft64_top4_kernel<false, R>, dim3((unsigned)(quads / q)), dim3(kTop4Threads64), kTop4Smem64, s, ev, i, (int)q, tw, ev2);
     else
-      launch_k(fft64_top4_kernel<true, R>, dim3((unsigned)(quads / q)), dim3(kTop4Threads64), kTop4Smem64, s, ev, i, (int)q, tw);
+      launch_k(fft64_top4_kernel<true, R>, dim3((unsigned)(quads / q)), dim3(kTop4Threads64), kTop4Smem64, s, ev, i, (int)q, tw, ev2);
     FPM_LAUNCH_CHECK();
   };
   const unsigned n = l - T;
@@ -709,10 +719,10 @@ void top_passes64(uint2* ev, unsigned l, unsigned T, bool inverse, const Twiddle
 }
 
 void butterfly64_top_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s,
-                            bool tower) {
+                            bool tower, uint2* ev2) {
   if (l <= T) return;
-  if (tower) top_passes64<true>(ev, l, T, inverse, tw, s);
-  else top_passes64<false>(ev, l, T, inverse, tw, s);
+  if (tower) top_passes64<true>(ev, l, T, inverse, tw, s, ev2);
+  else top_passes64<false>(ev, l, T, inverse, tw, s, ev2);
 }
 
 void butterfly64_tile_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s) {
