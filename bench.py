@@ -705,6 +705,13 @@ def main():
     roof["traffic"] = stage_traffic(dom, bits)
     roof["ncu_pipes"] = stage_pipes(dom, bits)
     roof["per_stage"] = {k: {kk: v[kk] for kk in ("bound", "frac", "t_roof_ms")} for k, v in per_stage.items()}
+    # the DRAM bytes each stage's kernels actually move (committed ncu launch list, per product) against
+    # the HBM peak: how close the sweeps run to HBM speed, beside the one-sweep algorithmic fraction
+    for k, v in roof["per_stage"].items():
+        tb = stage_traffic(k, bits)
+        if tb:
+            v["dram_bytes"] = tb
+            v["dram_frac"] = round(tb / (hbm * 1e9) / stages[k], 4)
     roof["step_frac"] = round(sum(v["t_roof_ms"] for v in per_stage.values()) / (sum(stages.values()) * 1e3), 4)
     roof["stage_ms"] = {k: round(v * 1e3, 3) for k, v in stages.items()}
 
