@@ -469,7 +469,10 @@ __device__ __forceinline__ int tsw(int k) { return k ^ (((k >> 3) & 1) * 7); }
 
 // CTA shape per tile depth: T <= 11 -> 256 threads, 2 CTAs/SM (<= 140 KiB of shared memory each at
 // T = 10); T = 12 (two 64 KiB tiles + the 64 KiB table, 207 KiB) -> 512 threads, 1 CTA/SM.
-__host__ __device__ constexpr int tower_threads(unsigned T) { return T >= 12 ? 512 : 256; }
+#ifndef FPM_TOWER12_THREADS
+#define FPM_TOWER12_THREADS 512
+#endif
+__host__ __device__ constexpr int tower_threads(unsigned T) { return T >= 12 ? FPM_TOWER12_THREADS : 256; }
 __host__ __device__ constexpr int tower_min_blocks(unsigned T) { return T >= 12 ? 1 : 2; }
 
 // Index in wz of (layer i, group g): layers ascending.
