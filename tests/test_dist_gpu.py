@@ -299,3 +299,76 @@ def test_sharded_peer_config5_split_conversions(gpu, P):
     keep.clear()
     assert not errs, errs
     assert out[P - 1] == c["blake2b128"]
+
+
+@pytest.mark.parametrize("Q", [2, 4])
+def test_b32_sharded_conversion_c_abi_sequence(gpu, Q):
+    """The sharded 2^32-bit conversion driven through its C-ABI exactly as INTEGRATION.md documents
+    (fpm_b32_*: L1_outer by window, regather, fix + rows by chunk, regather, T_d by column), Q replicas
+    on cuda:0: every column owner's columns equal fpm_basis_cvt_dev's conversion of the whole block;
+    then the sharded inverse (T_d^-1 by column, rows^-1 by chunk, L1_outer^-1 by window + fix) brings
+    every window owner's words back to the input."""
+    import ctypes as C
+    from paper_1803_11301_b200 import _lib
+    L = gpu.lib()
+    chk = _lib._check
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    words = 1 << 26  # 64-bit words of a 2^32-bit block
+    x = torch.from_numpy(gpu.random_bitpoly(1 << 32, 777).view(np.int64)).cuda()
+    want = x.clone()
+    chk(L.fpm_basis_cvt_dev(want.data_ptr(), 1 << 32, 1 << 32, s))
+    reps = [x.clone() for _ in range(Q)]
+    sides = [torch.empty(256 * 2048 // 2, dtype=torch.int64, device="cuda") for _ in range(Q)]
+    group = (C.c_void_p * Q)(*[r.data_ptr() for r in reps])
+    WINDOW, CHUNK, COLUMN = 0, 1, 2
+    for q in range(Q):
+        chk(L.fpm_b32_l1_outer_dev(reps[q].data_ptr(), sides[q].data_ptr(), 0, q, Q, s))
+    for q in range(Q):
+        chk(L.fpm_b32_regather_dev(reps[q].data_ptr(), group, WINDOW, CHUNK, q, Q, s))
+    for q in range(Q):
+        c0, c1 = q * 256 // Q, (q + 1) * 256 // Q
+        chk(L.fpm_b32_l1_outer_fix_dev(reps[q].data_ptr(), sides[Q - 1].data_ptr(), 0, c0, c1, s))
+        chk(L.fpm_b32_rows_dev(reps[q].data_ptr() + c0 * 256 * 2048 * 4, (c1 - c0) * 256, 0, s))
+    for q in range(Q):
+        chk(L.fpm_b32_regather_dev(reps[q].data_ptr(), group, CHUNK, COLUMN, q, Q, s))
+    for q in range(Q):
+        chk(L.fpm_b32_cols_dev(reps[q].data_ptr(), 0, q, Q, s))
+    torch.cuda.synchronize()
+    cols = 2048 // Q  # 32-bit words of a row per owner
+    for q in range(Q):
+        got = reps[q].view(torch.int32).view(65536, 2048)[:, q * cols:(q + 1) * cols]
+        ref = want.view(torch.int32).view(65536, 2048)[:, q * cols:(q + 1) * cols]
+        assert torch.equal(got, ref), q
+    # inverse, starting from the column owners
+    for q in range(Q):
+        chk(L.fpm_b32_cols_dev(reps[q].data_ptr(), 1, q, Q, s))
+    for q in range(Q):
+        chk(L.fpm_b32_regather_dev(reps[q].data_ptr(), group, COLUMN, CHUNK, q, Q, s))
+    for q in range(Q):
+        c0, c1 = q * 256 // Q, (q + 1) * 256 // Q
+        chk(L.fpm_b32_rows_dev(reps[q].data_ptr() + c0 * 256 * 2048 * 4, (c1 - c0) * 256, 1, s))
+    for q in range(Q):
+        chk(L.fpm_b32_regather_dev(reps[q].data_ptr(), group, CHUNK, WINDOW, q, Q, s))
+    for q in range(Q):
+        chk(L.fpm_b32_l1_outer_dev(reps[q].data_ptr(), sides[q].data_ptr(), 1, q, Q, s))
+    chk(L.fpm_b32_l1_outer_fix_dev(reps[0].data_ptr(), sides[Q - 1].data_ptr(), 1, 0, 256, s))
+    for q in range(Q):
+        chk(L.fpm_b32_regather_dev(reps[q].data_ptr(), group, WINDOW, CHUNK, q, Q, s))
+    torch.cuda.synchronize()
+    per = words // Q
+    for q in range(Q):
+        assert torch.equal(reps[q][q * per:(q + 1) * per], x[q * per:(q + 1) * per]), q
+
+
+def test_b32_c_abi_rejects_bad_arguments(gpu):
+    import ctypes as C
+    L = gpu.lib()
+    t = torch.zeros(1 << 10, dtype=torch.int64, device="cuda")
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    group = (C.c_void_p * 4)(*([t.data_ptr()] * 4))
+    assert L.fpm_b32_regather_dev(t.data_ptr(), group, 0, 1, 0, 3, s) == 1   # Q must be 2 or 4
+    assert L.fpm_b32_regather_dev(t.data_ptr(), group, 1, 1, 0, 2, s) == 1   # from == to
+    assert L.fpm_b32_l1_outer_dev(t.data_ptr(), None, 0, 0, 2, s) == 1      # no side buffer
+    assert L.fpm_b32_rows_dev(t.data_ptr(), 100, 0, s) == 1                  # not whole chunks
+    assert L.fpm_b32_cols_dev(t.data_ptr(), 0, 2, 2, s) == 1                 # q >= Q
+    assert L.fpm_b32_l1_outer_fix_dev(t.data_ptr(), t.data_ptr(), 0, 3, 300, s) == 1
