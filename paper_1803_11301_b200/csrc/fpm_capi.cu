@@ -1058,8 +1058,7 @@ fpm_status fpm_shard_local_product_dev(uint64_t* d_ea, uint64_t* d_eb, unsigned 
     const cudaStream_t s = (cudaStream_t)stream;
     uint4* ea = reinterpret_cast<uint4*>(d_ea);
     uint4* eb = reinterpret_cast<uint4*>(d_eb);
-    butterfly_top_device(ea, l, T, false, tw, s, true);
-    butterfly_top_device(eb, l, T, false, tw, s, true);
+    butterfly_top_device(ea, l, T, false, tw, s, true, eb);  // both operands per launch
     butterfly_tile_tower_device(ea, eb, l, T, tw, s);
     butterfly_top_device(eb, l, T, true, tw, s, true);
   });

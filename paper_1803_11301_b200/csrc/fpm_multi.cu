@@ -292,8 +292,7 @@ void polymul_multi(const uint64_t* a, size_t a_bits, const uint64_t* b, size_t b
     if (tower) {
       const TwiddleSrc tw = make_twiddle_src(r.dev, lp, cb);
       const unsigned T = pipeline_tile_log2(lp);
-      butterfly_top_device(ea, lp, T, false, tw, r.s, true);
-      butterfly_top_device(eb, lp, T, false, tw, r.s, true);
+      butterfly_top_device(ea, lp, T, false, tw, r.s, true, eb);  // both operands per launch
       butterfly_tile_tower_device(ea, eb, lp, T, tw, r.s);
       butterfly_top_device(eb, lp, T, true, tw, r.s, true);
     } else {
