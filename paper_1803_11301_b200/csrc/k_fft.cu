@@ -849,7 +849,10 @@ void top_passes(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSr
 #define FPM_TOP4_QMAX 16384  // 2^32-bit product: 46.09 -> 45.72 ms vs 8192 (half the table builds)
 #endif
   uint64_t qpc = FPM_TOP4_QMAX;
-  while (qpc > qmin && quads / qpc < (uint64_t)sms() * 4) qpc /= 2;
+#ifndef FPM_TOP4_WAVES
+#define FPM_TOP4_WAVES 4
+#endif
+  while (qpc > qmin && quads / qpc < (uint64_t)sms() * FPM_TOP4_WAVES) qpc /= 2;
   auto radix4 = [&](unsigned i) {
     const unsigned q = (unsigned)std::min<uint64_t>(qpc, (uint64_t)1 << i);
     // forward: 512 threads (pre-rotated lookups without spills; 11.04 vs 11.22 ms at 2^32 bits);
