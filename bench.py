@@ -542,11 +542,19 @@ def main():
 
     import paper_1803_11301_b200 as pkg
 
+    # FPM_BENCH_SHARE_GPU=1 (testing the N > 1 path on a one-GPU box only): every rank on cuda:0 with a
+    # gloo control plane (NCCL cannot run two ranks on one GPU); the data plane is CUDA IPC as always.
+    share = ws > 1 and os.environ.get("FPM_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if ws > 1:
@@ -744,7 +752,9 @@ def main():
         "parallelism": {"single": "single GPU", "replicas": f"{ws} independent products (replicas)",
                         "shard": f"one product sharded over {ws} GPUs: top {ws.bit_length() - 1} butterfly "
                                  f"layers exchanged ({exchange}), basis conversions "
-                                 + ("split over ranks 0/1 (peer memory)" if exchange == "peer" else "replicated")}[mode],
+                                 + (("sharded phase by phase, every 2^32-bit block on N/2 ranks (peer memory)"
+                                     if exchange == "peer" and plan is not None and pdist.PeerBackend._sharded(plan)
+                                     else "split over ranks 0/1 (peer memory)") if exchange == "peer" else "replicated")}[mode],
         "parity": parity,
         "e2e": {"value": round(e2e_ms / ws if mode == "replicas" else e2e_ms, 3), "unit": "ms", "steps": e2e_steps,
                 "h2d_bytes_per_step": 2 * words * 8, "d2h_bytes_per_step": out_words * 8,
