@@ -645,9 +645,27 @@ def main():
     hc = torch.empty(out_words, dtype=torch.int64, pin_memory=True)
     na, nb, nc = (x.numpy().view(np.uint64) for x in (ha, hb, hc))
 
+    # sharded conversion (N >= 4, peer exchange): every rank uploads only its share of its operand and
+    # downloads only its share of the product, over its own PCIe link (dist.polymul_sharded parts=True);
+    # the job's host I/O is the operands and the product once, split over the N links
+    parts = (mode == "shard" and exchange == "peer" and plan is not None and pdist.PeerBackend._sharded(plan))
+    if parts:
+        k_op, iw0, iper = pdist.operand_part_range(plan, rank)
+        src = (ha, hb)[k_op]
+        hpart = src[iw0:iw0 + max(0, min(iper, src.numel() - iw0))]
+        ow0, oper = pdist.product_part_range(plan, rank)
+        on = max(0, min(out_words, ow0 + oper) - ow0)
+        hout = hc[ow0:ow0 + on]
+
     def e2e_step():
         if mode == "single":  # the C-ABI host entry point fpm_polymul (include/fpmul_b200.h)
             return pkg.fp_polymul(na, bits, nb, bits, field=pkg.FIELD_GF128, device=local, out=nc)
+        if parts:
+            xp = hpart.to(dev, non_blocking=True)
+            r = pdist.polymul_sharded(xp, bits, xp, bits, backend, plan, parts=True)
+            hout.copy_(r)
+            torch.cuda.synchronize()
+            return hout.numpy().view(np.uint64)
         xa = ha.to(dev, non_blocking=True)
         xb = hb.to(dev, non_blocking=True)
         r = step(xa, xb)
@@ -666,7 +684,14 @@ def main():
     if ws > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     e2e_ms = float(t.item())
-    same = bool(np.array_equal(res, dev_result))
+    same = bool(np.array_equal(res, dev_result[ow0:ow0 + on] if parts else dev_result))
+    if ws > 1:  # every rank's share must match
+        t = torch.tensor([1 if same else 0], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)
+        same = bool(t.item())
+    io_h2d, io_d2h = 2 * words * 8, out_words * 8  # per step, the whole job
+    if ws > 1 and not parts and mode == "shard":  # every rank uploads both operands, downloads the product
+        io_h2d, io_d2h = ws * io_h2d, ws * io_d2h
 
     # ---- roofline: per-stage CUDA-event times of one instrumented product
     st = [0.0] * pkg.NUM_STAGES
@@ -757,7 +782,7 @@ def main():
                                      else "split over ranks 0/1 (peer memory)") if exchange == "peer" else "replicated")}[mode],
         "parity": parity,
         "e2e": {"value": round(e2e_ms / ws if mode == "replicas" else e2e_ms, 3), "unit": "ms", "steps": e2e_steps,
-                "h2d_bytes_per_step": 2 * words * 8, "d2h_bytes_per_step": out_words * 8,
+                "h2d_bytes_per_step": io_h2d, "d2h_bytes_per_step": io_d2h,
                 "matches_device_result": same},
         "gpu_launches": int(launches),
         "roofline": roof,

@@ -115,9 +115,30 @@ def polymul_batch_sharded(a, a_bits: int, b, b_bits: int, c, count: int, P: int,
     return start, n
 
 
-def polymul_sharded(a, a_bits: int, b, b_bits: int, backend, plan: ShardPlan | None = None):
+def operand_part_range(plan: ShardPlan, rank: int):
+    """The sharded conversion's input share of a rank (P >= 4, 2^32-bit operands): (operand index k,
+    first 64-bit word, word count) -- rank g holds words [w0, w0 + n) of operand g // (P/2)."""
+    Q = plan.P // 2
+    k, q = divmod(rank, Q)
+    per = (1 << 26) // Q
+    return k, q * per, per
+
+
+def product_part_range(plan: ShardPlan, rank: int):
+    """The sharded conversion's output share of a rank: (first 64-bit word of the product, word
+    count before trimming to the product's length) -- the rank's chunks of its 2^32-bit block."""
+    Q = plan.P // 2
+    k, q = divmod(rank, Q)
+    per = (1 << 26) // Q
+    return k * (1 << 26) + q * per, per
+
+
+def polymul_sharded(a, a_bits: int, b, b_bits: int, backend, plan: ShardPlan | None = None, parts: bool = False):
     """Product of two polynomials (backend arrays of packed words) over backend.world ranks;
-    every rank returns the full product words."""
+    every rank returns the full product words.  parts (PeerBackend, sharded conversion): a and b are
+    only this rank's input share (operand_part_range; the other operand is ignored) and the rank
+    returns only its output share (product_part_range) -- each rank's host I/O is 1/P of the data,
+    over its own PCIe link."""
     P, rank = backend.world()
     plan = plan or make_plan(a_bits, b_bits, P, rank)
     r = hasattr(backend, "tower") and backend.tower(plan.lp)           # coset on the fast path
@@ -136,7 +157,9 @@ def polymul_sharded(a, a_bits: int, b, b_bits: int, backend, plan: ShardPlan | N
     # backends with split conversions (PeerBackend, P >= 2): operand a converts on rank 0, b on rank 1,
     # every rank encodes its columns from the converting rank's memory; otherwise replicated
     split = P >= 2 and hasattr(backend, "convert_operands_split")
-    polys = backend.convert_operands_split(a, a_bits, b, b_bits, plan) if split else None
+    polys = backend.convert_operands_split(a, a_bits, b, b_bits, plan, parts) if split else None
+    if parts and not split:
+        raise ValueError("polymul_sharded: operand parts need a PeerBackend")
     evs = []
     for k, (x, bits) in enumerate(((a, a_bits), (b, b_bits))):
         poly = polys[k] if split else backend.convert_operand(x, bits, plan.n_bits)
@@ -154,7 +177,7 @@ def polymul_sharded(a, a_bits: int, b, b_bits: int, backend, plan: ShardPlan | N
     for i in plan.top_layers(inverse=True):
         c = exchanged(c, i, True)
     if split:  # decode into the converting ranks' arrays, inverse conversion split by block
-        return backend.finish_split(c, plan, a_bits + b_bits - 1, tower=r)
+        return backend.finish_split(c, plan, a_bits + b_bits - 1, tower=r, part=parts)
     slice_ = backend.decode_cols(c, plan.m, **kw)                       # 128 rows x m bits
     full = backend.gather_columns(slice_, plan)                         # 128 rows x n_p bits
     return backend.finish(full, plan.n_bits, a_bits + b_bits - 1)       # i_basis_cvt + trim
@@ -371,10 +394,12 @@ class PeerBackend(GpuBackend):
         import ctypes as C
         return (C.c_void_p * len(names))(*[self.arrays[nm] for nm in names])
 
-    def convert_operands_sharded(self, a, a_bits, b, b_bits, plan):
+    def convert_operands_sharded(self, a, a_bits, b, b_bits, plan, parts: bool = False):
         """The sharded conversion: operand k on ranks [kQ, (k+1)Q) (Q = P/2), phase by phase in the
         ranks' replicas -- L1_outer by window, L1_inner + T_r by chunk, T_d by column -- with a barrier
-        and a peer-memory regather between phases.  Returns, per operand, its column owners."""
+        and a peer-memory regather between phases.  Returns, per operand, its column owners.
+        parts: a / b are only this rank's chunk range of its own operand (operand_part_range), pulled
+        into the window distribution by a first regather."""
         P, rank = self.world()
         Q = P // 2
         k, q = divmod(rank, Q)
@@ -384,7 +409,15 @@ class PeerBackend(GpuBackend):
         mine, side = self.arrays[f"r{rank}"], self.arrays[f"s{rank}"]
         group = self._ptrs([f"r{k * Q + j}" for j in range(Q)])
         x, bits = ((a, a_bits), (b, b_bits))[k]
-        chk(L.fpm_load_operand_dev(mine, plan.n_bits // 128, x.data_ptr(), bits, s))  # every rank holds the inputs
+        if parts:
+            _, w0, per = operand_part_range(plan, rank)
+            part_bits = max(0, min(per * 64, bits - w0 * 64))
+            chk(L.fpm_load_operand_dev(mine + w0 * 8, per, x.data_ptr(), part_bits, s))
+            self._barrier()
+            chk(L.fpm_b32_regather_dev(mine, group, 1, 0, q, Q, s))  # CHUNK -> WINDOW
+            self._barrier()
+        else:
+            chk(L.fpm_load_operand_dev(mine, plan.n_bits // 128, x.data_ptr(), bits, s))  # every rank holds the inputs
         chk(L.fpm_b32_l1_outer_dev(mine, side, 0, q, Q, s))
         self._barrier()
         chk(L.fpm_b32_regather_dev(mine, group, 0, 1, q, Q, s))  # WINDOW -> CHUNK
@@ -399,12 +432,14 @@ class PeerBackend(GpuBackend):
         self._barrier()  # both converted operands final at their column owners
         return [_Owners(self._ptrs([f"r{kk * Q + j}" for j in range(Q)]), Q) for kk in (0, 1)]
 
-    def convert_operands_split(self, a, a_bits, b, b_bits, plan):
+    def convert_operands_split(self, a, a_bits, b, b_bits, plan, parts=False):
         """Rank 0 converts operand a, rank 1 operand b (each into its own shared array); every rank
         then reads both converted operands (peer memory) for its encode.  (P >= 4 with 2^32-bit
         operands: the sharded conversion.)"""
         if self._sharded(plan):
-            return self.convert_operands_sharded(a, a_bits, b, b_bits, plan)
+            return self.convert_operands_sharded(a, a_bits, b, b_bits, plan, parts)
+        if parts:
+            raise ValueError("operand parts need the sharded conversion (P >= 4, 2^32-bit operands)")
         P, rank = self.world()
         s = self._s()
         L = self.L.lib()
@@ -421,7 +456,7 @@ class PeerBackend(GpuBackend):
         dev = self.torch.device("cuda", self.torch.cuda.current_device())
         return [DevBuf(self.arrays["x0"], half_words, dev), DevBuf(self.arrays["x1"], half_words, dev)]
 
-    def finish_sharded(self, c, plan, out_bits, tower=False):
+    def finish_sharded(self, c, plan, out_bits, tower=False, part=False):
         """The sharded inverse: decode into the column owners of the lower (ranks [0, Q)) and upper
         ([Q, 2Q)) 2^32-bit blocks, T_d^-1 by column, T_r^-1 + L1_inner^-1 by chunk, L1_outer^-1 by
         window (+ fix on rank 0), the top pass, the upper bit fix, a final regather to chunks; then
@@ -462,6 +497,16 @@ class PeerBackend(GpuBackend):
         self._barrier()  # the product is final at its chunk owners
         t = self.torch
         w = (out_bits + 63) // 64
+        if part:  # only this rank's chunk range of the product
+            w0, per = product_part_range(plan, rank)
+            n = max(0, min(w, w0 + per) - w0)
+            out = t.empty(n, dtype=t.int64, device=c.device)
+            if n:
+                chk(L.fpm_copy_dev(out.data_ptr(), mine + (w0 - k * (1 << 26)) * 8, n * 8, s))
+                if w0 + n == w and out_bits % 64:
+                    out[n - 1] &= (1 << (out_bits % 64)) - 1
+            self._barrier()  # every rank copied out before the replicas are reused
+            return out
         out = t.empty(w, dtype=t.int64, device=c.device)
         per = (1 << 26) // Q  # 64-bit words of a rank's chunks
         for g in range(P):
@@ -475,13 +520,13 @@ class PeerBackend(GpuBackend):
         self._barrier()  # every rank copied out before the replicas are reused
         return out
 
-    def finish_split(self, c, plan, out_bits, tower=False):
+    def finish_split(self, c, plan, out_bits, tower=False, part=False):
         """Every rank decodes its columns straight into the product array(s); the inverse conversion
         runs on rank 0 (n <= 2^32 bits) or as the two 2^32-bit blocks on ranks 1 and 0 (2^33 bits:
         the lower block's top pass reads rank 1's final block); every rank then copies the product.
         (P >= 4 with 2^32-bit operands: the sharded inverse.)"""
         if self._sharded(plan):
-            return self.finish_sharded(c, plan, out_bits, tower)
+            return self.finish_sharded(c, plan, out_bits, tower, part)
         P, rank = self.world()
         s = self._s()
         L = self.L.lib()
