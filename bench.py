@@ -673,7 +673,8 @@ def main():
         torch.cuda.synchronize()
         return nc
 
-    e2e_step()
+    for _ in range(2):  # (small products: the second call captures the pipeline's CUDA graph)
+        e2e_step()
     e2e_steps = max(1, min(args.steps, 5))
     barrier()
     t0 = time.perf_counter()
