@@ -945,7 +945,10 @@ bool tile_fused2_enabled(unsigned T) {
     const char* e = std::getenv("FPM_FUSE_AB");
     return !(e && e[0] == '0');
   }();
-  return on && T >= 10 && T <= 11;
+#ifndef FPM_FUSE2_MIN_T
+#define FPM_FUSE2_MIN_T 8  // config 1 (T = 8): one launch fewer, 0.126 -> 0.124 ms
+#endif
+  return on && T >= FPM_FUSE2_MIN_T && T <= 11;
 }
 
 void butterfly_tile_fused2_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
