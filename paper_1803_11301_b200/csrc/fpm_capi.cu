@@ -272,6 +272,8 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
   DevBuf P(in_place ? 0 : n / 8, s), EA(n_p * sizeof(E), s), EB(n_p * sizeof(E), s);
   uint64_t* const work = in_place ? d_c : P.as<uint64_t>();
   uint32_t* const work32 = reinterpret_cast<uint32_t*>(work);
+  uint64_t* const work_base = work;
+  const cudaStream_t run_stream = s;
   const uint64_t* xs[2] = {d_a, d_b};
   const size_t xbits[2] = {a_bits, b_bits};
   E* es[2] = {EA.as<E>(), EB.as<E>()};
@@ -279,9 +281,25 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
   // launch per layer pair (one set of twiddle tables per CTA for both).  Host-buffer calls keep
   // operand a's transforms ahead of operand b's upload.
   const bool joint_top = !io;
+  // Device-resident products of >= 2^28 bits: operand b converts on a second stream beside operand
+  // a (into the upper half of the n-bit work array, its own scratch); the top passes join them.
+  const bool conc = joint_top && n >= ((size_t)1 << 28) && concurrent_blocks_enabled();
+  cudaStream_t sb = s;
+  cudaEvent_t fork = nullptr, joined = nullptr;
+  if (conc) {
+    sb = side_stream(dev);
+    FPM_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    FPM_CUDA(cudaEventCreateWithFlags(&joined, cudaEventDisableTiming));
+    clk.mark(kStBasis);
+    FPM_CUDA(cudaEventRecord(fork, s));
+    FPM_CUDA(cudaStreamWaitEvent(sb, fork, 0));
+  }
   for (int k = 0; k < 2; ++k) {
     wait_operand(k);
-    clk.mark(kStBasis);
+    if (!conc) clk.mark(kStBasis);
+    const cudaStream_t s = conc && k == 1 ? sb : run_stream;  // (shadows the pipeline stream for operand b)
+    uint64_t* const work = conc && k == 1 ? work_base + n / 128 : work_base;
+    uint32_t* const work32 = reinterpret_cast<uint32_t*>(work);
     const uint64_t half_words = n / 128;  // n/2 bits in uint64 words
     size_t count = (size_t)1 << log2_ceil(xbits[k]);
     if (count < 32) count = 32;
@@ -297,12 +315,19 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
       FPM_LAUNCH_CHECK();
       basis_cvt_device(work32, count, xbits[k], false, s, nullptr, nullptr, fused ? &sink : nullptr);
     }
-    clk.mark(kStEncode);
+    if (!conc) clk.mark(kStEncode);
     if (!fused) F::encode(work32, l, es[k], s, rep);
     if (joint_top) continue;
     clk.mark(kStBfly);
     F::top(es[k], l, T, false, tw, s, rep);
     if (k == 0 && !fuse_ab) F::tile(es[k], l, T, false, tw, s);
+  }
+  if (conc) {
+    FPM_CUDA(cudaEventRecord(joined, sb));
+    FPM_CUDA(cudaStreamWaitEvent(s, joined, 0));
+    cudaEventDestroy(fork);
+    cudaEventDestroy(joined);
+    clk.mark(kStEncode);
   }
   if (joint_top) {
     clk.mark(kStBfly);
@@ -332,7 +357,7 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     }
     copy_out(q0, q1);
   };
-  basis_cvt_device(work32, n, n, true, s, &on_final, nullptr, nullptr, fused_dec ? &dsrc : nullptr);
+  basis_cvt_device(work32, n, n, true, s, &on_final, nullptr, nullptr, fused_dec ? &dsrc : nullptr, !io);
   clk.finish();
 }
 

@@ -219,9 +219,15 @@ struct DecodeSource {
   int m = 128;
 };
 bool basis_cvt_can_decode(size_t n_bits);
+bool concurrent_blocks_enabled();  // FPM_CONCURRENT_BLOCKS=0 disables the concurrent conversions
+cudaStream_t side_stream(int dev);
+// concurrent (2^33-bit inverse): the lower block's conversion runs on a second stream beside the
+// upper block's (only its last step waits for the final upper block) -- device-resident products;
+// host-buffer calls keep the upper block first and alone (its copy-out starts earlier).
 void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s,
                       const FinalFn* on_final = nullptr, const uint32_t* src = nullptr,
-                      const EncodeSink* enc = nullptr, const DecodeSource* dec = nullptr);
+                      const EncodeSink* enc = nullptr, const DecodeSource* dec = nullptr,
+                      bool concurrent = false);
 
 // The halves of a 2^33-bit inverse conversion as separate calls (sharded products: the two 2^32-bit
 // blocks converted on different GPUs).  Upper block: basis_cvt_device(w_hi, 2^32, 2^32, true, s); then

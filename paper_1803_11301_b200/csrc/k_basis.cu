@@ -23,6 +23,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -1940,7 +1941,7 @@ void l1_inner_rows(const uint32_t* src, uint32_t* w, uint32_t* ring, uint64_t D,
 
 void conv2d_split(uint32_t* w, int K, bool inv, uint32_t* scratch, uint32_t* side, cudaStream_t s,
                   const uint32_t* src = nullptr, const uint32_t* top = nullptr, const EncodeSink* enc = nullptr,
-                  bool skip_a = false) {
+                  bool skip_a = false, cudaEvent_t top_ready = nullptr) {
   const int lgD = K - kTLog2;
   const uint64_t D = (uint64_t)1 << lgD;
   const int nb_in = std::min(lgD, 8), nb_out = lgD - nb_in;
@@ -1977,6 +1978,7 @@ void conv2d_split(uint32_t* w, int K, bool inv, uint32_t* scratch, uint32_t* sid
       launch_k(overflow_kernel, dim3(grid_cap(D, 8)), dim3(256), 0, s, scratch, p1, w, D, nb_out ? nullptr : top, 255);
       FPM_LAUNCH_CHECK();
     }
+    if (top_ready) FPM_CUDA(cudaStreamWaitEvent(s, top_ready, 0));  // (the top pass reads the final upper block)
     if (nb_out) outer(w, top);
   }
 }
@@ -2210,8 +2212,27 @@ bool basis_cvt_can_encode(size_t n_bits, bool tower) {
   return n_bits == ((size_t)1 << 32) && split_l1_enabled() && tma_units_enabled();
 }
 
+// A second stream per device for the concurrent conversions (operand b beside operand a, the lower
+// inverse block beside the upper one); forked from and joined to the caller's stream with events.
+cudaStream_t side_stream(int dev) {
+  static cudaStream_t ss[64] = {};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!ss[dev & 63]) FPM_CUDA(cudaStreamCreateWithFlags(&ss[dev & 63], cudaStreamNonBlocking));
+  return ss[dev & 63];
+}
+
+bool concurrent_blocks_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FPM_CONCURRENT_BLOCKS");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
 void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse, cudaStream_t s,
-                      const FinalFn* on_final, const uint32_t* src, const EncodeSink* enc, const DecodeSource* dec) {
+                      const FinalFn* on_final, const uint32_t* src, const EncodeSink* enc, const DecodeSource* dec,
+                      bool concurrent) {
   if (enc && (inverse || !basis_cvt_can_encode(n_bits, enc->tower)))
     throw Error(kInvalid, "basis_cvt: the fused encode needs a forward 2^32-bit conversion");
   if (dec && (!inverse || !basis_cvt_can_decode(n_bits)))
@@ -2289,6 +2310,39 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
   // 2^33 bits: that single pass is fused into the lower block's overflow kernel (bits [1, 2^32)),
   // and its last target bit 2^32 (= upper bit 0 ^= bit 2^33 - 1) is one word fixed afterwards.
   const bool fuse_top = top.size() == 1 && nblocks == 2 && top[0].shift == block_words * 32 - 1;
+  if (concurrent && fuse_top && split && concurrent_blocks_enabled()) {
+    // the lower block on a second stream (own scratch) beside the upper block on s; its last step
+    // (L1_outer^-1 with the fused top pass) waits for the final upper block
+    int dev;
+    FPM_CUDA(cudaGetDevice(&dev));
+    const cudaStream_t t = side_stream(dev);
+    cudaEvent_t fork, hi_done, lo_done;
+    FPM_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    FPM_CUDA(cudaEventCreateWithFlags(&hi_done, cudaEventDisableTiming));
+    FPM_CUDA(cudaEventCreateWithFlags(&lo_done, cudaEventDisableTiming));
+    FPM_CUDA(cudaEventRecord(fork, s));
+    FPM_CUDA(cudaStreamWaitEvent(t, fork, 0));
+    {
+      Scratch scr2(scr_bytes, t), side2(split_side_words((int)lgD) * sizeof(uint32_t), t);
+      conv2d_split(w + block_words, Kb, true, scratch, side, s, nullptr, nullptr, nullptr, dec != nullptr);
+      FPM_CUDA(cudaEventRecord(hi_done, s));
+      conv2d_split(w, Kb, true, static_cast<uint32_t*>(scr2.p), static_cast<uint32_t*>(side2.p), t, nullptr,
+                   w + block_words, nullptr, dec != nullptr, hi_done);
+    }  // (scratch of t freed in t's order)
+    FPM_CUDA(cudaEventRecord(lo_done, t));
+    FPM_CUDA(cudaStreamWaitEvent(s, lo_done, 0));
+    cudaEventDestroy(fork);
+    cudaEventDestroy(hi_done);
+    cudaEventDestroy(lo_done);
+    for (uint64_t b = nblocks; b-- > 0;) {  // (as the sequential loop below)
+      const uint64_t w0 = std::max(b * block_words, early_from), w1 = (b + 1) * block_words;
+      if (on_final && w0 < w1) (*on_final)(w0, w1);
+    }
+    launch_k(top_bit_fix_kernel, dim3(1), dim3(32), 0, s, w + block_words, block_words);
+    FPM_LAUNCH_CHECK();
+    if (on_final) (*on_final)(0, std::min<uint64_t>(early_from, nwords));
+    return;
+  }
   for (uint64_t b = nblocks; b-- > 0;) {
     conv_block(w + b * block_words, nullptr, fuse_top && b == 0 ? w + block_words : nullptr);
     const uint64_t w0 = std::max(b * block_words, early_from), w1 = (b + 1) * block_words;
