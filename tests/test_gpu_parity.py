@@ -474,3 +474,24 @@ def test_clmul_words_dev(gpu, checker):
         w = checker.polymul(a, 64 * wa, b, 64 * wb)
         want[: w.size] = w
         assert np.array_equal(got, want), (wa, wb)
+
+
+@pytest.mark.parametrize("la,lb", [(1 << 28, (1 << 27) + 12345), ((1 << 28) - 77, 1 << 28), (1 << 32, (1 << 31) + 999)])
+def test_concurrent_conversions_device_resident_vs_reference(gpu, ref, la, lb):
+    """Device-resident products of >= 2^28 bits convert the two operands on two streams (operand b in
+    the upper half of the work array, zero-filled when it does not fill its conversion) and the two
+    inverse 2^32-bit blocks of a 2^33-bit product concurrently: unequal and ragged operands,
+    bit-exact against the reference library (the F4 build at 2^33 bits)."""
+    import oracle
+    import torch
+    a = gpu.random_bitpoly(la, 91)
+    b = gpu.random_bitpoly(lb, 92)
+    R = oracle.ref(f4=True) if la + lb > (1 << 32) else ref
+    want = R.polymul(a, la, b, lb, field=0)
+    da = torch.from_numpy(a.view(np.int64)).cuda()
+    db = torch.from_numpy(b.view(np.int64)).cuda()
+    dc = torch.empty(len(want), dtype=torch.int64, device="cuda")
+    for field in (gpu.FIELD_GF128, gpu.FIELD_GF64):
+        gpu.fp_polymul_dev(da, la, db, lb, dc, field=field)
+        torch.cuda.synchronize()
+        assert np.array_equal(dc.cpu().numpy().view(np.uint64), want), field
