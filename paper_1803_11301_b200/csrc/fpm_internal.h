@@ -219,6 +219,10 @@ struct DecodeSource {
   int m = 128;
 };
 bool basis_cvt_can_decode(size_t n_bits);
+void conv_rows_batch16(uint32_t* data, uint64_t nwords, bool inv, cudaStream_t s);
+// config-2 batches in the tower representation (k_codec.cu): 2^16-bit operands / 2^17-bit products
+void encode_batch_r(const uint32_t* polys, uint64_t count, uint64_t stride_words, uint4* ev, cudaStream_t s);
+void decode_batch_r(const uint4* ev, uint64_t count, uint32_t* out, uint64_t stride_words, cudaStream_t s);
 bool concurrent_blocks_enabled();  // FPM_CONCURRENT_BLOCKS=0 disables the concurrent conversions
 cudaStream_t side_stream(int dev);
 // concurrent (2^33-bit inverse): the lower block's conversion runs on a second stream beside the
@@ -300,7 +304,8 @@ bool tile_tower_enabled(unsigned T);
 bool pipeline_fuses_operands(unsigned T);  // both operands' tile layers in one pass at depth T
 bool pipeline_tower(unsigned T);           // ... on tower-representation tiles
 void butterfly_tile_tower_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
-                                 cudaStream_t s);
+                                 cudaStream_t s,
+                                 uint64_t batch = 0);
 void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
                                  cudaStream_t s);
 

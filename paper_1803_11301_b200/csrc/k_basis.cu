@@ -2183,6 +2183,12 @@ std::vector<std::pair<uint64_t, uint64_t>> b32_window_ranges(int q, int Q) {
   return r;
 }
 
+// conv(2^16) (inverse: conv(2^16)^-1) of every 2048-word row of data (a batch of 2^16-bit arrays).
+void conv_rows_batch16(uint32_t* data, uint64_t nwords, bool inv, cudaStream_t s) {
+  set_smem_attr();
+  conv_rows(data, nwords, kTLog2, inv, s);
+}
+
 bool basis_cvt_can_decode(size_t n_bits) {
   return n_bits == ((size_t)1 << 33) && split_l1_enabled();
 }

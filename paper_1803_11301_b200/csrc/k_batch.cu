@@ -9,6 +9,8 @@
 // batch is sharded across GPUs (and CTAs) with no exchange.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "basis_dev.cuh"
@@ -241,7 +243,72 @@ __global__ void __launch_bounds__(256) batch_kernel(const uint64_t* __restrict__
   pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
+// ------------------------------------------------------------------ config 2 in the tower representation
+// Batches of 2^17-bit products (l = 10) as a handful of batch-wide kernels instead of one CTA per
+// product: operands padded to 2^16 bits, conv(2^16) of every operand (conv_rows), encode into the
+// tower representation, the tower tile pass with ONE tile per product (a whole 2^10-element
+// transform of both operands, the pointwise product and the inverse; every table serves both
+// operands and is built per product instead of the generic multiplies of batch_kernel), decode,
+// conv(2^16)^-1 of both halves and the single top pass of the 2^17-bit inverse, then the trimmed
+// product words.
+__global__ void batch_load_kernel(const uint64_t* __restrict__ x, uint64_t x_bits, uint64_t x_stride,
+                                  uint64_t* __restrict__ w, uint64_t count) {
+  pdl_wait();
+  constexpr uint64_t kWords = 1024;  // 2^16 bits
+  const uint64_t xw = (x_bits + 63) / 64;
+  for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < count * kWords; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t p = k / kWords, i = k % kWords;
+    uint64_t v = 0;
+    if (i < xw) {
+      v = x[p * x_stride + i];
+      if (i == xw - 1 && (x_bits & 63)) v &= ((uint64_t)1 << (x_bits & 63)) - 1;
+    }
+    w[k] = v;
+  }
+  pdl_trigger();
+}
+
+// Per product (one CTA): the inverse of the 2^17-bit array's single top pass (bits [1, 2^16] ^= bits
+// [2^16, 2^17 - 1], from the pre-pass values; as i_conv_17), then the product trimmed to out_bits into
+// c (c_stride words apart).
+__global__ void __launch_bounds__(256) batch_fold_store_kernel(const uint32_t* __restrict__ W, uint64_t* __restrict__ c,
+                                                               uint64_t c_stride, uint64_t out_bits, uint64_t count) {
+  pdl_wait();
+  __shared__ uint32_t t[2049];
+  const int tid = threadIdx.x;
+  const uint64_t out_words = (out_bits + 63) / 64;
+  for (uint64_t p = blockIdx.x; p < count; p += gridDim.x) {
+    const uint32_t* w = W + p * 4096;
+    for (int k = tid; k <= 2048; k += blockDim.x) {
+      const uint32_t lo = w[k + 2047], hi = k + 2048 < 4096 ? w[k + 2048] : 0u;
+      uint32_t v = __funnelshift_r(lo, hi, 31);
+      if (k == 0) v &= ~1u;
+      if (k == 2048) v &= 1u;
+      t[k] = v;
+    }
+    __syncthreads();
+    uint64_t* cc = c + p * c_stride;
+    for (uint64_t k = tid; k < out_words; k += blockDim.x) {
+      const uint32_t x0 = w[2 * k] ^ (2 * k <= 2048 ? t[2 * k] : 0u);
+      const uint32_t x1 = w[2 * k + 1] ^ (2 * k + 1 <= 2048 ? t[2 * k + 1] : 0u);
+      uint64_t v = (uint64_t)x0 | ((uint64_t)x1 << 32);
+      if (k == out_words - 1 && (out_bits & 63)) v &= (((uint64_t)1) << (out_bits & 63)) - 1;
+      cc[k] = v;
+    }
+    __syncthreads();
+  }
+  pdl_trigger();
+}
+
 }  // namespace
+
+bool batch_tower_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FPM_BATCH_TOWER");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
 
 void polymul_batch_device(const uint64_t* a, size_t a_bits, size_t a_stride_words, const uint64_t* b, size_t b_bits,
                           size_t b_stride_words, uint64_t* c, size_t c_stride_words, size_t count, cudaStream_t s) {
@@ -256,6 +323,29 @@ void polymul_batch_device(const uint64_t* a, size_t a_bits, size_t a_stride_word
   const unsigned l = logn - 7;
   int dev;
   FPM_CUDA(cudaGetDevice(&dev));
+  if (l == 10 && count >= 64 && batch_tower_enabled()) {  // config 2: the tower-representation batch pipeline
+    const TwiddleSrc tw = make_twiddle_src(dev, l, partition_base(l));
+    DevBuf WA(count * 8192, s), WB(count * 8192, s), EA(count * 1024 * 16, s), EB(count * 1024 * 16, s);
+    const int g1 = (int)std::min<uint64_t>((count * 1024 + 255) / 256, 148u * 16u);
+    launch_k(batch_load_kernel, dim3(g1), dim3(256), 0, s, a, (uint64_t)a_bits, (uint64_t)a_stride_words, WA.as<uint64_t>(), (uint64_t)count);
+    FPM_LAUNCH_CHECK();
+    launch_k(batch_load_kernel, dim3(g1), dim3(256), 0, s, b, (uint64_t)b_bits, (uint64_t)b_stride_words, WB.as<uint64_t>(), (uint64_t)count);
+    FPM_LAUNCH_CHECK();
+    conv_rows_batch16(WA.as<uint32_t>(), count * 2048, false, s);
+    conv_rows_batch16(WB.as<uint32_t>(), count * 2048, false, s);
+    encode_batch_r(WA.as<uint32_t>(), count, 2048, EA.as<uint4>(), s);
+    encode_batch_r(WB.as<uint32_t>(), count, 2048, EB.as<uint4>(), s);
+    butterfly_tile_tower_device(EA.as<uint4>(), EB.as<uint4>(), l, l, tw, s, count);
+    // the 2^17-bit products (4096 words each) reuse WA + WB (contiguous in the pool? not assumed:
+    // a separate array)
+    DevBuf WC(count * 16384, s);
+    decode_batch_r(EB.as<uint4>(), count, WC.as<uint32_t>(), 4096, s);
+    conv_rows_batch16(WC.as<uint32_t>(), count * 4096, true, s);
+    launch_k(batch_fold_store_kernel, dim3((unsigned)std::min<uint64_t>(count, 148u * 8u)), dim3(256), 0, s, WC.as<uint32_t>(), c,
+             (uint64_t)c_stride_words, (uint64_t)(a_bits + b_bits - 1), (uint64_t)count);
+    FPM_LAUNCH_CHECK();
+    return;
+  }
   const DeviceTables& dt = device_tables(dev);
   const size_t smem = kBatchSmemUint4 * sizeof(uint4);
   static PerDeviceOnce attr;

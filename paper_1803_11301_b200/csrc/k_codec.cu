@@ -28,9 +28,12 @@ constexpr int kPad = kSlabWords + 1;
 // polys: the operand, or (sharded conversion) the replicas of the 2^(11 - lgq)-word column owners:
 // a 32-word slab's column (word index mod 2048) selects polys.p[column >> (11 - lgq)].
 template <int ROWS>  // 64: rows >= 64 are known zero (pipeline); 128: general encode
+// slab_stride: words between consecutive slabs' first rows (kSlabWords: one polynomial's columns;
+// a batch of independent polynomials of 32-word rows: the polynomials' stride).
 __global__ void __launch_bounds__(256) encode_kernel(const RankPtrs polys, int lgq, uint64_t row_words,
                                                      uint64_t col0_words, uint64_t nslabs,
-                                                     const uint4* __restrict__ tab_g, uint4* __restrict__ ev) {
+                                                     const uint4* __restrict__ tab_g, uint4* __restrict__ ev,
+                                                     uint64_t slab_stride) {
   pdl_wait();
   extern __shared__ uint4 smem4[];
   // rotated 8-bit table of x*E (gf128.cuh m8 layout): chunks 0..7 (ROWS = 64) or all 16
@@ -49,7 +52,7 @@ __global__ void __launch_bounds__(256) encode_kernel(const RankPtrs polys, int l
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
       const int i = tid + 256 * j, r = i / kSlabWords, c = i % kSlabWords;
-      const uint64_t wc = col0_words + sl * kSlabWords;
+      const uint64_t wc = col0_words + sl * slab_stride;
       const uint32_t* poly = polys.p[lgq ? (int)((wc & 2047) >> (11 - lgq)) : 0];
       nx[j] = sl < nslabs ? __ldg(poly + (uint64_t)r * row_words + wc + c) : 0u;
     }
@@ -98,7 +101,8 @@ __global__ void __launch_bounds__(256) encode_kernel(const RankPtrs polys, int l
 __global__ void __launch_bounds__(256) decode_kernel(const uint4* __restrict__ ev, uint64_t nslabs,
                                                      uint64_t row_words,
                                                      const uint4* __restrict__ tab_g, const RankPtrs polys,
-                                                     const RankPtrs polys_hi, int lgq, uint64_t col0w) {
+                                                     const RankPtrs polys_hi, int lgq, uint64_t col0w,
+                                                     uint64_t slab_stride) {
   pdl_wait();
   extern __shared__ uint4 smem4[];
   uint4* tab = smem4;  // rotated 8-bit table of x*E^-1 (gf128.cuh m8 layout)
@@ -134,7 +138,7 @@ __global__ void __launch_bounds__(256) decode_kernel(const uint4* __restrict__ e
       slab[(3 * 32 + lane) * kPad + col] = tr(y.w);
     }
     __syncthreads();
-    const uint64_t wc = col0w + w0;
+    const uint64_t wc = col0w + sl * slab_stride;
     const int own = lgq ? (int)((wc & 2047) >> (11 - lgq)) : 0;
     uint32_t* const poly = polys.p[own];
     uint32_t* const poly_hi = polys_hi.p[own];
@@ -418,13 +422,48 @@ void encode_cols_owners(const RankPtrs& polys, int Q, unsigned l, uint64_t col0,
     const size_t smem = kM8Uint4 / 2 * sizeof(uint4) + 64 * kPad * sizeof(uint32_t);
     static PerDeviceOnce attr;
     attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
-    launch_k(encode_kernel<64>, dim3(resident_grid(encode_kernel<64>, 256, smem, nslabs)), dim3(256), smem, s, polys, lgq, n_p / 32, col0 / 32, nslabs, tab, ev);
+    launch_k(encode_kernel<64>, dim3(resident_grid(encode_kernel<64>, 256, smem, nslabs)), dim3(256), smem, s, polys, lgq, n_p / 32, col0 / 32, nslabs, tab, ev,
+             (uint64_t)kSlabWords);
   } else {
     const size_t smem = kM8Uint4 * sizeof(uint4) + 128 * kPad * sizeof(uint32_t);
     static PerDeviceOnce attr;
     attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
-    launch_k(encode_kernel<128>, dim3(resident_grid(encode_kernel<128>, 256, smem, nslabs)), dim3(256), smem, s, polys, lgq, n_p / 32, col0 / 32, nslabs, tab, ev);
+    launch_k(encode_kernel<128>, dim3(resident_grid(encode_kernel<128>, 256, smem, nslabs)), dim3(256), smem, s, polys, lgq, n_p / 32, col0 / 32, nslabs, tab, ev,
+             (uint64_t)kSlabWords);
   }
+  FPM_LAUNCH_CHECK();
+}
+
+// A batch of count independent 2^16-bit operands (l = 10: 64 live rows of 32 words each, operands
+// stride_words apart) -> count EvalVecs of 1024 elements in the tower representation, back to back.
+void encode_batch_r(const uint32_t* polys, uint64_t count, uint64_t stride_words, uint4* ev, cudaStream_t s) {
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  const DeviceTables& dt = device_tables(dev);
+  RankPtrs one{};
+  one.p[0] = const_cast<uint32_t*>(polys);
+  const size_t smem = kM8Uint4 / 2 * sizeof(uint4) + 64 * kPad * sizeof(uint32_t);
+  static PerDeviceOnce attr;
+  attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(encode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
+  launch_k(encode_kernel<64>, dim3(resident_grid(encode_kernel<64>, 256, smem, count)), dim3(256), smem, s, one, 0,
+           (uint64_t)32, (uint64_t)0, count, dt.enc_m8r, ev, stride_words);
+  FPM_LAUNCH_CHECK();
+}
+
+// count tower-representation EvalVecs of 1024 elements -> count 2^17-bit products (128 rows of 32
+// words), stride_words apart.
+void decode_batch_r(const uint4* ev, uint64_t count, uint32_t* out, uint64_t stride_words, cudaStream_t s) {
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  const DeviceTables& dt = device_tables(dev);
+  const size_t smem = kM8Uint4 * sizeof(uint4) + 128 * kPad * sizeof(uint32_t);
+  static PerDeviceOnce attr;
+  attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
+  RankPtrs lo{}, hi{};
+  lo.p[0] = out;
+  hi.p[0] = out + 64 * 32;
+  launch_k(decode_kernel, dim3(resident_grid(decode_kernel, 256, smem, count)), dim3(256), smem, s, ev, count, (uint64_t)32,
+           dt.dec_m8r, lo, hi, 0, (uint64_t)0, stride_words);
   FPM_LAUNCH_CHECK();
 }
 
@@ -457,7 +496,7 @@ void decode_cols_device(const uint4* ev, uint64_t ncols, uint32_t* slice, cudaSt
   lo.p[0] = slice;
   hi.p[0] = slice + 64 * (ncols / 32);
   launch_k(decode_kernel, dim3(resident_grid(decode_kernel, 256, smem, nslabs)), dim3(256), smem, s, ev, nslabs, ncols / 32, tower ? dt.dec_m8r : dt.dec_m8, lo, hi, 0,
-           (uint64_t)0);
+           (uint64_t)0, (uint64_t)kSlabWords);
   FPM_LAUNCH_CHECK();
 }
 
@@ -485,7 +524,7 @@ void decode_cols_owners(const uint4* ev, uint64_t ncols, uint64_t col0, uint64_t
   attr.run([&] { FPM_CUDA(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); });
   const uint64_t nslabs = ncols / 32 / kSlabWords;
   launch_k(decode_kernel, dim3(resident_grid(decode_kernel, 256, smem, nslabs)), dim3(256), smem, s, ev, nslabs, row_bits / 32, tower ? dt.dec_m8r : dt.dec_m8, los, his, lgq,
-           col0 / 32);
+           col0 / 32, (uint64_t)kSlabWords);
   FPM_LAUNCH_CHECK();
 }
 

@@ -604,10 +604,14 @@ size_t tower_smem(unsigned T) { return 2 * ((size_t)1 << T) * sizeof(uint4) + si
 // fft_tile_fused2_kernel on R tiles: forward layers [0, T) of both operands (one table per layer
 // serves both tiles), the pointwise product (R -> poly by an M8 table of to_poly, gf_mul, poly -> R
 // by an M8 table of to_r) and the inverse layers [0, T).
+// ntiles / tw_mask: a product's tiles (2^l >> T, each with its own twiddles: tw_mask = ~0), or a
+// batch of independent products of 2^T positions each (l = T; ntiles = count, tw_mask = 0: every
+// tile is a whole transform with tile 0's twiddles).
 template <unsigned T>
 __global__ void __launch_bounds__(tower_threads(T), tower_min_blocks(T)) fft_tile_tower_kernel(const uint4* __restrict__ ea,
                                                                           uint4* __restrict__ eb, unsigned l,
-                                                                          TwiddleSrc tw) {
+                                                                          TwiddleSrc tw, uint64_t ntiles,
+                                                                          uint64_t tw_mask) {
   pdl_wait();
   extern __shared__ uint4 s[];
   constexpr int n = 1 << T;
@@ -620,14 +624,14 @@ __global__ void __launch_bounds__(tower_threads(T), tower_min_blocks(T)) fft_til
     sm.rows_to_poly[tid + (tid >> 3)] = __ldg(tw.to_poly + tid);
   }
   const int ntab = tower_tables(T);
-  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     uint4* g = eb + (t << T);
     const uint4* ga = ea + (t << T);
+    const uint64_t tt = t & tw_mask;  // the tile's position in its transform (twiddles)
     if (tid < ntab) {  // wz[k]: layer i, group h of this tile: Z(i) ^ C2P(2 * 128 h)
       int i = 0, kk = tid;
       while (kk >= tower_groups(T, (unsigned)i)) kk -= tower_groups(T, (unsigned)i++);
-      const uint4 w = x4(twiddle(tw, l, (unsigned)i, t << (T - 1 - i)), c2p2(tw.c2p, (uint64_t)kk << 7));
+      const uint4 w = x4(twiddle(tw, l, (unsigned)i, tt << (T - 1 - i)), c2p2(tw.c2p, (uint64_t)kk << 7));
       sm.wz[tid] = w;
       if (i >= (int)kPolyLayers) {  // forward sequence position: the groups of the layers above i first
         int pos = kk;
@@ -649,7 +653,7 @@ __global__ void __launch_bounds__(tower_threads(T), tower_min_blocks(T)) fft_til
       // pair (2p, 2p+1) with the same twiddle: one register pass, one prepared twiddle
       for (int k = tid; k < 2 * n; k += blockDim.x) s[k] = m8_mul_r(mb, s[k], q);
       __syncthreads();
-      const uint4 Z = twiddle(tw, l, 0, t << (T - 1));
+      const uint4 Z = twiddle(tw, l, 0, tt << (T - 1));
       for (int p = tid; p < n / 2; p += blockDim.x) {
         const int i0 = tsw(2 * p), i1 = tsw(2 * p + 1);
         const GfPrep wp = gf_prep(x4(Z, c2p2(tw.c2p, (uint64_t)p)));
@@ -668,10 +672,10 @@ __global__ void __launch_bounds__(tower_threads(T), tower_min_blocks(T)) fft_til
     } else if (kPolyLayers) {
       for (int k = tid; k < 2 * n; k += blockDim.x) s[k] = m8_mul_r(mb, s[k], q);
       __syncthreads();
-      tile_layers_poly<false>(s, T, kPolyLayers, l, t, tw);
+      tile_layers_poly<false>(s, T, kPolyLayers, l, tt, tw);
       for (int k = tid; k < n; k += blockDim.x) s[k] = gf_mul(s[k], s[n + k]);
       __syncthreads();
-      tile_layers_poly<true>(s, T, kPolyLayers, l, t, tw);
+      tile_layers_poly<true>(s, T, kPolyLayers, l, tt, tw);
     } else {
       for (int k = tid; k < n; k += blockDim.x) s[k] = gf_mul(m8_mul_r(mb, s[k], q), m8_mul_r(mb, s[n + k], q));
       __syncthreads();
@@ -971,8 +975,9 @@ bool tile_tower_enabled(unsigned T) {
 }
 
 void butterfly_tile_tower_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
-                                 cudaStream_t s) {
+                                 cudaStream_t s, uint64_t batch) {
   if (T < 10 || T > 12 || l < T) throw Error(kInvalid, "tower tile pass: T must be 10, 11 or 12");
+  if (batch && l != T) throw Error(kInvalid, "tower tile pass: a batch of transforms needs l = T");
   static PerDeviceOnce attr;
   attr.run([&] {
     set_smem(fft_tile_tower_kernel<10>, tower_smem(10));
@@ -981,8 +986,9 @@ void butterfly_tile_tower_device(const uint4* ea, uint4* eb, unsigned l, unsigne
   });
   const size_t smem = tower_smem(T);
   auto kern = T == 10 ? fft_tile_tower_kernel<10> : T == 11 ? fft_tile_tower_kernel<11> : fft_tile_tower_kernel<12>;
-  const int grid = resident_grid(kern, tower_threads(T), smem, ((uint64_t)1 << l) >> T);
-  launch_k(kern, dim3(grid), dim3(tower_threads(T)), smem, s, ea, eb, l, tw);
+  const uint64_t ntiles = batch ? batch : ((uint64_t)1 << l) >> T;
+  const int grid = resident_grid(kern, tower_threads(T), smem, ntiles);
+  launch_k(kern, dim3(grid), dim3(tower_threads(T)), smem, s, ea, eb, l, tw, ntiles, batch ? (uint64_t)0 : ~(uint64_t)0);
   FPM_LAUNCH_CHECK();
 }
 

@@ -184,6 +184,36 @@ def test_batch(gpu, port, checker):
         assert np.array_equal(C[k], checker.polymul(A[k], la, B[k], lb)), k
 
 
+@pytest.mark.parametrize("la,lb,count", [((1 << 16) - 5, 40000, 64), (33000, 1 << 16, 100)])
+def test_batch_ragged_operands_tower_path(gpu, checker, la, lb, count):
+    """Batches of >= 64 2^17-bit products run the tower-representation batch pipeline (encode in
+    the tower representation, one tower tile pass tile per product, decode, the 2^17-bit inverse):
+    ragged operand lengths (tail masking, the product trimmed to la + lb - 1 bits) and strides wider
+    than the operands, against the oracle."""
+    import torch
+    A = np.zeros((count, 1100), np.uint64)
+    B = np.zeros((count, 1030), np.uint64)
+    for k in range(count):
+        a = gpu.random_bitpoly(la, 500 + k)
+        b = gpu.random_bitpoly(lb, 900 + k)
+        A[k, :len(a)] = a
+        B[k, :len(b)] = b
+        A[k, len(a):] = 0xFFFFFFFFFFFFFFFF  # beyond the operand: must be ignored
+    wc = (la + lb - 1 + 63) // 64
+    dA = torch.from_numpy(A.view(np.int64)).cuda()
+    dB = torch.from_numpy(B.view(np.int64)).cuda()
+    dC = torch.zeros((count, wc + 3), dtype=torch.int64, device="cuda")
+    gpu.fp_polymul_batch_dev(dA, la, 1100, dB, lb, 1030, dC, wc + 3, count)
+    torch.cuda.synchronize()
+    C = dC.cpu().numpy().view(np.uint64)
+    for k in (0, 1, count // 2, count - 1):
+        a = A[k, :(la + 63) // 64].copy()
+        if la % 64:
+            a[-1] &= (1 << (la % 64)) - 1
+        assert np.array_equal(C[k, :wc], checker.polymul(a, la, B[k, :(lb + 63) // 64], lb)), k
+        assert not C[k, wc:].any(), k  # nothing written past the product
+
+
 def _cfg2(gpu):
     import hashlib
     import json
