@@ -110,10 +110,15 @@ fpm_status fpm_polymul_dev(const uint64_t* d_a, size_t a_bits, const uint64_t* d
 
 /* `count` independent products of equal shapes (BASELINE config 2): operand k is at
  * d_a + k*a_stride_words etc.; product k at d_c + k*c_stride_words.  Requires
- * next_pow2(2*max(a_bits,b_bits)) <= 2^17 bits (one CTA per product, all in shared memory). */
+ * next_pow2(2*max(a_bits,b_bits)) <= 2^17 bits (batches of >= 64 2^17-bit products: batch-wide
+ * kernels in the tower representation; otherwise one CTA per product, all in shared memory). */
 fpm_status fpm_polymul_batch_dev(const uint64_t* d_a, size_t a_bits, size_t a_stride_words, const uint64_t* d_b,
                                  size_t b_bits, size_t b_stride_words, uint64_t* d_c, size_t c_stride_words,
                                  size_t count, void* stream);
+/* The same on HOST buffers (synchronous): the batch is cut into chunks whose uploads, products and
+ * downloads overlap on three streams (copy in / compute / copy out, triple-buffered device slots). */
+fpm_status fpm_polymul_batch(const uint64_t* a, size_t a_bits, size_t a_stride_words, const uint64_t* b, size_t b_bits,
+                             size_t b_stride_words, uint64_t* c, size_t c_stride_words, size_t count, int device);
 
 /* karatsuba_mul (proj/include/fpmul/polymul.hpp:85-87, polymul.cpp:268-282) on host buffers: the
  * exact product by word-level carry-less multiplication (no FFT), c as for fpm_polymul.  Also what

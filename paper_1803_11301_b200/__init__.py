@@ -29,6 +29,7 @@ from ._lib import (  # noqa: F401
     karatsuba_mul,
     naive_mul,
     clmul_words_dev,
+    fp_polymul_batch,
     fp_polymul_batch_dev,
     fp_polymul_dev,
     gf128_mul,

@@ -61,6 +61,7 @@ def lib():
         L.fpm_trim_pool.argtypes = [C.c_int]
         L.fpm_test_flip_encode_table.argtypes = [C.c_int]
         L.fpm_polymul_batch_dev.argtypes = [vp, sz, sz, vp, sz, sz, vp, sz, sz, vp]
+        L.fpm_polymul_batch.argtypes = [_u64p, sz, sz, _u64p, sz, sz, _u64p, sz, sz, C.c_int]
         L.fpm_basis_cvt_dev.argtypes = [vp, sz, sz, vp]
         L.fpm_i_basis_cvt_dev.argtypes = [vp, sz, vp]
         L.fpm_encode_dev.argtypes = [vp, C.c_uint, vp, vp]
@@ -423,6 +424,24 @@ def fp_polymul_batch_dev(a, a_bits: int, a_stride: int, b, b_bits: int, b_stride
                 raise ValueError(f"fp_polymul_batch_dev: tensor {name} shorter than (count-1)*stride + words")
     _check(lib().fpm_polymul_batch_dev(_dptr(a), a_bits, a_stride, _dptr(b), b_bits, b_stride, _dptr(c),
                                        c_stride, count, _stream(stream)))
+
+
+def fp_polymul_batch(a, a_bits: int, a_stride: int, b, b_bits: int, b_stride: int, c, c_stride: int, count: int,
+                     device: int = 0) -> None:
+    """fp_polymul_batch_dev on HOST numpy uint64 arrays (fpm_polymul_batch: chunked, uploads, products
+    and downloads overlapped); c is filled in place."""
+    a, b = _as_u64(a), _as_u64(b)
+    if c.dtype != np.uint64 or not c.flags.c_contiguous:
+        raise ValueError("fp_polymul_batch: c must be a contiguous uint64 array")
+    if count and a_bits and b_bits:
+        wa, wb, wc = _words(a_bits), _words(b_bits), _words(a_bits + b_bits - 1)
+        if a_stride < wa or b_stride < wb or c_stride < wc:
+            raise ValueError("fp_polymul_batch: a stride is shorter than its operand / product")
+        for t, stride, w, name in ((a, a_stride, wa, "a"), (b, b_stride, wb, "b"), (c, c_stride, wc, "c")):
+            if t.size < (count - 1) * stride + w:
+                raise ValueError(f"fp_polymul_batch: array {name} shorter than (count-1)*stride + words")
+    _check(lib().fpm_polymul_batch(_ptr(a), a_bits, a_stride, _ptr(b), b_bits, b_stride, _ptr(c), c_stride, count,
+                                   device))
 
 
 def stage_dev(name: str, *args, stream=None) -> None:

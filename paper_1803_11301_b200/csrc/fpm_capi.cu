@@ -933,6 +933,62 @@ fpm_status fpm_polymul_batch_dev(const uint64_t* d_a, size_t a_bits, size_t a_st
   });
 }
 
+fpm_status fpm_polymul_batch(const uint64_t* a, size_t a_bits, size_t a_stride_words, const uint64_t* b, size_t b_bits,
+                             size_t b_stride_words, uint64_t* c, size_t c_stride_words, size_t count, int device) {
+  return guard([&] {
+    if (!a_bits || !b_bits || !count) return;
+    if (!a || !b || !c) throw Error(kInvalid, "polymul_batch: null buffer");
+    const size_t wa = (a_bits + 63) / 64, wb = (b_bits + 63) / 64, wc = (a_bits + b_bits - 1 + 63) / 64;
+    if (a_stride_words < wa || b_stride_words < wb || c_stride_words < wc)
+      throw Error(kInvalid, "polymul_batch: a stride is shorter than its operand / product");
+    DeviceGuard g(device);
+    cudaStream_t s = host_stream(device), h2d = copy_stream(device, 0), d2h = copy_stream(device, 1);
+    // chunks of >= 64 products (the tower batch path), at most 8 of them; three device slots
+    const size_t chunk = std::max<size_t>(64, (count + 7) / 8);
+    const size_t nchunks = (count + chunk - 1) / chunk;
+    constexpr int kSlots = 3;
+    DevBuf A(kSlots * chunk * wa * 8, s), B(kSlots * chunk * wb * 8, s), Cb(kSlots * chunk * wc * 8, s);
+    struct DrainOnUnwind {
+      cudaStream_t a, b, c;
+      int pending = std::uncaught_exceptions();
+      ~DrainOnUnwind() {
+        if (std::uncaught_exceptions() > pending) {
+          cudaStreamSynchronize(a);
+          cudaStreamSynchronize(b);
+          cudaStreamSynchronize(c);
+        }
+      }
+    } drain{h2d, d2h, s};
+    Ev allocated;
+    FPM_CUDA(cudaEventRecord(allocated.e, s));
+    FPM_CUDA(cudaStreamWaitEvent(h2d, allocated.e, 0));
+    FPM_CUDA(cudaStreamWaitEvent(d2h, allocated.e, 0));
+    std::vector<Ev> in(nchunks), done(nchunks), out(nchunks);
+    for (size_t k = 0; k < nchunks; ++k) {
+      const size_t p0 = k * chunk, cnt = std::min(chunk, count - p0), slot = k % kSlots;
+      uint64_t* da = A.as<uint64_t>() + slot * chunk * wa;
+      uint64_t* db = B.as<uint64_t>() + slot * chunk * wb;
+      uint64_t* dc = Cb.as<uint64_t>() + slot * chunk * wc;
+      if (k >= kSlots) FPM_CUDA(cudaStreamWaitEvent(h2d, done[k - kSlots].e, 0));  // slot's inputs consumed
+      FPM_CUDA(cudaMemcpy2DAsync(da, wa * 8, a + p0 * a_stride_words, a_stride_words * 8, wa * 8, cnt,
+                                 cudaMemcpyHostToDevice, h2d));
+      FPM_CUDA(cudaMemcpy2DAsync(db, wb * 8, b + p0 * b_stride_words, b_stride_words * 8, wb * 8, cnt,
+                                 cudaMemcpyHostToDevice, h2d));
+      FPM_CUDA(cudaEventRecord(in[k].e, h2d));
+      FPM_CUDA(cudaStreamWaitEvent(s, in[k].e, 0));
+      if (k >= kSlots) FPM_CUDA(cudaStreamWaitEvent(s, out[k - kSlots].e, 0));  // slot's products copied out
+      polymul_batch_device(da, a_bits, wa, db, b_bits, wb, dc, wc, cnt, s);
+      FPM_CUDA(cudaEventRecord(done[k].e, s));
+      FPM_CUDA(cudaStreamWaitEvent(d2h, done[k].e, 0));
+      FPM_CUDA(cudaMemcpy2DAsync(c + p0 * c_stride_words, c_stride_words * 8, dc, wc * 8, wc * 8, cnt,
+                                 cudaMemcpyDeviceToHost, d2h));
+      FPM_CUDA(cudaEventRecord(out[k].e, d2h));
+    }
+    FPM_CUDA(cudaStreamWaitEvent(s, out[nchunks - 1].e, 0));  // frees below after the last copy
+    FPM_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 fpm_status fpm_clmul_words_dev(const uint64_t* d_a, size_t wa, const uint64_t* d_b, size_t wb, uint64_t* d_out,
                                void* stream) {
   return guard([&] {

@@ -214,6 +214,36 @@ def test_batch_ragged_operands_tower_path(gpu, checker, la, lb, count):
         assert not C[k, wc:].any(), k  # nothing written past the product
 
 
+@pytest.mark.parametrize("count,la,lb", [(300, 1 << 16, (1 << 16) - 9), (40, 20000, 30000)])
+def test_batch_host_buffers_pipelined(gpu, checker, count, la, lb):
+    """fpm_polymul_batch (host buffers): chunks of >= 64 products with uploads, products and
+    downloads overlapped over three device slots (300 products: 5 chunks, every slot reused),
+    strided host arrays; equal to the device-buffer batch and the oracle."""
+    import torch
+    sa, sb = (la + 63) // 64 + 3, (lb + 63) // 64 + 1
+    wc = (la + lb - 1 + 63) // 64
+    sc = wc + 2
+    A = np.zeros(count * sa, np.uint64)
+    B = np.zeros(count * sb, np.uint64)
+    for k in range(count):
+        a = gpu.random_bitpoly(la, 3000 + k)
+        b = gpu.random_bitpoly(lb, 4000 + k)
+        A[k * sa:k * sa + len(a)] = a
+        B[k * sb:k * sb + len(b)] = b
+    C = np.zeros(count * sc, np.uint64)
+    gpu.fp_polymul_batch(A, la, sa, B, lb, sb, C, sc, count)
+    dC = torch.zeros(count * sc, dtype=torch.int64, device="cuda")
+    gpu.fp_polymul_batch_dev(torch.from_numpy(A.view(np.int64)).cuda(), la, sa, torch.from_numpy(B.view(np.int64)).cuda(),
+                             lb, sb, dC, sc, count)
+    torch.cuda.synchronize()
+    D = dC.cpu().numpy().view(np.uint64)
+    for k in range(count):
+        assert np.array_equal(C[k * sc:k * sc + wc], D[k * sc:k * sc + wc]), k
+    for k in (0, count - 1):
+        want = checker.polymul(A[k * sa:k * sa + (la + 63) // 64], la, B[k * sb:k * sb + (lb + 63) // 64], lb)
+        assert np.array_equal(C[k * sc:k * sc + wc], want), k
+
+
 def _cfg2(gpu):
     import hashlib
     import json
