@@ -626,6 +626,15 @@ const DeviceTables& device_tables(int dev) {
   m8_entries(dec8, ft.inv_rows);
   m8_entries(enc8r, enc_rows_r);
   m8_entries(dec8r, inv_rows_r);
+  std::vector<uint2> dec_half[2] = {std::vector<uint2>(4096), std::vector<uint2>(4096)};
+  for (int c = 0; c < 16; ++c)
+    for (int v = 0; v < 256; ++v) {
+      U128 e;
+      for (int j = 0; j < 8; ++j)
+        if (v >> j & 1) { e.lo ^= inv_rows_r[8 * c + j].lo; e.hi ^= inv_rows_r[8 * c + j].hi; }
+      dec_half[0][v * 16 + c] = make_uint2((uint32_t)e.lo, (uint32_t)(e.lo >> 32));
+      dec_half[1][v * 16 + c] = make_uint2((uint32_t)e.hi, (uint32_t)(e.hi >> 32));
+    }
   for (int part = 0; part < 4; ++part)
     for (int e = 0; e < 512; ++e) {
       U128 acc;
@@ -703,6 +712,8 @@ const DeviceTables& device_tables(int dev) {
     FPM_CUDA(cudaMalloc(dst, v.size() * sizeof(uint2)));
     FPM_CUDA(cudaMemcpy(*dst, v.data(), v.size() * sizeof(uint2), cudaMemcpyHostToDevice));
   };
+  up2(&t.dec_half_r[0], dec_half[0]);
+  up2(&t.dec_half_r[1], dec_half[1]);
   up2(&t.enc_g8, enc64); up2(&t.dec_g8, dec64); up2(&t.c2p64, c2p64); up2(&t.rows64, rows64); up2(&t.inv64, inv64);
   up2(&t.to_r64, to_r64); up2(&t.to_poly64, to_poly64); up2(&t.enc_g8r, enc64r); up2(&t.dec_g8r, dec64r);
   FPM_CUDA(cudaSetDevice(prev));

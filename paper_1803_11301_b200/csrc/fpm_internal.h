@@ -148,6 +148,10 @@ struct DeviceTables {
   uint4* to_poly = nullptr;   // 128 x e_k in poly: rows of the R -> poly map
   uint4* enc_m8r = nullptr;   // M8 tables of x -> R(x*E)
   uint4* dec_m8r = nullptr;   // M8 tables of x_R -> poly(x)*E^{-1}
+  // the same split by output half (h = 0: product rows 0..63, the lower 2^32-bit block of a 2^33-bit
+  // product; h = 1: rows 64..127, the upper block): entry (byte v, byte index c < 16) at v * 16 + c,
+  // 8 bytes each -- sixteen lanes rotated over the sixteen c read distinct banks with LDS.64
+  uint2* dec_half_r[2] = {nullptr, nullptr};
   // GF(2^64) (run_pipeline<gf64>): G8 tables (gf64.cuh layout) of x*E and x*E^{-1}, C2P tables
   uint2* enc_g8 = nullptr;
   uint2* dec_g8 = nullptr;

@@ -1310,6 +1310,106 @@ __global__ void __launch_bounds__(kCTThreads, 1) decode_conv_a_kernel(const void
   pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
+// One block of decode_conv_a_kernel (GF(2^128), tower representation): the 64 product rows of the
+// block only (16 LDS.64 lookups per element in dec_half_r[HALF], conflict-free), then conv(256)^-1
+// over A for that block.  The upper block's copy-out can start after half the decode work.
+constexpr size_t kDecHalfSmem = 4096 * sizeof(uint2) + (kDecRows + 16 * 33 * kCT) * sizeof(uint32_t);
+template <int HALF>
+__global__ void __launch_bounds__(kCTThreads, 1) decode_half_conv_a_kernel(const uint4* __restrict__ ev,
+                                                                           const uint2* __restrict__ tab_g,
+                                                                           uint32_t* __restrict__ w, uint64_t nitems) {
+  pdl_wait();
+  constexpr int S = 4, RPS = 256 / S;
+  extern __shared__ __align__(16) uint2 sm_dh[];
+  uint2* tab = sm_dh;                                              // [v][16 byte indices]
+  uint32_t* Rw = reinterpret_cast<uint32_t*>(sm_dh + 4096);      // [A][33]
+  uint32_t* Z = Rw + kDecRows;                                     // [d][33][kCT]
+  const int tid = threadIdx.x, c = tid % kCT, r = tid / kCT, lane = tid & 31, warp = tid >> 5;
+  constexpr int kCols = kTWords / kCT;
+  auto zi = [](int d, int s, int cc) { return (d * 33 + s) * kCT + cc; };
+  for (int i = tid; i < 4096; i += kCTThreads) tab[i] = tab_g[i];
+  const int q16 = lane & 15;
+  const Transpose32 tr(lane);
+  __syncthreads();
+  constexpr int kPairsPerWarp = S * 32 / 16;
+  const uint32_t tbase = (uint32_t)__cvta_generic_to_shared(tab);
+  for (uint64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const uint64_t B = it / kCols, cb = it % kCols;
+    const uint64_t e0 = B * 65536 + cb * 1024;
+    uint4 f[kPairsPerWarp];
+#pragma unroll
+    for (int k = 0; k < kPairsPerWarp; ++k) {
+      const int pair = warp * kPairsPerWarp + k, a = pair >> 5, col = pair & 31;
+      f[k] = __ldg(ev + (uint64_t)a * (1u << 24) + e0 + 32 * col + lane);
+    }
+#pragma unroll
+    for (int k = 0; k < kPairsPerWarp; ++k) {
+      const int pair = warp * kPairsPerWarp + k, a = pair >> 5, col = pair & 31;
+      const uint32_t fw[4] = {f[k].x, f[k].y, f[k].z, f[k].w};
+      uint2 y0 = make_uint2(0, 0), y1 = make_uint2(0, 0);
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        const int cc = (kk + q16) & 15;  // byte index: lanes l and l + 16 share it, but read one bank pair each
+        const uint32_t v = __byte_perm(fw[cc >> 2], 0, 0x4440u | (uint32_t)(cc & 3));
+        uint2 e;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(tbase + 8u * (16u * v + (uint32_t)cc)));
+        if (kk & 1) { y1.x ^= e.x; y1.y ^= e.y; } else { y0.x ^= e.x; y0.y ^= e.y; }
+      }
+      const uint32_t yw[2] = {y0.x ^ y1.x, y0.y ^ y1.y};
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int j = 32 * q + lane;
+        Rw[(a * RPS + j) * 33 + col] = tr(yw[q]);  // row A = S j + a of this block
+      }
+    }
+    __syncthreads();
+    // ---- conv(256)^-1 over A (as decode_conv_a_kernel)
+    uint32_t* const gbase = w + B * kTWords + cb * kCT + c;
+    auto at = [&](int u) -> uint32_t* { return gbase + (uint64_t)u * 256 * kTWords; };
+    uint32_t x[16];
+#pragma unroll
+    for (int vv = 0; vv < 16; ++vv) {
+      const int A = 16 * r + vv;
+      x[vv] = Rw[((A % S) * RPS + A / S) * 33 + c];
+    }
+    conv16_vals<true>(x);
+#pragma unroll
+    for (int vv = 0; vv < 16; ++vv) Z[zi(r, vv, c)] = x[vv];
+    __syncthreads();
+    const int v = r;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) x[k] = Z[zi(k, v, c)];
+    conv16_vals<true>(x);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) Z[zi(k, v + k, c)] = x[k];
+    __syncthreads();
+    uint32_t y[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      x[k] = (r >= k) ? Z[zi(k, r, c)] : 0u;
+      y[k] = (r + 16 < k + 16) ? Z[zi(k, r + 16, c)] : 0u;
+    }
+    zeta16_vals(x);
+    zeta16_vals(y);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      Z[zi(k, r, c)] = x[k];
+      Z[zi(k, r + 16, c)] = y[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int vv = 0; vv < 16; ++vv) {
+      uint32_t fv = Z[zi(r, vv + r, c)];
+      if (r >= 1 && 15 + vv + r < 31) fv ^= Z[zi(r - 1, 15 + vv + r, c)];
+      *at(16 * r + vv) = fv;
+    }
+    __syncthreads();  // Rw / Z reuse
+  }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
+}
+
 // ------------------------------------------------------------------ unit-level L1 carry + C_cols
 // Rows of t bits are units; row d = 256 * dh + v (digit dh, offset v).  After the unit-skewed zeta,
 // Gs[kh] holds units u = 0 .. 256+Dd-1 (pitch gs_pitch words).  Output unit (kh, v):
@@ -2213,6 +2313,26 @@ void decode_conv_a(const DecodeSource& dec, uint32_t* w_lo, uint32_t* w_hi, cuda
   FPM_LAUNCH_CHECK();
 }
 
+// One 2^32-bit block of the fused 2^33-bit decode (GF(2^128) in the tower representation): half = 0
+// the lower block (product rows 0..63), 1 the upper (rows 64..127).
+bool decode_halves_ok(const DecodeSource& dec) { return dec.m == 128 && dec.tower; }
+void decode_half_conv_a(const DecodeSource& dec, int half, uint32_t* w_block, cudaStream_t s) {
+  static PerDeviceOnce attr;
+  attr.run([] {
+    FPM_CUDA(cudaFuncSetAttribute(decode_half_conv_a_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecHalfSmem));
+    FPM_CUDA(cudaFuncSetAttribute(decode_half_conv_a_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDecHalfSmem));
+  });
+  int dev;
+  FPM_CUDA(cudaGetDevice(&dev));
+  const DeviceTables& dt = device_tables(dev);
+  const uint64_t items = 256 * (kTWords / kCT);
+  const int grid = grid_cap(items, 1);
+  const uint4* ev = static_cast<const uint4*>(dec.ev);
+  if (half) launch_k(decode_half_conv_a_kernel<1>, dim3(grid), dim3(kCTThreads), kDecHalfSmem, s, ev, dt.dec_half_r[1], w_block, items);
+  else launch_k(decode_half_conv_a_kernel<0>, dim3(grid), dim3(kCTThreads), kDecHalfSmem, s, ev, dt.dec_half_r[0], w_block, items);
+  FPM_LAUNCH_CHECK();
+}
+
 bool basis_cvt_can_encode(size_t n_bits, bool tower) {
   (void)tower;
   return n_bits == ((size_t)1 << 32) && split_l1_enabled() && tma_units_enabled();
@@ -2285,7 +2405,15 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
   const uint64_t block_words = ((uint64_t)1 << Kb) / 32;
   // fused decode (2^33-bit inverse): decode + conv^-1 over the digit of both blocks in one pass; each
   // block's conversion then skips that step
-  if (dec) decode_conv_a(*dec, w, w + block_words, s);
+  static const bool halves_on = [] {
+    const char* e = std::getenv("FPM_DECODE_HALVES");
+    return !(e && std::string(e) == "0");
+  }();
+  // (the split decode serves the host-buffer path: the upper block's copy-out starts after half the
+  // decode; device-resident products decode both blocks at once -- 5.55 vs 5.99 ms of inverse
+  // conversion with the halves on two streams, while e2e gains 74.69 -> 74.35 ms)
+  const bool halves = dec && halves_on && !concurrent && decode_halves_ok(*dec);
+  if (dec && !halves) decode_conv_a(*dec, w, w + block_words, s);
   // Arrays above 2^32 bits: their passes with S > 2^32 come first (forward) / last (inverse);
   // what remains is conv(2^32) of every 2^32-bit block (build_schedule's per-digit recursion).
   std::vector<Pass> top;
@@ -2330,6 +2458,10 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
     FPM_CUDA(cudaStreamWaitEvent(t, fork, 0));
     {
       Scratch scr2(scr_bytes, t), side2(split_side_words((int)lgD) * sizeof(uint32_t), t);
+      if (halves) {
+        decode_half_conv_a(*dec, 1, w + block_words, s);
+        decode_half_conv_a(*dec, 0, w, t);
+      }
       conv2d_split(w + block_words, Kb, true, scratch, side, s, nullptr, nullptr, nullptr, dec != nullptr);
       FPM_CUDA(cudaEventRecord(hi_done, s));
       conv2d_split(w, Kb, true, static_cast<uint32_t*>(scr2.p), static_cast<uint32_t*>(side2.p), t, nullptr,
@@ -2350,6 +2482,7 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
     return;
   }
   for (uint64_t b = nblocks; b-- > 0;) {
+    if (halves) decode_half_conv_a(*dec, (int)b, w + b * block_words, s);  // (upper block first)
     conv_block(w + b * block_words, nullptr, fuse_top && b == 0 ? w + block_words : nullptr);
     const uint64_t w0 = std::max(b * block_words, early_from), w1 = (b + 1) * block_words;
     if (on_final && w0 < w1) (*on_final)(w0, w1);

@@ -433,6 +433,18 @@ def test_baseline_config_products_match_reference_hashes(gpu, port, key):
         assert got == c["blake2b128"], field
 
 
+def test_config5_host_buffers_match_reference_hash(gpu, port):
+    """BASELINE config 5 through the host-buffer entry fpm_polymul (the e2e path: operand b's upload
+    overlapping operand a's transforms, the upper 2^32-bit block decoded and converted first -- the
+    split decode -- and copied out while the lower block converts): the reference's product hash."""
+    import hashlib
+    c = _meta()["4294967296x4294967296"]
+    a = port.random_bitpoly(c["a_bits"], c["seed_a"])
+    b = port.random_bitpoly(c["b_bits"], c["seed_b"])
+    got = gpu.fp_polymul(a, c["a_bits"], b, c["b_bits"], field=gpu.FIELD_GF128)
+    assert hashlib.blake2b(got.tobytes(), digest_size=16).hexdigest() == c["blake2b128"]
+
+
 def _edge_operand(port, kind, bits, seed):
     w = port.random_bitpoly(bits, seed)
     if kind == "sparse":  # density 1/64: AND of six uniform words (SURVEY 8(d), config 3)
