@@ -123,7 +123,6 @@ __global__ void __launch_bounds__(256) decode_kernel(const uint4* __restrict__ e
   };
   fetch(blockIdx.x);
   for (uint64_t sl = blockIdx.x; sl < nslabs; sl += gridDim.x) {
-    const uint64_t w0 = sl * kSlabWords;
     uint4 cur[kCols];
 #pragma unroll
     for (int k = 0; k < kCols; ++k) cur[k] = nx[k];

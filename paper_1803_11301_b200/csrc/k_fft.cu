@@ -236,6 +236,124 @@ __global__ void __launch_bounds__(NT, 1) fft_top4_kernel(uint4* __restrict__ ev,
   pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
+// ------------------------------------------------------------------ top layers, three per pass (tower)
+// Layers i+2, i+1 and i in one HBM round trip, elements in the tower representation R.  A block of
+// 2^(i+3) elements splits into eighths a0..a7 of h = 2^i; layer i+2 pairs (a_k, a_k+4) with
+// W2 = w(i+2, B); layer i+1 pairs (a0,a2), (a1,a3) with W1 = w(i+1, 2B) and (a4,a6), (a5,a7) with
+// w(i+1, 2B+1) = W1 ^ C2P(2); layer i pairs (a_2m, a_2m+1) with w(i, 4B+m) = W0 ^ C2P(2m).  C2P(2m)
+// (m < 4) lies in the subfield GF(2^8), so the three tables of radix-4 serve three layers: the
+// sibling twiddles add a byte-permute scalar product (tower.cuh smul_t) instead of a table.
+constexpr size_t kTop8Smem = kTop4Smem + sizeof(SmulTabs);
+template <bool INV, int NT = 512>
+__global__ void __launch_bounds__(NT, 1) fft_top8_kernel(uint4* __restrict__ ev, unsigned l, unsigned i, int opc,
+                                                          TwiddleSrc tw, uint4* __restrict__ ev2) {
+  pdl_wait();
+  extern __shared__ uint4 sm8[];
+  uint4* rows = sm8 + 3 * kM8Uint4;  // 3 x 144
+  uint4* to_r = rows + 3 * 144;      // the conversion rows, to_r_pad layout
+  SmulTabs& stab = *reinterpret_cast<SmulTabs*>(to_r + 136);
+  const uint64_t h = (uint64_t)1 << i;
+  const uint64_t oct0 = (uint64_t)blockIdx.x * opc;  // opc <= h: a CTA never straddles a block
+  const uint64_t B = oct0 >> i;
+  const int tid = threadIdx.x, grp = tid >> 8, lt = tid & 255;
+  const int no = ev2 ? 2 * opc : opc;
+  constexpr int kRounds = (3 + NT / 256 - 1) / (NT / 256);
+  uint4 ws[kRounds];
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const int g = r * (NT / 256) + grp;
+    ws[r] = g == 0 ? twiddle(tw, l, i + 2, B)
+                   : g == 1 ? twiddle(tw, l, i + 1, 2 * B) : g == 2 ? twiddle(tw, l, i, 4 * B) : make_uint4(0, 0, 0, 0);
+  }
+  smul_tabs_build(stab, tw.tau, tid);
+  if (tid < 128) to_r[to_r_pad(tid)] = __ldg(tw.to_r + tid);
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const int g = r * (NT / 256) + grp;
+    uint4* tab = sm8 + g * kM8Uint4;
+    uint4* rs = rows + g * 144;
+    if (g < 3) rows_r<true>(rs, ws[r], lt, to_r);
+    __syncthreads();
+    if (g < 3) {
+      const int c = lt & 15, sv = lt >> 4;
+      uint4 rr[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) rr[j] = rs[9 * c + j];
+      uint4 t[16];
+      t[0] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (sv >> j & 1) t[0] = x4(t[0], rr[4 + j]);
+#pragma unroll
+      for (int u = 1; u < 16; ++u) t[u] = x4(t[u & (u - 1)], rr[(u & 1) ? 0 : (u & 2) ? 1 : (u & 4) ? 2 : 3]);
+      uint4* dst = tab + (c >> 3) * 2048 + 16 * sv * 8 + (c & 7);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) dst[u * 8] = t[u];
+    }
+    __syncthreads();
+  }
+  const int q = tid & 7;
+  const uint64_t off = (B << (i + 3)) + (oct0 & (h - 1));
+  const M8Base mb = m8_base(sm8, q);
+  constexpr uint32_t kT1 = kM8Uint4 * 16u, kT0 = 2u * kM8Uint4 * 16u;  // W1, W0 after W2
+  // u * (table twiddle ^ d_m) with the scalar part d_m = R(C2P(2m)), m = 1..3
+  auto mul = [&](uint4 u, uint32_t toff, int m) {
+    uint4 r = m8_mul_r(mb, u, q, toff);
+    if (m) r = x4(r, smul_t(u, smul_tab(stab, m)));
+    return r;
+  };
+#pragma unroll 1
+  for (int k = tid; k < no; k += NT) {
+    uint4* p = (k < opc ? ev + k : ev2 + (k - opc)) + off;
+    uint4 a[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) a[e] = ld_na(p + e * h);
+    if (!INV) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {  // layer i+2
+        a[e] = x4(a[e], mul(a[e + 4], 0, 0));
+        a[e + 4] = x4(a[e + 4], a[e]);
+      }
+#pragma unroll
+      for (int hb = 0; hb < 2; ++hb)  // layer i+1: blocks 2B (a0..a3), 2B+1 (a4..a7)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int u0 = 4 * hb + e, u1 = u0 + 2;
+          a[u0] = x4(a[u0], mul(a[u1], kT1, hb));
+          a[u1] = x4(a[u1], a[u0]);
+        }
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {  // layer i: blocks 4B + m
+        a[2 * m] = x4(a[2 * m], mul(a[2 * m + 1], kT0, m));
+        a[2 * m + 1] = x4(a[2 * m + 1], a[2 * m]);
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        a[2 * m + 1] = x4(a[2 * m + 1], a[2 * m]);
+        a[2 * m] = x4(a[2 * m], mul(a[2 * m + 1], kT0, m));
+      }
+#pragma unroll
+      for (int hb = 0; hb < 2; ++hb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int u0 = 4 * hb + e, u1 = u0 + 2;
+          a[u1] = x4(a[u1], a[u0]);
+          a[u0] = x4(a[u0], mul(a[u1], kT1, hb));
+        }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        a[e + 4] = x4(a[e + 4], a[e]);
+        a[e] = x4(a[e], mul(a[e + 4], 0, 0));
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) st_cs(p + e * h, a[e]);
+  }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
+}
+
 // ------------------------------------------------------------------ tile layers (i < T)
 // Layers i >= kTabLayer of a 256-thread tile have <= 2 twiddles per tile, each shared by >= 512
 // butterflies: those use an M8 table built in shared memory (tab != nullptr: 64 KiB + 144 rows
@@ -876,6 +994,40 @@ void top_passes(uint4* ev, unsigned l, unsigned T, bool inverse, const TwiddleSr
     FPM_LAUNCH_CHECK();
   };
   const unsigned n = l - T;
+#ifndef FPM_TOP8
+#define FPM_TOP8 1
+#endif
+  if (R && FPM_TOP8 && n >= 3) {
+    // tower representation: three layers per pass (fft_top8_kernel), the remainder at the bottom
+    static PerDeviceOnce attr8;
+    attr8.run([&] {
+      set_smem(fft_top8_kernel<false>, kTop8Smem);
+      set_smem(fft_top8_kernel<true>, kTop8Smem);
+    });
+    const uint64_t octs = ((uint64_t)1 << l) / 8;
+#ifndef FPM_TOP8_OMAX
+#define FPM_TOP8_OMAX (FPM_TOP4_QMAX / 2)
+#endif
+    uint64_t opc = FPM_TOP8_OMAX;
+    while (opc > 512 && octs / opc < (uint64_t)sms() * FPM_TOP4_WAVES) opc /= 2;
+    auto radix8 = [&](unsigned i) {
+      const unsigned o = (unsigned)std::min<uint64_t>(opc, (uint64_t)1 << i);
+      if (!inverse) launch_k(fft_top8_kernel<false>, dim3((unsigned)(octs / o)), dim3(512), kTop8Smem, s, ev, l, i, (int)o, tw, ev2);
+      else launch_k(fft_top8_kernel<true>, dim3((unsigned)(octs / o)), dim3(512), kTop8Smem, s, ev, l, i, (int)o, tw, ev2);
+      FPM_LAUNCH_CHECK();
+    };
+    const unsigned rem = n % 3;
+    if (!inverse) {
+      for (unsigned k = 0; k + 3 <= n; k += 3) radix8(l - 3 - k);
+      if (rem == 2) radix4(T);
+      if (rem == 1) radix2(T);
+    } else {
+      if (rem == 2) radix4(T);
+      if (rem == 1) radix2(T);
+      for (unsigned i = T + rem; i + 3 <= l; i += 3) radix8(i);
+    }
+    return;
+  }
   const bool odd = n & 1;
   if (!inverse) {
     for (unsigned k = 0; k + 1 < n; k += 2) radix4(l - 2 - k);
