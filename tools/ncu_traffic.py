@@ -13,7 +13,7 @@ import os
 import subprocess
 import sys
 
-STAGE_OF = [("fft_tile_fused_kernel", "pointwise"), ("fft_tile_fused2_kernel", "pointwise"),
+STAGE_OF = [("fft_top8_kernel<1", "ibutterfly"), ("fft_top8_kernel<0", "butterfly"), ("fft_tile_fused_kernel", "pointwise"), ("fft_tile_fused2_kernel", "pointwise"),
             ("fft_tile_tower_kernel", "pointwise"), ("fft_top4_kernel<1", "ibutterfly"),
             ("fft_top_kernel<1", "ibutterfly"), ("fft_top4_kernel<0", "butterfly"),
             ("fft_top_kernel<0", "butterfly"), ("fft_tile_kernel<0>", "butterfly"),
