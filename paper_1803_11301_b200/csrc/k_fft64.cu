@@ -179,6 +179,119 @@ __global__ void __launch_bounds__(kTop4Threads64, 2) fft64_top4_kernel(uint2* __
   pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
 
+// ------------------------------------------------------------------ top layers, three per pass (tower)
+// fft_top8_kernel (k_fft.cu) for GF(2^64): layers i+2, i+1, i per HBM round trip with the three G8
+// tables of w(i+2, B), w(i+1, 2B), w(i, 4B); the sibling twiddles differ by subfield elements
+// C2P(2m), m < 4, applied as byte-permute scalar products.
+constexpr size_t kTop8Smem64 = kTop4Smem64 + sizeof(SmulTabs);
+template <bool INV>
+__global__ void __launch_bounds__(kTop4Threads64, 2) fft64_top8_kernel(uint2* __restrict__ ev, unsigned i, int opc,
+                                                                       TwiddleSrc64 tw, uint2* __restrict__ ev2) {
+  pdl_wait();
+  extern __shared__ uint2 sm64[];
+  uint2* rows = sm64 + 3 * kG8Uint2;   // 3 x kG8Rows
+  uint2* to_r = rows + 3 * kG8Rows;    // conversion rows, to_r64_pad layout
+  SmulTabs& stab = *reinterpret_cast<SmulTabs*>(reinterpret_cast<uint4*>(to_r + 72));
+  const uint64_t h = (uint64_t)1 << i;
+  const uint64_t oct0 = (uint64_t)blockIdx.x * opc;  // opc <= h
+  const uint64_t B = oct0 >> i;
+  const int tid = threadIdx.x, grp = tid >> 7, lt = tid & 127;
+  const uint2 w = grp == 0 ? twiddle64(tw, i + 2, B) : grp == 1 ? twiddle64(tw, i + 1, 2 * B) : twiddle64(tw, i, 4 * B);
+  smul_tabs_build(stab, tw.tau, tid);
+  if (tid < 64) to_r[to_r64_pad(tid)] = __ldg(tw.to_r + tid);
+  __syncthreads();
+  {
+    uint2* tab = sm64 + grp * kG8Uint2;
+    uint2* rs = rows + grp * kG8Rows;
+    rows_r64(rs, w, lt, to_r);
+    __syncthreads();
+    const int c = lt & 7;
+    uint2 r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = rs[9 * c + j];
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int sv = (lt >> 3) + 16 * half;
+      uint2 t[8];
+      t[0] = make_uint2(0, 0);
+#pragma unroll
+      for (int j = 0; j < 5; ++j)
+        if (sv >> j & 1) t[0] = x2(t[0], r[3 + j]);
+#pragma unroll
+      for (int u = 1; u < 8; ++u) t[u] = x2(t[u & (u - 1)], r[(u & 1) ? 0 : (u & 2) ? 1 : 2]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        uint2* e = tab + (8 * sv + u) * 16 + c;
+        e[0] = t[u];
+        e[8] = t[u];
+      }
+    }
+    __syncthreads();
+  }
+  const int lane = tid & 31;
+  const G8Base gb = g8_base(sm64, lane);
+  constexpr uint32_t kT1 = kG8Uint2 * 8u, kT0 = 2u * kG8Uint2 * 8u;  // W1, W0 after W2
+  auto mul = [&](uint2 u, uint32_t toff, int m) {
+    uint2 r = g8_mul_r(gb, u, lane, toff);
+    if (m) r = x2(r, smul_t2(u, smul_tab(stab, m)));
+    return r;
+  };
+  auto oct = [&](uint2 (&a)[8]) {
+    if (!INV) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        a[e] = x2(a[e], mul(a[e + 4], 0, 0));
+        a[e + 4] = x2(a[e + 4], a[e]);
+      }
+#pragma unroll
+      for (int hb = 0; hb < 2; ++hb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int u0 = 4 * hb + e, u1 = u0 + 2;
+          a[u0] = x2(a[u0], mul(a[u1], kT1, hb));
+          a[u1] = x2(a[u1], a[u0]);
+        }
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        a[2 * m] = x2(a[2 * m], mul(a[2 * m + 1], kT0, m));
+        a[2 * m + 1] = x2(a[2 * m + 1], a[2 * m]);
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        a[2 * m + 1] = x2(a[2 * m + 1], a[2 * m]);
+        a[2 * m] = x2(a[2 * m], mul(a[2 * m + 1], kT0, m));
+      }
+#pragma unroll
+      for (int hb = 0; hb < 2; ++hb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int u0 = 4 * hb + e, u1 = u0 + 2;
+          a[u1] = x2(a[u1], a[u0]);
+          a[u0] = x2(a[u0], mul(a[u1], kT1, hb));
+        }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        a[e + 4] = x2(a[e + 4], a[e]);
+        a[e] = x2(a[e], mul(a[e + 4], 0, 0));
+      }
+    }
+  };
+  const int no = ev2 ? 2 * opc : opc;
+  const uint64_t off = (B << (i + 3)) + (oct0 & (h - 1));
+#pragma unroll 1
+  for (int k = tid; k < no; k += kTop4Threads64) {  // one octet per thread (8-byte accesses: no spills)
+    uint2* p = (k < opc ? ev + k : ev2 + (k - opc)) + off;
+    uint2 a[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) a[e] = p[e * h];
+    oct(a);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) p[e * h] = a[e];
+  }
+  pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
+}
+
 // ------------------------------------------------------------------ tile layers (i < T)
 #ifndef FPM_G8_LAYER
 #define FPM_G8_LAYER 9
@@ -708,6 +821,38 @@ void top_passes64(uint2* ev, unsigned l, unsigned T, bool inverse, const Twiddle
     FPM_LAUNCH_CHECK();
   };
   const unsigned n = l - T;
+#ifndef FPM_TOP8_64
+#define FPM_TOP8_64 1
+#endif
+  if (R && FPM_TOP8_64 && n >= 3) {  // three layers per pass (fft64_top8_kernel), the remainder at the bottom
+    static PerDeviceOnce attr8;
+    attr8.run([&] {
+      set_smem64(fft64_top8_kernel<false>, kTop8Smem64);
+      set_smem64(fft64_top8_kernel<true>, kTop8Smem64);
+    });
+    const uint64_t octs = ((uint64_t)1 << l) / 8;
+    uint64_t opc = FPM_TOP4_QMAX64 / 2;
+    while (opc > 512 && octs / opc < (uint64_t)sms64() * 4) opc /= 2;
+    auto radix8 = [&](unsigned i) {
+      const unsigned o = (unsigned)std::min<uint64_t>(opc, (uint64_t)1 << i);
+      if (!inverse)
+        launch_k(fft64_top8_kernel<false>, dim3((unsigned)(octs / o)), dim3(kTop4Threads64), kTop8Smem64, s, ev, i, (int)o, tw, ev2);
+      else
+        launch_k(fft64_top8_kernel<true>, dim3((unsigned)(octs / o)), dim3(kTop4Threads64), kTop8Smem64, s, ev, i, (int)o, tw, ev2);
+      FPM_LAUNCH_CHECK();
+    };
+    const unsigned rem = n % 3;
+    if (!inverse) {
+      for (unsigned k = 0; k + 3 <= n; k += 3) radix8(l - 3 - k);
+      if (rem == 2) radix4(T);
+      if (rem == 1) radix2(T);
+    } else {
+      if (rem == 2) radix4(T);
+      if (rem == 1) radix2(T);
+      for (unsigned i = T + rem; i + 3 <= l; i += 3) radix8(i);
+    }
+    return;
+  }
   const bool odd = n & 1;
   if (!inverse) {
     for (unsigned k = 0; k + 1 < n; k += 2) radix4(l - 2 - k);

@@ -8,4 +8,5 @@ OUT=$ROOT/build/exp/$NAME
 mkdir -p $OUT/obj
 NV="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr $*"
 make -s -C $ROOT/paper_1803_11301_b200/csrc -j8 OBJDIR=$OUT/obj OUT=$OUT/libfpmul_b200.so "NVFLAGS=$NV" $OUT/libfpmul_b200.so
+rm -rf $OUT/obj  # (gpurun snapshots are capped at 512 MiB)
 echo $OUT/libfpmul_b200.so
