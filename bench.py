@@ -244,15 +244,17 @@ def executed_work(stage: str, bits: int, T: int):
       smem_bytes      M8-table products: 16 LDS.128 = 256 B of shared memory each
       generic         generic products (IMAD-hole Karatsuba, GENERIC_CLK_PER_PRODUCT each per SM)
       hbm_bytes       one algorithmic sweep of the stage's data
-    butterfly/ibutterfly: radix-4 passes over layers [T, l) of both operands / the product (one M8
-    product per butterfly); pointwise: the fused tower tile pass (per element position: (T-1) tile
+    butterfly/ibutterfly: radix-8 (+ one radix-4) passes over layers [T, l) of both operands / the
+    product (one M8 product per butterfly); pointwise: the fused tower tile pass (per element position: (T-1) tile
     layers of both operands + (T-1) inverse, one M8 product per butterfly, 3 R<->poly conversions,
     2.5 generic products for layer 0 of both operands, the pointwise product and inverse layer 0)."""
     n = 2 * bits
     n_p = n // 128
     l = n_p.bit_length() - 1
     V = 16 * n_p
-    passes = (l - T + 1) // 2
+    # HBM passes of the top layers: radix-8 (three layers) in the tower pipeline, the remainder of one
+    # radix-4 / radix-2 pass at the bottom
+    passes = (l - T) // 3 + (1 if (l - T) % 3 else 0)
     w = {"smem_bytes": 0.0, "generic": 0.0, "hbm_bytes": 0.0}
     if stage == "basiscvt":
         w["hbm_bytes"] = 2 * 2 * (bits // 8)
@@ -743,8 +745,8 @@ def main():
     tower = fab and os.environ.get("FPM_TOWER", "1") != "0"  # tower-representation tile pass (k_fft.cu)
     roof["kernel"] = {"pointwise": ("fft_tile_tower_kernel" if tower else "fft_tile_fused2_kernel") if fab
                       else "fft_tile_fused_kernel",
-                      "butterfly": "fft_top4_kernel" if fab else "fft_top4_kernel + fft_tile_kernel",
-                      "ibutterfly": "fft_top4_kernel<inverse>"}.get(dom, dom)
+                      "butterfly": "fft_top8_kernel + fft_top4_kernel" if fab else "fft_top4_kernel + fft_tile_kernel",
+                      "ibutterfly": "fft_top8_kernel<inverse> + fft_top4_kernel<inverse>"}.get(dom, dom)
     roof["stage"] = dom
     roof["traffic"] = stage_traffic(dom, bits)
     roof["ncu_pipes"] = stage_pipes(dom, bits)
