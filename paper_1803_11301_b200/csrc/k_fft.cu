@@ -590,8 +590,11 @@ __device__ __forceinline__ int tsw(int k) { return k ^ (((k >> 3) & 1) * 7); }
 #ifndef FPM_TOWER12_THREADS
 #define FPM_TOWER12_THREADS 512
 #endif
-__host__ __device__ constexpr int tower_threads(unsigned T) { return T >= 12 ? FPM_TOWER12_THREADS : 256; }
-__host__ __device__ constexpr int tower_min_blocks(unsigned T) { return T >= 12 ? 1 : 2; }
+#ifndef FPM_TOWER_BIG_T
+#define FPM_TOWER_BIG_T 12  // tile depths from here on: one 512-thread CTA per SM
+#endif
+__host__ __device__ constexpr int tower_threads(unsigned T) { return T >= FPM_TOWER_BIG_T ? FPM_TOWER12_THREADS : 256; }
+__host__ __device__ constexpr int tower_min_blocks(unsigned T) { return T >= FPM_TOWER_BIG_T ? 1 : 2; }
 
 // Index in wz of (layer i, group g): layers ascending.
 __host__ __device__ constexpr int tower_wz_index(unsigned T, unsigned i, int g) {
@@ -905,7 +908,10 @@ unsigned fft_tile_log2(unsigned l) {
 // out of the HBM-bound radix-4 passes and shares each layer-(>= 4) table over 4096 positions
 // (2^32-bit product: 49.25 -> 46.97 ms).
 unsigned pipeline_tile_log2(unsigned l) {
-  if (!tile_log2_knob() && l >= 22 && tile_tower_enabled(12)) return 12;
+#ifndef FPM_TOWER_T
+#define FPM_TOWER_T 12
+#endif
+  if (!tile_log2_knob() && l >= 22 && tile_tower_enabled(FPM_TOWER_T)) return FPM_TOWER_T;
   if (!tile_log2_knob() && l >= 20 && tile_fused2_enabled(10)) return 10;
   return fft_tile_log2(l);
 }
