@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -281,9 +282,13 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
   // launch per layer pair (one set of twiddle tables per CTA for both).  Host-buffer calls keep
   // operand a's transforms ahead of operand b's upload.
   const bool joint_top = !io;
-  // Device-resident products of >= 2^28 bits: operand b converts on a second stream beside operand
+  // Device-resident products: operand b converts on a second stream beside operand
   // a (into the upper half of the n-bit work array, its own scratch); the top passes join them.
-  const bool conc = joint_top && n >= ((size_t)1 << 28) && concurrent_blocks_enabled();
+  static const unsigned conc_min_log2 = [] {  // FPM_CONC_MIN_LOG2: smallest n (log2) that forks
+    const char* e = std::getenv("FPM_CONC_MIN_LOG2");
+    return e ? (unsigned)std::atoi(e) : 18u;
+  }();
+  const bool conc = joint_top && n >= ((size_t)1 << conc_min_log2) && concurrent_blocks_enabled();
   cudaStream_t sb = s;
   cudaEvent_t fork = nullptr, joined = nullptr;
   if (conc) {
@@ -531,6 +536,54 @@ cudaStream_t copy_stream(int dev, int which) {
   if (!streams[dev][which]) FPM_CUDA(cudaStreamCreateWithFlags(&streams[dev][which], cudaStreamNonBlocking));
   return streams[dev][which];
 }
+
+// Stream sets for concurrent host-buffer callers of fpm_polymul: each call leases one set (pipeline
+// stream + upload + download stream), so that one caller's PCIe copies overlap another caller's
+// kernels instead of queueing behind them.  Set 0 is host_stream / copy_stream; a fifth concurrent
+// caller waits for a set.
+struct StreamLease {
+  static constexpr int kSets = 4;
+  struct Pool {
+    std::mutex mu;
+    std::condition_variable cv;
+    bool busy[kSets] = {};
+    cudaStream_t st[kSets][3] = {};
+  };
+  static Pool& pool(int dev) {
+    static Pool pools[64];
+    return pools[dev & 63];
+  }
+  Pool& p;
+  int k = -1;
+  cudaStream_t s = nullptr, h2d = nullptr, d2h = nullptr;
+  explicit StreamLease(int dev) : p(pool(dev)) {
+    std::unique_lock<std::mutex> lock(p.mu);
+    p.cv.wait(lock, [&] {
+      for (int i = 0; i < kSets; ++i)
+        if (!p.busy[i]) return true;
+      return false;
+    });
+    for (int i = 0; i < kSets && k < 0; ++i)
+      if (!p.busy[i]) k = i;
+    if (k == 0) {
+      p.st[0][0] = host_stream(dev), p.st[0][1] = copy_stream(dev, 0), p.st[0][2] = copy_stream(dev, 1);
+    } else {
+      for (int j = 0; j < 3; ++j)
+        if (!p.st[k][j]) FPM_CUDA(cudaStreamCreateWithFlags(&p.st[k][j], cudaStreamNonBlocking));
+    }
+    p.busy[k] = true;
+    s = p.st[k][0], h2d = p.st[k][1], d2h = p.st[k][2];
+  }
+  ~StreamLease() {
+    {
+      std::lock_guard<std::mutex> lock(p.mu);
+      p.busy[k] = false;
+    }
+    p.cv.notify_one();
+  }
+  StreamLease(const StreamLease&) = delete;
+  StreamLease& operator=(const StreamLease&) = delete;
+};
 
 struct Ev {
   cudaEvent_t e = nullptr;
@@ -898,7 +951,11 @@ fpm_status fpm_polymul(const uint64_t* a, size_t a_bits, const uint64_t* b, size
         return;
       }
     }
-    cudaStream_t h2d = copy_stream(device, 0), d2h = copy_stream(device, 1);
+    // concurrent callers: own pipeline / copy streams per call (declared before the buffers: they
+    // are freed on the leased stream and the stream is synchronized before the lease ends)
+    StreamLease lease(device);
+    s = lease.s;
+    cudaStream_t h2d = lease.h2d, d2h = lease.d2h;
     DevBuf A(wa * 8, s), B(wb * 8, s), C(wc * 8, s);
     // On an exception (e.g. an allocation failure inside the pipeline) the buffers above are freed
     // while the copy streams may still read or write them: drain both copy streams first (this

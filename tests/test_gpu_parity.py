@@ -509,6 +509,24 @@ def test_concurrent_host_calls(gpu, checker):
         assert np.array_equal(g, checker.polymul(a, la, b, lb)), (la, lb)
 
 
+def test_concurrent_host_calls_leased_streams(gpu, checker):
+    """Host-buffer products above the staged size lease a stream set per call (pipeline, upload and
+    download streams; four sets per device) so one caller's PCIe copies overlap another's kernels.
+    Six threads (more callers than sets: two wait for a lease) on 2^23..2^26-bit operands in both
+    fields; every product against the reference."""
+    import concurrent.futures as cf
+    rng = np.random.default_rng(78)
+    jobs = []
+    for k in range(12):
+        la = int(rng.choice([1 << 23, (1 << 24) + 77, 1 << 25, (1 << 26) - 5]))
+        lb = int(rng.choice([1 << 22, (1 << 24) - 1, 1 << 25]))
+        jobs.append((rnd_words(rng, la), la, rnd_words(rng, lb), lb, [gpu.FIELD_GF128, gpu.FIELD_AUTO][k % 2]))
+    with cf.ThreadPoolExecutor(6) as ex:
+        got = list(ex.map(lambda j: gpu.fp_polymul(j[0], j[1], j[2], j[3], field=j[4]), jobs))
+    for (a, la, b, lb, _), g in zip(jobs, got):
+        assert np.array_equal(g, checker.polymul(a, la, b, lb)), (la, lb)
+
+
 @pytest.mark.parametrize("la,lb", [(1, 1), (63, 64), (64, 65), (4095, 4095), (4096, 100), (700, 9000),
                                    (100_000, 77_777), (1 << 20, (1 << 19) + 3)])
 def test_karatsuba_mul(gpu, checker, la, lb):
