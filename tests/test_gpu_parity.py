@@ -585,3 +585,39 @@ def test_concurrent_conversions_device_resident_vs_reference(gpu, ref, la, lb):
         gpu.fp_polymul_dev(da, la, db, lb, dc, field=field)
         torch.cuda.synchronize()
         assert np.array_equal(dc.cpu().numpy().view(np.uint64), want), field
+
+
+def _fuzz_shapes():
+    """Seeded random operand lengths, log-uniform over every size class of the pipeline: the
+    Karatsuba bypass (< 4096 bits), the one-CTA products (n <= 2^17), graph-replayed small products,
+    the unfused / fused tile passes and the first radix-8 top passes (up to ~2^23 bits)."""
+    rng = np.random.default_rng(20261021)
+    shapes = []
+    for _ in range(36):
+        la = int(2 ** rng.uniform(0, 23)) + int(rng.integers(0, 3))
+        lb = int(2 ** rng.uniform(0, 23)) + int(rng.integers(0, 3))
+        shapes.append((la, lb))
+    # lengths straddling word and power-of-two boundaries
+    shapes += [(65, 127), (4096, 4097), ((1 << 17) - 1, (1 << 17) + 1), ((1 << 21) + 1, (1 << 21) - 1),
+               ((1 << 22) - 63, 64), (3, (1 << 22) + 65)]
+    return shapes
+
+
+@pytest.mark.parametrize("la,lb", _fuzz_shapes())
+def test_polymul_shape_fuzz(gpu, checker, port, la, lb):
+    """fp_polymul (polymul.cpp:223-239) on random ragged shapes: every field choice through the host
+    entry point and the device entry point (twice: the second call replays the CUDA graph)."""
+    import torch
+    a = port.random_bitpoly(la, 7000 + la)
+    b = port.random_bitpoly(lb, 8000 + lb)
+    want = checker.polymul(a, la, b, lb)
+    for field in (gpu.FIELD_GF128, gpu.FIELD_GF64, gpu.FIELD_AUTO):
+        assert np.array_equal(gpu.fp_polymul(a, la, b, lb, field=field), want), field
+    da = torch.from_numpy(a.view(np.int64)).cuda()
+    db = torch.from_numpy(b.view(np.int64)).cuda()
+    dc = torch.empty(len(want), dtype=torch.int64, device="cuda")
+    for rep in range(2):
+        dc.fill_(-1)
+        gpu.fp_polymul_dev(da, la, db, lb, dc, field=gpu.FIELD_GF128)
+        torch.cuda.synchronize()
+        assert np.array_equal(dc.cpu().numpy().view(np.uint64), want), rep
