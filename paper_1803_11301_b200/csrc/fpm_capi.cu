@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <optional>
 #include <tuple>
 #include <exception>
 #include <mutex>
@@ -290,14 +291,14 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
   }();
   const bool conc = joint_top && n >= ((size_t)1 << conc_min_log2) && concurrent_blocks_enabled();
   cudaStream_t sb = s;
-  cudaEvent_t fork = nullptr, joined = nullptr;
+  std::optional<Ev> fork, joined;  // (released on every exit path)
   if (conc) {
     sb = side_stream(dev);
-    FPM_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    FPM_CUDA(cudaEventCreateWithFlags(&joined, cudaEventDisableTiming));
+    fork.emplace();
+    joined.emplace();
     clk.mark(kStBasis);
-    FPM_CUDA(cudaEventRecord(fork, s));
-    FPM_CUDA(cudaStreamWaitEvent(sb, fork, 0));
+    FPM_CUDA(cudaEventRecord(fork->e, s));
+    FPM_CUDA(cudaStreamWaitEvent(sb, fork->e, 0));
   }
   for (int k = 0; k < 2; ++k) {
     wait_operand(k);
@@ -328,10 +329,8 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     if (k == 0 && !fuse_ab) F::tile(es[k], l, T, false, tw, s);
   }
   if (conc) {
-    FPM_CUDA(cudaEventRecord(joined, sb));
-    FPM_CUDA(cudaStreamWaitEvent(s, joined, 0));
-    cudaEventDestroy(fork);
-    cudaEventDestroy(joined);
+    FPM_CUDA(cudaEventRecord(joined->e, sb));
+    FPM_CUDA(cudaStreamWaitEvent(s, joined->e, 0));
     clk.mark(kStEncode);
   }
   if (joint_top) {
@@ -585,13 +584,6 @@ struct StreamLease {
   StreamLease& operator=(const StreamLease&) = delete;
 };
 
-struct Ev {
-  cudaEvent_t e = nullptr;
-  Ev() { FPM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
-  ~Ev() { if (e) cudaEventDestroy(e); }
-  Ev(const Ev&) = delete;
-  Ev& operator=(const Ev&) = delete;
-};
 
 }  // namespace
 

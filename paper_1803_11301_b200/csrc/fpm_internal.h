@@ -78,6 +78,16 @@ struct DevBuf {
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+// A timing-disabled event released on every exit path (destroying an event with waits still pending
+// is allowed: the waits complete and the event is freed afterwards).
+struct Ev {
+  cudaEvent_t e = nullptr;
+  Ev() { FPM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+  ~Ev() { if (e) cudaEventDestroy(e); }
+  Ev(const Ev&) = delete;
+  Ev& operator=(const Ev&) = delete;
+};
+
 // Programmatic dependent launch (sm_90+).  Every library kernel begins with pdl_wait() (the
 // previous kernel of its stream has completed and its writes are visible -- nothing is read before
 // it) and pdl_trigger() (the stream's next kernel may be scheduled now; its CTAs park at their own

@@ -2450,12 +2450,9 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
     int dev;
     FPM_CUDA(cudaGetDevice(&dev));
     const cudaStream_t t = side_stream(dev);
-    cudaEvent_t fork, hi_done, lo_done;
-    FPM_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    FPM_CUDA(cudaEventCreateWithFlags(&hi_done, cudaEventDisableTiming));
-    FPM_CUDA(cudaEventCreateWithFlags(&lo_done, cudaEventDisableTiming));
-    FPM_CUDA(cudaEventRecord(fork, s));
-    FPM_CUDA(cudaStreamWaitEvent(t, fork, 0));
+    Ev fork, hi_done, lo_done;
+    FPM_CUDA(cudaEventRecord(fork.e, s));
+    FPM_CUDA(cudaStreamWaitEvent(t, fork.e, 0));
     {
       Scratch scr2(scr_bytes, t), side2(split_side_words((int)lgD) * sizeof(uint32_t), t);
       if (halves) {
@@ -2463,15 +2460,12 @@ void basis_cvt_device(uint32_t* w, size_t n_bits, size_t live_bits, bool inverse
         decode_half_conv_a(*dec, 0, w, t);
       }
       conv2d_split(w + block_words, Kb, true, scratch, side, s, nullptr, nullptr, nullptr, dec != nullptr);
-      FPM_CUDA(cudaEventRecord(hi_done, s));
+      FPM_CUDA(cudaEventRecord(hi_done.e, s));
       conv2d_split(w, Kb, true, static_cast<uint32_t*>(scr2.p), static_cast<uint32_t*>(side2.p), t, nullptr,
-                   w + block_words, nullptr, dec != nullptr, hi_done);
+                   w + block_words, nullptr, dec != nullptr, hi_done.e);
     }  // (scratch of t freed in t's order)
-    FPM_CUDA(cudaEventRecord(lo_done, t));
-    FPM_CUDA(cudaStreamWaitEvent(s, lo_done, 0));
-    cudaEventDestroy(fork);
-    cudaEventDestroy(hi_done);
-    cudaEventDestroy(lo_done);
+    FPM_CUDA(cudaEventRecord(lo_done.e, t));
+    FPM_CUDA(cudaStreamWaitEvent(s, lo_done.e, 0));
     for (uint64_t b = nblocks; b-- > 0;) {  // (as the sequential loop below)
       const uint64_t w0 = std::max(b * block_words, early_from), w1 = (b + 1) * block_words;
       if (on_final && w0 < w1) (*on_final)(w0, w1);

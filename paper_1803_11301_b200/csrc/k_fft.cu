@@ -716,6 +716,9 @@ __device__ __forceinline__ void tile_layers_poly(uint4* __restrict__ s, unsigned
   }
 }
 
+#ifndef FPM_TOWER_FUSE_TOPOLY
+#define FPM_TOWER_FUSE_TOPOLY 1
+#endif
 #ifndef FPM_TOWER_POLY
 #define FPM_TOWER_POLY 1
 #endif
@@ -772,13 +775,24 @@ __global__ void __launch_bounds__(tower_threads(T), tower_min_blocks(T)) fft_til
     if (kPolyLayers == 1) {
       // layer 0 forward on both operands, the pointwise product and inverse layer 0 act on the same
       // pair (2p, 2p+1) with the same twiddle: one register pass, one prepared twiddle
+      // (FPM_TOWER_FUSE_TOPOLY: the R -> poly lookups of a pair run inside this loop, so that the
+      // shared-memory lookups of some warps overlap the IMAD-pipe products of others instead of
+      // forming a lookup-only pass with its own barrier)
+#if !FPM_TOWER_FUSE_TOPOLY
       for (int k = tid; k < 2 * n; k += blockDim.x) s[k] = m8_mul_r(mb, s[k], q);
       __syncthreads();
+#endif
       const uint4 Z = twiddle(tw, l, 0, tt << (T - 1));
       for (int p = tid; p < n / 2; p += blockDim.x) {
         const int i0 = tsw(2 * p), i1 = tsw(2 * p + 1);
         const GfPrep wp = gf_prep(x4(Z, c2p2(tw.c2p, (uint64_t)p)));
         uint4 a0 = s[i0], a1 = s[i1], b0 = s[n + i0], b1 = s[n + i1];
+#if FPM_TOWER_FUSE_TOPOLY
+        a0 = m8_mul_r(mb, a0, q);
+        a1 = m8_mul_r(mb, a1, q);
+        b0 = m8_mul_r(mb, b0, q);
+        b1 = m8_mul_r(mb, b1, q);
+#endif
         a0 = x4(a0, gf_mul_prep(wp, a1));
         a1 = x4(a1, a0);
         b0 = x4(b0, gf_mul_prep(wp, b1));
