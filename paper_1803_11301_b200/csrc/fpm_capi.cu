@@ -197,9 +197,17 @@ struct Gf128Ops {
   }
   // both operands' tile layers in the fused pass (no separate tile pass of operand a)
   static bool fuse_ab(unsigned T) { return pipeline_fuses_operands(T); }
-  static void fused2(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s, bool r) {
-    if (r) butterfly_tile_tower_device(ea, eb, l, T, tw, s);
+  static void fused2(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s, bool r,
+                     uint64_t pre_tiles = 0) {
+    if (r) butterfly_tile_tower_device(ea, eb, l, T, tw, s, 0, pre_tiles);
     else butterfly_tile_fused2_device(ea, eb, l, T, tw, s);
+  }
+  // Host-buffer products: part of operand a's tile layers ahead of the fused pass (returns the
+  // number of tiles done), in the window before operand b has arrived.
+  static uint64_t pre_pass(E* ea, unsigned l, unsigned T, const Tw& tw, cudaStream_t s, bool r) {
+    const uint64_t k = r ? tower_pre_tiles(l, T) : 0;
+    butterfly_tile_tower_pre_device(ea, l, T, tw, k, s);
+    return k;
   }
 };
 struct Gf64Ops {
@@ -224,10 +232,12 @@ struct Gf64Ops {
     butterfly64_tile_fused_device(ea, eb, l, T, tw, s);
   }
   static bool fuse_ab(unsigned T) { return tile64_fused2_enabled(T); }
-  static void fused2(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s, bool r) {
+  static void fused2(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s, bool r,
+                     uint64_t = 0) {
     if (r) butterfly64_tile_tower_device(ea, eb, l, T, tw, s);
     else butterfly64_tile_fused2_device(ea, eb, l, T, tw, s);
   }
+  static uint64_t pre_pass(E*, unsigned, unsigned, const Tw&, cudaStream_t, bool) { return 0; }
 };
 
 // fp_polymul on device buffers.  field: FPM_FIELD_GF128, FPM_FIELD_GF64, or FPM_FIELD_AUTO (the
@@ -300,6 +310,7 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     FPM_CUDA(cudaEventRecord(fork->e, s));
     FPM_CUDA(cudaStreamWaitEvent(sb, fork->e, 0));
   }
+  uint64_t pre_tiles = 0;  // operand a's tiles whose forward tile layers ran ahead (host-buffer calls)
   for (int k = 0; k < 2; ++k) {
     wait_operand(k);
     if (!conc) clk.mark(kStBasis);
@@ -327,6 +338,7 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     clk.mark(kStBfly);
     F::top(es[k], l, T, false, tw, s, rep);
     if (k == 0 && !fuse_ab) F::tile(es[k], l, T, false, tw, s);
+    if (k == 0 && fuse_ab) pre_tiles = F::pre_pass(es[0], l, T, tw, s, rep);
   }
   if (conc) {
     FPM_CUDA(cudaEventRecord(joined->e, sb));
@@ -339,7 +351,7 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     if (!fuse_ab) F::tile(es[0], l, T, false, tw, s);
   }
   clk.mark(kStPointwise);  // + operand b's (and a's) bottom T forward and the bottom T inverse layers (fused)
-  if (fuse_ab) F::fused2(EA.as<E>(), EB.as<E>(), l, T, tw, s, rep);
+  if (fuse_ab) F::fused2(EA.as<E>(), EB.as<E>(), l, T, tw, s, rep, pre_tiles);
   else F::fused(EA.as<E>(), EB.as<E>(), l, T, tw, s);
   clk.mark(kStIBfly);
   F::top(EB.as<E>(), l, T, true, tw, s, rep);

@@ -319,7 +319,12 @@ bool pipeline_fuses_operands(unsigned T);  // both operands' tile layers in one 
 bool pipeline_tower(unsigned T);           // ... on tower-representation tiles
 void butterfly_tile_tower_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
                                  cudaStream_t s,
-                                 uint64_t batch = 0);
+                                 uint64_t batch = 0, uint64_t pre_tiles = 0);
+// Host-buffer products: the forward R layers of operand a's first tower_pre_tiles(l, T) tiles run
+// ahead of the fused pass, while operand b is still being uploaded.
+uint64_t tower_pre_tiles(unsigned l, unsigned T);
+void butterfly_tile_tower_pre_device(uint4* ev, unsigned l, unsigned T, const TwiddleSrc& tw, uint64_t pre_tiles,
+                                     cudaStream_t s);
 void butterfly_tile_fused_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
                                  cudaStream_t s);
 

@@ -731,11 +731,15 @@ size_t tower_smem(unsigned T) { return 2 * ((size_t)1 << T) * sizeof(uint4) + si
 // ntiles / tw_mask: a product's tiles (2^l >> T, each with its own twiddles: tw_mask = ~0), or a
 // batch of independent products of 2^T positions each (l = T; ntiles = count, tw_mask = 0: every
 // tile is a whole transform with tile 0's twiddles).
-template <unsigned T>
+// MODE (host-buffer products, whose operand a arrives and is transformed while operand b is still
+// being uploaded): 2 = the pre-pass -- forward R layers of the tiles [tile0, ntiles) of ONE EvalVec
+// (eb), in place; 1 = the fused pass over tiles whose operand-a tile the pre-pass already
+// transformed (forward R layers of operand b only); 0 = the fused pass.
+template <unsigned T, int MODE = 0>
 __global__ void __launch_bounds__(tower_threads(T), tower_min_blocks(T)) fft_tile_tower_kernel(const uint4* __restrict__ ea,
                                                                           uint4* __restrict__ eb, unsigned l,
                                                                           TwiddleSrc tw, uint64_t ntiles,
-                                                                          uint64_t tw_mask) {
+                                                                          uint64_t tw_mask, uint64_t tile0) {
   pdl_wait();
   extern __shared__ uint4 s[];
   constexpr int n = 1 << T;
@@ -748,7 +752,7 @@ __global__ void __launch_bounds__(tower_threads(T), tower_min_blocks(T)) fft_til
     sm.rows_to_poly[tid + (tid >> 3)] = __ldg(tw.to_poly + tid);
   }
   const int ntab = tower_tables(T);
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  for (uint64_t t = tile0 + blockIdx.x; t < ntiles; t += gridDim.x) {
     uint4* g = eb + (t << T);
     const uint4* ga = ea + (t << T);
     const uint64_t tt = t & tw_mask;  // the tile's position in its transform (twiddles)
@@ -763,12 +767,20 @@ __global__ void __launch_bounds__(tower_threads(T), tower_min_blocks(T)) fft_til
         sm.wzf[pos] = w;
       }
     }
+    if constexpr (MODE == 2) {  // pre-pass: this EvalVec's forward R layers only
+      for (int k = tid; k < n; k += blockDim.x) s[tsw(k)] = g[k];
+      __syncthreads();
+      tile_layers_r<false, 1, T, kPolyLayers>(s, sm);
+      for (int k = tid; k < n; k += blockDim.x) g[k] = s[tsw(k)];
+      __syncthreads();
+    } else {
     for (int k = tid; k < n; k += blockDim.x) {
       s[tsw(k)] = ga[k];
       s[n + tsw(k)] = g[k];
     }
     __syncthreads();
-    tile_layers_r<false, 2, T, kPolyLayers>(s, sm);
+    if (MODE == 1) tile_layers_r<false, 1, T, kPolyLayers>(s + n, sm);
+    else tile_layers_r<false, 2, T, kPolyLayers>(s, sm);
     m8_expand(sm.tab, sm.rows_to_poly, tid);
     __syncthreads();
     const M8Base mb = m8_base(sm.tab, q);
@@ -832,6 +844,7 @@ __global__ void __launch_bounds__(tower_threads(T), tower_min_blocks(T)) fft_til
     tile_layers_r<true, 1, T, kPolyLayers>(s, sm);
     for (int k = tid; k < n; k += blockDim.x) g[k] = s[tsw(k)];
     __syncthreads();
+    }  // (MODE != 2)
   }
   pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
@@ -1146,21 +1159,75 @@ bool tile_tower_enabled(unsigned T) {
   return on && T >= 10 && T <= 12;
 }
 
-void butterfly_tile_tower_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
-                                 cudaStream_t s, uint64_t batch) {
-  if (T < 10 || T > 12 || l < T) throw Error(kInvalid, "tower tile pass: T must be 10, 11 or 12");
-  if (batch && l != T) throw Error(kInvalid, "tower tile pass: a batch of transforms needs l = T");
+void tower_set_smem() {
   static PerDeviceOnce attr;
   attr.run([&] {
     set_smem(fft_tile_tower_kernel<10>, tower_smem(10));
     set_smem(fft_tile_tower_kernel<11>, tower_smem(11));
     set_smem(fft_tile_tower_kernel<12>, tower_smem(12));
+    set_smem(fft_tile_tower_kernel<12, 1>, tower_smem(12));
+    set_smem(fft_tile_tower_kernel<12, 2>, tower_smem(12));
   });
+}
+
+// pre_tiles: operand a's tiles [0, pre_tiles) already hold their forward R layers
+// (butterfly_tile_tower_pre_device); T = 12 only.
+void butterfly_tile_tower_device(const uint4* ea, uint4* eb, unsigned l, unsigned T, const TwiddleSrc& tw,
+                                 cudaStream_t s, uint64_t batch, uint64_t pre_tiles) {
+  if (T < 10 || T > 12 || l < T) throw Error(kInvalid, "tower tile pass: T must be 10, 11 or 12");
+  if (batch && l != T) throw Error(kInvalid, "tower tile pass: a batch of transforms needs l = T");
+  tower_set_smem();
   const size_t smem = tower_smem(T);
   auto kern = T == 10 ? fft_tile_tower_kernel<10> : T == 11 ? fft_tile_tower_kernel<11> : fft_tile_tower_kernel<12>;
   const uint64_t ntiles = batch ? batch : ((uint64_t)1 << l) >> T;
-  const int grid = resident_grid(kern, tower_threads(T), smem, ntiles);
-  launch_k(kern, dim3(grid), dim3(tower_threads(T)), smem, s, ea, eb, l, tw, ntiles, batch ? (uint64_t)0 : ~(uint64_t)0);
+  const uint64_t mask = batch ? (uint64_t)0 : ~(uint64_t)0;
+  if (pre_tiles) {
+    if (T != 12 || batch || pre_tiles > ntiles) throw Error(kInvalid, "tower tile pass: pre-passed tiles need T = 12");
+    const int g1 = resident_grid(fft_tile_tower_kernel<12, 1>, tower_threads(T), smem, pre_tiles);
+    launch_k(fft_tile_tower_kernel<12, 1>, dim3(g1), dim3(tower_threads(T)), smem, s, ea, eb, l, tw, pre_tiles, mask,
+             (uint64_t)0);
+    FPM_LAUNCH_CHECK();
+    if (pre_tiles == ntiles) return;
+  }
+  const int grid = resident_grid(kern, tower_threads(T), smem, ntiles - pre_tiles);
+  launch_k(kern, dim3(grid), dim3(tower_threads(T)), smem, s, ea, eb, l, tw, ntiles, mask, pre_tiles);
+  FPM_LAUNCH_CHECK();
+}
+
+// Host-buffer products: the share of operand a's tiles whose forward R layers run ahead of the fused
+// pass, in the window between the end of operand a's transforms and the arrival of operand b
+// (FPM_PRE_A_FRAC, default 0.5; 0 disables).  A whole number of waves of the resident grid.
+// Measured (host-buffer 2^33-bit products, tools/e2e_time.py): 75.0-75.2 ms without, 73.65-73.97
+// with 0.5, 73.9-74.0 with 0.3 / 0.4, 74.5-74.6 with 0.6 / 0.7; no gain for 2^31- / 2^32-bit
+// products (39.1-39.2 vs 39.4 ms, 19.5 vs 19.3-19.6), so only l >= 26 takes it (FPM_PRE_A_MIN_L).
+uint64_t tower_pre_tiles(unsigned l, unsigned T) {
+  static const unsigned min_l = [] {
+    const char* e = std::getenv("FPM_PRE_A_MIN_L");
+    return e ? (unsigned)std::atoi(e) : 26u;
+  }();
+  if (l < min_l) return 0;
+  static const double frac = [] {
+    const char* e = std::getenv("FPM_PRE_A_FRAC");
+    return e ? std::atof(e) : 0.5;
+  }();
+  if (T != 12 || l < T || !(frac > 0)) return 0;
+  tower_set_smem();
+  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
+  const uint64_t grid = (uint64_t)resident_grid(fft_tile_tower_kernel<12, 2>, tower_threads(T), tower_smem(T), ntiles);
+  const uint64_t waves = (uint64_t)(std::min(frac, 1.0) * (double)ntiles / (double)grid);
+  return std::min(ntiles, waves * grid);
+}
+
+// Forward R layers of the tiles [0, pre_tiles) of one EvalVec, in place (fft_tile_tower_kernel<12, 2>).
+void butterfly_tile_tower_pre_device(uint4* ev, unsigned l, unsigned T, const TwiddleSrc& tw, uint64_t pre_tiles,
+                                     cudaStream_t s) {
+  if (!pre_tiles) return;
+  if (T != 12 || l < T || pre_tiles > (((uint64_t)1 << l) >> T)) throw Error(kInvalid, "tower pre-pass: T = 12 only");
+  tower_set_smem();
+  const size_t smem = tower_smem(T);
+  const int grid = resident_grid(fft_tile_tower_kernel<12, 2>, tower_threads(T), smem, pre_tiles);
+  launch_k(fft_tile_tower_kernel<12, 2>, dim3(grid), dim3(tower_threads(T)), smem, s, (const uint4*)nullptr, ev, l, tw,
+           pre_tiles, ~(uint64_t)0, (uint64_t)0);
   FPM_LAUNCH_CHECK();
 }
 

@@ -445,6 +445,40 @@ def test_config5_host_buffers_match_reference_hash(gpu, port):
     assert hashlib.blake2b(got.tobytes(), digest_size=16).hexdigest() == c["blake2b128"]
 
 
+@pytest.mark.parametrize("frac", ["0.5", "1.0", "0.13"])
+def test_host_buffers_operand_a_pre_pass(port, frac):
+    """Host-buffer products run part of operand a's tower tile layers ahead of the fused pass
+    (fft_tile_tower_kernel modes 2 / 1, FPM_PRE_A_FRAC) while operand b is uploaded; by default only
+    2^33-bit products do.  Forced here at l = 22 / 23 (tile depth 12) for several shares, including
+    every tile: BASELINE config 4's reference hash and a ragged shape against the device-resident
+    product of the default schedule (child process: the knobs are read once)."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+    c = _meta()["268435456x268435456"]
+    la, lb = (1 << 29) - 12345, (1 << 28) + 777
+    code = (
+        "import hashlib, numpy as np, torch, paper_1803_11301_b200 as g\n"
+        f"a, b = g.random_bitpoly({c['a_bits']}, {c['seed_a']}), g.random_bitpoly({c['b_bits']}, {c['seed_b']})\n"
+        f"p = g.fp_polymul(a, {c['a_bits']}, b, {c['b_bits']}, field=g.FIELD_GF128)\n"
+        "print(hashlib.blake2b(p.tobytes(), digest_size=16).hexdigest())\n"
+        f"a, b = g.random_bitpoly({la}, 71), g.random_bitpoly({lb}, 72)\n"
+        f"p = g.fp_polymul(a, {la}, b, {lb}, field=g.FIELD_GF128)\n"
+        "da, db = (torch.from_numpy(x.view(np.int64)).cuda() for x in (a, b))\n"
+        "dc = torch.empty(p.size, dtype=torch.int64, device='cuda')\n"
+        f"g.fp_polymul_dev(da, {la}, db, {lb}, dc, field=g.FIELD_GF128)\n"
+        "torch.cuda.synchronize()\n"
+        "print(bool(np.array_equal(dc.cpu().numpy().view(np.uint64), p)))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=900,
+                       env=dict(os.environ, FPM_PRE_A_FRAC=frac, FPM_PRE_A_MIN_L="22"))
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = r.stdout.split()
+    assert out[0] == c["blake2b128"], frac
+    assert out[1] == "True", frac
+
+
 def _edge_operand(port, kind, bits, seed):
     w = port.random_bitpoly(bits, seed)
     if kind == "sparse":  # density 1/64: AND of six uniform words (SURVEY 8(d), config 3)
