@@ -169,6 +169,10 @@ struct HostIO {
   cudaEvent_t ready[2] = {nullptr, nullptr};
   uint64_t* h_out = nullptr;
   cudaStream_t d2h = nullptr;
+  // no other host-buffer call in flight on this device: the GPU idles while operand b is uploaded,
+  // and part of operand a's tile layers runs in that window (with concurrent callers the window is
+  // another caller's compute time, and the split pass would only add table builds)
+  bool alone = true;
 };
 
 // Field plumbing of run_pipeline<F> (polymul.cpp:78-135) for the two fields built on the GPU.
@@ -338,7 +342,7 @@ void run_pipeline(const uint64_t* d_a, size_t a_bits, const uint64_t* d_b, size_
     clk.mark(kStBfly);
     F::top(es[k], l, T, false, tw, s, rep);
     if (k == 0 && !fuse_ab) F::tile(es[k], l, T, false, tw, s);
-    if (k == 0 && fuse_ab) pre_tiles = F::pre_pass(es[0], l, T, tw, s, rep);
+    if (k == 0 && fuse_ab && io->alone) pre_tiles = F::pre_pass(es[0], l, T, tw, s, rep);
   }
   if (conc) {
     FPM_CUDA(cudaEventRecord(joined->e, sb));
@@ -559,6 +563,7 @@ struct StreamLease {
     std::condition_variable cv;
     bool busy[kSets] = {};
     cudaStream_t st[kSets][3] = {};
+    std::chrono::steady_clock::time_point last_overlap{};  // last time two leases were held at once
   };
   static Pool& pool(int dev) {
     static Pool pools[64];
@@ -584,6 +589,7 @@ struct StreamLease {
     }
     p.busy[k] = true;
     s = p.st[k][0], h2d = p.st[k][1], d2h = p.st[k][2];
+    if (held() > 1) p.last_overlap = std::chrono::steady_clock::now();
   }
   ~StreamLease() {
     {
@@ -591,6 +597,17 @@ struct StreamLease {
       p.busy[k] = false;
     }
     p.cv.notify_one();
+  }
+  int held() const {  // (p.mu held) leases on this device, this one included
+    int n = 0;
+    for (int i = 0; i < kSets; ++i) n += p.busy[i] ? 1 : 0;
+    return n;
+  }
+  // No other host-buffer call on this device now or within the last second (concurrent callers
+  // start their calls at different times: one of them may find the device momentarily free).
+  bool alone() {
+    std::lock_guard<std::mutex> lock(p.mu);
+    return held() == 1 && std::chrono::steady_clock::now() - p.last_overlap > std::chrono::seconds(1);
   }
   StreamLease(const StreamLease&) = delete;
   StreamLease& operator=(const StreamLease&) = delete;
@@ -624,6 +641,14 @@ cudaMemPool_t library_pool(int dev) {
     FPM_CUDA(cudaMemPoolCreate(&pools[dev], &props));
     uint64_t thr = UINT64_MAX;  // keep freed memory cached across calls (per-call GiB scratch)
     FPM_CUDA(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr));
+    // Concurrent callers allocate on their own streams.  By default the pool may satisfy caller B's
+    // allocation with memory whose free is still PENDING on caller A's stream, making B's stream
+    // wait for A's pipeline to reach that free: the two products then run one after the other
+    // (measured: two callers 49-50 ms per 2^33-bit product in most runs but 75-150 ms in one of
+    // three).  Without internal dependencies an allocation only reuses memory that is already free
+    // (or whose free the allocating stream already follows by an event); otherwise the pool grows.
+    int off = 0;
+    FPM_CUDA(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolReuseAllowInternalDependencies, &off));
   }
   return pools[dev];
 }
@@ -987,6 +1012,7 @@ fpm_status fpm_polymul(const uint64_t* a, size_t a_bits, const uint64_t* b, size
     io.ready[1] = ready_b.e;
     io.h_out = c;
     io.d2h = d2h;
+    io.alone = lease.alone();
     polymul_device(A.as<uint64_t>(), a_bits, B.as<uint64_t>(), b_bits, C.as<uint64_t>(), field, s, stage_seconds, &io);
     FPM_CUDA(cudaEventRecord(copied.e, d2h));
     FPM_CUDA(cudaStreamWaitEvent(s, copied.e, 0));  // frees below are ordered after the copies

@@ -34,6 +34,12 @@ for k in range(3):  # warm every buffer (pool growth, graph capture for small pr
     caller(k, 2)
 want = nouts[0].copy()
 for C in (1, 2, 3):
+    if C > 1:  # untimed concurrent round: the pool grows once for every extra concurrent caller
+        warm = [threading.Thread(target=caller, args=(k, 1)) for k in range(C)]
+        for t in warm:
+            t.start()
+        for t in warm:
+            t.join()
     for k in range(C):
         nouts[k][:] = 0
     th = [threading.Thread(target=caller, args=(k, per)) for k in range(C)]
