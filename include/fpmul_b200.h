@@ -305,6 +305,13 @@ fpm_status fpm_test_flip_encode_table(int device);
  * device's default pool is never modified) on `device` to the driver. */
 fpm_status fpm_trim_pool(int device);
 
+/* Grows the library's pool on `device` to at least `bytes` of cached scratch ahead of time.  The
+ * first product (and the first product of every additional concurrent caller) otherwise pays for
+ * fresh device memory inside the call -- hundreds of milliseconds for the ~5 GiB a 2^33-bit product
+ * takes.  A serving process calls this once at start-up (about 5 GiB per concurrent 2^33-bit
+ * caller).  No counterpart in the reference (its scratch is std::vector, polymul.cpp:78-135). */
+fpm_status fpm_reserve_pool(int device, size_t bytes);
+
 /* Number of kernel launches issued by this library on the calling thread since the last reset
  * (for the bench's gpu_launches accounting). */
 uint64_t fpm_launch_count(int reset);

@@ -48,6 +48,8 @@ from ._lib import (  # noqa: F401
     plan_mul,
     pointwise_mul,
     random_bitpoly,
+    reserve_pool,
+    trim_pool,
     stage_dev,
     tables128,
     tower_tables,

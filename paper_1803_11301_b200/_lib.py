@@ -59,6 +59,7 @@ def lib():
         L.fpm_polymul_multi.argtypes = [_u64p, sz, _u64p, sz, _u64p, C.c_int, C.POINTER(C.c_int), C.c_int]
         L.fpm_polymul_n.argtypes = [_u64p, sz, _u64p, sz, _u64p, C.c_int, C.c_int]
         L.fpm_trim_pool.argtypes = [C.c_int]
+        L.fpm_reserve_pool.argtypes = [C.c_int, C.c_size_t]
         L.fpm_test_flip_encode_table.argtypes = [C.c_int]
         L.fpm_polymul_batch_dev.argtypes = [vp, sz, sz, vp, sz, sz, vp, sz, sz, vp]
         L.fpm_polymul_batch.argtypes = [_u64p, sz, sz, _u64p, sz, sz, _u64p, sz, sz, C.c_int]
@@ -145,6 +146,17 @@ def _as_u64(a) -> np.ndarray:
 
 def device_count() -> int:
     return int(lib().fpm_device_count())
+
+
+def trim_pool(device: int = 0) -> None:
+    """Returns the library's cached device scratch to the driver (fpm_trim_pool)."""
+    _check(lib().fpm_trim_pool(int(device)))
+
+
+def reserve_pool(nbytes: int, device: int = 0) -> None:
+    """Grows the library's scratch pool ahead of time (fpm_reserve_pool): about 5 GiB per concurrent
+    2^33-bit host-buffer caller, so that no product pays for fresh device memory inside its call."""
+    _check(lib().fpm_reserve_pool(int(device), int(nbytes)))
 
 
 def launch_count(reset: bool = False) -> int:

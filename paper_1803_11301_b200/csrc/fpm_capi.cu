@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <optional>
 #include <tuple>
 #include <exception>
@@ -896,6 +897,24 @@ fpm_status fpm_trim_pool(int device) {
   return guard([&] {
     require_device();
     trim_pool(device);
+  });
+}
+
+fpm_status fpm_reserve_pool(int device, size_t bytes) {
+  return guard([&] {
+    DeviceGuard g(device);
+    if (!bytes) return;
+    cudaStream_t s = host_stream(device);
+    // blocks of at most 1 GiB (the size class of the large per-product buffers), all live at once,
+    // then freed: they stay cached in the pool (release threshold: never)
+    std::vector<std::unique_ptr<DevBuf>> blocks;
+    for (size_t left = bytes; left;) {
+      const size_t b = std::min<size_t>(left, (size_t)1 << 30);
+      blocks.emplace_back(new DevBuf(b, s));
+      left -= b;
+    }
+    blocks.clear();
+    FPM_CUDA(cudaStreamSynchronize(s));
   });
 }
 

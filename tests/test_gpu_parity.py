@@ -655,3 +655,16 @@ def test_polymul_shape_fuzz(gpu, checker, port, la, lb):
         gpu.fp_polymul_dev(da, la, db, lb, dc, field=gpu.FIELD_GF128)
         torch.cuda.synchronize()
         assert np.array_equal(dc.cpu().numpy().view(np.uint64), want), rep
+
+
+def test_reserve_and_trim_pool(gpu, checker, port):
+    """fpm_reserve_pool / fpm_trim_pool: products are unaffected by either (the pool only caches)."""
+    la, lb = 300000, 1 << 19
+    a, b = port.random_bitpoly(la, 5), port.random_bitpoly(lb, 6)
+    want = checker.polymul(a, la, b, lb)
+    gpu.reserve_pool(3 << 29)
+    assert np.array_equal(gpu.fp_polymul(a, la, b, lb, field=gpu.FIELD_GF128), want)
+    gpu.trim_pool()
+    assert np.array_equal(gpu.fp_polymul(a, la, b, lb, field=gpu.FIELD_GF128), want)
+    with pytest.raises(Exception):
+        gpu.reserve_pool(1 << 20, device=63)
