@@ -238,11 +238,15 @@ struct Gf64Ops {
   }
   static bool fuse_ab(unsigned T) { return tile64_fused2_enabled(T); }
   static void fused2(const E* ea, E* eb, unsigned l, unsigned T, const Tw& tw, cudaStream_t s, bool r,
-                     uint64_t = 0) {
-    if (r) butterfly64_tile_tower_device(ea, eb, l, T, tw, s);
+                     uint64_t pre_tiles = 0) {
+    if (r) butterfly64_tile_tower_device(ea, eb, l, T, tw, s, pre_tiles);
     else butterfly64_tile_fused2_device(ea, eb, l, T, tw, s);
   }
-  static uint64_t pre_pass(E*, unsigned, unsigned, const Tw&, cudaStream_t, bool) { return 0; }
+  static uint64_t pre_pass(E* ea, unsigned l, unsigned T, const Tw& tw, cudaStream_t s, bool r) {
+    const uint64_t k = r ? tower64_pre_tiles(l, T) : 0;
+    butterfly64_tile_tower_pre_device(ea, l, T, tw, k, s);
+    return k;
+  }
 };
 
 // fp_polymul on device buffers.  field: FPM_FIELD_GF128, FPM_FIELD_GF64, or FPM_FIELD_AUTO (the

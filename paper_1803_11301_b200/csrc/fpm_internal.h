@@ -335,7 +335,10 @@ void butterfly64_top_device(uint2* ev, unsigned l, unsigned T, bool inverse, con
                             bool tower = false, uint2* ev2 = nullptr);
 bool tile64_tower_enabled(unsigned T);
 void butterfly64_tile_tower_device(const uint2* ea, uint2* eb, unsigned l, unsigned T, const TwiddleSrc64& tw,
-                                   cudaStream_t s);
+                                   cudaStream_t s, uint64_t pre_tiles = 0);
+uint64_t tower64_pre_tiles(unsigned l, unsigned T);
+void butterfly64_tile_tower_pre_device(uint2* ev, unsigned l, unsigned T, const TwiddleSrc64& tw, uint64_t pre_tiles,
+                                       cudaStream_t s);
 void butterfly64_tile_device(uint2* ev, unsigned l, unsigned T, bool inverse, const TwiddleSrc64& tw, cudaStream_t s);
 void butterfly64_tile_fused_device(const uint2* ea, uint2* eb, unsigned l, unsigned T, const TwiddleSrc64& tw,
                                    cudaStream_t s);

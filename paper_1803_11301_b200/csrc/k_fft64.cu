@@ -605,8 +605,13 @@ __device__ __forceinline__ void tile_layers_poly64(uint2* __restrict__ s, unsign
 constexpr unsigned kPolyLayers64 = FPM_TOWER64_POLY;
 size_t tower64_smem(unsigned T) { return 2 * ((size_t)1 << T) * sizeof(uint2) + sizeof(TowerSmem64); }
 
+// MODE as fft_tile_tower_kernel (k_fft.cu): 0 = the fused pass over tiles [tile0, ntiles); 2 = the
+// pre-pass (forward R layers of one EvalVec's tiles, in place on eb); 1 = the fused pass over tiles
+// whose operand-a tile the pre-pass already transformed.
+template <int MODE>
 __global__ void __launch_bounds__(256, 3) fft64_tile_tower_kernel(const uint2* __restrict__ ea, uint2* __restrict__ eb,
-                                                                  unsigned l, unsigned T, TwiddleSrc64 tw) {
+                                                                  unsigned l, unsigned T, TwiddleSrc64 tw,
+                                                                  uint64_t tile0, uint64_t ntiles) {
   pdl_wait();
   extern __shared__ uint2 s64[];
   const int n = 1 << T, tid = threadIdx.x, lane = tid & 31;
@@ -618,8 +623,7 @@ __global__ void __launch_bounds__(256, 3) fft64_tile_tower_kernel(const uint2* _
     sm.rows_to_poly[tid + (tid >> 3)] = __ldg(tw.to_poly + tid);
   }
   const int ntab = tower64_tables(T);
-  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
-  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  for (uint64_t t = tile0 + blockIdx.x; t < ntiles; t += gridDim.x) {
     uint2* g = eb + (t << T);
     const uint2* ga = ea + (t << T);
     for (int k = tid; k < ntab; k += blockDim.x) {
@@ -627,12 +631,20 @@ __global__ void __launch_bounds__(256, 3) fft64_tile_tower_kernel(const uint2* _
       while (kk >= tower64_groups(T, (unsigned)i)) kk -= tower64_groups(T, (unsigned)i++);
       sm.wz[k] = x2(twiddle64(tw, (unsigned)i, t << (T - 1 - i)), c2p2_64(tw.c2p, (uint64_t)kk << 7));
     }
+    if constexpr (MODE == 2) {
+      for (int k = tid; k < n; k += blockDim.x) s64[tsw64(k)] = g[k];
+      __syncthreads();
+      tile_layers_r64<false, 1>(s64, T, kPolyLayers64, sm);
+      for (int k = tid; k < n; k += blockDim.x) g[k] = s64[tsw64(k)];
+      __syncthreads();
+    } else {
     for (int k = tid; k < n; k += blockDim.x) {
       s64[tsw64(k)] = ga[k];
       s64[n + tsw64(k)] = g[k];
     }
     __syncthreads();
-    tile_layers_r64<false, 2>(s64, T, kPolyLayers64, sm);
+    if (MODE == 1) tile_layers_r64<false, 1>(s64 + n, T, kPolyLayers64, sm);
+    else tile_layers_r64<false, 2>(s64, T, kPolyLayers64, sm);
     g8_expand(sm.tab, sm.rows_to_poly, tid);
     __syncthreads();
     if (kPolyLayers64) {
@@ -662,6 +674,7 @@ __global__ void __launch_bounds__(256, 3) fft64_tile_tower_kernel(const uint2* _
     tile_layers_r64<true, 1>(s64, T, kPolyLayers64, sm);
     for (int k = tid; k < n; k += blockDim.x) g[k] = s64[tsw64(k)];
     __syncthreads();
+    }  // (MODE != 2)
   }
   pdl_trigger();  // (late: the next kernel is scheduled as this grid drains)
 }
@@ -754,14 +767,64 @@ bool tile64_tower_enabled(unsigned T) {
   return on && T >= 10 && T <= 12;
 }
 
-void butterfly64_tile_tower_device(const uint2* ea, uint2* eb, unsigned l, unsigned T, const TwiddleSrc64& tw,
-                                   cudaStream_t s) {
-  if (T < 10 || T > 12 || l < T) throw Error(kInvalid, "tower tile pass (GF(2^64)): T must be 10..12");
+void tower64_set_smem() {
   static PerDeviceOnce attr;
-  attr.run([&] { set_smem64(fft64_tile_tower_kernel, tower64_smem(12)); });
+  attr.run([&] {
+    set_smem64(fft64_tile_tower_kernel<0>, tower64_smem(12));
+    set_smem64(fft64_tile_tower_kernel<1>, tower64_smem(12));
+    set_smem64(fft64_tile_tower_kernel<2>, tower64_smem(12));
+  });
+}
+
+// pre_tiles: operand a's tiles [0, pre_tiles) already hold their forward R layers
+// (butterfly64_tile_tower_pre_device).
+void butterfly64_tile_tower_device(const uint2* ea, uint2* eb, unsigned l, unsigned T, const TwiddleSrc64& tw,
+                                   cudaStream_t s, uint64_t pre_tiles) {
+  if (T < 10 || T > 12 || l < T) throw Error(kInvalid, "tower tile pass (GF(2^64)): T must be 10..12");
+  tower64_set_smem();
   const size_t smem = tower64_smem(T);
-  const int grid = resident_grid(fft64_tile_tower_kernel, 256, smem, ((uint64_t)1 << l) >> T);
-  launch_k(fft64_tile_tower_kernel, dim3(grid), dim3(256), smem, s, ea, eb, l, T, tw);
+  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
+  if (pre_tiles > ntiles) throw Error(kInvalid, "tower tile pass (GF(2^64)): more pre-passed tiles than tiles");
+  if (pre_tiles) {
+    const int g1 = resident_grid(fft64_tile_tower_kernel<1>, 256, smem, pre_tiles);
+    launch_k(fft64_tile_tower_kernel<1>, dim3(g1), dim3(256), smem, s, ea, eb, l, T, tw, (uint64_t)0, pre_tiles);
+    FPM_LAUNCH_CHECK();
+    if (pre_tiles == ntiles) return;
+  }
+  const int grid = resident_grid(fft64_tile_tower_kernel<0>, 256, smem, ntiles - pre_tiles);
+  launch_k(fft64_tile_tower_kernel<0>, dim3(grid), dim3(256), smem, s, ea, eb, l, T, tw, pre_tiles, ntiles);
+  FPM_LAUNCH_CHECK();
+}
+
+// Host-buffer products (as tower_pre_tiles / butterfly_tile_tower_pre_device in k_fft.cu): the share
+// of operand a's tiles whose forward R layers run while operand b is still being uploaded.
+uint64_t tower64_pre_tiles(unsigned l, unsigned T) {
+  static const double frac = [] {
+    const char* e = std::getenv("FPM_PRE_A_FRAC");
+    return e ? std::atof(e) : 0.5;
+  }();
+  static const unsigned min_l = [] {
+    const char* e = std::getenv("FPM_PRE_A_MIN_L");
+    return e ? (unsigned)std::atoi(e) : 27u;  // 2^33-bit products: l = 27 in GF(2^64)
+  }();
+  if (T < 10 || T > 12 || l < T || l < min_l || !(frac > 0)) return 0;
+  tower64_set_smem();
+  const uint64_t ntiles = ((uint64_t)1 << l) >> T;
+  const uint64_t grid = (uint64_t)resident_grid(fft64_tile_tower_kernel<2>, 256, tower64_smem(T), ntiles);
+  const uint64_t waves = (uint64_t)(std::min(frac, 1.0) * (double)ntiles / (double)grid);
+  return std::min(ntiles, waves * grid);
+}
+
+void butterfly64_tile_tower_pre_device(uint2* ev, unsigned l, unsigned T, const TwiddleSrc64& tw, uint64_t pre_tiles,
+                                       cudaStream_t s) {
+  if (!pre_tiles) return;
+  if (T < 10 || T > 12 || l < T || pre_tiles > (((uint64_t)1 << l) >> T))
+    throw Error(kInvalid, "tower pre-pass (GF(2^64)): bad tile count");
+  tower64_set_smem();
+  const size_t smem = tower64_smem(T);
+  const int grid = resident_grid(fft64_tile_tower_kernel<2>, 256, smem, pre_tiles);
+  launch_k(fft64_tile_tower_kernel<2>, dim3(grid), dim3(256), smem, s, (const uint2*)nullptr, ev, l, T, tw, (uint64_t)0,
+           pre_tiles);
   FPM_LAUNCH_CHECK();
 }
 

@@ -447,6 +447,16 @@ def test_config5_host_buffers_match_reference_hash(gpu, port):
 
 @pytest.mark.parametrize("frac", ["0.5", "1.0", "0.13"])
 def test_host_buffers_operand_a_pre_pass(port, frac):
+    _pre_pass_case(frac, "FIELD_GF128")
+
+
+@pytest.mark.parametrize("frac", ["0.5", "1.0"])
+def test_host_buffers_operand_a_pre_pass_gf64(port, frac):
+    """The same for the GF(2^64) pipeline (fft64_tile_tower_kernel modes 2 / 1)."""
+    _pre_pass_case(frac, "FIELD_GF64")
+
+
+def _pre_pass_case(frac, field):
     """Host-buffer products run part of operand a's tower tile layers ahead of the fused pass
     (fft_tile_tower_kernel modes 2 / 1, FPM_PRE_A_FRAC) while operand b is uploaded; by default only
     2^33-bit products do.  Forced here at l = 22 / 23 (tile depth 12) for several shares, including
@@ -461,10 +471,10 @@ def test_host_buffers_operand_a_pre_pass(port, frac):
     code = (
         "import hashlib, numpy as np, torch, paper_1803_11301_b200 as g\n"
         f"a, b = g.random_bitpoly({c['a_bits']}, {c['seed_a']}), g.random_bitpoly({c['b_bits']}, {c['seed_b']})\n"
-        f"p = g.fp_polymul(a, {c['a_bits']}, b, {c['b_bits']}, field=g.FIELD_GF128)\n"
+        f"p = g.fp_polymul(a, {c['a_bits']}, b, {c['b_bits']}, field=g.{field})\n"
         "print(hashlib.blake2b(p.tobytes(), digest_size=16).hexdigest())\n"
         f"a, b = g.random_bitpoly({la}, 71), g.random_bitpoly({lb}, 72)\n"
-        f"p = g.fp_polymul(a, {la}, b, {lb}, field=g.FIELD_GF128)\n"
+        f"p = g.fp_polymul(a, {la}, b, {lb}, field=g.{field})\n"
         "da, db = (torch.from_numpy(x.view(np.int64)).cuda() for x in (a, b))\n"
         "dc = torch.empty(p.size, dtype=torch.int64, device='cuda')\n"
         f"g.fp_polymul_dev(da, {la}, db, {lb}, dc, field=g.FIELD_GF128)\n"
