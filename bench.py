@@ -813,6 +813,15 @@ def main():
                       "value": round(auto_ms, 3), "unit": "ms", "steps": k2,
                       "same_product": bool(np.array_equal(c.cpu().numpy().view(np.uint64), dev_result)),
                       "stage_ms": {k: round(v * 1e3, 3) for k, v in zip(pkg.STAGE_NAMES, st)}}
+        # the same through the host entry point (what a caller of the reference's fp_polymul with
+        # default options gets): host buffers, both PCIe copies inside
+        for _ in range(2):
+            pkg.fp_polymul(na, bits, nb, bits, field=pkg.FIELD_AUTO, device=local, out=nc)
+        t0 = time.perf_counter()
+        for _ in range(k2):
+            res = pkg.fp_polymul(na, bits, nb, bits, field=pkg.FIELD_AUTO, device=local, out=nc)
+        auto_field["e2e"] = {"value": round((time.perf_counter() - t0) * 1e3 / k2, 3), "unit": "ms", "steps": k2,
+                             "matches_device_result": bool(np.array_equal(res, dev_result))}
 
     line = {
         "metric": METRIC, "value": round(ms_max / ws if mode == "replicas" else ms_max, 3), "unit": "ms",
