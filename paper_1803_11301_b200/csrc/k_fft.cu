@@ -587,6 +587,9 @@ __device__ __forceinline__ int tsw(int k) { return k ^ (((k >> 3) & 1) * 7); }
 
 // CTA shape per tile depth: T <= 11 -> 256 threads, 2 CTAs/SM (<= 140 KiB of shared memory each at
 // T = 10); T = 12 (two 64 KiB tiles + the 64 KiB table, 207 KiB) -> 512 threads, 1 CTA/SM.
+#ifndef FPM_TOWER_IDX2
+#define FPM_TOWER_IDX2 1  // strength-reduced pair indices in tile_layers_r
+#endif
 #ifndef FPM_TOWER12_THREADS
 #define FPM_TOWER12_THREADS 512
 #endif
@@ -644,13 +647,30 @@ __device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, TowerSmem& 
       } else {
         pp0 = 256 * c + tid - 256, stride = NTH - 256, cnt = c;
       }
+#if FPM_TOWER_IDX2
+      // i0 = (blk << (i + 1)) + j = p + (p & ~(2^i - 1)) (+ the group's base, + the operand's
+      // tile); every stride is a multiple of 128, so the low four bits of i0 and i1 -- all the
+      // swizzle looks at -- are the same for every r
+      const int mlg = (1 << lg) - 1, nmi = ~((1 << i) - 1), hb = h << (i + 1);
+      const int pf = pp0 & mlg, i0f = hb + pf + (pf & nmi);
+      const int sw0 = ((i0f >> 3) & 1) * 7, sw1 = (((i0f + (1 << i)) >> 3) & 1) * 7;
+#endif
       for (int r = 0; r < cnt; ++r) {
         const int pp = pp0 + stride * r;
+#if FPM_TOWER_IDX2
+        const int p = pp & mlg;
+        const int i0 = hb + p + (p & nmi) + (NT == 1 ? 0 : (pp >> lg) * n), i1 = i0 + (1 << i);
+        const int d = (h + (p >> i)) & 127;  // subfield part of the twiddle (zero iff d == 0)
+        const int x0 = i0 ^ sw0, x1 = i1 ^ sw1;
+        uint4 u0 = s[x0], u1 = s[x1];
+#else
         const int p = pp & ((1 << lg) - 1), tt = pp >> lg;
         const int blk = h + (p >> i), j = p & ((1 << i) - 1);
         const int i0 = (blk << (i + 1)) + j + tt * n, i1 = i0 + (1 << i);
         const int d = blk & 127;  // subfield part of the twiddle (zero iff d == 0)
-        uint4 u0 = s[tsw(i0)], u1 = s[tsw(i1)];
+        const int x0 = tsw(i0), x1 = tsw(i1);
+        uint4 u0 = s[x0], u1 = s[x1];
+#endif
         if (!INV) {
           uint4 m = m8_mul_r(mb, u1, q);
 #ifndef FPM_EXP_NO_SMUL
@@ -666,8 +686,8 @@ __device__ __forceinline__ void tile_layers_r(uint4* __restrict__ s, TowerSmem& 
 #endif
           u0 = x4(u0, m);
         }
-        s[tsw(i0)] = u0;
-        s[tsw(i1)] = u1;
+        s[x0] = u0;
+        s[x1] = u1;
       }
       __syncthreads();  // lookups of table k and this layer's butterflies done; rows of k+1 ready
       if (k + 1 < ntab) {
