@@ -421,10 +421,15 @@ constexpr int kPipeSlots = 2 * FPM_PIPE_LAG;  // skewed-row ring (chunks); > kPi
 constexpr int kPipeZW = 65;    // zeta windows per skewed row: (2^16 + 1024) / 1024
 constexpr int kPipeORows = 4;  // overflow rows per item (inverse, no T_r^-1)
 constexpr uint64_t kPipeP1 = (kT + 32 * kZW) / 32;  // skewed row pitch (words)
+// CTAs per SM: forward (zeta + carry / T_r) 3 at 80 registers; inverse (zeta + overflow) 4 at 64
+// without spills (inverse conversions of a 2^33-bit product 5.55 -> 5.46 ms; forward unchanged at 4)
 #ifndef FPM_PIPE_CTAS
 #define FPM_PIPE_CTAS 3
 #endif
-constexpr int kPipeCtas = FPM_PIPE_CTAS;  // CTAs per SM
+#ifndef FPM_PIPE_CTAS_INV
+#define FPM_PIPE_CTAS_INV 4
+#endif
+constexpr int pipe_ctas(bool inv) { return inv ? FPM_PIPE_CTAS_INV : FPM_PIPE_CTAS; }
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -657,7 +662,7 @@ __device__ __forceinline__ PipeItem pipe_item(int k, int nch) {
 // kPipeP1); top: as overflow_kernel.  INV: zeta + overflow (L1_inner^-1); ICONV: with the rows'
 // conv(2^16)^-1 (T_r^-1) first.
 template <bool INV, bool ICONV>
-__global__ void __launch_bounds__(256, kPipeCtas) l1_inner_rows_kernel(const uint32_t* src, uint32_t* w, uint32_t* ring,
+__global__ void __launch_bounds__(256, pipe_ctas(INV)) l1_inner_rows_kernel(const uint32_t* src, uint32_t* w, uint32_t* ring,
                                                                 int nch, int* cnt, const uint32_t* __restrict__ top) {
   pdl_wait();
   extern __shared__ __align__(16) uint32_t smem[];  // max(zeta 256 x kZP, row tile kTileSmem)
@@ -2032,7 +2037,7 @@ void l1_inner_rows(const uint32_t* src, uint32_t* w, uint32_t* ring, uint64_t D,
   DevBuf cnt((3 * nch + 1) * sizeof(int), s);
   FPM_CUDA(cudaMemsetAsync(cnt.p, 0, (3 * nch + 1) * sizeof(int), s));
   const int items = nch * (kPipeZW + (mode == 1 ? 256 / kPipeORows : 256) + (mode == 2 ? 256 : 0));
-  const int grid = grid_cap((uint64_t)items, kPipeCtas);
+  const int grid = grid_cap((uint64_t)items, pipe_ctas(mode != 0));
   if (mode == 2) launch_k(l1_inner_rows_kernel<true, true>, dim3(grid), dim3(256), smem, s, src, w, ring, nch, cnt.as<int>(), top);
   else if (mode == 1) launch_k(l1_inner_rows_kernel<true, false>, dim3(grid), dim3(256), smem, s, src, w, ring, nch, cnt.as<int>(), top);
   else launch_k(l1_inner_rows_kernel<false, false>, dim3(grid), dim3(256), smem, s, src, w, ring, nch, cnt.as<int>(), top);
