@@ -110,7 +110,7 @@ __device__ __forceinline__ void l1_tile(uint32_t (&m)[8], uint32_t* sc, int g, i
     for (int i = 0; i < 16; ++i) G[i] = __funnelshift_r(U[i], U[i + 1], bs);
   }
   // carry (forward) / overflow (inverse) with the previous row's high half H_{d-1}
-  __syncthreads();
+  // (no barrier before these stores: since the last one every thread has read only its own row)
 #pragma unroll
   for (int i = 0; i < 8; ++i) my[i] = G[8 + i];
   __syncthreads();
