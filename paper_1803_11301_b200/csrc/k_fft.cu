@@ -774,7 +774,7 @@ __global__ void __launch_bounds__(tower_threads(T), tower_min_blocks(T)) fft_til
   const int ntab = tower_tables(T);
   for (uint64_t t = tile0 + blockIdx.x; t < ntiles; t += gridDim.x) {
     uint4* g = eb + (t << T);
-    const uint4* ga = ea + (t << T);
+    const uint4* ga = MODE == 2 ? nullptr : ea + (t << T);  // (the pre-pass has one EvalVec: eb)
     const uint64_t tt = t & tw_mask;  // the tile's position in its transform (twiddles)
     if (tid < ntab) {  // wz[k]: layer i, group h of this tile: Z(i) ^ C2P(2 * 128 h)
       int i = 0, kk = tid;

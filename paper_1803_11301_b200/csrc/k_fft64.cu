@@ -625,7 +625,7 @@ __global__ void __launch_bounds__(256, 3) fft64_tile_tower_kernel(const uint2* _
   const int ntab = tower64_tables(T);
   for (uint64_t t = tile0 + blockIdx.x; t < ntiles; t += gridDim.x) {
     uint2* g = eb + (t << T);
-    const uint2* ga = ea + (t << T);
+    const uint2* ga = MODE == 2 ? nullptr : ea + (t << T);  // (the pre-pass has one EvalVec: eb)
     for (int k = tid; k < ntab; k += blockDim.x) {
       int i = 0, kk = k;
       while (kk >= tower64_groups(T, (unsigned)i)) kk -= tower64_groups(T, (unsigned)i++);
