@@ -83,7 +83,10 @@ fpm_status fpm_random_bitpoly(size_t n_bits, uint64_t seed, uint64_t* out);
  * c receives ceil((a_bits+b_bits-1)/64) words (bits >= a_bits+b_bits-1 cleared); nothing is
  * written when either length is 0.  field: FPM_FIELD_AUTO (short inputs: karatsuba_mul, else
  * plan_mul's field), FPM_FIELD_GF64 or FPM_FIELD_GF128.  stage_seconds: NULL or
- * double[FPM_NUM_STAGES] (accumulated).  device: CUDA ordinal. */
+ * double[FPM_NUM_STAGES] (accumulated).  device: CUDA ordinal.
+ * Any host memory works; page-locked buffers (cudaHostAlloc / cudaHostRegister) let the uploads and
+ * the download run at the PCIe rate and overlap the kernels (pageable memory is staged by the
+ * driver).  Reentrant: concurrent callers overlap one another's copies and kernels. */
 fpm_status fpm_polymul(const uint64_t* a, size_t a_bits, const uint64_t* b, size_t b_bits, uint64_t* c,
                        int field, int device, double* stage_seconds);
 
