@@ -678,3 +678,20 @@ def test_reserve_and_trim_pool(gpu, checker, port):
     assert np.array_equal(gpu.fp_polymul(a, la, b, lb, field=gpu.FIELD_GF128), want)
     with pytest.raises(Exception):
         gpu.reserve_pool(1 << 20, device=63)
+
+
+def test_host_buffers_ragged_2p33_product_matches_device_path(gpu):
+    """A ragged 2^33-bit-class product through the host entry point (operand-a pre-pass, split decode,
+    overlapped copies) equals the device-resident product of the same operands, which
+    test_concurrent_conversions_device_resident_vs_reference pins to the reference."""
+    import torch
+    la, lb = 1 << 32, (1 << 31) + 999
+    a, b = gpu.random_bitpoly(la, 91), gpu.random_bitpoly(lb, 92)
+    got = gpu.fp_polymul(a, la, b, lb, field=gpu.FIELD_GF128)
+    da, db = (torch.from_numpy(x.view(np.int64)).cuda() for x in (a, b))
+    dc = torch.empty(got.size, dtype=torch.int64, device="cuda")
+    gpu.fp_polymul_dev(da, la, db, lb, dc, field=gpu.FIELD_GF128)
+    torch.cuda.synchronize()
+    assert np.array_equal(dc.cpu().numpy().view(np.uint64), got)
+    got64 = gpu.fp_polymul(b, lb, a, la, field=gpu.FIELD_AUTO)  # (operands swapped, GF(2^64))
+    assert np.array_equal(got64, got)
