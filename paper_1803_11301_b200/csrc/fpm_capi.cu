@@ -44,6 +44,9 @@ fpm_status guard(Fn&& fn) {
     return FPM_OK;
   } catch (const Error& e) {
     g_err = e.what();
+    // a failed runtime call also stays behind as the thread's "last error": clear it, or the next
+    // call's launch check (cudaGetLastError) would report this call's failure as its own
+    if (e.code == kCuda) cudaGetLastError();
     return (fpm_status)e.code;
   } catch (const std::bad_alloc& e) {
     g_err = e.what();

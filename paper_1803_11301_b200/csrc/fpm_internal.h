@@ -42,6 +42,7 @@ int fpm_guard_impl(Fn&& fn) {
     return kOk;
   } catch (const Error& e) {
     set_last_error(e.what());
+    if (e.code == kCuda) cudaGetLastError();  // (clear the runtime's own last-error slot, as guard() in fpm_capi.cu)
     return e.code;
   } catch (const std::bad_alloc& e) {
     set_last_error(e.what());

@@ -678,6 +678,8 @@ def test_reserve_and_trim_pool(gpu, checker, port):
     assert np.array_equal(gpu.fp_polymul(a, la, b, lb, field=gpu.FIELD_GF128), want)
     with pytest.raises(Exception):
         gpu.reserve_pool(1 << 20, device=63)
+    # a failed call leaves no stale CUDA error behind for the next one's launch checks
+    assert np.array_equal(gpu.fp_polymul(a, la, b, lb, field=gpu.FIELD_GF128), want)
 
 
 def test_host_buffers_ragged_2p33_product_matches_device_path(gpu):
