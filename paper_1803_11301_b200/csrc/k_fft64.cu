@@ -537,12 +537,17 @@ __device__ __forceinline__ void tile_layers_r64(uint2* __restrict__ s, unsigned 
     for (int h = 0; h < nblk; h += 128, ++k) {
       if (k + 1 < ntab) rows_r64(sm.rows[(k + 1) & 1], sm.wz[wz_of(k + 1)], tid, sm.to_r);
       const G8Base gb = g8_base(sm.tab, lane);
+      // pair indices as in tile_layers_r (k_fft.cu): i0 = p + (p & ~(2^i - 1)) + the group's base
+      // (+ the operand's tile); the stride (256) keeps the low bits the swizzle looks at fixed
+      const int mlg = (1 << lg) - 1, nmi = ~((1 << i) - 1), hb = h << (i + 1);
+      const int pf = tid & mlg, i0f = hb + pf + (pf & nmi);
+      const int sw0 = ((i0f >> 4) & 1) * 15, sw1 = (((i0f + (1 << i)) >> 4) & 1) * 15;
       for (int pp = tid; pp < (NT << lg); pp += blockDim.x) {
-        const int p = pp & ((1 << lg) - 1), tt = pp >> lg;
-        const int blk = h + (p >> i), j = p & ((1 << i) - 1);
-        const int i0 = (blk << (i + 1)) + j + tt * n, i1 = i0 + (1 << i);
-        const int d = blk & 127;
-        uint2 u0 = s[tsw64(i0)], u1 = s[tsw64(i1)];
+        const int p = pp & mlg;
+        const int i0 = hb + p + (p & nmi) + (NT == 1 ? 0 : (pp >> lg) * n), i1 = i0 + (1 << i);
+        const int d = (h + (p >> i)) & 127;
+        const int x0 = i0 ^ sw0, x1 = i1 ^ sw1;
+        uint2 u0 = s[x0], u1 = s[x1];
         if (!INV) {
           uint2 m = g8_mul_r(gb, u1, lane);
           if (d) m = x2(m, smul_t2(u1, smul_tab(sm.stab, d)));
@@ -554,8 +559,8 @@ __device__ __forceinline__ void tile_layers_r64(uint2* __restrict__ s, unsigned 
           if (d) m = x2(m, smul_t2(u1, smul_tab(sm.stab, d)));
           u0 = x2(u0, m);
         }
-        s[tsw64(i0)] = u0;
-        s[tsw64(i1)] = u1;
+        s[x0] = u0;
+        s[x1] = u1;
       }
       __syncthreads();
       if (k + 1 < ntab) {
